@@ -1,0 +1,39 @@
+# Builds the product library paper_2311_01635_b200/librtpb.so (sm_100a only)
+# and the CPU oracle (oracle/, test infrastructure).
+NVCC    ?= /usr/local/cuda/bin/nvcc
+SITE    ?= $(shell python -c "import sysconfig;print(sysconfig.get_paths()['purelib'])" 2>/dev/null)
+NCCL_DIR ?= $(SITE)/nvidia/nccl
+PKG     := paper_2311_01635_b200
+CSRC    := $(PKG)/csrc
+OBJDIR  := build/obj
+ARCH    := -gencode arch=compute_100a,code=sm_100a
+NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -Wall --expt-relaxed-constexpr \
+           -Iinclude -I$(CSRC) -I$(NCCL_DIR)/include -Xptxas -v
+CXX     ?= g++
+CXXFLAGS := -std=c++20 -O2 -g -fPIC -Wall -Wextra -Wno-unused-parameter -Iinclude -I$(CSRC) \
+            -I/usr/local/cuda/include -I$(NCCL_DIR)/include
+CU_SRC  := $(CSRC)/kernels/gemm_launch.cu $(CSRC)/kernels/elementwise.cu $(CSRC)/capi_steps.cu
+CPP_SRC := $(wildcard $(CSRC)/host/*.cpp)
+OBJS    := $(patsubst $(CSRC)/%.cu,$(OBJDIR)/%.o,$(CU_SRC)) $(patsubst $(CSRC)/%.cpp,$(OBJDIR)/%.o,$(CPP_SRC))
+HDRS    := $(wildcard include/*.h include/rtpb/*.hpp $(CSRC)/kernels/*.cuh $(CSRC)/kernels/*.hpp $(CSRC)/host/*.hpp)
+
+.PHONY: all lib oracle clean
+all: lib oracle
+lib: $(PKG)/librtpb.so
+oracle:
+	$(MAKE) -s -C oracle oracle
+
+$(OBJDIR)/%.o: $(CSRC)/%.cu $(HDRS)
+	@mkdir -p $(dir $@)
+	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $@.log || (cat $@.log; false)
+
+$(OBJDIR)/%.o: $(CSRC)/%.cpp $(HDRS)
+	@mkdir -p $(dir $@)
+	$(CXX) $(CXXFLAGS) -c $< -o $@
+
+$(PKG)/librtpb.so: $(OBJS)
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -L$(NCCL_DIR)/lib -l:libnccl.so.2 \
+	    -Xlinker -rpath,$(NCCL_DIR)/lib -lpthread
+
+clean:
+	rm -rf build $(PKG)/librtpb.so

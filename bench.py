@@ -1,0 +1,374 @@
+"""RTP MLP fwd+bwd benchmark (BASELINE.json metric: "RTP MLP fwd+bwd TFLOP/s/GPU
+& peak HBM/GPU at 1/2/4/8 B200 vs CPU ref").
+
+Workload (config (b) of BASELINE.json, the metric's single-GPU config): one
+RTP MLP block ffn1 768->3072 -> GELU -> ffn2 3072->768, bf16, Flyweight init
+(SplitMix64 seed 42), 8192 tokens per GPU (GPT-2 seq 512 x 16, SURVEY §8d;
+global T = 8192 x N, batch-major row shards: weak scaling). A step = zero
+grads + forward + backward of the block through the library's public API.
+FLOPs per step = 12 * T * h * f (fwd, dX, dW at 2*T*h*f per linear).
+
+python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+N > 1: launch with torch.distributed.run, one process per GPU, NCCL ring.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+H, F, TOKENS_PER_GPU, SEED = 768, 3072, 8192, 42
+METRIC = "RTP MLP fwd+bwd TFLOP/s/GPU & peak HBM/GPU at 1/2/4/8 B200 vs CPU ref"
+UNIT = "TFLOP/s"
+
+
+def flops_per_step(tokens: int) -> float:
+    return 12.0 * tokens * H * F
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["bf16_tflops"]), float(p.get("bf16_tflops_sustained", p["bf16_tflops"])), "measured"
+    except Exception:
+        return 1590.0, 1400.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.samples = []
+        self._stop = threading.Event()
+        self._proc = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self._proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}",
+                                           "--format=csv,noheader,nounits", "-lms", "100"],
+                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._read, daemon=True).start()
+        except Exception:
+            self._proc = None
+        return self
+
+    def _read(self):
+        for line in self._proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 7:
+                self.samples.append(parts)
+
+    def __exit__(self, *a):
+        if self._proc:
+            time.sleep(0.25)
+            self._proc.terminate()
+            try:
+                self._proc.wait(timeout=5)
+            except Exception:
+                self._proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no-samples"], "samples": 0}
+
+        def num(x):
+            try:
+                return float(x)
+            except ValueError:
+                return None
+        sm = [num(s[0]) for s in self.samples if num(s[0]) is not None]
+        mx = [num(s[1]) for s in self.samples if num(s[1]) is not None]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[3 + i].lower().startswith("active")})
+        loaded = [v for v in sm if v and v > 600] or sm
+        loaded.sort()
+        return {"sm_mhz": loaded[len(loaded) // 2] if loaded else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples),
+                "power_w_max": max((num(s[2]) or 0) for s in self.samples)}
+
+
+def dist_env():
+    return int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), \
+        int(os.environ.get("LOCAL_RANK", "0"))
+
+
+# ------------------------------------------------------------------ reference arm
+def cpu_reference(sample_rows: int | None = None, target_s: float = 12.0, iters: int = 1):
+    """Times the reference's own CPU implementation of the path (oracle/_ref:
+    the reference sources compiled by path; RtpLinear x2 + gelu on the
+    Concurrent transport, one worker thread per host core, fp64) on a bounded
+    row sample of the same workload. Falls back to the C restatement."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as orc
+    cores = os.cpu_count() or 1
+    workers = 1
+    while workers * 2 <= cores and (F % (workers * 2) == 0) and (H % (workers * 2) == 0):
+        workers *= 2
+    try:
+        R = orc.Reference()
+        kind = "reference"
+
+        def run(rows):
+            return R.time_mlp(workers, rows, H, F, SEED, iters=1, concurrent=True)
+    except Exception:
+        O = orc.Oracle()
+        kind = "port"
+        import numpy as np
+        rng = np.random.default_rng(SEED)
+        w1, b1 = rng.uniform(-0.1, 0.1, (H, F)), rng.uniform(-0.1, 0.1, F)
+        w2, b2 = rng.uniform(-0.1, 0.1, (F, H)), rng.uniform(-0.1, 0.1, H)
+
+        def run(rows):
+            x, dy = rng.uniform(-1, 1, (rows, H)), rng.uniform(-1, 1, (rows, H))
+            t0 = time.perf_counter()
+            O.rtp_mlp(workers, w1, b1, w2, b2, x, dy)
+            return time.perf_counter() - t0
+    if sample_rows is None:
+        probe = 32 * workers
+        t = run(probe)
+        rate = flops_per_step(probe) / max(t, 1e-6)
+        sample_rows = int(target_s * rate / flops_per_step(1))
+        sample_rows = max(workers, min(TOKENS_PER_GPU, (sample_rows // workers) * workers))
+    secs = sum(run(sample_rows) for _ in range(iters))
+    value = flops_per_step(sample_rows) * iters / secs / 1e12
+    return {"value": value, "unit": UNIT, "cores": workers, "kind": kind,
+            "sample": f"{iters}x MLP fwd+bwd over {sample_rows} of {TOKENS_PER_GPU} tokens (768->3072->768, fp64, "
+                      f"{workers} Concurrent-transport workers), {secs:.1f} s"}
+
+
+def run_reference_arm(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    steps = []
+    # bounded sample per step so --steps K --warmup W ends within minutes
+    per_step_target = max(2.0, 60.0 / max(1, args.steps + args.warmup))
+    base = cpu_reference(target_s=per_step_target)
+    rows = int(base["sample"].split(" over ")[1].split(" ")[0])
+    for _ in range(args.warmup):
+        cpu_reference(sample_rows=rows)
+    for _ in range(args.steps):
+        steps.append(cpu_reference(sample_rows=rows))
+    value = sum(s["value"] for s in steps) / len(steps)
+    ms = flops_per_step(rows) / (value * 1e12) * 1e3
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "rtp_mlp_768x3072x768", "tokens": rows, "tokens_per_gpu": TOKENS_PER_GPU,
+                       "note": "bounded row sample of the same workload on host cores"},
+            "impl": "reference",
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": steps[0]["cores"], "kind": steps[0]["kind"],
+                             "sample": steps[0]["sample"]},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ our arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=300)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--mode", default="outofplace", choices=["inplace", "outofplace"])
+    ap.add_argument("--tokens-per-gpu", type=int, default=TOKENS_PER_GPU)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference_arm(args)
+        return
+    if args.warmup < 3:
+        args.warmup = 3
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2311_01635_b200 import _lib, rtp
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+        uid = torch.zeros(128, dtype=torch.uint8, device=dev)
+        if rank == 0:
+            uid.copy_(torch.frombuffer(bytearray(rtp.WorkerGroup.nccl_unique_id()), dtype=torch.uint8))
+        dist.broadcast(uid, 0)
+        grp = rtp.WorkerGroup.nccl(world, rank, local, bytes(uid.cpu().numpy().tobytes()))
+    else:
+        grp = rtp.WorkerGroup(1)
+    M = args.tokens_per_gpu
+    T = M * world
+    mlp = rtp.RtpMlp(grp, "block0", H, F, "bf16", seed=SEED, stream_base=0)  # Flyweight init on device
+    mlp.set_rotation_mode(args.mode)
+    mlp.begin_step()
+
+    g = torch.Generator(device=dev).manual_seed(SEED + rank)
+    x = (torch.rand(M, H, device=dev, generator=g) * 2 - 1).to(torch.bfloat16)
+    dy = (torch.rand(M, H, device=dev, generator=g) * 2 - 1).to(torch.bfloat16)
+    y = torch.empty(M, H, dtype=torch.bfloat16, device=dev)
+    dx = torch.empty(M, H, dtype=torch.bfloat16, device=dev)
+    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # 512 MiB > 126 MB L2
+
+    def step():
+        mlp.zero_grads()
+        mlp.forward([x], out=[y])
+        mlp.backward([dy], out=[dx])
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+
+    # ---- timed region: exactly K steps, L2 flushed before each, CUDA events on our stream
+    stream = torch.cuda.current_stream(dev)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    _lib.lib.rtpb_profile_enable(1)
+    _lib.lib.rtpb_profile_read(None, None, None, 0)
+    launches0 = rtp.launch_count()
+    grp.reset_ledger_peaks()
+    torch.cuda.reset_peak_memory_stats(dev)
+    with ClockSampler(local) as clocks:
+        barrier()
+        for i in range(args.steps):
+            flush.zero_()
+            ev[i][0].record(stream)
+            step()
+            ev[i][1].record(stream)
+        barrier()
+    launches = rtp.launch_count() - launches0
+    _lib.lib.rtpb_profile_enable(0)
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    total_ms = sum(step_ms)
+    if world > 1:
+        t = torch.tensor([total_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    value = flops_per_step(T) / (ms_per_step * 1e-3) / 1e12  # whole-job aggregate
+
+    # ---- per-launch GEMM timing (the roofline numerator)
+    import ctypes as C
+    cnt = _lib.lib.rtpb_profile_read(None, None, None, 0)
+    kinds = (C.c_int * cnt)()
+    fl = (C.c_double * cnt)()
+    ms = (C.c_float * cnt)()
+    _lib.lib.rtpb_profile_read(kinds, fl, ms, cnt)
+    per_kind = {}
+    for k, f_, m_ in zip(kinds, fl, ms):
+        d = per_kind.setdefault({0: "fwd", 1: "dgrad", 2: "wgrad"}[k], [0.0, 0.0, 0])
+        d[0] += f_
+        d[1] += m_
+        d[2] += 1
+    gemm_flops = sum(d[0] for d in per_kind.values())
+    gemm_ms = sum(d[1] for d in per_kind.values())
+    burst, sustained, peak_src = load_peaks()
+    achieved = gemm_flops / (gemm_ms * 1e-3) / 1e12 if gemm_ms else 0.0
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
+            traffic = json.load(fh).get("dram_bytes_per_launch")
+    except Exception:
+        pass
+    roofline = {"bound": "tensor", "achieved": achieved, "peak": burst, "unit": "TFLOP/s",
+                "frac": achieved / burst, "traffic": traffic,
+                "kernel": "rtp_gemm_kernel (tcgen05 step GEMMs: fwd, dgrad, wgrad)",
+                "peak_source": f"{peak_src} bf16 burst; sustained {sustained}",
+                "frac_of_sustained": achieved / sustained,
+                "gemm_share_of_step": gemm_ms / total_ms if total_ms else None,
+                "per_kernel": {k: {"tflops": v[0] / (v[1] * 1e-3) / 1e12, "launches": v[2],
+                                   "avg_us": v[1] / v[2] * 1e3} for k, v in per_kind.items()}}
+
+    # ---- memory: device ledger (params, grads, comm, activations, workspace) + caller tensors
+    led = grp.ledger(rank)
+    torch_peak = torch.cuda.max_memory_allocated(dev) - flush.numel() * 4
+    shard_w = mlp.ffn1.shard_len() * 2 + mlp.ffn2.shard_len() * 2
+    shard_g = mlp.ffn1.shard_len() * 4 + mlp.ffn2.shard_len() * 4
+    W_total, G_total = shard_w * world, shard_g * world
+    mem = {"peak_hbm_bytes_per_gpu": led["peak_total"] + torch_peak,
+           "ledger_peak": {k[5:]: v for k, v in led.items() if k.startswith("peak_")},
+           "caller_activations_bytes": torch_peak,
+           "model_inplace_bytes": (W_total + G_total) // world,
+           "model_outofplace_bytes": (W_total + G_total + max(W_total, G_total)) // world,
+           "param_grad_comm_bytes": led["peak_param"] + led["peak_grad"] + led["peak_comm"]}
+
+    # ---- e2e through the public API with host buffers (pinned), copies timed
+    e2e = None
+    if rank == 0 or world > 1:
+        hx = x.cpu().pin_memory()
+        hdy = dy.cpu().pin_memory()
+        hdx = torch.empty(M, H, dtype=torch.bfloat16).pin_memory()
+        e2e_steps = max(10, min(args.steps, 100))
+        for _ in range(3):
+            xd = hx.to(dev, non_blocking=True)
+            dyd = hdy.to(dev, non_blocking=True)
+            mlp.zero_grads()
+            mlp.forward([xd])
+            hdx.copy_(mlp.backward([dyd])[0], non_blocking=True)
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(e2e_steps):
+            xd = hx.to(dev, non_blocking=True)
+            dyd = hdy.to(dev, non_blocking=True)
+            mlp.zero_grads()
+            mlp.forward([xd])
+            hdx.copy_(mlp.backward([dyd])[0], non_blocking=True)
+        e1.record(stream)
+        barrier()
+        e2e_ms = e0.elapsed_time(e1) / e2e_steps
+        if world > 1:
+            t = torch.tensor([e2e_ms], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_ms = float(t.item())
+        e2e = {"value": flops_per_step(T) / (e2e_ms * 1e-3) / 1e12, "unit": UNIT,
+               "h2d_bytes_per_step": 2 * M * H * 2, "d2h_bytes_per_step": M * H * 2, "ms_per_step": e2e_ms,
+               "path": "RtpMlp.forward/backward (C ABI) from pinned host X, dY; dX read back"}
+
+    if rank == 0:
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            try:
+                cpu = cpu_reference(target_s=12.0)
+            except Exception as exc:  # noqa
+                cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "unavailable", "sample": repr(exc)}
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "bf16", "data": "synthetic (uniform activations, Flyweight "
+                                                             "SplitMix64 weights, seed 42)",
+                "config": {"workload": "rtp_mlp_768x3072x768 (config b)", "h": H, "f": F,
+                           "tokens_per_gpu": M, "global_tokens": T, "rotation_mode": args.mode,
+                           "parallelism": f"rtp{world}", "l2": "flushed (512 MiB write) before every timed step",
+                           "flops_per_step": flops_per_step(T)},
+                "tflops_per_gpu": value / world,
+                "gpu_launches": int(launches),
+                "roofline": roofline,
+                "memory": mem,
+                "cpu_baseline": cpu,
+                "e2e": e2e,
+                "clocks": clocks.summary()}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

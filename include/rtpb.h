@@ -1,0 +1,232 @@
+/* rtpb.h — C ABI of the B200-native RTP (Rotated Tensor Parallelism) hot path.
+ *
+ * Plain pointers and sizes only; no torch types. Two layers:
+ *
+ *  (1) Step kernels: the device replacement for the reference's op plug-in
+ *      point, the rtp::kern::Kernels table (proj/include/rtp/kernels.hpp:17-47,
+ *      dispatched through kern::active(), proj/src/kernels.cpp:23-27). One call
+ *      = one rotation step of one RtpLinear on one worker, asynchronous on the
+ *      given cudaStream_t. No allocation, no host sync.
+ *
+ *  (2) Group / layer handles: the reference's host API
+ *      (WorkerGroup proj/include/rtp/ring.hpp:65-125, RtpLinear
+ *      proj/include/rtp/layers.hpp:129-147, the ffn1->gelu->ffn2 block of
+ *      proj/src/model.cpp:77-83,99-105) over device shards. The C++ classes in
+ *      include/rtpb/rtp.hpp implement it; these functions expose them to
+ *      FFI callers (ctypes in paper_2311_01635_b200/_lib.py).
+ *
+ * Errors: every function returns RTPB_OK (0) or one of the codes below, which
+ * mirror the reference's exception taxonomy (proj/include/rtp/errors.hpp:8-33);
+ * rtpb_last_error() returns the thread-local message.
+ *
+ * Device dtypes: RTPB_BF16 (bf16 operands, fp32 accumulation) or RTPB_F32
+ * (fp32 operands, 3xTF32 tensor-core products). Gradient shards are fp32.
+ * Alignment: operand base pointers 16-byte aligned, row strides multiples of
+ * 16 bytes (in_dim, out_dim/N multiples of 8) — RTPB_ERR_CONFIG otherwise.
+ */
+#ifndef RTPB_H
+#define RTPB_H
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RTPB_OK 0
+#define RTPB_ERR_GENERIC 1
+#define RTPB_ERR_CONFIG 2    /* rtp::ConfigError    */
+#define RTPB_ERR_DIMENSION 3 /* rtp::DimensionError */
+#define RTPB_ERR_PROTOCOL 4  /* rtp::ProtocolError  */
+#define RTPB_ERR_STATE 5     /* rtp::StateError     */
+#define RTPB_ERR_INDEX 6     /* rtp::IndexError     */
+#define RTPB_ERR_CUDA 7
+#define RTPB_ERR_NCCL 8
+
+#define RTPB_BF16 0
+#define RTPB_F32 1
+
+/* Step-kernel epilogue flags (rtpb_fwd_step / rtpb_dgrad_step). */
+#define RTPB_EPI_GELU 1      /* fwd: also write gelu(pre) to `act` (model.cpp:80)       */
+#define RTPB_EPI_FIRST 2     /* dgrad: first step, overwrite the fp32 accumulator        */
+#define RTPB_EPI_LAST 4      /* dgrad: last step, emit dX in the activation dtype        */
+#define RTPB_EPI_GELU_BWD 8  /* dgrad last step: dX *= gelu'(pre) (model.cpp:101-104)   */
+#define RTPB_EPI_STORE_PRE 16 /* fwd: write X.W_j + b_j to `y` (default for plain linear) */
+
+const char* rtpb_last_error(void);
+const char* rtpb_version(void);
+/* Number of device kernels this library has launched (all threads). */
+uint64_t rtpb_launch_count(void);
+
+/* ------------------------------------------------------------------ */
+/* (1) Step kernels                                                    */
+/* ------------------------------------------------------------------ */
+
+/* Flyweight shard initialisation (replaces Tensor::uniform + split +
+ * shard_view: serial.cpp:329-353, tensor.cpp:99-103, layers_common.cpp:33-45,
+ * partition.cpp:49-56). Writes shard j of a linear I->O whose weight draws
+ * start at SplitMix64 stream index `stream_base`:
+ *   dst[i*per + c]   = U(stream_base + i*O + j*per + c)
+ *   dst[I*per + c]   = U(stream_base + I*O + j*per + c)          (bias)
+ * with U(k) = lo + (hi-lo)*((splitmix64(seed, k) >> 11) * 2^-53) evaluated in
+ * fp64 without contraction, then rounded to nearest into `dtype`. */
+int rtpb_flyweight_init(void* dst, int dtype, uint64_t seed, uint64_t stream_base, size_t I, size_t O,
+                        size_t n, size_t j, double lo, double hi, void* stream);
+
+/* Forward step (layers_linear.cpp:29-37): for the shard w_shard = [W_j | b_j]
+ *   pre = X . W_j + b_j   (M x per)
+ *   y[:, col0 : col0+per]   = pre          if flags & RTPB_EPI_STORE_PRE
+ *   act[:, col0 : col0+per] = gelu(pre)    if flags & RTPB_EPI_GELU
+ * X: M x I (row stride ldx). Workspace: rtpb_step_workspace_bytes(0, ...). */
+int rtpb_fwd_step(int dtype, const void* x, size_t ldx, const void* w_shard, void* y, size_t ldy, size_t col0,
+                  void* act, size_t ld_act, size_t M, size_t I, size_t per, int flags, void* workspace,
+                  size_t workspace_bytes, void* stream);
+
+/* dX step (layers_linear.cpp:65, kern::matmul_nt_acc):
+ *   acc (+)= dY[:, col0:col0+per] . W_j^T     (fp32 accumulator, M x I, ld_acc)
+ * RTPB_EPI_FIRST: acc is overwritten instead of read. RTPB_EPI_LAST: the sum
+ * is written to dx (dtype, ldx) instead of acc, multiplied by gelu'(pre) when
+ * RTPB_EPI_GELU_BWD. FIRST|LAST (N = 1) never touches acc. */
+int rtpb_dgrad_step(int dtype, const void* dy, size_t ldy, size_t col0, const void* w_shard, float* acc,
+                    size_t ld_acc, void* dx, size_t ldx, const void* pre, size_t ldpre, size_t M, size_t I,
+                    size_t per, int flags, void* workspace, size_t workspace_bytes, void* stream);
+
+/* dW step with the travelling-gradient accumulation fused into the epilogue
+ * (layers_linear.cpp:61-63, kern::matmul_tn_acc + bias column sums):
+ *   g_out[0 : I*per]      = g_in[0 : I*per] + X^T . dY[:, col0:col0+per]
+ *   g_out[I*per : +per]   = g_in[I*per : +per] + colsum(dY[:, col0:col0+per])
+ * g_in may equal g_out (in-place accumulation). */
+int rtpb_wgrad_step(int dtype, const void* x, size_t ldx, const void* dy, size_t ldy, size_t col0,
+                    const float* g_in, float* g_out, size_t M, size_t I, size_t per, void* workspace,
+                    size_t workspace_bytes, void* stream);
+
+/* Workspace bytes for a step kernel: which = 0 fwd, 1 dgrad, 2 wgrad. */
+size_t rtpb_step_workspace_bytes(int which, int dtype, size_t M, size_t I, size_t per);
+
+/* Exact-erf GELU and derivative (tensor.cpp:323-351), elementwise. */
+int rtpb_gelu(int dtype, const void* x, void* y, size_t count, void* stream);
+int rtpb_gelu_backward(int dtype, const void* x, const void* upstream, void* out, size_t count, void* stream);
+
+/* Per-launch timing of the step GEMMs: when enabled, a CUDA event pair is
+ * recorded on the launching stream around every step GEMM. profile_read
+ * returns the record count; with cap > 0 it fills kind (0 fwd, 1 dgrad,
+ * 2 wgrad), algorithmic flops and milliseconds, then clears the records. */
+void rtpb_profile_enable(int on);
+size_t rtpb_profile_read(int* kinds, double* flops, float* ms, size_t cap);
+
+/* Test hook: force the GEMM tile width (0 = heuristic; 64/128/256). */
+void rtpb_debug_force_bn(int bn);
+
+/* Ring schedule of an RtpLinear pass, pure host logic shared by every
+ * transport: the logical shard id `rank` holds at (phase, step) — forward
+ * (phase 0) (rank - step) mod n, backward (phase 1) (rank + 1 + step) mod n
+ * (layers_common.cpp:135-151) — and the peers of the rotation that follows
+ * that step (clockwise forward, counter-clockwise backward; ring.cpp:265-293).
+ * send_to / recv_from are -1 after the last step. */
+int rtpb_ring_plan(size_t n, size_t rank, int phase, size_t step, int64_t* logical_id, int64_t* send_to,
+                   int64_t* recv_from);
+
+/* ------------------------------------------------------------------ */
+/* (2) Group / layer handles                                           */
+/* ------------------------------------------------------------------ */
+
+typedef struct rtpb_group_s* rtpb_group;
+typedef struct rtpb_linear_s* rtpb_linear;
+typedef struct rtpb_mlp_s* rtpb_mlp;
+
+#define RTPB_TRANSPORT_LOCKSTEP 0   /* one host thread drives all local workers        */
+#define RTPB_TRANSPORT_CONCURRENT 1 /* one host thread per local worker                */
+#define RTPB_TRANSPORT_NCCL 2       /* one process per GPU, ncclSend/ncclRecv on NVLink */
+
+#define RTPB_MODE_TRAIN 0
+#define RTPB_MODE_EVAL 1
+#define RTPB_ROT_INPLACE 0
+#define RTPB_ROT_OUTOFPLACE 1
+
+/* Memory ledger categories (ledger.hpp:10). */
+#define RTPB_MEM_PARAM 0
+#define RTPB_MEM_GRAD 1
+#define RTPB_MEM_ACTIVATION 2
+#define RTPB_MEM_COMMBUFFER 3
+#define RTPB_MEM_OTHER 4
+
+/* WorkerGroup(n, kind) with all n workers in this process; devices[r] is the
+ * CUDA device of worker r (several workers may share one device: the ring
+ * exchange is then a device-local copy, mirroring the Lockstep transport). */
+int rtpb_group_create(size_t n, int transport, const int* devices, rtpb_group* out);
+/* Distributed group: this process is worker `rank` of `n` on `device`; the
+ * ring exchange is ncclSend/ncclRecv. nccl_id: 128 bytes from
+ * rtpb_nccl_unique_id() on rank 0, broadcast by the caller. */
+int rtpb_nccl_unique_id(void* out128);
+int rtpb_group_create_nccl(size_t n, size_t rank, int device, const void* nccl_id, rtpb_group* out);
+int rtpb_group_destroy(rtpb_group g);
+size_t rtpb_group_size(rtpb_group g);
+/* Local worker ranks hosted by this process (count returned, ranks written). */
+size_t rtpb_group_local_ranks(rtpb_group g, size_t* ranks);
+/* Compute / comm stream of a local worker (cudaStream_t as void*), its device. */
+void* rtpb_group_stream(rtpb_group g, size_t rank, int comm);
+int rtpb_group_device(rtpb_group g, size_t rank);
+int rtpb_group_synchronize(rtpb_group g);
+/* Traffic log (ring.hpp:41-46): kind 0 rotation_cw, 1 rotation_ccw, 2 allgather. */
+size_t rtpb_group_traffic(rtpb_group g, int64_t* kinds, int64_t* w_elems, int64_t* g_elems, size_t cap);
+void rtpb_group_clear_traffic(rtpb_group g);
+/* WorkerGroup::corrupt_next_exchange (ring.cpp:223-238): what 1 = Tag, 2 = ShardId. */
+int rtpb_group_corrupt_next_exchange(rtpb_group g, size_t rank, int what);
+/* Per-worker ledger (ledger.hpp:23-41): current/peak bytes per category, peak total. */
+int rtpb_group_ledger(rtpb_group g, size_t rank, size_t* current5, size_t* peak5, size_t* peak_total);
+int rtpb_group_reset_ledger_peaks(rtpb_group g);
+/* Ring primitive on raw device slots (test / micro-bench entry, ring.cpp:265-333):
+ * weight[r], grad[r]: device buffers of `w_bytes` / `g_bytes` for local rank r.
+ * op: 0 cw(W), 1 ccw(W+G), 2 cw(W+G), 3 ccw(W); spare != NULL -> out-of-place W. */
+int rtpb_group_rotate(rtpb_group g, int op, void** weight, void** grad, void** spare, size_t w_bytes,
+                      size_t g_bytes);
+/* ring_allgather (ring.cpp:335-376) of `bytes` per rank into out (n*bytes). */
+int rtpb_group_allgather(rtpb_group g, void** in, void** out, size_t bytes);
+
+/* RtpLinear(group, label, weight, bias, n) (layers_linear.cpp:6-16): w (I x O)
+ * and b (O) are fp64 host arrays as in the reference; pass w = b = NULL for
+ * Flyweight initialisation from (seed, stream_base) instead — each worker's
+ * shard is generated on its device, the full weight never exists. */
+int rtpb_linear_create(rtpb_group g, const char* label, size_t in_dim, size_t out_dim, int dtype,
+                       const double* w, const double* b, uint64_t seed, uint64_t stream_base, rtpb_linear* out);
+int rtpb_linear_destroy(rtpb_linear l);
+int rtpb_linear_set_rotation_mode(rtpb_linear l, int mode);
+int rtpb_linear_allocate_comm_spares(rtpb_linear l);
+int rtpb_linear_release_comm_spares(rtpb_linear l);
+int rtpb_linear_zero_grads(rtpb_linear l);
+size_t rtpb_linear_shard_len(rtpb_linear l);
+/* forward(x, mode) / backward(dy) (layers_linear.cpp:18-72). x[k], y[k], dy[k],
+ * dx[k]: device activations of the k-th local rank, `rows` rows each,
+ * contiguous (ld = in_dim / out_dim). x must stay valid until backward. */
+int rtpb_linear_forward(rtpb_linear l, const void* const* x, size_t rows, void* const* y, int mode);
+int rtpb_linear_backward(rtpb_linear l, const void* const* dy, size_t rows, void* const* dx);
+/* Slot state of local rank r: logical_id, rotation_offset, device pointers. */
+int rtpb_linear_slot(rtpb_linear l, size_t rank, int64_t* logical_id, int64_t* rotation_offset, void** weight,
+                     void** grad);
+/* Per-(phase, step, rank) logical ids seen by the last forward/backward:
+ * ids[phase*n*n + step*n + rank] (phase 0 fwd, 1 bwd), -1 where not local. */
+int rtpb_linear_trace(rtpb_linear l, int64_t* ids);
+/* Synchronous copy of the shard resident at local rank r into dst (device
+ * memory): which 0 = weight [W_j | b_j] (layer dtype), 1 = grad_acc (fp32). */
+int rtpb_linear_read_shard(rtpb_linear l, size_t rank, int which, void* dst);
+
+/* The FFN block (model.cpp:77-83, 99-105): ffn1 (h->f) -> gelu -> ffn2 (f->h),
+ * GELU fused into ffn1's forward epilogue and ffn2's last dX epilogue.
+ * Flyweight init when w1..b2 are NULL: ffn1 draws from stream_base, ffn2 from
+ * stream_base + h*f + f (SerialModel order, serial.cpp:349-350). */
+int rtpb_mlp_create(rtpb_group g, const char* label, size_t h, size_t f, int dtype, const double* w1,
+                    const double* b1, const double* w2, const double* b2, uint64_t seed, uint64_t stream_base,
+                    rtpb_mlp* out);
+int rtpb_mlp_destroy(rtpb_mlp m);
+int rtpb_mlp_set_rotation_mode(rtpb_mlp m, int mode);
+int rtpb_mlp_begin_step(rtpb_mlp m); /* RtpModel::begin_step (model.cpp:54-57) */
+int rtpb_mlp_zero_grads(rtpb_mlp m);
+int rtpb_mlp_forward(rtpb_mlp m, const void* const* x, size_t rows, void* const* y, int mode);
+int rtpb_mlp_backward(rtpb_mlp m, const void* const* dy, size_t rows, void* const* dx);
+/* layer 0 = ffn1, 1 = ffn2 */
+rtpb_linear rtpb_mlp_layer(rtpb_mlp m, int layer);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RTPB_H */

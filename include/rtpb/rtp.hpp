@@ -1,0 +1,353 @@
+// rtpb/rtp.hpp — C++ host API of the B200-native RTP hot path.
+//
+// Mirrors the reference's layer API (proj/include/rtp/{errors,ledger,ring,
+// layers}.hpp) with device-resident shards: same class names, argument
+// meaning and exception types, so callers written against rtp::RtpLinear /
+// rtp::WorkerGroup switch by changing the namespace and passing device
+// activations. Compute goes through the step kernels of include/rtpb.h;
+// rotation through the group's Transport (device copies in-process, or
+// ncclSend/ncclRecv with one process per GPU).
+#pragma once
+#include <array>
+#include <cstddef>
+#include <cstdint>
+#include <functional>
+#include <memory>
+#include <span>
+#include <stdexcept>
+#include <string>
+#include <string_view>
+#include <vector>
+
+#include "../rtpb.h"
+
+namespace rtpb {
+
+// ---- errors (errors.hpp:8-33) ----
+struct DimensionError : std::invalid_argument {
+  using std::invalid_argument::invalid_argument;
+};
+struct ConfigError : std::invalid_argument {
+  using std::invalid_argument::invalid_argument;
+};
+struct ProtocolError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct StateError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct IndexError : std::out_of_range {
+  using std::out_of_range::out_of_range;
+};
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct NcclError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+// Throws the exception class matching an rtpb.h status code.
+void throw_status(int code, const std::string& msg);
+void check_status(int code);
+
+enum class Mode { Train, Eval };
+enum class RotationMode { InPlace, OutOfPlace };
+enum class Direction { Clockwise, CounterClockwise };
+enum class TransportKind { Lockstep, Concurrent, Nccl };
+enum class PayloadKind { Weight, WeightAndGrad };
+enum class DType { BF16 = RTPB_BF16, F32 = RTPB_F32 };
+inline size_t dtype_size(DType d) { return d == DType::F32 ? 4 : 2; }
+
+// ---- ledger (ledger.hpp:10-41), per worker, device bytes ----
+enum class MemCategory : uint8_t { Param, Grad, Activation, CommBuffer, Other };
+inline constexpr size_t kNumMemCategories = 5;
+
+class MemoryLedger {
+ public:
+  void on_alloc(MemCategory c, size_t bytes);
+  void on_release(MemCategory c, size_t bytes);
+  size_t current(MemCategory c) const { return current_[size_t(c)]; }
+  size_t peak(MemCategory c) const { return peak_[size_t(c)]; }
+  size_t current_total() const { return current_total_; }
+  size_t peak_total() const { return peak_total_; }
+  void reset_peaks();
+
+ private:
+  std::array<size_t, kNumMemCategories> current_{};
+  std::array<size_t, kNumMemCategories> peak_{};
+  size_t current_total_ = 0;
+  size_t peak_total_ = 0;
+};
+
+// Owning device allocation charged to a worker ledger under one category
+// (the device analogue of Tensor::register_bytes, tensor.cpp:86-97).
+class DeviceBuffer {
+ public:
+  DeviceBuffer() = default;
+  DeviceBuffer(int device, size_t bytes, MemoryLedger* ledger, MemCategory cat, bool zero = true);
+  ~DeviceBuffer();
+  DeviceBuffer(const DeviceBuffer&) = delete;
+  DeviceBuffer& operator=(const DeviceBuffer&) = delete;
+  DeviceBuffer(DeviceBuffer&& o) noexcept;
+  DeviceBuffer& operator=(DeviceBuffer&& o) noexcept;
+
+  void* data() const { return ptr_; }
+  size_t bytes() const { return bytes_; }
+  int device() const { return device_; }
+  bool empty() const { return ptr_ == nullptr; }
+  void reset();
+  // Exchange storage between equal-sized buffers without touching either
+  // charge (swap_data, tensor.hpp:65-72): rotation moves contents, not residency.
+  friend void swap_data(DeviceBuffer& a, DeviceBuffer& b);
+
+ private:
+  void* ptr_ = nullptr;
+  size_t bytes_ = 0;
+  int device_ = 0;
+  MemoryLedger* ledger_ = nullptr;
+  MemCategory cat_ = MemCategory::Other;
+};
+
+// ---- ring (ring.hpp:23-46) ----
+struct ShardSlot {
+  DeviceBuffer weight;    // [W_j : I x per | b_j : per] in the layer dtype
+  DeviceBuffer grad_acc;  // same element layout, fp32
+  size_t logical_id = 0;
+  long rotation_offset = 0;
+};
+
+struct CommRecord {
+  std::string label;
+  const char* kind;  // "rotation_cw" | "rotation_ccw" | "allgather"
+  size_t weight_elems_per_worker;
+  size_t grad_elems_per_worker;
+};
+
+struct Worker;
+class Transport;
+
+class WorkerGroup {
+ public:
+  // All n workers in this process; devices[r] hosts worker r (empty: all on
+  // the current device). kind: Lockstep (one host thread) or Concurrent
+  // (a host thread per worker).
+  WorkerGroup(size_t n, TransportKind kind, std::vector<int> devices = {});
+  // One process per GPU: this process is worker `rank` of `n`.
+  WorkerGroup(size_t n, size_t rank, int device, const void* nccl_unique_id);
+  ~WorkerGroup();
+  WorkerGroup(const WorkerGroup&) = delete;
+  WorkerGroup& operator=(const WorkerGroup&) = delete;
+
+  size_t size() const { return n_; }
+  TransportKind kind() const { return kind_; }
+  const std::vector<size_t>& local_ranks() const { return local_; }
+  bool is_local(size_t rank) const;
+  Worker& worker(size_t rank);
+
+  // Runs fn(rank) for every LOCAL rank (all ranks in-process; the own rank
+  // under NCCL), in rank order or one host thread per worker; exceptions are
+  // re-thrown in rank order (ring.cpp:134-174).
+  void each(const std::function<void(size_t)>& fn);
+
+  // Ring steps on slots (ring.cpp:265-333). Device transfers are enqueued on
+  // each worker's comm stream behind its compute stream and the compute
+  // stream then waits for them: stream-ordered, no host sync.
+  // shard_elems: elements per shard, for the traffic log (ring.hpp:41-46).
+  void rotate_clockwise(std::span<ShardSlot> slots, PayloadKind kind = PayloadKind::Weight,
+                        std::string_view label = {}, size_t shard_elems = 0);
+  void rotate_counterclockwise(std::span<ShardSlot> slots, PayloadKind kind = PayloadKind::WeightAndGrad,
+                               std::string_view label = {}, size_t shard_elems = 0);
+  void rotate_outofplace(std::span<ShardSlot> slots, std::span<DeviceBuffer> spares, Direction dir,
+                         PayloadKind kind = PayloadKind::Weight, std::string_view label = {},
+                         size_t shard_elems = 0);
+  // ring_allgather (ring.cpp:335-376): out[r] holds all n chunks in canonical order.
+  void ring_allgather(std::span<void* const> in, std::span<void* const> out, size_t bytes,
+                      std::string_view label = {}, size_t elem_size = 1);
+
+  // Lower-level pieces used by the layers' overlap scheduler.
+  // Raw ring shift of per-local-rank buffers: recv[dest(r)] <- send[r];
+  // send == recv means in place (chunked through a staging buffer).
+  void exchange(Direction dir, std::span<void* const> send, std::span<void* const> recv, size_t bytes);
+  // Advances slot bookkeeping for one hop (ids, offsets, tag, fault hook,
+  // traffic record) exactly as the reference's install_payload does.
+  void advance_slots(std::span<ShardSlot> slots, Direction dir, PayloadKind kind, std::string_view label,
+                     size_t shard_elems);
+
+  // compute stream <-> comm stream fencing per local worker.
+  void comm_after_compute();
+  void compute_after_comm();
+  void synchronize();
+
+  const std::vector<CommRecord>& traffic() const { return traffic_; }
+  void clear_traffic() { traffic_.clear(); }
+  uint64_t next_tag() const { return tag_; }
+  enum class Corrupt { None, Tag, ShardId };
+  void corrupt_next_exchange(size_t rank, Corrupt what);
+
+  MemoryLedger& ledger_of(size_t rank);
+
+ private:
+  friend class Transport;
+  size_t n_;
+  TransportKind kind_;
+  std::vector<size_t> local_;
+  std::vector<std::unique_ptr<Worker>> workers_;  // indexed by rank; null when remote
+  std::unique_ptr<Transport> transport_;
+  std::vector<CommRecord> traffic_;
+  uint64_t tag_ = 0;
+  size_t corrupt_rank_ = 0;
+  Corrupt corrupt_ = Corrupt::None;
+};
+
+// ---- layers (layers.hpp:22-147) ----
+template <typename Saved>
+class ReplayTape {
+ public:
+  void record(size_t logical_id, Saved saved) { entries_.push_back(Entry{logical_id, std::move(saved)}); }
+  Saved replay(size_t resident_id) {
+    if (entries_.empty()) throw StateError("backward invoked without a matching forward");
+    Entry& e = entries_.back();
+    if (e.logical_id != resident_id)
+      throw ProtocolError("shard identity mismatch on replay: resident shard " + std::to_string(resident_id) +
+                          ", tape recorded " + std::to_string(e.logical_id));
+    Saved s = std::move(e.saved);
+    entries_.pop_back();
+    return s;
+  }
+  size_t size() const { return entries_.size(); }
+  bool empty() const { return entries_.empty(); }
+  void clear() { entries_.clear(); }
+
+ private:
+  struct Entry {
+    size_t logical_id;
+    Saved saved;
+  };
+  std::vector<Entry> entries_;
+};
+
+struct Empty {};
+
+// Device activation view for one local rank: rows x cols, row stride ld.
+struct DView {
+  void* data = nullptr;
+  size_t ld = 0;
+};
+
+class RtpLayerBase {
+ public:
+  RtpLayerBase(WorkerGroup& group, std::string label, DType dtype);
+  virtual ~RtpLayerBase() = default;
+
+  const std::string& label() const { return label_; }
+  size_t n() const { return group_->size(); }
+  std::span<ShardSlot> slots() { return slots_; }
+  size_t shard_len() const { return shard_len_; }
+  size_t flat_param_bytes() const { return shard_len_ * n() * dtype_size(dtype_); }
+  size_t flat_grad_bytes() const { return shard_len_ * n() * sizeof(float); }
+  DType dtype() const { return dtype_; }
+
+  virtual void zero_grads();
+  bool all_home() const;
+  void allocate_comm_spares();
+  void release_comm_spares();
+  bool has_comm_spares() const { return !spares_.empty(); }
+  void set_rotation_mode(RotationMode m) { rotation_mode_ = m; }
+  RotationMode rotation_mode() const { return rotation_mode_; }
+  // Logical id seen by (phase 0 fwd / 1 bwd, step, rank) in the last pass.
+  const std::vector<int64_t>& trace() const { return trace_; }
+
+ protected:
+  void init_slots_alloc();
+  void require_home(const char* op) const;
+  void check_forward_position(size_t rank, size_t step) const;
+  void check_backward_position(size_t rank, size_t step) const;
+  void rotate_forward();
+  void rotate_backward();
+  void rehome_after_eval();
+  bool oop() const { return rotation_mode_ == RotationMode::OutOfPlace && !spares_.empty(); }
+
+  WorkerGroup* group_;
+  std::string label_;
+  DType dtype_;
+  std::vector<ShardSlot> slots_;  // indexed by rank (remote entries stay empty)
+  std::vector<DeviceBuffer> spares_;
+  size_t shard_len_ = 0;
+  RotationMode rotation_mode_ = RotationMode::InPlace;
+  std::vector<int64_t> trace_;
+};
+
+// Linear layer sharded on output features (layers_linear.cpp:6-72).
+class RtpLinear : public RtpLayerBase {
+ public:
+  // Host fp64 weight (in x out, row-major) and bias (out), as the reference.
+  RtpLinear(WorkerGroup& group, std::string label, const double* weight, const double* bias, size_t in_dim,
+            size_t out_dim, size_t n, DType dtype = DType::BF16);
+  // Flyweight: shard r generated on worker r's device from SplitMix64(seed)
+  // starting at stream index stream_base; the full weight never exists.
+  RtpLinear(WorkerGroup& group, std::string label, size_t in_dim, size_t out_dim, size_t n, uint64_t seed,
+            uint64_t stream_base, DType dtype = DType::BF16);
+
+  size_t in_dim() const { return in_; }
+  size_t out_dim() const { return out_; }
+  size_t per() const { return per_; }
+
+  // x[k] / y[k]: activations of local rank k (rows x in / rows x out).
+  void forward(std::span<const DView> x, size_t rows, std::span<const DView> y, Mode mode);
+  void backward(std::span<const DView> dy, size_t rows, std::span<const DView> dx);
+
+  // Fused variants used by RtpMlp (GELU in the epilogues).
+  struct FwdEpi {
+    std::span<const DView> act;  // gelu(pre) outputs (nullable span)
+    bool store_pre = true;
+  };
+  struct BwdEpi {
+    std::span<const DView> pre;  // multiply the final dX by gelu'(pre)
+  };
+  void forward_ex(std::span<const DView> x, size_t rows, std::span<const DView> y, Mode mode, const FwdEpi& e);
+  void backward_ex(std::span<const DView> dy, size_t rows, std::span<const DView> dx, const BwdEpi& e);
+
+ private:
+  void build(size_t in_dim, size_t out_dim, size_t n);
+  void ensure_scratch(size_t rows);
+
+  size_t in_ = 0, out_ = 0, per_ = 0;
+  std::vector<ReplayTape<Empty>> tapes_;
+  std::vector<DView> x_cache_;          // per rank: caller-owned X kept for backward
+  std::vector<DeviceBuffer> dx_acc_;    // per rank: fp32 cross-step dX accumulator
+  std::vector<DeviceBuffer> workspace_; // per rank: step-kernel workspace
+  size_t scratch_rows_ = 0;
+  size_t cached_rows_ = 0;
+};
+
+// ffn1 (h -> f) -> gelu -> ffn2 (f -> h), composed as model.cpp:77-83,99-105.
+class RtpMlp {
+ public:
+  RtpMlp(WorkerGroup& group, std::string label, size_t h, size_t f, DType dtype, const double* w1,
+         const double* b1, const double* w2, const double* b2);
+  RtpMlp(WorkerGroup& group, std::string label, size_t h, size_t f, DType dtype, uint64_t seed,
+         uint64_t stream_base);
+
+  void set_rotation_mode(RotationMode m);
+  void begin_step();  // RtpModel::begin_step (model.cpp:54-57)
+  void zero_grads();
+  void forward(std::span<const DView> x, size_t rows, std::span<const DView> y, Mode mode);
+  void backward(std::span<const DView> dy, size_t rows, std::span<const DView> dx);
+  RtpLinear& ffn1() { return *ffn1_; }
+  RtpLinear& ffn2() { return *ffn2_; }
+
+ private:
+  void ensure_acts(size_t rows);
+  WorkerGroup* group_;
+  size_t h_, f_;
+  DType dtype_;
+  RotationMode mode_ = RotationMode::InPlace;
+  std::unique_ptr<RtpLinear> ffn1_, ffn2_;
+  std::vector<DeviceBuffer> pre_, act_, dpre_;  // per rank, rows x f (Activation)
+  size_t act_rows_ = 0;
+};
+
+// Host fp64 -> device dtype, round-to-nearest-even from the double (no
+// double rounding through fp32).
+uint16_t double_to_bf16_rne(double v);
+
+}  // namespace rtpb

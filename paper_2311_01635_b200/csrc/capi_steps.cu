@@ -1,0 +1,256 @@
+// C ABI, layer (1): per-rotation-step kernels (include/rtpb.h). Each entry
+// validates its geometry, carves the caller's workspace and enqueues the
+// tcgen05 GEMM (+ helpers) on the given stream. No allocation, no sync.
+#include <atomic>
+#include <cstdio>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "kernels/launch.hpp"
+
+namespace rtpb {
+
+namespace {
+thread_local std::string g_last_error;
+std::atomic<uint64_t> g_launches{0};
+int g_force_bn = 0;
+
+size_t align256(size_t b) { return (b + 255) & ~size_t(255); }
+
+struct Carve {
+  char* p;
+  size_t left;
+  bool ok = true;
+  float* take(size_t floats) {
+    const size_t b = align256(floats * sizeof(float));
+    if (b > left) {
+      ok = false;
+      return nullptr;
+    }
+    float* r = reinterpret_cast<float*>(p);
+    p += b;
+    left -= b;
+    return r;
+  }
+};
+
+int check_geom(size_t M, size_t I, size_t per) {
+  if (M == 0 || I == 0 || per == 0) return set_error(RTPB_ERR_DIMENSION, "step: dimensions must be positive");
+  if (I % 8 || per % 8)
+    return set_error(RTPB_ERR_CONFIG,
+                     "step: in_dim and out_dim/N must be multiples of 8 for 16-byte TMA rows; choose "
+                     "dimensions that are a multiple of 8 times the worker count");
+  if (M > (1u << 30) || I > (1u << 30) || per > (1u << 30))
+    return set_error(RTPB_ERR_DIMENSION, "step: dimension too large");
+  return RTPB_OK;
+}
+
+cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
+
+// Optional per-launch timing of the step GEMMs: a CUDA event pair recorded on
+// the launching stream around each GEMM (bench.py's roofline numerator).
+struct ProfRec {
+  int kind;
+  double flops;
+  cudaEvent_t a, b;
+};
+std::mutex g_prof_mu;
+bool g_prof_on = false;
+std::vector<ProfRec> g_prof;
+std::vector<cudaEvent_t> g_prof_pool;
+
+cudaEvent_t prof_event() {
+  if (!g_prof_pool.empty()) {
+    cudaEvent_t e = g_prof_pool.back();
+    g_prof_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+
+// Runs `launch` between two recorded events when profiling is on.
+template <class F>
+int timed(int kind, double flops, cudaStream_t s, F&& launch) {
+  if (!g_prof_on) return launch();
+  cudaEvent_t a, b;
+  {
+    std::lock_guard lk(g_prof_mu);
+    a = prof_event();
+    b = prof_event();
+  }
+  cudaEventRecord(a, s);
+  const int rc = launch();
+  cudaEventRecord(b, s);
+  std::lock_guard lk(g_prof_mu);
+  g_prof.push_back({kind, flops, a, b});
+  return rc;
+}
+}  // namespace
+
+int set_error(int code, const char* msg) {
+  g_last_error = msg ? msg : "";
+  return code;
+}
+
+int set_cuda_error(cudaError_t e, const char* where) {
+  char buf[256];
+  std::snprintf(buf, sizeof buf, "%s: %s (%s)", where, cudaGetErrorString(e), cudaGetErrorName(e));
+  g_last_error = buf;
+  return RTPB_ERR_CUDA;
+}
+
+void count_launch(uint64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+}  // namespace rtpb
+
+using namespace rtpb;
+
+extern "C" {
+
+const char* rtpb_last_error(void) { return g_last_error.c_str(); }
+const char* rtpb_version(void) { return "rtpb 0.1 (sm_100a tcgen05)"; }
+uint64_t rtpb_launch_count(void) { return g_launches.load(); }
+void rtpb_debug_force_bn(int bn) { g_force_bn = bn; }
+
+size_t rtpb_step_workspace_bytes(int which, int dtype, size_t M, size_t I, size_t per) {
+  const bool f32 = dtype == RTPB_F32;
+  size_t b = 0;
+  if (which == 2) b += align256(colsum_workspace_bytes(M, per));
+  if (f32) {
+    if (which == 0) b += 2 * align256(M * I * 4) + 2 * align256(I * per * 4);
+    if (which == 1) b += 2 * align256(M * per * 4) + 2 * align256(I * per * 4);
+    if (which == 2) b += 2 * align256(M * I * 4) + 2 * align256(M * per * 4);
+  }
+  return b;
+}
+
+int rtpb_flyweight_init(void* dst, int dtype, uint64_t seed, uint64_t stream_base, size_t I, size_t O, size_t n,
+                        size_t j, double lo, double hi, void* stream) {
+  if (!dst) return set_error(RTPB_ERR_DIMENSION, "flyweight_init: null destination");
+  return flyweight_init(dst, dtype == RTPB_F32, seed, stream_base, I, O, n, j, lo, hi, as_stream(stream));
+}
+
+int rtpb_fwd_step(int dtype, const void* x, size_t ldx, const void* w_shard, void* y, size_t ldy, size_t col0,
+                  void* act, size_t ld_act, size_t M, size_t I, size_t per, int flags, void* workspace,
+                  size_t workspace_bytes, void* stream) {
+  int rc = check_geom(M, I, per);
+  if (rc) return rc;
+  if ((flags & RTPB_EPI_STORE_PRE) && !y) return set_error(RTPB_ERR_DIMENSION, "fwd_step: null y");
+  if ((flags & RTPB_EPI_GELU) && !act) return set_error(RTPB_ERR_DIMENSION, "fwd_step: null act");
+  if (!(flags & (RTPB_EPI_STORE_PRE | RTPB_EPI_GELU))) flags |= RTPB_EPI_STORE_PRE;
+  const bool f32 = dtype == RTPB_F32;
+  const size_t esz = f32 ? 4 : 2;
+  cudaStream_t s = as_stream(stream);
+  StepFwd p{};
+  p.x = x; p.ldx = ldx; p.w = w_shard;
+  p.bias = static_cast<const char*>(w_shard) + I * per * esz;
+  p.y = y; p.ldy = ldy; p.col0 = col0; p.act = act; p.ld_act = ld_act;
+  p.M = M; p.I = I; p.per = per; p.flags = flags; p.force_bn = g_force_bn;
+  if (f32) {
+    Carve c{static_cast<char*>(workspace), workspace ? workspace_bytes : 0};
+    float *xh = c.take(M * I), *xl = c.take(M * I), *wh = c.take(I * per), *wl = c.take(I * per);
+    if (!c.ok) return set_error(RTPB_ERR_DIMENSION, "fwd_step: workspace too small");
+    if ((rc = tf32_split(static_cast<const float*>(x), M, I, ldx, xh, xl, s))) return rc;
+    if ((rc = tf32_split_t(static_cast<const float*>(w_shard), I, per, per, wh, wl, s))) return rc;
+    p.x = xh; p.x_lo = xl; p.ldx = I; p.w = wh; p.w_lo = wl;
+  }
+  return timed(0, 2.0 * M * I * per, s, [&] { return gemm_fwd(f32, p, s); });
+}
+
+int rtpb_dgrad_step(int dtype, const void* dy, size_t ldy, size_t col0, const void* w_shard, float* acc,
+                    size_t ld_acc, void* dx, size_t ldx, const void* pre, size_t ldpre, size_t M, size_t I,
+                    size_t per, int flags, void* workspace, size_t workspace_bytes, void* stream) {
+  int rc = check_geom(M, I, per);
+  if (rc) return rc;
+  const bool first = flags & RTPB_EPI_FIRST, last = flags & RTPB_EPI_LAST;
+  if (!(first && last) && !acc) return set_error(RTPB_ERR_DIMENSION, "dgrad_step: null fp32 accumulator");
+  if (last && !dx) return set_error(RTPB_ERR_DIMENSION, "dgrad_step: null dx");
+  if ((flags & RTPB_EPI_GELU_BWD) && !pre) return set_error(RTPB_ERR_DIMENSION, "dgrad_step: null pre");
+  const bool f32 = dtype == RTPB_F32;
+  const size_t esz = f32 ? 4 : 2;
+  cudaStream_t s = as_stream(stream);
+  StepDgrad p{};
+  p.dy = static_cast<const char*>(dy) + col0 * esz; p.ldy = ldy;
+  p.w = w_shard; p.acc = acc; p.ld_acc = ld_acc; p.dx = dx; p.ldx = ldx; p.pre = pre; p.ldpre = ldpre;
+  p.M = M; p.I = I; p.per = per; p.flags = flags; p.force_bn = g_force_bn;
+  if (f32) {
+    Carve c{static_cast<char*>(workspace), workspace ? workspace_bytes : 0};
+    float *dh = c.take(M * per), *dl = c.take(M * per), *wh = c.take(I * per), *wl = c.take(I * per);
+    if (!c.ok) return set_error(RTPB_ERR_DIMENSION, "dgrad_step: workspace too small");
+    if ((rc = tf32_split(static_cast<const float*>(p.dy), M, per, ldy, dh, dl, s))) return rc;
+    if ((rc = tf32_split(static_cast<const float*>(w_shard), I, per, per, wh, wl, s))) return rc;
+    p.dy = dh; p.dy_lo = dl; p.ldy = per; p.w = wh; p.w_lo = wl;
+  }
+  return timed(1, 2.0 * M * I * per, s, [&] { return gemm_dgrad(f32, p, s); });
+}
+
+int rtpb_wgrad_step(int dtype, const void* x, size_t ldx, const void* dy, size_t ldy, size_t col0,
+                    const float* g_in, float* g_out, size_t M, size_t I, size_t per, void* workspace,
+                    size_t workspace_bytes, void* stream) {
+  int rc = check_geom(M, I, per);
+  if (rc) return rc;
+  if (!g_in || !g_out) return set_error(RTPB_ERR_DIMENSION, "wgrad_step: null gradient shard");
+  const bool f32 = dtype == RTPB_F32;
+  const size_t esz = f32 ? 4 : 2;
+  cudaStream_t s = as_stream(stream);
+  Carve c{static_cast<char*>(workspace), workspace ? workspace_bytes : 0};
+  float* part = c.take(colsum_workspace_bytes(M, per) / sizeof(float));
+  StepWgrad p{};
+  p.x = x; p.ldx = ldx; p.dy = static_cast<const char*>(dy) + col0 * esz; p.ldy = ldy;
+  p.g_in = g_in; p.g_out = g_out; p.M = M; p.I = I; p.per = per; p.force_bn = g_force_bn;
+  if (f32) {
+    float *xh = c.take(M * I), *xl = c.take(M * I), *dh = c.take(M * per), *dl = c.take(M * per);
+    if (!c.ok) return set_error(RTPB_ERR_DIMENSION, "wgrad_step: workspace too small");
+    if ((rc = tf32_split_t(static_cast<const float*>(x), M, I, ldx, xh, xl, s))) return rc;
+    if ((rc = tf32_split_t(static_cast<const float*>(p.dy), M, per, ldy, dh, dl, s))) return rc;
+    p.x = xh; p.x_lo = xl; p.ldx = M; p.dy = dh; p.dy_lo = dl; p.ldy = M;
+  }
+  if (!c.ok) return set_error(RTPB_ERR_DIMENSION, "wgrad_step: workspace too small");
+  // Bias part first (reads dY only), then the GEMM with the fused G_in + P epilogue.
+  if ((rc = colsum_bias_grad(f32, static_cast<const char*>(dy) + col0 * esz, ldy, M, per, g_in + I * per,
+                             g_out + I * per, part, s)))
+    return rc;
+  return timed(2, 2.0 * M * I * per, s, [&] { return gemm_wgrad(f32, p, s); });
+}
+
+void rtpb_profile_enable(int on) {
+  std::lock_guard lk(g_prof_mu);
+  g_prof_on = on != 0;
+}
+
+size_t rtpb_profile_read(int* kinds, double* flops, float* ms, size_t cap) {
+  std::lock_guard lk(g_prof_mu);
+  const size_t n = g_prof.size();
+  for (size_t i = 0; i < n; ++i) {
+    ProfRec& r = g_prof[i];
+    if (i < cap) {
+      cudaEventSynchronize(r.b);
+      float t = 0.f;
+      cudaEventElapsedTime(&t, r.a, r.b);
+      if (kinds) kinds[i] = r.kind;
+      if (flops) flops[i] = r.flops;
+      if (ms) ms[i] = t;
+    }
+  }
+  if (cap) {  // reading consumes the records
+    for (auto& r : g_prof) {
+      g_prof_pool.push_back(r.a);
+      g_prof_pool.push_back(r.b);
+    }
+    g_prof.clear();
+  }
+  return n;
+}
+
+int rtpb_gelu(int dtype, const void* x, void* y, size_t count, void* stream) {
+  return gelu_fwd(dtype == RTPB_F32, x, y, count, as_stream(stream));
+}
+
+int rtpb_gelu_backward(int dtype, const void* x, const void* upstream, void* out, size_t count, void* stream) {
+  return gelu_bwd(dtype == RTPB_F32, x, upstream, out, count, as_stream(stream));
+}
+
+}  // extern "C"

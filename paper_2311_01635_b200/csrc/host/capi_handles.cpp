@@ -1,0 +1,386 @@
+// C ABI, layer (2): group / layer handles over the C++ classes of
+// include/rtpb/rtp.hpp. Exceptions become status codes + rtpb_last_error().
+#include <nccl.h>
+
+#include <cstring>
+
+#include "kernels/launch.hpp"
+#include "worker.hpp"
+
+using namespace rtpb;
+
+struct rtpb_group_s {
+  std::unique_ptr<WorkerGroup> g;
+};
+struct rtpb_linear_s {
+  rtpb_group_s* grp;
+  std::unique_ptr<RtpLinear> l;
+  bool owned = true;
+};
+struct rtpb_mlp_s {
+  rtpb_group_s* grp;
+  std::unique_ptr<RtpMlp> m;
+  rtpb_linear_s ffn1, ffn2;  // non-owning views for rtpb_mlp_layer
+};
+
+namespace {
+
+template <class F>
+int guard(F&& f) {
+  try {
+    f();
+    return RTPB_OK;
+  } catch (const ConfigError& e) {
+    return set_error(RTPB_ERR_CONFIG, e.what());
+  } catch (const DimensionError& e) {
+    return set_error(RTPB_ERR_DIMENSION, e.what());
+  } catch (const ProtocolError& e) {
+    return set_error(RTPB_ERR_PROTOCOL, e.what());
+  } catch (const StateError& e) {
+    return set_error(RTPB_ERR_STATE, e.what());
+  } catch (const IndexError& e) {
+    return set_error(RTPB_ERR_INDEX, e.what());
+  } catch (const CudaError& e) {
+    return set_error(RTPB_ERR_CUDA, e.what());
+  } catch (const NcclError& e) {
+    return set_error(RTPB_ERR_NCCL, e.what());
+  } catch (const std::exception& e) {
+    return set_error(RTPB_ERR_GENERIC, e.what());
+  }
+}
+
+std::vector<DView> views(const void* const* p, size_t count) {
+  std::vector<DView> v(count);
+  for (size_t k = 0; k < count; ++k) v[k] = {const_cast<void*>(p[k]), 0};
+  return v;
+}
+
+DType dt(int d) {
+  if (d != RTPB_BF16 && d != RTPB_F32) throw ConfigError("unknown dtype " + std::to_string(d));
+  return d == RTPB_F32 ? DType::F32 : DType::BF16;
+}
+
+}  // namespace
+
+extern "C" {
+
+int rtpb_ring_plan(size_t n, size_t rank, int phase, size_t step, int64_t* logical_id, int64_t* send_to,
+                   int64_t* recv_from) {
+  if (n == 0 || rank >= n) return set_error(RTPB_ERR_CONFIG, "ring_plan: rank out of range");
+  if (phase != 0 && phase != 1) return set_error(RTPB_ERR_CONFIG, "ring_plan: phase must be 0 or 1");
+  const size_t s = step % n;
+  if (logical_id) *logical_id = int64_t(phase == 0 ? (rank + n - s) % n : (rank + 1 + s) % n);
+  const bool rotates = step + 1 < n;
+  const Direction d = phase == 0 ? Direction::Clockwise : Direction::CounterClockwise;
+  if (send_to) *send_to = rotates ? int64_t(ring_dest(rank, n, d)) : -1;
+  if (recv_from) *recv_from = rotates ? int64_t(ring_src(rank, n, d)) : -1;
+  return RTPB_OK;
+}
+
+int rtpb_group_create(size_t n, int transport, const int* devices, rtpb_group* out) {
+  return guard([&] {
+    if (transport == RTPB_TRANSPORT_NCCL) throw ConfigError("use rtpb_group_create_nccl for NCCL groups");
+    std::vector<int> dev;
+    if (devices) dev.assign(devices, devices + n);
+    auto h = std::make_unique<rtpb_group_s>();
+    h->g = std::make_unique<WorkerGroup>(
+        n, transport == RTPB_TRANSPORT_CONCURRENT ? TransportKind::Concurrent : TransportKind::Lockstep, dev);
+    *out = h.release();
+  });
+}
+
+int rtpb_nccl_unique_id(void* out128) {
+  return guard([&] {
+    ncclUniqueId id;
+    const ncclResult_t r = ncclGetUniqueId(&id);
+    if (r != ncclSuccess) throw NcclError(std::string("ncclGetUniqueId: ") + ncclGetErrorString(r));
+    static_assert(sizeof(id) == 128, "ncclUniqueId is 128 bytes");
+    std::memcpy(out128, &id, sizeof id);
+  });
+}
+
+int rtpb_group_create_nccl(size_t n, size_t rank, int device, const void* nccl_id, rtpb_group* out) {
+  return guard([&] {
+    auto h = std::make_unique<rtpb_group_s>();
+    h->g = std::make_unique<WorkerGroup>(n, rank, device, nccl_id);
+    *out = h.release();
+  });
+}
+
+int rtpb_group_destroy(rtpb_group g) {
+  return guard([&] { delete g; });
+}
+
+size_t rtpb_group_size(rtpb_group g) { return g ? g->g->size() : 0; }
+
+size_t rtpb_group_local_ranks(rtpb_group g, size_t* ranks) {
+  const auto& l = g->g->local_ranks();
+  if (ranks)
+    for (size_t k = 0; k < l.size(); ++k) ranks[k] = l[k];
+  return l.size();
+}
+
+void* rtpb_group_stream(rtpb_group g, size_t rank, int comm) {
+  try {
+    Worker& w = g->g->worker(rank);
+    return comm ? w.comm : w.compute;
+  } catch (...) {
+    return nullptr;
+  }
+}
+
+int rtpb_group_device(rtpb_group g, size_t rank) {
+  try {
+    return g->g->worker(rank).device;
+  } catch (...) {
+    return -1;
+  }
+}
+
+int rtpb_group_synchronize(rtpb_group g) {
+  return guard([&] { g->g->synchronize(); });
+}
+
+size_t rtpb_group_traffic(rtpb_group g, int64_t* kinds, int64_t* w_elems, int64_t* g_elems, size_t cap) {
+  const auto& t = g->g->traffic();
+  for (size_t k = 0; k < t.size() && k < cap; ++k) {
+    const std::string kind = t[k].kind;
+    if (kinds) kinds[k] = kind == "rotation_cw" ? 0 : kind == "rotation_ccw" ? 1 : 2;
+    if (w_elems) w_elems[k] = int64_t(t[k].weight_elems_per_worker);
+    if (g_elems) g_elems[k] = int64_t(t[k].grad_elems_per_worker);
+  }
+  return t.size();
+}
+
+void rtpb_group_clear_traffic(rtpb_group g) { g->g->clear_traffic(); }
+
+int rtpb_group_corrupt_next_exchange(rtpb_group g, size_t rank, int what) {
+  return guard([&] {
+    g->g->corrupt_next_exchange(rank, what == 1   ? WorkerGroup::Corrupt::Tag
+                                      : what == 2 ? WorkerGroup::Corrupt::ShardId
+                                                  : WorkerGroup::Corrupt::None);
+  });
+}
+
+int rtpb_group_ledger(rtpb_group g, size_t rank, size_t* current5, size_t* peak5, size_t* peak_total) {
+  return guard([&] {
+    MemoryLedger& l = g->g->ledger_of(rank);
+    for (size_t c = 0; c < kNumMemCategories; ++c) {
+      if (current5) current5[c] = l.current(MemCategory(c));
+      if (peak5) peak5[c] = l.peak(MemCategory(c));
+    }
+    if (peak_total) *peak_total = l.peak_total();
+  });
+}
+
+int rtpb_group_reset_ledger_peaks(rtpb_group g) {
+  return guard([&] {
+    for (size_t r : g->g->local_ranks()) g->g->ledger_of(r).reset_peaks();
+  });
+}
+
+int rtpb_group_rotate(rtpb_group g, int op, void** weight, void** grad, void** spare, size_t w_bytes,
+                      size_t g_bytes) {
+  return guard([&] {
+    WorkerGroup& G = *g->g;
+    const size_t n = G.size();
+    const auto& local = G.local_ranks();
+    std::vector<void*> w(n, nullptr), gr(n, nullptr), sp(n, nullptr);
+    for (size_t k = 0; k < local.size(); ++k) {
+      w[local[k]] = weight[k];
+      gr[local[k]] = grad ? grad[k] : nullptr;
+      sp[local[k]] = spare ? spare[k] : nullptr;
+    }
+    const Direction dir = (op == 0 || op == 2) ? Direction::Clockwise : Direction::CounterClockwise;
+    const bool with_grad = op == 1 || op == 2;
+    if (n == 1) return;
+    G.comm_after_compute();
+    G.exchange(dir, w, spare ? sp : w, w_bytes);
+    if (with_grad) G.exchange(dir, gr, gr, g_bytes);
+    G.compute_after_comm();
+    if (spare) {
+      // out-of-place: the received weight is in the spare; copy it home so
+      // the caller's pointers keep their roles (raw-buffer test entry).
+      for (size_t r : local) {
+        Worker& wk = G.worker(r);
+        DeviceGuard dg(wk.device);
+        cuda_check(cudaMemcpyAsync(w[r], sp[r], w_bytes, cudaMemcpyDeviceToDevice, wk.compute), "spare copy");
+      }
+    }
+  });
+}
+
+int rtpb_group_allgather(rtpb_group g, void** in, void** out, size_t bytes) {
+  return guard([&] {
+    WorkerGroup& G = *g->g;
+    const size_t n = G.size();
+    const auto& local = G.local_ranks();
+    std::vector<void*> i(n, nullptr), o(n, nullptr);
+    for (size_t k = 0; k < local.size(); ++k) {
+      i[local[k]] = in[k];
+      o[local[k]] = out[k];
+    }
+    G.ring_allgather(i, o, bytes, "allgather", 1);
+  });
+}
+
+int rtpb_linear_create(rtpb_group g, const char* label, size_t in_dim, size_t out_dim, int dtype, const double* w,
+                       const double* b, uint64_t seed, uint64_t stream_base, rtpb_linear* out) {
+  return guard([&] {
+    auto h = std::make_unique<rtpb_linear_s>();
+    h->grp = g;
+    const size_t n = g->g->size();
+    if ((w == nullptr) != (b == nullptr)) throw DimensionError("linear_create: pass both weight and bias, or neither");
+    if (w)
+      h->l = std::make_unique<RtpLinear>(*g->g, label ? label : "linear", w, b, in_dim, out_dim, n, dt(dtype));
+    else
+      h->l = std::make_unique<RtpLinear>(*g->g, label ? label : "linear", in_dim, out_dim, n, seed, stream_base,
+                                         dt(dtype));
+    *out = h.release();
+  });
+}
+
+int rtpb_linear_destroy(rtpb_linear l) {
+  return guard([&] {
+    if (l && l->owned) delete l;
+  });
+}
+
+int rtpb_linear_set_rotation_mode(rtpb_linear l, int mode) {
+  return guard([&] {
+    l->l->set_rotation_mode(mode == RTPB_ROT_OUTOFPLACE ? RotationMode::OutOfPlace : RotationMode::InPlace);
+  });
+}
+
+int rtpb_linear_allocate_comm_spares(rtpb_linear l) {
+  return guard([&] { l->l->allocate_comm_spares(); });
+}
+
+int rtpb_linear_release_comm_spares(rtpb_linear l) {
+  return guard([&] { l->l->release_comm_spares(); });
+}
+
+int rtpb_linear_zero_grads(rtpb_linear l) {
+  return guard([&] { l->l->zero_grads(); });
+}
+
+size_t rtpb_linear_shard_len(rtpb_linear l) { return l->l->shard_len(); }
+
+int rtpb_linear_forward(rtpb_linear l, const void* const* x, size_t rows, void* const* y, int mode) {
+  return guard([&] {
+    const size_t k = l->grp->g->local_ranks().size();
+    auto xv = views(x, k);
+    auto yv = views(y, k);
+    l->l->forward(xv, rows, yv, mode == RTPB_MODE_EVAL ? Mode::Eval : Mode::Train);
+  });
+}
+
+int rtpb_linear_backward(rtpb_linear l, const void* const* dy, size_t rows, void* const* dx) {
+  return guard([&] {
+    const size_t k = l->grp->g->local_ranks().size();
+    auto dyv = views(dy, k);
+    auto dxv = views(dx, k);
+    l->l->backward(dyv, rows, dxv);
+  });
+}
+
+int rtpb_linear_slot(rtpb_linear l, size_t rank, int64_t* logical_id, int64_t* rotation_offset, void** weight,
+                     void** grad) {
+  return guard([&] {
+    if (!l->grp->g->is_local(rank)) throw IndexError("slot of a non-local rank");
+    ShardSlot& s = l->l->slots()[rank];
+    if (logical_id) *logical_id = int64_t(s.logical_id);
+    if (rotation_offset) *rotation_offset = s.rotation_offset;
+    if (weight) *weight = s.weight.data();
+    if (grad) *grad = s.grad_acc.data();
+  });
+}
+
+int rtpb_linear_trace(rtpb_linear l, int64_t* ids) {
+  return guard([&] {
+    const auto& t = l->l->trace();
+    std::memcpy(ids, t.data(), t.size() * sizeof(int64_t));
+  });
+}
+
+int rtpb_linear_read_shard(rtpb_linear l, size_t rank, int which, void* dst) {
+  return guard([&] {
+    WorkerGroup& G = *l->grp->g;
+    Worker& w = G.worker(rank);
+    DeviceGuard dg(w.device);
+    G.synchronize();
+    const DeviceBuffer& b = which ? l->l->slots()[rank].grad_acc : l->l->slots()[rank].weight;
+    cuda_check(cudaMemcpy(dst, b.data(), b.bytes(), cudaMemcpyDeviceToDevice), "read_shard");
+  });
+}
+
+int rtpb_mlp_create(rtpb_group g, const char* label, size_t h, size_t f, int dtype, const double* w1,
+                    const double* b1, const double* w2, const double* b2, uint64_t seed, uint64_t stream_base,
+                    rtpb_mlp* out) {
+  return guard([&] {
+    auto m = std::make_unique<rtpb_mlp_s>();
+    m->grp = g;
+    const std::string lab = label ? label : "mlp";
+    if (w1 || b1 || w2 || b2) {
+      if (!(w1 && b1 && w2 && b2)) throw DimensionError("mlp_create: pass all four parameters, or none");
+      m->m = std::make_unique<RtpMlp>(*g->g, lab, h, f, dt(dtype), w1, b1, w2, b2);
+    } else {
+      m->m = std::make_unique<RtpMlp>(*g->g, lab, h, f, dt(dtype), seed, stream_base);
+    }
+    m->ffn1.grp = g;
+    m->ffn2.grp = g;
+    m->ffn1.owned = m->ffn2.owned = false;
+    *out = m.release();
+  });
+}
+
+int rtpb_mlp_destroy(rtpb_mlp m) {
+  return guard([&] {
+    if (!m) return;
+    m->ffn1.l.release();
+    m->ffn2.l.release();
+    delete m;
+  });
+}
+
+int rtpb_mlp_set_rotation_mode(rtpb_mlp m, int mode) {
+  return guard([&] {
+    m->m->set_rotation_mode(mode == RTPB_ROT_OUTOFPLACE ? RotationMode::OutOfPlace : RotationMode::InPlace);
+  });
+}
+
+int rtpb_mlp_begin_step(rtpb_mlp m) {
+  return guard([&] { m->m->begin_step(); });
+}
+
+int rtpb_mlp_zero_grads(rtpb_mlp m) {
+  return guard([&] { m->m->zero_grads(); });
+}
+
+int rtpb_mlp_forward(rtpb_mlp m, const void* const* x, size_t rows, void* const* y, int mode) {
+  return guard([&] {
+    const size_t k = m->grp->g->local_ranks().size();
+    auto xv = views(x, k);
+    auto yv = views(y, k);
+    m->m->forward(xv, rows, yv, mode == RTPB_MODE_EVAL ? Mode::Eval : Mode::Train);
+  });
+}
+
+int rtpb_mlp_backward(rtpb_mlp m, const void* const* dy, size_t rows, void* const* dx) {
+  return guard([&] {
+    const size_t k = m->grp->g->local_ranks().size();
+    auto dyv = views(dy, k);
+    auto dxv = views(dx, k);
+    m->m->backward(dyv, rows, dxv);
+  });
+}
+
+rtpb_linear rtpb_mlp_layer(rtpb_mlp m, int layer) {
+  rtpb_linear_s& v = layer == 0 ? m->ffn1 : m->ffn2;
+  // Non-owning view: the unique_ptr aliases the MLP's layer and is released
+  // (never deleted) in rtpb_mlp_destroy.
+  if (!v.l) v.l.reset(layer == 0 ? &m->m->ffn1() : &m->m->ffn2());
+  return &v;
+}
+
+}  // extern "C"

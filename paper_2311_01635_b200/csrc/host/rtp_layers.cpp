@@ -1,0 +1,435 @@
+// RtpLayerBase / RtpLinear / RtpMlp over device shards.
+// Reference: proj/src/layers_common.cpp:97-181, layers_linear.cpp:6-72,
+// model.cpp:54-57,77-83,99-105.
+//
+// Per step the host does the reference's bookkeeping (position laws, replay
+// tape, logical ids, traffic) and enqueues device work:
+//   compute stream : the step GEMMs (rtpb_fwd_step / dgrad / wgrad)
+//   comm stream    : the ring shifts
+// Overlap (out-of-place mode): the shard for step s+1 is sent/received into
+// the spare while step s computes on the resident copy. Backward: the weight
+// shift overlaps dX and dW of the step; the gradient shard (carrying its
+// accumulation) is shifted right after dW and overlaps the next step's dX;
+// the next dW waits only for it. In-place mode: the weight shift follows dX
+// (overlapping dW), the gradient shift follows dW (overlapping the next dX);
+// forward shifts are exposed, as the paper accepts.
+#include <cstring>
+
+#include "worker.hpp"
+
+namespace rtpb {
+
+namespace {
+int dtype_code(DType d) { return d == DType::F32 ? RTPB_F32 : RTPB_BF16; }
+}  // namespace
+
+// ------------------------------------------------------------------ base
+RtpLayerBase::RtpLayerBase(WorkerGroup& group, std::string label, DType dtype)
+    : group_(&group), label_(std::move(label)), dtype_(dtype) {}
+
+void RtpLayerBase::init_slots_alloc() {
+  const size_t n = group_->size();
+  slots_.resize(n);
+  group_->each([&](size_t r) {
+    Worker& w = group_->worker(r);
+    ShardSlot& s = slots_[r];
+    s.weight = DeviceBuffer(w.device, shard_len_ * dtype_size(dtype_), &w.ledger, MemCategory::Param, false);
+    s.grad_acc = DeviceBuffer(w.device, shard_len_ * sizeof(float), &w.ledger, MemCategory::Grad, true);
+    s.logical_id = r;
+    s.rotation_offset = 0;
+  });
+}
+
+void RtpLayerBase::zero_grads() {
+  group_->each([&](size_t r) {
+    Worker& w = group_->worker(r);
+    cuda_check(cudaMemsetAsync(slots_[r].grad_acc.data(), 0, slots_[r].grad_acc.bytes(), w.compute),
+               "zero_grads");
+  });
+}
+
+bool RtpLayerBase::all_home() const {
+  for (size_t r : group_->local_ranks())
+    if (slots_[r].logical_id != r) return false;
+  return true;
+}
+
+void RtpLayerBase::require_home(const char* op) const {
+  if (!all_home()) throw StateError(label_ + ": " + op + " requires every slot at its home position");
+}
+
+void RtpLayerBase::check_forward_position(size_t rank, size_t step) const {
+  int64_t id = 0;
+  check_status(rtpb_ring_plan(group_->size(), rank, 0, step, &id, nullptr, nullptr));
+  const size_t expected = size_t(id);
+  if (slots_[rank].logical_id != expected)
+    throw ProtocolError(label_ + ": worker " + std::to_string(rank) + " holds shard " +
+                        std::to_string(slots_[rank].logical_id) + " at forward step " + std::to_string(step) +
+                        ", expected " + std::to_string(expected));
+}
+
+void RtpLayerBase::check_backward_position(size_t rank, size_t step) const {
+  int64_t id = 0;
+  check_status(rtpb_ring_plan(group_->size(), rank, 1, step, &id, nullptr, nullptr));
+  const size_t expected = size_t(id);
+  if (slots_[rank].logical_id != expected)
+    throw ProtocolError(label_ + ": worker " + std::to_string(rank) + " holds shard " +
+                        std::to_string(slots_[rank].logical_id) + " at backward step " + std::to_string(step) +
+                        ", expected " + std::to_string(expected));
+}
+
+void RtpLayerBase::allocate_comm_spares() {
+  if (group_->size() == 1) return;  // no rotation, no buffer (layers_common.cpp:153-160)
+  // One weight-shard-sized spare per worker, as the reference (shard_len
+  // elements of the weight dtype): the incoming W lands there while the
+  // resident W is still read; gradients move in place (ring.cpp:314,328).
+  spares_.resize(group_->size());
+  const size_t bytes = shard_len_ * dtype_size(dtype_);
+  group_->each([&](size_t r) {
+    Worker& w = group_->worker(r);
+    spares_[r] = DeviceBuffer(w.device, bytes, &w.ledger, MemCategory::CommBuffer, false);
+  });
+}
+
+void RtpLayerBase::release_comm_spares() {
+  group_->synchronize();
+  spares_.clear();
+}
+
+void RtpLayerBase::rotate_forward() {
+  if (oop())
+    group_->rotate_outofplace(slots_, spares_, Direction::Clockwise, PayloadKind::Weight, label_, shard_len_);
+  else
+    group_->rotate_clockwise(slots_, PayloadKind::Weight, label_, shard_len_);
+}
+
+void RtpLayerBase::rotate_backward() {
+  if (oop())
+    group_->rotate_outofplace(slots_, spares_, Direction::CounterClockwise, PayloadKind::WeightAndGrad, label_,
+                              shard_len_);
+  else
+    group_->rotate_counterclockwise(slots_, PayloadKind::WeightAndGrad, label_, shard_len_);
+}
+
+void RtpLayerBase::rehome_after_eval() {
+  if (group_->size() > 1) rotate_forward();
+}
+
+// ------------------------------------------------------------------ linear
+void RtpLinear::build(size_t in_dim, size_t out_dim, size_t n) {
+  if (n != group_->size())
+    throw ConfigError("RtpLinear: n = " + std::to_string(n) + " does not match the group of " +
+                      std::to_string(group_->size()));
+  if (n == 0) throw ConfigError("layout_linear: shard count must be >= 1");
+  if (in_dim == 0 || out_dim == 0) throw ConfigError("layout_linear: dimensions must be positive");
+  if (out_dim % n != 0)
+    throw ConfigError("layout_linear: out_dim " + std::to_string(out_dim) + " not divisible by " +
+                      std::to_string(n) + " shards; choose out_dim as a multiple of the worker count");
+  in_ = in_dim;
+  out_ = out_dim;
+  per_ = out_dim / n;
+  if (in_ % 8 || per_ % 8)
+    throw ConfigError("RtpLinear " + label_ + ": in_dim and out_dim/N must be multiples of 8 on the device path "
+                      "(16-byte TMA rows); choose out_dim as a multiple of 8 times the worker count");
+  shard_len_ = in_ * per_ + per_;
+  init_slots_alloc();
+  tapes_.assign(n, {});
+  x_cache_.assign(n, {});
+  dx_acc_.resize(n);
+  workspace_.resize(n);
+  trace_.assign(2 * n * n, -1);
+}
+
+RtpLinear::RtpLinear(WorkerGroup& group, std::string label, const double* weight, const double* bias,
+                     size_t in_dim, size_t out_dim, size_t n, DType dtype)
+    : RtpLayerBase(group, std::move(label), dtype) {
+  build(in_dim, out_dim, n);
+  // linear_shard_groups + flatten_shards + shard_view (layers_common.cpp:33-45):
+  // shard r = [W[:, r*per:(r+1)*per] row-major | b[r*per:(r+1)*per]].
+  group_->each([&](size_t r) {
+    std::vector<double> host(shard_len_);
+    for (size_t i = 0; i < in_; ++i)
+      std::memcpy(&host[i * per_], weight + i * out_ + r * per_, per_ * sizeof(double));
+    std::memcpy(&host[in_ * per_], bias + r * per_, per_ * sizeof(double));
+    if (dtype_ == DType::F32) {
+      std::vector<float> f(shard_len_);
+      for (size_t e = 0; e < shard_len_; ++e) f[e] = static_cast<float>(host[e]);
+      cuda_check(cudaMemcpy(slots_[r].weight.data(), f.data(), f.size() * 4, cudaMemcpyHostToDevice), "upload");
+    } else {
+      std::vector<uint16_t> h(shard_len_);
+      for (size_t e = 0; e < shard_len_; ++e) h[e] = double_to_bf16_rne(host[e]);
+      cuda_check(cudaMemcpy(slots_[r].weight.data(), h.data(), h.size() * 2, cudaMemcpyHostToDevice), "upload");
+    }
+  });
+}
+
+RtpLinear::RtpLinear(WorkerGroup& group, std::string label, size_t in_dim, size_t out_dim, size_t n,
+                     uint64_t seed, uint64_t stream_base, DType dtype)
+    : RtpLayerBase(group, std::move(label), dtype) {
+  build(in_dim, out_dim, n);
+  group_->each([&](size_t r) {
+    Worker& w = group_->worker(r);
+    check_status(rtpb_flyweight_init(slots_[r].weight.data(), dtype_code(dtype_), seed, stream_base, in_, out_, n,
+                                     r, -0.1, 0.1, w.compute));
+  });
+}
+
+void RtpLinear::ensure_scratch(size_t rows) {
+  if (rows == scratch_rows_) return;
+  group_->synchronize();
+  const size_t n = group_->size();
+  const int dt = dtype_code(dtype_);
+  size_t ws = 0;
+  for (int which = 0; which < 3; ++which) ws = std::max(ws, rtpb_step_workspace_bytes(which, dt, rows, in_, per_));
+  group_->each([&](size_t r) {
+    Worker& w = group_->worker(r);
+    dx_acc_[r] = n > 1 ? DeviceBuffer(w.device, rows * in_ * sizeof(float), &w.ledger, MemCategory::Activation, false)
+                       : DeviceBuffer();
+    workspace_[r] = ws ? DeviceBuffer(w.device, ws, &w.ledger, MemCategory::Other, false) : DeviceBuffer();
+  });
+  scratch_rows_ = rows;
+}
+
+void RtpLinear::forward(std::span<const DView> x, size_t rows, std::span<const DView> y, Mode mode) {
+  forward_ex(x, rows, y, mode, FwdEpi{});
+}
+
+void RtpLinear::backward(std::span<const DView> dy, size_t rows, std::span<const DView> dx) {
+  backward_ex(dy, rows, dx, BwdEpi{});
+}
+
+void RtpLinear::forward_ex(std::span<const DView> x, size_t rows, std::span<const DView> y, Mode mode,
+                           const FwdEpi& e) {
+  require_home("forward");
+  const auto& local = group_->local_ranks();
+  if (x.size() != local.size() || (e.store_pre && y.size() != local.size()))
+    throw DimensionError(label_ + ": forward expects one activation per local worker");
+  if (!e.act.empty() && e.act.size() != local.size())
+    throw DimensionError(label_ + ": forward expects one gelu output per local worker");
+  if (rows == 0) throw DimensionError(label_ + ": forward needs at least one row");
+  const size_t n = group_->size();
+  ensure_scratch(rows);
+  std::vector<size_t> k_of(n, 0);
+  for (size_t k = 0; k < local.size(); ++k) k_of[local[k]] = k;
+  if (mode == Mode::Train) {
+    for (size_t k = 0; k < local.size(); ++k) x_cache_[local[k]] = x[k];
+    cached_rows_ = rows;
+  }
+  std::fill(trace_.begin(), trace_.begin() + n * n, -1);
+  const int dt = dtype_code(dtype_);
+  const bool prefetch = oop();
+  std::vector<void*> wp(n, nullptr), sp(n, nullptr);
+
+  for (size_t s = 0; s < n; ++s) {
+    group_->each([&](size_t r) {
+      check_forward_position(r, s);
+      trace_[s * n + r] = int64_t(slots_[r].logical_id);
+      if (mode == Mode::Train) tapes_[r].record(slots_[r].logical_id, {});
+    });
+    const bool rotate = s + 1 < n;
+    if (rotate && prefetch) {
+      // Shard for step s+1 streams into the spare while step s computes.
+      group_->comm_after_compute();  // spare's last reader (step s-1) is done
+      for (size_t r : local) {
+        wp[r] = slots_[r].weight.data();
+        sp[r] = spares_[r].data();
+      }
+      group_->exchange(Direction::Clockwise, wp, sp, slots_[local[0]].weight.bytes());
+    }
+    group_->each([&](size_t r) {
+      Worker& w = group_->worker(r);
+      const size_t k = k_of[r];
+      const size_t j = slots_[r].logical_id;
+      int flags = e.store_pre ? RTPB_EPI_STORE_PRE : 0;
+      void* act = nullptr;
+      size_t ld_act = 0;
+      if (!e.act.empty()) {
+        flags |= RTPB_EPI_GELU;
+        act = e.act[k].data;
+        ld_act = e.act[k].ld ? e.act[k].ld : out_;
+      }
+      void* yp = e.store_pre ? y[k].data : nullptr;
+      const size_t ldy = e.store_pre && y[k].ld ? y[k].ld : out_;
+      check_status(rtpb_fwd_step(dt, x[k].data, x[k].ld ? x[k].ld : in_, slots_[r].weight.data(), yp, ldy, j * per_,
+                                 act, ld_act, rows, in_, per_, flags, workspace_[r].data(), workspace_[r].bytes(),
+                                 w.compute));
+    });
+    if (!rotate) break;
+    if (prefetch) {
+      group_->compute_after_comm();
+      for (size_t r : local) swap_data(slots_[r].weight, spares_[r]);
+      group_->advance_slots(slots_, Direction::Clockwise, PayloadKind::Weight, label_, shard_len_);
+    } else {
+      rotate_forward();
+    }
+  }
+  if (mode == Mode::Eval) rehome_after_eval();
+}
+
+void RtpLinear::backward_ex(std::span<const DView> dy, size_t rows, std::span<const DView> dx, const BwdEpi& e) {
+  const auto& local = group_->local_ranks();
+  if (dy.size() != local.size() || dx.size() != local.size())
+    throw DimensionError(label_ + ": backward expects one gradient per local worker");
+  const size_t n = group_->size();
+  for (size_t r : local)
+    if (tapes_[r].empty()) throw StateError("backward invoked without a matching forward");
+  if (rows != cached_rows_) throw DimensionError(label_ + ": backward rows differ from the cached forward");
+  std::vector<size_t> k_of(n, 0);
+  for (size_t k = 0; k < local.size(); ++k) k_of[local[k]] = k;
+  std::fill(trace_.begin() + n * n, trace_.end(), -1);
+  const int dt = dtype_code(dtype_);
+  const bool oopm = oop();
+  std::vector<void*> wp(n, nullptr), sp(n, nullptr), gp(n, nullptr);
+
+  for (size_t s = 0; s < n; ++s) {
+    group_->each([&](size_t r) {
+      const size_t j = slots_[r].logical_id;
+      tapes_[r].replay(j);
+      check_backward_position(r, s);
+      trace_[n * n + s * n + r] = int64_t(j);
+    });
+    const bool rotate = s + 1 < n;
+    if (s > 0) {
+      // dX of this step needs the shifted weight.
+      for (size_t r : local) group_->worker(r).wait(Ev::WDone, false);
+    }
+    if (rotate && oopm) {
+      group_->comm_after_compute();
+      for (size_t r : local) {
+        wp[r] = slots_[r].weight.data();
+        sp[r] = spares_[r].data();
+      }
+      group_->exchange(Direction::CounterClockwise, wp, sp, slots_[local[0]].weight.bytes());
+      for (size_t r : local) group_->worker(r).record(Ev::WDone, true);
+    }
+    // dX (+)= dY_j . W_j^T
+    group_->each([&](size_t r) {
+      Worker& w = group_->worker(r);
+      const size_t k = k_of[r];
+      const size_t j = slots_[r].logical_id;
+      int flags = (s == 0 ? RTPB_EPI_FIRST : 0) | (s + 1 == n ? RTPB_EPI_LAST : 0);
+      const void* pre = nullptr;
+      size_t ldpre = 0;
+      if (!e.pre.empty() && s + 1 == n) {
+        flags |= RTPB_EPI_GELU_BWD;
+        pre = e.pre[k].data;
+        ldpre = e.pre[k].ld ? e.pre[k].ld : in_;
+      }
+      float* acc = n > 1 ? static_cast<float*>(dx_acc_[r].data()) : nullptr;
+      check_status(rtpb_dgrad_step(dt, dy[k].data, dy[k].ld ? dy[k].ld : out_, j * per_, slots_[r].weight.data(), acc,
+                                   in_, dx[k].data, dx[k].ld ? dx[k].ld : in_, pre, ldpre, rows, in_, per_, flags,
+                                   workspace_[r].data(), workspace_[r].bytes(), w.compute));
+    });
+    if (rotate && !oopm) {
+      // In place: the weight is free once dX has read it; shift it under dW.
+      group_->comm_after_compute();
+      for (size_t r : local) wp[r] = slots_[r].weight.data();
+      group_->exchange(Direction::CounterClockwise, wp, wp, slots_[local[0]].weight.bytes());
+      for (size_t r : local) group_->worker(r).record(Ev::WDone, true);
+    }
+    if (s > 0) {
+      // dW accumulates into the travelling gradient shard: wait for its arrival.
+      for (size_t r : local) group_->worker(r).wait(Ev::GDone, false);
+    }
+    // G_j += X^T . dY_j (+ bias column sums), in place on the resident shard.
+    group_->each([&](size_t r) {
+      Worker& w = group_->worker(r);
+      const size_t k = k_of[r];
+      const size_t j = slots_[r].logical_id;
+      float* g = static_cast<float*>(slots_[r].grad_acc.data());
+      check_status(rtpb_wgrad_step(dt, x_cache_[r].data, x_cache_[r].ld ? x_cache_[r].ld : in_, dy[k].data,
+                                   dy[k].ld ? dy[k].ld : out_, j * per_, g, g, rows, in_, per_, workspace_[r].data(),
+                                   workspace_[r].bytes(), w.compute));
+    });
+    if (!rotate) break;
+    group_->comm_after_compute();
+    for (size_t r : local) gp[r] = slots_[r].grad_acc.data();
+    group_->exchange(Direction::CounterClockwise, gp, gp, slots_[local[0]].grad_acc.bytes());
+    for (size_t r : local) group_->worker(r).record(Ev::GDone, true);
+    if (oopm)
+      for (size_t r : local) swap_data(slots_[r].weight, spares_[r]);
+    group_->advance_slots(slots_, Direction::CounterClockwise, PayloadKind::WeightAndGrad, label_, shard_len_);
+  }
+  for (size_t r : local) x_cache_[r] = {};
+  require_home("end of backward");
+}
+
+// ------------------------------------------------------------------ MLP
+RtpMlp::RtpMlp(WorkerGroup& group, std::string label, size_t h, size_t f, DType dtype, const double* w1,
+               const double* b1, const double* w2, const double* b2)
+    : group_(&group), h_(h), f_(f), dtype_(dtype) {
+  ffn1_ = std::make_unique<RtpLinear>(group, label + "/ffn1", w1, b1, h, f, group.size(), dtype);
+  ffn2_ = std::make_unique<RtpLinear>(group, label + "/ffn2", w2, b2, f, h, group.size(), dtype);
+}
+
+RtpMlp::RtpMlp(WorkerGroup& group, std::string label, size_t h, size_t f, DType dtype, uint64_t seed,
+               uint64_t stream_base)
+    : group_(&group), h_(h), f_(f), dtype_(dtype) {
+  // SerialModel order (serial.cpp:349-350): ffn1.w, ffn1.b, ffn2.w, ffn2.b.
+  ffn1_ = std::make_unique<RtpLinear>(group, label + "/ffn1", h, f, group.size(), seed, stream_base, dtype);
+  ffn2_ = std::make_unique<RtpLinear>(group, label + "/ffn2", f, h, group.size(), seed, stream_base + h * f + f,
+                                      dtype);
+}
+
+void RtpMlp::set_rotation_mode(RotationMode m) {
+  mode_ = m;
+  ffn1_->set_rotation_mode(m);
+  ffn2_->set_rotation_mode(m);
+}
+
+void RtpMlp::begin_step() {
+  if (mode_ == RotationMode::OutOfPlace) {
+    if (!ffn1_->has_comm_spares()) ffn1_->allocate_comm_spares();
+    if (!ffn2_->has_comm_spares()) ffn2_->allocate_comm_spares();
+  }
+}
+
+void RtpMlp::zero_grads() {
+  ffn1_->zero_grads();
+  ffn2_->zero_grads();
+}
+
+void RtpMlp::ensure_acts(size_t rows) {
+  if (rows == act_rows_) return;
+  group_->synchronize();
+  const size_t n = group_->size();
+  pre_.resize(n);
+  act_.resize(n);
+  group_->each([&](size_t r) {
+    Worker& w = group_->worker(r);
+    const size_t b = rows * f_ * dtype_size(dtype_);
+    pre_[r] = DeviceBuffer(w.device, b, &w.ledger, MemCategory::Activation, false);
+    act_[r] = DeviceBuffer(w.device, b, &w.ledger, MemCategory::Activation, false);
+  });
+  act_rows_ = rows;
+}
+
+void RtpMlp::forward(std::span<const DView> x, size_t rows, std::span<const DView> y, Mode mode) {
+  ensure_acts(rows);
+  const auto& local = group_->local_ranks();
+  std::vector<DView> pre(local.size()), act(local.size());
+  for (size_t k = 0; k < local.size(); ++k) {
+    pre[k] = {pre_[local[k]].data(), f_};
+    act[k] = {act_[local[k]].data(), f_};
+  }
+  // pre = ffn1(x); act = gelu(pre) fused into ffn1's epilogue (model.cpp:77-82)
+  RtpLinear::FwdEpi e1;
+  e1.act = act;
+  e1.store_pre = mode == Mode::Train;
+  ffn1_->forward_ex(x, rows, pre, mode, e1);
+  ffn2_->forward(act, rows, y, mode);  // model.cpp:83
+}
+
+void RtpMlp::backward(std::span<const DView> dy, size_t rows, std::span<const DView> dx) {
+  const auto& local = group_->local_ranks();
+  std::vector<DView> pre(local.size());
+  for (size_t k = 0; k < local.size(); ++k) pre[k] = {pre_[local[k]].data(), f_};
+  // dh = ffn2'(dy); dpre = gelu'(pre, dh) fused into ffn2's last dX epilogue,
+  // written over pre (same element reads then writes it) (model.cpp:99-104)
+  RtpLinear::BwdEpi e2;
+  e2.pre = pre;
+  ffn2_->backward_ex(dy, rows, pre, e2);
+  ffn1_->backward(pre, rows, dx);  // model.cpp:105
+}
+
+}  // namespace rtpb

@@ -1,0 +1,72 @@
+// Internal: per-worker device state and the Transport interface.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <functional>
+#include <span>
+
+#include "rtpb/rtp.hpp"
+
+namespace rtpb {
+
+// RAII cudaSetDevice scope.
+class DeviceGuard {
+ public:
+  explicit DeviceGuard(int dev);
+  ~DeviceGuard();
+
+ private:
+  int prev_ = 0;
+};
+
+void cuda_check(cudaError_t e, const char* where);
+
+// Stream-ordering markers of one worker. Compute: last enqueued compute
+// work; WDone / GDone: completion of the latest weight / gradient exchange.
+enum class Ev : int { Compute = 0, WDone = 1, GDone = 2, Comm = 3, Ready = 4, Consumed = 5, Staged = 6, kCount = 7 };
+
+struct Worker {
+  Worker(size_t rank, int device);
+  ~Worker();
+  size_t rank;
+  int device;
+  cudaStream_t compute = nullptr;
+  cudaStream_t comm = nullptr;
+  cudaEvent_t ev[int(Ev::kCount)] = {};
+  MemoryLedger ledger;
+  DeviceBuffer stage;  // in-place rotation staging chunk (CommBuffer)
+
+  void record(Ev e, bool on_comm) { cuda_check(cudaEventRecord(ev[int(e)], on_comm ? comm : compute), "record"); }
+  void wait(Ev e, bool on_comm) {
+    cuda_check(cudaStreamWaitEvent(on_comm ? comm : compute, ev[int(e)], 0), "wait");
+  }
+  // Staging for an in-place shift of `bytes`: one chunk, charged as CommBuffer.
+  void* staging(size_t bytes, size_t* chunk);
+};
+
+// In-place rotation staging chunk: a small fraction of the shard so the
+// in-place mode stays within its (W+G)/N memory model.
+size_t inplace_chunk_bytes(size_t shard_bytes);
+
+class Transport {
+ public:
+  virtual ~Transport() = default;
+  virtual void each(const std::function<void(size_t)>& fn) = 0;
+  // recv[dest(r)] <- send[r] for every rank r; arrays indexed by rank (only
+  // local entries are read). Enqueued on the comm streams; send == recv at a
+  // rank means in place. On return the comm streams are ordered after the
+  // transfer (both the rank's receive and its send).
+  virtual void shift(Direction dir, std::span<void* const> send, std::span<void* const> recv, size_t bytes) = 0;
+};
+
+std::unique_ptr<Transport> make_local_transport(WorkerGroup& g, bool concurrent);
+std::unique_ptr<Transport> make_nccl_transport(WorkerGroup& g, size_t rank, const void* nccl_id);
+
+inline size_t ring_dest(size_t r, size_t n, Direction d) {
+  return d == Direction::Clockwise ? (r + 1) % n : (r + n - 1) % n;
+}
+inline size_t ring_src(size_t r, size_t n, Direction d) {
+  return d == Direction::Clockwise ? (r + n - 1) % n : (r + 1) % n;
+}
+
+}  // namespace rtpb

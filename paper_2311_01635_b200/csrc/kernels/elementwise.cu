@@ -1,0 +1,266 @@
+// HBM-bound helper kernels of the RTP path: Flyweight shard init, bias-grad
+// column sums, 3xTF32 operand split, standalone GELU. Grid-stride loops with
+// grids sized in multiples of the SM count.
+#include <cuda_bf16.h>
+
+#include "launch.hpp"
+
+namespace rtpb {
+
+namespace {
+
+constexpr uint64_t kGolden = 0x9E3779B97F4A7C15ULL;
+
+__device__ __forceinline__ uint64_t splitmix_at(uint64_t seed, uint64_t k) {
+  // rng.hpp:16-22 in counter form: the k-th next_u64() of SplitMix64(seed).
+  uint64_t z = seed + (k + 1) * kGolden;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+  return z ^ (z >> 31);
+}
+
+int grid_for(size_t work, int threads, int max_waves = 8) {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  size_t blocks = (work + threads - 1) / threads;
+  const size_t cap = size_t(sms) * max_waves;
+  if (blocks > cap) blocks = cap;
+  if (blocks == 0) blocks = 1;
+  return int(blocks);
+}
+
+template <typename T>
+__global__ void flyweight_kernel(T* __restrict__ dst, uint64_t seed, uint64_t base, uint64_t I, uint64_t O,
+                                 uint64_t per, uint64_t j, double lo, double hi) {
+  const uint64_t wn = I * per, total = wn + per;
+  const double span = __dsub_rn(hi, lo);
+  for (uint64_t e = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; e < total;
+       e += uint64_t(gridDim.x) * blockDim.x) {
+    uint64_t k;
+    if (e < wn) {
+      const uint64_t i = e / per, c = e - i * per;
+      k = base + i * O + j * per + c;  // W[i, j*per + c], row-major draw order
+    } else {
+      k = base + I * O + j * per + (e - wn);  // bias follows the weight
+    }
+    // tensor.cpp:99-103 / rng.hpp:25-27 without FMA contraction.
+    const double unit = __dmul_rn(__ull2double_rn(splitmix_at(seed, k) >> 11), 0x1.0p-53);
+    const double v = __dadd_rn(lo, __dmul_rn(span, unit));
+    if constexpr (sizeof(T) == 4)
+      dst[e] = __double2float_rn(v);
+    else
+      dst[e] = __double2bfloat16(v);
+  }
+}
+
+// Phase 1: partial column sums of a strided M x per block over row splits.
+// Block = 32 row lanes x 8 column groups of 8 columns (64 columns).
+template <bool F32>
+__global__ void colsum_partial_kernel(const void* __restrict__ dy, size_t ldy, int M, int per, int rows_per_split,
+                                      float* __restrict__ partial) {
+  __shared__ float red[32][65];
+  const int cg = threadIdx.x & 7, rl = threadIdx.x >> 3;  // 8 col groups, 32 row lanes
+  const int c0 = blockIdx.x * 64 + cg * 8;
+  const int r_begin = blockIdx.y * rows_per_split;
+  const int r_end = min(M, r_begin + rows_per_split);
+  float s[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  if (c0 < per) {
+    for (int r = r_begin + rl; r < r_end; r += 32) {
+      if constexpr (F32) {
+        const float4* p = reinterpret_cast<const float4*>(static_cast<const float*>(dy) + size_t(r) * ldy + c0);
+        const float4 a = p[0], b = p[1];
+        s[0] += a.x; s[1] += a.y; s[2] += a.z; s[3] += a.w; s[4] += b.x; s[5] += b.y; s[6] += b.z; s[7] += b.w;
+      } else {
+        const uint4 u = *reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(dy) + size_t(r) * ldy + c0);
+        const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          s[2 * q] += __uint_as_float(w[q] << 16);
+          s[2 * q + 1] += __uint_as_float(w[q] & 0xFFFF0000u);
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < 8; ++q) red[rl][cg * 8 + q] = s[q];
+  __syncthreads();
+  if (threadIdx.x < 64) {
+    const int c = blockIdx.x * 64 + threadIdx.x;
+    float acc = 0.f;
+    for (int l = 0; l < 32; ++l) acc += red[l][threadIdx.x];  // fixed order: deterministic
+    if (c < per) partial[size_t(blockIdx.y) * per + c] = acc;
+  }
+}
+
+__global__ void colsum_final_kernel(const float* __restrict__ partial, int splits, int per,
+                                    const float* __restrict__ g_in, float* __restrict__ g_out) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= per) return;
+  float acc = 0.f;
+  for (int s = 0; s < splits; ++s) acc += partial[size_t(s) * per + c];
+  g_out[c] = g_in[c] + acc;
+}
+
+int colsum_splits(size_t M, size_t per) {
+  const int col_blocks = int((per + 63) / 64);
+  int splits = (2 * 148 + col_blocks - 1) / col_blocks;  // ~2 waves of CTAs
+  const int max_splits = int((M + 255) / 256);         // >= 256 rows per split
+  if (splits > max_splits) splits = max_splits;
+  return splits < 1 ? 1 : splits;
+}
+
+__global__ void tf32_split_kernel(const float* __restrict__ src, size_t rows, size_t cols, size_t ld,
+                                  float* __restrict__ hi, float* __restrict__ lo) {
+  const size_t total = rows * cols;
+  for (size_t e = blockIdx.x * size_t(blockDim.x) + threadIdx.x; e < total; e += size_t(gridDim.x) * blockDim.x) {
+    const size_t r = e / cols, c = e - r * cols;
+    const float x = src[r * ld + c];
+    const float h = __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);  // exactly representable in tf32
+    hi[e] = h;
+    lo[e] = x - h;  // exact in fp32
+  }
+}
+
+// Split + transpose through a 32x32 smem tile: out[c][r] (ld_out = rows).
+__global__ void tf32_split_t_kernel(const float* __restrict__ src, size_t rows, size_t cols, size_t ld,
+                                    float* __restrict__ hi, float* __restrict__ lo) {
+  __shared__ float tile[32][33];
+  const size_t r0 = size_t(blockIdx.y) * 32, c0 = size_t(blockIdx.x) * 32;
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const size_t r = r0 + i, c = c0 + threadIdx.x;
+    tile[i][threadIdx.x] = (r < rows && c < cols) ? src[r * ld + c] : 0.f;
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const size_t c = c0 + i, r = r0 + threadIdx.x;
+    if (r < rows && c < cols) {
+      const float x = tile[threadIdx.x][i];
+      const float h = __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
+      hi[c * rows + r] = h;
+      lo[c * rows + r] = x - h;
+    }
+  }
+}
+
+template <typename T>
+__device__ __forceinline__ float ld_f(const T* p, size_t i) {
+  if constexpr (sizeof(T) == 4) return p[i];
+  else return __bfloat162float(p[i]);
+}
+template <typename T>
+__device__ __forceinline__ void st_f(T* p, size_t i, float v) {
+  if constexpr (sizeof(T) == 4) p[i] = v;
+  else p[i] = __float2bfloat16_rn(v);
+}
+
+template <typename T>
+__global__ void gelu_kernel(const T* __restrict__ x, T* __restrict__ y, size_t n) {
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x) {
+    const float v = ld_f(x, i);
+    st_f(y, i, v * 0.5f * (1.0f + erff(v * 0.70710678118654752f)));
+  }
+}
+
+template <typename T>
+__global__ void gelu_bwd_kernel(const T* __restrict__ x, const T* __restrict__ up, T* __restrict__ out, size_t n) {
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x) {
+    const float v = ld_f(x, i);
+    const float phi = 0.5f * (1.0f + erff(v * 0.70710678118654752f));
+    const float pdf = 0.39894228040143267794f * __expf(-0.5f * v * v);
+    st_f(out, i, ld_f(up, i) * (phi + v * pdf));
+  }
+}
+
+__global__ void cast_kernel(const float* __restrict__ src, __nv_bfloat16* __restrict__ dst, size_t n) {
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x)
+    dst[i] = __float2bfloat16_rn(src[i]);
+}
+
+int post_launch(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_cuda_error(e, what);
+  count_launch();
+  return RTPB_OK;
+}
+
+}  // namespace
+
+int flyweight_init(void* dst, bool f32, uint64_t seed, uint64_t base, size_t I, size_t O, size_t n, size_t j,
+                   double lo, double hi, cudaStream_t s) {
+  if (n == 0 || O % n) return set_error(RTPB_ERR_CONFIG, "flyweight_init: out_dim not divisible by n");
+  if (j >= n) return set_error(RTPB_ERR_CONFIG, "flyweight_init: shard index out of range");
+  const size_t per = O / n, total = I * per + per;
+  const int grid = grid_for(total, 256);
+  if (f32)
+    flyweight_kernel<float><<<grid, 256, 0, s>>>(static_cast<float*>(dst), seed, base, I, O, per, j, lo, hi);
+  else
+    flyweight_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(static_cast<__nv_bfloat16*>(dst), seed, base, I, O, per,
+                                                         j, lo, hi);
+  return post_launch("flyweight_kernel");
+}
+
+size_t colsum_workspace_bytes(size_t M, size_t per) {
+  return size_t(colsum_splits(M, per)) * per * sizeof(float);
+}
+
+int colsum_bias_grad(bool f32, const void* dy, size_t ldy, size_t M, size_t per, const float* g_in, float* g_out,
+                     void* ws, cudaStream_t s) {
+  if (per % 8) return set_error(RTPB_ERR_CONFIG, "bias grad: per must be a multiple of 8");
+  const int splits = colsum_splits(M, per);
+  const int rows_per_split = int((M + splits - 1) / splits);
+  dim3 grid(unsigned((per + 63) / 64), unsigned(splits));
+  float* partial = static_cast<float*>(ws);
+  if (f32)
+    colsum_partial_kernel<true><<<grid, 256, 0, s>>>(dy, ldy, int(M), int(per), rows_per_split, partial);
+  else
+    colsum_partial_kernel<false><<<grid, 256, 0, s>>>(dy, ldy, int(M), int(per), rows_per_split, partial);
+  int rc = post_launch("colsum_partial_kernel");
+  if (rc) return rc;
+  colsum_final_kernel<<<unsigned((per + 255) / 256), 256, 0, s>>>(partial, splits, int(per), g_in, g_out);
+  return post_launch("colsum_final_kernel");
+}
+
+int tf32_split(const float* src, size_t rows, size_t cols, size_t ld, float* hi, float* lo, cudaStream_t s) {
+  tf32_split_kernel<<<grid_for(rows * cols, 256), 256, 0, s>>>(src, rows, cols, ld, hi, lo);
+  return post_launch("tf32_split_kernel");
+}
+
+int tf32_split_t(const float* src, size_t rows, size_t cols, size_t ld, float* hi, float* lo, cudaStream_t s) {
+  dim3 grid(unsigned((cols + 31) / 32), unsigned((rows + 31) / 32));
+  tf32_split_t_kernel<<<grid, dim3(32, 8), 0, s>>>(src, rows, cols, ld, hi, lo);
+  return post_launch("tf32_split_t_kernel");
+}
+
+int gelu_fwd(bool f32, const void* x, void* y, size_t n, cudaStream_t s) {
+  const int g = grid_for(n, 256);
+  if (f32)
+    gelu_kernel<float><<<g, 256, 0, s>>>(static_cast<const float*>(x), static_cast<float*>(y), n);
+  else
+    gelu_kernel<__nv_bfloat16><<<g, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(x),
+                                                  static_cast<__nv_bfloat16*>(y), n);
+  return post_launch("gelu_kernel");
+}
+
+int gelu_bwd(bool f32, const void* x, const void* up, void* out, size_t n, cudaStream_t s) {
+  const int g = grid_for(n, 256);
+  if (f32)
+    gelu_bwd_kernel<float><<<g, 256, 0, s>>>(static_cast<const float*>(x), static_cast<const float*>(up),
+                                              static_cast<float*>(out), n);
+  else
+    gelu_bwd_kernel<__nv_bfloat16><<<g, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(x),
+                                                      static_cast<const __nv_bfloat16*>(up),
+                                                      static_cast<__nv_bfloat16*>(out), n);
+  return post_launch("gelu_bwd_kernel");
+}
+
+int cast_f32_to_bf16(const float* src, void* dst, size_t n, cudaStream_t s) {
+  cast_kernel<<<grid_for(n, 256), 256, 0, s>>>(src, static_cast<__nv_bfloat16*>(dst), n);
+  return post_launch("cast_kernel");
+}
+
+}  // namespace rtpb

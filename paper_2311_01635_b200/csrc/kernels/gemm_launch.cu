@@ -1,0 +1,213 @@
+// Host-side launchers for the tcgen05 step GEMMs: TMA descriptor encoding,
+// tile-size choice, persistent grid sizing. No allocation, no sync.
+#include <cudaTypedefs.h>
+
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+
+#include "gemm_sm100.cuh"
+#include "launch.hpp"
+
+namespace rtpb {
+
+namespace {
+
+PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+std::once_flag g_encode_once;
+
+cudaError_t get_encode() {
+  std::call_once(g_encode_once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  });
+  return g_encode ? cudaSuccess : cudaErrorNotSupported;
+}
+
+// 2-D row-major operand: `outer` rows of `inner` contiguous elements, row
+// stride `ld` elements; box = box_inner x box_outer elements, SWIZZLE_128B.
+int encode_2d(CUtensorMap* m, const void* ptr, bool f32, uint64_t inner, uint64_t outer, uint64_t ld,
+              uint32_t box_inner, uint32_t box_outer) {
+  if (get_encode() != cudaSuccess) return set_error(RTPB_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  const uint64_t esz = f32 ? 4 : 2;
+  if ((reinterpret_cast<uintptr_t>(ptr) & 15) || (ld * esz) % 16)
+    return set_error(RTPB_ERR_CONFIG,
+                     "operand base must be 16-byte aligned and its row stride a multiple of 16 bytes "
+                     "(choose dimensions that are multiples of 8)");
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {ld * esz};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = g_encode(m, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                        const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    char buf[160];
+    std::snprintf(buf, sizeof buf, "cuTensorMapEncodeTiled failed (%d): inner=%llu outer=%llu ld=%llu", int(r),
+                  (unsigned long long)inner, (unsigned long long)outer, (unsigned long long)ld);
+    return set_error(RTPB_ERR_CUDA, buf);
+  }
+  return RTPB_OK;
+}
+
+int sm_count() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+// Operand description: row-major (outer x inner, stride ld) plus whether the
+// GEMM reads it MN-major (inner = the M/N dimension) or K-major (inner = K).
+struct Op {
+  const void* ptr;
+  const void* lo;  // TF32X3 low part (same geometry) or nullptr
+  uint64_t inner, outer, ld;
+};
+
+template <class Cfg>
+int launch_cfg(const Op& a, const Op& b, const GemmArgs& args, cudaStream_t stream) {
+  GemmMaps maps;
+  std::memset(&maps, 0, sizeof maps);
+  constexpr bool F32 = Cfg::TF32;
+  const uint32_t a_box_in = Cfg::A_MN ? Cfg::ATOM_MN : Cfg::BK;
+  const uint32_t a_box_out = Cfg::A_MN ? Cfg::BK : Cfg::BM;
+  const uint32_t b_box_in = Cfg::B_MN ? Cfg::ATOM_MN : Cfg::BK;
+  const uint32_t b_box_out = Cfg::B_MN ? Cfg::BK : Cfg::BN;
+  int rc;
+  if ((rc = encode_2d(&maps.a, a.ptr, F32, a.inner, a.outer, a.ld, a_box_in, a_box_out))) return rc;
+  if ((rc = encode_2d(&maps.b, b.ptr, F32, b.inner, b.outer, b.ld, b_box_in, b_box_out))) return rc;
+  if constexpr (Cfg::TF32) {
+    if ((rc = encode_2d(&maps.a_lo, a.lo, F32, a.inner, a.outer, a.ld, a_box_in, a_box_out))) return rc;
+    if ((rc = encode_2d(&maps.b_lo, b.lo, F32, b.inner, b.outer, b.ld, b_box_in, b_box_out))) return rc;
+  }
+  static bool attr_set = false;  // per instantiation
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(rtp_gemm_kernel<Cfg>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         Cfg::SMEM_BYTES);
+    if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute(gemm)");
+    attr_set = true;
+  }
+  const int tiles = ((args.M + Cfg::BM - 1) / Cfg::BM) * ((args.N + Cfg::BN - 1) / Cfg::BN);
+  const int grid = tiles < sm_count() ? tiles : sm_count();
+  rtp_gemm_kernel<Cfg><<<grid, Cfg::THREADS, Cfg::SMEM_BYTES, stream>>>(maps, args);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_cuda_error(e, "rtp_gemm_kernel launch");
+  count_launch();
+  return RTPB_OK;
+}
+
+// Wave-quantisation aware tile width: minimise ceil(tiles/SMs) * (BN + 48).
+int choose_bn(int M, int N, bool tf32, bool b_mn) {
+  const int cands_bf16[3] = {256, 128, 64};
+  const int cands_tf32[2] = {128, 64};
+  const int* c = tf32 ? cands_tf32 : cands_bf16;
+  const int nc = tf32 ? 2 : 3;
+  const int sms = sm_count();
+  int best = c[nc - 1];
+  long best_cost = -1;
+  for (int i = 0; i < nc; ++i) {
+    const int bn = c[i];
+    if (b_mn && bn % (tf32 ? 32 : 64)) continue;
+    const long tiles = long((M + 127) / 128) * ((N + bn - 1) / bn);
+    const long waves = (tiles + sms - 1) / sms;
+    const long cost = waves * (bn + 48);
+    if (best_cost < 0 || cost < best_cost) {
+      best_cost = cost;
+      best = bn;
+    }
+  }
+  return best;
+}
+
+template <int EPI, bool TF32>
+int dispatch_bn(int bn, const Op& a, const Op& b, const GemmArgs& args, cudaStream_t s) {
+  constexpr int EW = (EPI == EPI_FWD) ? 8 : 4;
+  constexpr bool AMN = !TF32 && EPI == EPI_WGRAD;
+  constexpr bool BMN = !TF32 && EPI != EPI_DGRAD;
+  switch (bn) {
+    case 64: return launch_cfg<GemmCfg<EPI, 64, TF32, EW, AMN, BMN>>(a, b, args, s);
+    case 128: return launch_cfg<GemmCfg<EPI, 128, TF32, EW, AMN, BMN>>(a, b, args, s);
+    default:
+      if constexpr (!TF32) return launch_cfg<GemmCfg<EPI, 256, false, EW, AMN, BMN>>(a, b, args, s);
+      return launch_cfg<GemmCfg<EPI, 128, TF32, EW, AMN, BMN>>(a, b, args, s);
+  }
+}
+
+template <int EPI>
+int dispatch(bool tf32, const Op& a, const Op& b, GemmArgs args, cudaStream_t s, int force_bn) {
+  const bool b_mn = !tf32 && (EPI != EPI_DGRAD);
+  const int bn = force_bn ? force_bn : choose_bn(args.M, args.N, tf32, b_mn);
+  const int num_n = (args.N + bn - 1) / bn;
+  // Raster n fastest when the B operand (all n-blocks x K) fits comfortably in
+  // L2: concurrent CTAs then share each A row-block, which is read once.
+  const double b_bytes = double(num_n) * bn * args.K * (tf32 ? 4.0 : 2.0);
+  args.n_fastest = (EPI != EPI_WGRAD) && b_bytes < 48e6;
+  return tf32 ? dispatch_bn<EPI, true>(bn, a, b, args, s) : dispatch_bn<EPI, false>(bn, a, b, args, s);
+}
+
+}  // namespace
+
+int gemm_fwd(bool f32, const StepFwd& p, cudaStream_t s) {
+  // C[M x per] = X[M x I] . W_j[I x per]; A K-major, B MN-major.
+  Op a{p.x, p.x_lo, p.I, p.M, p.ldx};
+  // bf16: W_j read MN-major in place. tf32: the pre-pass wrote W_j^T (per x I).
+  Op b = f32 ? Op{p.w, p.w_lo, p.I, p.per, p.I} : Op{p.w, p.w_lo, p.per, p.I, p.per};
+  GemmArgs g{};
+  g.M = int(p.M);
+  g.N = int(p.per);
+  g.K = int(p.I);
+  g.flags = p.flags;
+  g.out0 = p.y;
+  g.ld0 = int64_t(p.ldy);
+  g.out1 = p.act;
+  g.ld1 = int64_t(p.ld_act);
+  g.aux = p.bias;
+  g.col0 = int(p.col0);
+  return dispatch<EPI_FWD>(f32, a, b, g, s, p.force_bn);
+}
+
+int gemm_dgrad(bool f32, const StepDgrad& p, cudaStream_t s) {
+  // C[M x I] = dY_blk[M x per] . W_j^T; A K-major (ld = ldy), B = W_j rows (K-major).
+  Op a{p.dy, p.dy_lo, p.per, p.M, p.ldy};
+  Op b{p.w, p.w_lo, p.per, p.I, p.per};
+  GemmArgs g{};
+  g.M = int(p.M);
+  g.N = int(p.I);
+  g.K = int(p.per);
+  g.flags = p.flags;
+  g.out0 = p.dx;
+  g.ld0 = int64_t(p.ldx);
+  g.aux = p.pre;
+  g.ld_aux = int64_t(p.ldpre);
+  g.acc = p.acc;
+  g.ld_acc = int64_t(p.ld_acc);
+  return dispatch<EPI_DGRAD>(f32, a, b, g, s, p.force_bn);
+}
+
+int gemm_wgrad(bool f32, const StepWgrad& p, cudaStream_t s) {
+  // C[I x per] = X^T . dY_blk; A = X read MN-major, B = dY_blk read MN-major.
+  // bf16: X and dY_blk read MN-major in place. tf32: the pre-pass wrote
+  // X^T (I x M) and dY_blk^T (per x M), both K-major.
+  Op a = f32 ? Op{p.x, p.x_lo, p.M, p.I, p.M} : Op{p.x, p.x_lo, p.I, p.M, p.ldx};
+  Op b = f32 ? Op{p.dy, p.dy_lo, p.M, p.per, p.M} : Op{p.dy, p.dy_lo, p.per, p.M, p.ldy};
+  GemmArgs g{};
+  g.M = int(p.I);
+  g.N = int(p.per);
+  g.K = int(p.M);
+  g.out0 = p.g_out;
+  g.ld0 = int64_t(p.per);
+  g.aux = p.g_in;
+  g.ld_aux = int64_t(p.per);
+  return dispatch<EPI_WGRAD>(f32, a, b, g, s, p.force_bn);
+}
+
+}  // namespace rtpb

@@ -1,0 +1,385 @@
+// Persistent, warp-specialised tcgen05 GEMM for the three per-rotation-step
+// products of an RTP linear (layers_linear.cpp:35, :61, :65):
+//
+//   FWD   : Y[:, col0 + n] = X . W_j + b_j        A = X (K-major), B = W_j (MN-major)
+//           (+ optional exact-erf GELU: writes pre and gelu(pre))
+//   DGRAD : dXacc += dY[:, blk_j] . W_j^T         A = dY blk (K-major), B = W_j (K-major)
+//           (fp32 cross-step accumulator; last step casts, optionally * gelu'(pre))
+//   WGRAD : G_out = G_in + X^T . dY[:, blk_j]     A = X (MN-major), B = dY blk (MN-major)
+//           (the travelling gradient shard is accumulated in the epilogue)
+//
+// Roles (one CTA per SM, grid = min(tiles, SMs), static round-robin tiles):
+//   warp 0        : TMA producer (one elected lane), STAGES-deep smem ring
+//   warp 1        : TMEM allocator + MMA issuer (one elected lane)
+//   warps 2..2+E  : epilogue, TMEM -> registers -> global, double-buffered
+//                   accumulators so tile t's epilogue overlaps tile t+1's MMAs.
+// Tile: BM = 128 rows (UMMA M=128, cta_group::1) x BN columns, BK = 128 bytes
+// of K per stage (64 bf16 / 32 fp32), SWIZZLE_128B operands.
+// TF32X3: fp32 operands split (and, where the GEMM would read them MN-major,
+// transposed to K-major) by a pre-pass into hi (low 13 mantissa bits zeroed)
+// and lo = x - hi; D += Ahi.Bhi + Ahi.Blo + Alo.Bhi on kind::tf32.
+#pragma once
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "ptx.cuh"
+
+namespace rtpb {
+
+enum EpiKind : int { EPI_FWD = 0, EPI_DGRAD = 1, EPI_WGRAD = 2 };
+enum EpiFlags : int {
+  EF_GELU = 1,      // FWD: also emit gelu(pre) into out1
+  EF_FIRST = 2,     // DGRAD: first step (no read of the fp32 accumulator)
+  EF_LAST = 4,      // DGRAD: last step (emit the cast result into out0)
+  EF_GELU_BWD = 8,  // DGRAD last step: multiply by gelu'(pre)
+  EF_STORE_PRE = 16 // FWD: store pre into out0 (else only out1 is written)
+};
+
+struct GemmArgs {
+  int M, N, K;
+  int flags;
+  int n_fastest;       // tile raster: n-block fastest (A streamed once)
+  void* out0;          // FWD: pre/Y (dtype) | DGRAD: dX (dtype) | WGRAD: G_out (f32)
+  int64_t ld0;
+  void* out1;          // FWD: gelu(pre) (dtype)
+  int64_t ld1;
+  const void* aux;     // FWD: bias (dtype) | DGRAD: pre (dtype) | WGRAD: G_in (f32)
+  int64_t ld_aux;
+  float* acc;          // DGRAD: fp32 cross-step accumulator
+  int64_t ld_acc;
+  int col0;            // FWD: column offset of the block in out0/out1
+};
+
+template <int EPI_, int BN_, bool TF32_, int EPI_WARPS_, bool A_MN_, bool B_MN_>
+struct GemmCfg {
+  static constexpr int EPI = EPI_;
+  static constexpr int BM = 128;
+  static constexpr int BN = BN_;
+  static constexpr bool TF32 = TF32_;
+  static constexpr int ELEM = TF32 ? 4 : 2;
+  static constexpr int BK = 128 / ELEM;          // K elements per stage
+  static constexpr int UMMA_K = 32 / ELEM;       // 16 bf16 / 8 tf32
+  static constexpr int KSTEPS = BK / UMMA_K;     // 4
+  static constexpr int ATOM_MN = 128 / ELEM;     // MN elements per 128B swizzle row
+  static constexpr bool A_MN = A_MN_;  // bf16: FWD (K,MN), DGRAD (K,K), WGRAD (MN,MN)
+  static constexpr bool B_MN = B_MN_;  // tf32: always (K,K) — operands pre-transposed
+  static constexpr int A_BYTES = BM * 128;
+  static constexpr int B_BYTES = BN * 128;
+  static constexpr int NOPS = TF32 ? 2 : 1;      // hi (+ lo) copies per operand
+  static constexpr int STAGE_BYTES = NOPS * (A_BYTES + B_BYTES);
+  static constexpr int SMEM_BUDGET = 220 * 1024;
+  static constexpr int STAGES_RAW = (SMEM_BUDGET - 2048) / STAGE_BYTES;
+  static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
+  static constexpr int EPI_WARPS = EPI_WARPS_;
+  static constexpr int THREADS = 64 + 32 * EPI_WARPS;
+  static constexpr int TMEM_COLS = (2 * BN <= 32) ? 32 : (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128
+                                   : (2 * BN <= 256) ? 256 : 512;
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 512 /*barriers*/;
+  static constexpr uint32_t IDESC = ptx::idesc_make(BM, BN, TF32 ? 2 : 1, A_MN, B_MN);
+  static_assert(STAGES >= 2, "not enough shared memory for 2 stages");
+  static_assert(BN % 32 == 0 && BN >= 32 && BN <= 256, "BN");
+};
+
+struct GemmMaps {
+  CUtensorMap a, b, a_lo, b_lo;
+};
+
+namespace detail {
+
+__device__ __forceinline__ float bf16lo(uint32_t u) { return __uint_as_float(u << 16); }
+__device__ __forceinline__ float bf16hi(uint32_t u) { return __uint_as_float(u & 0xFFFF0000u); }
+__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+__device__ __forceinline__ float gelu_f(float x) { return x * 0.5f * (1.0f + erff(x * 0.70710678118654752f)); }
+__device__ __forceinline__ float gelu_grad_f(float x) {
+  const float phi = 0.5f * (1.0f + erff(x * 0.70710678118654752f));
+  const float pdf = 0.39894228040143267794f * __expf(-0.5f * x * x);
+  return phi + x * pdf;
+}
+
+// Load 8 consecutive values of `dtype` (bf16 when !F32) as fp32.
+template <bool F32>
+__device__ __forceinline__ void load8(const void* base, int64_t off, float (&o)[8]) {
+  if constexpr (F32) {
+    const float4* p = reinterpret_cast<const float4*>(static_cast<const float*>(base) + off);
+    float4 a = p[0], b = p[1];
+    o[0] = a.x; o[1] = a.y; o[2] = a.z; o[3] = a.w; o[4] = b.x; o[5] = b.y; o[6] = b.z; o[7] = b.w;
+  } else {
+    uint4 u = *reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(base) + off);
+    o[0] = bf16lo(u.x); o[1] = bf16hi(u.x); o[2] = bf16lo(u.y); o[3] = bf16hi(u.y);
+    o[4] = bf16lo(u.z); o[5] = bf16hi(u.z); o[6] = bf16lo(u.w); o[7] = bf16hi(u.w);
+  }
+}
+template <bool F32>
+__device__ __forceinline__ void store8(void* base, int64_t off, const float (&v)[8]) {
+  if constexpr (F32) {
+    float4* p = reinterpret_cast<float4*>(static_cast<float*>(base) + off);
+    p[0] = make_float4(v[0], v[1], v[2], v[3]);
+    p[1] = make_float4(v[4], v[5], v[6], v[7]);
+  } else {
+    uint4 u;
+    u.x = pack_bf16(v[0], v[1]); u.y = pack_bf16(v[2], v[3]);
+    u.z = pack_bf16(v[4], v[5]); u.w = pack_bf16(v[6], v[7]);
+    *reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(base) + off) = u;
+  }
+}
+__device__ __forceinline__ void load8f(const float* p, float (&o)[8]) {
+  const float4* q = reinterpret_cast<const float4*>(p);
+  float4 a = q[0], b = q[1];
+  o[0] = a.x; o[1] = a.y; o[2] = a.z; o[3] = a.w; o[4] = b.x; o[5] = b.y; o[6] = b.z; o[7] = b.w;
+}
+__device__ __forceinline__ void store8f(float* p, const float (&v)[8]) {
+  float4* q = reinterpret_cast<float4*>(p);
+  q[0] = make_float4(v[0], v[1], v[2], v[3]);
+  q[1] = make_float4(v[4], v[5], v[6], v[7]);
+}
+
+}  // namespace detail
+
+template <class Cfg>
+__global__ void __launch_bounds__(Cfg::THREADS, 1)
+    rtp_gemm_kernel(const __grid_constant__ GemmMaps maps, const GemmArgs args) {
+  using namespace ptx;
+  constexpr int BM = Cfg::BM, BN = Cfg::BN, BK = Cfg::BK, STAGES = Cfg::STAGES;
+  constexpr bool F32 = Cfg::TF32;  // activation / output dtype is fp32 in TF32 mode
+
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* stage_base = smem;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * Cfg::STAGE_BYTES);
+  uint64_t* full_bar = bars;                    // [STAGES]
+  uint64_t* empty_bar = bars + STAGES;          // [STAGES]
+  uint64_t* tfull_bar = bars + 2 * STAGES;      // [2]
+  uint64_t* tempty_bar = bars + 2 * STAGES + 2; // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 4);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  const int num_m = (args.M + BM - 1) / BM;
+  const int num_n = (args.N + BN - 1) / BN;
+  const int num_tiles = num_m * num_n;
+  const int num_kb = (args.K + BK - 1) / BK;
+
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&maps.a);
+    prefetch_tmap(&maps.b);
+    if constexpr (Cfg::TF32) {
+      prefetch_tmap(&maps.a_lo);
+      prefetch_tmap(&maps.b_lo);
+    }
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull_bar[s], 1);
+      mbar_init(&tempty_bar[s], Cfg::EPI_WARPS * 32);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, Cfg::TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  auto tile_coords = [&](int t, int& mb, int& nb) {
+    if (args.n_fastest) {
+      nb = t % num_n;
+      mb = t / num_n;
+    } else {
+      mb = t % num_m;
+      nb = t / num_m;
+    }
+  };
+
+  if (warp == 0) {
+    // ===================== TMA producer =====================
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        int mb, nb;
+        tile_coords(t, mb, nb);
+        const int m0 = mb * BM, n0 = nb * BN;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&empty_bar[stage], phase ^ 1);
+          uint8_t* sA = stage_base + stage * Cfg::STAGE_BYTES;
+          uint8_t* sB = sA + Cfg::A_BYTES;
+          mbar_expect_tx(&full_bar[stage], Cfg::STAGE_BYTES);
+          const int k0 = kb * BK;
+          for (int op = 0; op < Cfg::NOPS; ++op) {
+            const CUtensorMap* ma = op ? &maps.a_lo : &maps.a;
+            const CUtensorMap* mbm = op ? &maps.b_lo : &maps.b;
+            uint8_t* dA = sA + op * (Cfg::A_BYTES + Cfg::B_BYTES);
+            uint8_t* dB = dA + Cfg::A_BYTES;
+            if constexpr (Cfg::A_MN) {
+#pragma unroll
+              for (int c = 0; c < BM / Cfg::ATOM_MN; ++c)
+                tma_load_2d(dA + c * (BK * 128), ma, &full_bar[stage], m0 + c * Cfg::ATOM_MN, k0);
+            } else {
+              tma_load_2d(dA, ma, &full_bar[stage], k0, m0);
+            }
+            if constexpr (Cfg::B_MN) {
+#pragma unroll
+              for (int c = 0; c < BN / Cfg::ATOM_MN; ++c)
+                tma_load_2d(dB + c * (BK * 128), mbm, &full_bar[stage], n0 + c * Cfg::ATOM_MN, k0);
+            } else {
+              tma_load_2d(dB, mbm, &full_bar[stage], k0, n0);
+            }
+          }
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ===================== MMA issuer =====================
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&full_bar[stage], phase);
+          tc_fence_after();
+          const uint32_t a_base = smem_u32(stage_base + stage * Cfg::STAGE_BYTES);
+          const uint32_t b_base = a_base + Cfg::A_BYTES;
+#pragma unroll
+          for (int kk = 0; kk < Cfg::KSTEPS; ++kk) {
+            // K-major: advance 32 B inside the 128B swizzle row.
+            // MN-major: advance UMMA_K rows of 128 B (whole swizzle atoms).
+            const uint32_t a_off = Cfg::A_MN ? kk * Cfg::UMMA_K * 128 : kk * 32;
+            const uint32_t b_off = Cfg::B_MN ? kk * Cfg::UMMA_K * 128 : kk * 32;
+            const uint32_t a_lbo = Cfg::A_MN ? BK * 128 : 16;
+            const uint32_t b_lbo = Cfg::B_MN ? BK * 128 : 16;
+            const uint64_t adesc = sdesc_sw128(a_base + a_off, a_lbo, 1024);
+            const uint64_t bdesc = sdesc_sw128(b_base + b_off, b_lbo, 1024);
+            const uint32_t accum = (kb | kk) != 0;
+            if constexpr (Cfg::TF32) {
+              constexpr uint32_t LO = Cfg::A_BYTES + Cfg::B_BYTES;
+              const uint64_t adesc_lo = sdesc_sw128(a_base + LO + a_off, a_lbo, 1024);
+              const uint64_t bdesc_lo = sdesc_sw128(b_base + LO + b_off, b_lbo, 1024);
+              umma_tf32(d_tmem, adesc, bdesc, Cfg::IDESC, accum);
+              umma_tf32(d_tmem, adesc, bdesc_lo, Cfg::IDESC, 1);
+              umma_tf32(d_tmem, adesc_lo, bdesc, Cfg::IDESC, 1);
+            } else {
+              umma_f16(d_tmem, adesc, bdesc, Cfg::IDESC, accum);
+            }
+          }
+          umma_commit(&empty_bar[stage]);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        umma_commit(&tfull_bar[acc]);
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+      }
+    }
+  } else {
+    // ===================== Epilogue =====================
+    const int ew = warp - 2;          // 0..EPI_WARPS-1
+    const int q = warp & 3;           // TMEM lane quarter this warp may access
+    const int half = ew / 4;          // column interleave when EPI_WARPS == 8
+    constexpr int NSPLIT = Cfg::EPI_WARPS / 4;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      int mb, nb;
+      tile_coords(t, mb, nb);
+      const int m0 = mb * BM, n0 = nb * BN;
+      mbar_wait(&tfull_bar[acc], acc_phase);
+      tc_fence_after();
+      const int row = m0 + q * 32 + lane;
+      const bool row_ok = row < args.M;
+      const uint32_t t_row = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN;
+#pragma unroll 1
+      for (int ch = half; ch < BN / 32; ch += NSPLIT) {
+        const int nc = n0 + ch * 32;
+        if (nc >= args.N) break;  // warp-uniform
+        uint32_t v[32];
+        tmem_ld_32x32b_x32(t_row + ch * 32, v);
+        tmem_ld_wait();
+        if (!row_ok) continue;
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+          const int n = nc + g * 8;
+          if (n >= args.N) break;
+          float x[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) x[e] = __uint_as_float(v[g * 8 + e]);
+          if constexpr (Cfg::EPI == EPI_FWD) {
+            float bias[8];
+            detail::load8<F32>(args.aux, n, bias);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) x[e] += bias[e];
+            const int64_t col = args.col0 + n;
+            if (args.flags & EF_STORE_PRE) detail::store8<F32>(args.out0, row * args.ld0 + col, x);
+            if (args.flags & EF_GELU) {
+              float y[8];
+#pragma unroll
+              for (int e = 0; e < 8; ++e) y[e] = detail::gelu_f(x[e]);
+              detail::store8<F32>(args.out1, row * args.ld1 + col, y);
+            }
+          } else if constexpr (Cfg::EPI == EPI_DGRAD) {
+            float* accp = args.acc + row * args.ld_acc + n;
+            if (!(args.flags & EF_FIRST)) {
+              float old[8];
+              detail::load8f(accp, old);
+#pragma unroll
+              for (int e = 0; e < 8; ++e) x[e] = old[e] + x[e];
+            }
+            if (args.flags & EF_LAST) {
+              if (args.flags & EF_GELU_BWD) {
+                float pre[8];
+                detail::load8<F32>(args.aux, row * args.ld_aux + n, pre);
+#pragma unroll
+                for (int e = 0; e < 8; ++e) x[e] = x[e] * detail::gelu_grad_f(pre[e]);
+              }
+              detail::store8<F32>(args.out0, row * args.ld0 + n, x);
+            } else {
+              detail::store8f(accp, x);
+            }
+          } else {  // EPI_WGRAD: G_out = G_in + P
+            float gin[8];
+            detail::load8f(static_cast<const float*>(args.aux) + row * args.ld_aux + n, gin);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) x[e] = gin[e] + x[e];
+            detail::store8f(static_cast<float*>(args.out0) + row * args.ld0 + n, x);
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&tempty_bar[acc]);
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, Cfg::TMEM_COLS);
+  }
+}
+
+}  // namespace rtpb

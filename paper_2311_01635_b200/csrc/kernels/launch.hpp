@@ -1,0 +1,65 @@
+// Internal launcher interface shared by the kernels and the C-ABI layer.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+
+#include "../../../include/rtpb.h"
+
+namespace rtpb {
+
+// Thread-local error slot behind rtpb_last_error(); returns `code`.
+int set_error(int code, const char* msg);
+int set_cuda_error(cudaError_t e, const char* where);
+// Counts kernel launches issued by this library (bench.py's gpu_launches).
+void count_launch(uint64_t n = 1);
+
+struct StepFwd {
+  const void* x; const void* x_lo; size_t ldx;
+  const void* w; const void* w_lo;  // I x per block of the shard
+  const void* bias;                 // per values (dtype)
+  void* y; size_t ldy; size_t col0; // pre / Y output (EF_STORE_PRE)
+  void* act; size_t ld_act;         // gelu(pre) output (EF_GELU)
+  size_t M, I, per;
+  int flags;
+  int force_bn;
+};
+
+struct StepDgrad {
+  const void* dy; const void* dy_lo; size_t ldy;  // dy points at the column block
+  const void* w; const void* w_lo;
+  float* acc; size_t ld_acc;
+  void* dx; size_t ldx;
+  const void* pre; size_t ldpre;
+  size_t M, I, per;
+  int flags;
+  int force_bn;
+};
+
+struct StepWgrad {
+  const void* x; const void* x_lo; size_t ldx;
+  const void* dy; const void* dy_lo; size_t ldy;  // dy points at the column block
+  const float* g_in; float* g_out;                // I x per block of the grad shard
+  size_t M, I, per;
+  int force_bn;
+};
+
+int gemm_fwd(bool f32, const StepFwd& p, cudaStream_t s);
+int gemm_dgrad(bool f32, const StepDgrad& p, cudaStream_t s);
+int gemm_wgrad(bool f32, const StepWgrad& p, cudaStream_t s);
+
+// elementwise.cu
+int flyweight_init(void* dst, bool f32, uint64_t seed, uint64_t base, size_t I, size_t O, size_t n, size_t j,
+                   double lo, double hi, cudaStream_t s);
+size_t colsum_workspace_bytes(size_t M, size_t per);
+int colsum_bias_grad(bool f32, const void* dy, size_t ldy, size_t M, size_t per, const float* g_in,
+                     float* g_out, void* ws, cudaStream_t s);
+int tf32_split(const float* src, size_t rows, size_t cols, size_t ld, float* hi, float* lo, cudaStream_t s);
+// Split and transpose: hi/lo are cols x rows (row stride = rows).
+int tf32_split_t(const float* src, size_t rows, size_t cols, size_t ld, float* hi, float* lo, cudaStream_t s);
+int gelu_fwd(bool f32, const void* x, void* y, size_t count, cudaStream_t s);
+int gelu_bwd(bool f32, const void* x, const void* up, void* out, size_t count, cudaStream_t s);
+int cast_f32_to_bf16(const float* src, void* dst, size_t count, cudaStream_t s);
+
+}  // namespace rtpb

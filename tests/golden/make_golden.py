@@ -1,0 +1,123 @@
+"""Generate tests/golden/*.npz from the REFERENCE ITSELF.
+
+Runs oracle/_ref/librtpref.so — the unmodified reference sources under
+/root/reference/proj/src compiled by path (oracle/Makefile) behind the
+extern "C" shim oracle/ref_shim.cpp — and stores small inputs and outputs.
+tests/test_oracle.py pins our C restatement (oracle/rtp_oracle.c) to these
+bit-for-bit; the GPU parity tests then compare the CUDA path to the oracle.
+
+Inputs follow the reference's conventions: weights from
+SplitMix64(seed) in SerialModel FFN order (serial.cpp:349-350) with
+U[-0.1, 0.1]; activations X then dY from SplitMix64(seed ^ 0xA5A5A5A5A5A5A5A5)
+(model.cpp:143) with U[-1, 1] (layers_test.cpp:90-91).
+
+Usage: python tests/golden/make_golden.py   (needs /root/reference)
+"""
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, os.path.join(ROOT, "oracle"))
+from oracle import Reference, build_oracle  # noqa: E402
+
+FIX = 0xA5A5A5A5A5A5A5A5
+
+
+def acts(R, seed, rows, i_dim, o_dim):
+    x = R.uniform(seed ^ FIX, 0, rows * i_dim, -1.0, 1.0).reshape(rows, i_dim)
+    dy = R.uniform(seed ^ FIX, rows * i_dim, rows * o_dim, -1.0, 1.0).reshape(rows, o_dim)
+    return x, dy
+
+
+def main():
+    build_oracle(with_ref=True)
+    R = Reference()
+    out = {}
+
+    # 1. SplitMix64 uniform stream (rng.hpp:10-32, tensor.cpp:99-103)
+    out["uniform"] = dict(seed42=R.uniform(42, 0, 4096, -0.1, 0.1),
+                          seed7_skip1000=R.uniform(7, 1000, 512, -1.0, 1.0))
+
+    # 2. Flyweight shards: shard_view(flatten_shards(linear_shard_groups)) for
+    #    both FFN linears of a 2-block stack (block 1 tests the stream base).
+    h, f, blocks, n = 32, 64, 2, 4
+    p = R.mlp_params(42, h, f, blocks)
+    fly = {"h": h, "f": f, "blocks": blocks, "n": n, "seed": 42}
+    off = 0
+    for blk in range(blocks):
+        for name, (i_dim, o_dim) in (("ffn1", (h, f)), ("ffn2", (f, h))):
+            w = p[off: off + i_dim * o_dim].reshape(i_dim, o_dim)
+            b = p[off + i_dim * o_dim: off + i_dim * o_dim + o_dim]
+            fly[f"b{blk}_{name}_base"] = off
+            for j in range(n):
+                fly[f"b{blk}_{name}_s{j}"] = R.linear_shard(w, b, n, j)
+            off += i_dim * o_dim + o_dim
+    out["flyweight"] = fly
+
+    # 3. RtpLinear fwd+bwd (layers_linear.cpp:18-72), N in {1,2,4,8}, both
+    #    rotation modes; plus SerialLinear (serial.cpp:59-77).
+    rows, i_dim, o_dim = 64, 32, 64
+    p = R.mlp_params(3, i_dim, o_dim, 1)
+    w = p[: i_dim * o_dim].reshape(i_dim, o_dim)
+    b = p[i_dim * o_dim: i_dim * o_dim + o_dim]
+    x, dy = acts(R, 3, rows, i_dim, o_dim)
+    lin = {"w": w, "b": b, "x": x, "dy": dy}
+    s = R.serial_linear(w, b, x, dy)
+    for k, v in s.items():
+        lin[f"serial_{k}"] = v
+    for nn in (1, 2, 4, 8):
+        for oop in (0, 1):
+            r = R.rtp_linear(nn, w, b, x, dy, outofplace=bool(oop))
+            for k, v in r.items():
+                lin[f"n{nn}_oop{oop}_{k}"] = v
+    out["linear"] = lin
+
+    # 4. MLP block (model.cpp:77-83, 99-105), N in {1,2,4,8}
+    rows, h, f = 64, 32, 128
+    p = R.mlp_params(42, h, f, 1)
+    w1 = p[: h * f].reshape(h, f)
+    b1 = p[h * f: h * f + f]
+    w2 = p[h * f + f: h * f + f + f * h].reshape(f, h)
+    b2 = p[h * f + f + f * h:]
+    x, dy = acts(R, 42, rows, h, h)
+    mlp = {"w1": w1, "b1": b1, "w2": w2, "b2": b2, "x": x, "dy": dy, "seed": 42}
+    for nn in (1, 2, 4, 8):
+        r = R.rtp_mlp(nn, w1, b1, w2, b2, x, dy)
+        for k, v in r.items():
+            mlp[f"n{nn}_{k}"] = v
+    out["mlp"] = mlp
+
+    # 5. Ring primitive (ring.cpp:265-293) on id-encoded slots (ring_test.cpp:16-28)
+    rng = np.random.default_rng(77)
+    ring = {}
+    for nn in (1, 2, 3, 4, 8):
+        ops = rng.integers(0, 4, size=40).astype(np.int32)
+        r = R.ring_ops(nn, ops.tolist(), length=6)
+        ring[f"n{nn}_ops"] = ops
+        for k, v in r.items():
+            ring[f"n{nn}_{k}"] = v
+    out["ring"] = ring
+
+    # 6. Ledger peaks for one MLP step (analysis.cpp:236-333 style binding)
+    led = {}
+    for nn in (1, 2, 4, 8):
+        for oop in (0, 1):
+            r = R.mlp_ledger(nn, oop, 64, 32, 128)
+            for k, v in r.items():
+                led[f"n{nn}_oop{oop}_{k}"] = np.int64(v)
+    # table1_memory RTP rows (analysis.cpp:45-46): strategy ids 5=Rtp, 6=RtpInplace
+    for st in (5, 6):
+        for N in (1, 2, 4, 8):
+            led[f"table1_s{st}_N{N}"] = np.array(R.table1(st, 1000, 2000, 300, 40, N), np.int64)
+    out["ledger"] = led
+
+    for name, d in out.items():
+        np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **{k: np.asarray(v) for k, v in d.items()})
+        print("wrote", name, len(d), "arrays")
+
+
+if __name__ == "__main__":
+    main()
