@@ -122,7 +122,8 @@ size_t rtpb_step_workspace_bytes(int which, int dtype, size_t M, size_t I, size_
   if (f32) {
     if (which == 0) b += 2 * align256(M * I * 4) + 2 * align256(I * per * 4);
     if (which == 1) b += 2 * align256(M * per * 4) + 2 * align256(I * per * 4);
-    if (which == 2) b += 2 * align256(M * I * 4) + 2 * align256(M * per * 4);
+    const size_t Mp = (M + 7) & ~size_t(7);  // transposed operands: 16-byte rows
+    if (which == 2) b += 2 * align256(Mp * I * 4) + 2 * align256(Mp * per * 4);
   }
   return b;
 }
@@ -202,11 +203,12 @@ int rtpb_wgrad_step(int dtype, const void* x, size_t ldx, const void* dy, size_t
   p.x = x; p.ldx = ldx; p.dy = static_cast<const char*>(dy) + col0 * esz; p.ldy = ldy;
   p.g_in = g_in; p.g_out = g_out; p.M = M; p.I = I; p.per = per; p.force_bn = g_force_bn;
   if (f32) {
-    float *xh = c.take(M * I), *xl = c.take(M * I), *dh = c.take(M * per), *dl = c.take(M * per);
+    const size_t Mp = (M + 7) & ~size_t(7);
+    float *xh = c.take(Mp * I), *xl = c.take(Mp * I), *dh = c.take(Mp * per), *dl = c.take(Mp * per);
     if (!c.ok) return set_error(RTPB_ERR_DIMENSION, "wgrad_step: workspace too small");
     if ((rc = tf32_split_t(static_cast<const float*>(x), M, I, ldx, xh, xl, s))) return rc;
     if ((rc = tf32_split_t(static_cast<const float*>(p.dy), M, per, ldy, dh, dl, s))) return rc;
-    p.x = xh; p.x_lo = xl; p.ldx = M; p.dy = dh; p.dy_lo = dl; p.ldy = M;
+    p.x = xh; p.x_lo = xl; p.ldx = Mp; p.dy = dh; p.dy_lo = dl; p.ldy = Mp;
   }
   if (!c.ok) return set_error(RTPB_ERR_DIMENSION, "wgrad_step: workspace too small");
   // Bias part first (reads dY only), then the GEMM with the fused G_in + P epilogue.

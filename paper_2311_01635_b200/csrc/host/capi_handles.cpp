@@ -9,9 +9,15 @@
 
 using namespace rtpb;
 
+// Layers keep their group alive: the WorkerGroup (worker streams, ledgers)
+// is destroyed only after its last layer, whatever order FFI callers free in.
 struct rtpb_group_s {
   std::unique_ptr<WorkerGroup> g;
+  int refs = 1;
 };
+static void group_release(rtpb_group_s* g) {
+  if (g && --g->refs == 0) delete g;
+}
 struct rtpb_linear_s {
   rtpb_group_s* grp;
   std::unique_ptr<RtpLinear> l;
@@ -108,7 +114,7 @@ int rtpb_group_create_nccl(size_t n, size_t rank, int device, const void* nccl_i
 }
 
 int rtpb_group_destroy(rtpb_group g) {
-  return guard([&] { delete g; });
+  return guard([&] { group_release(g); });
 }
 
 size_t rtpb_group_size(rtpb_group g) { return g ? g->g->size() : 0; }
@@ -236,13 +242,18 @@ int rtpb_linear_create(rtpb_group g, const char* label, size_t in_dim, size_t ou
     else
       h->l = std::make_unique<RtpLinear>(*g->g, label ? label : "linear", in_dim, out_dim, n, seed, stream_base,
                                          dt(dtype));
+    ++g->refs;
     *out = h.release();
   });
 }
 
 int rtpb_linear_destroy(rtpb_linear l) {
   return guard([&] {
-    if (l && l->owned) delete l;
+    if (l && l->owned) {
+      rtpb_group_s* g = l->grp;
+      delete l;
+      group_release(g);
+    }
   });
 }
 
@@ -330,6 +341,7 @@ int rtpb_mlp_create(rtpb_group g, const char* label, size_t h, size_t f, int dty
     m->ffn1.grp = g;
     m->ffn2.grp = g;
     m->ffn1.owned = m->ffn2.owned = false;
+    ++g->refs;
     *out = m.release();
   });
 }
@@ -339,7 +351,9 @@ int rtpb_mlp_destroy(rtpb_mlp m) {
     if (!m) return;
     m->ffn1.l.release();
     m->ffn2.l.release();
+    rtpb_group_s* g = m->grp;
     delete m;
+    group_release(g);
   });
 }
 

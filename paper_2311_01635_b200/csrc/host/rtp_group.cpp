@@ -162,6 +162,7 @@ void* Worker::staging(size_t bytes, size_t* chunk) {
   const size_t want = inplace_chunk_bytes(bytes);
   if (stage.bytes() < want) {
     cuda_check(cudaStreamSynchronize(comm), "stage sync");
+    stage.reset();  // release before growing: one staging chunk is ever resident
     stage = DeviceBuffer(device, want, &ledger, MemCategory::CommBuffer, false);
   }
   *chunk = std::min(stage.bytes(), bytes);

@@ -141,8 +141,9 @@ __global__ void tf32_split_t_kernel(const float* __restrict__ src, size_t rows, 
     if (r < rows && c < cols) {
       const float x = tile[threadIdx.x][i];
       const float h = __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
-      hi[c * rows + r] = h;
-      lo[c * rows + r] = x - h;
+      const size_t ld_out = (rows + 7) & ~size_t(7);  // 16-byte TMA rows
+      hi[c * ld_out + r] = h;
+      lo[c * ld_out + r] = x - h;
     }
   }
 }

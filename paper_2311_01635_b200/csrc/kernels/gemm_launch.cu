@@ -197,8 +197,8 @@ int gemm_wgrad(bool f32, const StepWgrad& p, cudaStream_t s) {
   // C[I x per] = X^T . dY_blk; A = X read MN-major, B = dY_blk read MN-major.
   // bf16: X and dY_blk read MN-major in place. tf32: the pre-pass wrote
   // X^T (I x M) and dY_blk^T (per x M), both K-major.
-  Op a = f32 ? Op{p.x, p.x_lo, p.M, p.I, p.M} : Op{p.x, p.x_lo, p.I, p.M, p.ldx};
-  Op b = f32 ? Op{p.dy, p.dy_lo, p.M, p.per, p.M} : Op{p.dy, p.dy_lo, p.per, p.M, p.ldy};
+  Op a = f32 ? Op{p.x, p.x_lo, p.M, p.I, p.ldx} : Op{p.x, p.x_lo, p.I, p.M, p.ldx};
+  Op b = f32 ? Op{p.dy, p.dy_lo, p.M, p.per, p.ldy} : Op{p.dy, p.dy_lo, p.per, p.M, p.ldy};
   GemmArgs g{};
   g.M = int(p.I);
   g.N = int(p.per);

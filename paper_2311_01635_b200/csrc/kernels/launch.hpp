@@ -56,7 +56,7 @@ size_t colsum_workspace_bytes(size_t M, size_t per);
 int colsum_bias_grad(bool f32, const void* dy, size_t ldy, size_t M, size_t per, const float* g_in,
                      float* g_out, void* ws, cudaStream_t s);
 int tf32_split(const float* src, size_t rows, size_t cols, size_t ld, float* hi, float* lo, cudaStream_t s);
-// Split and transpose: hi/lo are cols x rows (row stride = rows).
+// Split and transpose: hi/lo are cols x rows, row stride round_up(rows, 8).
 int tf32_split_t(const float* src, size_t rows, size_t cols, size_t ld, float* hi, float* lo, cudaStream_t s);
 int gelu_fwd(bool f32, const void* x, void* y, size_t count, cudaStream_t s);
 int gelu_bwd(bool f32, const void* x, const void* up, void* out, size_t count, cudaStream_t s);

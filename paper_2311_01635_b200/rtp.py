@@ -117,14 +117,15 @@ class WorkerGroup:
         check(lib.rtpb_group_reset_ledger_peaks(self._h))
 
     # ---- stream interop: our streams <-> torch's current stream ----
+    # Every call makes the worker streams wait for torch's current stream on
+    # entry and torch's current stream wait for them on exit, so torch's
+    # caching allocator can only reuse a caller tensor's memory after the
+    # library is done with it (no record_stream on library-owned streams,
+    # which may be destroyed before the tensors are freed).
     def _enter(self, tensors_per_rank):
-        for k, r in enumerate(self.local_ranks):
+        for r in self.local_ranks:
             s = self.stream(r)
-            cur = torch.cuda.current_stream(s.device)
-            s.wait_stream(cur)
-            for t in tensors_per_rank[k]:
-                if t is not None:
-                    t.record_stream(s)
+            s.wait_stream(torch.cuda.current_stream(s.device))
 
     def _leave(self):
         for r in self.local_ranks:
@@ -243,6 +244,8 @@ class RtpLinear(_Layer):
         check(lib.rtpb_linear_forward(self._h, ptr_array(xs), rows, ptr_array(ys),
                                       _lib.MODE_EVAL if mode == "eval" else _lib.MODE_TRAIN))
         self.group._leave()
+        if mode != "eval":
+            self._x_keep = list(xs)  # the layer reads X again in backward (x_cache_)
         return ys
 
     def backward(self, dys, out=None):
@@ -251,6 +254,7 @@ class RtpLinear(_Layer):
         self.group._enter([[a, b] for a, b in zip(dys, dxs)])
         check(lib.rtpb_linear_backward(self._h, ptr_array(dys), rows, ptr_array(dxs)))
         self.group._leave()
+        self._x_keep = None
         return dxs
 
     def slot(self, rank: int) -> dict:
@@ -328,6 +332,8 @@ class RtpMlp(_Layer):
         check(lib.rtpb_mlp_forward(self._h, ptr_array(xs), rows, ptr_array(ys),
                                    _lib.MODE_EVAL if mode == "eval" else _lib.MODE_TRAIN))
         self.group._leave()
+        if mode != "eval":
+            self._x_keep = list(xs)  # ffn1 reads X again in backward
         return ys
 
     def backward(self, dys, out=None):
@@ -336,6 +342,7 @@ class RtpMlp(_Layer):
         self.group._enter([[a, b] for a, b in zip(dys, dxs)])
         check(lib.rtpb_mlp_backward(self._h, ptr_array(dys), rows, ptr_array(dxs)))
         self.group._leave()
+        self._x_keep = None
         return dxs
 
     def close(self):
