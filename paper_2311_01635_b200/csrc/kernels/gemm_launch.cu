@@ -1,5 +1,6 @@
-// Host-side launchers for the tcgen05 step GEMMs: TMA descriptor encoding,
-// tile-size choice, persistent grid sizing. No allocation, no sync.
+// Host-side launchers for the tcgen05 step GEMMs: TMA descriptor encoding
+// (operand loads and epilogue stores), tile-size choice, persistent grid
+// sizing. No allocation, no sync.
 #include <cudaTypedefs.h>
 
 #include <cstdio>
@@ -27,12 +28,13 @@ cudaError_t get_encode() {
   return g_encode ? cudaSuccess : cudaErrorNotSupported;
 }
 
-// 2-D row-major operand: `outer` rows of `inner` contiguous elements, row
-// stride `ld` elements; box = box_inner x box_outer elements, SWIZZLE_128B.
+// 2-D row-major tensor: `outer` rows of `inner` contiguous elements, row
+// stride `ld` elements; box = box_inner x box_outer elements.
 int encode_2d(CUtensorMap* m, const void* ptr, bool f32, uint64_t inner, uint64_t outer, uint64_t ld,
-              uint32_t box_inner, uint32_t box_outer) {
+              uint32_t box_inner, uint32_t box_outer, CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
   if (get_encode() != cudaSuccess) return set_error(RTPB_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   const uint64_t esz = f32 ? 4 : 2;
+  if (!ptr) return set_error(RTPB_ERR_DIMENSION, "null operand");
   if ((reinterpret_cast<uintptr_t>(ptr) & 15) || (ld * esz) % 16)
     return set_error(RTPB_ERR_CONFIG,
                      "operand base must be 16-byte aligned and its row stride a multiple of 16 bytes "
@@ -42,9 +44,8 @@ int encode_2d(CUtensorMap* m, const void* ptr, bool f32, uint64_t inner, uint64_
   cuuint32_t box[2] = {box_inner, box_outer};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = g_encode(m, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
-                        const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                        const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     char buf[160];
     std::snprintf(buf, sizeof buf, "cuTensorMapEncodeTiled failed (%d): inner=%llu outer=%llu ld=%llu", int(r),
@@ -52,6 +53,12 @@ int encode_2d(CUtensorMap* m, const void* ptr, bool f32, uint64_t inner, uint64_
     return set_error(RTPB_ERR_CUDA, buf);
   }
   return RTPB_OK;
+}
+
+// Epilogue store/reduce map: 32 x 32 boxes, swizzle matching stage_row<>.
+int encode_out(CUtensorMap* m, const void* ptr, bool f32, uint64_t cols, uint64_t rows, uint64_t ld) {
+  return encode_2d(m, ptr, f32, cols, rows, ld, 32, 32,
+                   f32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B);
 }
 
 int sm_count() {
@@ -65,16 +72,23 @@ int sm_count() {
   return n;
 }
 
-// Operand description: row-major (outer x inner, stride ld) plus whether the
-// GEMM reads it MN-major (inner = the M/N dimension) or K-major (inner = K).
+// Operand: row-major (outer x inner, stride ld); the GEMM reads it MN-major
+// (inner = the M/N dimension) or K-major (inner = K) per the kernel config.
 struct Op {
   const void* ptr;
   const void* lo;  // TF32X3 low part (same geometry) or nullptr
   uint64_t inner, outer, ld;
 };
 
+// Epilogue outputs: c0 (required) and c1 (FWD gelu output, optional).
+struct Out {
+  const void* ptr;
+  bool f32;
+  uint64_t cols, rows, ld;
+};
+
 template <class Cfg>
-int launch_cfg(const Op& a, const Op& b, const GemmArgs& args, cudaStream_t stream) {
+int launch_cfg(const Op& a, const Op& b, const Out& c0, const Out* c1, const GemmArgs& args, cudaStream_t stream) {
   GemmMaps maps;
   std::memset(&maps, 0, sizeof maps);
   constexpr bool F32 = Cfg::TF32;
@@ -89,6 +103,9 @@ int launch_cfg(const Op& a, const Op& b, const GemmArgs& args, cudaStream_t stre
     if ((rc = encode_2d(&maps.a_lo, a.lo, F32, a.inner, a.outer, a.ld, a_box_in, a_box_out))) return rc;
     if ((rc = encode_2d(&maps.b_lo, b.lo, F32, b.inner, b.outer, b.ld, b_box_in, b_box_out))) return rc;
   }
+  if ((rc = encode_out(&maps.c0, c0.ptr, c0.f32, c0.cols, c0.rows, c0.ld))) return rc;
+  const Out& o1 = c1 ? *c1 : c0;  // keep c1 a valid map even when unused
+  if ((rc = encode_out(&maps.c1, o1.ptr, o1.f32, o1.cols, o1.rows, o1.ld))) return rc;
   static bool attr_set = false;  // per instantiation
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(rtp_gemm_kernel<Cfg>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -128,22 +145,25 @@ int choose_bn(int M, int N, bool tf32, bool b_mn) {
   return best;
 }
 
+constexpr int kEpiWarps = 8;
+
 template <int EPI, bool TF32>
-int dispatch_bn(int bn, const Op& a, const Op& b, const GemmArgs& args, cudaStream_t s) {
-  constexpr int EW = (EPI == EPI_FWD) ? 8 : 4;
+int dispatch_bn(int bn, const Op& a, const Op& b, const Out& c0, const Out* c1, const GemmArgs& args,
+                cudaStream_t s) {
   constexpr bool AMN = !TF32 && EPI == EPI_WGRAD;
   constexpr bool BMN = !TF32 && EPI != EPI_DGRAD;
   switch (bn) {
-    case 64: return launch_cfg<GemmCfg<EPI, 64, TF32, EW, AMN, BMN>>(a, b, args, s);
-    case 128: return launch_cfg<GemmCfg<EPI, 128, TF32, EW, AMN, BMN>>(a, b, args, s);
+    case 64: return launch_cfg<GemmCfg<EPI, 64, TF32, kEpiWarps, AMN, BMN>>(a, b, c0, c1, args, s);
+    case 128: return launch_cfg<GemmCfg<EPI, 128, TF32, kEpiWarps, AMN, BMN>>(a, b, c0, c1, args, s);
     default:
-      if constexpr (!TF32) return launch_cfg<GemmCfg<EPI, 256, false, EW, AMN, BMN>>(a, b, args, s);
-      return launch_cfg<GemmCfg<EPI, 128, TF32, EW, AMN, BMN>>(a, b, args, s);
+      if constexpr (!TF32) return launch_cfg<GemmCfg<EPI, 256, false, kEpiWarps, AMN, BMN>>(a, b, c0, c1, args, s);
+      return launch_cfg<GemmCfg<EPI, 128, TF32, kEpiWarps, AMN, BMN>>(a, b, c0, c1, args, s);
   }
 }
 
 template <int EPI>
-int dispatch(bool tf32, const Op& a, const Op& b, GemmArgs args, cudaStream_t s, int force_bn) {
+int dispatch(bool tf32, const Op& a, const Op& b, const Out& c0, const Out* c1, GemmArgs args, cudaStream_t s,
+             int force_bn) {
   const bool b_mn = !tf32 && (EPI != EPI_DGRAD);
   const int bn = force_bn ? force_bn : choose_bn(args.M, args.N, tf32, b_mn);
   const int num_n = (args.N + bn - 1) / bn;
@@ -151,7 +171,8 @@ int dispatch(bool tf32, const Op& a, const Op& b, GemmArgs args, cudaStream_t s,
   // L2: concurrent CTAs then share each A row-block, which is read once.
   const double b_bytes = double(num_n) * bn * args.K * (tf32 ? 4.0 : 2.0);
   args.n_fastest = (EPI != EPI_WGRAD) && b_bytes < 48e6;
-  return tf32 ? dispatch_bn<EPI, true>(bn, a, b, args, s) : dispatch_bn<EPI, false>(bn, a, b, args, s);
+  return tf32 ? dispatch_bn<EPI, true>(bn, a, b, c0, c1, args, s)
+              : dispatch_bn<EPI, false>(bn, a, b, c0, c1, args, s);
 }
 
 }  // namespace
@@ -161,18 +182,20 @@ int gemm_fwd(bool f32, const StepFwd& p, cudaStream_t s) {
   Op a{p.x, p.x_lo, p.I, p.M, p.ldx};
   // bf16: W_j read MN-major in place. tf32: the pre-pass wrote W_j^T (per x I).
   Op b = f32 ? Op{p.w, p.w_lo, p.I, p.per, p.I} : Op{p.w, p.w_lo, p.per, p.I, p.per};
+  const size_t esz = f32 ? 4 : 2;
   GemmArgs g{};
   g.M = int(p.M);
   g.N = int(p.per);
   g.K = int(p.I);
   g.flags = p.flags;
-  g.out0 = p.y;
-  g.ld0 = int64_t(p.ldy);
-  g.out1 = p.act;
-  g.ld1 = int64_t(p.ld_act);
   g.aux = p.bias;
-  g.col0 = int(p.col0);
-  return dispatch<EPI_FWD>(f32, a, b, g, s, p.force_bn);
+  // Output blocks start at column col0 of Y / act: the maps' base pointers.
+  Out y{p.y ? static_cast<const char*>(p.y) + p.col0 * esz : nullptr, f32, p.per, p.M, p.ldy};
+  Out act{p.act ? static_cast<const char*>(p.act) + p.col0 * esz : nullptr, f32, p.per, p.M, p.ld_act};
+  const bool has_y = (p.flags & EF_STORE_PRE) && p.y;
+  const bool has_act = (p.flags & EF_GELU) && p.act;
+  const Out& c0 = has_y ? y : act;
+  return dispatch<EPI_FWD>(f32, a, b, c0, has_act ? &act : nullptr, g, s, p.force_bn);
 }
 
 int gemm_dgrad(bool f32, const StepDgrad& p, cudaStream_t s) {
@@ -184,30 +207,32 @@ int gemm_dgrad(bool f32, const StepDgrad& p, cudaStream_t s) {
   g.N = int(p.I);
   g.K = int(p.per);
   g.flags = p.flags;
-  g.out0 = p.dx;
-  g.ld0 = int64_t(p.ldx);
   g.aux = p.pre;
   g.ld_aux = int64_t(p.ldpre);
   g.acc = p.acc;
   g.ld_acc = int64_t(p.ld_acc);
-  return dispatch<EPI_DGRAD>(f32, a, b, g, s, p.force_bn);
+  const bool last = p.flags & EF_LAST;
+  // last step: emit dX in the activation dtype; otherwise store / reduce-add fp32.
+  Out c0 = last ? Out{p.dx, f32, p.I, p.M, p.ldx} : Out{p.acc, true, p.I, p.M, p.ld_acc};
+  return dispatch<EPI_DGRAD>(f32, a, b, c0, nullptr, g, s, p.force_bn);
 }
 
 int gemm_wgrad(bool f32, const StepWgrad& p, cudaStream_t s) {
-  // C[I x per] = X^T . dY_blk; A = X read MN-major, B = dY_blk read MN-major.
-  // bf16: X and dY_blk read MN-major in place. tf32: the pre-pass wrote
-  // X^T (I x M) and dY_blk^T (per x M), both K-major.
+  // C[I x per] = X^T . dY_blk; bf16: X and dY_blk read MN-major in place.
+  // tf32: the pre-pass wrote X^T (I x M) and dY_blk^T (per x M), both K-major.
   Op a = f32 ? Op{p.x, p.x_lo, p.M, p.I, p.ldx} : Op{p.x, p.x_lo, p.I, p.M, p.ldx};
   Op b = f32 ? Op{p.dy, p.dy_lo, p.M, p.per, p.ldy} : Op{p.dy, p.dy_lo, p.per, p.M, p.ldy};
   GemmArgs g{};
   g.M = int(p.I);
   g.N = int(p.per);
   g.K = int(p.M);
-  g.out0 = p.g_out;
-  g.ld0 = int64_t(p.per);
-  g.aux = p.g_in;
-  g.ld_aux = int64_t(p.per);
-  return dispatch<EPI_WGRAD>(f32, a, b, g, s, p.force_bn);
+  // G_out = G_in + P: the epilogue reduce-adds into G_out, so seed it with G_in.
+  if (p.g_out != p.g_in) {
+    cudaError_t e = cudaMemcpyAsync(p.g_out, p.g_in, p.I * p.per * sizeof(float), cudaMemcpyDeviceToDevice, s);
+    if (e != cudaSuccess) return set_cuda_error(e, "wgrad: seed G_out");
+  }
+  Out c0{p.g_out, true, p.per, p.I, p.per};
+  return dispatch<EPI_WGRAD>(f32, a, b, c0, nullptr, g, s, p.force_bn);
 }
 
 }  // namespace rtpb

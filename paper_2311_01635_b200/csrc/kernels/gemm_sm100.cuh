@@ -5,14 +5,17 @@
 //           (+ optional exact-erf GELU: writes pre and gelu(pre))
 //   DGRAD : dXacc += dY[:, blk_j] . W_j^T         A = dY blk (K-major), B = W_j (K-major)
 //           (fp32 cross-step accumulator; last step casts, optionally * gelu'(pre))
-//   WGRAD : G_out = G_in + X^T . dY[:, blk_j]     A = X (MN-major), B = dY blk (MN-major)
-//           (the travelling gradient shard is accumulated in the epilogue)
+//   WGRAD : G += X^T . dY[:, blk_j]               A = X (MN-major), B = dY blk (MN-major)
+//           (the travelling gradient shard is accumulated by the epilogue)
 //
 // Roles (one CTA per SM, grid = min(tiles, SMs), static round-robin tiles):
 //   warp 0        : TMA producer (one elected lane), STAGES-deep smem ring
 //   warp 1        : TMEM allocator + MMA issuer (one elected lane)
-//   warps 2..2+E  : epilogue, TMEM -> registers -> global, double-buffered
-//                   accumulators so tile t's epilogue overlaps tile t+1's MMAs.
+//   warps 2..2+E  : epilogue: TMEM -> registers -> swizzled smem staging ->
+//                   TMA store (bf16 / fp32) or TMA reduce-add (fp32, done in
+//                   L2: the dX cross-step accumulation and G += dW never make
+//                   the SMs read the accumulator). Double-buffered TMEM
+//                   accumulators overlap tile t's epilogue with tile t+1's MMAs.
 // Tile: BM = 128 rows (UMMA M=128, cta_group::1) x BN columns, BK = 128 bytes
 // of K per stage (64 bf16 / 32 fp32), SWIZZLE_128B operands.
 // TF32X3: fp32 operands split (and, where the GEMM would read them MN-major,
@@ -31,26 +34,21 @@ namespace rtpb {
 
 enum EpiKind : int { EPI_FWD = 0, EPI_DGRAD = 1, EPI_WGRAD = 2 };
 enum EpiFlags : int {
-  EF_GELU = 1,      // FWD: also emit gelu(pre) into out1
-  EF_FIRST = 2,     // DGRAD: first step (no read of the fp32 accumulator)
-  EF_LAST = 4,      // DGRAD: last step (emit the cast result into out0)
+  EF_GELU = 1,      // FWD: also emit gelu(pre) through map c1
+  EF_FIRST = 2,     // DGRAD: first step (accumulator not read)
+  EF_LAST = 4,      // DGRAD: last step (emit the cast result through map c0)
   EF_GELU_BWD = 8,  // DGRAD last step: multiply by gelu'(pre)
-  EF_STORE_PRE = 16 // FWD: store pre into out0 (else only out1 is written)
+  EF_STORE_PRE = 16 // FWD: store pre through map c0
 };
 
 struct GemmArgs {
   int M, N, K;
   int flags;
   int n_fastest;       // tile raster: n-block fastest (A streamed once)
-  void* out0;          // FWD: pre/Y (dtype) | DGRAD: dX (dtype) | WGRAD: G_out (f32)
-  int64_t ld0;
-  void* out1;          // FWD: gelu(pre) (dtype)
-  int64_t ld1;
-  const void* aux;     // FWD: bias (dtype) | DGRAD: pre (dtype) | WGRAD: G_in (f32)
+  const void* aux;     // FWD: bias (dtype, N values) | DGRAD: pre (dtype, M x N, ld_aux)
   int64_t ld_aux;
-  float* acc;          // DGRAD: fp32 cross-step accumulator
+  const float* acc;    // DGRAD LAST && !FIRST: fp32 accumulator read (M x N, ld_acc)
   int64_t ld_acc;
-  int col0;            // FWD: column offset of the block in out0/out1
 };
 
 template <int EPI_, int BN_, bool TF32_, int EPI_WARPS_, bool A_MN_, bool B_MN_>
@@ -70,21 +68,35 @@ struct GemmCfg {
   static constexpr int B_BYTES = BN * 128;
   static constexpr int NOPS = TF32 ? 2 : 1;      // hi (+ lo) copies per operand
   static constexpr int STAGE_BYTES = NOPS * (A_BYTES + B_BYTES);
-  static constexpr int SMEM_BUDGET = 220 * 1024;
-  static constexpr int STAGES_RAW = (SMEM_BUDGET - 2048) / STAGE_BYTES;
-  static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
   static constexpr int EPI_WARPS = EPI_WARPS_;
+  // Epilogue staging per warp: one 32 x 32 tile per output. FWD writes two
+  // outputs (pre, gelu(pre)) in the activation dtype; DGRAD may stage fp32
+  // (accumulator steps), WGRAD always does.
+  static constexpr int NOUT = EPI == EPI_FWD ? 2 : 1;
+  static constexpr int STG_ONE = 32 * 32 * (EPI == EPI_FWD ? ELEM : 4);
+  static constexpr int STG_WARP = NOUT * STG_ONE;
+  static constexpr int STG_BYTES = EPI_WARPS * STG_WARP;
+  static constexpr int SMEM_LIMIT = 232448;     // 227 KB opt-in per block
+  static constexpr int RESERVE = 1024 /*align*/ + 512 /*barriers*/ + STG_BYTES;
+  static constexpr int STAGES_RAW = (SMEM_LIMIT - RESERVE) / STAGE_BYTES;
+  static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
   static constexpr int THREADS = 64 + 32 * EPI_WARPS;
   static constexpr int TMEM_COLS = (2 * BN <= 32) ? 32 : (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128
                                    : (2 * BN <= 256) ? 256 : 512;
-  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 512 /*barriers*/;
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + RESERVE;
   static constexpr uint32_t IDESC = ptx::idesc_make(BM, BN, TF32 ? 2 : 1, A_MN, B_MN);
   static_assert(STAGES >= 2, "not enough shared memory for 2 stages");
   static_assert(BN % 32 == 0 && BN >= 32 && BN <= 256, "BN");
+  static_assert(EPI_WARPS == 4 || EPI_WARPS == 8, "epilogue warps");
 };
 
+// a, b (+ lo parts): operand loads. c0, c1: epilogue stores / reductions,
+// box 32 x 32 (SWIZZLE_64B for bf16 rows of 64 B, SWIZZLE_128B for fp32).
+//   FWD   c0 = pre / Y (dtype), c1 = gelu(pre) (dtype)
+//   DGRAD c0 = dX (dtype) when EF_LAST, else the fp32 accumulator
+//   WGRAD c0 = G (fp32, reduce-add)
 struct GemmMaps {
-  CUtensorMap a, b, a_lo, b_lo;
+  CUtensorMap a, b, a_lo, b_lo, c0, c1;
 };
 
 namespace detail {
@@ -102,9 +114,9 @@ __device__ __forceinline__ float gelu_grad_f(float x) {
   return phi + x * pdf;
 }
 
-// Load 8 consecutive values of `dtype` (bf16 when !F32) as fp32.
+// Load 8 consecutive values of the activation dtype as fp32.
 template <bool F32>
-__device__ __forceinline__ void load8(const void* base, int64_t off, float (&o)[8]) {
+__device__ __forceinline__ void load8(const void* base, int64_t off, float* o) {
   if constexpr (F32) {
     const float4* p = reinterpret_cast<const float4*>(static_cast<const float*>(base) + off);
     float4 a = p[0], b = p[1];
@@ -115,28 +127,33 @@ __device__ __forceinline__ void load8(const void* base, int64_t off, float (&o)[
     o[4] = bf16lo(u.z); o[5] = bf16hi(u.z); o[6] = bf16lo(u.w); o[7] = bf16hi(u.w);
   }
 }
-template <bool F32>
-__device__ __forceinline__ void store8(void* base, int64_t off, const float (&v)[8]) {
-  if constexpr (F32) {
-    float4* p = reinterpret_cast<float4*>(static_cast<float*>(base) + off);
-    p[0] = make_float4(v[0], v[1], v[2], v[3]);
-    p[1] = make_float4(v[4], v[5], v[6], v[7]);
+
+// Thread `row` (0..31) writes its 32 values into a 32x32 staging tile laid
+// out as the TMA box expects: bf16 rows of 64 B under SWIZZLE_64B (16 B
+// chunk c -> c ^ ((row >> 1) & 3)), fp32 rows of 128 B under SWIZZLE_128B
+// (chunk c -> c ^ (row & 7)). Conflict-free for 16-byte stores.
+template <bool F32OUT>
+__device__ __forceinline__ void stage_row(uint8_t* stg, int row, const float* v) {
+  if constexpr (F32OUT) {
+    uint8_t* base = stg + row * 128;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const int pc = c ^ (row & 7);
+      *reinterpret_cast<float4*>(base + pc * 16) = make_float4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+    }
   } else {
-    uint4 u;
-    u.x = pack_bf16(v[0], v[1]); u.y = pack_bf16(v[2], v[3]);
-    u.z = pack_bf16(v[4], v[5]); u.w = pack_bf16(v[6], v[7]);
-    *reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(base) + off) = u;
+    uint8_t* base = stg + row * 64;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int pc = c ^ ((row >> 1) & 3);
+      uint4 u;
+      u.x = pack_bf16(v[8 * c + 0], v[8 * c + 1]);
+      u.y = pack_bf16(v[8 * c + 2], v[8 * c + 3]);
+      u.z = pack_bf16(v[8 * c + 4], v[8 * c + 5]);
+      u.w = pack_bf16(v[8 * c + 6], v[8 * c + 7]);
+      *reinterpret_cast<uint4*>(base + pc * 16) = u;
+    }
   }
-}
-__device__ __forceinline__ void load8f(const float* p, float (&o)[8]) {
-  const float4* q = reinterpret_cast<const float4*>(p);
-  float4 a = q[0], b = q[1];
-  o[0] = a.x; o[1] = a.y; o[2] = a.z; o[3] = a.w; o[4] = b.x; o[5] = b.y; o[6] = b.z; o[7] = b.w;
-}
-__device__ __forceinline__ void store8f(float* p, const float (&v)[8]) {
-  float4* q = reinterpret_cast<float4*>(p);
-  q[0] = make_float4(v[0], v[1], v[2], v[3]);
-  q[1] = make_float4(v[4], v[5], v[6], v[7]);
 }
 
 }  // namespace detail
@@ -151,7 +168,8 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* stage_base = smem;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * Cfg::STAGE_BYTES);
+  uint8_t* stg_base = smem + STAGES * Cfg::STAGE_BYTES;  // 1024-aligned (stage bytes are multiples of 1 KB)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(stg_base + Cfg::STG_BYTES);
   uint64_t* full_bar = bars;                    // [STAGES]
   uint64_t* empty_bar = bars + STAGES;          // [STAGES]
   uint64_t* tfull_bar = bars + 2 * STAGES;      // [2]
@@ -173,6 +191,8 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
       prefetch_tmap(&maps.a_lo);
       prefetch_tmap(&maps.b_lo);
     }
+    prefetch_tmap(&maps.c0);
+    if constexpr (Cfg::NOUT > 1) prefetch_tmap(&maps.c1);
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full_bar[s], 1);
       mbar_init(&empty_bar[s], 1);
@@ -211,7 +231,6 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
         for (int kb = 0; kb < num_kb; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
           uint8_t* sA = stage_base + stage * Cfg::STAGE_BYTES;
-          uint8_t* sB = sA + Cfg::A_BYTES;
           mbar_expect_tx(&full_bar[stage], Cfg::STAGE_BYTES);
           const int k0 = kb * BK;
           for (int op = 0; op < Cfg::NOPS; ++op) {
@@ -298,16 +317,22 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
     const int q = warp & 3;           // TMEM lane quarter this warp may access
     const int half = ew / 4;          // column interleave when EPI_WARPS == 8
     constexpr int NSPLIT = Cfg::EPI_WARPS / 4;
+    uint8_t* stg0 = stg_base + ew * Cfg::STG_WARP;
+    uint8_t* stg1 = stg0 + Cfg::STG_ONE;
+    const bool last = args.flags & EF_LAST;
+    const bool first = args.flags & EF_FIRST;
+    bool pending = false;
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
       int mb, nb;
       tile_coords(t, mb, nb);
       const int m0 = mb * BM, n0 = nb * BN;
+      const int row0 = m0 + q * 32;     // first row of this warp's 32-row slab
+      const int row = row0 + lane;
+      const bool row_ok = row < args.M;
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
-      const int row = m0 + q * 32 + lane;
-      const bool row_ok = row < args.M;
       const uint32_t t_row = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN;
 #pragma unroll 1
       for (int ch = half; ch < BN / 32; ch += NSPLIT) {
@@ -316,54 +341,78 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
         uint32_t v[32];
         tmem_ld_32x32b_x32(t_row + ch * 32, v);
         tmem_ld_wait();
-        if (!row_ok) continue;
+        float x[32];
 #pragma unroll
-        for (int g = 0; g < 4; ++g) {
-          const int n = nc + g * 8;
-          if (n >= args.N) break;
-          float x[8];
-#pragma unroll
-          for (int e = 0; e < 8; ++e) x[e] = __uint_as_float(v[g * 8 + e]);
-          if constexpr (Cfg::EPI == EPI_FWD) {
-            float bias[8];
-            detail::load8<F32>(args.aux, n, bias);
-#pragma unroll
-            for (int e = 0; e < 8; ++e) x[e] += bias[e];
-            const int64_t col = args.col0 + n;
-            if (args.flags & EF_STORE_PRE) detail::store8<F32>(args.out0, row * args.ld0 + col, x);
-            if (args.flags & EF_GELU) {
-              float y[8];
-#pragma unroll
-              for (int e = 0; e < 8; ++e) y[e] = detail::gelu_f(x[e]);
-              detail::store8<F32>(args.out1, row * args.ld1 + col, y);
-            }
-          } else if constexpr (Cfg::EPI == EPI_DGRAD) {
-            float* accp = args.acc + row * args.ld_acc + n;
-            if (!(args.flags & EF_FIRST)) {
-              float old[8];
-              detail::load8f(accp, old);
-#pragma unroll
-              for (int e = 0; e < 8; ++e) x[e] = old[e] + x[e];
-            }
-            if (args.flags & EF_LAST) {
-              if (args.flags & EF_GELU_BWD) {
-                float pre[8];
-                detail::load8<F32>(args.aux, row * args.ld_aux + n, pre);
-#pragma unroll
-                for (int e = 0; e < 8; ++e) x[e] = x[e] * detail::gelu_grad_f(pre[e]);
-              }
-              detail::store8<F32>(args.out0, row * args.ld0 + n, x);
-            } else {
-              detail::store8f(accp, x);
-            }
-          } else {  // EPI_WGRAD: G_out = G_in + P
-            float gin[8];
-            detail::load8f(static_cast<const float*>(args.aux) + row * args.ld_aux + n, gin);
-#pragma unroll
-            for (int e = 0; e < 8; ++e) x[e] = gin[e] + x[e];
-            detail::store8f(static_cast<float*>(args.out0) + row * args.ld0 + n, x);
-          }
+        for (int e = 0; e < 32; ++e) x[e] = __uint_as_float(v[e]);
+        // staging buffers free again (previous chunk's bulk stores read them)
+        if (pending) {
+          if (lane == 0) bulk_wait_read0();
+          __syncwarp();
         }
+        if constexpr (Cfg::EPI == EPI_FWD) {
+#pragma unroll
+          for (int g = 0; g < 4; ++g) {
+            float bias[8];
+            if (nc + g * 8 < args.N) {
+              detail::load8<F32>(args.aux, nc + g * 8, bias);
+            } else {
+#pragma unroll
+              for (int e = 0; e < 8; ++e) bias[e] = 0.f;
+            }
+#pragma unroll
+            for (int e = 0; e < 8; ++e) x[g * 8 + e] += bias[e];
+          }
+          if (args.flags & EF_STORE_PRE) detail::stage_row<F32>(stg0, lane, x);
+          if (args.flags & EF_GELU) {
+#pragma unroll
+            for (int e = 0; e < 32; ++e) x[e] = detail::gelu_f(x[e]);
+            detail::stage_row<F32>(stg1, lane, x);
+          }
+        } else if constexpr (Cfg::EPI == EPI_DGRAD) {
+          if (last && !first && row_ok) {
+#pragma unroll
+            for (int g = 0; g < 4; ++g)
+              if (nc + g * 8 < args.N) {
+                const float4* p = reinterpret_cast<const float4*>(args.acc + row * args.ld_acc + nc + g * 8);
+                const float4 a = p[0], b = p[1];
+                x[g * 8 + 0] += a.x; x[g * 8 + 1] += a.y; x[g * 8 + 2] += a.z; x[g * 8 + 3] += a.w;
+                x[g * 8 + 4] += b.x; x[g * 8 + 5] += b.y; x[g * 8 + 6] += b.z; x[g * 8 + 7] += b.w;
+              }
+          }
+          if (last && (args.flags & EF_GELU_BWD) && row_ok) {
+#pragma unroll
+            for (int g = 0; g < 4; ++g)
+              if (nc + g * 8 < args.N) {
+                float pre[8];
+                detail::load8<F32>(args.aux, row * args.ld_aux + nc + g * 8, pre);
+#pragma unroll
+                for (int e = 0; e < 8; ++e) x[g * 8 + e] *= detail::gelu_grad_f(pre[e]);
+              }
+          }
+          if (last)
+            detail::stage_row<F32>(stg0, lane, x);
+          else
+            detail::stage_row<true>(stg0, lane, x);
+        } else {
+          detail::stage_row<true>(stg0, lane, x);
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          if constexpr (Cfg::EPI == EPI_FWD) {
+            if (args.flags & EF_STORE_PRE) tma_store_2d(&maps.c0, stg0, nc, row0);
+            if (args.flags & EF_GELU) tma_store_2d(&maps.c1, stg1, nc, row0);
+          } else if constexpr (Cfg::EPI == EPI_DGRAD) {
+            if (last || first)
+              tma_store_2d(&maps.c0, stg0, nc, row0);  // dX (dtype) or first partial (fp32)
+            else
+              tma_reduce_add_2d(&maps.c0, stg0, nc, row0);  // acc += partial, in L2
+          } else {
+            tma_reduce_add_2d(&maps.c0, stg0, nc, row0);  // travelling G += dW tile
+          }
+          bulk_commit();
+        }
+        pending = true;
       }
       tc_fence_before();
       mbar_arrive(&tempty_bar[acc]);
@@ -372,6 +421,8 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
         acc_phase ^= 1;
       }
     }
+    if (lane == 0) bulk_wait0();
+    __syncwarp();
   }
 
   tc_fence_before();
