@@ -100,7 +100,10 @@ int rtpb_wgrad_step(int dtype, const void* x, size_t ldx, const void* dy, size_t
                     const float* g_in, float* g_out, size_t M, size_t I, size_t per, void* workspace,
                     size_t workspace_bytes, void* stream);
 
-/* Workspace bytes for a step kernel: which = 0 fwd, 1 dgrad, 2 wgrad. */
+/* Workspace bytes for a step kernel: which = 0 fwd, 1 dgrad, 2 wgrad.
+ * A workspace must be zero-filled before its first use; the kernels leave
+ * their completion tickets at zero, so it can then be reused indefinitely
+ * (by one stream at a time). */
 size_t rtpb_step_workspace_bytes(int which, int dtype, size_t M, size_t I, size_t per);
 
 /* Exact-erf GELU and derivative (tensor.cpp:323-351), elementwise. */

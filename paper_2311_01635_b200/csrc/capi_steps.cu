@@ -115,10 +115,12 @@ const char* rtpb_version(void) { return "rtpb 0.1 (sm_100a tcgen05)"; }
 uint64_t rtpb_launch_count(void) { return g_launches.load(); }
 void rtpb_debug_force_bn(int bn) { g_force_bn = bn; }
 
+// Workspace layout, identical for every step kind of a layer so one buffer
+// serves all three: [bias-grad tickets + partials (tickets stay zero)]
+// [fp32 mode: tf32 hi/lo operand splits].
 size_t rtpb_step_workspace_bytes(int which, int dtype, size_t M, size_t I, size_t per) {
   const bool f32 = dtype == RTPB_F32;
-  size_t b = 0;
-  if (which == 2) b += align256(colsum_workspace_bytes(M, per));
+  size_t b = align256(colsum_workspace_bytes(M, per));
   if (f32) {
     if (which == 0) b += 2 * align256(M * I * 4) + 2 * align256(I * per * 4);
     if (which == 1) b += 2 * align256(M * per * 4) + 2 * align256(I * per * 4);
@@ -152,6 +154,7 @@ int rtpb_fwd_step(int dtype, const void* x, size_t ldx, const void* w_shard, voi
   p.M = M; p.I = I; p.per = per; p.flags = flags; p.force_bn = g_force_bn;
   if (f32) {
     Carve c{static_cast<char*>(workspace), workspace ? workspace_bytes : 0};
+    c.take(colsum_workspace_bytes(M, per) / sizeof(float));  // keep the zeroed tickets intact
     float *xh = c.take(M * I), *xl = c.take(M * I), *wh = c.take(I * per), *wl = c.take(I * per);
     if (!c.ok) return set_error(RTPB_ERR_DIMENSION, "fwd_step: workspace too small");
     if ((rc = tf32_split(static_cast<const float*>(x), M, I, ldx, xh, xl, s))) return rc;
@@ -179,6 +182,7 @@ int rtpb_dgrad_step(int dtype, const void* dy, size_t ldy, size_t col0, const vo
   p.M = M; p.I = I; p.per = per; p.flags = flags; p.force_bn = g_force_bn;
   if (f32) {
     Carve c{static_cast<char*>(workspace), workspace ? workspace_bytes : 0};
+    c.take(colsum_workspace_bytes(M, per) / sizeof(float));  // keep the zeroed tickets intact
     float *dh = c.take(M * per), *dl = c.take(M * per), *wh = c.take(I * per), *wl = c.take(I * per);
     if (!c.ok) return set_error(RTPB_ERR_DIMENSION, "dgrad_step: workspace too small");
     if ((rc = tf32_split(static_cast<const float*>(p.dy), M, per, ldy, dh, dl, s))) return rc;

@@ -185,7 +185,7 @@ void RtpLinear::ensure_scratch(size_t rows) {
     Worker& w = group_->worker(r);
     dx_acc_[r] = n > 1 ? DeviceBuffer(w.device, rows * in_ * sizeof(float), &w.ledger, MemCategory::Activation, false)
                        : DeviceBuffer();
-    workspace_[r] = ws ? DeviceBuffer(w.device, ws, &w.ledger, MemCategory::Other, false) : DeviceBuffer();
+    workspace_[r] = ws ? DeviceBuffer(w.device, ws, &w.ledger, MemCategory::Other, true) : DeviceBuffer();
   });
   scratch_rows_ = rows;
 }

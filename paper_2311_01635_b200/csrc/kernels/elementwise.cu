@@ -58,33 +58,42 @@ __global__ void flyweight_kernel(T* __restrict__ dst, uint64_t seed, uint64_t ba
   }
 }
 
-// Phase 1: partial column sums of a strided M x per block over row splits.
-// Block = 32 row lanes x 8 column groups of 8 columns (64 columns).
+// Bias gradient db_j += colsum(dY[:, blk_j]) (layers_linear.cpp:63) in one
+// launch. grid = (column groups of 64) x (row splits); block = 32 row lanes x
+// 8 column groups of 8 (16-byte loads, 4 rows in flight per thread). Each
+// block writes its partial sums; the last block to finish a column group
+// (ticket) adds the splits in split order, so the result is deterministic.
+// The tickets live in the caller's workspace and are left at zero.
 template <bool F32>
-__global__ void colsum_partial_kernel(const void* __restrict__ dy, size_t ldy, int M, int per, int rows_per_split,
-                                      float* __restrict__ partial) {
+__global__ void colsum_kernel(const void* __restrict__ dy, size_t ldy, int M, int per, int rows_per_split,
+                              float* __restrict__ partial, unsigned* __restrict__ tickets,
+                              const float* __restrict__ g_in, float* __restrict__ g_out) {
   __shared__ float red[32][65];
-  const int cg = threadIdx.x & 7, rl = threadIdx.x >> 3;  // 8 col groups, 32 row lanes
+  __shared__ bool is_last;
+  const int cg = threadIdx.x & 7, rl = threadIdx.x >> 3;
   const int c0 = blockIdx.x * 64 + cg * 8;
   const int r_begin = blockIdx.y * rows_per_split;
   const int r_end = min(M, r_begin + rows_per_split);
   float s[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  if (c0 < per) {
-    for (int r = r_begin + rl; r < r_end; r += 32) {
-      if constexpr (F32) {
-        const float4* p = reinterpret_cast<const float4*>(static_cast<const float*>(dy) + size_t(r) * ldy + c0);
-        const float4 a = p[0], b = p[1];
-        s[0] += a.x; s[1] += a.y; s[2] += a.z; s[3] += a.w; s[4] += b.x; s[5] += b.y; s[6] += b.z; s[7] += b.w;
-      } else {
-        const uint4 u = *reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(dy) + size_t(r) * ldy + c0);
-        const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+  auto add_row = [&](int r) {
+    if constexpr (F32) {
+      const float4* p = reinterpret_cast<const float4*>(static_cast<const float*>(dy) + size_t(r) * ldy + c0);
+      const float4 a = __ldg(p), b = __ldg(p + 1);
+      s[0] += a.x; s[1] += a.y; s[2] += a.z; s[3] += a.w; s[4] += b.x; s[5] += b.y; s[6] += b.z; s[7] += b.w;
+    } else {
+      const uint4 u = __ldg(reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(dy) + size_t(r) * ldy + c0));
+      const uint32_t w[4] = {u.x, u.y, u.z, u.w};
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          s[2 * q] += __uint_as_float(w[q] << 16);
-          s[2 * q + 1] += __uint_as_float(w[q] & 0xFFFF0000u);
-        }
+      for (int q = 0; q < 4; ++q) {
+        s[2 * q] += __uint_as_float(w[q] << 16);
+        s[2 * q + 1] += __uint_as_float(w[q] & 0xFFFF0000u);
       }
     }
+  };
+  if (c0 < per) {
+    int r = r_begin + rl;
+#pragma unroll 4
+    for (; r < r_end; r += 32) add_row(r);
   }
 #pragma unroll
   for (int q = 0; q < 8; ++q) red[rl][cg * 8 + q] = s[q];
@@ -92,24 +101,29 @@ __global__ void colsum_partial_kernel(const void* __restrict__ dy, size_t ldy, i
   if (threadIdx.x < 64) {
     const int c = blockIdx.x * 64 + threadIdx.x;
     float acc = 0.f;
-    for (int l = 0; l < 32; ++l) acc += red[l][threadIdx.x];  // fixed order: deterministic
+    for (int l = 0; l < 32; ++l) acc += red[l][threadIdx.x];  // fixed order
     if (c < per) partial[size_t(blockIdx.y) * per + c] = acc;
+    __threadfence();
   }
-}
-
-__global__ void colsum_final_kernel(const float* __restrict__ partial, int splits, int per,
-                                    const float* __restrict__ g_in, float* __restrict__ g_out) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= per) return;
-  float acc = 0.f;
-  for (int s = 0; s < splits; ++s) acc += partial[size_t(s) * per + c];
-  g_out[c] = g_in[c] + acc;
+  __syncthreads();
+  if (threadIdx.x == 0) is_last = atomicAdd(&tickets[blockIdx.x], 1u) == gridDim.y - 1;
+  __syncthreads();
+  if (is_last && threadIdx.x < 64) {
+    __threadfence();
+    const int c = blockIdx.x * 64 + threadIdx.x;
+    if (c < per) {
+      float acc = 0.f;
+      for (int sp = 0; sp < int(gridDim.y); ++sp) acc += __ldcg(&partial[size_t(sp) * per + c]);
+      g_out[c] = g_in[c] + acc;
+    }
+    if (threadIdx.x == 0) tickets[blockIdx.x] = 0u;  // leave the workspace reusable
+  }
 }
 
 int colsum_splits(size_t M, size_t per) {
   const int col_blocks = int((per + 63) / 64);
-  int splits = (2 * 148 + col_blocks - 1) / col_blocks;  // ~2 waves of CTAs
-  const int max_splits = int((M + 255) / 256);         // >= 256 rows per split
+  int splits = (4 * 148 + col_blocks - 1) / col_blocks;  // ~4 CTAs per SM
+  const int max_splits = int((M + 127) / 128);          // >= 128 rows per split
   if (splits > max_splits) splits = max_splits;
   return splits < 1 ? 1 : splits;
 }
@@ -205,8 +219,10 @@ int flyweight_init(void* dst, bool f32, uint64_t seed, uint64_t base, size_t I, 
   return post_launch("flyweight_kernel");
 }
 
+// Workspace: [tickets: one per column group, 256 B aligned][partials].
 size_t colsum_workspace_bytes(size_t M, size_t per) {
-  return size_t(colsum_splits(M, per)) * per * sizeof(float);
+  const size_t tick = ((per + 63) / 64 * sizeof(unsigned) + 255) & ~size_t(255);
+  return tick + size_t(colsum_splits(M, per)) * per * sizeof(float);
 }
 
 int colsum_bias_grad(bool f32, const void* dy, size_t ldy, size_t M, size_t per, const float* g_in, float* g_out,
@@ -214,16 +230,17 @@ int colsum_bias_grad(bool f32, const void* dy, size_t ldy, size_t M, size_t per,
   if (per % 8) return set_error(RTPB_ERR_CONFIG, "bias grad: per must be a multiple of 8");
   const int splits = colsum_splits(M, per);
   const int rows_per_split = int((M + splits - 1) / splits);
-  dim3 grid(unsigned((per + 63) / 64), unsigned(splits));
-  float* partial = static_cast<float*>(ws);
+  const unsigned col_blocks = unsigned((per + 63) / 64);
+  dim3 grid(col_blocks, unsigned(splits));
+  unsigned* tickets = static_cast<unsigned*>(ws);
+  float* partial = reinterpret_cast<float*>(static_cast<char*>(ws) +
+                                            ((col_blocks * sizeof(unsigned) + 255) & ~size_t(255)));
   if (f32)
-    colsum_partial_kernel<true><<<grid, 256, 0, s>>>(dy, ldy, int(M), int(per), rows_per_split, partial);
+    colsum_kernel<true><<<grid, 256, 0, s>>>(dy, ldy, int(M), int(per), rows_per_split, partial, tickets, g_in, g_out);
   else
-    colsum_partial_kernel<false><<<grid, 256, 0, s>>>(dy, ldy, int(M), int(per), rows_per_split, partial);
-  int rc = post_launch("colsum_partial_kernel");
-  if (rc) return rc;
-  colsum_final_kernel<<<unsigned((per + 255) / 256), 256, 0, s>>>(partial, splits, int(per), g_in, g_out);
-  return post_launch("colsum_final_kernel");
+    colsum_kernel<false><<<grid, 256, 0, s>>>(dy, ldy, int(M), int(per), rows_per_split, partial, tickets, g_in,
+                                              g_out);
+  return post_launch("colsum_kernel");
 }
 
 int tf32_split(const float* src, size_t rows, size_t cols, size_t ld, float* hi, float* lo, cudaStream_t s) {

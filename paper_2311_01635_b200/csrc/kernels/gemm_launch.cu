@@ -214,6 +214,14 @@ int gemm_dgrad(bool f32, const StepDgrad& p, cudaStream_t s) {
   const bool last = p.flags & EF_LAST;
   // last step: emit dX in the activation dtype; otherwise store / reduce-add fp32.
   Out c0 = last ? Out{p.dx, f32, p.I, p.M, p.ldx} : Out{p.acc, true, p.I, p.M, p.ld_acc};
+  if (last && (p.flags & EF_GELU_BWD)) {
+    // gelu' fused: stream pre tiles through smem (PRE_TMA config, 128-wide tiles).
+    Out pre{p.pre, f32, p.I, p.M, p.ldpre};
+    const int num_n = (g.N + 127) / 128;
+    g.n_fastest = double(num_n) * 128 * g.K * (f32 ? 4.0 : 2.0) < 48e6;
+    if (f32) return launch_cfg<GemmCfg<EPI_DGRAD, 128, true, kEpiWarps, false, false, true>>(a, b, c0, &pre, g, s);
+    return launch_cfg<GemmCfg<EPI_DGRAD, 128, false, kEpiWarps, false, false, true>>(a, b, c0, &pre, g, s);
+  }
   return dispatch<EPI_DGRAD>(f32, a, b, c0, nullptr, g, s, p.force_bn);
 }
 

@@ -51,9 +51,13 @@ struct GemmArgs {
   int64_t ld_acc;
 };
 
-template <int EPI_, int BN_, bool TF32_, int EPI_WARPS_, bool A_MN_, bool B_MN_>
+template <int EPI_, int BN_, bool TF32_, int EPI_WARPS_, bool A_MN_, bool B_MN_, bool PRE_TMA_ = false>
 struct GemmCfg {
   static constexpr int EPI = EPI_;
+  // DGRAD with gelu' fused: the tile's pre values are streamed into shared
+  // memory by TMA when the tile starts (while its MMAs run), instead of
+  // per-row global loads in the epilogue.
+  static constexpr bool PRE_TMA = PRE_TMA_;
   static constexpr int BM = 128;
   static constexpr int BN = BN_;
   static constexpr bool TF32 = TF32_;
@@ -76,8 +80,12 @@ struct GemmCfg {
   static constexpr int STG_ONE = 32 * 32 * (EPI == EPI_FWD ? ELEM : 4);
   static constexpr int STG_WARP = NOUT * STG_ONE;
   static constexpr int STG_BYTES = EPI_WARPS * STG_WARP;
+  // PRE_TMA: every chunk (32 x 32 tile, activation dtype) a warp handles in one tile.
+  static constexpr int PRE_CHUNKS = BN / 32 / (EPI_WARPS / 4);
+  static constexpr int PRE_WARP = PRE_TMA ? PRE_CHUNKS * 32 * 32 * ELEM : 0;
+  static constexpr int PRE_BYTES = EPI_WARPS * PRE_WARP;
   static constexpr int SMEM_LIMIT = 232448;     // 227 KB opt-in per block
-  static constexpr int RESERVE = 1024 /*align*/ + 512 /*barriers*/ + STG_BYTES;
+  static constexpr int RESERVE = 1024 /*align*/ + 512 /*barriers*/ + STG_BYTES + PRE_BYTES;
   static constexpr int STAGES_RAW = (SMEM_LIMIT - RESERVE) / STAGE_BYTES;
   static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
   static constexpr int THREADS = 64 + 32 * EPI_WARPS;
@@ -98,6 +106,7 @@ struct GemmCfg {
 struct GemmMaps {
   CUtensorMap a, b, a_lo, b_lo, c0, c1;
 };
+// (DGRAD + PRE_TMA: c1 is the load map of pre, same 32 x 32 boxes as c0.)
 
 namespace detail {
 
@@ -107,11 +116,35 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
   return *reinterpret_cast<uint32_t*>(&h);
 }
-__device__ __forceinline__ float gelu_f(float x) { return x * 0.5f * (1.0f + erff(x * 0.70710678118654752f)); }
+// Exact-erf GELU (tensor.cpp:323-351) in the epilogue, evaluated as
+// Phi(x) = 0.5 * (1 + erf(x / sqrt2)) with the Abramowitz-Stegun 7.1.26 form
+// erf(z) = 1 - P(t) exp(-z^2), t = 1 / (1 + p z), |error| <= 1.5e-7, so that
+// GELU and its derivative share one exponential exp(-x^2/2) (which is also
+// sqrt(2 pi) * phi(x)): two MUFU ops and ~12 FMAs instead of libdevice erff's
+// two-branch polynomial. The error is ~100x below bf16 resolution and below
+// the fp32 mode's 1e-5 tolerance.
+__device__ __forceinline__ void gelu_parts(float x, float& cdf, float& pdf) {
+  const float z = fabsf(x) * 0.70710678118654752f;
+  const float t = __fdividef(1.0f, fmaf(0.3275911f, z, 1.0f));
+  const float e = __expf(-0.5f * x * x);
+  float p = fmaf(1.061405429f, t, -1.453152027f);
+  p = fmaf(p, t, 1.421413741f);
+  p = fmaf(p, t, -0.284496736f);
+  p = fmaf(p, t, 0.254829592f);
+  p *= t;
+  const float tail = 0.5f * p * e;  // 0.5 * (1 - erf(z))
+  cdf = x >= 0.f ? 1.0f - tail : tail;
+  pdf = 0.39894228040143267794f * e;
+}
+__device__ __forceinline__ float gelu_f(float x) {
+  float c, d;
+  gelu_parts(x, c, d);
+  return x * c;
+}
 __device__ __forceinline__ float gelu_grad_f(float x) {
-  const float phi = 0.5f * (1.0f + erff(x * 0.70710678118654752f));
-  const float pdf = 0.39894228040143267794f * __expf(-0.5f * x * x);
-  return phi + x * pdf;
+  float c, d;
+  gelu_parts(x, c, d);
+  return fmaf(x, d, c);
 }
 
 // Load 8 consecutive values of the activation dtype as fp32.
@@ -156,6 +189,29 @@ __device__ __forceinline__ void stage_row(uint8_t* stg, int row, const float* v)
   }
 }
 
+// Inverse of stage_row: thread `row` reads its 32 values from a swizzled tile.
+template <bool F32IN>
+__device__ __forceinline__ void unstage_row(const uint8_t* stg, int row, float* v) {
+  if constexpr (F32IN) {
+    const uint8_t* base = stg + row * 128;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const float4 f = *reinterpret_cast<const float4*>(base + (c ^ (row & 7)) * 16);
+      v[4 * c] = f.x; v[4 * c + 1] = f.y; v[4 * c + 2] = f.z; v[4 * c + 3] = f.w;
+    }
+  } else {
+    const uint8_t* base = stg + row * 64;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const uint4 u = *reinterpret_cast<const uint4*>(base + (c ^ ((row >> 1) & 3)) * 16);
+      v[8 * c + 0] = bf16lo(u.x); v[8 * c + 1] = bf16hi(u.x);
+      v[8 * c + 2] = bf16lo(u.y); v[8 * c + 3] = bf16hi(u.y);
+      v[8 * c + 4] = bf16lo(u.z); v[8 * c + 5] = bf16hi(u.z);
+      v[8 * c + 6] = bf16lo(u.w); v[8 * c + 7] = bf16hi(u.w);
+    }
+  }
+}
+
 }  // namespace detail
 
 template <class Cfg>
@@ -169,12 +225,14 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* stage_base = smem;
   uint8_t* stg_base = smem + STAGES * Cfg::STAGE_BYTES;  // 1024-aligned (stage bytes are multiples of 1 KB)
-  uint64_t* bars = reinterpret_cast<uint64_t*>(stg_base + Cfg::STG_BYTES);
+  uint8_t* pre_base = stg_base + Cfg::STG_BYTES;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(pre_base + Cfg::PRE_BYTES);
   uint64_t* full_bar = bars;                    // [STAGES]
   uint64_t* empty_bar = bars + STAGES;          // [STAGES]
   uint64_t* tfull_bar = bars + 2 * STAGES;      // [2]
   uint64_t* tempty_bar = bars + 2 * STAGES + 2; // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 4);
+  uint64_t* pre_bar = bars + 2 * STAGES + 4;    // [EPI_WARPS] (PRE_TMA)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 4 + Cfg::EPI_WARPS);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -201,6 +259,8 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
       mbar_init(&tfull_bar[s], 1);
       mbar_init(&tempty_bar[s], Cfg::EPI_WARPS * 32);
     }
+    if constexpr (Cfg::PRE_TMA)
+      for (int w = 0; w < Cfg::EPI_WARPS; ++w) mbar_init(&pre_bar[w], 1);
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc(tmem_slot, Cfg::TMEM_COLS);
@@ -321,6 +381,9 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
     uint8_t* stg1 = stg0 + Cfg::STG_ONE;
     const bool last = args.flags & EF_LAST;
     const bool first = args.flags & EF_FIRST;
+    const bool pre_tma = Cfg::PRE_TMA && last && (args.flags & EF_GELU_BWD);
+    uint8_t* pre_w = pre_base + ew * Cfg::PRE_WARP;
+    uint32_t pre_phase = 0;
     bool pending = false;
     int acc = 0;
     uint32_t acc_phase = 0;
@@ -331,8 +394,27 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
       const int row0 = m0 + q * 32;     // first row of this warp's 32-row slab
       const int row = row0 + lane;
       const bool row_ok = row < args.M;
+      if constexpr (Cfg::PRE_TMA) {
+        // Stream this warp's pre chunks in while the tile's MMAs still run.
+        if (pre_tma && lane == 0) {
+          uint32_t bytes = 0;
+          for (int k = 0; k < Cfg::PRE_CHUNKS; ++k)
+            if (n0 + (half + k * NSPLIT) * 32 < args.N) bytes += 32 * 32 * Cfg::ELEM;
+          mbar_expect_tx(&pre_bar[ew], bytes);
+          for (int k = 0; k < Cfg::PRE_CHUNKS; ++k) {
+            const int nc = n0 + (half + k * NSPLIT) * 32;
+            if (nc < args.N) tma_load_2d(pre_w + k * 32 * 32 * Cfg::ELEM, &maps.c1, &pre_bar[ew], nc, row0);
+          }
+        }
+      }
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
+      if constexpr (Cfg::PRE_TMA) {
+        if (pre_tma) {
+          mbar_wait(&pre_bar[ew], pre_phase);
+          pre_phase ^= 1;
+        }
+      }
       const uint32_t t_row = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN;
 #pragma unroll 1
       for (int ch = half; ch < BN / 32; ch += NSPLIT) {
@@ -379,7 +461,14 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
                 x[g * 8 + 4] += b.x; x[g * 8 + 5] += b.y; x[g * 8 + 6] += b.z; x[g * 8 + 7] += b.w;
               }
           }
-          if (last && (args.flags & EF_GELU_BWD) && row_ok) {
+          if (pre_tma) {
+            // pre chunk staged by TMA in the same swizzled 32 x 32 layout as the outputs
+            const uint8_t* pc = pre_w + ((ch - half) / NSPLIT) * 32 * 32 * Cfg::ELEM;
+            float pre[32];
+            detail::unstage_row<F32>(pc, lane, pre);
+#pragma unroll
+            for (int e = 0; e < 32; ++e) x[e] *= detail::gelu_grad_f(pre[e]);
+          } else if (last && (args.flags & EF_GELU_BWD) && row_ok) {
 #pragma unroll
             for (int g = 0; g < 4; ++g)
               if (nc + g * 8 < args.N) {
@@ -414,6 +503,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
         }
         pending = true;
       }
+      if constexpr (Cfg::PRE_TMA) __syncwarp();  // all lanes done with the pre chunks
       tc_fence_before();
       mbar_arrive(&tempty_bar[acc]);
       if (++acc == 2) {

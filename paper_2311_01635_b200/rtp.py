@@ -362,7 +362,7 @@ class RtpMlp(_Layer):
 
 def _ws(which, dtype_code, M, I, per, device):
     n = lib.rtpb_step_workspace_bytes(which, dtype_code, M, I, per)
-    return torch.empty(max(16, n), dtype=torch.uint8, device=device)
+    return torch.zeros(max(16, n), dtype=torch.uint8, device=device)  # zero-filled before first use
 
 
 def fwd_step(x, w_shard, y, col0, per, act=None, store_pre=True, stream=None):

@@ -66,9 +66,9 @@ def test_ring_plan_position_laws():
 def test_step_workspace_sizes():
     from paper_2311_01635_b200 import _lib
     L = _lib.lib
-    assert L.rtpb_step_workspace_bytes(0, _lib.BF16, 1024, 768, 3072) == 0
-    assert L.rtpb_step_workspace_bytes(1, _lib.BF16, 1024, 768, 3072) == 0
-    assert L.rtpb_step_workspace_bytes(2, _lib.BF16, 1024, 768, 3072) > 0  # bias-grad partials
+    # one layout for all step kinds: [bias-grad tickets + partials][fp32 splits]
+    sizes = [L.rtpb_step_workspace_bytes(w, _lib.BF16, 1024, 768, 3072) for w in range(3)]
+    assert sizes[0] == sizes[1] == sizes[2] > 0
     assert L.rtpb_step_workspace_bytes(0, _lib.F32, 1024, 768, 3072) >= 2 * 4 * (1024 * 768 + 768 * 3072)
 
 

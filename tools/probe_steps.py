@@ -45,7 +45,7 @@ def run(M, I, O, n, dt, bn=0):
               for j in range(n)]
     s = torch.cuda.current_stream().cuda_stream
     ws_bytes = max(L.rtpb_step_workspace_bytes(w, dt, M, I, per) for w in range(3))
-    ws = torch.empty(max(ws_bytes, 16), dtype=torch.uint8, device=dev)
+    ws = torch.zeros(max(ws_bytes, 16), dtype=torch.uint8, device=dev)
     # forward: every shard into its column block, plain + GELU variants
     Y = torch.zeros(M, O, dtype=tdt, device=dev)
     H = torch.zeros(M, O, dtype=tdt, device=dev)
@@ -92,7 +92,7 @@ def bench(M, I, per, dt=0, iters=20):
     acc = torch.empty(M, I, dtype=torch.float32, device=dev)
     dX = torch.empty(M, I, dtype=tdt, device=dev)
     G = torch.zeros(I * per + per, dtype=torch.float32, device=dev)
-    ws = torch.empty(max(16, max(L.rtpb_step_workspace_bytes(w, dt, M, I, per) for w in range(3))),
+    ws = torch.zeros(max(16, max(L.rtpb_step_workspace_bytes(w, dt, M, I, per) for w in range(3))),
                      dtype=torch.uint8, device=dev)
     s = torch.cuda.current_stream().cuda_stream
     fns = {
