@@ -3,6 +3,7 @@
 // sizing. No allocation, no sync.
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <cstdio>
 #include <cstring>
 #include <mutex>
@@ -95,7 +96,7 @@ int launch_cfg(const Op& a, const Op& b, const Out& c0, const Out* c1, const Gem
   const uint32_t a_box_in = Cfg::A_MN ? Cfg::ATOM_MN : Cfg::BK;
   const uint32_t a_box_out = Cfg::A_MN ? Cfg::BK : Cfg::BM;
   const uint32_t b_box_in = Cfg::B_MN ? Cfg::ATOM_MN : Cfg::BK;
-  const uint32_t b_box_out = Cfg::B_MN ? Cfg::BK : Cfg::BN;
+  const uint32_t b_box_out = Cfg::B_MN ? Cfg::BK : Cfg::B_ROWS;  // pair: each CTA stages BN/2 rows
   int rc;
   if ((rc = encode_2d(&maps.a, a.ptr, F32, a.inner, a.outer, a.ld, a_box_in, a_box_out))) return rc;
   if ((rc = encode_2d(&maps.b, b.ptr, F32, b.inner, b.outer, b.ld, b_box_in, b_box_out))) return rc;
@@ -113,33 +114,61 @@ int launch_cfg(const Op& a, const Op& b, const Out& c0, const Out* c1, const Gem
     if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute(gemm)");
     attr_set = true;
   }
-  const int tiles = ((args.M + Cfg::BM - 1) / Cfg::BM) * ((args.N + Cfg::BN - 1) / Cfg::BN);
-  const int grid = tiles < sm_count() ? tiles : sm_count();
-  rtp_gemm_kernel<Cfg><<<grid, Cfg::THREADS, Cfg::SMEM_BYTES, stream>>>(maps, args);
-  cudaError_t e = cudaGetLastError();
+  const int tiles = ((args.M + Cfg::TILE_M - 1) / Cfg::TILE_M) * ((args.N + Cfg::BN - 1) / Cfg::BN);
+  cudaError_t e;
+  if constexpr (Cfg::PAIR) {
+    // one CTA pair (cluster of 2 on a TPC) per 256-row tile slot, persistent
+    const int pairs = std::min(tiles, sm_count() / 2);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(unsigned(2 * pairs));
+    cfg.blockDim = dim3(Cfg::THREADS);
+    cfg.dynamicSmemBytes = Cfg::SMEM_BYTES;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(&cfg, rtp_gemm_kernel<Cfg>, maps, args);
+  } else {
+    const int grid = tiles < sm_count() ? tiles : sm_count();
+    rtp_gemm_kernel<Cfg><<<grid, Cfg::THREADS, Cfg::SMEM_BYTES, stream>>>(maps, args);
+    e = cudaGetLastError();
+  }
   if (e != cudaSuccess) return set_cuda_error(e, "rtp_gemm_kernel launch");
   count_launch();
   return RTPB_OK;
 }
 
-// Wave-quantisation aware tile width: minimise ceil(tiles/SMs) * (BN + 48).
-int choose_bn(int M, int N, bool tf32, bool b_mn) {
-  const int cands_bf16[3] = {256, 128, 64};
-  const int cands_tf32[2] = {128, 64};
-  const int* c = tf32 ? cands_tf32 : cands_bf16;
-  const int nc = tf32 ? 2 : 3;
+// Tile shape: a CTA pair computing 256 x BN (cta_group::2) or one CTA
+// computing 128 x BN. Code = BN for single-CTA tiles, 1000 + BN for pairs.
+// Choice minimises wave-quantised time: ceil(tiles / slots) * per-tile cost,
+// per-tile cost = per-SM work / relative MMA efficiency + fixed overhead
+// (relative efficiencies from measured B200 throughput of each shape).
+int choose_tile(int M, int N, bool tf32) {
+  struct Cand {
+    int code, rows, bn;
+    double eff;
+  };
+  static const Cand bf16[] = {{1256, 256, 256, 1.00}, {1128, 256, 128, 0.95}, {256, 128, 256, 0.90},
+                              {128, 128, 128, 0.72}, {64, 128, 64, 0.50}};
+  static const Cand f32[] = {{128, 128, 128, 1.0}, {64, 128, 64, 0.7}};
+  const Cand* c = tf32 ? f32 : bf16;
+  const int nc = tf32 ? 2 : 5;
   const int sms = sm_count();
-  int best = c[nc - 1];
-  long best_cost = -1;
+  int best = c[0].code;
+  double best_cost = -1;
   for (int i = 0; i < nc; ++i) {
-    const int bn = c[i];
-    if (b_mn && bn % (tf32 ? 32 : 64)) continue;
-    const long tiles = long((M + 127) / 128) * ((N + bn - 1) / bn);
-    const long waves = (tiles + sms - 1) / sms;
-    const long cost = waves * (bn + 48);
+    const bool pair = c[i].code > 1000;
+    const long tiles = long((M + c[i].rows - 1) / c[i].rows) * ((N + c[i].bn - 1) / c[i].bn);
+    const long slots = pair ? sms / 2 : sms;
+    const long waves = (tiles + slots - 1) / slots;
+    const double cost = double(waves) * (128.0 * c[i].bn / c[i].eff + 48.0 * 128.0);
     if (best_cost < 0 || cost < best_cost) {
       best_cost = cost;
-      best = bn;
+      best = c[i].code;
     }
   }
   return best;
@@ -148,31 +177,33 @@ int choose_bn(int M, int N, bool tf32, bool b_mn) {
 constexpr int kEpiWarps = 8;
 
 template <int EPI, bool TF32>
-int dispatch_bn(int bn, const Op& a, const Op& b, const Out& c0, const Out* c1, const GemmArgs& args,
-                cudaStream_t s) {
+int dispatch_tile(int code, const Op& a, const Op& b, const Out& c0, const Out* c1, const GemmArgs& args,
+                  cudaStream_t s) {
   constexpr bool AMN = !TF32 && EPI == EPI_WGRAD;
   constexpr bool BMN = !TF32 && EPI != EPI_DGRAD;
-  switch (bn) {
-    case 64: return launch_cfg<GemmCfg<EPI, 64, TF32, kEpiWarps, AMN, BMN>>(a, b, c0, c1, args, s);
-    case 128: return launch_cfg<GemmCfg<EPI, 128, TF32, kEpiWarps, AMN, BMN>>(a, b, c0, c1, args, s);
-    default:
-      if constexpr (!TF32) return launch_cfg<GemmCfg<EPI, 256, false, kEpiWarps, AMN, BMN>>(a, b, c0, c1, args, s);
-      return launch_cfg<GemmCfg<EPI, 128, TF32, kEpiWarps, AMN, BMN>>(a, b, c0, c1, args, s);
+  if constexpr (!TF32) {
+    if (code == 1256) return launch_cfg<GemmCfg<EPI, 256, false, kEpiWarps, AMN, BMN, false, true>>(a, b, c0, c1, args, s);
+    if (code == 1128) return launch_cfg<GemmCfg<EPI, 128, false, kEpiWarps, AMN, BMN, false, true>>(a, b, c0, c1, args, s);
+    if (code == 256) return launch_cfg<GemmCfg<EPI, 256, false, kEpiWarps, AMN, BMN>>(a, b, c0, c1, args, s);
   }
+  if (code == 64) return launch_cfg<GemmCfg<EPI, 64, TF32, kEpiWarps, AMN, BMN>>(a, b, c0, c1, args, s);
+  return launch_cfg<GemmCfg<EPI, 128, TF32, kEpiWarps, AMN, BMN>>(a, b, c0, c1, args, s);
 }
 
 template <int EPI>
 int dispatch(bool tf32, const Op& a, const Op& b, const Out& c0, const Out* c1, GemmArgs args, cudaStream_t s,
-             int force_bn) {
-  const bool b_mn = !tf32 && (EPI != EPI_DGRAD);
-  const int bn = force_bn ? force_bn : choose_bn(args.M, args.N, tf32, b_mn);
+             int force) {
+  int code = force ? force : choose_tile(args.M, args.N, tf32);
+  if (tf32 && code > 1000) code -= 1000;  // no pair tiles in the fp32 (3xTF32) mode
+  if (tf32 && code == 256) code = 128;
+  const int bn = code % 1000;
   const int num_n = (args.N + bn - 1) / bn;
   // Raster n fastest when the B operand (all n-blocks x K) fits comfortably in
   // L2: concurrent CTAs then share each A row-block, which is read once.
   const double b_bytes = double(num_n) * bn * args.K * (tf32 ? 4.0 : 2.0);
   args.n_fastest = (EPI != EPI_WGRAD) && b_bytes < 48e6;
-  return tf32 ? dispatch_bn<EPI, true>(bn, a, b, c0, c1, args, s)
-              : dispatch_bn<EPI, false>(bn, a, b, c0, c1, args, s);
+  return tf32 ? dispatch_tile<EPI, true>(code, a, b, c0, c1, args, s)
+              : dispatch_tile<EPI, false>(code, a, b, c0, c1, args, s);
 }
 
 }  // namespace

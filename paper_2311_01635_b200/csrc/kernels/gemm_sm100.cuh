@@ -51,9 +51,17 @@ struct GemmArgs {
   int64_t ld_acc;
 };
 
-template <int EPI_, int BN_, bool TF32_, int EPI_WARPS_, bool A_MN_, bool B_MN_, bool PRE_TMA_ = false>
+template <int EPI_, int BN_, bool TF32_, int EPI_WARPS_, bool A_MN_, bool B_MN_, bool PRE_TMA_ = false,
+          bool PAIR_ = false>
 struct GemmCfg {
   static constexpr int EPI = EPI_;
+  // PAIR: a CTA pair (cluster of 2) computes a 256 x BN tile with
+  // tcgen05.mma.cta_group::2: each CTA stages its own 128 rows of A and half
+  // of B's BN columns, the leader issues the MMAs, each CTA's TMEM holds its
+  // 128 accumulator rows. Halves per-SM smem traffic for B.
+  static constexpr bool PAIR = PAIR_;
+  static constexpr int TILE_M = PAIR ? 256 : 128;
+  static constexpr int B_ROWS = PAIR ? BN_ / 2 : BN_;  // B rows (N) staged per CTA
   // DGRAD with gelu' fused: the tile's pre values are streamed into shared
   // memory by TMA when the tile starts (while its MMAs run), instead of
   // per-row global loads in the epilogue.
@@ -69,7 +77,7 @@ struct GemmCfg {
   static constexpr bool A_MN = A_MN_;  // bf16: FWD (K,MN), DGRAD (K,K), WGRAD (MN,MN)
   static constexpr bool B_MN = B_MN_;  // tf32: always (K,K) — operands pre-transposed
   static constexpr int A_BYTES = BM * 128;
-  static constexpr int B_BYTES = BN * 128;
+  static constexpr int B_BYTES = B_ROWS * 128;
   static constexpr int NOPS = TF32 ? 2 : 1;      // hi (+ lo) copies per operand
   static constexpr int STAGE_BYTES = NOPS * (A_BYTES + B_BYTES);
   static constexpr int EPI_WARPS = EPI_WARPS_;
@@ -92,7 +100,8 @@ struct GemmCfg {
   static constexpr int TMEM_COLS = (2 * BN <= 32) ? 32 : (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128
                                    : (2 * BN <= 256) ? 256 : 512;
   static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + RESERVE;
-  static constexpr uint32_t IDESC = ptx::idesc_make(BM, BN, TF32 ? 2 : 1, A_MN, B_MN);
+  static constexpr uint32_t IDESC = ptx::idesc_make(TILE_M, BN, TF32 ? 2 : 1, A_MN, B_MN);
+  static_assert(!PAIR || (!TF32 && (!B_MN || B_ROWS % ATOM_MN == 0)), "pair tiles: bf16, B halves in whole atoms");
   static_assert(STAGES >= 2, "not enough shared memory for 2 stages");
   static_assert(BN % 32 == 0 && BN >= 32 && BN <= 256, "BN");
   static_assert(EPI_WARPS == 4 || EPI_WARPS == 8, "epilogue warps");
@@ -237,7 +246,11 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
 
-  const int num_m = (args.M + BM - 1) / BM;
+  // Pair mode: both CTAs of a cluster work on the same 256-row tile.
+  const uint32_t rank = Cfg::PAIR ? cluster_ctarank() : 0;
+  const int unit = Cfg::PAIR ? int(blockIdx.x >> 1) : int(blockIdx.x);
+  const int units = Cfg::PAIR ? int(gridDim.x >> 1) : int(gridDim.x);
+  const int num_m = (args.M + Cfg::TILE_M - 1) / Cfg::TILE_M;
   const int num_n = (args.N + BN - 1) / BN;
   const int num_tiles = num_m * num_n;
   const int num_kb = (args.K + BK - 1) / BK;
@@ -257,15 +270,23 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull_bar[s], 1);
-      mbar_init(&tempty_bar[s], Cfg::EPI_WARPS * 32);
+      mbar_init(&tempty_bar[s], (Cfg::PAIR ? 2 : 1) * Cfg::EPI_WARPS * 32);  // both CTAs drain
     }
     if constexpr (Cfg::PRE_TMA)
       for (int w = 0; w < Cfg::EPI_WARPS; ++w) mbar_init(&pre_bar[w], 1);
     fence_mbar_init();
   }
-  if (warp == 1) tmem_alloc(tmem_slot, Cfg::TMEM_COLS);
+  if (warp == 1) {
+    if constexpr (Cfg::PAIR)
+      tmem_alloc_pair(tmem_slot, Cfg::TMEM_COLS);  // same warp id in both CTAs
+    else
+      tmem_alloc(tmem_slot, Cfg::TMEM_COLS);
+  }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (Cfg::PAIR)
+    cluster_sync();  // peer barriers initialised before any remote arrive / TMA
+  else
+    __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
@@ -284,14 +305,47 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      auto load = [&](void* dst, const CUtensorMap* m, uint64_t* bar, int c0, int c1) {
+        if constexpr (Cfg::PAIR)
+          tma_load_2d_pair(dst, m, bar, c0, c1);  // bytes counted on the leader's barrier
+        else
+          tma_load_2d(dst, m, bar, c0, c1);
+      };
+      // A box that lies entirely outside the tensor completes without
+      // crediting bytes, so such boxes are skipped and the leader expects only
+      // the bytes both CTAs actually request (their smem is never read into a
+      // stored result: those rows / columns are clipped by the output maps).
+      auto a_bytes = [&](int ma0) {
+        int b = 0;
+        if constexpr (Cfg::A_MN) {
+          for (int c = 0; c < BM / Cfg::ATOM_MN; ++c)
+            if (ma0 + c * Cfg::ATOM_MN < args.M) b += BK * 128;
+        } else {
+          if (ma0 < args.M) b = Cfg::A_BYTES;
+        }
+        return b * Cfg::NOPS;
+      };
+      auto b_bytes = [&](int nb0) {
+        int b = 0;
+        if constexpr (Cfg::B_MN) {
+          for (int c = 0; c < Cfg::B_ROWS / Cfg::ATOM_MN; ++c)
+            if (nb0 + c * Cfg::ATOM_MN < args.N) b += BK * 128;
+        } else {
+          if (nb0 < args.N) b = Cfg::B_BYTES;
+        }
+        return b * Cfg::NOPS;
+      };
+      for (int t = unit; t < num_tiles; t += units) {
         int mb, nb;
         tile_coords(t, mb, nb);
-        const int m0 = mb * BM, n0 = nb * BN;
+        // this CTA's A rows and B columns (pair: its half of the 256 x BN tile)
+        const int m0 = mb * Cfg::TILE_M + int(rank) * BM, n0 = nb * BN + int(rank) * Cfg::B_ROWS;
+        int expect = a_bytes(mb * Cfg::TILE_M) + b_bytes(nb * BN);
+        if constexpr (Cfg::PAIR) expect += a_bytes(mb * Cfg::TILE_M + BM) + b_bytes(nb * BN + Cfg::B_ROWS);
         for (int kb = 0; kb < num_kb; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
           uint8_t* sA = stage_base + stage * Cfg::STAGE_BYTES;
-          mbar_expect_tx(&full_bar[stage], Cfg::STAGE_BYTES);
+          if (rank == 0) mbar_expect_tx(&full_bar[stage], uint32_t(expect));
           const int k0 = kb * BK;
           for (int op = 0; op < Cfg::NOPS; ++op) {
             const CUtensorMap* ma = op ? &maps.a_lo : &maps.a;
@@ -301,16 +355,18 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
             if constexpr (Cfg::A_MN) {
 #pragma unroll
               for (int c = 0; c < BM / Cfg::ATOM_MN; ++c)
-                tma_load_2d(dA + c * (BK * 128), ma, &full_bar[stage], m0 + c * Cfg::ATOM_MN, k0);
+                if (m0 + c * Cfg::ATOM_MN < args.M)
+                  load(dA + c * (BK * 128), ma, &full_bar[stage], m0 + c * Cfg::ATOM_MN, k0);
             } else {
-              tma_load_2d(dA, ma, &full_bar[stage], k0, m0);
+              if (m0 < args.M) load(dA, ma, &full_bar[stage], k0, m0);
             }
             if constexpr (Cfg::B_MN) {
 #pragma unroll
-              for (int c = 0; c < BN / Cfg::ATOM_MN; ++c)
-                tma_load_2d(dB + c * (BK * 128), mbm, &full_bar[stage], n0 + c * Cfg::ATOM_MN, k0);
+              for (int c = 0; c < Cfg::B_ROWS / Cfg::ATOM_MN; ++c)
+                if (n0 + c * Cfg::ATOM_MN < args.N)
+                  load(dB + c * (BK * 128), mbm, &full_bar[stage], n0 + c * Cfg::ATOM_MN, k0);
             } else {
-              tma_load_2d(dB, mbm, &full_bar[stage], k0, n0);
+              if (n0 < args.N) load(dB, mbm, &full_bar[stage], k0, n0);
             }
           }
           if (++stage == STAGES) {
@@ -321,13 +377,13 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
       }
     }
   } else if (warp == 1) {
-    // ===================== MMA issuer =====================
-    if (lane == 0) {
+    // ===================== MMA issuer (pair: leader CTA only) =====================
+    if (lane == 0 && rank == 0) {
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      for (int t = unit; t < num_tiles; t += units) {
         mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
@@ -354,17 +410,26 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
               umma_tf32(d_tmem, adesc, bdesc, Cfg::IDESC, accum);
               umma_tf32(d_tmem, adesc, bdesc_lo, Cfg::IDESC, 1);
               umma_tf32(d_tmem, adesc_lo, bdesc, Cfg::IDESC, 1);
+            } else if constexpr (Cfg::PAIR) {
+              umma_f16_pair(d_tmem, adesc, bdesc, Cfg::IDESC, accum);
             } else {
               umma_f16(d_tmem, adesc, bdesc, Cfg::IDESC, accum);
             }
           }
-          umma_commit(&empty_bar[stage]);
+          // free the stage in both CTAs / signal both CTAs' epilogues
+          if constexpr (Cfg::PAIR)
+            umma_commit_pair(&empty_bar[stage]);
+          else
+            umma_commit(&empty_bar[stage]);
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
-        umma_commit(&tfull_bar[acc]);
+        if constexpr (Cfg::PAIR)
+          umma_commit_pair(&tfull_bar[acc]);
+        else
+          umma_commit(&tfull_bar[acc]);
         if (++acc == 2) {
           acc = 0;
           acc_phase ^= 1;
@@ -387,10 +452,10 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
     bool pending = false;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+    for (int t = unit; t < num_tiles; t += units) {
       int mb, nb;
       tile_coords(t, mb, nb);
-      const int m0 = mb * BM, n0 = nb * BN;
+      const int m0 = mb * Cfg::TILE_M + int(rank) * BM, n0 = nb * BN;  // this CTA's 128 rows
       const int row0 = m0 + q * 32;     // first row of this warp's 32-row slab
       const int row = row0 + lane;
       const bool row_ok = row < args.M;
@@ -505,7 +570,10 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
       }
       if constexpr (Cfg::PRE_TMA) __syncwarp();  // all lanes done with the pre chunks
       tc_fence_before();
-      mbar_arrive(&tempty_bar[acc]);
+      if constexpr (Cfg::PAIR)
+        mbar_arrive_cluster(&tempty_bar[acc], 0);  // the leader's MMA reuses both halves
+      else
+        mbar_arrive(&tempty_bar[acc]);
       if (++acc == 2) {
         acc = 0;
         acc_phase ^= 1;
@@ -516,10 +584,16 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
   }
 
   tc_fence_before();
-  __syncthreads();
+  if constexpr (Cfg::PAIR)
+    cluster_sync();  // both CTAs done with TMEM / remote barriers before release
+  else
+    __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc(tmem_base, Cfg::TMEM_COLS);
+    if constexpr (Cfg::PAIR)
+      tmem_dealloc_pair(tmem_base, Cfg::TMEM_COLS);
+    else
+      tmem_dealloc(tmem_base, Cfg::TMEM_COLS);
   }
 }
 

@@ -28,10 +28,14 @@ def make(M, I, O, n, dt, seed=0):
 
 
 CASES = [
-    # M, I, O, n, dtype, forced tile width (0 = heuristic)
+    # M, I, O, n, dtype, forced tile (0 = heuristic; BN for one CTA, 1000+BN for a CTA pair)
     (256, 128, 256, 2, "bf16", 64),
     (256, 128, 256, 2, "bf16", 128),
     (256, 128, 512, 2, "bf16", 256),
+    (512, 128, 512, 2, "bf16", 1256),  # cta_group::2, 256 x 256 tiles
+    (512, 128, 512, 2, "bf16", 1128),  # cta_group::2, 256 x 128 tiles
+    (1000, 768, 3072, 4, "bf16", 1256),  # pair tiles with a ragged last 256-row tile
+    (300, 64, 256, 1, "bf16", 1128),
     (200, 64, 192, 3, "bf16", 0),     # ragged M, per = 64
     (1000, 768, 3072, 4, "bf16", 0),  # GPT-2 width, tail rows
     (8, 8, 16, 2, "bf16", 0),         # minimal aligned shape
@@ -105,7 +109,7 @@ def test_gpt2_width_bench_shapes_all_tile_widths():
     M, I, O = 2048, 768, 3072
     X, dY, W, b, shards = make(M, I, O, 1, "bf16", seed=3)
     ref = X.double() @ W.double() + b.double()
-    for bn in (64, 128, 256):
+    for bn in (64, 128, 256, 1128, 1256):
         _lib.lib.rtpb_debug_force_bn(bn)
         try:
             Y = torch.zeros(M, O, dtype=torch.bfloat16, device="cuda")
