@@ -48,6 +48,12 @@ int check_geom(size_t M, size_t I, size_t per) {
 
 cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
 
+// Zero-initialised, self-resetting part of a step workspace.
+size_t split_flag_bytes(size_t I, size_t per) { return ((I + 255) / 256) * ((per + 255) / 256) * sizeof(unsigned); }
+size_t persistent_ws_bytes(size_t M, size_t I, size_t per) {
+  return align256(colsum_workspace_bytes(M, per)) + align256(split_flag_bytes(I, per));
+}
+
 // Optional per-launch timing of the step GEMMs: a CUDA event pair recorded on
 // the launching stream around each GEMM (bench.py's roofline numerator).
 struct ProfRec {
@@ -116,11 +122,11 @@ uint64_t rtpb_launch_count(void) { return g_launches.load(); }
 void rtpb_debug_force_bn(int bn) { g_force_bn = bn; }
 
 // Workspace layout, identical for every step kind of a layer so one buffer
-// serves all three: [bias-grad tickets + partials (tickets stay zero)]
-// [fp32 mode: tf32 hi/lo operand splits].
+// serves all three: [bias-grad tickets + partials][dW split-K tile counters]
+// (both left at zero by the kernels) [fp32 mode: tf32 hi/lo operand splits].
 size_t rtpb_step_workspace_bytes(int which, int dtype, size_t M, size_t I, size_t per) {
   const bool f32 = dtype == RTPB_F32;
-  size_t b = align256(colsum_workspace_bytes(M, per));
+  size_t b = persistent_ws_bytes(M, I, per);
   if (f32) {
     if (which == 0) b += 2 * align256(M * I * 4) + 2 * align256(I * per * 4);
     if (which == 1) b += 2 * align256(M * per * 4) + 2 * align256(I * per * 4);
@@ -154,7 +160,7 @@ int rtpb_fwd_step(int dtype, const void* x, size_t ldx, const void* w_shard, voi
   p.M = M; p.I = I; p.per = per; p.flags = flags; p.force_bn = g_force_bn;
   if (f32) {
     Carve c{static_cast<char*>(workspace), workspace ? workspace_bytes : 0};
-    c.take(colsum_workspace_bytes(M, per) / sizeof(float));  // keep the zeroed tickets intact
+    c.take(persistent_ws_bytes(M, I, per) / sizeof(float));  // keep the zeroed counters intact
     float *xh = c.take(M * I), *xl = c.take(M * I), *wh = c.take(I * per), *wl = c.take(I * per);
     if (!c.ok) return set_error(RTPB_ERR_DIMENSION, "fwd_step: workspace too small");
     if ((rc = tf32_split(static_cast<const float*>(x), M, I, ldx, xh, xl, s))) return rc;
@@ -182,7 +188,7 @@ int rtpb_dgrad_step(int dtype, const void* dy, size_t ldy, size_t col0, const vo
   p.M = M; p.I = I; p.per = per; p.flags = flags; p.force_bn = g_force_bn;
   if (f32) {
     Carve c{static_cast<char*>(workspace), workspace ? workspace_bytes : 0};
-    c.take(colsum_workspace_bytes(M, per) / sizeof(float));  // keep the zeroed tickets intact
+    c.take(persistent_ws_bytes(M, I, per) / sizeof(float));  // keep the zeroed counters intact
     float *dh = c.take(M * per), *dl = c.take(M * per), *wh = c.take(I * per), *wl = c.take(I * per);
     if (!c.ok) return set_error(RTPB_ERR_DIMENSION, "dgrad_step: workspace too small");
     if ((rc = tf32_split(static_cast<const float*>(p.dy), M, per, ldy, dh, dl, s))) return rc;
@@ -203,9 +209,11 @@ int rtpb_wgrad_step(int dtype, const void* x, size_t ldx, const void* dy, size_t
   cudaStream_t s = as_stream(stream);
   Carve c{static_cast<char*>(workspace), workspace ? workspace_bytes : 0};
   float* part = c.take(colsum_workspace_bytes(M, per) / sizeof(float));
+  unsigned* flags = reinterpret_cast<unsigned*>(c.take(split_flag_bytes(I, per) / sizeof(float)));
   StepWgrad p{};
   p.x = x; p.ldx = ldx; p.dy = static_cast<const char*>(dy) + col0 * esz; p.ldy = ldy;
   p.g_in = g_in; p.g_out = g_out; p.M = M; p.I = I; p.per = per; p.force_bn = g_force_bn;
+  p.split_flags = flags;
   if (f32) {
     const size_t Mp = (M + 7) & ~size_t(7);
     float *xh = c.take(Mp * I), *xl = c.take(Mp * I), *dh = c.take(Mp * per), *dl = c.take(Mp * per);

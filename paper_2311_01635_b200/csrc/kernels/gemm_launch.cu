@@ -114,7 +114,8 @@ int launch_cfg(const Op& a, const Op& b, const Out& c0, const Out* c1, const Gem
     if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute(gemm)");
     attr_set = true;
   }
-  const int tiles = ((args.M + Cfg::TILE_M - 1) / Cfg::TILE_M) * ((args.N + Cfg::BN - 1) / Cfg::BN);
+  const int tiles = ((args.M + Cfg::TILE_M - 1) / Cfg::TILE_M) * ((args.N + Cfg::BN - 1) / Cfg::BN) *
+                    (args.k_splits > 1 ? args.k_splits : 1);  // work units
   cudaError_t e;
   if constexpr (Cfg::PAIR) {
     // one CTA pair (cluster of 2 on a TPC) per 256-row tile slot, persistent
@@ -196,6 +197,21 @@ int dispatch(bool tf32, const Op& a, const Op& b, const Out& c0, const Out* c1, 
   int code = force ? force : choose_tile(args.M, args.N, tf32);
   if (tf32 && code > 1000) code -= 1000;  // no pair tiles in the fp32 (3xTF32) mode
   if (tf32 && code == 256) code = 128;
+  args.k_splits = 1;
+  if (EPI == EPI_WGRAD && !tf32 && args.split_flags) {
+    // dW outputs (I x per) are small and K (tokens) long: too few 256x256
+    // tiles to occupy every CTA pair. Split K instead of shrinking tiles.
+    const int pairs = sm_count() / 2;
+    const int tiles = ((args.M + 255) / 256) * ((args.N + 255) / 256);
+    const int kb = (args.K + 63) / 64;
+    if (!force && tiles < pairs) {
+      int s = std::min(pairs / tiles, std::min(8, kb / 8));
+      if (s >= 2) {
+        code = 1256;
+        args.k_splits = s;
+      }
+    }
+  }
   const int bn = code % 1000;
   const int num_n = (args.N + bn - 1) / bn;
   // Raster n fastest when the B operand (all n-blocks x K) fits comfortably in
@@ -271,6 +287,7 @@ int gemm_wgrad(bool f32, const StepWgrad& p, cudaStream_t s) {
     if (e != cudaSuccess) return set_cuda_error(e, "wgrad: seed G_out");
   }
   Out c0{p.g_out, true, p.per, p.I, p.per};
+  g.split_flags = p.split_flags;
   return dispatch<EPI_WGRAD>(f32, a, b, c0, nullptr, g, s, p.force_bn);
 }
 

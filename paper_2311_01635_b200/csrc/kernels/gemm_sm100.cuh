@@ -49,6 +49,12 @@ struct GemmArgs {
   int64_t ld_aux;
   const float* acc;    // DGRAD LAST && !FIRST: fp32 accumulator read (M x N, ld_acc)
   int64_t ld_acc;
+  // WGRAD split-K: work unit = (tile, split); split s reduce-adds its partial
+  // into G only after split s-1 of the same tile has completed its writes
+  // (per-tile counter in zeroed workspace, reset by the last split), so the
+  // summation order is fixed and results are bitwise reproducible.
+  int k_splits;
+  unsigned* split_flags;
 };
 
 template <int EPI_, int BN_, bool TF32_, int EPI_WARPS_, bool A_MN_, bool B_MN_, bool PRE_TMA_ = false,
@@ -254,6 +260,17 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
   const int num_n = (args.N + BN - 1) / BN;
   const int num_tiles = num_m * num_n;
   const int num_kb = (args.K + BK - 1) / BK;
+  // Work unit u = split * num_tiles + tile: every split-s unit precedes every
+  // split-(s+1) unit in each CTA's sequence, so the ordered reduction below
+  // always waits on work that is running or done (no deadlock).
+  const int splits = args.k_splits > 1 ? args.k_splits : 1;
+  const int num_units = num_tiles * splits;
+  const int kb_per = (num_kb + splits - 1) / splits;
+  auto unit_kb = [&](int u, int& kb0, int& kb1) {
+    const int s = u / num_tiles;
+    kb0 = s * kb_per;
+    kb1 = min(num_kb, kb0 + kb_per);
+  };
 
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&maps.a);
@@ -335,14 +352,15 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
         }
         return b * Cfg::NOPS;
       };
-      for (int t = unit; t < num_tiles; t += units) {
-        int mb, nb;
-        tile_coords(t, mb, nb);
+      for (int u = unit; u < num_units; u += units) {
+        int mb, nb, kb0, kb1;
+        tile_coords(u % num_tiles, mb, nb);
+        unit_kb(u, kb0, kb1);
         // this CTA's A rows and B columns (pair: its half of the 256 x BN tile)
         const int m0 = mb * Cfg::TILE_M + int(rank) * BM, n0 = nb * BN + int(rank) * Cfg::B_ROWS;
         int expect = a_bytes(mb * Cfg::TILE_M) + b_bytes(nb * BN);
         if constexpr (Cfg::PAIR) expect += a_bytes(mb * Cfg::TILE_M + BM) + b_bytes(nb * BN + Cfg::B_ROWS);
-        for (int kb = 0; kb < num_kb; ++kb) {
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
           uint8_t* sA = stage_base + stage * Cfg::STAGE_BYTES;
           if (rank == 0) mbar_expect_tx(&full_bar[stage], uint32_t(expect));
@@ -383,11 +401,13 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int t = unit; t < num_tiles; t += units) {
+      for (int u = unit; u < num_units; u += units) {
+        int kb0, kb1;
+        unit_kb(u, kb0, kb1);
         mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
-        for (int kb = 0; kb < num_kb; ++kb) {
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full_bar[stage], phase);
           tc_fence_after();
           const uint32_t a_base = smem_u32(stage_base + stage * Cfg::STAGE_BYTES);
@@ -402,7 +422,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
             const uint32_t b_lbo = Cfg::B_MN ? BK * 128 : 16;
             const uint64_t adesc = sdesc_sw128(a_base + a_off, a_lbo, 1024);
             const uint64_t bdesc = sdesc_sw128(b_base + b_off, b_lbo, 1024);
-            const uint32_t accum = (kb | kk) != 0;
+            const uint32_t accum = (kb != kb0) || kk != 0;
             if constexpr (Cfg::TF32) {
               constexpr uint32_t LO = Cfg::A_BYTES + Cfg::B_BYTES;
               const uint64_t adesc_lo = sdesc_sw128(a_base + LO + a_off, a_lbo, 1024);
@@ -452,7 +472,9 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
     bool pending = false;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int t = unit; t < num_tiles; t += units) {
+    const int wgroup = Cfg::EPI_WARPS * (Cfg::PAIR ? 2 : 1);  // epilogue warps per tile
+    for (int u = unit; u < num_units; u += units) {
+      const int t = u % num_tiles, split = u / num_tiles;
       int mb, nb;
       tile_coords(t, mb, nb);
       const int m0 = mb * Cfg::TILE_M + int(rank) * BM, n0 = nb * BN;  // this CTA's 128 rows
@@ -460,20 +482,36 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
       const int row = row0 + lane;
       const bool row_ok = row < args.M;
       if constexpr (Cfg::PRE_TMA) {
-        // Stream this warp's pre chunks in while the tile's MMAs still run.
+        // Stream this warp's pre chunks in while the tile's MMAs still run
+        // (boxes entirely outside the tensor are skipped: they credit no bytes).
         if (pre_tma && lane == 0) {
           uint32_t bytes = 0;
           for (int k = 0; k < Cfg::PRE_CHUNKS; ++k)
-            if (n0 + (half + k * NSPLIT) * 32 < args.N) bytes += 32 * 32 * Cfg::ELEM;
+            if (n0 + (half + k * NSPLIT) * 32 < args.N && row0 < args.M) bytes += 32 * 32 * Cfg::ELEM;
           mbar_expect_tx(&pre_bar[ew], bytes);
           for (int k = 0; k < Cfg::PRE_CHUNKS; ++k) {
             const int nc = n0 + (half + k * NSPLIT) * 32;
-            if (nc < args.N) tma_load_2d(pre_w + k * 32 * 32 * Cfg::ELEM, &maps.c1, &pre_bar[ew], nc, row0);
+            if (nc < args.N && row0 < args.M)
+              tma_load_2d(pre_w + k * 32 * 32 * Cfg::ELEM, &maps.c1, &pre_bar[ew], nc, row0);
           }
         }
       }
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
+      if constexpr (Cfg::EPI == EPI_WGRAD) {
+        if (split > 0) {
+          // ordered split-K: wait until every warp of split-1 has landed its sums
+          if (lane == 0) {
+            const unsigned need = unsigned(split * wgroup);
+            unsigned seen;
+            do {
+              asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(args.split_flags + t) : "memory");
+            } while (seen < need);
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+          }
+          __syncwarp();
+        }
+      }
       if constexpr (Cfg::PRE_TMA) {
         if (pre_tma) {
           mbar_wait(&pre_bar[ew], pre_phase);
@@ -567,6 +605,19 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
           bulk_commit();
         }
         pending = true;
+      }
+      if constexpr (Cfg::EPI == EPI_WGRAD) {
+        if (splits > 1) {
+          // publish: this warp's reduce-adds for (tile, split) are performed
+          if (lane == 0) {
+            bulk_wait0();
+            __threadfence();
+            const unsigned old = atomicAdd(args.split_flags + t, 1u);
+            if (old + 1 == unsigned(splits * wgroup)) args.split_flags[t] = 0u;  // last arrival re-zeroes
+          }
+          __syncwarp();
+          pending = false;
+        }
       }
       if constexpr (Cfg::PRE_TMA) __syncwarp();  // all lanes done with the pre chunks
       tc_fence_before();

@@ -41,6 +41,7 @@ struct StepWgrad {
   const void* x; const void* x_lo; size_t ldx;
   const void* dy; const void* dy_lo; size_t ldy;  // dy points at the column block
   const float* g_in; float* g_out;                // I x per block of the grad shard
+  unsigned* split_flags;                          // zeroed per-tile counters (split-K order)
   size_t M, I, per;
   int force_bn;
 };
