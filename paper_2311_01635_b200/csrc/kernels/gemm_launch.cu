@@ -153,8 +153,9 @@ int choose_tile(int M, int N, bool tf32) {
     int code, rows, bn;
     double eff;
   };
-  static const Cand bf16[] = {{1256, 256, 256, 1.00}, {1128, 256, 128, 0.95}, {256, 128, 256, 0.90},
-                              {128, 128, 128, 0.72}, {64, 128, 64, 0.50}};
+  // (eff: measured on B200 at the config (b)/(d) step shapes, tools/tile_sweep.py)
+  static const Cand bf16[] = {{1256, 256, 256, 1.00}, {1128, 256, 128, 0.60}, {256, 128, 256, 0.85},
+                              {128, 128, 128, 0.62}, {64, 128, 64, 0.32}};
   static const Cand f32[] = {{128, 128, 128, 1.0}, {64, 128, 64, 0.7}};
   const Cand* c = tf32 ? f32 : bf16;
   const int nc = tf32 ? 2 : 5;
@@ -262,11 +263,16 @@ int gemm_dgrad(bool f32, const StepDgrad& p, cudaStream_t s) {
   // last step: emit dX in the activation dtype; otherwise store / reduce-add fp32.
   Out c0 = last ? Out{p.dx, f32, p.I, p.M, p.ldx} : Out{p.acc, true, p.I, p.M, p.ld_acc};
   if (last && (p.flags & EF_GELU_BWD)) {
-    // gelu' fused: stream pre tiles through smem (PRE_TMA config, 128-wide tiles).
+    // gelu' fused: stream pre tiles through smem (PRE_TMA configs): CTA-pair
+    // 256 x 256 tiles (4 stages) when they fill the machine, else 128 x 128.
     Out pre{p.pre, f32, p.I, p.M, p.ldpre};
-    const int num_n = (g.N + 127) / 128;
-    g.n_fastest = double(num_n) * 128 * g.K * (f32 ? 4.0 : 2.0) < 48e6;
+    int code = p.force_bn ? p.force_bn : choose_tile(g.M, g.N, f32);
+    const int bn = (!f32 && code == 1256) ? 256 : 128;
+    const int num_n = (g.N + bn - 1) / bn;
+    g.n_fastest = double(num_n) * bn * g.K * (f32 ? 4.0 : 2.0) < 48e6;
     if (f32) return launch_cfg<GemmCfg<EPI_DGRAD, 128, true, kEpiWarps, false, false, true>>(a, b, c0, &pre, g, s);
+    if (bn == 256)
+      return launch_cfg<GemmCfg<EPI_DGRAD, 256, false, kEpiWarps, false, false, true, true>>(a, b, c0, &pre, g, s);
     return launch_cfg<GemmCfg<EPI_DGRAD, 128, false, kEpiWarps, false, false, true>>(a, b, c0, &pre, g, s);
   }
   return dispatch<EPI_DGRAD>(f32, a, b, c0, nullptr, g, s, p.force_bn);

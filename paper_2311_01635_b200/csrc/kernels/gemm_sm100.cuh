@@ -98,8 +98,12 @@ struct GemmCfg {
   static constexpr int PRE_CHUNKS = BN / 32 / (EPI_WARPS / 4);
   static constexpr int PRE_WARP = PRE_TMA ? PRE_CHUNKS * 32 * 32 * ELEM : 0;
   static constexpr int PRE_BYTES = EPI_WARPS * PRE_WARP;
+  // FWD: each warp's bias slice for a tile (fp32), fetched before the
+  // accumulator wait so the loads overlap the tile's MMAs.
+  static constexpr int BIAS_WARP = EPI == EPI_FWD ? PRE_CHUNKS * 32 * 4 : 0;
+  static constexpr int BIAS_BYTES = EPI_WARPS * BIAS_WARP;
   static constexpr int SMEM_LIMIT = 232448;     // 227 KB opt-in per block
-  static constexpr int RESERVE = 1024 /*align*/ + 512 /*barriers*/ + STG_BYTES + PRE_BYTES;
+  static constexpr int RESERVE = 1024 /*align*/ + 512 /*barriers*/ + STG_BYTES + PRE_BYTES + BIAS_BYTES;
   static constexpr int STAGES_RAW = (SMEM_LIMIT - RESERVE) / STAGE_BYTES;
   static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
   static constexpr int THREADS = 64 + 32 * EPI_WARPS;
@@ -241,7 +245,8 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
   uint8_t* stage_base = smem;
   uint8_t* stg_base = smem + STAGES * Cfg::STAGE_BYTES;  // 1024-aligned (stage bytes are multiples of 1 KB)
   uint8_t* pre_base = stg_base + Cfg::STG_BYTES;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(pre_base + Cfg::PRE_BYTES);
+  float* bias_base = reinterpret_cast<float*>(pre_base + Cfg::PRE_BYTES);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(pre_base + Cfg::PRE_BYTES + Cfg::BIAS_BYTES);
   uint64_t* full_bar = bars;                    // [STAGES]
   uint64_t* empty_bar = bars + STAGES;          // [STAGES]
   uint64_t* tfull_bar = bars + 2 * STAGES;      // [2]
@@ -496,6 +501,24 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
           }
         }
       }
+      float* bias_w = bias_base + ew * (Cfg::BIAS_WARP / 4);
+      if constexpr (Cfg::EPI == EPI_FWD) {
+        __syncwarp();  // every lane finished reading the previous tile's bias
+        // lane i fetches column i of each of this warp's chunks (previous tile's
+        // readers are done: the warp synchronised before releasing TMEM)
+        for (int k = 0; k < Cfg::PRE_CHUNKS; ++k) {
+          const int col = n0 + (half + k * NSPLIT) * 32 + lane;
+          float bv = 0.f;
+          if (col < args.N) {
+            if constexpr (F32)
+              bv = static_cast<const float*>(args.aux)[col];
+            else
+              bv = __bfloat162float(static_cast<const __nv_bfloat16*>(args.aux)[col]);
+          }
+          bias_w[k * 32 + lane] = bv;
+        }
+        __syncwarp();
+      }
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
       if constexpr (Cfg::EPI == EPI_WGRAD) {
@@ -535,17 +558,14 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
           __syncwarp();
         }
         if constexpr (Cfg::EPI == EPI_FWD) {
+          const float4* bsm = reinterpret_cast<const float4*>(bias_w + ((ch - half) / NSPLIT) * 32);
 #pragma unroll
-          for (int g = 0; g < 4; ++g) {
-            float bias[8];
-            if (nc + g * 8 < args.N) {
-              detail::load8<F32>(args.aux, nc + g * 8, bias);
-            } else {
-#pragma unroll
-              for (int e = 0; e < 8; ++e) bias[e] = 0.f;
-            }
-#pragma unroll
-            for (int e = 0; e < 8; ++e) x[g * 8 + e] += bias[e];
+          for (int g = 0; g < 8; ++g) {  // broadcast smem reads
+            const float4 b4 = bsm[g];
+            x[4 * g] += b4.x;
+            x[4 * g + 1] += b4.y;
+            x[4 * g + 2] += b4.z;
+            x[4 * g + 3] += b4.w;
           }
           if (args.flags & EF_STORE_PRE) detail::stage_row<F32>(stg0, lane, x);
           if (args.flags & EF_GELU) {
