@@ -70,6 +70,8 @@ __global__ void colsum_kernel(const void* __restrict__ dy, size_t ldy, int M, in
                               const float* __restrict__ g_in, float* __restrict__ g_out) {
   __shared__ float red[32][65];
   __shared__ bool is_last;
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // PDL: predecessor's dY complete
+  asm volatile("griddepcontrol.launch_dependents;" :::);
   const int cg = threadIdx.x & 7, rl = threadIdx.x >> 3;
   const int c0 = blockIdx.x * 64 + cg * 8;
   const int r_begin = blockIdx.y * rows_per_split;
@@ -235,11 +237,21 @@ int colsum_bias_grad(bool f32, const void* dy, size_t ldy, size_t M, size_t per,
   unsigned* tickets = static_cast<unsigned*>(ws);
   float* partial = reinterpret_cast<float*>(static_cast<char*>(ws) +
                                             ((col_blocks * sizeof(unsigned) + 255) & ~size_t(255)));
-  if (f32)
-    colsum_kernel<true><<<grid, 256, 0, s>>>(dy, ldy, int(M), int(per), rows_per_split, partial, tickets, g_in, g_out);
-  else
-    colsum_kernel<false><<<grid, 256, 0, s>>>(dy, ldy, int(M), int(per), rows_per_split, partial, tickets, g_in,
-                                              g_out);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(256);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  const int Mi = int(M), peri = int(per);
+  cudaError_t e = f32 ? cudaLaunchKernelEx(&cfg, colsum_kernel<true>, dy, ldy, Mi, peri, rows_per_split, partial,
+                                           tickets, g_in, g_out)
+                      : cudaLaunchKernelEx(&cfg, colsum_kernel<false>, dy, ldy, Mi, peri, rows_per_split, partial,
+                                           tickets, g_in, g_out);
+  if (e != cudaSuccess) return set_cuda_error(e, "colsum_kernel launch");
   return post_launch("colsum_kernel");
 }
 

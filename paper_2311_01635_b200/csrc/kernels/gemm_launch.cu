@@ -116,28 +116,30 @@ int launch_cfg(const Op& a, const Op& b, const Out& c0, const Out* c1, const Gem
   }
   const int tiles = ((args.M + Cfg::TILE_M - 1) / Cfg::TILE_M) * ((args.N + Cfg::BN - 1) / Cfg::BN) *
                     (args.k_splits > 1 ? args.k_splits : 1);  // work units
-  cudaError_t e;
+  // Persistent grid: one CTA pair (cluster of 2 on a TPC) per 256-row tile
+  // slot, or one CTA per SM. Programmatic stream serialization lets the
+  // kernel's prologue run under the previous kernel's tail (griddep_wait()
+  // guards every global access).
+  cudaLaunchConfig_t cfg{};
+  cfg.blockDim = dim3(Cfg::THREADS);
+  cfg.dynamicSmemBytes = Cfg::SMEM_BYTES;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
   if constexpr (Cfg::PAIR) {
-    // one CTA pair (cluster of 2 on a TPC) per 256-row tile slot, persistent
-    const int pairs = std::min(tiles, sm_count() / 2);
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(unsigned(2 * pairs));
-    cfg.blockDim = dim3(Cfg::THREADS);
-    cfg.dynamicSmemBytes = Cfg::SMEM_BYTES;
-    cfg.stream = stream;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = 2;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    e = cudaLaunchKernelEx(&cfg, rtp_gemm_kernel<Cfg>, maps, args);
+    cfg.gridDim = dim3(unsigned(2 * std::min(tiles, sm_count() / 2)));
+    attr[1].id = cudaLaunchAttributeClusterDimension;
+    attr[1].val.clusterDim.x = 2;
+    attr[1].val.clusterDim.y = 1;
+    attr[1].val.clusterDim.z = 1;
+    cfg.numAttrs = 2;
   } else {
-    const int grid = tiles < sm_count() ? tiles : sm_count();
-    rtp_gemm_kernel<Cfg><<<grid, Cfg::THREADS, Cfg::SMEM_BYTES, stream>>>(maps, args);
-    e = cudaGetLastError();
+    cfg.gridDim = dim3(unsigned(std::min(tiles, sm_count())));
   }
+  cudaError_t e = cudaLaunchKernelEx(&cfg, rtp_gemm_kernel<Cfg>, maps, args);
   if (e != cudaSuccess) return set_cuda_error(e, "rtp_gemm_kernel launch");
   count_launch();
   return RTPB_OK;

@@ -80,6 +80,13 @@ __device__ __forceinline__ void tma_load_2d(void* smem_dst, const void* tmap, ui
       : "memory");
 }
 
+// ---------------- programmatic dependent launch ----------------
+// Block until the preceding grid in the stream has completed and its memory
+// is visible (no-op when launched without programmatic serialization).
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// Allow the next grid in the stream to be scheduled (its pre-wait prologue).
+__device__ __forceinline__ void griddep_launch() { asm volatile("griddepcontrol.launch_dependents;" :::); }
+
 // ---------------- clusters (CTA pairs) ----------------
 __device__ __forceinline__ uint32_t cluster_ctarank() {
   uint32_t r;

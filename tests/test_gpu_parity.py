@@ -137,6 +137,36 @@ def test_mlp_eight_workers_vs_oracle(oracle, mode):
         assert nerr(out["grads2"][r], ref["grads2"][r]) < 2e-2
 
 
+@pytest.mark.parametrize("mode", ["inplace", "outofplace"])
+def test_eval_forward_rehomes_and_records_no_tape(golden, mode):
+    """Mode::Eval: N-1 hops plus one re-homing hop (layers_common.cpp:179-181),
+    same outputs as Train, nothing recorded for backward."""
+    import torch
+    from helpers import to_dev, to_np
+    from paper_2311_01635_b200 import rtp
+    g = golden("linear")
+    n = 4
+    grp = rtp.WorkerGroup(n)
+    i_dim, o_dim = g["w"].shape
+    lin = rtp.RtpLinear(grp, "lin", i_dim, o_dim, "bf16", weight=g["w"], bias=g["b"])
+    lin.set_rotation_mode(mode)
+    if mode == "outofplace":
+        lin.allocate_comm_spares()
+    M = g["x"].shape[0] // n
+    xs = [to_dev(g["x"][r * M:(r + 1) * M], "bf16") for r in range(n)]
+    ys = lin.forward(xs, mode="eval")
+    y = np.concatenate([to_np(t) for t in ys])
+    assert nerr(y, g["n4_oop0_y"]) < 2e-2
+    assert [lin.slot(r)["logical_id"] for r in range(n)] == list(range(n))
+    assert [lin.slot(r)["rotation_offset"] for r in range(n)] == [n] * n
+    assert len(grp.traffic()) == n  # N-1 forward hops + 1 re-homing hop
+    dys = [torch.zeros(M, o_dim, dtype=torch.bfloat16, device="cuda") for _ in range(n)]
+    with pytest.raises(rtp.StateError):
+        lin.backward(dys)
+    lin.close()
+    grp.close()
+
+
 # ---------------------------------------------------------------- errors
 def test_error_taxonomy():
     from paper_2311_01635_b200 import rtp
