@@ -95,7 +95,9 @@ int rtpb_dgrad_step(int dtype, const void* dy, size_t ldy, size_t col0, const vo
  * (layers_linear.cpp:61-63, kern::matmul_tn_acc + bias column sums):
  *   g_out[0 : I*per]      = g_in[0 : I*per] + X^T . dY[:, col0:col0+per]
  *   g_out[I*per : +per]   = g_in[I*per : +per] + colsum(dY[:, col0:col0+per])
- * g_in may equal g_out (in-place accumulation). */
+ * g_in may equal g_out (in-place accumulation), or be NULL when the gradient
+ * is known to be zero (the reference's zero_grads): then g_out = X^T . dY
+ * (+ colsum) is written without reading anything. */
 int rtpb_wgrad_step(int dtype, const void* x, size_t ldx, const void* dy, size_t ldy, size_t col0,
                     const float* g_in, float* g_out, size_t M, size_t I, size_t per, void* workspace,
                     size_t workspace_bytes, void* stream);

@@ -246,7 +246,12 @@ class RtpLayerBase {
   size_t flat_grad_bytes() const { return shard_len_ * n() * sizeof(float); }
   DType dtype() const { return dtype_; }
 
+  // zero_grads (layers_common.cpp:120-122) is lazy: the next backward's first
+  // dW step overwrites the resident gradient instead of accumulating into it
+  // (no memset). materialize_grads() performs the zero fill for readers that
+  // look at grad_acc before that backward.
   virtual void zero_grads();
+  void materialize_grads();
   bool all_home() const;
   void allocate_comm_spares();
   void release_comm_spares();
@@ -274,6 +279,7 @@ class RtpLayerBase {
   size_t shard_len_ = 0;
   RotationMode rotation_mode_ = RotationMode::InPlace;
   std::vector<int64_t> trace_;
+  bool grads_zero_pending_ = false;
 };
 
 // Linear layer sharded on output features (layers_linear.cpp:6-72).

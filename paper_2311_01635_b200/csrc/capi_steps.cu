@@ -203,7 +203,7 @@ int rtpb_wgrad_step(int dtype, const void* x, size_t ldx, const void* dy, size_t
                     size_t workspace_bytes, void* stream) {
   int rc = check_geom(M, I, per);
   if (rc) return rc;
-  if (!g_in || !g_out) return set_error(RTPB_ERR_DIMENSION, "wgrad_step: null gradient shard");
+  if (!g_out) return set_error(RTPB_ERR_DIMENSION, "wgrad_step: null gradient shard");
   const bool f32 = dtype == RTPB_F32;
   const size_t esz = f32 ? 4 : 2;
   cudaStream_t s = as_stream(stream);
@@ -224,8 +224,8 @@ int rtpb_wgrad_step(int dtype, const void* x, size_t ldx, const void* dy, size_t
   }
   if (!c.ok) return set_error(RTPB_ERR_DIMENSION, "wgrad_step: workspace too small");
   // Bias part first (reads dY only), then the GEMM with the fused G_in + P epilogue.
-  if ((rc = colsum_bias_grad(f32, static_cast<const char*>(dy) + col0 * esz, ldy, M, per, g_in + I * per,
-                             g_out + I * per, part, s)))
+  if ((rc = colsum_bias_grad(f32, static_cast<const char*>(dy) + col0 * esz, ldy, M, per,
+                             g_in ? g_in + I * per : nullptr, g_out + I * per, part, s)))
     return rc;
   return timed(2, 2.0 * M * I * per, s, [&] { return gemm_wgrad(f32, p, s); });
 }

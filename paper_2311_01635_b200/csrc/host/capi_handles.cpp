@@ -320,6 +320,10 @@ int rtpb_linear_read_shard(rtpb_linear l, size_t rank, int which, void* dst) {
     Worker& w = G.worker(rank);
     DeviceGuard dg(w.device);
     G.synchronize();
+    if (which) {
+      l->l->materialize_grads();
+      G.synchronize();
+    }
     const DeviceBuffer& b = which ? l->l->slots()[rank].grad_acc : l->l->slots()[rank].weight;
     cuda_check(cudaMemcpy(dst, b.data(), b.bytes(), cudaMemcpyDeviceToDevice), "read_shard");
   });

@@ -40,12 +40,16 @@ void RtpLayerBase::init_slots_alloc() {
   });
 }
 
-void RtpLayerBase::zero_grads() {
+void RtpLayerBase::zero_grads() { grads_zero_pending_ = true; }
+
+void RtpLayerBase::materialize_grads() {
+  if (!grads_zero_pending_) return;
   group_->each([&](size_t r) {
     Worker& w = group_->worker(r);
     cuda_check(cudaMemsetAsync(slots_[r].grad_acc.data(), 0, slots_[r].grad_acc.bytes(), w.compute),
                "zero_grads");
   });
+  grads_zero_pending_ = false;
 }
 
 bool RtpLayerBase::all_home() const {
@@ -104,6 +108,7 @@ void RtpLayerBase::rotate_forward() {
 }
 
 void RtpLayerBase::rotate_backward() {
+  materialize_grads();  // gradients travel: make a pending zero fill real first
   if (oop())
     group_->rotate_outofplace(slots_, spares_, Direction::CounterClockwise, PayloadKind::WeightAndGrad, label_,
                               shard_len_);
@@ -337,9 +342,11 @@ void RtpLinear::backward_ex(std::span<const DView> dy, size_t rows, std::span<co
       const size_t k = k_of[r];
       const size_t j = slots_[r].logical_id;
       float* g = static_cast<float*>(slots_[r].grad_acc.data());
+      // step 0 after zero_grads(): every resident gradient is zero -> overwrite
+      const float* g_in = (grads_zero_pending_ && s == 0) ? nullptr : g;
       check_status(rtpb_wgrad_step(dt, x_cache_[r].data, x_cache_[r].ld ? x_cache_[r].ld : in_, dy[k].data,
-                                   dy[k].ld ? dy[k].ld : out_, j * per_, g, g, rows, in_, per_, workspace_[r].data(),
-                                   workspace_[r].bytes(), w.compute));
+                                   dy[k].ld ? dy[k].ld : out_, j * per_, g_in, g, rows, in_, per_,
+                                   workspace_[r].data(), workspace_[r].bytes(), w.compute));
     });
     if (!rotate) break;
     group_->comm_after_compute();
@@ -350,6 +357,7 @@ void RtpLinear::backward_ex(std::span<const DView> dy, size_t rows, std::span<co
       for (size_t r : local) swap_data(slots_[r].weight, spares_[r]);
     group_->advance_slots(slots_, Direction::CounterClockwise, PayloadKind::WeightAndGrad, label_, shard_len_);
   }
+  grads_zero_pending_ = false;
   for (size_t r : local) x_cache_[r] = {};
   require_home("end of backward");
 }

@@ -116,7 +116,7 @@ __global__ void colsum_kernel(const void* __restrict__ dy, size_t ldy, int M, in
     if (c < per) {
       float acc = 0.f;
       for (int sp = 0; sp < int(gridDim.y); ++sp) acc += __ldcg(&partial[size_t(sp) * per + c]);
-      g_out[c] = g_in[c] + acc;
+      g_out[c] = (g_in ? g_in[c] : 0.f) + acc;  // g_in == nullptr: gradient known zero
     }
     if (threadIdx.x == 0) tickets[blockIdx.x] = 0u;  // leave the workspace reusable
   }

@@ -290,7 +290,9 @@ int gemm_wgrad(bool f32, const StepWgrad& p, cudaStream_t s) {
   g.N = int(p.per);
   g.K = int(p.M);
   // G_out = G_in + P: the epilogue reduce-adds into G_out, so seed it with G_in.
-  if (p.g_out != p.g_in) {
+  // G_in == nullptr: G is known zero, the first split stores instead.
+  g.flags = p.g_in ? 0 : EF_FIRST;
+  if (p.g_in && p.g_out != p.g_in) {
     cudaError_t e = cudaMemcpyAsync(p.g_out, p.g_in, p.I * p.per * sizeof(float), cudaMemcpyDeviceToDevice, s);
     if (e != cudaSuccess) return set_cuda_error(e, "wgrad: seed G_out");
   }

@@ -652,7 +652,10 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
             else
               tma_reduce_add_2d(&maps.c0, stg0, nc, row0);  // acc += partial, in L2
           } else {
-            tma_reduce_add_2d(&maps.c0, stg0, nc, row0);  // travelling G += dW tile
+            if (first && split == 0)
+              tma_store_2d(&maps.c0, stg0, nc, row0);  // G known zero: G = dW tile (split 0 lands first)
+            else
+              tma_reduce_add_2d(&maps.c0, stg0, nc, row0);  // travelling G += dW tile
           }
           bulk_commit();
         }

@@ -395,8 +395,9 @@ def wgrad_step(x, dy, col0, g_in, g_out, per, stream=None):
     M, I = x.shape
     ws = _ws(2, dt, M, I, per, x.device)
     s = (stream or torch.cuda.current_stream(x.device)).cuda_stream
-    check(lib.rtpb_wgrad_step(dt, x.data_ptr(), x.stride(0), dy.data_ptr(), dy.stride(0), col0, g_in.data_ptr(),
-                              g_out.data_ptr(), M, I, per, ws.data_ptr(), ws.numel(), s))
+    check(lib.rtpb_wgrad_step(dt, x.data_ptr(), x.stride(0), dy.data_ptr(), dy.stride(0), col0,
+                              None if g_in is None else g_in.data_ptr(), g_out.data_ptr(), M, I, per, ws.data_ptr(),
+                              ws.numel(), s))
 
 
 def flyweight_init(dst, seed, stream_base, I, O, n, j, lo=-0.1, hi=0.1, stream=None):

@@ -89,6 +89,10 @@ def test_step_kernels_vs_torch(M, I, O, n, dt, bn):
             rtp.wgrad_step(X, dY, j * per, G, G2, per)
             assert nerr(G2, refg * 1.5) < TOL[dt]
             assert nerr(G, refg) < TOL[dt]
+            # known-zero gradient (g_in = NULL): G_out = P, nothing read
+            G3 = torch.full_like(G, float("nan"))
+            rtp.wgrad_step(X, dY, j * per, None, G3, per)
+            assert nerr(G3, refg * 0.5) < TOL[dt]
         torch.cuda.synchronize()
     finally:
         _lib.lib.rtpb_debug_force_bn(0)
