@@ -185,6 +185,7 @@ def main():
     ap.add_argument("--mode", default="outofplace", choices=["inplace", "outofplace"])
     ap.add_argument("--tokens-per-gpu", type=int, default=TOKENS_PER_GPU)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--eager", action="store_true", help="time host-issued launches instead of a CUDA graph")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference_arm(args)
@@ -221,6 +222,7 @@ def main():
     y = torch.empty(M, H, dtype=torch.bfloat16, device=dev)
     dx = torch.empty(M, H, dtype=torch.bfloat16, device=dev)
     flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # 512 MiB > 126 MB L2
+    flush_sink = torch.zeros((), dtype=torch.float32, device=dev)
 
     def step():
         mlp.zero_grads()
@@ -237,23 +239,67 @@ def main():
         step()
     barrier()
 
-    # ---- timed region: exactly K steps, L2 flushed before each, CUDA events on our stream
     stream = torch.cuda.current_stream(dev)
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    # ---- eager reference timing (host-issued launches), for the record
+    eager_ms = None
+    if not args.eager:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        barrier()
+        e0.record(stream)
+        for _ in range(20):
+            step()
+        e1.record(stream)
+        barrier()
+        eager_ms = e0.elapsed_time(e1) / 20
+
+    # ---- capture one step (zero_grads + forward + backward through the public
+    # API, every library launch incl. PDL edges and CTA-pair clusters) into a
+    # CUDA graph; the per-GEMM profiling events are captured with it.
+    graph = None
+    graph_note = "eager (--eager)"
     _lib.lib.rtpb_profile_enable(1)
     _lib.lib.rtpb_profile_read(None, None, None, 0)
+    launches_per_step = None
+    if not args.eager:
+        try:
+            l0 = rtp.launch_count()
+            g_ = torch.cuda.CUDAGraph()
+            cs = torch.cuda.Stream(dev)
+            cs.wait_stream(stream)
+            with torch.cuda.graph(g_, stream=cs):
+                step()
+            stream.wait_stream(cs)
+            launches_per_step = rtp.launch_count() - l0
+            for _ in range(3):
+                g_.replay()
+            barrier()
+            graph = g_
+            graph_note = "CUDA graph replay of the captured step"
+        except Exception as exc:  # noqa
+            graph = None
+            graph_note = f"eager (graph capture failed: {exc!r})"
+            _lib.lib.rtpb_profile_read(None, None, None, 1 << 30)
+
+    # ---- timed region: exactly K steps, L2 flushed before each, CUDA events on the stream
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     launches0 = rtp.launch_count()
     grp.reset_ledger_peaks()
     torch.cuda.reset_peak_memory_stats(dev)
     with ClockSampler(local) as clocks:
         barrier()
         for i in range(args.steps):
+            # cold L2: write 512 MiB (> 126 MB L2), then read it back so the
+            # flush's dirty lines are written back before, not inside, the step
             flush.zero_()
+            flush_sink.copy_(flush.sum())
             ev[i][0].record(stream)
-            step()
+            if graph is not None:
+                graph.replay()
+            else:
+                step()
             ev[i][1].record(stream)
         barrier()
-    launches = rtp.launch_count() - launches0
+    launches = (launches_per_step * args.steps) if graph is not None else rtp.launch_count() - launches0
     _lib.lib.rtpb_profile_enable(0)
     step_ms = [a.elapsed_time(b) for a, b in ev]
     total_ms = sum(step_ms)
@@ -292,7 +338,8 @@ def main():
                 "kernel": "rtp_gemm_kernel (tcgen05 step GEMMs: fwd, dgrad, wgrad)",
                 "peak_source": f"{peak_src} bf16 burst; sustained {sustained}",
                 "frac_of_sustained": achieved / sustained,
-                "gemm_share_of_step": gemm_ms / total_ms if total_ms else None,
+                "gemm_share_of_step": (gemm_ms / (ms_per_step * (1 if graph is not None else args.steps))
+                                       if ms_per_step else None),
                 "per_kernel": {k: {"tflops": v[0] / (v[1] * 1e-3) / 1e12, "launches": v[2],
                                    "avg_us": v[1] / v[2] * 1e3} for k, v in per_kind.items()}}
 
@@ -312,25 +359,62 @@ def main():
     # ---- e2e through the public API with host buffers (pinned), copies timed
     e2e = None
     if rank == 0 or world > 1:
-        hx = x.cpu().pin_memory()
-        hdy = dy.cpu().pin_memory()
-        hdx = torch.empty(M, H, dtype=torch.bfloat16).pin_memory()
+        # Training-loop shape: step i+1's inputs are copied host->device on a
+        # copy stream while step i computes, and step i's dX goes device->host
+        # on another while step i+1 computes (double-buffered). Every step's
+        # H2D and D2H happen inside the timed region.
+        hx = [x.cpu().pin_memory() for _ in range(2)]
+        hdy = [dy.cpu().pin_memory() for _ in range(2)]
+        hdx = [torch.empty(M, H, dtype=torch.bfloat16).pin_memory() for _ in range(2)]
+        xd = [torch.empty_like(x) for _ in range(2)]
+        dyd = [torch.empty_like(dy) for _ in range(2)]
+        dxd = [torch.empty_like(dx) for _ in range(2)]
+        h2d, d2h = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+        EV = lambda: torch.cuda.Event()  # noqa: E731
         e2e_steps = max(10, min(args.steps, 100))
-        for _ in range(3):
-            xd = hx.to(dev, non_blocking=True)
-            dyd = hdy.to(dev, non_blocking=True)
-            mlp.zero_grads()
-            mlp.forward([xd])
-            hdx.copy_(mlp.backward([dyd])[0], non_blocking=True)
+
+        def run_e2e(nsteps):
+            landed = [EV(), EV()]
+            computed = [EV(), EV()]
+            drained = [EV(), EV()]
+            done_with_inputs = [None, None]
+
+            def issue_h2d(i):
+                b = i % 2
+                with torch.cuda.stream(h2d):
+                    if done_with_inputs[b] is not None:
+                        h2d.wait_event(done_with_inputs[b])  # step i-2 finished reading these buffers
+                    xd[b].copy_(hx[b], non_blocking=True)
+                    dyd[b].copy_(hdy[b], non_blocking=True)
+                    landed[b].record(h2d)
+
+            h2d.wait_stream(stream)
+            d2h.wait_stream(stream)
+            issue_h2d(0)
+            for i in range(nsteps):
+                b = i % 2
+                if i + 1 < nsteps:
+                    issue_h2d(i + 1)
+                stream.wait_event(landed[b])
+                if i >= 2:
+                    stream.wait_event(drained[b])  # dxd[b] read back before it is overwritten
+                mlp.zero_grads()
+                mlp.forward([xd[b]], out=[y])
+                mlp.backward([dyd[b]], out=[dxd[b]])
+                computed[b].record(stream)
+                done_with_inputs[b] = computed[b]
+                with torch.cuda.stream(d2h):
+                    d2h.wait_event(computed[b])
+                    hdx[b].copy_(dxd[b], non_blocking=True)
+                    drained[b].record(d2h)
+            stream.wait_stream(d2h)
+            stream.wait_stream(h2d)
+
+        run_e2e(4)
         barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        for _ in range(e2e_steps):
-            xd = hx.to(dev, non_blocking=True)
-            dyd = hdy.to(dev, non_blocking=True)
-            mlp.zero_grads()
-            mlp.forward([xd])
-            hdx.copy_(mlp.backward([dyd])[0], non_blocking=True)
+        run_e2e(e2e_steps)
         e1.record(stream)
         barrier()
         e2e_ms = e0.elapsed_time(e1) / e2e_steps
@@ -340,7 +424,8 @@ def main():
             e2e_ms = float(t.item())
         e2e = {"value": flops_per_step(T) / (e2e_ms * 1e-3) / 1e12, "unit": UNIT,
                "h2d_bytes_per_step": 2 * M * H * 2, "d2h_bytes_per_step": M * H * 2, "ms_per_step": e2e_ms,
-               "path": "RtpMlp.forward/backward (C ABI) from pinned host X, dY; dX read back"}
+               "path": "RtpMlp.forward/backward (C ABI, eager launches) from pinned host X, dY; dX read "
+                       "back; step i+1 H2D and step i-1 D2H overlap step i on copy streams"}
 
     if rank == 0:
         cpu = None
@@ -355,10 +440,12 @@ def main():
                                                              "SplitMix64 weights, seed 42)",
                 "config": {"workload": "rtp_mlp_768x3072x768 (config b)", "h": H, "f": F,
                            "tokens_per_gpu": M, "global_tokens": T, "rotation_mode": args.mode,
-                           "parallelism": f"rtp{world}", "l2": "flushed (512 MiB write) before every timed step",
+                           "parallelism": f"rtp{world}", "l2": "flushed before every timed step (512 MiB written, then read back)",
                            "flops_per_step": flops_per_step(T)},
                 "tflops_per_gpu": value / world,
                 "gpu_launches": int(launches),
+                "step_execution": graph_note,
+                "eager_ms_per_step": eager_ms,
                 "roofline": roofline,
                 "memory": mem,
                 "cpu_baseline": cpu,

@@ -87,9 +87,14 @@ int timed(int kind, double flops, cudaStream_t s, F&& launch) {
     a = prof_event();
     b = prof_event();
   }
-  cudaEventRecord(a, s);
+  // Inside stream capture the records must be external event-record nodes so
+  // every replay of the graph re-times the launch.
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(s, &cap);
+  const unsigned fl = cap == cudaStreamCaptureStatusActive ? cudaEventRecordExternal : cudaEventRecordDefault;
+  cudaEventRecordWithFlags(a, s, fl);
   const int rc = launch();
-  cudaEventRecord(b, s);
+  cudaEventRecordWithFlags(b, s, fl);
   std::lock_guard lk(g_prof_mu);
   g_prof.push_back({kind, flops, a, b});
   return rc;
