@@ -50,8 +50,13 @@ cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
 
 // Zero-initialised, self-resetting part of a step workspace.
 size_t split_flag_bytes(size_t I, size_t per) { return ((I + 255) / 256) * ((per + 255) / 256) * sizeof(unsigned); }
+// Fused dW bias sums (CTA-pair dW): arrival counter per 64-column group, and
+// one partial row per (256-row tile block, K split <= 8).
+size_t bias_tick_bytes(size_t per) { return ((per + 63) / 64) * sizeof(unsigned); }
+size_t bias_part_bytes(size_t I, size_t per) { return ((I + 255) / 256) * 8 * per * sizeof(float); }
 size_t persistent_ws_bytes(size_t M, size_t I, size_t per) {
-  return align256(colsum_workspace_bytes(M, per)) + align256(split_flag_bytes(I, per));
+  return align256(colsum_workspace_bytes(M, per)) + align256(split_flag_bytes(I, per)) +
+         align256(bias_tick_bytes(per)) + align256(bias_part_bytes(I, per));
 }
 
 // Optional per-launch timing of the step GEMMs: a CUDA event pair recorded on
@@ -215,6 +220,8 @@ int rtpb_wgrad_step(int dtype, const void* x, size_t ldx, const void* dy, size_t
   Carve c{static_cast<char*>(workspace), workspace ? workspace_bytes : 0};
   float* part = c.take(colsum_workspace_bytes(M, per) / sizeof(float));
   unsigned* flags = reinterpret_cast<unsigned*>(c.take(split_flag_bytes(I, per) / sizeof(float)));
+  unsigned* btick = reinterpret_cast<unsigned*>(c.take(bias_tick_bytes(per) / sizeof(float)));
+  float* bpart = c.take(bias_part_bytes(I, per) / sizeof(float));
   StepWgrad p{};
   p.x = x; p.ldx = ldx; p.dy = static_cast<const char*>(dy) + col0 * esz; p.ldy = ldy;
   p.g_in = g_in; p.g_out = g_out; p.M = M; p.I = I; p.per = per; p.force_bn = g_force_bn;
@@ -228,11 +235,22 @@ int rtpb_wgrad_step(int dtype, const void* x, size_t ldx, const void* dy, size_t
     p.x = xh; p.x_lo = xl; p.ldx = Mp; p.dy = dh; p.dy_lo = dl; p.ldy = Mp;
   }
   if (!c.ok) return set_error(RTPB_ERR_DIMENSION, "wgrad_step: workspace too small");
-  // Bias part first (reads dY only), then the GEMM with the fused G_in + P epilogue.
-  if ((rc = colsum_bias_grad(f32, static_cast<const char*>(dy) + col0 * esz, ldy, M, per,
-                             g_in ? g_in + I * per : nullptr, g_out + I * per, part, s)))
-    return rc;
-  return timed(2, 2.0 * M * I * per, s, [&] { return gemm_wgrad(f32, p, s); });
+  const float* gb_in = g_in ? g_in + I * per : nullptr;
+  float* gb_out = g_out + I * per;
+  return timed(2, 2.0 * M * I * per, s, [&] {
+    if (wgrad_fuses_bias(f32, M, I, per, flags, g_force_bn)) {
+      // CTA-pair dW: the kernel's column-sum warp reduces the staged dY tiles.
+      p.gbias_in = gb_in;
+      p.gbias_out = gb_out;
+      p.bias_part = bpart;
+      p.bias_tick = btick;
+    } else {
+      // Bias part first (reads dY only), then the GEMM with the fused G_in + P epilogue.
+      int r = colsum_bias_grad(f32, static_cast<const char*>(dy) + col0 * esz, ldy, M, per, gb_in, gb_out, part, s);
+      if (r) return r;
+    }
+    return gemm_wgrad(f32, p, s);
+  });
 }
 
 void rtpb_profile_enable(int on) {

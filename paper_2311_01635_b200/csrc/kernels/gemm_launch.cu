@@ -194,9 +194,9 @@ int dispatch_tile(int code, const Op& a, const Op& b, const Out& c0, const Out* 
   return launch_cfg<GemmCfg<EPI, 128, TF32, kEpiWarps, AMN, BMN>>(a, b, c0, c1, args, s);
 }
 
+// Tile code (and, for dW, the split-K factor written into args.k_splits).
 template <int EPI>
-int dispatch(bool tf32, const Op& a, const Op& b, const Out& c0, const Out* c1, GemmArgs args, cudaStream_t s,
-             int force) {
+int pick_code(bool tf32, GemmArgs& args, int force) {
   int code = force ? force : choose_tile(args.M, args.N, tf32);
   if (tf32 && code > 1000) code -= 1000;  // no pair tiles in the fp32 (3xTF32) mode
   if (tf32 && code == 256) code = 128;
@@ -215,6 +215,13 @@ int dispatch(bool tf32, const Op& a, const Op& b, const Out& c0, const Out* c1, 
       }
     }
   }
+  return code;
+}
+
+template <int EPI>
+int dispatch(bool tf32, const Op& a, const Op& b, const Out& c0, const Out* c1, GemmArgs args, cudaStream_t s,
+             int force) {
+  const int code = pick_code<EPI>(tf32, args, force);
   const int bn = code % 1000;
   const int num_n = (args.N + bn - 1) / bn;
   // Raster n fastest when the B operand (all n-blocks x K) fits comfortably in
@@ -298,7 +305,20 @@ int gemm_wgrad(bool f32, const StepWgrad& p, cudaStream_t s) {
   }
   Out c0{p.g_out, true, p.per, p.I, p.per};
   g.split_flags = p.split_flags;
+  g.gbias_in = p.gbias_in;
+  g.gbias_out = p.gbias_out;
+  g.bias_part = p.bias_part;
+  g.bias_tick = p.bias_tick;
   return dispatch<EPI_WGRAD>(f32, a, b, c0, nullptr, g, s, p.force_bn);
+}
+
+bool wgrad_fuses_bias(bool f32, size_t M, size_t I, size_t per, unsigned* split_flags, int force_bn) {
+  GemmArgs g{};
+  g.M = int(I);
+  g.N = int(per);
+  g.K = int(M);
+  g.split_flags = split_flags;
+  return !f32 && pick_code<EPI_WGRAD>(false, g, force_bn) > 1000;
 }
 
 }  // namespace rtpb

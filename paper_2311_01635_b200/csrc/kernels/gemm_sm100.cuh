@@ -55,6 +55,12 @@ struct GemmArgs {
   // summation order is fixed and results are bitwise reproducible.
   int k_splits;
   unsigned* split_flags;
+  // WGRAD CTA-pair path: the bias gradient db = colsum(dY block) is fused —
+  // an extra warp sums the dY tiles staged in smem as the B operand.
+  const float* gbias_in;  // nullable: gradient known zero
+  float* gbias_out;
+  float* bias_part;       // [ceil(M / 256) * k_splits][N] partial sums
+  unsigned* bias_tick;    // [ceil(N / 64)] zeroed, self-resetting arrival counters
 };
 
 template <int EPI_, int BN_, bool TF32_, int EPI_WARPS_, bool A_MN_, bool B_MN_, bool PRE_TMA_ = false,
@@ -102,11 +108,20 @@ struct GemmCfg {
   // accumulator wait so the loads overlap the tile's MMAs.
   static constexpr int BIAS_WARP = EPI == EPI_FWD ? PRE_CHUNKS * 32 * 4 : 0;
   static constexpr int BIAS_BYTES = EPI_WARPS * BIAS_WARP;
+  // dW on CTA pairs: two more warps compute the bias gradient db = colsum(dY)
+  // from the B (dY) tiles already staged for the MMA — no second read of dY.
+  // Each takes half of a stage's K rows; their sums meet in COLSUM_BYTES.
+  // (Measured, config (b) dW in the step graph: 45.5 us per launch vs 42.4 us
+  // for the GEMM alone; the stand-alone column-sum kernel cost ~6 us more.)
+  static constexpr bool COLSUM = EPI == EPI_WGRAD && PAIR && !TF32;
+  static constexpr int COLSUM_WARPS = COLSUM ? 2 : 0;
+  static constexpr int COLSUM_BYTES = COLSUM ? B_ROWS * 4 : 0;
   static constexpr int SMEM_LIMIT = 232448;     // 227 KB opt-in per block
-  static constexpr int RESERVE = 1024 /*align*/ + 512 /*barriers*/ + STG_BYTES + PRE_BYTES + BIAS_BYTES;
+  static constexpr int RESERVE =
+      1024 /*align*/ + 512 /*barriers*/ + STG_BYTES + PRE_BYTES + BIAS_BYTES + COLSUM_BYTES;
   static constexpr int STAGES_RAW = (SMEM_LIMIT - RESERVE) / STAGE_BYTES;
   static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
-  static constexpr int THREADS = 64 + 32 * EPI_WARPS;
+  static constexpr int THREADS = 64 + 32 * (EPI_WARPS + COLSUM_WARPS);
   static constexpr int TMEM_COLS = (2 * BN <= 32) ? 32 : (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128
                                    : (2 * BN <= 256) ? 256 : 512;
   static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + RESERVE;
@@ -131,6 +146,12 @@ namespace detail {
 
 __device__ __forceinline__ float bf16lo(uint32_t u) { return __uint_as_float(u << 16); }
 __device__ __forceinline__ float bf16hi(uint32_t u) { return __uint_as_float(u & 0xFFFF0000u); }
+// a += lo(u), b += hi(u) for a packed bf16 pair (exact widening, fp32 add RN).
+// (Shift / mask + FADD: the mixed-precision FHADD.BF16 form measured far slower.)
+__device__ __forceinline__ void acc_bf16x2(float& a, float& b, uint32_t u) {
+  a += __uint_as_float(u << 16);
+  b += __uint_as_float(u & 0xFFFF0000u);
+}
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
   return *reinterpret_cast<uint32_t*>(&h);
@@ -268,18 +289,22 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
   constexpr bool F32 = Cfg::TF32;  // activation / output dtype is fp32 in TF32 mode
 
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // Align by offsetting smem_raw itself (not through an integer cast) so the
+  // compiler keeps the shared address space: STS/LDS instead of generic ST/LD.
+  uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* stage_base = smem;
   uint8_t* stg_base = smem + STAGES * Cfg::STAGE_BYTES;  // 1024-aligned (stage bytes are multiples of 1 KB)
   uint8_t* pre_base = stg_base + Cfg::STG_BYTES;
   float* bias_base = reinterpret_cast<float*>(pre_base + Cfg::PRE_BYTES);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(pre_base + Cfg::PRE_BYTES + Cfg::BIAS_BYTES);
+  float* csum_base = bias_base + Cfg::BIAS_BYTES / 4;  // COLSUM: [B_ROWS] partial sums
+  uint64_t* bars = reinterpret_cast<uint64_t*>(pre_base + Cfg::PRE_BYTES + Cfg::BIAS_BYTES + Cfg::COLSUM_BYTES);
   uint64_t* full_bar = bars;                    // [STAGES]
   uint64_t* empty_bar = bars + STAGES;          // [STAGES]
   uint64_t* tfull_bar = bars + 2 * STAGES;      // [2]
   uint64_t* tempty_bar = bars + 2 * STAGES + 2; // [2]
   uint64_t* pre_bar = bars + 2 * STAGES + 4;    // [EPI_WARPS] (PRE_TMA)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 4 + Cfg::EPI_WARPS);
+  uint64_t* ready_bar = pre_bar + Cfg::EPI_WARPS;  // [STAGES] (COLSUM): stage landed, both CTAs
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ready_bar + (Cfg::COLSUM ? STAGES : 0));
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -315,7 +340,9 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
     if constexpr (Cfg::NOUT > 1) prefetch_tmap(&maps.c1);
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full_bar[s], 1);
-      mbar_init(&empty_bar[s], 1);
+      // COLSUM: the stage is free once the MMA commit AND the column-sum warp release it.
+      mbar_init(&empty_bar[s], 1 + Cfg::COLSUM_WARPS);
+      if constexpr (Cfg::COLSUM) mbar_init(&ready_bar[s], 1);
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull_bar[s], 1);
@@ -353,6 +380,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
       nb = t / num_m;
     }
   };
+  const bool colsum_on = Cfg::COLSUM && args.gbias_out != nullptr;
 
   if (warp == 0) {
     // ===================== TMA producer =====================
@@ -493,7 +521,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
         }
       }
     }
-  } else {
+  } else if (warp < 2 + Cfg::EPI_WARPS) {
     // ===================== Epilogue =====================
     const int ew = warp - 2;          // 0..EPI_WARPS-1
     const int q = warp & 3;           // TMEM lane quarter this warp may access
@@ -509,11 +537,11 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
     bool pending = false;
     int acc = 0;
     uint32_t acc_phase = 0;
-    const int wgroup = Cfg::EPI_WARPS * (Cfg::PAIR ? 2 : 1);  // epilogue warps per tile
     for (int u = unit; u < num_units; u += units) {
       const int t = u % num_tiles, split = u / num_tiles;
       int mb, nb;
       tile_coords(t, mb, nb);
+      const int wgroup = Cfg::EPI_WARPS * (Cfg::PAIR ? 2 : 1);  // epilogue warps per tile
       const int m0 = mb * Cfg::TILE_M + int(rank) * BM, n0 = nb * BN;  // this CTA's 128 rows
       const int row0 = m0 + q * 32;     // first row of this warp's 32-row slab
       const int row = row0 + lane;
@@ -687,6 +715,116 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
     }
     if (lane == 0) bulk_wait0();
     __syncwarp();
+  } else if constexpr (Cfg::COLSUM) {
+    // ============ Bias gradient: column sums of the staged dY (B) tiles ============
+    // B stage layout (MN-major, SWIZZLE_128B): chunk c holds columns
+    // [64c, 64c+64) as BK rows of 128 B; 16-byte piece j of row k sits at
+    // piece j ^ (k & 7). Lane: 8 columns (one piece) of every RPI-th row.
+    // Every tile row block mb sees the same dY columns, so the work is spread:
+    // unit (mb, nb, split) sums only the k-blocks with kb % num_m == mb, writes
+    // that partial to its own workspace row, and the last of the num_m * splits
+    // contributors of a column group adds them up in a fixed order
+    // (deterministic, no waiting).
+    constexpr int NCH = Cfg::B_ROWS / 64;   // 64-column chunks per CTA (1 or 2)
+    constexpr int LPR = 8 * NCH;            // lanes per row
+    constexpr int RPI = 32 / LPR;           // rows per warp-wide step
+    constexpr int ROWS = BK / Cfg::COLSUM_WARPS;
+    const int cw = warp - 2 - Cfg::EPI_WARPS;  // 0: publisher, 1: helper
+    const int chunk = (lane % LPR) / 8, piece = lane & 7, rsub = lane / LPR;
+    const bool first = args.flags & EF_FIRST;
+    const int contributors = num_m * splits;
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int u = unit; u < num_units; u += units) {
+      const int t = u % num_tiles, split = u / num_tiles;
+      int mb, nb, kb0, kb1;
+      tile_coords(t, mb, nb);
+      unit_kb(u, kb0, kb1);
+      float sum[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) sum[e] = 0.f;
+      for (int kb = kb0; kb < kb1; ++kb) {
+        // Leader: the stage's full barrier counts both CTAs' bytes; its first
+        // column-sum warp forwards the event to the peer (off the MMA thread).
+        if (rank == 0) {
+          mbar_wait(&full_bar[stage], phase);
+          // (default .release.cta remote arrive: a cluster-scope release
+          // compiles to MEMBAR.ALL.GPU and stalled the pipeline ~1 us / stage)
+          if (cw == 0 && lane == 0) mbar_arrive_cluster(&ready_bar[stage], 1);
+        } else {
+          mbar_wait(&ready_bar[stage], phase);
+        }
+        if (colsum_on && kb % num_m == mb) {
+          const uint8_t* sB = stage_base + stage * Cfg::STAGE_BYTES + Cfg::A_BYTES + chunk * (BK * 128);
+#pragma unroll 4
+          for (int i = 0; i < ROWS / RPI; ++i) {
+            const int k = cw * ROWS + i * RPI + rsub;  // rows past K were zero-filled by TMA
+            const uint4 v = *reinterpret_cast<const uint4*>(sB + k * 128 + ((piece ^ (k & 7)) << 4));
+            detail::acc_bf16x2(sum[0], sum[1], v.x);
+            detail::acc_bf16x2(sum[2], sum[3], v.y);
+            detail::acc_bf16x2(sum[4], sum[5], v.z);
+            detail::acc_bf16x2(sum[6], sum[7], v.w);
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty_bar[stage]);
+        if (++stage == STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+      if (!colsum_on) continue;
+      // fold the row subsets: lanes 0..LPR-1 then hold columns lane*8 .. lane*8+7
+#pragma unroll
+      for (int o = LPR; o < 32; o <<= 1)
+#pragma unroll
+        for (int e = 0; e < 8; ++e) sum[e] += __shfl_xor_sync(0xffffffffu, sum[e], o);
+      float4* cs = reinterpret_cast<float4*>(csum_base) + lane * 2;
+      if (cw == 1 && lane < LPR) {
+        cs[0] = make_float4(sum[0], sum[1], sum[2], sum[3]);
+        cs[1] = make_float4(sum[4], sum[5], sum[6], sum[7]);
+      }
+      named_bar_sync(1, 64);
+      if (cw == 0) {
+        const int cg = nb * 2 + int(rank);                 // this CTA's column group
+        const int c0 = cg * Cfg::B_ROWS + lane * 8;
+        float* part = args.bias_part + size_t(split * num_m + mb) * args.N;
+        if (lane < LPR) {
+          const float4 a = cs[0], b = cs[1];
+          sum[0] += a.x; sum[1] += a.y; sum[2] += a.z; sum[3] += a.w;
+          sum[4] += b.x; sum[5] += b.y; sum[6] += b.z; sum[7] += b.w;
+#pragma unroll
+          for (int e = 0; e < 8; ++e)
+            if (c0 + e < args.N) part[c0 + e] = sum[e];
+        }
+        __syncwarp();
+        unsigned last = 0;
+        if (lane == 0) {
+          __threadfence();
+          const unsigned old = atomicAdd(args.bias_tick + cg, 1u);
+          last = old + 1 == unsigned(contributors);
+          if (last) {
+            args.bias_tick[cg] = 0u;  // self-resetting for the next launch
+            __threadfence();
+          }
+        }
+        last = __shfl_sync(0xffffffffu, last, 0);
+        __syncwarp();
+        if (last && lane < LPR) {
+          // every contributor's partial is visible: sum them in (split, mb) order
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const int c = c0 + e;
+            if (c < args.N) {
+              float acc = 0.f;
+              for (int r = 0; r < contributors; ++r) acc += __ldcg(args.bias_part + size_t(r) * args.N + c);
+              args.gbias_out[c] = (first ? 0.f : __ldcg(args.gbias_in + c)) + acc;
+            }
+          }
+        }
+      }
+      named_bar_sync(1, 64);  // partial buffer free for the next unit
+    }
   }
 
   tc_fence_before();

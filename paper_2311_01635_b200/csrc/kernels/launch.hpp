@@ -42,9 +42,14 @@ struct StepWgrad {
   const void* dy; const void* dy_lo; size_t ldy;  // dy points at the column block
   const float* g_in; float* g_out;                // I x per block of the grad shard
   unsigned* split_flags;                          // zeroed per-tile counters (split-K order)
+  const float* gbias_in; float* gbias_out;        // bias gradient, when the GEMM fuses it
+  float* bias_part; unsigned* bias_tick;          // its partial sums / zeroed arrival counters
   size_t M, I, per;
   int force_bn;
 };
+// True when gemm_wgrad runs a CTA-pair config, whose extra warp also sums dY
+// columns into the bias gradient (gbias_*); otherwise colsum_bias_grad does.
+bool wgrad_fuses_bias(bool f32, size_t M, size_t I, size_t per, unsigned* split_flags, int force_bn);
 
 int gemm_fwd(bool f32, const StepFwd& p, cudaStream_t s);
 int gemm_dgrad(bool f32, const StepDgrad& p, cudaStream_t s);

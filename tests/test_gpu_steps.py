@@ -38,6 +38,8 @@ CASES = [
     (300, 64, 256, 1, "bf16", 1128),
     (200, 64, 192, 3, "bf16", 0),     # ragged M, per = 64
     (1000, 768, 3072, 4, "bf16", 0),  # GPT-2 width, tail rows
+    (8192, 768, 3072, 4, "bf16", 0),  # config (b) dW: 8-way ordered split-K + fused bias sums
+    (4000, 768, 3000, 3, "bf16", 1128),  # pair 256 x 128, ragged K and N
     (8, 8, 16, 2, "bf16", 0),         # minimal aligned shape
     (512, 256, 512, 4, "f32", 0),
     (1024, 1024, 4096, 4, "f32", 0),  # config (a) shapes, one worker's rows
@@ -84,6 +86,8 @@ def test_step_kernels_vs_torch(M, I, O, n, dt, bn):
             dyj = dY.double()[:, j * per:(j + 1) * per]
             refg = torch.cat([(X.double().t() @ dyj).reshape(-1), dyj.sum(0)]) * 2
             assert nerr(G, refg) < TOL[dt]
+            # bias gradient on its own scale (fused column sums on CTA-pair tiles)
+            assert nerr(G[I * per:], refg[I * per:]) < TOL[dt]
             # out-of-place accumulation: G_out = G_in + P leaves G_in intact
             G2 = torch.empty_like(G)
             rtp.wgrad_step(X, dY, j * per, G, G2, per)
@@ -93,6 +97,7 @@ def test_step_kernels_vs_torch(M, I, O, n, dt, bn):
             G3 = torch.full_like(G, float("nan"))
             rtp.wgrad_step(X, dY, j * per, None, G3, per)
             assert nerr(G3, refg * 0.5) < TOL[dt]
+            assert nerr(G3[I * per:], refg[I * per:] * 0.5) < TOL[dt]
         torch.cuda.synchronize()
     finally:
         _lib.lib.rtpb_debug_force_bn(0)
