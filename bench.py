@@ -318,6 +318,9 @@ def main():
     ms = (C.c_float * cnt)()
     _lib.lib.rtpb_profile_read(kinds, fl, ms, cnt)
     per_kind = {}
+    per_launch = [{"kind": {0: "fwd", 1: "dgrad", 2: "wgrad"}[k], "us": round(m_ * 1e3, 2),
+                   "tflops": round(f_ / (m_ * 1e-3) / 1e12, 1) if m_ else None}
+                  for k, f_, m_ in list(zip(kinds, fl, ms))[:12]]
     for k, f_, m_ in zip(kinds, fl, ms):
         d = per_kind.setdefault({0: "fwd", 1: "dgrad", 2: "wgrad"}[k], [0.0, 0.0, 0])
         d[0] += f_
@@ -341,7 +344,8 @@ def main():
                 "gemm_share_of_step": (gemm_ms / (ms_per_step * (1 if graph is not None else args.steps))
                                        if ms_per_step else None),
                 "per_kernel": {k: {"tflops": v[0] / (v[1] * 1e-3) / 1e12, "launches": v[2],
-                                   "avg_us": v[1] / v[2] * 1e3} for k, v in per_kind.items()}}
+                                   "avg_us": v[1] / v[2] * 1e3} for k, v in per_kind.items()},
+                "per_launch_in_step_order": per_launch}
 
     # ---- memory: device ledger (params, grads, comm, activations, workspace) + caller tensors
     led = grp.ledger(rank)

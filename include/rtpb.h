@@ -121,6 +121,10 @@ size_t rtpb_profile_read(int* kinds, double* flops, float* ms, size_t cap);
 
 /* Test hook: force the GEMM tile width (0 = heuristic; 64/128/256). */
 void rtpb_debug_force_bn(int bn);
+/* Debug hook: the following step-GEMM launches write per-CTA %globaltimer
+ * stamps (80 u64 per CTA, layout in gemm_sm100.cuh GemmArgs::trace) into
+ * consecutive blocks of this device buffer until it is full; NULL disables. */
+void rtpb_debug_trace(void* device_buf, size_t bytes);
 
 /* Ring schedule of an RtpLinear pass, pure host logic shared by every
  * transport: the logical shard id `rank` holds at (phase, step) — forward

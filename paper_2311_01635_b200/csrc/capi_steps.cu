@@ -130,6 +130,7 @@ const char* rtpb_last_error(void) { return g_last_error.c_str(); }
 const char* rtpb_version(void) { return "rtpb 0.1 (sm_100a tcgen05)"; }
 uint64_t rtpb_launch_count(void) { return g_launches.load(); }
 void rtpb_debug_force_bn(int bn) { g_force_bn = bn; }
+void rtpb_debug_trace(void* device_buf, size_t bytes) { set_trace(device_buf, bytes); }
 
 // Workspace layout, identical for every step kind of a layer so one buffer
 // serves all three: [bias-grad tickets + partials][dW split-K tile counters]

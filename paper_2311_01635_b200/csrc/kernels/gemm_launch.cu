@@ -62,6 +62,20 @@ int encode_out(CUtensorMap* m, const void* ptr, bool f32, uint64_t cols, uint64_
                    f32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B);
 }
 
+// Debug timeline buffer (rtpb_debug_trace): each launch takes the next
+// gridDim x TRACE_STRIDE block of u64 stamps while space is left.
+unsigned long long* g_trace = nullptr;
+size_t g_trace_cap = 0, g_trace_next = 0;
+
+unsigned long long* next_trace(unsigned grid) {
+  if (!g_trace) return nullptr;
+  const size_t need = size_t(grid) * TRACE_STRIDE;
+  if (g_trace_next + need > g_trace_cap) return nullptr;
+  unsigned long long* p = g_trace + g_trace_next;
+  g_trace_next += need;
+  return p;
+}
+
 int sm_count() {
   static int n = 0;
   if (!n) {
@@ -139,7 +153,9 @@ int launch_cfg(const Op& a, const Op& b, const Out& c0, const Out* c1, const Gem
   } else {
     cfg.gridDim = dim3(unsigned(std::min(tiles, sm_count())));
   }
-  cudaError_t e = cudaLaunchKernelEx(&cfg, rtp_gemm_kernel<Cfg>, maps, args);
+  GemmArgs a_ = args;
+  a_.trace = next_trace(cfg.gridDim.x);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, rtp_gemm_kernel<Cfg>, maps, a_);
   if (e != cudaSuccess) return set_cuda_error(e, "rtp_gemm_kernel launch");
   count_launch();
   return RTPB_OK;
@@ -233,6 +249,12 @@ int dispatch(bool tf32, const Op& a, const Op& b, const Out& c0, const Out* c1, 
 }
 
 }  // namespace
+
+void set_trace(void* buf, size_t bytes) {
+  g_trace = static_cast<unsigned long long*>(buf);
+  g_trace_cap = buf ? bytes / sizeof(unsigned long long) : 0;
+  g_trace_next = 0;
+}
 
 int gemm_fwd(bool f32, const StepFwd& p, cudaStream_t s) {
   // C[M x per] = X[M x I] . W_j[I x per]; A K-major, B MN-major.

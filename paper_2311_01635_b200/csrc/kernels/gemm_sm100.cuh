@@ -61,7 +61,15 @@ struct GemmArgs {
   float* gbias_out;
   float* bias_part;       // [ceil(M / 256) * k_splits][N] partial sums
   unsigned* bias_tick;    // [ceil(N / 64)] zeroed, self-resetting arrival counters
+  // Debug timeline (nullable; rtpb_debug_trace): per CTA TRACE_STRIDE u64 of
+  // %globaltimer stamps: [0] entry, [1] after griddep_wait, then per local
+  // work unit i < TRACE_UNITS at 2 + 6 i: MMA starts waiting for a free
+  // accumulator, accumulator free, first stage landed, last MMA committed,
+  // epilogue sees the accumulator, epilogue released it; last slot = gridDim.x.
+  unsigned long long* trace;
 };
+constexpr int TRACE_UNITS = 13;
+constexpr int TRACE_STRIDE = 80;
 
 template <int EPI_, int BN_, bool TF32_, int EPI_WARPS_, bool A_MN_, bool B_MN_, bool PRE_TMA_ = false,
           bool PAIR_ = false>
@@ -143,6 +151,15 @@ struct GemmMaps {
 // (DGRAD + PRE_TMA: c1 is the load map of pre, same 32 x 32 boxes as c0.)
 
 namespace detail {
+
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void trace_at(unsigned long long* tr, int slot) {
+  if (tr) tr[blockIdx.x * TRACE_STRIDE + slot] = gtime();
+}
 
 __device__ __forceinline__ float bf16lo(uint32_t u) { return __uint_as_float(u << 16); }
 __device__ __forceinline__ float bf16hi(uint32_t u) { return __uint_as_float(u & 0xFFFF0000u); }
@@ -365,11 +382,17 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
     __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  unsigned long long* const trace = args.trace;
+  if (threadIdx.x == 0) {
+    detail::trace_at(trace, 0);
+    if (trace) trace[blockIdx.x * TRACE_STRIDE + TRACE_STRIDE - 1] = gridDim.x;  // lets readers walk the launches
+  }
   // PDL: everything above (barrier init, TMEM alloc, descriptor prefetch)
   // overlapped the previous kernel's tail; global data is touched only after
   // it has completed. Then let the next kernel's prologue start.
   griddep_wait();
   griddep_launch();
+  if (threadIdx.x == 0) detail::trace_at(trace, 1);
 
   auto tile_coords = [&](int t, int& mb, int& nb) {
     if (args.n_fastest) {
@@ -466,15 +489,20 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int u = unit; u < num_units; u += units) {
+      int li = 0;
+      for (int u = unit; u < num_units; u += units, ++li) {
         int kb0, kb1;
         unit_kb(u, kb0, kb1);
+        const bool tr = trace && li < TRACE_UNITS;
+        if (tr) detail::trace_at(trace, 2 + 6 * li);
         mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
         tc_fence_after();
+        if (tr) detail::trace_at(trace, 3 + 6 * li);
         const uint32_t d_tmem = tmem_base + acc * BN;
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full_bar[stage], phase);
           tc_fence_after();
+          if (tr && kb == kb0) detail::trace_at(trace, 4 + 6 * li);
           const uint32_t a_base = smem_u32(stage_base + stage * Cfg::STAGE_BYTES);
           const uint32_t b_base = a_base + Cfg::A_BYTES;
 #pragma unroll
@@ -515,6 +543,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
           umma_commit_pair(&tfull_bar[acc]);
         else
           umma_commit(&tfull_bar[acc]);
+        if (tr) detail::trace_at(trace, 5 + 6 * li);
         if (++acc == 2) {
           acc = 0;
           acc_phase ^= 1;
@@ -537,7 +566,9 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
     bool pending = false;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int u = unit; u < num_units; u += units) {
+    int li = 0;
+    for (int u = unit; u < num_units; u += units, ++li) {
+      const bool tr = trace && li < TRACE_UNITS && ew == 0 && lane == 0;
       const int t = u % num_tiles, split = u / num_tiles;
       int mb, nb;
       tile_coords(t, mb, nb);
@@ -581,6 +612,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
       }
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
+      if (tr) detail::trace_at(trace, 6 + 6 * li);
       if constexpr (Cfg::EPI == EPI_WGRAD) {
         if (split > 0) {
           // ordered split-K: wait until every warp of split-1 has landed its sums
@@ -703,6 +735,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
         }
       }
       if constexpr (Cfg::PRE_TMA) __syncwarp();  // all lanes done with the pre chunks
+      if (tr) detail::trace_at(trace, 7 + 6 * li);
       tc_fence_before();
       if constexpr (Cfg::PAIR)
         mbar_arrive_cluster(&tempty_bar[acc], 0);  // the leader's MMA reuses both halves

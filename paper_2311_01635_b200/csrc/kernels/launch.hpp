@@ -52,6 +52,8 @@ struct StepWgrad {
 bool wgrad_fuses_bias(bool f32, size_t M, size_t I, size_t per, unsigned* split_flags, int force_bn);
 
 int gemm_fwd(bool f32, const StepFwd& p, cudaStream_t s);
+// Debug: route per-CTA timeline stamps of the following GEMM launches into buf.
+void set_trace(void* buf, size_t bytes);
 int gemm_dgrad(bool f32, const StepDgrad& p, cudaStream_t s);
 int gemm_wgrad(bool f32, const StepWgrad& p, cudaStream_t s);
 

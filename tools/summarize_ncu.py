@@ -64,8 +64,8 @@ try:
         return None, None
 
     lines.append("## Full capture (`ncu --set full`, step GEMMs)\n")
-    lines.append("| kernel | grid | time us | tensor pipe % | DRAM read MB | DRAM write MB | issue % | regs |")
-    lines.append("|---|---|---:|---:|---:|---:|---:|---:|")
+    lines.append("| kernel | grid | time us | tensor pipe % | L2 % | SM MHz | DRAM read MB | DRAM write MB | issue % | regs |")
+    lines.append("|---|---|---:|---:|---:|---:|---:|---:|---:|---:|")
     for r in rows[2:]:
         name = short(r[idx["Kernel Name"]])
         t, _ = g(r, "gpu__time_duration.sum")
@@ -74,6 +74,8 @@ try:
         dw, dwu = g(r, "dram__bytes_write.sum")
         iss, _ = g(r, "sm__inst_issued.avg.pct_of_peak_sustained_active")
         regs, _ = g(r, "launch__registers_per_thread")
+        l2, _ = g(r, "lts__throughput.avg.pct_of_peak_sustained_elapsed")
+        clk, clku = g(r, "sm__cycles_elapsed.avg.per_second")
         grid, _ = g(r, "Grid Size")
 
         def mb(v, u):
@@ -84,9 +86,11 @@ try:
             return v * {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3}.get(u, 1.0)
         rec = {"kernel": name, "grid": grid, "time_us": float(t) if t else None,
                "tensor_pipe_pct": float(tp) if tp else None, "dram_read_MB": mb(dr, dru),
-               "dram_write_MB": mb(dw, dwu), "issue_pct": float(iss) if iss else None, "regs": regs}
+               "dram_write_MB": mb(dw, dwu), "issue_pct": float(iss) if iss else None, "regs": regs,
+               "l2_pct": float(l2) if l2 else None,
+               "sm_mhz": (float(clk) * {"Ghz": 1e3, "hz": 1e-6, "Khz": 1e-3, "Mhz": 1.0}.get(clku, 1.0)) if clk else None}
         summary["kernels"].append(rec)
-        lines.append(f"| `{name[:70]}` | {grid} | {rec['time_us']:.1f} | {rec['tensor_pipe_pct'] or 0:.1f} | "
+        lines.append(f"| `{name[:70]}` | {grid} | {rec['time_us']:.1f} | {rec['tensor_pipe_pct'] or 0:.1f} | {rec['l2_pct'] or 0:.1f} | {rec['sm_mhz'] or 0:.0f} | "
                      f"{rec['dram_read_MB'] or 0:.1f} | {rec['dram_write_MB'] or 0:.1f} | {rec['issue_pct'] or 0:.1f} "
                      f"| {regs} |")
 except (FileNotFoundError, IndexError):
