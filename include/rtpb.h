@@ -126,6 +126,12 @@ void rtpb_debug_force_bn(int bn);
  * consecutive blocks of this device buffer until it is full; NULL disables. */
 void rtpb_debug_trace(void* device_buf, size_t bytes);
 
+/* Measurement hook: while on, every ring shift of every group keeps its
+ * schedule, events and bookkeeping but moves no bytes — the compute-only
+ * baseline from which bench.py derives the exposed rotation time. Results
+ * are wrong while it is on. */
+void rtpb_debug_skip_comm(int on);
+
 /* Ring schedule of an RtpLinear pass, pure host logic shared by every
  * transport: the logical shard id `rank` holds at (phase, step) — forward
  * (phase 0) (rank - step) mod n, backward (phase 1) (rank + 1 + step) mod n
@@ -186,7 +192,10 @@ int rtpb_group_ledger(rtpb_group g, size_t rank, size_t* current5, size_t* peak5
 int rtpb_group_reset_ledger_peaks(rtpb_group g);
 /* Ring primitive on raw device slots (test / micro-bench entry, ring.cpp:265-333):
  * weight[r], grad[r]: device buffers of `w_bytes` / `g_bytes` for local rank r.
- * op: 0 cw(W), 1 ccw(W+G), 2 cw(W+G), 3 ccw(W); spare != NULL -> out-of-place W. */
+ * op: 0 cw(W), 1 ccw(W+G), 2 cw(W+G), 3 ccw(W); spare != NULL -> out-of-place W
+ * (received into spare[r], then copied back into weight[r] unless op has
+ * RTPB_ROTATE_KEEP_SPARE, in which case the caller swaps the two roles). */
+#define RTPB_ROTATE_KEEP_SPARE 8
 int rtpb_group_rotate(rtpb_group g, int op, void** weight, void** grad, void** spare, size_t w_bytes,
                       size_t g_bytes);
 /* ring_allgather (ring.cpp:335-376) of `bytes` per rank into out (n*bytes). */

@@ -31,6 +31,7 @@ _SIGS = {
     "rtpb_launch_count": (_u64, []),
     "rtpb_debug_force_bn": (None, [_int]),
     "rtpb_debug_trace": (None, [_vp, _sz]),
+    "rtpb_debug_skip_comm": (None, [_int]),
     "rtpb_profile_enable": (None, [_int]),
     "rtpb_profile_read": (_sz, [C.POINTER(_int), C.POINTER(_dbl), C.POINTER(C.c_float), _sz]),
     "rtpb_step_workspace_bytes": (_sz, [_int, _int, _sz, _sz, _sz]),

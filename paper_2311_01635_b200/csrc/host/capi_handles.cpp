@@ -2,12 +2,17 @@
 // include/rtpb/rtp.hpp. Exceptions become status codes + rtpb_last_error().
 #include <nccl.h>
 
+#include <atomic>
 #include <cstring>
 
 #include "kernels/launch.hpp"
 #include "worker.hpp"
 
 using namespace rtpb;
+
+namespace rtpb {
+extern std::atomic<int> g_skip_comm;  // rtp_group.cpp
+}
 
 // Layers keep their group alive: the WorkerGroup (worker streams, ledgers)
 // is destroyed only after its last layer, whatever order FFI callers free in.
@@ -197,6 +202,9 @@ int rtpb_group_rotate(rtpb_group g, int op, void** weight, void** grad, void** s
       gr[local[k]] = grad ? grad[k] : nullptr;
       sp[local[k]] = spare ? spare[k] : nullptr;
     }
+    const bool keep_spare = op & RTPB_ROTATE_KEEP_SPARE;
+    op &= ~RTPB_ROTATE_KEEP_SPARE;
+    if (op < 0 || op > 3) throw ConfigError("rotate: op must be 0..3 (optionally | RTPB_ROTATE_KEEP_SPARE)");
     const Direction dir = (op == 0 || op == 2) ? Direction::Clockwise : Direction::CounterClockwise;
     const bool with_grad = op == 1 || op == 2;
     if (n == 1) return;
@@ -204,7 +212,7 @@ int rtpb_group_rotate(rtpb_group g, int op, void** weight, void** grad, void** s
     G.exchange(dir, w, spare ? sp : w, w_bytes);
     if (with_grad) G.exchange(dir, gr, gr, g_bytes);
     G.compute_after_comm();
-    if (spare) {
+    if (spare && !keep_spare) {
       // out-of-place: the received weight is in the spare; copy it home so
       // the caller's pointers keep their roles (raw-buffer test entry).
       for (size_t r : local) {
@@ -215,6 +223,8 @@ int rtpb_group_rotate(rtpb_group g, int op, void** weight, void** grad, void** s
     }
   });
 }
+
+void rtpb_debug_skip_comm(int on) { g_skip_comm.store(on ? 1 : 0); }
 
 int rtpb_group_allgather(rtpb_group g, void** in, void** out, size_t bytes) {
   return guard([&] {

@@ -4,6 +4,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <condition_variable>
 #include <cstring>
@@ -451,8 +452,13 @@ MemoryLedger& WorkerGroup::ledger_of(size_t rank) { return worker(rank).ledger; 
 
 void WorkerGroup::each(const std::function<void(size_t)>& fn) { transport_->each(fn); }
 
+std::atomic<int> g_skip_comm{0};
+
 void WorkerGroup::exchange(Direction dir, std::span<void* const> send, std::span<void* const> recv, size_t bytes) {
   if (send.size() != n_ || recv.size() != n_) throw ConfigError("exchange: buffer arrays must have n entries");
+  // rtpb_debug_skip_comm: the schedule, events and bookkeeping stay; only the
+  // bytes do not move (compute-only baseline for the exposed-comm measurement).
+  if (g_skip_comm.load(std::memory_order_relaxed)) return;
   transport_->shift(dir, send, recv, bytes);
 }
 

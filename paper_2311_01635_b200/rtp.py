@@ -132,10 +132,11 @@ class WorkerGroup:
             s = self.stream(r)
             torch.cuda.current_stream(s.device).wait_stream(s)
 
-    def rotate(self, op: str, weights, grads=None, spares=None, w_bytes=None, g_bytes=None):
+    def rotate(self, op: str, weights, grads=None, spares=None, w_bytes=None, g_bytes=None, keep_spare=False):
         """Ring primitive on raw per-rank device buffers (ring.cpp:265-333).
-        op: "cw" (W), "ccw" (W+G), "cw_wg", "ccw_w"."""
-        code = {"cw": 0, "ccw": 1, "cw_wg": 2, "ccw_w": 3}[op]
+        op: "cw" (W), "ccw" (W+G), "cw_wg", "ccw_w". With spares (out of
+        place) and keep_spare=True the received shard stays in spares[k]."""
+        code = {"cw": 0, "ccw": 1, "cw_wg": 2, "ccw_w": 3}[op] | (8 if keep_spare else 0)
         self._enter([[w] + ([grads[k]] if grads else []) + ([spares[k]] if spares else [])
                      for k, w in enumerate(weights)])
         wb = w_bytes if w_bytes is not None else weights[0].numel() * weights[0].element_size()
