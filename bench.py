@@ -258,7 +258,7 @@ def main():
     graph = None
     graph_note = "eager (--eager)"
     _lib.lib.rtpb_profile_enable(1)
-    _lib.lib.rtpb_profile_read(None, None, None, 0)
+    _lib.lib.rtpb_profile_read(None, None, None, None, None, 1 << 30)  # drop warm-up records
     launches_per_step = None
     if not args.eager:
         try:
@@ -278,7 +278,7 @@ def main():
         except Exception as exc:  # noqa
             graph = None
             graph_note = f"eager (graph capture failed: {exc!r})"
-            _lib.lib.rtpb_profile_read(None, None, None, 1 << 30)
+            _lib.lib.rtpb_profile_read(None, None, None, None, None, 1 << 30)
 
     # ---- timed region: exactly K steps, L2 flushed before each, CUDA events on the stream
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
@@ -310,26 +310,49 @@ def main():
     ms_per_step = total_ms / args.steps
     value = flops_per_step(T) / (ms_per_step * 1e-3) / 1e12  # whole-job aggregate
 
-    # ---- per-launch GEMM timing (the roofline numerator)
+    # ---- per-launch GEMM timing (the roofline numerator), last timed step
     import ctypes as C
-    cnt = _lib.lib.rtpb_profile_read(None, None, None, 0)
+    cnt = _lib.lib.rtpb_profile_read(None, None, None, None, None, 0)
     kinds = (C.c_int * cnt)()
     fl = (C.c_double * cnt)()
     ms = (C.c_float * cnt)()
-    _lib.lib.rtpb_profile_read(kinds, fl, ms, cnt)
+    st = (C.c_float * cnt)()
+    smc = (C.c_int * cnt)()
+    _lib.lib.rtpb_profile_read(kinds, fl, ms, st, smc, cnt)
+    per_step = cnt if graph is not None else max(1, cnt // args.steps)
+    recs = list(zip(kinds, fl, ms, st, smc))[cnt - per_step:]
+    t_first = min(r[3] for r in recs) if recs else 0.0
+    names = {0: "fwd", 1: "dgrad", 2: "wgrad"}
+    all_sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    per_launch = [{"kind": names[k], "us": round(m_ * 1e3, 2), "start_us": round((t0 - t_first) * 1e3, 2),
+                   "sms": int(sm_), "tflops": round(f_ / (m_ * 1e-3) / 1e12, 1) if m_ else None}
+                  for k, f_, m_, t0, sm_ in recs]
     per_kind = {}
-    per_launch = [{"kind": {0: "fwd", 1: "dgrad", 2: "wgrad"}[k], "us": round(m_ * 1e3, 2),
-                   "tflops": round(f_ / (m_ * 1e-3) / 1e12, 1) if m_ else None}
-                  for k, f_, m_ in list(zip(kinds, fl, ms))[:12]]
-    for k, f_, m_ in zip(kinds, fl, ms):
-        d = per_kind.setdefault({0: "fwd", 1: "dgrad", 2: "wgrad"}[k], [0.0, 0.0, 0])
+    for k, f_, m_, t0, sm_ in recs:
+        d = per_kind.setdefault(names[k], [0.0, 0.0, 0, 0.0])
         d[0] += f_
         d[1] += m_
         d[2] += 1
+        d[3] += m_ * sm_ / all_sms  # GPU-time: duration x share of the SMs the launch was sized for
     gemm_flops = sum(d[0] for d in per_kind.values())
-    gemm_ms = sum(d[1] for d in per_kind.values())
+    gemm_gpu_ms = sum(d[3] for d in per_kind.values())
+    # wall time with at least one step GEMM running (union of launch intervals)
+    iv = sorted((t0, t0 + m_) for _, _, m_, t0, _ in recs)
+    busy, cur_a, cur_b = 0.0, None, None
+    for a_, b_ in iv:
+        if cur_b is None or a_ > cur_b:
+            if cur_b is not None:
+                busy += cur_b - cur_a
+            cur_a, cur_b = a_, b_
+        else:
+            cur_b = max(cur_b, b_)
+    if cur_b is not None:
+        busy += cur_b - cur_a
     burst, sustained, peak_src = load_peaks()
-    achieved = gemm_flops / (gemm_ms * 1e-3) / 1e12 if gemm_ms else 0.0
+    # achieved: algorithmic flops per unit of GPU time the GEMM launches held
+    # (duration x their share of the SMs: two GEMMs side by side on halves of
+    # the machine are each compared with half the peak)
+    achieved = gemm_flops / (gemm_gpu_ms * 1e-3) / 1e12 if gemm_gpu_ms else 0.0
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
@@ -341,9 +364,9 @@ def main():
                 "kernel": "rtp_gemm_kernel (tcgen05 step GEMMs: fwd, dgrad, wgrad)",
                 "peak_source": f"{peak_src} bf16 burst; sustained {sustained}",
                 "frac_of_sustained": achieved / sustained,
-                "gemm_share_of_step": (gemm_ms / (ms_per_step * (1 if graph is not None else args.steps))
-                                       if ms_per_step else None),
-                "per_kernel": {k: {"tflops": v[0] / (v[1] * 1e-3) / 1e12, "launches": v[2],
+                "achieved_over_gemm_wall": gemm_flops / (busy * 1e-3) / 1e12 if busy else None,
+                "gemm_busy_share_of_step": busy / ms_per_step if ms_per_step else None,
+                "per_kernel": {k: {"tflops_per_gpu_time": v[0] / (v[3] * 1e-3) / 1e12, "launches": v[2],
                                    "avg_us": v[1] / v[2] * 1e3} for k, v in per_kind.items()},
                 "per_launch_in_step_order": per_launch}
 
@@ -359,6 +382,42 @@ def main():
            "model_inplace_bytes": (W_total + G_total) // world,
            "model_outofplace_bytes": (W_total + G_total + max(W_total, G_total)) // world,
            "param_grad_comm_bytes": led["peak_param"] + led["peak_grad"] + led["peak_comm"]}
+
+    # ---- exposed rotation time: T(step) - T(step without moving bytes)
+    exposed = {"ms_per_step": 0.0, "frac": 0.0, "method": "N=1: no rotation, nothing to expose"}
+    if world > 1:
+        def eager_ms(k=10):
+            barrier()
+            a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a_.record(stream)
+            for _ in range(k):
+                step()
+            b_.record(stream)
+            barrier()
+            t_ = torch.tensor([a_.elapsed_time(b_) / k], device=dev, dtype=torch.float64)
+            dist.all_reduce(t_, op=dist.ReduceOp.MAX)
+            return float(t_.item())
+        t_with = eager_ms()
+        _lib.lib.rtpb_debug_skip_comm(1)
+        try:
+            step()
+            t_without = eager_ms()
+        finally:
+            _lib.lib.rtpb_debug_skip_comm(0)
+        exposed = {"ms_per_step": max(0.0, t_with - t_without), "frac": max(0.0, t_with - t_without) / t_with,
+                   "ms_step_eager": t_with, "ms_step_compute_only": t_without,
+                   "method": "eager steps with and without rtpb_debug_skip_comm (same schedule, no bytes moved), "
+                             "max over ranks"}
+    nvl_bw = 900e9  # NVLink 5 per direction per GPU
+    w_all = (mlp.ffn1.shard_len() + mlp.ffn2.shard_len()) * world
+    sent = (world - 1) / world * (2 * w_all * 2 + w_all * 4) if world > 1 else 0.0  # bf16 W fwd+bwd, fp32 G bwd
+    t_gemm_peak = flops_per_step(T) / world / (burst * 1e12) * 1e3
+    t_nvl = sent / nvl_bw * 1e3
+    step_roofline = {"gemm_ms_at_peak": t_gemm_peak, "nvlink_ms": t_nvl, "bytes_sent_per_gpu": sent,
+                     "bound": "tensor" if t_gemm_peak >= t_nvl else "nvlink",
+                     "roofline_ms": max(t_gemm_peak, t_nvl), "frac": max(t_gemm_peak, t_nvl) / ms_per_step,
+                     "note": "north_star roofline: slower of the step's GEMM flops at the bf16 peak and its "
+                             "rotation bytes over NVLink (900 GB/s/direction)"}
 
     # ---- e2e through the public API with host buffers (pinned), copies timed
     e2e = None
@@ -451,6 +510,8 @@ def main():
                 "step_execution": graph_note,
                 "eager_ms_per_step": eager_ms,
                 "roofline": roofline,
+                "step_roofline": step_roofline,
+                "exposed_comm": exposed,
                 "memory": mem,
                 "cpu_baseline": cpu,
                 "e2e": e2e,

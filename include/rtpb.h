@@ -114,10 +114,17 @@ int rtpb_gelu_backward(int dtype, const void* x, const void* upstream, void* out
 
 /* Per-launch timing of the step GEMMs: when enabled, a CUDA event pair is
  * recorded on the launching stream around every step GEMM. profile_read
- * returns the record count; with cap > 0 it fills kind (0 fwd, 1 dgrad,
- * 2 wgrad), algorithmic flops and milliseconds, then clears the records. */
+ * returns the record count; with cap > 0 it fills (each array nullable) kind
+ * (0 fwd, 1 dgrad, 2 wgrad), algorithmic flops, duration in ms, start in ms
+ * after the first record's start, and the SMs the launch was sized for, then
+ * clears the records. */
 void rtpb_profile_enable(int on);
-size_t rtpb_profile_read(int* kinds, double* flops, float* ms, size_t cap);
+size_t rtpb_profile_read(int* kinds, double* flops, float* ms, float* start_ms, int* sms, size_t cap);
+
+/* The calling thread's following step-kernel launches occupy at most `sms`
+ * SMs (persistent grid, tile and split-K choice sized for them); 0 = all.
+ * Lets a caller run two step GEMMs side by side on two streams. */
+void rtpb_set_sm_budget(int sms);
 
 /* Test hook: force the GEMM tile width (0 = heuristic; 64/128/256). */
 void rtpb_debug_force_bn(int bn);

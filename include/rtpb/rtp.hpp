@@ -176,6 +176,8 @@ class WorkerGroup {
   void comm_after_compute();
   void compute_after_comm();
   void synchronize();
+  // Orders each local worker's compute stream after its aux stream.
+  void join_aux();
 
   const std::vector<CommRecord>& traffic() const { return traffic_; }
   void clear_traffic() { traffic_.clear(); }

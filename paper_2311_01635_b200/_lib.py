@@ -33,7 +33,9 @@ _SIGS = {
     "rtpb_debug_trace": (None, [_vp, _sz]),
     "rtpb_debug_skip_comm": (None, [_int]),
     "rtpb_profile_enable": (None, [_int]),
-    "rtpb_profile_read": (_sz, [C.POINTER(_int), C.POINTER(_dbl), C.POINTER(C.c_float), _sz]),
+    "rtpb_profile_read": (_sz, [C.POINTER(_int), C.POINTER(_dbl), C.POINTER(C.c_float), C.POINTER(C.c_float),
+                                C.POINTER(_int), _sz]),
+    "rtpb_set_sm_budget": (None, [_int]),
     "rtpb_step_workspace_bytes": (_sz, [_int, _int, _sz, _sz, _sz]),
     "rtpb_flyweight_init": (_int, [_vp, _int, _u64, _u64, _sz, _sz, _sz, _sz, _dbl, _dbl, _vp]),
     "rtpb_fwd_step": (_int, [_int, _vp, _sz, _vp, _vp, _sz, _sz, _vp, _sz, _sz, _sz, _sz, _int, _vp, _sz, _vp]),

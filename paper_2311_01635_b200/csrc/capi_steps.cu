@@ -65,6 +65,7 @@ struct ProfRec {
   int kind;
   double flops;
   cudaEvent_t a, b;
+  int sms;  // SM budget of the launch
 };
 std::mutex g_prof_mu;
 bool g_prof_on = false;
@@ -101,7 +102,7 @@ int timed(int kind, double flops, cudaStream_t s, F&& launch) {
   const int rc = launch();
   cudaEventRecordWithFlags(b, s, fl);
   std::lock_guard lk(g_prof_mu);
-  g_prof.push_back({kind, flops, a, b});
+  g_prof.push_back({kind, flops, a, b, sm_budget()});
   return rc;
 }
 }  // namespace
@@ -130,6 +131,7 @@ const char* rtpb_last_error(void) { return g_last_error.c_str(); }
 const char* rtpb_version(void) { return "rtpb 0.1 (sm_100a tcgen05)"; }
 uint64_t rtpb_launch_count(void) { return g_launches.load(); }
 void rtpb_debug_force_bn(int bn) { g_force_bn = bn; }
+void rtpb_set_sm_budget(int sms) { set_sm_budget(sms); }
 void rtpb_debug_trace(void* device_buf, size_t bytes) { set_trace(device_buf, bytes); }
 
 // Workspace layout, identical for every step kind of a layer so one buffer
@@ -259,18 +261,21 @@ void rtpb_profile_enable(int on) {
   g_prof_on = on != 0;
 }
 
-size_t rtpb_profile_read(int* kinds, double* flops, float* ms, size_t cap) {
+size_t rtpb_profile_read(int* kinds, double* flops, float* ms, float* start_ms, int* sms, size_t cap) {
   std::lock_guard lk(g_prof_mu);
   const size_t n = g_prof.size();
   for (size_t i = 0; i < n; ++i) {
     ProfRec& r = g_prof[i];
     if (i < cap) {
       cudaEventSynchronize(r.b);
-      float t = 0.f;
+      float t = 0.f, t0 = 0.f;
       cudaEventElapsedTime(&t, r.a, r.b);
+      if (i) cudaEventElapsedTime(&t0, g_prof[0].a, r.a);
       if (kinds) kinds[i] = r.kind;
       if (flops) flops[i] = r.flops;
       if (ms) ms[i] = t;
+      if (start_ms) start_ms[i] = t0;
+      if (sms) sms[i] = r.sms;
     }
   }
   if (cap) {  // reading consumes the records

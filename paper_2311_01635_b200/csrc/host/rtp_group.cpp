@@ -140,14 +140,17 @@ Worker::Worker(size_t r, int dev) : rank(r), device(dev) {
   DeviceGuard g(dev);
   cuda_check(cudaStreamCreateWithFlags(&compute, cudaStreamNonBlocking), "stream");
   cuda_check(cudaStreamCreateWithFlags(&comm, cudaStreamNonBlocking), "stream");
+  cuda_check(cudaStreamCreateWithFlags(&aux, cudaStreamNonBlocking), "stream");
   for (auto& e : ev) cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
 }
 Worker::~Worker() {
   DeviceGuard g(device);
   cudaStreamSynchronize(compute);
   cudaStreamSynchronize(comm);
+  cudaStreamSynchronize(aux);
   stage.reset();
   for (auto& e : ev) cudaEventDestroy(e);
+  cudaStreamDestroy(aux);
   cudaStreamDestroy(compute);
   cudaStreamDestroy(comm);
 }
@@ -480,10 +483,19 @@ void WorkerGroup::compute_after_comm() {
   }
 }
 
+void WorkerGroup::join_aux() {
+  for (size_t r : local_) {
+    Worker& w = *workers_[r];
+    DeviceGuard dg(w.device);
+    w.join_aux();
+  }
+}
+
 void WorkerGroup::synchronize() {
   for (size_t r : local_) {
     Worker& w = *workers_[r];
     DeviceGuard dg(w.device);
+    cuda_check(cudaStreamSynchronize(w.aux), "sync aux");
     cuda_check(cudaStreamSynchronize(w.compute), "sync compute");
     cuda_check(cudaStreamSynchronize(w.comm), "sync comm");
   }

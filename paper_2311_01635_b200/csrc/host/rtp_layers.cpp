@@ -13,14 +13,47 @@
 // the next dW waits only for it. In-place mode: the weight shift follows dX
 // (overlapping dW), the gradient shift follows dW (overlapping the next dX);
 // forward shifts are exposed, as the paper accepts.
+#include <cmath>
+#include <cstdlib>
 #include <cstring>
 
+#include "kernels/launch.hpp"
 #include "worker.hpp"
 
 namespace rtpb {
 
 namespace {
 int dtype_code(DType d) { return d == DType::F32 ? RTPB_F32 : RTPB_BF16; }
+
+// SMs for dX when dX and dW of one step run side by side (N = 1): the split
+// minimising the slower of the two under a wave-quantised cost model of the
+// CTA-pair kernels (256 x 256 tiles, ~0.35 us per 64-deep K block per pair
+// when TMA-fed from L2, plus a per-tile epilogue / prologue share; dW splits
+// K over idle pairs and pays an ordered reduction per split).
+// RTPB_OVERLAP_DX_SMS overrides it (measurement).
+int overlap_dx_sms(size_t M, size_t I, size_t per, bool gelu_bwd) {
+  if (const char* e = std::getenv("RTPB_OVERLAP_DX_SMS")) return std::atoi(e);
+  const int sms = sm_budget();
+  auto cdiv = [](double a, double b) { return std::ceil(a / b); };
+  const double kd = cdiv(double(per), 64), kw = cdiv(double(M), 64);
+  const double tiles_d = cdiv(double(M), 256) * cdiv(double(I), 256);
+  const double tiles_w = cdiv(double(I), 256) * cdiv(double(per), 256);
+  const double ck = 0.35, ck_d = gelu_bwd ? 0.45 : 0.35;
+  double best = 1e30;
+  int best_sms = sms / 2;
+  for (int d = 16; d <= sms - 16; d += 2) {
+    const double pd = d / 2, pw = (sms - d) / 2;
+    const double t_d = cdiv(tiles_d, pd) * (kd * ck_d + 0.8) + 2.0;
+    const double split = std::max(1.0, std::min(8.0, std::floor(pw / tiles_w)));
+    const double t_w = cdiv(tiles_w * split, pw) * (kw / split * ck + 0.8) + 2.5 * split;
+    const double t = std::max(t_d, t_w);
+    if (t < best) {
+      best = t;
+      best_sms = d;
+    }
+  }
+  return best_sms;
+}
 }  // namespace
 
 // ------------------------------------------------------------------ base
@@ -201,6 +234,7 @@ void RtpLinear::forward(std::span<const DView> x, size_t rows, std::span<const D
 
 void RtpLinear::backward(std::span<const DView> dy, size_t rows, std::span<const DView> dx) {
   backward_ex(dy, rows, dx, BwdEpi{});
+  group_->join_aux();
 }
 
 void RtpLinear::forward_ex(std::span<const DView> x, size_t rows, std::span<const DView> y, Mode mode,
@@ -285,6 +319,48 @@ void RtpLinear::backward_ex(std::span<const DView> dy, size_t rows, std::span<co
   const int dt = dtype_code(dtype_);
   const bool oopm = oop();
   std::vector<void*> wp(n, nullptr), sp(n, nullptr), gp(n, nullptr);
+
+  if (n == 1 && dtype_ == DType::BF16 && !std::getenv("RTPB_NO_OVERLAP")) {
+    // No rotation: dX and dW of the single step are independent GEMMs. dW
+    // runs on the aux stream beside dX, each persistent kernel sized to its
+    // share of the SMs, so neither pays a wave-quantisation tail alone.
+    // (bf16 only: the fp32 mode's operand-split pre-passes share the layer
+    // workspace.) The caller joins aux back into compute.
+    const size_t r = local[0];
+    Worker& w = group_->worker(r);
+    const size_t j = slots_[r].logical_id;
+    tapes_[r].replay(j);
+    check_backward_position(r, 0);
+    trace_[n * n] = int64_t(j);
+    const bool gelu = !e.pre.empty();
+    const int all = sm_budget();
+    const int d_sms = overlap_dx_sms(rows, in_, per_, gelu);
+    w.fork_aux();  // aux: dY (and, for ffn1, dpre) are complete
+    set_sm_budget(d_sms);
+    int flags = RTPB_EPI_FIRST | RTPB_EPI_LAST;
+    const void* pre = nullptr;
+    size_t ldpre = 0;
+    if (gelu) {
+      flags |= RTPB_EPI_GELU_BWD;
+      pre = e.pre[0].data;
+      ldpre = e.pre[0].ld ? e.pre[0].ld : in_;
+    }
+    int rc = rtpb_dgrad_step(dt, dy[0].data, dy[0].ld ? dy[0].ld : out_, 0, slots_[r].weight.data(), nullptr, in_,
+                             dx[0].data, dx[0].ld ? dx[0].ld : in_, pre, ldpre, rows, in_, per_, flags,
+                             workspace_[r].data(), workspace_[r].bytes(), w.compute);
+    if (rc == RTPB_OK) {
+      set_sm_budget(all - d_sms);
+      float* g = static_cast<float*>(slots_[r].grad_acc.data());
+      rc = rtpb_wgrad_step(dt, x_cache_[r].data, x_cache_[r].ld ? x_cache_[r].ld : in_, dy[0].data,
+                           dy[0].ld ? dy[0].ld : out_, 0, grads_zero_pending_ ? nullptr : g, g, rows, in_, per_,
+                           workspace_[r].data(), workspace_[r].bytes(), w.aux);
+    }
+    set_sm_budget(0);
+    check_status(rc);
+    grads_zero_pending_ = false;
+    x_cache_[r] = {};
+    return;
+  }
 
   for (size_t s = 0; s < n; ++s) {
     group_->each([&](size_t r) {
@@ -437,7 +513,8 @@ void RtpMlp::backward(std::span<const DView> dy, size_t rows, std::span<const DV
   RtpLinear::BwdEpi e2;
   e2.pre = pre;
   ffn2_->backward_ex(dy, rows, pre, e2);
-  ffn1_->backward(pre, rows, dx);  // model.cpp:105
+  ffn1_->backward_ex(pre, rows, dx, RtpLinear::BwdEpi{});  // model.cpp:105
+  group_->join_aux();
 }
 
 }  // namespace rtpb

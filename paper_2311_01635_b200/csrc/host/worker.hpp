@@ -23,7 +23,10 @@ void cuda_check(cudaError_t e, const char* where);
 
 // Stream-ordering markers of one worker. Compute: last enqueued compute
 // work; WDone / GDone: completion of the latest weight / gradient exchange.
-enum class Ev : int { Compute = 0, WDone = 1, GDone = 2, Comm = 3, Ready = 4, Consumed = 5, Staged = 6, kCount = 7 };
+// Fork / Join: compute <-> aux stream hand-offs (N = 1 dX || dW overlap).
+enum class Ev : int {
+  Compute = 0, WDone = 1, GDone = 2, Comm = 3, Ready = 4, Consumed = 5, Staged = 6, Fork = 7, Join = 8, kCount = 9
+};
 
 struct Worker {
   Worker(size_t rank, int device);
@@ -32,6 +35,10 @@ struct Worker {
   int device;
   cudaStream_t compute = nullptr;
   cudaStream_t comm = nullptr;
+  // Second compute stream: with no rotation to wait for (N = 1), dW runs here
+  // beside dX, each GEMM on its share of the SMs (RtpLinear::backward_ex).
+  cudaStream_t aux = nullptr;
+  bool aux_pending = false;  // aux has work compute has not joined yet
   cudaEvent_t ev[int(Ev::kCount)] = {};
   MemoryLedger ledger;
   DeviceBuffer stage;  // in-place rotation staging chunk (CommBuffer)
@@ -39,6 +46,19 @@ struct Worker {
   void record(Ev e, bool on_comm) { cuda_check(cudaEventRecord(ev[int(e)], on_comm ? comm : compute), "record"); }
   void wait(Ev e, bool on_comm) {
     cuda_check(cudaStreamWaitEvent(on_comm ? comm : compute, ev[int(e)], 0), "wait");
+  }
+  // aux waits for everything enqueued on compute so far.
+  void fork_aux() {
+    cuda_check(cudaEventRecord(ev[int(Ev::Fork)], compute), "record fork");
+    cuda_check(cudaStreamWaitEvent(aux, ev[int(Ev::Fork)], 0), "wait fork");
+    aux_pending = true;
+  }
+  // compute waits for everything enqueued on aux so far.
+  void join_aux() {
+    if (!aux_pending) return;
+    cuda_check(cudaEventRecord(ev[int(Ev::Join)], aux), "record join");
+    cuda_check(cudaStreamWaitEvent(compute, ev[int(Ev::Join)], 0), "wait join");
+    aux_pending = false;
   }
   // Staging for an in-place shift of `bytes`: one chunk, charged as CommBuffer.
   void* staging(size_t bytes, size_t* chunk);

@@ -76,7 +76,7 @@ unsigned long long* next_trace(unsigned grid) {
   return p;
 }
 
-int sm_count() {
+int device_sms() {
   static int n = 0;
   if (!n) {
     int dev = 0;
@@ -85,6 +85,15 @@ int sm_count() {
     if (n <= 0) n = 148;
   }
   return n;
+}
+
+// SMs the next launches of this thread may occupy (set_sm_budget): the
+// persistent grid and the tile / split-K choice are sized for them, so two
+// GEMMs issued on two streams run side by side instead of queueing.
+thread_local int t_sm_budget = 0;
+int sm_count() {
+  const int all = device_sms();
+  return (t_sm_budget >= 2 && t_sm_budget < all) ? (t_sm_budget & ~1) : all;
 }
 
 // Operand: row-major (outer x inner, stride ld); the GEMM reads it MN-major
@@ -249,6 +258,9 @@ int dispatch(bool tf32, const Op& a, const Op& b, const Out& c0, const Out* c1, 
 }
 
 }  // namespace
+
+void set_sm_budget(int sms) { t_sm_budget = sms; }
+int sm_budget() { return sm_count(); }
 
 void set_trace(void* buf, size_t bytes) {
   g_trace = static_cast<unsigned long long*>(buf);

@@ -52,6 +52,10 @@ struct StepWgrad {
 bool wgrad_fuses_bias(bool f32, size_t M, size_t I, size_t per, unsigned* split_flags, int force_bn);
 
 int gemm_fwd(bool f32, const StepFwd& p, cudaStream_t s);
+// Caps the SMs the calling thread's following GEMM launches occupy (0 = all);
+// sm_budget() returns the effective count.
+void set_sm_budget(int sms);
+int sm_budget();
 // Debug: route per-CTA timeline stamps of the following GEMM launches into buf.
 void set_trace(void* buf, size_t bytes);
 int gemm_dgrad(bool f32, const StepDgrad& p, cudaStream_t s);
