@@ -5,13 +5,16 @@ SITE    ?= $(shell python -c "import sysconfig;print(sysconfig.get_paths()['pure
 NCCL_DIR ?= $(SITE)/nvidia/nccl
 PKG     := paper_2311_01635_b200
 CSRC    := $(PKG)/csrc
-OBJDIR  := build/obj
+OBJDIR  ?= build/obj
+OUT     ?= $(PKG)/librtpb.so
+# EXTRA: extra nvcc/g++ defines for A/B builds (tools/build_variant.sh)
+EXTRA   ?=
 ARCH    := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -Wall --expt-relaxed-constexpr \
-           -Iinclude -I$(CSRC) -I$(NCCL_DIR)/include -Xptxas -v
+           -Iinclude -I$(CSRC) -I$(NCCL_DIR)/include -Xptxas -v $(EXTRA)
 CXX     ?= g++
 CXXFLAGS := -std=c++20 -O2 -g -fPIC -Wall -Wextra -Wno-unused-parameter -Iinclude -I$(CSRC) \
-            -I/usr/local/cuda/include -I$(NCCL_DIR)/include
+            -I/usr/local/cuda/include -I$(NCCL_DIR)/include $(EXTRA)
 CU_SRC  := $(CSRC)/kernels/gemm_launch.cu $(CSRC)/kernels/elementwise.cu $(CSRC)/capi_steps.cu
 CPP_SRC := $(wildcard $(CSRC)/host/*.cpp)
 OBJS    := $(patsubst $(CSRC)/%.cu,$(OBJDIR)/%.o,$(CU_SRC)) $(patsubst $(CSRC)/%.cpp,$(OBJDIR)/%.o,$(CPP_SRC))
@@ -19,7 +22,7 @@ HDRS    := $(wildcard include/*.h include/rtpb/*.hpp $(CSRC)/kernels/*.cuh $(CSR
 
 .PHONY: all lib oracle clean
 all: lib oracle
-lib: $(PKG)/librtpb.so
+lib: $(OUT)
 oracle:
 	$(MAKE) -s -C oracle oracle
 
@@ -31,7 +34,8 @@ $(OBJDIR)/%.o: $(CSRC)/%.cpp $(HDRS)
 	@mkdir -p $(dir $@)
 	$(CXX) $(CXXFLAGS) -c $< -o $@
 
-$(PKG)/librtpb.so: $(OBJS)
+$(OUT): $(OBJS)
+	@mkdir -p $(dir $@)
 	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -L$(NCCL_DIR)/lib -l:libnccl.so.2 \
 	    -Xlinker -rpath,$(NCCL_DIR)/lib -lpthread
 

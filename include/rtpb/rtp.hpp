@@ -313,6 +313,11 @@ class RtpLinear : public RtpLayerBase {
   };
   void forward_ex(std::span<const DView> x, size_t rows, std::span<const DView> y, Mode mode, const FwdEpi& e);
   void backward_ex(std::span<const DView> dy, size_t rows, std::span<const DView> dx, const BwdEpi& e);
+  // N = 1 (no rotation): the bookkeeping of forward_ex (position law, replay
+  // tape, X kept for backward, trace) without a launch; returns the resident
+  // shard [W_0 | b_0] for a caller that issues the GEMM itself (RtpMlp's
+  // fused forward).
+  const void* begin_forward_n1(const DView& x, size_t rows, Mode mode);
 
  private:
   void build(size_t in_dim, size_t out_dim, size_t n);
@@ -352,6 +357,13 @@ class RtpMlp {
   std::unique_ptr<RtpLinear> ffn1_, ffn2_;
   std::vector<DeviceBuffer> pre_, act_, dpre_;  // per rank, rows x f (Activation)
   size_t act_rows_ = 0;
+  // N = 1 fused forward: unit schedule + row-block counters (Other), per rows.
+  void ensure_fused(size_t rows);
+  DeviceBuffer fused_ws_;
+  size_t fused_rows_ = 0;
+  int fused_slots_ = 0, fused_dep_rows_ = 0, fused_splits2_ = 1, fused_tiles2_ = 0;
+  unsigned fused_dep_target_ = 0;
+  size_t fused_sched_ints_ = 0, fused_acc_off_ = 0;
 };
 
 // Host fp64 -> device dtype, round-to-nearest-even from the double (no

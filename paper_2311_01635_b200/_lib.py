@@ -10,7 +10,8 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "librtpb.so")
+# RTPB_LIB: load an A/B build of the same library (tools/build_variant.sh)
+LIB_PATH = os.environ.get("RTPB_LIB") or os.path.join(HERE, "librtpb.so")
 
 RTPB_OK = 0
 ERR_NAMES = {1: "Generic", 2: "Config", 3: "Dimension", 4: "Protocol", 5: "State", 6: "Index", 7: "Cuda", 8: "Nccl"}

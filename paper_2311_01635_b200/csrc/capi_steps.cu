@@ -121,6 +121,24 @@ int set_cuda_error(cudaError_t e, const char* where) {
 
 void count_launch(uint64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
+int fused_fwd_step(const void* x, size_t ldx, const void* w1_shard, void* pre, void* act, const void* w2_shard,
+                   void* y, size_t ldy, size_t M, size_t h, size_t f, bool store_pre, const FusedFwdPlan& plan,
+                   const FusedFwdWs& ws, cudaStream_t s) {
+  int rc;
+  if ((rc = check_geom(M, h, f))) return rc;
+  const auto* w1 = static_cast<const uint16_t*>(w1_shard);  // bf16 elements
+  const auto* w2 = static_cast<const uint16_t*>(w2_shard);
+  StepFwd p0{};
+  p0.x = x; p0.ldx = ldx; p0.w = w1; p0.bias = w1 + h * f;
+  p0.y = pre; p0.ldy = f; p0.act = act; p0.ld_act = f;
+  p0.M = M; p0.I = h; p0.per = f;
+  p0.flags = RTPB_EPI_GELU | (store_pre ? RTPB_EPI_STORE_PRE : 0);
+  StepFwd p1{};
+  p1.x = act; p1.ldx = f; p1.w = w2; p1.bias = w2 + f * h;
+  p1.y = y; p1.ldy = ldy; p1.M = M; p1.I = f; p1.per = h; p1.flags = RTPB_EPI_STORE_PRE;
+  return timed(0, 4.0 * M * h * f, s, [&] { return gemm_fwd_fused(p0, p1, plan, ws, s); });
+}
+
 }  // namespace rtpb
 
 using namespace rtpb;
@@ -238,6 +256,8 @@ int rtpb_wgrad_step(int dtype, const void* x, size_t ldx, const void* dy, size_t
     p.x = xh; p.x_lo = xl; p.ldx = Mp; p.dy = dh; p.dy_lo = dl; p.ldy = Mp;
   }
   if (!c.ok) return set_error(RTPB_ERR_DIMENSION, "wgrad_step: workspace too small");
+  if ((reinterpret_cast<uintptr_t>(g_out) | reinterpret_cast<uintptr_t>(g_in)) & 15)
+    return set_error(RTPB_ERR_CONFIG, "wgrad_step: gradient shards must be 16-byte aligned");
   const float* gb_in = g_in ? g_in + I * per : nullptr;
   float* gb_out = g_out + I * per;
   return timed(2, 2.0 * M * I * per, s, [&] {

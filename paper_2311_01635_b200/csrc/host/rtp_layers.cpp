@@ -305,6 +305,22 @@ void RtpLinear::forward_ex(std::span<const DView> x, size_t rows, std::span<cons
   if (mode == Mode::Eval) rehome_after_eval();
 }
 
+const void* RtpLinear::begin_forward_n1(const DView& x, size_t rows, Mode mode) {
+  require_home("forward");
+  if (group_->size() != 1) throw StateError(label_ + ": begin_forward_n1 needs a single-worker group");
+  if (rows == 0) throw DimensionError(label_ + ": forward needs at least one row");
+  ensure_scratch(rows);
+  const size_t r = group_->local_ranks()[0];
+  check_forward_position(r, 0);
+  trace_[0] = int64_t(slots_[r].logical_id);
+  if (mode == Mode::Train) {
+    tapes_[r].record(slots_[r].logical_id, {});
+    x_cache_[r] = x;
+    cached_rows_ = rows;
+  }
+  return slots_[r].weight.data();
+}
+
 void RtpLinear::backward_ex(std::span<const DView> dy, size_t rows, std::span<const DView> dx, const BwdEpi& e) {
   const auto& local = group_->local_ranks();
   if (dy.size() != local.size() || dx.size() != local.size())
@@ -488,8 +504,57 @@ void RtpMlp::ensure_acts(size_t rows) {
   act_rows_ = rows;
 }
 
+void RtpMlp::ensure_fused(size_t rows) {
+  if (rows == fused_rows_) return;
+  FusedFwdPlan plan;
+  if (!plan_fused_fwd(rows, h_, f_, plan)) throw ConfigError("RtpMlp: no fused forward schedule for this shape");
+  group_->synchronize();
+  const size_t r = group_->local_ranks()[0];
+  Worker& w = group_->worker(r);
+  fused_sched_ints_ = plan.sched.size();
+  // [schedule][row-block counters][done][ffn2 split counters] then, when ffn2
+  // is split over K, its fp32 partial sums (rows x h)
+  const size_t ints = fused_sched_ints_ + size_t(plan.dep_rows) + 1 + size_t(plan.tiles2);
+  fused_acc_off_ = (ints * sizeof(int) + 255) & ~size_t(255);
+  const size_t bytes = fused_acc_off_ + (plan.k_splits2 > 1 ? rows * h_ * sizeof(float) : 0);
+  fused_ws_ = DeviceBuffer(w.device, bytes, &w.ledger, MemCategory::Other, true);  // counters start at zero
+  cuda_check(cudaMemcpy(fused_ws_.data(), plan.sched.data(), fused_sched_ints_ * sizeof(int), cudaMemcpyHostToDevice),
+             "upload fused schedule");
+  fused_slots_ = plan.slots;
+  fused_dep_rows_ = plan.dep_rows;
+  fused_dep_target_ = plan.dep_target;
+  fused_splits2_ = plan.k_splits2;
+  fused_tiles2_ = plan.tiles2;
+  fused_rows_ = rows;
+}
+
 void RtpMlp::forward(std::span<const DView> x, size_t rows, std::span<const DView> y, Mode mode) {
   ensure_acts(rows);
+  if (group_->size() == 1 && dtype_ == DType::BF16 && !std::getenv("RTPB_NO_FUSED_FWD")) {
+    // N = 1: no rotation between ffn1 and ffn2, so both GEMMs run as one
+    // scheduled persistent launch (ffn2's row blocks start as soon as ffn1
+    // has written them); the layers keep their reference bookkeeping.
+    if (x.size() != 1 || y.size() != 1) throw DimensionError("RtpMlp: forward expects one activation per worker");
+    const size_t r = group_->local_ranks()[0];
+    ensure_fused(rows);
+    const void* w1 = ffn1_->begin_forward_n1(x[0], rows, mode);
+    const void* w2 = ffn2_->begin_forward_n1({act_[r].data(), f_}, rows, mode);
+    Worker& w = group_->worker(r);
+    int* base = static_cast<int*>(fused_ws_.data());
+    unsigned* dep = reinterpret_cast<unsigned*>(base + fused_sched_ints_);
+    FusedFwdPlan plan;
+    plan.slots = fused_slots_;
+    plan.dep_rows = fused_dep_rows_;
+    plan.dep_target = fused_dep_target_;
+    plan.k_splits2 = fused_splits2_;
+    plan.tiles2 = fused_tiles2_;
+    FusedFwdWs ws{base, dep, dep + fused_dep_rows_, dep + fused_dep_rows_ + 1,
+                  fused_splits2_ > 1 ? reinterpret_cast<float*>(reinterpret_cast<char*>(base) + fused_acc_off_)
+                                     : nullptr};
+    check_status(fused_fwd_step(x[0].data, x[0].ld ? x[0].ld : h_, w1, pre_[r].data(), act_[r].data(), w2, y[0].data,
+                                y[0].ld ? y[0].ld : h_, rows, h_, f_, mode == Mode::Train, plan, ws, w.compute));
+    return;
+  }
   const auto& local = group_->local_ranks();
   std::vector<DView> pre(local.size()), act(local.size());
   for (size_t k = 0; k < local.size(); ++k) {

@@ -5,11 +5,16 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
 #include "gemm_sm100.cuh"
 #include "launch.hpp"
+
+#ifndef RTPB_L2_PROMO
+#define RTPB_L2_PROMO CU_TENSOR_MAP_L2_PROMOTION_L2_256B
+#endif
 
 namespace rtpb {
 
@@ -46,7 +51,7 @@ int encode_2d(CUtensorMap* m, const void* ptr, bool f32, uint64_t inner, uint64_
   cuuint32_t estr[2] = {1, 1};
   CUresult r = g_encode(m, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
                         const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
-                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                        RTPB_L2_PROMO, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     char buf[160];
     std::snprintf(buf, sizeof buf, "cuTensorMapEncodeTiled failed (%d): inner=%llu outer=%llu ld=%llu", int(r),
@@ -112,8 +117,7 @@ struct Out {
 };
 
 template <class Cfg>
-int launch_cfg(const Op& a, const Op& b, const Out& c0, const Out* c1, const GemmArgs& args, cudaStream_t stream) {
-  GemmMaps maps;
+int encode_maps(const Op& a, const Op& b, const Out& c0, const Out* c1, GemmMaps& maps) {
   std::memset(&maps, 0, sizeof maps);
   constexpr bool F32 = Cfg::TF32;
   const uint32_t a_box_in = Cfg::A_MN ? Cfg::ATOM_MN : Cfg::BK;
@@ -130,6 +134,17 @@ int launch_cfg(const Op& a, const Op& b, const Out& c0, const Out* c1, const Gem
   if ((rc = encode_out(&maps.c0, c0.ptr, c0.f32, c0.cols, c0.rows, c0.ld))) return rc;
   const Out& o1 = c1 ? *c1 : c0;  // keep c1 a valid map even when unused
   if ((rc = encode_out(&maps.c1, o1.ptr, o1.f32, o1.cols, o1.rows, o1.ld))) return rc;
+  return RTPB_OK;
+}
+
+// maps2: problem 1 of a scheduled launch (args.sched); slots_override: the
+// unit slots (CTA pairs / CTAs) the schedule was built for.
+template <class Cfg>
+int launch_cfg(const Op& a, const Op& b, const Out& c0, const Out* c1, const GemmArgs& args, cudaStream_t stream,
+               const GemmMaps* maps2 = nullptr, int slots_override = 0) {
+  GemmMaps maps;
+  int rc;
+  if ((rc = encode_maps<Cfg>(a, b, c0, c1, maps))) return rc;
   static bool attr_set = false;  // per instantiation
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(rtp_gemm_kernel<Cfg>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -152,19 +167,20 @@ int launch_cfg(const Op& a, const Op& b, const Out& c0, const Out* c1, const Gem
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  const int slots = slots_override > 0 ? slots_override : std::min(tiles, Cfg::PAIR ? sm_count() / 2 : sm_count());
   if constexpr (Cfg::PAIR) {
-    cfg.gridDim = dim3(unsigned(2 * std::min(tiles, sm_count() / 2)));
+    cfg.gridDim = dim3(unsigned(2 * slots));
     attr[1].id = cudaLaunchAttributeClusterDimension;
     attr[1].val.clusterDim.x = 2;
     attr[1].val.clusterDim.y = 1;
     attr[1].val.clusterDim.z = 1;
     cfg.numAttrs = 2;
   } else {
-    cfg.gridDim = dim3(unsigned(std::min(tiles, sm_count())));
+    cfg.gridDim = dim3(unsigned(slots));
   }
   GemmArgs a_ = args;
   a_.trace = next_trace(cfg.gridDim.x);
-  cudaError_t e = cudaLaunchKernelEx(&cfg, rtp_gemm_kernel<Cfg>, maps, a_);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, rtp_gemm_kernel<Cfg>, maps, maps2 ? *maps2 : maps, a_);
   if (e != cudaSuccess) return set_cuda_error(e, "rtp_gemm_kernel launch");
   count_launch();
   return RTPB_OK;
@@ -208,8 +224,13 @@ constexpr int kEpiWarps = 8;
 template <int EPI, bool TF32>
 int dispatch_tile(int code, const Op& a, const Op& b, const Out& c0, const Out* c1, const GemmArgs& args,
                   cudaStream_t s) {
+#ifdef RTPB_WGRAD_KMAJOR_PROBE  // dev A/B: wgrad fed pre-transposed (K-major) operands
+  constexpr bool AMN = false;
+  constexpr bool BMN = !TF32 && EPI == EPI_FWD;
+#else
   constexpr bool AMN = !TF32 && EPI == EPI_WGRAD;
   constexpr bool BMN = !TF32 && EPI != EPI_DGRAD;
+#endif
   if constexpr (!TF32) {
     if (code == 1256) return launch_cfg<GemmCfg<EPI, 256, false, kEpiWarps, AMN, BMN, false, true>>(a, b, c0, c1, args, s);
     if (code == 1128) return launch_cfg<GemmCfg<EPI, 128, false, kEpiWarps, AMN, BMN, false, true>>(a, b, c0, c1, args, s);
@@ -252,12 +273,155 @@ int dispatch(bool tf32, const Op& a, const Op& b, const Out& c0, const Out* c1, 
   // Raster n fastest when the B operand (all n-blocks x K) fits comfortably in
   // L2: concurrent CTAs then share each A row-block, which is read once.
   const double b_bytes = double(num_n) * bn * args.K * (tf32 ? 4.0 : 2.0);
+#ifdef RTPB_WGRAD_NFAST  // dev A/B
+  args.n_fastest = b_bytes < 48e6;
+#else
   args.n_fastest = (EPI != EPI_WGRAD) && b_bytes < 48e6;
+#endif
   return tf32 ? dispatch_tile<EPI, true>(code, a, b, c0, c1, args, s)
               : dispatch_tile<EPI, false>(code, a, b, c0, c1, args, s);
 }
 
 }  // namespace
+
+// ------------------------------------------------------------------ fused MLP forward (N = 1)
+// ffn1 (h -> f, + bias, GELU) and ffn2 (f -> h, + bias) in ONE persistent
+// launch on 256 x 256 CTA-pair tiles: problem 0 = ffn1's tiles, problem 1 =
+// ffn2's, whose row block mb reads the act rows ffn1's row block mb writes.
+// The host assigns units to CTA pairs by greedy list scheduling over a cost
+// model (each pair's list in simulated start order, which also makes the
+// row-block waits deadlock-free: the earliest-starting blocked unit's
+// producers all started earlier and are not blocked), so the two GEMMs share
+// one tail instead of paying two wave-quantisation tails.
+namespace {
+constexpr int kFusedBN = 256;
+using FusedFwdCfg = GemmCfg<EPI_FWD, kFusedBN, false, kEpiWarps, false, true, false, true>;
+
+double fused_unit_cost(size_t K, int outputs) {
+  // us per 256 x 256 pair tile: ~0.36 us per 64-deep K block when TMA-fed
+  // from L2, plus the epilogue share that does not hide under the next tile
+  return double((K + 63) / 64) * 0.36 + 0.4 + 0.3 * outputs;
+}
+}  // namespace
+
+bool plan_fused_fwd(size_t M, size_t h, size_t f, FusedFwdPlan& plan) {
+  const int P = sm_count() / 2;
+  const int nm = int((M + 255) / 256), n0 = int((f + kFusedBN - 1) / kFusedBN), n1 = int((h + kFusedBN - 1) / kFusedBN);
+  const int T0 = nm * n0, T1 = nm * n1;
+  if (P < 2 || T0 + 3 * T1 >= (1 << 20)) return false;
+  const double c0 = fused_unit_cost(h, 2);
+  double best = 1e300;
+  // ffn2 K splits: 1 by default. (Measured, config (b): 2 splits 104 us and 3
+  // splits 163 us vs 75 us unsplit — the ordered partial-sum epilogues chain
+  // across pairs.) RTPB_FUSED_SPLITS forces a count (A/B).
+  int s_lo = 1, s_hi = 1;
+  if (const char* e = std::getenv("RTPB_FUSED_SPLITS")) s_lo = s_hi = std::max(1, std::atoi(e));
+  for (int S = s_lo; S <= s_hi; ++S) {  // ffn2 K splits
+    const size_t kb1 = ((f + 63) / 64 + S - 1) / S;
+    // a partial split stores fp32 (2 outputs' worth); the last one also reads it back
+    const double c1 = S == 1 ? fused_unit_cost(f, 1) : double(kb1) * 0.36 + 0.4 + 0.6;
+    for (int policy = 0; policy < 2; ++policy) {  // 0: ready ffn2 units first, 1: ffn1 tiles first
+      std::vector<std::vector<int>> lists(P);
+      std::vector<double> free_at(P, 0.0), row_ready(nm, 0.0);
+      std::vector<int> row_left(nm, n0);
+      std::vector<int> ready1;  // row blocks whose ffn2 units are ready, in readiness order
+      size_t r1 = 0;            // next ready row block to take ffn2 units from
+      int r1_u = 0;             // next unit (column block x split, split fastest) within it
+      int next0 = 0;
+      double makespan = 0;
+      std::vector<double> split_done(size_t(T1), 0.0);
+      for (int done = 0; done < T0 + S * T1; ++done) {
+        int p = 0;
+        for (int i = 1; i < P; ++i)
+          if (free_at[i] < free_at[p]) p = i;
+        const double tp = free_at[p];
+        const bool have1 = r1 < ready1.size();
+        const bool ready_now = have1 && row_ready[ready1[r1]] <= tp;
+        const bool take1 = next0 >= T0 || (have1 && policy == 0 && ready_now);
+        double fin;
+        if (take1) {
+          const int mb = ready1[r1], nb = r1_u / S, sp = r1_u % S, t = mb * n1 + nb;  // n-fastest tile index
+          const double start = std::max(tp, row_ready[mb]);
+          // the epilogue of split sp waits for split sp - 1 to have landed
+          fin = std::max(start + c1, sp ? split_done[size_t(t)] + 0.6 : 0.0);
+          split_done[size_t(t)] = fin;
+          lists[p].push_back((1 << 28) | (sp << 20) | t);
+          if (++r1_u == n1 * S) {
+            r1_u = 0;
+            ++r1;
+          }
+        } else {
+          const int t = next0++, mb = t / n0;
+          fin = tp + c0;
+          lists[p].push_back(t);
+          row_ready[mb] = std::max(row_ready[mb], fin);
+          if (--row_left[mb] == 0) ready1.push_back(mb);
+        }
+        free_at[p] = fin;
+        makespan = std::max(makespan, fin);
+      }
+      if (makespan < best) {
+        best = makespan;
+        plan.sched.assign(P + 1, 0);
+        int off = P + 1;
+        for (int i = 0; i < P; ++i) {
+          plan.sched[i] = off;
+          off += int(lists[i].size());
+        }
+        plan.sched[P] = off;
+        for (int i = 0; i < P; ++i) plan.sched.insert(plan.sched.end(), lists[i].begin(), lists[i].end());
+        plan.k_splits2 = S;
+      }
+    }
+  }
+  plan.slots = P;
+  plan.dep_rows = nm;
+  plan.dep_target = unsigned(n0) * 2u * kEpiWarps;
+  plan.tiles2 = T1;
+  plan.est_us = best;
+  if (std::getenv("RTPB_DEBUG_PLAN"))
+    std::fprintf(stderr, "fused fwd plan: M=%zu h=%zu f=%zu slots=%d splits2=%d est %.1f us\n", M, h, f, P,
+                 plan.k_splits2, best);
+  return true;
+}
+
+int gemm_fwd_fused(const StepFwd& p0, const StepFwd& p1, const FusedFwdPlan& plan, const FusedFwdWs& ws,
+                   cudaStream_t s) {
+  // problem 0: pre = X . W1 + b1 (store_pre) and act = gelu(pre); problem 1: Y = act . W2 + b2
+  Op a0{p0.x, nullptr, p0.I, p0.M, p0.ldx}, b0{p0.w, nullptr, p0.per, p0.I, p0.per};
+  Op a1{p1.x, nullptr, p1.I, p1.M, p1.ldx}, b1{p1.w, nullptr, p1.per, p1.I, p1.per};
+  Out y0{p0.y, false, p0.per, p0.M, p0.ldy}, act0{p0.act, false, p0.per, p0.M, p0.ld_act};
+  Out y1{p1.y, false, p1.per, p1.M, p1.ldy};
+  const bool split = plan.k_splits2 > 1;
+  Out acc1{split ? static_cast<const void*>(ws.acc2) : p1.y, split, p1.per, p1.M, split ? p1.per : p1.ldy};
+  GemmMaps m1;
+  int rc;
+  if ((rc = encode_maps<FusedFwdCfg>(a1, b1, y1, &acc1, m1))) return rc;
+  GemmArgs g{};
+  g.M = int(p0.M);
+  g.N = int(p0.per);
+  g.K = int(p0.I);
+  g.flags = p0.flags;
+  g.aux = p0.bias;
+  g.n_fastest = 1;
+  g.k_splits = 1;
+  g.sched = ws.sched;
+  g.M2 = int(p1.M);
+  g.N2 = int(p1.per);
+  g.K2 = int(p1.I);
+  g.flags2 = p1.flags;
+  g.aux2 = p1.bias;
+  g.n_fastest2 = 1;
+  g.k_splits2 = plan.k_splits2;
+  g.split_flags2 = ws.split_flags2;
+  g.acc2 = ws.acc2;
+  g.ld_acc2 = int64_t(p1.per);
+  g.dep_count = ws.dep_count;
+  g.dep_target = plan.dep_target;
+  g.dep_rows = plan.dep_rows;
+  g.done_ctas = ws.done_ctas;
+  return launch_cfg<FusedFwdCfg>(a0, b0, y0, &act0, g, s, &m1, plan.slots);
+}
 
 void set_sm_budget(int sms) { t_sm_budget = sms; }
 int sm_budget() { return sm_count(); }
@@ -324,8 +488,13 @@ int gemm_dgrad(bool f32, const StepDgrad& p, cudaStream_t s) {
 int gemm_wgrad(bool f32, const StepWgrad& p, cudaStream_t s) {
   // C[I x per] = X^T . dY_blk; bf16: X and dY_blk read MN-major in place.
   // tf32: the pre-pass wrote X^T (I x M) and dY_blk^T (per x M), both K-major.
-  Op a = f32 ? Op{p.x, p.x_lo, p.M, p.I, p.ldx} : Op{p.x, p.x_lo, p.I, p.M, p.ldx};
-  Op b = f32 ? Op{p.dy, p.dy_lo, p.M, p.per, p.ldy} : Op{p.dy, p.dy_lo, p.per, p.M, p.ldy};
+#ifdef RTPB_WGRAD_KMAJOR_PROBE
+  const bool kmaj = true;
+#else
+  const bool kmaj = f32;
+#endif
+  Op a = kmaj ? Op{p.x, p.x_lo, p.M, p.I, p.ldx} : Op{p.x, p.x_lo, p.I, p.M, p.ldx};
+  Op b = kmaj ? Op{p.dy, p.dy_lo, p.M, p.per, p.ldy} : Op{p.dy, p.dy_lo, p.per, p.M, p.ldy};
   GemmArgs g{};
   g.M = int(p.I);
   g.N = int(p.per);
@@ -352,6 +521,9 @@ bool wgrad_fuses_bias(bool f32, size_t M, size_t I, size_t per, unsigned* split_
   g.N = int(per);
   g.K = int(M);
   g.split_flags = split_flags;
+#ifdef RTPB_NO_COLSUM
+  return false;
+#endif
   return !f32 && pick_code<EPI_WGRAD>(false, g, force_bn) > 1000;
 }
 

@@ -67,6 +67,30 @@ struct GemmArgs {
   // accumulator, accumulator free, first stage landed, last MMA committed,
   // epilogue sees the accumulator, epilogue released it; last slot = gridDim.x.
   unsigned long long* trace;
+  // Scheduled multi-problem launch (nullable sched: static round-robin over
+  // problem 0's units). Unit slot s (a CTA pair, or a CTA) processes the units
+  // sched[sched[s] .. sched[s + 1]), each encoded prob << 28 | split << 20 |
+  // tile, in that order. Problem 1 (same kernel config, its maps in the second
+  // GemmMaps) has geometry M2 x N2 x K2 and epilogue flags2 / aux2; its tile
+  // row block mb may start loading only when dep_count[mb] >= dep_target,
+  // which problem 0's epilogue warps advance (one arrival per warp per tile
+  // of that row block) once their stores of the tile are complete. The last
+  // CTA to finish re-zeroes dep_count[0 .. dep_rows) and done_ctas.
+  const int* sched;
+  int M2, N2, K2, flags2, n_fastest2;
+  const void* aux2;
+  // Problem 1 split over K (FWD only): split s < k_splits2 - 1 stores (s = 0)
+  // or reduce-adds its fp32 partial into acc2 (M2 x N2, map c1 of the second
+  // GemmMaps), in split order via split_flags2[tile]; the last split adds
+  // acc2, the bias and writes the output. Deterministic.
+  int k_splits2;
+  unsigned* split_flags2;
+  const float* acc2;
+  int64_t ld_acc2;
+  unsigned* dep_count;
+  unsigned dep_target;
+  int dep_rows;
+  unsigned* done_ctas;
 };
 constexpr int TRACE_UNITS = 13;
 constexpr int TRACE_STRIDE = 80;
@@ -121,7 +145,11 @@ struct GemmCfg {
   // Each takes half of a stage's K rows; their sums meet in COLSUM_BYTES.
   // (Measured, config (b) dW in the step graph: 45.5 us per launch vs 42.4 us
   // for the GEMM alone; the stand-alone column-sum kernel cost ~6 us more.)
+#ifdef RTPB_NO_COLSUM
+  static constexpr bool COLSUM = false;
+#else
   static constexpr bool COLSUM = EPI == EPI_WGRAD && PAIR && !TF32;
+#endif
   static constexpr int COLSUM_WARPS = COLSUM ? 2 : 0;
   static constexpr int COLSUM_BYTES = COLSUM ? B_ROWS * 4 : 0;
   static constexpr int SMEM_LIMIT = 232448;     // 227 KB opt-in per block
@@ -300,7 +328,8 @@ __device__ __forceinline__ void unstage_row(const uint8_t* stg, int row, float* 
 
 template <class Cfg>
 __global__ void __launch_bounds__(Cfg::THREADS, 1)
-    rtp_gemm_kernel(const __grid_constant__ GemmMaps maps, const GemmArgs args) {
+    rtp_gemm_kernel(const __grid_constant__ GemmMaps maps, const __grid_constant__ GemmMaps maps2,
+                    const GemmArgs args) {
   using namespace ptx;
   constexpr int BM = Cfg::BM, BN = Cfg::BN, BK = Cfg::BK, STAGES = Cfg::STAGES;
   constexpr bool F32 = Cfg::TF32;  // activation / output dtype is fp32 in TF32 mode
@@ -340,10 +369,53 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
   const int splits = args.k_splits > 1 ? args.k_splits : 1;
   const int num_units = num_tiles * splits;
   const int kb_per = (num_kb + splits - 1) / splits;
-  auto unit_kb = [&](int u, int& kb0, int& kb1) {
-    const int s = u / num_tiles;
-    kb0 = s * kb_per;
-    kb1 = min(num_kb, kb0 + kb_per);
+  // This slot's unit sequence: a static round-robin over problem 0, or its
+  // list in the scheduled multi-problem launch.
+  int it_beg = unit, it_end = num_units, it_step = units;
+  if (args.sched) {
+    it_beg = __ldg(args.sched + unit);
+    it_end = __ldg(args.sched + unit + 1);
+    it_step = 1;
+  }
+  const int num_m2 = (args.M2 + Cfg::TILE_M - 1) / Cfg::TILE_M;
+  const int num_n2 = (args.N2 + BN - 1) / BN;
+  const int num_kb2 = (args.K2 + BK - 1) / BK;
+  const int splits2 = args.k_splits2 > 1 ? args.k_splits2 : 1;
+  const int kb_per2 = (num_kb2 + splits2 - 1) / splits2;
+  struct Unit {
+    int prob, t, mb, nb, split, kb0, kb1, M, N, flags;
+  };
+  auto decode = [&](int it) {
+    Unit x;
+    if (args.sched) {
+      const int e = __ldg(args.sched + it);
+      x.prob = e >> 28;
+      x.split = (e >> 20) & 0xFF;
+      x.t = e & 0xFFFFF;
+    } else {
+      x.prob = 0;
+      x.t = it % num_tiles;
+      x.split = it / num_tiles;
+    }
+    const int nm = x.prob ? num_m2 : num_m, nn = x.prob ? num_n2 : num_n;
+    if (x.prob ? args.n_fastest2 : args.n_fastest) {
+      x.nb = x.t % nn;
+      x.mb = x.t / nn;
+    } else {
+      x.mb = x.t % nm;
+      x.nb = x.t / nm;
+    }
+    if (x.prob) {
+      x.kb0 = x.split * kb_per2;
+      x.kb1 = min(num_kb2, x.kb0 + kb_per2);
+    } else {
+      x.kb0 = x.split * kb_per;
+      x.kb1 = min(num_kb, x.kb0 + kb_per);
+    }
+    x.M = x.prob ? args.M2 : args.M;
+    x.N = x.prob ? args.N2 : args.N;
+    x.flags = x.prob ? args.flags2 : args.flags;
+    return x;
   };
 
   if (warp == 0 && lane == 0) {
@@ -394,15 +466,6 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
   griddep_launch();
   if (threadIdx.x == 0) detail::trace_at(trace, 1);
 
-  auto tile_coords = [&](int t, int& mb, int& nb) {
-    if (args.n_fastest) {
-      nb = t % num_n;
-      mb = t / num_n;
-    } else {
-      mb = t % num_m;
-      nb = t / num_m;
-    }
-  };
   const bool colsum_on = Cfg::COLSUM && args.gbias_out != nullptr;
 
   if (warp == 0) {
@@ -420,59 +483,69 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
       // crediting bytes, so such boxes are skipped and the leader expects only
       // the bytes both CTAs actually request (their smem is never read into a
       // stored result: those rows / columns are clipped by the output maps).
-      auto a_bytes = [&](int ma0) {
+      auto a_bytes = [&](int ma0, int M_) {
         int b = 0;
         if constexpr (Cfg::A_MN) {
           for (int c = 0; c < BM / Cfg::ATOM_MN; ++c)
-            if (ma0 + c * Cfg::ATOM_MN < args.M) b += BK * 128;
+            if (ma0 + c * Cfg::ATOM_MN < M_) b += BK * 128;
         } else {
-          if (ma0 < args.M) b = Cfg::A_BYTES;
+          if (ma0 < M_) b = Cfg::A_BYTES;
         }
         return b * Cfg::NOPS;
       };
-      auto b_bytes = [&](int nb0) {
+      auto b_bytes = [&](int nb0, int N_) {
         int b = 0;
         if constexpr (Cfg::B_MN) {
           for (int c = 0; c < Cfg::B_ROWS / Cfg::ATOM_MN; ++c)
-            if (nb0 + c * Cfg::ATOM_MN < args.N) b += BK * 128;
+            if (nb0 + c * Cfg::ATOM_MN < N_) b += BK * 128;
         } else {
-          if (nb0 < args.N) b = Cfg::B_BYTES;
+          if (nb0 < N_) b = Cfg::B_BYTES;
         }
         return b * Cfg::NOPS;
       };
-      for (int u = unit; u < num_units; u += units) {
-        int mb, nb, kb0, kb1;
-        tile_coords(u % num_tiles, mb, nb);
-        unit_kb(u, kb0, kb1);
+      for (int it = it_beg; it < it_end; it += it_step) {
+        const Unit x = decode(it);
+        const int mb = x.mb, nb = x.nb, kb0 = x.kb0, kb1 = x.kb1, uM = x.M, uN = x.N;
+        const GemmMaps& mp = x.prob ? maps2 : maps;
+        if (x.prob && args.dep_count) {
+          // problem 1 reads problem 0's output rows of this row block: wait
+          // until every warp of every problem-0 tile of the block has landed
+          // its stores, then order the async-proxy (TMA) reads after them.
+          unsigned seen;
+          do {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(args.dep_count + mb) : "memory");
+          } while (seen < args.dep_target);
+          asm volatile("fence.proxy.async.global;" ::: "memory");
+        }
         // this CTA's A rows and B columns (pair: its half of the 256 x BN tile)
         const int m0 = mb * Cfg::TILE_M + int(rank) * BM, n0 = nb * BN + int(rank) * Cfg::B_ROWS;
-        int expect = a_bytes(mb * Cfg::TILE_M) + b_bytes(nb * BN);
-        if constexpr (Cfg::PAIR) expect += a_bytes(mb * Cfg::TILE_M + BM) + b_bytes(nb * BN + Cfg::B_ROWS);
+        int expect = a_bytes(mb * Cfg::TILE_M, uM) + b_bytes(nb * BN, uN);
+        if constexpr (Cfg::PAIR) expect += a_bytes(mb * Cfg::TILE_M + BM, uM) + b_bytes(nb * BN + Cfg::B_ROWS, uN);
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
           uint8_t* sA = stage_base + stage * Cfg::STAGE_BYTES;
           if (rank == 0) mbar_expect_tx(&full_bar[stage], uint32_t(expect));
           const int k0 = kb * BK;
           for (int op = 0; op < Cfg::NOPS; ++op) {
-            const CUtensorMap* ma = op ? &maps.a_lo : &maps.a;
-            const CUtensorMap* mbm = op ? &maps.b_lo : &maps.b;
+            const CUtensorMap* ma = op ? &mp.a_lo : &mp.a;
+            const CUtensorMap* mbm = op ? &mp.b_lo : &mp.b;
             uint8_t* dA = sA + op * (Cfg::A_BYTES + Cfg::B_BYTES);
             uint8_t* dB = dA + Cfg::A_BYTES;
             if constexpr (Cfg::A_MN) {
 #pragma unroll
               for (int c = 0; c < BM / Cfg::ATOM_MN; ++c)
-                if (m0 + c * Cfg::ATOM_MN < args.M)
+                if (m0 + c * Cfg::ATOM_MN < uM)
                   load(dA + c * (BK * 128), ma, &full_bar[stage], m0 + c * Cfg::ATOM_MN, k0);
             } else {
-              if (m0 < args.M) load(dA, ma, &full_bar[stage], k0, m0);
+              if (m0 < uM) load(dA, ma, &full_bar[stage], k0, m0);
             }
             if constexpr (Cfg::B_MN) {
 #pragma unroll
               for (int c = 0; c < Cfg::B_ROWS / Cfg::ATOM_MN; ++c)
-                if (n0 + c * Cfg::ATOM_MN < args.N)
+                if (n0 + c * Cfg::ATOM_MN < uN)
                   load(dB + c * (BK * 128), mbm, &full_bar[stage], n0 + c * Cfg::ATOM_MN, k0);
             } else {
-              if (n0 < args.N) load(dB, mbm, &full_bar[stage], k0, n0);
+              if (n0 < uN) load(dB, mbm, &full_bar[stage], k0, n0);
             }
           }
           if (++stage == STAGES) {
@@ -490,9 +563,9 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
       int acc = 0;
       uint32_t acc_phase = 0;
       int li = 0;
-      for (int u = unit; u < num_units; u += units, ++li) {
-        int kb0, kb1;
-        unit_kb(u, kb0, kb1);
+      for (int it = it_beg; it < it_end; it += it_step, ++li) {
+        const Unit x = decode(it);
+        const int kb0 = x.kb0, kb1 = x.kb1;
         const bool tr = trace && li < TRACE_UNITS;
         if (tr) detail::trace_at(trace, 2 + 6 * li);
         mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
@@ -558,37 +631,38 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
     constexpr int NSPLIT = Cfg::EPI_WARPS / 4;
     uint8_t* stg0 = stg_base + ew * Cfg::STG_WARP;
     uint8_t* stg1 = stg0 + Cfg::STG_ONE;
-    const bool last = args.flags & EF_LAST;
-    const bool first = args.flags & EF_FIRST;
-    const bool pre_tma = Cfg::PRE_TMA && last && (args.flags & EF_GELU_BWD);
     uint8_t* pre_w = pre_base + ew * Cfg::PRE_WARP;
     uint32_t pre_phase = 0;
     bool pending = false;
     int acc = 0;
     uint32_t acc_phase = 0;
     int li = 0;
-    for (int u = unit; u < num_units; u += units, ++li) {
+    for (int it = it_beg; it < it_end; it += it_step, ++li) {
       const bool tr = trace && li < TRACE_UNITS && ew == 0 && lane == 0;
-      const int t = u % num_tiles, split = u / num_tiles;
-      int mb, nb;
-      tile_coords(t, mb, nb);
+      const Unit x_ = decode(it);
+      const int t = x_.t, split = x_.split, mb = x_.mb, nb = x_.nb, uM = x_.M, uN = x_.N, uflags = x_.flags;
+      const GemmMaps& mp = x_.prob ? maps2 : maps;
+      const void* uaux = x_.prob ? args.aux2 : args.aux;
+      const bool last = uflags & EF_LAST;
+      const bool first = uflags & EF_FIRST;
+      const bool pre_tma = Cfg::PRE_TMA && last && (uflags & EF_GELU_BWD);
       const int wgroup = Cfg::EPI_WARPS * (Cfg::PAIR ? 2 : 1);  // epilogue warps per tile
       const int m0 = mb * Cfg::TILE_M + int(rank) * BM, n0 = nb * BN;  // this CTA's 128 rows
       const int row0 = m0 + q * 32;     // first row of this warp's 32-row slab
       const int row = row0 + lane;
-      const bool row_ok = row < args.M;
+      const bool row_ok = row < uM;
       if constexpr (Cfg::PRE_TMA) {
         // Stream this warp's pre chunks in while the tile's MMAs still run
         // (boxes entirely outside the tensor are skipped: they credit no bytes).
         if (pre_tma && lane == 0) {
           uint32_t bytes = 0;
           for (int k = 0; k < Cfg::PRE_CHUNKS; ++k)
-            if (n0 + (half + k * NSPLIT) * 32 < args.N && row0 < args.M) bytes += 32 * 32 * Cfg::ELEM;
+            if (n0 + (half + k * NSPLIT) * 32 < uN && row0 < uM) bytes += 32 * 32 * Cfg::ELEM;
           mbar_expect_tx(&pre_bar[ew], bytes);
           for (int k = 0; k < Cfg::PRE_CHUNKS; ++k) {
             const int nc = n0 + (half + k * NSPLIT) * 32;
-            if (nc < args.N && row0 < args.M)
-              tma_load_2d(pre_w + k * 32 * 32 * Cfg::ELEM, &maps.c1, &pre_bar[ew], nc, row0);
+            if (nc < uN && row0 < uM)
+              tma_load_2d(pre_w + k * 32 * 32 * Cfg::ELEM, &mp.c1, &pre_bar[ew], nc, row0);
           }
         }
       }
@@ -600,11 +674,11 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
         for (int k = 0; k < Cfg::PRE_CHUNKS; ++k) {
           const int col = n0 + (half + k * NSPLIT) * 32 + lane;
           float bv = 0.f;
-          if (col < args.N) {
+          if (col < uN) {
             if constexpr (F32)
-              bv = static_cast<const float*>(args.aux)[col];
+              bv = static_cast<const float*>(uaux)[col];
             else
-              bv = __bfloat162float(static_cast<const __nv_bfloat16*>(args.aux)[col]);
+              bv = __bfloat162float(static_cast<const __nv_bfloat16*>(uaux)[col]);
           }
           bias_w[k * 32 + lane] = bv;
         }
@@ -613,6 +687,22 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
       if (tr) detail::trace_at(trace, 6 + 6 * li);
+      // FWD problem 1 split over K: partial splits go to the fp32 workspace,
+      // in split order; the last split folds the workspace into its output.
+      const bool split2 = Cfg::EPI == EPI_FWD && x_.prob == 1 && splits2 > 1;
+      const bool part2 = split2 && split < splits2 - 1;
+      const bool fin2 = split2 && split == splits2 - 1;
+      if (split2 && split > 0) {
+        if (lane == 0) {
+          const unsigned need = unsigned(split * wgroup);
+          unsigned seen;
+          do {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(args.split_flags2 + t) : "memory");
+          } while (seen < need);
+          asm volatile("fence.proxy.async.global;" ::: "memory");
+        }
+        __syncwarp();
+      }
       if constexpr (Cfg::EPI == EPI_WGRAD) {
         if (split > 0) {
           // ordered split-K: wait until every warp of split-1 has landed its sums
@@ -637,7 +727,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
 #pragma unroll 1
       for (int ch = half; ch < BN / 32; ch += NSPLIT) {
         const int nc = n0 + ch * 32;
-        if (nc >= args.N) break;  // warp-uniform
+        if (nc >= uN) break;  // warp-uniform
         uint32_t v[32];
         tmem_ld_32x32b_x32(t_row + ch * 32, v);
         tmem_ld_wait();
@@ -650,26 +740,40 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
           __syncwarp();
         }
         if constexpr (Cfg::EPI == EPI_FWD) {
-          const float4* bsm = reinterpret_cast<const float4*>(bias_w + ((ch - half) / NSPLIT) * 32);
+          if (part2) {
+            detail::stage_row<true>(stg0, lane, x);  // fp32 partial (stg0 + stg1: 4 KB)
+          } else {
+            if (fin2 && row_ok) {
 #pragma unroll
-          for (int g = 0; g < 8; ++g) {  // broadcast smem reads
-            const float4 b4 = bsm[g];
-            x[4 * g] += b4.x;
-            x[4 * g + 1] += b4.y;
-            x[4 * g + 2] += b4.z;
-            x[4 * g + 3] += b4.w;
-          }
-          if (args.flags & EF_STORE_PRE) detail::stage_row<F32>(stg0, lane, x);
-          if (args.flags & EF_GELU) {
+              for (int g = 0; g < 4; ++g)
+                if (nc + g * 8 < uN) {
+                  const float4* p = reinterpret_cast<const float4*>(args.acc2 + row * args.ld_acc2 + nc + g * 8);
+                  const float4 a = __ldcg(p), b = __ldcg(p + 1);
+                  x[g * 8 + 0] += a.x; x[g * 8 + 1] += a.y; x[g * 8 + 2] += a.z; x[g * 8 + 3] += a.w;
+                  x[g * 8 + 4] += b.x; x[g * 8 + 5] += b.y; x[g * 8 + 6] += b.z; x[g * 8 + 7] += b.w;
+                }
+            }
+            const float4* bsm = reinterpret_cast<const float4*>(bias_w + ((ch - half) / NSPLIT) * 32);
 #pragma unroll
-            for (int e = 0; e < 32; ++e) x[e] = detail::gelu_f<F32>(x[e]);
-            detail::stage_row<F32>(stg1, lane, x);
+            for (int g = 0; g < 8; ++g) {  // broadcast smem reads
+              const float4 b4 = bsm[g];
+              x[4 * g] += b4.x;
+              x[4 * g + 1] += b4.y;
+              x[4 * g + 2] += b4.z;
+              x[4 * g + 3] += b4.w;
+            }
+            if (uflags & EF_STORE_PRE) detail::stage_row<F32>(stg0, lane, x);
+            if (uflags & EF_GELU) {
+#pragma unroll
+              for (int e = 0; e < 32; ++e) x[e] = detail::gelu_f<F32>(x[e]);
+              detail::stage_row<F32>(stg1, lane, x);
+            }
           }
         } else if constexpr (Cfg::EPI == EPI_DGRAD) {
           if (last && !first && row_ok) {
 #pragma unroll
             for (int g = 0; g < 4; ++g)
-              if (nc + g * 8 < args.N) {
+              if (nc + g * 8 < uN) {
                 const float4* p = reinterpret_cast<const float4*>(args.acc + row * args.ld_acc + nc + g * 8);
                 const float4 a = p[0], b = p[1];
                 x[g * 8 + 0] += a.x; x[g * 8 + 1] += a.y; x[g * 8 + 2] += a.z; x[g * 8 + 3] += a.w;
@@ -683,12 +787,12 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
             detail::unstage_row<F32>(pc, lane, pre);
 #pragma unroll
             for (int e = 0; e < 32; ++e) x[e] *= detail::gelu_grad_f<F32>(pre[e]);
-          } else if (last && (args.flags & EF_GELU_BWD) && row_ok) {
+          } else if (last && (uflags & EF_GELU_BWD) && row_ok) {
 #pragma unroll
             for (int g = 0; g < 4; ++g)
-              if (nc + g * 8 < args.N) {
+              if (nc + g * 8 < uN) {
                 float pre[8];
-                detail::load8<F32>(args.aux, row * args.ld_aux + nc + g * 8, pre);
+                detail::load8<F32>(uaux, row * args.ld_aux + nc + g * 8, pre);
 #pragma unroll
                 for (int e = 0; e < 8; ++e) x[g * 8 + e] *= detail::gelu_grad_f<F32>(pre[e]);
               }
@@ -704,22 +808,45 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
         __syncwarp();
         if (lane == 0) {
           if constexpr (Cfg::EPI == EPI_FWD) {
-            if (args.flags & EF_STORE_PRE) tma_store_2d(&maps.c0, stg0, nc, row0);
-            if (args.flags & EF_GELU) tma_store_2d(&maps.c1, stg1, nc, row0);
+            if (part2) {
+              if (split == 0)
+                tma_store_2d(&mp.c1, stg0, nc, row0);  // workspace = partial 0
+              else
+                tma_reduce_add_2d(&mp.c1, stg0, nc, row0);  // workspace += partial s
+            } else {
+              if (uflags & EF_STORE_PRE) tma_store_2d(&mp.c0, stg0, nc, row0);
+              if (uflags & EF_GELU) tma_store_2d(&mp.c1, stg1, nc, row0);
+            }
           } else if constexpr (Cfg::EPI == EPI_DGRAD) {
             if (last || first)
-              tma_store_2d(&maps.c0, stg0, nc, row0);  // dX (dtype) or first partial (fp32)
+              tma_store_2d(&mp.c0, stg0, nc, row0);  // dX (dtype) or first partial (fp32)
             else
-              tma_reduce_add_2d(&maps.c0, stg0, nc, row0);  // acc += partial, in L2
+              tma_reduce_add_2d(&mp.c0, stg0, nc, row0);  // acc += partial, in L2
           } else {
+#ifdef RTPB_WGRAD_STORE  // dev A/B: timing only, results wrong
+            if (true)
+#else
             if (first && split == 0)
-              tma_store_2d(&maps.c0, stg0, nc, row0);  // G known zero: G = dW tile (split 0 lands first)
+#endif
+              tma_store_2d(&mp.c0, stg0, nc, row0);  // G known zero: G = dW tile (split 0 lands first)
             else
-              tma_reduce_add_2d(&maps.c0, stg0, nc, row0);  // travelling G += dW tile
+              tma_reduce_add_2d(&mp.c0, stg0, nc, row0);  // travelling G += dW tile
           }
           bulk_commit();
         }
         pending = true;
+      }
+      if (split2) {
+        // publish (tile, split) done; the last arrival of the last split re-zeroes
+        if (lane == 0) {
+          bulk_wait0();
+          asm volatile("fence.proxy.async.global;" ::: "memory");
+          __threadfence();
+          const unsigned old = atomicAdd(args.split_flags2 + t, 1u);
+          if (old + 1 == unsigned(splits2 * wgroup)) args.split_flags2[t] = 0u;
+        }
+        __syncwarp();
+        pending = false;
       }
       if constexpr (Cfg::EPI == EPI_WGRAD) {
         if (splits > 1) {
@@ -745,6 +872,18 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
         acc = 0;
         acc_phase ^= 1;
       }
+      if (args.dep_count && x_.prob == 0) {
+        // publish: this warp's stores of the tile are complete (problem 1
+        // reads them as its A operand), after the accumulator was released
+        if (lane == 0) {
+          bulk_wait0();
+          asm volatile("fence.proxy.async.global;" ::: "memory");
+          __threadfence();
+          atomicAdd(args.dep_count + mb, 1u);
+        }
+        __syncwarp();
+        pending = false;
+      }
     }
     if (lane == 0) bulk_wait0();
     __syncwarp();
@@ -768,11 +907,9 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
     const int contributors = num_m * splits;
     int stage = 0;
     uint32_t phase = 0;
-    for (int u = unit; u < num_units; u += units) {
-      const int t = u % num_tiles, split = u / num_tiles;
-      int mb, nb, kb0, kb1;
-      tile_coords(t, mb, nb);
-      unit_kb(u, kb0, kb1);
+    for (int it = it_beg; it < it_end; it += it_step) {
+      const Unit x_ = decode(it);
+      const int split = x_.split, mb = x_.mb, nb = x_.nb, kb0 = x_.kb0, kb1 = x_.kb1;
       float sum[8];
 #pragma unroll
       for (int e = 0; e < 8; ++e) sum[e] = 0.f;
@@ -843,16 +980,60 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
         }
         last = __shfl_sync(0xffffffffu, last, 0);
         __syncwarp();
-        if (last && lane < LPR) {
-          // every contributor's partial is visible: sum them in (split, mb) order
+        if (last) {
+          // Every contributor's partial is visible. All 32 lanes help: lane
+          // group g = lane / LPR sums contributors r = g, g + G, ... in
+          // ascending order (loads of 4 contributors in flight at a time,
+          // float4-wide), then the G group sums are added in group order:
+          // a fixed order, so the result is bitwise reproducible. (A serial
+          // per-column loop here held the stage release of this CTA's next
+          // unit for tens of microseconds.)
+          constexpr int G = 32 / LPR;
+          const int grp = lane / LPR, cl = cg * Cfg::B_ROWS + (lane % LPR) * 8;
+          float4 s0 = make_float4(0.f, 0.f, 0.f, 0.f), s1 = s0;
+          if (cl < args.N) {
+            const float* base = args.bias_part + cl;
+            int r = grp;
+            for (; r + 3 * G < contributors; r += 4 * G) {
+              float4 v[8];
 #pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            const int c = c0 + e;
-            if (c < args.N) {
-              float acc = 0.f;
-              for (int r = 0; r < contributors; ++r) acc += __ldcg(args.bias_part + size_t(r) * args.N + c);
-              args.gbias_out[c] = (first ? 0.f : __ldcg(args.gbias_in + c)) + acc;
+              for (int q = 0; q < 4; ++q) {
+                const float4* p = reinterpret_cast<const float4*>(base + size_t(r + q * G) * args.N);
+                v[2 * q] = __ldcg(p);
+                v[2 * q + 1] = __ldcg(p + 1);
+              }
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                s0.x += v[2 * q].x; s0.y += v[2 * q].y; s0.z += v[2 * q].z; s0.w += v[2 * q].w;
+                s1.x += v[2 * q + 1].x; s1.y += v[2 * q + 1].y; s1.z += v[2 * q + 1].z; s1.w += v[2 * q + 1].w;
+              }
             }
+            for (; r < contributors; r += G) {
+              const float4* p = reinterpret_cast<const float4*>(base + size_t(r) * args.N);
+              const float4 a = __ldcg(p), b = __ldcg(p + 1);
+              s0.x += a.x; s0.y += a.y; s0.z += a.z; s0.w += a.w;
+              s1.x += b.x; s1.y += b.y; s1.z += b.z; s1.w += b.w;
+            }
+          }
+          const float4 t0 = s0, t1 = s1;  // group sums, read unmodified by the shuffles
+#pragma unroll
+          for (int g = 1; g < G; ++g) {
+            const int src = (lane + g * LPR) & 31;
+            s0.x += __shfl_sync(0xffffffffu, t0.x, src); s0.y += __shfl_sync(0xffffffffu, t0.y, src);
+            s0.z += __shfl_sync(0xffffffffu, t0.z, src); s0.w += __shfl_sync(0xffffffffu, t0.w, src);
+            s1.x += __shfl_sync(0xffffffffu, t1.x, src); s1.y += __shfl_sync(0xffffffffu, t1.y, src);
+            s1.z += __shfl_sync(0xffffffffu, t1.z, src); s1.w += __shfl_sync(0xffffffffu, t1.w, src);
+          }
+          if (lane < LPR && cl < args.N) {
+            float4* o = reinterpret_cast<float4*>(args.gbias_out + cl);
+            if (!first) {
+              const float4* gi = reinterpret_cast<const float4*>(args.gbias_in + cl);
+              const float4 a = __ldcg(gi), b = __ldcg(gi + 1);
+              s0 = make_float4(a.x + s0.x, a.y + s0.y, a.z + s0.z, a.w + s0.w);
+              s1 = make_float4(b.x + s1.x, b.y + s1.y, b.z + s1.z, b.w + s1.w);
+            }
+            o[0] = s0;
+            o[1] = s1;
           }
         }
       }
@@ -871,6 +1052,16 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
       tmem_dealloc_pair(tmem_base, Cfg::TMEM_COLS);
     else
       tmem_dealloc(tmem_base, Cfg::TMEM_COLS);
+  }
+  if (args.dep_count && threadIdx.x == 0) {
+    // every thread of this CTA is past its last dependency read: the last CTA
+    // out re-zeroes the row-block counters for the next launch
+    __threadfence();
+    if (atomicAdd(args.done_ctas, 1u) == gridDim.x - 1) {
+      for (int r = 0; r < args.dep_rows; ++r) args.dep_count[r] = 0u;
+      *args.done_ctas = 0u;
+      __threadfence();
+    }
   }
 }
 

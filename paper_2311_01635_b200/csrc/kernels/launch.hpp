@@ -4,6 +4,7 @@
 
 #include <cstddef>
 #include <cstdint>
+#include <vector>
 
 #include "../../../include/rtpb.h"
 
@@ -52,6 +53,34 @@ struct StepWgrad {
 bool wgrad_fuses_bias(bool f32, size_t M, size_t I, size_t per, unsigned* split_flags, int force_bn);
 
 int gemm_fwd(bool f32, const StepFwd& p, cudaStream_t s);
+// Fused N = 1 MLP forward (ffn1 + GELU and ffn2 in one scheduled launch).
+struct FusedFwdPlan {
+  std::vector<int> sched;  // [slots + 1 offsets][unit codes], uploaded by the caller
+  int slots = 0;           // CTA pairs the schedule is built for
+  int dep_rows = 0;        // row-block counters (zeroed device memory, self-resetting)
+  unsigned dep_target = 0;
+  int k_splits2 = 1;       // ffn2 K splits (> 1: fp32 partials in acc2, ordered)
+  int tiles2 = 0;          // ffn2 tiles (split counters)
+  double est_us = 0;       // cost-model makespan
+};
+// Device workspace of the fused forward: zero-filled once, then self-resetting.
+struct FusedFwdWs {
+  const int* sched;
+  unsigned* dep_count;     // [dep_rows]
+  unsigned* done_ctas;     // [1]
+  unsigned* split_flags2;  // [tiles2]
+  float* acc2;             // M x h fp32 (k_splits2 > 1)
+};
+bool plan_fused_fwd(size_t M, size_t h, size_t f, FusedFwdPlan& plan);
+int gemm_fwd_fused(const StepFwd& p0, const StepFwd& p1, const FusedFwdPlan& plan, const FusedFwdWs& ws,
+                   cudaStream_t s);
+
+// The fused forward as a step (capi_steps.cu): bf16, shards [W | b];
+// store_pre: also write pre (Train). Timed as one fwd launch when profiling.
+int fused_fwd_step(const void* x, size_t ldx, const void* w1_shard, void* pre, void* act, const void* w2_shard,
+                   void* y, size_t ldy, size_t M, size_t h, size_t f, bool store_pre, const FusedFwdPlan& plan,
+                   const FusedFwdWs& ws, cudaStream_t s);
+
 // Caps the SMs the calling thread's following GEMM launches occupy (0 = all);
 // sm_budget() returns the effective count.
 void set_sm_budget(int sms);

@@ -3,6 +3,7 @@ for ncu captures (-k regex:rtp_gemm -s 3 -c 3) and quick timing.
 
 python tools/gemm_one.py M I per [kinds=fwd,dgrad,wgrad] [tile code]
 """
+import os
 import sys
 
 import torch
@@ -21,9 +22,28 @@ Y = torch.empty(M, per, dtype=torch.bfloat16, device=dev)
 dY = torch.randn(M, per, device=dev).to(torch.bfloat16)
 dX = torch.empty(M, I, dtype=torch.bfloat16, device=dev)
 G = torch.zeros(I * per + per, dtype=torch.float32, device=dev)
+Hh = torch.empty(M, per, dtype=torch.bfloat16, device=dev)
+pre = torch.randn(M, I, device=dev).to(torch.bfloat16)
 fns = {"fwd": lambda: rtp.fwd_step(X, sh, Y, 0, per),
+       "fwd_gelu": lambda: rtp.fwd_step(X, sh, Y, 0, per, act=Hh),
+       "fwd_actonly": lambda: rtp.fwd_step(X, sh, None, 0, per, act=Hh, store_pre=False),
+       "dgrad_gelu": lambda: rtp.dgrad_step(dY, 0, sh, None, dX, M, I, per, True, True, pre=pre),
        "dgrad": lambda: rtp.dgrad_step(dY, 0, sh, None, dX, M, I, per, True, True),
        "wgrad": lambda: rtp.wgrad_step(X, dY, 0, G, G, per)}
+if "wgrad_as_dgrad" in kinds:  # the dW product on the dgrad kernel: X^T (I x M) . (dY^T (per x M))^T
+    XT2 = X.t().contiguous()
+    WT = torch.empty(per * M + M, dtype=torch.bfloat16, device=dev)
+    WT[:per * M].view(per, M).copy_(dY.t())
+    OUT = torch.empty(I, per, dtype=torch.bfloat16, device=dev)
+    fns["wgrad_as_dgrad"] = lambda: rtp.dgrad_step(XT2, 0, WT, None, OUT, I, per, M, True, True)
+if "wgrad_t" in kinds:  # needs an RTPB_WGRAD_KMAJOR_PROBE build: X^T (I x M) and dY^T (per x M)
+    import ctypes as C
+    XT, dYT = X.t().contiguous(), dY.t().contiguous()
+    ws = rtp._ws(2, 0, M, I, per, X.device)
+    fns["wgrad_t"] = lambda: _lib.check(_lib.lib.rtpb_wgrad_step(0, XT.data_ptr(), M, dYT.data_ptr(), M, 0,
+                                                                 G.data_ptr(), G.data_ptr(), M, I, per,
+                                                                 ws.data_ptr(), ws.numel(),
+                                                                 torch.cuda.current_stream().cuda_stream))
 fl = 2.0 * M * I * per
 for k in kinds:
     f = fns[k]
@@ -38,3 +58,30 @@ for k in kinds:
     torch.cuda.synchronize()
     us = a.elapsed_time(b) / 10 * 1e3
     print(f"{k:6s} M={M} I={I} per={per} tile={code}: {us:8.1f} us {fl / us / 1e6:6.0f} TF/s", flush=True)
+
+if os.environ.get("TRACE"):
+    import numpy as np
+    STRIDE, UNITS = 80, 13
+    for k in kinds:
+        buf = torch.zeros(148 * STRIDE + 64, dtype=torch.int64, device=dev)
+        torch.cuda.synchronize()
+        _lib.lib.rtpb_debug_trace(buf.data_ptr(), buf.numel() * 8)
+        fns[k]()
+        torch.cuda.synchronize()
+        _lib.lib.rtpb_debug_trace(None, 0)
+        tr = buf.cpu().numpy().astype(np.float64)
+        g = int(tr[STRIDE - 1]) if 0 < tr[STRIDE - 1] <= 148 else 148
+        blk = tr[:g * STRIDE].reshape(g, STRIDE)
+        t0 = blk[:, 0].min()
+        u = blk[:, 2:2 + 6 * UNITS].reshape(g, UNITS, 6)
+        lead = u[:, :, 2] > 0
+        epi = u[:, :, 4] > 0
+        ml = (u[:, :, 3] - u[:, :, 2])[lead] / 1e3
+        ep = (u[:, :, 5] - u[:, :, 4])[epi] / 1e3
+        accw = (u[:, :, 1] - u[:, :, 0])[lead] / 1e3
+        # gap between a unit's last commit and the next unit's first stage (same CTA)
+        ends = np.where(epi, u[:, :, 5], 0).max(1)
+        print(f"  trace {k}: grid {g} units/CTA {epi.sum(1).min()}..{epi.sum(1).max()} mainloop {ml.mean():.2f} "
+              f"(min {ml.min():.2f} max {ml.max():.2f}) us  epilogue {ep.mean():.2f} (max {ep.max():.2f})  acc-wait "
+              f"{accw.mean():.2f} (max {accw.max():.2f})  span {(ends.max() - t0) / 1e3:.1f}  first-stage "
+              f"{(np.where(lead, u[:, :, 2], np.inf).min() - t0) / 1e3:.2f}")

@@ -16,7 +16,9 @@ STRIDE, UNITS = 80, 13
 M = int(sys.argv[1]) if len(sys.argv) > 1 else 8192
 H = int(sys.argv[2]) if len(sys.argv) > 2 else 768
 F = int(sys.argv[3]) if len(sys.argv) > 3 else 3072
-NAMES = ["fwd1", "fwd2", "dgrad2", "wgrad2", "dgrad1", "wgrad1"]
+import os
+NAMES = (["fwd1", "fwd2", "dgrad2", "wgrad2", "dgrad1", "wgrad1"] if os.environ.get("RTPB_NO_FUSED_FWD")
+         else ["fwd1+fwd2", "dgrad2", "wgrad2", "dgrad1", "wgrad1"])
 
 dev = torch.device("cuda", 0)
 grp = rtp.WorkerGroup(1)
@@ -78,6 +80,10 @@ for li, name in enumerate(NAMES):
             if mma_lead[c, i] and epi[c, i]:
                 lat.append(u[c, i, 4] - u[c, i, 3])
     units_per_cta = epi.sum(1)
+    if os.environ.get("UNITS") and li == 0:
+        for c in range(0, g, 2):
+            print("   cta", c, " ".join(f"[{rel(u[c, i, 2]):.1f}>{rel(u[c, i, 4]):.1f}:{rel(u[c, i, 5]):.1f}]"
+                                      for i in range(UNITS) if u[c, i, 2] > 0))
     print(f"{name:7s} grid {g:3d} entry {rel(entry.min()):7.1f}..{rel(entry.max()):7.1f}  griddep_wait done "
           f"{rel(gdw.min()):7.1f}..{rel(gdw.max()):7.1f}  first stage {rel(first_mma):7.1f}  last epi done "
           f"{rel(last_epi):7.1f}  span {(last_epi - entry.min()) / 1e3:6.1f}")
