@@ -126,6 +126,10 @@ size_t rtpb_profile_read(int* kinds, double* flops, float* ms, float* start_ms, 
  * Lets a caller run two step GEMMs side by side on two streams. */
 void rtpb_set_sm_budget(int sms);
 
+/* Debug: cost-model makespan (us) of the fused N = 1 MLP schedule for rows M,
+ * hidden h, ffn f: which 0 = forward, 1 = backward (-1 if no plan). */
+double rtpb_debug_fused_plan(size_t M, size_t h, size_t f, int which);
+
 /* Test hook: force the GEMM tile width (0 = heuristic; 64/128/256). */
 void rtpb_debug_force_bn(int bn);
 /* Debug hook: the following step-GEMM launches write per-CTA %globaltimer

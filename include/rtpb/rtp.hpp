@@ -318,6 +318,18 @@ class RtpLinear : public RtpLayerBase {
   // shard [W_0 | b_0] for a caller that issues the GEMM itself (RtpMlp's
   // fused forward).
   const void* begin_forward_n1(const DView& x, size_t rows, Mode mode);
+  // N = 1 backward for a caller that issues the GEMMs itself (RtpMlp's fused
+  // backward): replay / position checks and trace, then what the step needs.
+  struct N1Bwd {
+    const void* weight;  // resident shard [W | b]
+    float* grad;         // resident gradient shard (fp32)
+    bool grad_zero;      // zero_grads() pending: overwrite instead of accumulate
+    DView x;             // X cached by forward
+    void* workspace;
+    size_t workspace_bytes;
+  };
+  N1Bwd begin_backward_n1(size_t rows);
+  void end_backward_n1();
 
  private:
   void build(size_t in_dim, size_t out_dim, size_t n);
@@ -364,6 +376,12 @@ class RtpMlp {
   int fused_slots_ = 0, fused_dep_rows_ = 0, fused_splits2_ = 1, fused_tiles2_ = 0;
   unsigned fused_dep_target_ = 0;
   size_t fused_sched_ints_ = 0, fused_acc_off_ = 0;
+  // N = 1 fused backward: D / W schedules + shared row-block counters.
+  void ensure_fused_bwd(size_t rows);
+  DeviceBuffer fused_bwd_ws_;
+  size_t fused_bwd_rows_ = 0, fused_bwd_sd_ints_ = 0, fused_bwd_sw_ints_ = 0;
+  int fused_bwd_slots_d_ = 0, fused_bwd_slots_w_ = 0, fused_bwd_dep_rows_ = 0;
+  unsigned fused_bwd_dep_target_ = 0;
 };
 
 // Host fp64 -> device dtype, round-to-nearest-even from the double (no

@@ -37,6 +37,7 @@ _SIGS = {
     "rtpb_profile_read": (_sz, [C.POINTER(_int), C.POINTER(_dbl), C.POINTER(C.c_float), C.POINTER(C.c_float),
                                 C.POINTER(_int), _sz]),
     "rtpb_set_sm_budget": (None, [_int]),
+    "rtpb_debug_fused_plan": (_dbl, [_sz, _sz, _sz, _int]),
     "rtpb_step_workspace_bytes": (_sz, [_int, _int, _sz, _sz, _sz]),
     "rtpb_flyweight_init": (_int, [_vp, _int, _u64, _u64, _sz, _sz, _sz, _sz, _dbl, _dbl, _vp]),
     "rtpb_fwd_step": (_int, [_int, _vp, _sz, _vp, _vp, _sz, _sz, _vp, _sz, _sz, _sz, _sz, _int, _vp, _sz, _vp]),

@@ -139,6 +139,44 @@ int fused_fwd_step(const void* x, size_t ldx, const void* w1_shard, void* pre, v
   return timed(0, 4.0 * M * h * f, s, [&] { return gemm_fwd_fused(p0, p1, plan, ws, s); });
 }
 
+int fused_bwd_step(FusedBwdArgs a, void* ws1, size_t ws1_bytes, void* ws2, size_t ws2_bytes,
+                   const FusedBwdPlan& plan, const FusedBwdWs& ws, cudaStream_t compute, cudaStream_t aux) {
+  int rc;
+  if ((rc = check_geom(a.M, a.h, a.f))) return rc;
+  // each layer's persistent workspace part, carved as rtpb_wgrad_step does
+  auto carve = [&](void* w, size_t bytes, size_t I, size_t per, float** part, unsigned** tick, unsigned** flags) {
+    Carve c{static_cast<char*>(w), w ? bytes : 0};
+    c.take(colsum_workspace_bytes(a.M, per) / sizeof(float));
+    *flags = reinterpret_cast<unsigned*>(c.take(split_flag_bytes(I, per) / sizeof(float)));
+    *tick = reinterpret_cast<unsigned*>(c.take(bias_tick_bytes(per) / sizeof(float)));
+    *part = c.take(bias_part_bytes(I, per) / sizeof(float));
+    return c.ok;
+  };
+  if (!carve(ws1, ws1_bytes, a.h, a.f, &a.bias_part1, &a.bias_tick1, &a.split_flags1) ||
+      !carve(ws2, ws2_bytes, a.f, a.h, &a.bias_part2, &a.bias_tick2, &a.split_flags2))
+    return set_error(RTPB_ERR_DIMENSION, "fused backward: layer workspace too small");
+  // profiled as the two launches: D (both dX GEMMs) and W (both dW GEMMs)
+  const double fl = 2.0 * double(a.M) * double(a.h) * double(a.f) * 2.0;
+  if (!g_prof_on) return gemm_bwd_fused(a, plan, ws, compute, aux);
+  cudaEvent_t e[4];
+  {
+    std::lock_guard lk(g_prof_mu);
+    for (auto& x : e) x = prof_event();
+  }
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(compute, &cap);
+  const unsigned flg = cap == cudaStreamCaptureStatusActive ? cudaEventRecordExternal : cudaEventRecordDefault;
+  cudaEventRecordWithFlags(e[0], compute, flg);
+  cudaEventRecordWithFlags(e[2], aux, flg);
+  rc = gemm_bwd_fused(a, plan, ws, compute, aux);
+  cudaEventRecordWithFlags(e[1], compute, flg);
+  cudaEventRecordWithFlags(e[3], aux, flg);
+  std::lock_guard lk(g_prof_mu);
+  g_prof.push_back({1, fl, e[0], e[1], 2 * plan.slots_d});
+  g_prof.push_back({2, fl, e[2], e[3], 2 * plan.slots_w});
+  return rc;
+}
+
 }  // namespace rtpb
 
 using namespace rtpb;
@@ -150,6 +188,15 @@ const char* rtpb_version(void) { return "rtpb 0.1 (sm_100a tcgen05)"; }
 uint64_t rtpb_launch_count(void) { return g_launches.load(); }
 void rtpb_debug_force_bn(int bn) { g_force_bn = bn; }
 void rtpb_set_sm_budget(int sms) { set_sm_budget(sms); }
+
+double rtpb_debug_fused_plan(size_t M, size_t h, size_t f, int which) {
+  if (which == 0) {
+    FusedFwdPlan p;
+    return plan_fused_fwd(M, h, f, p) ? p.est_us : -1.0;
+  }
+  FusedBwdPlan p;
+  return plan_fused_bwd(M, h, f, p) ? p.est_us : -1.0;
+}
 void rtpb_debug_trace(void* device_buf, size_t bytes) { set_trace(device_buf, bytes); }
 
 // Workspace layout, identical for every step kind of a layer so one buffer

@@ -321,6 +321,25 @@ const void* RtpLinear::begin_forward_n1(const DView& x, size_t rows, Mode mode) 
   return slots_[r].weight.data();
 }
 
+RtpLinear::N1Bwd RtpLinear::begin_backward_n1(size_t rows) {
+  if (group_->size() != 1) throw StateError(label_ + ": begin_backward_n1 needs a single-worker group");
+  const size_t r = group_->local_ranks()[0];
+  if (tapes_[r].empty()) throw StateError("backward invoked without a matching forward");
+  if (rows != cached_rows_) throw DimensionError(label_ + ": backward rows differ from the cached forward");
+  const size_t j = slots_[r].logical_id;
+  tapes_[r].replay(j);
+  check_backward_position(r, 0);
+  trace_[1] = int64_t(j);
+  return {slots_[r].weight.data(), static_cast<float*>(slots_[r].grad_acc.data()), grads_zero_pending_,
+          x_cache_[r], workspace_[r].data(), workspace_[r].bytes()};
+}
+
+void RtpLinear::end_backward_n1() {
+  grads_zero_pending_ = false;
+  for (size_t r : group_->local_ranks()) x_cache_[r] = {};
+  require_home("end of backward");
+}
+
 void RtpLinear::backward_ex(std::span<const DView> dy, size_t rows, std::span<const DView> dx, const BwdEpi& e) {
   const auto& local = group_->local_ranks();
   if (dy.size() != local.size() || dx.size() != local.size())
@@ -569,7 +588,66 @@ void RtpMlp::forward(std::span<const DView> x, size_t rows, std::span<const DVie
   ffn2_->forward(act, rows, y, mode);  // model.cpp:83
 }
 
+void RtpMlp::ensure_fused_bwd(size_t rows) {
+  if (rows == fused_bwd_rows_) return;
+  FusedBwdPlan plan;
+  if (!plan_fused_bwd(rows, h_, f_, plan)) throw ConfigError("RtpMlp: no fused backward schedule for this shape");
+  group_->synchronize();
+  const size_t r = group_->local_ranks()[0];
+  Worker& w = group_->worker(r);
+  fused_bwd_sd_ints_ = plan.sched_d.size();
+  fused_bwd_sw_ints_ = plan.sched_w.size();
+  const size_t ints = fused_bwd_sd_ints_ + fused_bwd_sw_ints_ + size_t(plan.dep_rows) + 1;
+  fused_bwd_ws_ = DeviceBuffer(w.device, ints * sizeof(int), &w.ledger, MemCategory::Other, true);
+  int* base = static_cast<int*>(fused_bwd_ws_.data());
+  cuda_check(cudaMemcpy(base, plan.sched_d.data(), fused_bwd_sd_ints_ * sizeof(int), cudaMemcpyHostToDevice),
+             "upload fused schedule");
+  cuda_check(cudaMemcpy(base + fused_bwd_sd_ints_, plan.sched_w.data(), fused_bwd_sw_ints_ * sizeof(int),
+                        cudaMemcpyHostToDevice),
+             "upload fused schedule");
+  fused_bwd_slots_d_ = plan.slots_d;
+  fused_bwd_slots_w_ = plan.slots_w;
+  fused_bwd_dep_rows_ = plan.dep_rows;
+  fused_bwd_dep_target_ = plan.dep_target;
+  fused_bwd_rows_ = rows;
+}
+
 void RtpMlp::backward(std::span<const DView> dy, size_t rows, std::span<const DView> dx) {
+  if (group_->size() == 1 && dtype_ == DType::BF16 && !std::getenv("RTPB_NO_FUSED_BWD")) {
+    // N = 1: the four backward GEMMs as two concurrent scheduled launches
+    // (dX chain on compute, dW pair on aux); ffn1's dW streams dpre row blocks
+    // as the dX launch publishes them.
+    if (dy.size() != 1 || dx.size() != 1) throw DimensionError("RtpMlp: backward expects one gradient per worker");
+    const size_t r = group_->local_ranks()[0];
+    ensure_fused_bwd(rows);
+    const RtpLinear::N1Bwd b2 = ffn2_->begin_backward_n1(rows);
+    const RtpLinear::N1Bwd b1 = ffn1_->begin_backward_n1(rows);
+    Worker& w = group_->worker(r);
+    FusedBwdArgs a{};
+    a.dy = dy[0].data; a.ldy = dy[0].ld ? dy[0].ld : h_;
+    a.act = b2.x.data;
+    a.x = b1.x.data; a.ldx = b1.x.ld ? b1.x.ld : h_;
+    a.pre = pre_[r].data();
+    a.dx = dx[0].data; a.lddx = dx[0].ld ? dx[0].ld : h_;
+    a.w1 = b1.weight; a.w2 = b2.weight;
+    a.g1 = b1.grad; a.g2 = b2.grad; a.g1_zero = b1.grad_zero; a.g2_zero = b2.grad_zero;
+    a.M = rows; a.h = h_; a.f = f_;
+    int* base = static_cast<int*>(fused_bwd_ws_.data());
+    unsigned* dep = reinterpret_cast<unsigned*>(base + fused_bwd_sd_ints_ + fused_bwd_sw_ints_);
+    FusedBwdPlan plan;
+    plan.slots_d = fused_bwd_slots_d_;
+    plan.slots_w = fused_bwd_slots_w_;
+    plan.dep_rows = fused_bwd_dep_rows_;
+    plan.dep_target = fused_bwd_dep_target_;
+    FusedBwdWs ws{base, base + fused_bwd_sd_ints_, dep, dep + fused_bwd_dep_rows_};
+    w.fork_aux();  // aux: dY, act, X and pre are complete
+    check_status(fused_bwd_step(a, b1.workspace, b1.workspace_bytes, b2.workspace, b2.workspace_bytes, plan, ws,
+                                w.compute, w.aux));
+    ffn2_->end_backward_n1();
+    ffn1_->end_backward_n1();
+    group_->join_aux();
+    return;
+  }
   const auto& local = group_->local_ranks();
   std::vector<DView> pre(local.size());
   for (size_t k = 0; k < local.size(); ++k) pre[k] = {pre_[local[k]].data(), f_};

@@ -297,10 +297,202 @@ namespace {
 constexpr int kFusedBN = 256;
 using FusedFwdCfg = GemmCfg<EPI_FWD, kFusedBN, false, kEpiWarps, false, true, false, true>;
 
-double fused_unit_cost(size_t K, int outputs) {
-  // us per 256 x 256 pair tile: ~0.36 us per 64-deep K block when TMA-fed
-  // from L2, plus the epilogue share that does not hide under the next tile
-  return double((K + 63) / 64) * 0.36 + 0.4 + 0.3 * outputs;
+// Cost model of a 256 x 256 CTA-pair tile (us), calibrated on config (b)
+// step traces (tools/timeline.py): ~0.36 us per 64-deep K block when TMA-fed
+// from L2, plus ~0.85 us per bf16-tile-equivalent written by the epilogue
+// (the tile's share of the SM's L2 port), plus a fixed ~0.4 us.
+double tile_cost(size_t K, double outputs) { return double((K + 63) / 64) * 0.36 + 0.85 * outputs + 0.4; }
+
+// Two problems on P unit slots. Problem 0: T0 tiles in order (n fastest, n0
+// per row block). Problem 1: T1 tiles x S1 K-splits (consecutive units; the
+// epilogue of split s follows split s - 1), ready when their row block of
+// problem 0 is done (dep 1), when the rows of their K range have been
+// published by another launch (dep 2, ext_ready per 256-row block), or at once.
+struct TwoProb {
+  int T0 = 0, n0 = 0;
+  double c0 = 0;
+  int T1 = 0, n1 = 0, S1 = 1;
+  double c1 = 0;
+  int dep = 0;
+  const std::vector<double>* ext_ready = nullptr;
+  size_t K1 = 0;  // dep 2: problem 1's K (rows of the producing launch)
+};
+
+// Greedy list schedule (earliest-free slot takes the next unit). alpha trades
+// the two problems: a ready problem-1 unit is taken while its completed
+// fraction is <= alpha x problem 0's (alpha < 0: only once problem 0 is
+// exhausted). Each slot's list is in simulated start order, which makes the
+// kernel's waits deadlock-free. Returns the makespan.
+double list_schedule(int P, const TwoProb& q, double alpha, std::vector<int>& sched,
+                     std::vector<double>* row_ready_out = nullptr) {
+  std::vector<std::vector<int>> lists(static_cast<size_t>(P));
+  std::vector<double> free_at(static_cast<size_t>(P), 0.0);
+  const int nm = q.n0 ? (q.T0 + q.n0 - 1) / q.n0 : 1;
+  std::vector<double> row_ready(size_t(nm), 0.0);
+  std::vector<int> row_left(size_t(nm), q.n0);
+  std::vector<int> ready_rows;
+  std::vector<double> split_fin(size_t(std::max(q.T1, 1)), 0.0);
+  size_t r1 = 0;
+  int r1_u = 0, next0 = 0, next1 = 0, taken1 = 0;
+  const int U1 = q.T1 * q.S1;
+  double makespan = 0;
+  for (int done = 0; done < q.T0 + U1; ++done) {
+    int p = 0;
+    for (int i = 1; i < P; ++i)
+      if (free_at[size_t(i)] < free_at[size_t(p)]) p = i;
+    const double tp = free_at[size_t(p)];
+    // candidate problem-1 unit and its readiness
+    int t1 = -1, sp = 0;
+    double rdy = 0.0;
+    if (q.dep == 1) {
+      if (r1 < ready_rows.size()) {
+        const int mb = ready_rows[r1];
+        t1 = mb * q.n1 + r1_u / q.S1;
+        sp = r1_u % q.S1;
+        rdy = row_ready[size_t(mb)];
+      }
+    } else if (next1 < U1) {
+      t1 = next1 / q.S1;
+      sp = next1 % q.S1;
+      if (q.dep == 2 && q.ext_ready && !q.ext_ready->empty()) {
+        const size_t rows_per = (q.K1 + size_t(q.S1) - 1) / size_t(q.S1);
+        const size_t r_hi = std::min(q.K1, rows_per * size_t(sp + 1));
+        const size_t rb = std::min(q.ext_ready->size() - 1, (r_hi ? r_hi - 1 : 0) / 256);
+        rdy = (*q.ext_ready)[rb] - 0.9 * q.c1;  // K blocks stream in as rows land
+      }
+    }
+    const double f0 = q.T0 ? double(next0) / q.T0 : 1.0, f1 = U1 ? double(taken1) / U1 : 1.0;
+    bool take1 = false;
+    if (next0 >= q.T0) take1 = true;
+    else if (t1 >= 0 && rdy <= tp && alpha >= 0 && f1 <= alpha * f0) take1 = true;
+    double fin;
+    if (take1) {
+      fin = std::max(tp, rdy) + q.c1;
+      if (sp > 0) fin = std::max(fin, split_fin[size_t(t1)] + 0.5);
+      split_fin[size_t(t1)] = fin;
+      lists[size_t(p)].push_back((1 << 28) | (sp << 20) | t1);
+      ++taken1;
+      if (q.dep == 1) {
+        if (++r1_u == q.n1 * q.S1) {
+          r1_u = 0;
+          ++r1;
+        }
+      } else {
+        ++next1;
+      }
+    } else {
+      const int t = next0++;
+      fin = tp + q.c0;
+      lists[size_t(p)].push_back(t);
+      if (q.n0) {
+        const int mb = t / q.n0;
+        row_ready[size_t(mb)] = std::max(row_ready[size_t(mb)], fin);
+        if (--row_left[size_t(mb)] == 0) ready_rows.push_back(mb);
+      }
+    }
+    free_at[size_t(p)] = fin;
+    makespan = std::max(makespan, fin);
+  }
+  sched.assign(size_t(P) + 1, 0);
+  int off = P + 1;
+  for (int i = 0; i < P; ++i) {
+    sched[size_t(i)] = off;
+    off += int(lists[size_t(i)].size());
+  }
+  sched[size_t(P)] = off;
+  for (int i = 0; i < P; ++i) sched.insert(sched.end(), lists[size_t(i)].begin(), lists[size_t(i)].end());
+  if (row_ready_out) *row_ready_out = row_ready;
+  return makespan;
+}
+
+// The same problem scheduled backwards in time (dep 1, S1 = 1): the long
+// problem-1 tiles are placed first, then each row block's problem-0 tiles once
+// all of that row block's problem-1 tiles are placed; reversing every slot's
+// list gives a valid forward schedule whose ragged edge falls on the start,
+// among the short problem-0 tiles, instead of on the final long tiles.
+double list_schedule_reverse(int P, const TwoProb& q, std::vector<int>& sched, std::vector<double>* row_ready_out) {
+  const int nm = q.n0 ? (q.T0 + q.n0 - 1) / q.n0 : 1;
+  std::vector<std::vector<std::pair<double, int>>> lists(static_cast<size_t>(P));  // (rev start, code)
+  std::vector<double> free_at(static_cast<size_t>(P), 0.0);
+  std::vector<double> row_rel(size_t(nm), 0.0);  // rev time all problem-1 tiles of the row are done
+  std::vector<int> row_left1(size_t(nm), q.n1);
+  std::vector<int> released;  // row blocks in release order
+  size_t rel_i = 0;
+  int rel_nb = 0, next1 = 0;
+  double makespan = 0;
+  for (int done = 0; done < q.T0 + q.T1; ++done) {
+    int p = 0;
+    for (int i = 1; i < P; ++i)
+      if (free_at[size_t(i)] < free_at[size_t(p)]) p = i;
+    const double tp = free_at[size_t(p)];
+    double start, fin;
+    if (next1 < q.T1) {
+      const int t = next1++, mb = t / q.n1;
+      start = tp;
+      fin = start + q.c1;
+      lists[size_t(p)].push_back({start, (1 << 28) | t});
+      row_rel[size_t(mb)] = std::max(row_rel[size_t(mb)], fin);
+      if (--row_left1[size_t(mb)] == 0) released.push_back(mb);
+    } else {
+      // problem-1 tiles all placed: rows are released in order of their release time
+      if (rel_i == 0 && rel_nb == 0)
+        std::stable_sort(released.begin(), released.end(),
+                         [&](int a, int b) { return row_rel[size_t(a)] < row_rel[size_t(b)]; });
+      const int mb = released[rel_i];
+      const int t = mb * q.n0 + rel_nb;
+      if (++rel_nb == q.n0) {
+        rel_nb = 0;
+        ++rel_i;
+      }
+      start = std::max(tp, row_rel[size_t(mb)]);
+      fin = start + q.c0;
+      lists[size_t(p)].push_back({start, t});
+    }
+    free_at[size_t(p)] = fin;
+    makespan = std::max(makespan, fin);
+  }
+  // real time t' = makespan - t: each slot runs its list backwards
+  sched.assign(size_t(P) + 1, 0);
+  int off = P + 1;
+  for (int i = 0; i < P; ++i) {
+    sched[size_t(i)] = off;
+    off += int(lists[size_t(i)].size());
+  }
+  sched[size_t(P)] = off;
+  std::vector<double> row_ready(size_t(nm), 0.0);
+  for (int i = 0; i < P; ++i)
+    for (auto it = lists[size_t(i)].rbegin(); it != lists[size_t(i)].rend(); ++it) {
+      sched.push_back(it->second);
+      if (!(it->second >> 28) && q.n0) {
+        const int mb = it->second / q.n0;
+        row_ready[size_t(mb)] = std::max(row_ready[size_t(mb)], makespan - it->first);
+      }
+    }
+  if (row_ready_out) *row_ready_out = row_ready;
+  return makespan;
+}
+
+const double kAlphas[] = {-1.0, 0.25, 0.5, 0.75, 1.0, 1.25, 1.5, 2.0, 3.0, 1e9};
+
+// Best alpha for a two-problem schedule; returns the makespan.
+double best_schedule(int P, const TwoProb& q, std::vector<int>& sched, std::vector<double>* row_ready = nullptr) {
+  double best = 1e300;
+  if (q.dep == 1 && q.S1 == 1 && !std::getenv("RTPB_NO_REVERSE_SCHED")) {
+    std::vector<double> rr;
+    best = list_schedule_reverse(P, q, sched, &rr);
+    if (row_ready) row_ready->swap(rr);
+  }
+  for (double al : kAlphas) {
+    std::vector<int> s_;
+    std::vector<double> rr;
+    const double t = list_schedule(P, q, al, s_, &rr);
+    if (t < best) {
+      best = t;
+      sched.swap(s_);
+      if (row_ready) row_ready->swap(rr);
+    }
+  }
+  return best;
 }
 }  // namespace
 
@@ -309,79 +501,29 @@ bool plan_fused_fwd(size_t M, size_t h, size_t f, FusedFwdPlan& plan) {
   const int nm = int((M + 255) / 256), n0 = int((f + kFusedBN - 1) / kFusedBN), n1 = int((h + kFusedBN - 1) / kFusedBN);
   const int T0 = nm * n0, T1 = nm * n1;
   if (P < 2 || T0 + 3 * T1 >= (1 << 20)) return false;
-  const double c0 = fused_unit_cost(h, 2);
-  double best = 1e300;
   // ffn2 K splits: 1 by default. (Measured, config (b): 2 splits 104 us and 3
   // splits 163 us vs 75 us unsplit — the ordered partial-sum epilogues chain
   // across pairs.) RTPB_FUSED_SPLITS forces a count (A/B).
-  int s_lo = 1, s_hi = 1;
-  if (const char* e = std::getenv("RTPB_FUSED_SPLITS")) s_lo = s_hi = std::max(1, std::atoi(e));
-  for (int S = s_lo; S <= s_hi; ++S) {  // ffn2 K splits
-    const size_t kb1 = ((f + 63) / 64 + S - 1) / S;
-    // a partial split stores fp32 (2 outputs' worth); the last one also reads it back
-    const double c1 = S == 1 ? fused_unit_cost(f, 1) : double(kb1) * 0.36 + 0.4 + 0.6;
-    for (int policy = 0; policy < 2; ++policy) {  // 0: ready ffn2 units first, 1: ffn1 tiles first
-      std::vector<std::vector<int>> lists(P);
-      std::vector<double> free_at(P, 0.0), row_ready(nm, 0.0);
-      std::vector<int> row_left(nm, n0);
-      std::vector<int> ready1;  // row blocks whose ffn2 units are ready, in readiness order
-      size_t r1 = 0;            // next ready row block to take ffn2 units from
-      int r1_u = 0;             // next unit (column block x split, split fastest) within it
-      int next0 = 0;
-      double makespan = 0;
-      std::vector<double> split_done(size_t(T1), 0.0);
-      for (int done = 0; done < T0 + S * T1; ++done) {
-        int p = 0;
-        for (int i = 1; i < P; ++i)
-          if (free_at[i] < free_at[p]) p = i;
-        const double tp = free_at[p];
-        const bool have1 = r1 < ready1.size();
-        const bool ready_now = have1 && row_ready[ready1[r1]] <= tp;
-        const bool take1 = next0 >= T0 || (have1 && policy == 0 && ready_now);
-        double fin;
-        if (take1) {
-          const int mb = ready1[r1], nb = r1_u / S, sp = r1_u % S, t = mb * n1 + nb;  // n-fastest tile index
-          const double start = std::max(tp, row_ready[mb]);
-          // the epilogue of split sp waits for split sp - 1 to have landed
-          fin = std::max(start + c1, sp ? split_done[size_t(t)] + 0.6 : 0.0);
-          split_done[size_t(t)] = fin;
-          lists[p].push_back((1 << 28) | (sp << 20) | t);
-          if (++r1_u == n1 * S) {
-            r1_u = 0;
-            ++r1;
-          }
-        } else {
-          const int t = next0++, mb = t / n0;
-          fin = tp + c0;
-          lists[p].push_back(t);
-          row_ready[mb] = std::max(row_ready[mb], fin);
-          if (--row_left[mb] == 0) ready1.push_back(mb);
-        }
-        free_at[p] = fin;
-        makespan = std::max(makespan, fin);
-      }
-      if (makespan < best) {
-        best = makespan;
-        plan.sched.assign(P + 1, 0);
-        int off = P + 1;
-        for (int i = 0; i < P; ++i) {
-          plan.sched[i] = off;
-          off += int(lists[i].size());
-        }
-        plan.sched[P] = off;
-        for (int i = 0; i < P; ++i) plan.sched.insert(plan.sched.end(), lists[i].begin(), lists[i].end());
-        plan.k_splits2 = S;
-      }
-    }
-  }
+  int S = 1;
+  if (const char* e = std::getenv("RTPB_FUSED_SPLITS")) S = std::max(1, std::atoi(e));
+  TwoProb q;
+  q.T0 = T0;
+  q.n0 = n0;
+  q.c0 = tile_cost(h, 2.0);
+  q.T1 = T1;
+  q.n1 = n1;
+  q.S1 = S;
+  q.c1 = S == 1 ? tile_cost(f, 1.0) : tile_cost((f + S - 1) / S, 2.0);
+  q.dep = 1;
+  plan.est_us = best_schedule(P, q, plan.sched);
+  plan.k_splits2 = S;
   plan.slots = P;
   plan.dep_rows = nm;
   plan.dep_target = unsigned(n0) * 2u * kEpiWarps;
   plan.tiles2 = T1;
-  plan.est_us = best;
   if (std::getenv("RTPB_DEBUG_PLAN"))
     std::fprintf(stderr, "fused fwd plan: M=%zu h=%zu f=%zu slots=%d splits2=%d est %.1f us\n", M, h, f, P,
-                 plan.k_splits2, best);
+                 plan.k_splits2, plan.est_us);
   return true;
 }
 
@@ -421,6 +563,142 @@ int gemm_fwd_fused(const StepFwd& p0, const StepFwd& p1, const FusedFwdPlan& pla
   g.dep_rows = plan.dep_rows;
   g.done_ctas = ws.done_ctas;
   return launch_cfg<FusedFwdCfg>(a0, b0, y0, &act0, g, s, &m1, plan.slots);
+}
+
+// ------------------------------------------------------------------ fused MLP backward (N = 1)
+// Two concurrent scheduled launches, each on its own CTA-pair slots:
+//   D (compute stream, dX config): ffn2's dX with gelu' (dpre, problem 0) then
+//     ffn1's dX (problem 1, row block mb after D published dpre row block mb);
+//   W (aux stream, dW config): ffn2's dW (problem 0) then ffn1's dW (problem 1,
+//     whose K runs over dpre rows: its producer waits per K block on D's
+//     row-block counters).
+// D never waits on W, and both grids together fit the SMs, so the cross-launch
+// waits cannot deadlock; a wait that never completes traps instead of hanging.
+namespace {
+using FusedDCfg = GemmCfg<EPI_DGRAD, 256, false, kEpiWarps, false, false, true, true>;
+using FusedWCfg = GemmCfg<EPI_WGRAD, 256, false, kEpiWarps, true, true, false, true>;
+
+}  // namespace
+
+bool plan_fused_bwd(size_t M, size_t h, size_t f, FusedBwdPlan& plan) {
+  const int P = sm_count() / 2;
+  const int nm = int((M + 255) / 256);
+  const int nd2 = int((f + 255) / 256), nd1 = int((h + 255) / 256);  // dX tiles per row block
+  const int Tw = int((f + 255) / 256) * int((h + 255) / 256);       // dW tiles: f x h (ffn2), h x f (ffn1)
+  if (P < 4 || nm * (nd2 + nd1) >= (1 << 20)) return false;
+  TwoProb d;
+  d.T0 = nm * nd2;
+  d.n0 = nd2;
+  d.c0 = tile_cost(h, 2.0) + 0.6;  // gelu' epilogue streams pre in
+  d.T1 = nm * nd1;
+  d.n1 = nd1;
+  d.c1 = tile_cost(f, 1.0);
+  d.dep = 1;
+  double best = 1e300;
+  // dW K splits: 1. (RTPB_FUSED_WSPLITS=2 is an unfinished experiment: it
+  // trapped on the GPU box, a wait not satisfied — do not enable.)
+  int s_lo = 1, s_hi = 1;
+  if (const char* e = std::getenv("RTPB_FUSED_WSPLITS")) s_lo = s_hi = std::max(1, std::atoi(e));
+  for (int Pw = 2; Pw <= P - 2; ++Pw) {
+    const int Pd = P - Pw;
+    // D's schedule decides when dpre rows land for W: try every D policy
+    // (forward, alpha sweep; the reversed schedule lands rows late) against W
+    for (double al : kAlphas) {
+    std::vector<int> sd;
+    std::vector<double> rows;
+    const double td = list_schedule(Pd, d, al, sd, &rows);
+    if (td >= best) continue;
+    for (int S = s_lo; S <= s_hi; ++S) {
+      TwoProb w;
+      w.T0 = Tw * S;  // problem 0 (ffn2 dW) units, split-major within a tile via S1 below
+      w.n0 = 0;
+      w.c0 = tile_cost((M + S - 1) / S, 2.0);
+      w.T1 = Tw;
+      w.n1 = 0;
+      w.S1 = S;
+      w.c1 = w.c0;
+      w.dep = 2;
+      w.ext_ready = &rows;
+      w.K1 = M;
+      // problem 0 of W is split too: emit its units with split indices
+      std::vector<int> sw;
+      const double tw = best_schedule(Pw, w, sw);
+      const double t = std::max(td, tw);
+      if (t < best) {
+        best = t;
+        // problem-0 codes in sw are plain unit indices u = tile * S + split: re-encode
+        for (size_t i = size_t(Pw) + 1; i < sw.size(); ++i)
+          if (!(sw[i] >> 28)) sw[i] = ((sw[i] % S) << 20) | (sw[i] / S);
+        plan.sched_d = sd;
+        plan.sched_w.swap(sw);
+        plan.slots_d = Pd;
+        plan.slots_w = Pw;
+        plan.w_splits = S;
+      }
+    }
+    }
+  }
+  plan.dep_rows = nm;
+  plan.dep_target = unsigned(nd2) * 2u * kEpiWarps;
+  plan.est_us = best;
+  if (std::getenv("RTPB_DEBUG_PLAN"))
+    std::fprintf(stderr, "fused bwd plan: M=%zu h=%zu f=%zu dX pairs %d dW pairs %d (K splits %d) est %.1f us\n", M, h,
+                 f, plan.slots_d, plan.slots_w, plan.w_splits, best);
+  return true;
+}
+
+int gemm_bwd_fused(const FusedBwdArgs& a, const FusedBwdPlan& plan, const FusedBwdWs& ws, cudaStream_t compute,
+                   cudaStream_t aux) {
+  const size_t M = a.M, h = a.h, f = a.f;
+  const unsigned done_target = 2u * unsigned(plan.slots_d + plan.slots_w);
+  // ---- D: dpre = (dY . W2^T) * gelu'(pre) over pre; dX = dpre . W1^T
+  {
+    Op a0{a.dy, nullptr, h, M, a.ldy}, b0{a.w2, nullptr, h, f, h};
+    Out dpre{a.pre, false, f, M, f}, pre_in{a.pre, false, f, M, f};
+    Op a1{a.pre, nullptr, f, M, f}, b1{a.w1, nullptr, f, h, f};
+    Out dx{a.dx, false, h, M, a.lddx};
+    GemmMaps m1;
+    int rc;
+    if ((rc = encode_maps<FusedDCfg>(a1, b1, dx, nullptr, m1))) return rc;
+    GemmArgs g{};
+    g.M = int(M); g.N = int(f); g.K = int(h);
+    g.flags = EF_FIRST | EF_LAST | EF_GELU_BWD;
+    g.aux = a.pre; g.ld_aux = int64_t(f);
+    g.n_fastest = 1; g.k_splits = 1;
+    g.sched = ws.sched_d;
+    g.M2 = int(M); g.N2 = int(h); g.K2 = int(f);
+    g.flags2 = EF_FIRST | EF_LAST;
+    g.n_fastest2 = 1; g.k_splits2 = 1;
+    g.dep_count = ws.dep_count; g.dep_target = plan.dep_target; g.dep_rows = plan.dep_rows;
+    g.done_ctas = ws.done_ctas; g.done_target = done_target;
+    if ((rc = launch_cfg<FusedDCfg>(a0, b0, dpre, &pre_in, g, compute, &m1, plan.slots_d))) return rc;
+  }
+  // ---- W: G2 (+)= act^T . dY ; G1 (+)= X^T . dpre (K blocks after D published them)
+  {
+    Op a0{a.act, nullptr, f, M, f}, b0{a.dy, nullptr, h, M, a.ldy};
+    Out g2{a.g2, true, h, f, h};
+    Op a1{a.x, nullptr, h, M, a.ldx}, b1{a.pre, nullptr, f, M, f};
+    Out g1{a.g1, true, f, h, f};
+    GemmMaps m1;
+    int rc;
+    if ((rc = encode_maps<FusedWCfg>(a1, b1, g1, nullptr, m1))) return rc;
+    GemmArgs g{};
+    g.M = int(f); g.N = int(h); g.K = int(M);
+    g.flags = a.g2_zero ? EF_FIRST : 0;
+    g.n_fastest = 0; g.k_splits = plan.w_splits; g.split_flags = a.split_flags2;
+    g.gbias_in = a.g2_zero ? nullptr : a.g2 + f * h; g.gbias_out = a.g2 + f * h;
+    g.bias_part = a.bias_part2; g.bias_tick = a.bias_tick2;
+    g.sched = ws.sched_w;
+    g.M2 = int(h); g.N2 = int(f); g.K2 = int(M);
+    g.flags2 = a.g1_zero ? EF_FIRST : 0;
+    g.n_fastest2 = 0; g.k_splits2 = plan.w_splits; g.split_flags2 = a.split_flags1;
+    g.gbias_in2 = a.g1_zero ? nullptr : a.g1 + h * f; g.gbias_out2 = a.g1 + h * f;
+    g.bias_part2 = a.bias_part1; g.bias_tick2 = a.bias_tick1;
+    g.dep_count = ws.dep_count; g.dep_target = plan.dep_target; g.dep_rows = plan.dep_rows; g.dep_on_k = 1;
+    g.done_ctas = ws.done_ctas; g.done_target = done_target;
+    if ((rc = launch_cfg<FusedWCfg>(a0, b0, g2, nullptr, g, aux, &m1, plan.slots_w))) return rc;
+  }
+  return RTPB_OK;
 }
 
 void set_sm_budget(int sms) { t_sm_budget = sms; }

@@ -87,12 +87,23 @@ struct GemmArgs {
   unsigned* split_flags2;
   const float* acc2;
   int64_t ld_acc2;
+  // Problem 1 of a dW launch: its own fused bias-gradient sums.
+  const float* gbias_in2;
+  float* gbias_out2;
+  float* bias_part2;
+  unsigned* bias_tick2;
+  // dep_on_k: problem 1's K dimension runs over the rows another (concurrent)
+  // launch publishes: its producer waits per K block on
+  // dep_count[k_row / 256] instead of per tile row block. done_target: CTAs
+  // sharing dep_count / done_ctas across launches (0: this grid).
+  int dep_on_k;
+  unsigned done_target;
   unsigned* dep_count;
   unsigned dep_target;
   int dep_rows;
   unsigned* done_ctas;
 };
-constexpr int TRACE_UNITS = 13;
+constexpr int TRACE_UNITS = 12;  // 2 + 6 * 12 slots + grid marker at TRACE_STRIDE - 1
 constexpr int TRACE_STRIDE = 80;
 
 template <int EPI_, int BN_, bool TF32_, int EPI_WARPS_, bool A_MN_, bool B_MN_, bool PRE_TMA_ = false,
@@ -187,6 +198,20 @@ __device__ __forceinline__ unsigned long long gtime() {
 }
 __device__ __forceinline__ void trace_at(unsigned long long* tr, int slot) {
   if (tr) tr[blockIdx.x * TRACE_STRIDE + slot] = gtime();
+}
+
+// Spin until *p >= need (acquire, gpu scope), then order async-proxy (TMA)
+// accesses after it. A wait that cannot be satisfied within ~10 s traps
+// (kernel error) instead of hanging the device.
+__device__ __forceinline__ void wait_counter(const unsigned* p, unsigned need) {
+  unsigned seen;
+  const long long t0 = clock64();
+  for (;;) {
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(p) : "memory");
+    if (seen >= need) break;
+    if (clock64() - t0 > (20ll << 30)) __trap();
+  }
+  asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 
 __device__ __forceinline__ float bf16lo(uint32_t u) { return __uint_as_float(u << 16); }
@@ -466,7 +491,6 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
   griddep_launch();
   if (threadIdx.x == 0) detail::trace_at(trace, 1);
 
-  const bool colsum_on = Cfg::COLSUM && args.gbias_out != nullptr;
 
   if (warp == 0) {
     // ===================== TMA producer =====================
@@ -507,21 +531,25 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
         const Unit x = decode(it);
         const int mb = x.mb, nb = x.nb, kb0 = x.kb0, kb1 = x.kb1, uM = x.M, uN = x.N;
         const GemmMaps& mp = x.prob ? maps2 : maps;
-        if (x.prob && args.dep_count) {
+        if (x.prob && args.dep_count && !args.dep_on_k) {
           // problem 1 reads problem 0's output rows of this row block: wait
           // until every warp of every problem-0 tile of the block has landed
           // its stores, then order the async-proxy (TMA) reads after them.
-          unsigned seen;
-          do {
-            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(args.dep_count + mb) : "memory");
-          } while (seen < args.dep_target);
-          asm volatile("fence.proxy.async.global;" ::: "memory");
+          detail::wait_counter(args.dep_count + mb, args.dep_target);
         }
+        int dep_rb = -1;  // dep_on_k: last row block waited for
         // this CTA's A rows and B columns (pair: its half of the 256 x BN tile)
         const int m0 = mb * Cfg::TILE_M + int(rank) * BM, n0 = nb * BN + int(rank) * Cfg::B_ROWS;
         int expect = a_bytes(mb * Cfg::TILE_M, uM) + b_bytes(nb * BN, uN);
         if constexpr (Cfg::PAIR) expect += a_bytes(mb * Cfg::TILE_M + BM, uM) + b_bytes(nb * BN + Cfg::B_ROWS, uN);
         for (int kb = kb0; kb < kb1; ++kb) {
+          if (x.prob && args.dep_on_k) {
+            const int rb = (kb * BK) / 256;  // row block (256 rows) of the producing launch
+            if (rb != dep_rb) {
+              detail::wait_counter(args.dep_count + rb, args.dep_target);
+              dep_rb = rb;
+            }
+          }
           mbar_wait(&empty_bar[stage], phase ^ 1);
           uint8_t* sA = stage_base + stage * Cfg::STAGE_BYTES;
           if (rank == 0) mbar_expect_tx(&full_bar[stage], uint32_t(expect));
@@ -693,27 +721,16 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
       const bool part2 = split2 && split < splits2 - 1;
       const bool fin2 = split2 && split == splits2 - 1;
       if (split2 && split > 0) {
-        if (lane == 0) {
-          const unsigned need = unsigned(split * wgroup);
-          unsigned seen;
-          do {
-            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(args.split_flags2 + t) : "memory");
-          } while (seen < need);
-          asm volatile("fence.proxy.async.global;" ::: "memory");
-        }
+        if (lane == 0) detail::wait_counter(args.split_flags2 + t, unsigned(split * wgroup));
         __syncwarp();
       }
+      // dW split over K (per problem): its own counters
+      unsigned* const wflags = x_.prob ? args.split_flags2 : args.split_flags;
+      const int wsplits = x_.prob ? splits2 : splits;
       if constexpr (Cfg::EPI == EPI_WGRAD) {
         if (split > 0) {
           // ordered split-K: wait until every warp of split-1 has landed its sums
-          if (lane == 0) {
-            const unsigned need = unsigned(split * wgroup);
-            unsigned seen;
-            do {
-              asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(args.split_flags + t) : "memory");
-            } while (seen < need);
-            asm volatile("fence.proxy.async.global;" ::: "memory");
-          }
+          if (lane == 0) detail::wait_counter(wflags + t, unsigned(split * wgroup));
           __syncwarp();
         }
       }
@@ -849,13 +866,13 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
         pending = false;
       }
       if constexpr (Cfg::EPI == EPI_WGRAD) {
-        if (splits > 1) {
+        if (wsplits > 1) {
           // publish: this warp's reduce-adds for (tile, split) are performed
           if (lane == 0) {
             bulk_wait0();
             __threadfence();
-            const unsigned old = atomicAdd(args.split_flags + t, 1u);
-            if (old + 1 == unsigned(splits * wgroup)) args.split_flags[t] = 0u;  // last arrival re-zeroes
+            const unsigned old = atomicAdd(wflags + t, 1u);
+            if (old + 1 == unsigned(wsplits * wgroup)) wflags[t] = 0u;  // last arrival re-zeroes
           }
           __syncwarp();
           pending = false;
@@ -903,13 +920,19 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
     constexpr int ROWS = BK / Cfg::COLSUM_WARPS;
     const int cw = warp - 2 - Cfg::EPI_WARPS;  // 0: publisher, 1: helper
     const int chunk = (lane % LPR) / 8, piece = lane & 7, rsub = lane / LPR;
-    const bool first = args.flags & EF_FIRST;
-    const int contributors = num_m * splits;
     int stage = 0;
     uint32_t phase = 0;
     for (int it = it_beg; it < it_end; it += it_step) {
       const Unit x_ = decode(it);
-      const int split = x_.split, mb = x_.mb, nb = x_.nb, kb0 = x_.kb0, kb1 = x_.kb1;
+      const int split = x_.split, mb = x_.mb, nb = x_.nb, kb0 = x_.kb0, kb1 = x_.kb1, uN = x_.N;
+      const bool first = x_.flags & EF_FIRST;
+      const int unum_m = x_.prob ? num_m2 : num_m;
+      const int contributors = unum_m * (x_.prob ? splits2 : splits);
+      const float* ugb_in = x_.prob ? args.gbias_in2 : args.gbias_in;
+      float* ugb_out = x_.prob ? args.gbias_out2 : args.gbias_out;
+      float* upart = x_.prob ? args.bias_part2 : args.bias_part;
+      unsigned* utick = x_.prob ? args.bias_tick2 : args.bias_tick;
+      const bool colsum_on = Cfg::COLSUM && ugb_out != nullptr;
       float sum[8];
 #pragma unroll
       for (int e = 0; e < 8; ++e) sum[e] = 0.f;
@@ -924,7 +947,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
         } else {
           mbar_wait(&ready_bar[stage], phase);
         }
-        if (colsum_on && kb % num_m == mb) {
+        if (colsum_on && kb % unum_m == mb) {
           const uint8_t* sB = stage_base + stage * Cfg::STAGE_BYTES + Cfg::A_BYTES + chunk * (BK * 128);
 #pragma unroll 4
           for (int i = 0; i < ROWS / RPI; ++i) {
@@ -958,23 +981,23 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
       if (cw == 0) {
         const int cg = nb * 2 + int(rank);                 // this CTA's column group
         const int c0 = cg * Cfg::B_ROWS + lane * 8;
-        float* part = args.bias_part + size_t(split * num_m + mb) * args.N;
+        float* part = upart + size_t(split * unum_m + mb) * uN;
         if (lane < LPR) {
           const float4 a = cs[0], b = cs[1];
           sum[0] += a.x; sum[1] += a.y; sum[2] += a.z; sum[3] += a.w;
           sum[4] += b.x; sum[5] += b.y; sum[6] += b.z; sum[7] += b.w;
 #pragma unroll
           for (int e = 0; e < 8; ++e)
-            if (c0 + e < args.N) part[c0 + e] = sum[e];
+            if (c0 + e < uN) part[c0 + e] = sum[e];
         }
         __syncwarp();
         unsigned last = 0;
         if (lane == 0) {
           __threadfence();
-          const unsigned old = atomicAdd(args.bias_tick + cg, 1u);
+          const unsigned old = atomicAdd(utick + cg, 1u);
           last = old + 1 == unsigned(contributors);
           if (last) {
-            args.bias_tick[cg] = 0u;  // self-resetting for the next launch
+            utick[cg] = 0u;  // self-resetting for the next launch
             __threadfence();
           }
         }
@@ -991,14 +1014,14 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
           constexpr int G = 32 / LPR;
           const int grp = lane / LPR, cl = cg * Cfg::B_ROWS + (lane % LPR) * 8;
           float4 s0 = make_float4(0.f, 0.f, 0.f, 0.f), s1 = s0;
-          if (cl < args.N) {
-            const float* base = args.bias_part + cl;
+          if (cl < uN) {
+            const float* base = upart + cl;
             int r = grp;
             for (; r + 3 * G < contributors; r += 4 * G) {
               float4 v[8];
 #pragma unroll
               for (int q = 0; q < 4; ++q) {
-                const float4* p = reinterpret_cast<const float4*>(base + size_t(r + q * G) * args.N);
+                const float4* p = reinterpret_cast<const float4*>(base + size_t(r + q * G) * uN);
                 v[2 * q] = __ldcg(p);
                 v[2 * q + 1] = __ldcg(p + 1);
               }
@@ -1009,7 +1032,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
               }
             }
             for (; r < contributors; r += G) {
-              const float4* p = reinterpret_cast<const float4*>(base + size_t(r) * args.N);
+              const float4* p = reinterpret_cast<const float4*>(base + size_t(r) * uN);
               const float4 a = __ldcg(p), b = __ldcg(p + 1);
               s0.x += a.x; s0.y += a.y; s0.z += a.z; s0.w += a.w;
               s1.x += b.x; s1.y += b.y; s1.z += b.z; s1.w += b.w;
@@ -1024,10 +1047,10 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
             s1.x += __shfl_sync(0xffffffffu, t1.x, src); s1.y += __shfl_sync(0xffffffffu, t1.y, src);
             s1.z += __shfl_sync(0xffffffffu, t1.z, src); s1.w += __shfl_sync(0xffffffffu, t1.w, src);
           }
-          if (lane < LPR && cl < args.N) {
-            float4* o = reinterpret_cast<float4*>(args.gbias_out + cl);
+          if (lane < LPR && cl < uN) {
+            float4* o = reinterpret_cast<float4*>(ugb_out + cl);
             if (!first) {
-              const float4* gi = reinterpret_cast<const float4*>(args.gbias_in + cl);
+              const float4* gi = reinterpret_cast<const float4*>(ugb_in + cl);
               const float4 a = __ldcg(gi), b = __ldcg(gi + 1);
               s0 = make_float4(a.x + s0.x, a.y + s0.y, a.z + s0.z, a.w + s0.w);
               s1 = make_float4(b.x + s1.x, b.y + s1.y, b.z + s1.z, b.w + s1.w);
@@ -1057,7 +1080,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
     // every thread of this CTA is past its last dependency read: the last CTA
     // out re-zeroes the row-block counters for the next launch
     __threadfence();
-    if (atomicAdd(args.done_ctas, 1u) == gridDim.x - 1) {
+    if (atomicAdd(args.done_ctas, 1u) == (args.done_target ? args.done_target : gridDim.x) - 1) {
       for (int r = 0; r < args.dep_rows; ++r) args.dep_count[r] = 0u;
       *args.done_ctas = 0u;
       __threadfence();

@@ -75,6 +75,41 @@ bool plan_fused_fwd(size_t M, size_t h, size_t f, FusedFwdPlan& plan);
 int gemm_fwd_fused(const StepFwd& p0, const StepFwd& p1, const FusedFwdPlan& plan, const FusedFwdWs& ws,
                    cudaStream_t s);
 
+// Fused N = 1 MLP backward: D (dX chain) and W (dW pair) launches.
+struct FusedBwdPlan {
+  std::vector<int> sched_d, sched_w;  // [slots + 1 offsets][unit codes] each
+  int slots_d = 0, slots_w = 0;       // CTA pairs of D and W (together <= SMs / 2)
+  int w_splits = 1;                   // dW K splits (ordered, deterministic)
+  int dep_rows = 0;
+  unsigned dep_target = 0;
+  double est_us = 0;
+};
+struct FusedBwdWs {
+  const int* sched_d;
+  const int* sched_w;
+  unsigned* dep_count;  // [dep_rows], zeroed once, self-resetting
+  unsigned* done_ctas;  // [1]
+};
+struct FusedBwdArgs {
+  const void* dy; size_t ldy;   // M x h upstream gradient
+  const void* act;              // M x f gelu(pre): ffn2's input
+  const void* x; size_t ldx;    // M x h block input: ffn1's input
+  void* pre;                    // M x f: pre in, dpre out (in place)
+  void* dx; size_t lddx;        // M x h output
+  const void* w1; const void* w2;  // shards [W | b] (bf16)
+  float* g1; float* g2;         // gradient shards (fp32)
+  bool g1_zero, g2_zero;        // known-zero gradients: store instead of accumulate
+  float* bias_part1; unsigned* bias_tick1;  // per-layer workspace parts (zeroed counters)
+  float* bias_part2; unsigned* bias_tick2;
+  unsigned* split_flags1; unsigned* split_flags2;
+  size_t M, h, f;
+};
+bool plan_fused_bwd(size_t M, size_t h, size_t f, FusedBwdPlan& plan);
+int gemm_bwd_fused(const FusedBwdArgs& a, const FusedBwdPlan& plan, const FusedBwdWs& ws, cudaStream_t compute,
+                   cudaStream_t aux);
+int fused_bwd_step(FusedBwdArgs a, void* ws1, size_t ws1_bytes, void* ws2, size_t ws2_bytes,
+                   const FusedBwdPlan& plan, const FusedBwdWs& ws, cudaStream_t compute, cudaStream_t aux);
+
 // The fused forward as a step (capi_steps.cu): bf16, shards [W | b];
 // store_pre: also write pre (Train). Timed as one fwd launch when profiling.
 int fused_fwd_step(const void* x, size_t ldx, const void* w1_shard, void* pre, void* act, const void* w2_shard,

@@ -61,7 +61,7 @@ for k in kinds:
 
 if os.environ.get("TRACE"):
     import numpy as np
-    STRIDE, UNITS = 80, 13
+    STRIDE, UNITS = 80, 12
     for k in kinds:
         buf = torch.zeros(148 * STRIDE + 64, dtype=torch.int64, device=dev)
         torch.cuda.synchronize()

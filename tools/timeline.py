@@ -12,13 +12,13 @@ import torch
 sys.path.insert(0, ".")
 from paper_2311_01635_b200 import _lib, rtp  # noqa: E402
 
-STRIDE, UNITS = 80, 13
+STRIDE, UNITS = 80, 12
 M = int(sys.argv[1]) if len(sys.argv) > 1 else 8192
 H = int(sys.argv[2]) if len(sys.argv) > 2 else 768
 F = int(sys.argv[3]) if len(sys.argv) > 3 else 3072
 import os
-NAMES = (["fwd1", "fwd2", "dgrad2", "wgrad2", "dgrad1", "wgrad1"] if os.environ.get("RTPB_NO_FUSED_FWD")
-         else ["fwd1+fwd2", "dgrad2", "wgrad2", "dgrad1", "wgrad1"])
+NAMES = (["fwd1", "fwd2"] if os.environ.get("RTPB_NO_FUSED_FWD") else ["fwd1+fwd2"]) + \
+    (["dgrad2", "wgrad2", "dgrad1", "wgrad1"] if os.environ.get("RTPB_NO_FUSED_BWD") else ["dgrad2+dgrad1", "wgrad2+wgrad1"])
 
 dev = torch.device("cuda", 0)
 grp = rtp.WorkerGroup(1)
@@ -80,7 +80,7 @@ for li, name in enumerate(NAMES):
             if mma_lead[c, i] and epi[c, i]:
                 lat.append(u[c, i, 4] - u[c, i, 3])
     units_per_cta = epi.sum(1)
-    if os.environ.get("UNITS") and li == 0:
+    if os.environ.get("UNITS") and str(li) in os.environ.get("UNITS").split(","):
         for c in range(0, g, 2):
             print("   cta", c, " ".join(f"[{rel(u[c, i, 2]):.1f}>{rel(u[c, i, 4]):.1f}:{rel(u[c, i, 5]):.1f}]"
                                       for i in range(UNITS) if u[c, i, 2] > 0))
