@@ -143,3 +143,14 @@ def test_two_process_gloo_ring_protocol():
     for p in procs:
         p.join(timeout=60)
     assert sorted(res) == [(0, "ok"), (1, "ok")], res
+
+
+def test_fused_n1_schedules_cover_the_config_shapes():
+    """Host-side list scheduling of the fused N = 1 MLP launches (no GPU):
+    every BASELINE config shape gets a plan with a finite cost-model makespan."""
+    import math
+    from paper_2311_01635_b200 import _lib
+    for M, h, f in ((8192, 768, 3072), (16384, 4096, 16384), (4096, 8192, 28672), (1000, 768, 3072), (8, 8, 16)):
+        for which in (0, 1):
+            t = _lib.lib.rtpb_debug_fused_plan(M, h, f, which)
+            assert t > 0 and math.isfinite(t), (M, h, f, which)
