@@ -380,7 +380,7 @@ class RtpMlp {
   void ensure_fused_bwd(size_t rows);
   DeviceBuffer fused_bwd_ws_;
   size_t fused_bwd_rows_ = 0, fused_bwd_sd_ints_ = 0, fused_bwd_sw_ints_ = 0;
-  int fused_bwd_slots_d_ = 0, fused_bwd_slots_w_ = 0, fused_bwd_dep_rows_ = 0;
+  int fused_bwd_slots_d_ = 0, fused_bwd_slots_w_ = 0, fused_bwd_dep_rows_ = 0, fused_bwd_w_splits_ = 1;
   unsigned fused_bwd_dep_target_ = 0;
 };
 

@@ -609,6 +609,7 @@ void RtpMlp::ensure_fused_bwd(size_t rows) {
   fused_bwd_slots_w_ = plan.slots_w;
   fused_bwd_dep_rows_ = plan.dep_rows;
   fused_bwd_dep_target_ = plan.dep_target;
+  fused_bwd_w_splits_ = plan.w_splits;
   fused_bwd_rows_ = rows;
 }
 
@@ -639,6 +640,7 @@ void RtpMlp::backward(std::span<const DView> dy, size_t rows, std::span<const DV
     plan.slots_w = fused_bwd_slots_w_;
     plan.dep_rows = fused_bwd_dep_rows_;
     plan.dep_target = fused_bwd_dep_target_;
+    plan.w_splits = fused_bwd_w_splits_;
     FusedBwdWs ws{base, base + fused_bwd_sd_ints_, dep, dep + fused_bwd_dep_rows_};
     w.fork_aux();  // aux: dY, act, X and pre are complete
     check_status(fused_bwd_step(a, b1.workspace, b1.workspace_bytes, b2.workspace, b2.workspace_bytes, plan, ws,

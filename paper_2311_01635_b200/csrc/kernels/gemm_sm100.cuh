@@ -889,9 +889,10 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
         acc = 0;
         acc_phase ^= 1;
       }
-      if (args.dep_count && x_.prob == 0) {
+      if (args.dep_count && !args.dep_on_k && x_.prob == 0) {
         // publish: this warp's stores of the tile are complete (problem 1
-        // reads them as its A operand), after the accumulator was released
+        // reads them as its A operand), after the accumulator was released.
+        // (A dep_on_k launch only consumes another launch's counters.)
         if (lane == 0) {
           bulk_wait0();
           asm volatile("fence.proxy.async.global;" ::: "memory");
