@@ -54,6 +54,30 @@ int overlap_dx_sms(size_t M, size_t I, size_t per, bool gelu_bwd) {
   }
   return best_sms;
 }
+// NCCL's send/recv kernels need SMs, and a persistent step GEMM holds every
+// SM it is given (one CTA per SM, ~225 KB of shared memory), so with the NCCL
+// transport the layers leave RTPB_NCCL_RESERVED_SMS (default 8) SMs free for
+// the rotation to progress under the GEMMs instead of queueing behind them.
+// The local transports move bytes with copy engines and reserve nothing.
+class SmReserve {
+ public:
+  explicit SmReserve(const WorkerGroup& g) {
+    if (g.kind() != TransportKind::Nccl || g.size() < 2) return;
+    int reserve = 8;
+    if (const char* e = std::getenv("RTPB_NCCL_RESERVED_SMS")) reserve = std::max(0, std::atoi(e));
+    if (reserve == 0) return;
+    set_sm_budget(0);
+    const int all = sm_budget();
+    set_sm_budget(std::max(2, all - reserve));
+    active_ = true;
+  }
+  ~SmReserve() {
+    if (active_) set_sm_budget(0);
+  }
+
+ private:
+  bool active_ = false;
+};
 }  // namespace
 
 // ------------------------------------------------------------------ base
@@ -240,6 +264,7 @@ void RtpLinear::backward(std::span<const DView> dy, size_t rows, std::span<const
 void RtpLinear::forward_ex(std::span<const DView> x, size_t rows, std::span<const DView> y, Mode mode,
                            const FwdEpi& e) {
   require_home("forward");
+  SmReserve sm_reserve(*group_);
   const auto& local = group_->local_ranks();
   if (x.size() != local.size() || (e.store_pre && y.size() != local.size()))
     throw DimensionError(label_ + ": forward expects one activation per local worker");
@@ -341,6 +366,7 @@ void RtpLinear::end_backward_n1() {
 }
 
 void RtpLinear::backward_ex(std::span<const DView> dy, size_t rows, std::span<const DView> dx, const BwdEpi& e) {
+  SmReserve sm_reserve(*group_);
   const auto& local = group_->local_ranks();
   if (dy.size() != local.size() || dx.size() != local.size())
     throw DimensionError(label_ + ": backward expects one gradient per local worker");

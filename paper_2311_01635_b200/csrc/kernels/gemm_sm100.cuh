@@ -203,14 +203,18 @@ __device__ __forceinline__ void trace_at(unsigned long long* tr, int slot) {
 // Spin until *p >= need (acquire, gpu scope), then order async-proxy (TMA)
 // accesses after it. A wait that cannot be satisfied within ~10 s traps
 // (kernel error) instead of hanging the device.
-__device__ __forceinline__ void wait_counter(const unsigned* p, unsigned need) {
-  unsigned seen;
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void wait_counter_nofence(const unsigned* p, unsigned need) {
   const long long t0 = clock64();
-  for (;;) {
-    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(p) : "memory");
-    if (seen >= need) break;
+  while (ld_acquire(p) < need)
     if (clock64() - t0 > (20ll << 30)) __trap();
-  }
+}
+__device__ __forceinline__ void wait_counter(const unsigned* p, unsigned need) {
+  wait_counter_nofence(p, need);
   asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 
@@ -545,9 +549,15 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
         for (int kb = kb0; kb < kb1; ++kb) {
           if (x.prob && args.dep_on_k) {
             const int rb = (kb * BK) / 256;  // row block (256 rows) of the producing launch
-            if (rb != dep_rb) {
-              detail::wait_counter(args.dep_count + rb, args.dep_target);
-              dep_rb = rb;
+            if (rb > dep_rb) {
+              // wait for this row block, extend over the ones already complete
+              // (up to the unit's last), then ONE proxy fence for all of them
+              detail::wait_counter_nofence(args.dep_count + rb, args.dep_target);
+              int r = rb;
+              const int rb_last = ((kb1 - 1) * BK) / 256;
+              while (r < rb_last && detail::ld_acquire(args.dep_count + r + 1) >= args.dep_target) ++r;
+              asm volatile("fence.proxy.async.global;" ::: "memory");
+              dep_rb = r;
             }
           }
           mbar_wait(&empty_bar[stage], phase ^ 1);
