@@ -186,6 +186,10 @@ def main():
     ap.add_argument("--tokens-per-gpu", type=int, default=TOKENS_PER_GPU)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--eager", action="store_true", help="time host-issued launches instead of a CUDA graph")
+    ap.add_argument("--transport", default="nccl", choices=["nccl", "ipc"],
+                    help="N > 1 ring shift: ncclSend/ncclRecv (default) or copy-engine pushes through CUDA IPC")
+    ap.add_argument("--same-device", action="store_true",
+                    help="test mode: every rank on GPU 0 (IPC transport, gloo plumbing); numbers not meaningful")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference_arm(args)
@@ -199,17 +203,33 @@ def main():
     from paper_2311_01635_b200 import _lib, rtp
 
     rank, world, local = dist_env()
+    if args.same_device:
+        local = 0
+        args.transport = "ipc"
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
-        uid = torch.zeros(128, dtype=torch.uint8, device=dev)
-        if rank == 0:
-            uid.copy_(torch.frombuffer(bytearray(rtp.WorkerGroup.nccl_unique_id()), dtype=torch.uint8))
-        dist.broadcast(uid, 0)
-        grp = rtp.WorkerGroup.nccl(world, rank, local, bytes(uid.cpu().numpy().tobytes()))
+        # plumbing only (barriers, max over ranks, the id broadcast)
+        if args.same_device:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
+        make_uid = rtp.WorkerGroup.ipc_unique_id if args.transport == "ipc" else rtp.WorkerGroup.nccl_unique_id
+        box = [make_uid() if rank == 0 else None]
+        dist.broadcast_object_list(box, 0)
+        make = rtp.WorkerGroup.ipc if args.transport == "ipc" else rtp.WorkerGroup.nccl
+        grp = make(world, rank, local, box[0])
+        if args.transport == "ipc":
+            args.eager = True  # the IPC flags carry per-shift sequence numbers: no graph replay
     else:
         grp = rtp.WorkerGroup(1)
+
+    def allmax(v: float) -> float:
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device="cpu" if args.same_device else dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
     M = args.tokens_per_gpu
     T = M * world
     mlp = rtp.RtpMlp(grp, "block0", H, F, "bf16", seed=SEED, stream_base=0)  # Flyweight init on device
@@ -303,10 +323,7 @@ def main():
     _lib.lib.rtpb_profile_enable(0)
     step_ms = [a.elapsed_time(b) for a, b in ev]
     total_ms = sum(step_ms)
-    if world > 1:
-        t = torch.tensor([total_ms], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
+    total_ms = allmax(total_ms)
     ms_per_step = total_ms / args.steps
     value = flops_per_step(T) / (ms_per_step * 1e-3) / 1e12  # whole-job aggregate
 
@@ -386,7 +403,7 @@ def main():
     # ---- exposed rotation time: T(step) - T(step without moving bytes)
     exposed = {"ms_per_step": 0.0, "frac": 0.0, "method": "N=1: no rotation, nothing to expose"}
     if world > 1:
-        def eager_ms(k=10):
+        def eager_step_ms(k=10):
             barrier()
             a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a_.record(stream)
@@ -394,14 +411,12 @@ def main():
                 step()
             b_.record(stream)
             barrier()
-            t_ = torch.tensor([a_.elapsed_time(b_) / k], device=dev, dtype=torch.float64)
-            dist.all_reduce(t_, op=dist.ReduceOp.MAX)
-            return float(t_.item())
-        t_with = eager_ms()
+            return allmax(a_.elapsed_time(b_) / k)
+        t_with = eager_step_ms()
         _lib.lib.rtpb_debug_skip_comm(1)
         try:
             step()
-            t_without = eager_ms()
+            t_without = eager_step_ms()
         finally:
             _lib.lib.rtpb_debug_skip_comm(0)
         exposed = {"ms_per_step": max(0.0, t_with - t_without), "frac": max(0.0, t_with - t_without) / t_with,
@@ -481,10 +496,7 @@ def main():
         e1.record(stream)
         barrier()
         e2e_ms = e0.elapsed_time(e1) / e2e_steps
-        if world > 1:
-            t = torch.tensor([e2e_ms], device=dev, dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e2e_ms = float(t.item())
+        e2e_ms = allmax(e2e_ms)
         e2e = {"value": flops_per_step(T) / (e2e_ms * 1e-3) / 1e12, "unit": UNIT,
                "h2d_bytes_per_step": 2 * M * H * 2, "d2h_bytes_per_step": M * H * 2, "ms_per_step": e2e_ms,
                "path": "RtpMlp.forward/backward (C ABI, eager launches) from pinned host X, dY; dX read "
@@ -503,7 +515,8 @@ def main():
                                                              "SplitMix64 weights, seed 42)",
                 "config": {"workload": "rtp_mlp_768x3072x768 (config b)", "h": H, "f": F,
                            "tokens_per_gpu": M, "global_tokens": T, "rotation_mode": args.mode,
-                           "parallelism": f"rtp{world}", "l2": "flushed before every timed step (512 MiB written, then read back)",
+                           "parallelism": f"rtp{world}", "transport": args.transport if world > 1 else None,
+                           "same_device_test": bool(args.same_device and world > 1), "l2": "flushed before every timed step (512 MiB written, then read back)",
                            "flops_per_step": flops_per_step(T)},
                 "tflops_per_gpu": value / world,
                 "gpu_launches": int(launches),

@@ -163,6 +163,7 @@ typedef struct rtpb_mlp_s* rtpb_mlp;
 #define RTPB_TRANSPORT_LOCKSTEP 0   /* one host thread drives all local workers        */
 #define RTPB_TRANSPORT_CONCURRENT 1 /* one host thread per local worker                */
 #define RTPB_TRANSPORT_NCCL 2       /* one process per GPU, ncclSend/ncclRecv on NVLink */
+#define RTPB_TRANSPORT_IPC 3        /* one process per GPU, copy-engine pushes via CUDA IPC */
 
 #define RTPB_MODE_TRAIN 0
 #define RTPB_MODE_EVAL 1
@@ -185,6 +186,14 @@ int rtpb_group_create(size_t n, int transport, const int* devices, rtpb_group* o
  * rtpb_nccl_unique_id() on rank 0, broadcast by the caller. */
 int rtpb_nccl_unique_id(void* out128);
 int rtpb_group_create_nccl(size_t n, size_t rank, int device, const void* nccl_id, rtpb_group* out);
+/* Distributed group on the IPC transport: the ring shift is a copy-engine
+ * push into the neighbour's buffer through a CUDA IPC mapping (NVLink P2P,
+ * or a device-local copy when workers share a GPU), ordered by stream memory
+ * operations — no SMs used. Processes on one node; id: 128 bytes from
+ * rtpb_ipc_unique_id() on rank 0, broadcast by the caller. Not capturable in
+ * a CUDA graph (the flags carry per-shift sequence numbers). */
+int rtpb_ipc_unique_id(void* out128);
+int rtpb_group_create_ipc(size_t n, size_t rank, int device, const void* id, rtpb_group* out);
 int rtpb_group_destroy(rtpb_group g);
 size_t rtpb_group_size(rtpb_group g);
 /* Local worker ranks hosted by this process (count returned, ranks written). */

@@ -52,7 +52,7 @@ void check_status(int code);
 enum class Mode { Train, Eval };
 enum class RotationMode { InPlace, OutOfPlace };
 enum class Direction { Clockwise, CounterClockwise };
-enum class TransportKind { Lockstep, Concurrent, Nccl };
+enum class TransportKind { Lockstep, Concurrent, Nccl, Ipc };
 enum class PayloadKind { Weight, WeightAndGrad };
 enum class DType { BF16 = RTPB_BF16, F32 = RTPB_F32 };
 inline size_t dtype_size(DType d) { return d == DType::F32 ? 4 : 2; }
@@ -131,8 +131,10 @@ class WorkerGroup {
   // the current device). kind: Lockstep (one host thread) or Concurrent
   // (a host thread per worker).
   WorkerGroup(size_t n, TransportKind kind, std::vector<int> devices = {});
-  // One process per GPU: this process is worker `rank` of `n`.
-  WorkerGroup(size_t n, size_t rank, int device, const void* nccl_unique_id);
+  // One process per GPU: this process is worker `rank` of `n`. kind Nccl:
+  // ncclSend/ncclRecv (unique id from ncclGetUniqueId); kind Ipc: copy-engine
+  // pushes through CUDA IPC mappings (unique id from rtpb_ipc_unique_id).
+  WorkerGroup(size_t n, size_t rank, int device, const void* unique_id, TransportKind kind = TransportKind::Nccl);
   ~WorkerGroup();
   WorkerGroup(const WorkerGroup&) = delete;
   WorkerGroup& operator=(const WorkerGroup&) = delete;

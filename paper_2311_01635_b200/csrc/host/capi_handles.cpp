@@ -3,6 +3,7 @@
 #include <nccl.h>
 
 #include <atomic>
+#include <cstdio>
 #include <cstring>
 
 #include "kernels/launch.hpp"
@@ -114,6 +115,25 @@ int rtpb_group_create_nccl(size_t n, size_t rank, int device, const void* nccl_i
   return guard([&] {
     auto h = std::make_unique<rtpb_group_s>();
     h->g = std::make_unique<WorkerGroup>(n, rank, device, nccl_id);
+    *out = h.release();
+  });
+}
+
+int rtpb_ipc_unique_id(void* out128) {
+  return guard([&] {
+    unsigned char b[128] = {};
+    FILE* f = std::fopen("/dev/urandom", "rb");
+    const size_t got = f ? std::fread(b, 1, sizeof b, f) : 0;
+    if (f) std::fclose(f);
+    if (got != sizeof b) throw ConfigError("rtpb_ipc_unique_id: /dev/urandom unavailable");
+    std::memcpy(out128, b, sizeof b);
+  });
+}
+
+int rtpb_group_create_ipc(size_t n, size_t rank, int device, const void* id, rtpb_group* out) {
+  return guard([&] {
+    auto h = std::make_unique<rtpb_group_s>();
+    h->g = std::make_unique<WorkerGroup>(n, rank, device, id, TransportKind::Ipc);
     *out = h.release();
   });
 }

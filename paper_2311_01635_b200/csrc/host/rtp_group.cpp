@@ -75,7 +75,12 @@ DeviceBuffer::DeviceBuffer(int device, size_t bytes, MemoryLedger* ledger, MemCa
     : bytes_(bytes), device_(device), ledger_(ledger), cat_(cat) {
   if (bytes == 0) return;
   DeviceGuard g(device);
-  cuda_check(cudaMalloc(&ptr_, bytes), "cudaMalloc");
+  // Whole 2 MiB pages: the driver packs smaller cudaMalloc allocations into a
+  // shared page block, and a CUDA IPC mapping covers the block, so two packed
+  // buffers could not both be mapped by a peer (the IPC transport exports
+  // receive buffers). The ledger keeps the requested size.
+  const size_t page = size_t(2) << 20;
+  cuda_check(cudaMalloc(&ptr_, (bytes + page - 1) / page * page), "cudaMalloc");
   if (zero) cuda_check(cudaMemset(ptr_, 0, bytes), "cudaMemset");
   if (ledger_) ledger_->on_alloc(cat_, bytes_);
 }
@@ -426,14 +431,17 @@ WorkerGroup::WorkerGroup(size_t n, TransportKind kind, std::vector<int> devices)
   transport_ = make_local_transport(*this, kind == TransportKind::Concurrent);
 }
 
-WorkerGroup::WorkerGroup(size_t n, size_t rank, int device, const void* nccl_id)
-    : n_(n), kind_(TransportKind::Nccl) {
+WorkerGroup::WorkerGroup(size_t n, size_t rank, int device, const void* unique_id, TransportKind kind)
+    : n_(n), kind_(kind) {
+  if (kind != TransportKind::Nccl && kind != TransportKind::Ipc)
+    throw ConfigError("one-process-per-worker groups use the NCCL or IPC transport");
   if (n == 0) throw ConfigError("worker group needs at least one worker");
   if (rank >= n) throw ConfigError("rank " + std::to_string(rank) + " out of range for " + std::to_string(n));
   workers_.resize(n);
   workers_[rank] = std::make_unique<Worker>(rank, device);
   local_.push_back(rank);
-  transport_ = make_nccl_transport(*this, rank, nccl_id);
+  transport_ = kind == TransportKind::Ipc ? make_ipc_transport(*this, rank, unique_id)
+                                          : make_nccl_transport(*this, rank, unique_id);
 }
 
 WorkerGroup::~WorkerGroup() {
@@ -521,7 +529,7 @@ void WorkerGroup::advance_slots(std::span<ShardSlot> slots, Direction dir, Paylo
   if (what == Corrupt::Tag && is_local(victim))
     throw ProtocolError("step tag mismatch at worker " + std::to_string(victim) + ": got " +
                         std::to_string(tag ^ 1) + ", expected " + std::to_string(tag));
-  if (kind_ == TransportKind::Nccl) {
+  if (kind_ == TransportKind::Nccl || kind_ == TransportKind::Ipc) {
     // SPMD: every rank holds the same offset, so the incoming id is the
     // sender's, i.e. ours shifted by one position against the direction.
     for (size_t r : local_) {

@@ -65,6 +65,21 @@ class WorkerGroup:
         check(lib.rtpb_group_create_nccl(n, rank, device, buf, C.byref(h)))
         return cls(n, _handle=h)
 
+    @staticmethod
+    def ipc_unique_id() -> bytes:
+        buf = C.create_string_buffer(128)
+        check(lib.rtpb_ipc_unique_id(buf))
+        return buf.raw
+
+    @classmethod
+    def ipc(cls, n: int, rank: int, device: int, unique_id: bytes) -> "WorkerGroup":
+        """One process per worker, copy-engine ring shifts through CUDA IPC
+        (processes on one node; workers may share a GPU)."""
+        h = C.c_void_p()
+        buf = C.create_string_buffer(bytes(unique_id), 128)
+        check(lib.rtpb_group_create_ipc(n, rank, device, buf, C.byref(h)))
+        return cls(n, _handle=h)
+
     def size(self) -> int:
         return self.n
 
