@@ -194,6 +194,11 @@ int rtpb_group_create_nccl(size_t n, size_t rank, int device, const void* nccl_i
  * a CUDA graph (the flags carry per-shift sequence numbers). */
 int rtpb_ipc_unique_id(void* out128);
 int rtpb_group_create_ipc(size_t n, size_t rank, int device, const void* id, rtpb_group* out);
+/* Measurement group: worker `rank` of an n-worker ring with no peers present;
+ * every ring shift is skipped (schedule, events, bookkeeping unchanged), so one
+ * GPU runs one rank's N-way step at its real shapes. Results are not the
+ * model's (shards do not move). */
+int rtpb_group_create_solo(size_t n, size_t rank, int device, rtpb_group* out);
 int rtpb_group_destroy(rtpb_group g);
 size_t rtpb_group_size(rtpb_group g);
 /* Local worker ranks hosted by this process (count returned, ranks written). */

@@ -52,7 +52,8 @@ void check_status(int code);
 enum class Mode { Train, Eval };
 enum class RotationMode { InPlace, OutOfPlace };
 enum class Direction { Clockwise, CounterClockwise };
-enum class TransportKind { Lockstep, Concurrent, Nccl, Ipc };
+// Solo: one rank of an n-rank ring with no peers (shifts skipped; measurement only).
+enum class TransportKind { Lockstep, Concurrent, Nccl, Ipc, Solo };
 enum class PayloadKind { Weight, WeightAndGrad };
 enum class DType { BF16 = RTPB_BF16, F32 = RTPB_F32 };
 inline size_t dtype_size(DType d) { return d == DType::F32 ? 4 : 2; }

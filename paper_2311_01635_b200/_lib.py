@@ -53,6 +53,7 @@ _SIGS = {
     "rtpb_group_create_nccl": (_int, [_sz, _sz, _int, _vp, _vpp]),
     "rtpb_ipc_unique_id": (_int, [_vp]),
     "rtpb_group_create_ipc": (_int, [_sz, _sz, _int, _vp, _vpp]),
+    "rtpb_group_create_solo": (_int, [_sz, _sz, _int, _vpp]),
     "rtpb_group_destroy": (_int, [_vp]),
     "rtpb_group_size": (_sz, [_vp]),
     "rtpb_group_local_ranks": (_sz, [_vp, C.POINTER(_sz)]),

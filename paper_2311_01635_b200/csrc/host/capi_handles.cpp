@@ -138,6 +138,14 @@ int rtpb_group_create_ipc(size_t n, size_t rank, int device, const void* id, rtp
   });
 }
 
+int rtpb_group_create_solo(size_t n, size_t rank, int device, rtpb_group* out) {
+  return guard([&] {
+    auto h = std::make_unique<rtpb_group_s>();
+    h->g = std::make_unique<WorkerGroup>(n, rank, device, nullptr, TransportKind::Solo);
+    *out = h.release();
+  });
+}
+
 int rtpb_group_destroy(rtpb_group g) {
   return guard([&] { group_release(g); });
 }

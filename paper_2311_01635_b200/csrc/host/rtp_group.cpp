@@ -407,6 +407,29 @@ class NcclTransport final : public Transport {
 
 }  // namespace
 
+namespace {
+// One rank of an n-rank ring with no peers present: every shift is skipped
+// (the schedule, events and bookkeeping run as under NCCL). Measurement only:
+// the per-GPU compute of an N-way step at its real shapes on one GPU.
+class SoloTransport final : public Transport {
+ public:
+  SoloTransport(WorkerGroup& g, size_t rank) : g_(g), rank_(rank) {}
+  void each(const std::function<void(size_t)>& fn) override {
+    DeviceGuard dg(g_.worker(rank_).device);
+    fn(rank_);
+  }
+  void shift(Direction, std::span<void* const>, std::span<void* const>, size_t) override {}
+
+ private:
+  WorkerGroup& g_;
+  size_t rank_;
+};
+}  // namespace
+
+std::unique_ptr<Transport> make_solo_transport(WorkerGroup& g, size_t rank) {
+  return std::make_unique<SoloTransport>(g, rank);
+}
+
 std::unique_ptr<Transport> make_local_transport(WorkerGroup& g, bool concurrent) {
   return std::make_unique<LocalTransport>(g, concurrent);
 }
@@ -433,15 +456,16 @@ WorkerGroup::WorkerGroup(size_t n, TransportKind kind, std::vector<int> devices)
 
 WorkerGroup::WorkerGroup(size_t n, size_t rank, int device, const void* unique_id, TransportKind kind)
     : n_(n), kind_(kind) {
-  if (kind != TransportKind::Nccl && kind != TransportKind::Ipc)
-    throw ConfigError("one-process-per-worker groups use the NCCL or IPC transport");
+  if (kind != TransportKind::Nccl && kind != TransportKind::Ipc && kind != TransportKind::Solo)
+    throw ConfigError("one-process-per-worker groups use the NCCL, IPC or Solo transport");
   if (n == 0) throw ConfigError("worker group needs at least one worker");
   if (rank >= n) throw ConfigError("rank " + std::to_string(rank) + " out of range for " + std::to_string(n));
   workers_.resize(n);
   workers_[rank] = std::make_unique<Worker>(rank, device);
   local_.push_back(rank);
-  transport_ = kind == TransportKind::Ipc ? make_ipc_transport(*this, rank, unique_id)
-                                          : make_nccl_transport(*this, rank, unique_id);
+  transport_ = kind == TransportKind::Ipc    ? make_ipc_transport(*this, rank, unique_id)
+               : kind == TransportKind::Solo ? make_solo_transport(*this, rank)
+                                             : make_nccl_transport(*this, rank, unique_id);
 }
 
 WorkerGroup::~WorkerGroup() {
@@ -529,7 +553,7 @@ void WorkerGroup::advance_slots(std::span<ShardSlot> slots, Direction dir, Paylo
   if (what == Corrupt::Tag && is_local(victim))
     throw ProtocolError("step tag mismatch at worker " + std::to_string(victim) + ": got " +
                         std::to_string(tag ^ 1) + ", expected " + std::to_string(tag));
-  if (kind_ == TransportKind::Nccl || kind_ == TransportKind::Ipc) {
+  if (kind_ == TransportKind::Nccl || kind_ == TransportKind::Ipc || kind_ == TransportKind::Solo) {
     // SPMD: every rank holds the same offset, so the incoming id is the
     // sender's, i.e. ours shifted by one position against the direction.
     for (size_t r : local_) {

@@ -59,6 +59,17 @@ int overlap_dx_sms(size_t M, size_t I, size_t per, bool gelu_bwd) {
 // transport the layers leave RTPB_NCCL_RESERVED_SMS (default 8) SMs free for
 // the rotation to progress under the GEMMs instead of queueing behind them.
 // The local transports move bytes with copy engines and reserve nothing.
+// Single-worker GEMM scheduling pays off while a step GEMM is a few waves of
+// 256 x 256 CTA-pair tiles (wave-quantisation tails, one GEMM not filling the
+// machine). For large GEMMs the plain per-step kernels on the whole machine
+// were measured faster (config (d), 16384 x 4096 x 16384: 1094 TFLOP/s plain,
+// 1071 fused, 1046 with dX || dW): beyond 12 waves the N = 1 fusions and the
+// dX || dW split are off.
+bool n1_scheduling_pays(size_t rows, size_t a, size_t b) {
+  const size_t tiles = ((rows + 255) / 256) * ((std::max(a, b) + 255) / 256);
+  return tiles <= size_t(12) * size_t(std::max(1, sm_budget() / 2));
+}
+
 class SmReserve {
  public:
   explicit SmReserve(const WorkerGroup& g) {
@@ -381,7 +392,7 @@ void RtpLinear::backward_ex(std::span<const DView> dy, size_t rows, std::span<co
   const bool oopm = oop();
   std::vector<void*> wp(n, nullptr), sp(n, nullptr), gp(n, nullptr);
 
-  if (n == 1 && dtype_ == DType::BF16 && !std::getenv("RTPB_NO_OVERLAP")) {
+  if (n == 1 && dtype_ == DType::BF16 && !std::getenv("RTPB_NO_OVERLAP") && n1_scheduling_pays(rows, in_, out_)) {
     // No rotation: dX and dW of the single step are independent GEMMs. dW
     // runs on the aux stream beside dX, each persistent kernel sized to its
     // share of the SMs, so neither pays a wave-quantisation tail alone.
@@ -575,7 +586,8 @@ void RtpMlp::ensure_fused(size_t rows) {
 
 void RtpMlp::forward(std::span<const DView> x, size_t rows, std::span<const DView> y, Mode mode) {
   ensure_acts(rows);
-  if (group_->size() == 1 && dtype_ == DType::BF16 && !std::getenv("RTPB_NO_FUSED_FWD")) {
+  if (group_->size() == 1 && dtype_ == DType::BF16 && !std::getenv("RTPB_NO_FUSED_FWD") &&
+      n1_scheduling_pays(rows, h_, f_)) {
     // N = 1: no rotation between ffn1 and ffn2, so both GEMMs run as one
     // scheduled persistent launch (ffn2's row blocks start as soon as ffn1
     // has written them); the layers keep their reference bookkeeping.
@@ -640,7 +652,8 @@ void RtpMlp::ensure_fused_bwd(size_t rows) {
 }
 
 void RtpMlp::backward(std::span<const DView> dy, size_t rows, std::span<const DView> dx) {
-  if (group_->size() == 1 && dtype_ == DType::BF16 && !std::getenv("RTPB_NO_FUSED_BWD")) {
+  if (group_->size() == 1 && dtype_ == DType::BF16 && !std::getenv("RTPB_NO_FUSED_BWD") &&
+      n1_scheduling_pays(rows, h_, f_)) {
     // N = 1: the four backward GEMMs as two concurrent scheduled launches
     // (dX chain on compute, dW pair on aux); ffn1's dW streams dpre row blocks
     // as the dX launch publishes them.

@@ -82,6 +82,7 @@ class Transport {
 std::unique_ptr<Transport> make_local_transport(WorkerGroup& g, bool concurrent);
 std::unique_ptr<Transport> make_nccl_transport(WorkerGroup& g, size_t rank, const void* nccl_id);
 std::unique_ptr<Transport> make_ipc_transport(WorkerGroup& g, size_t rank, const void* unique_id);
+std::unique_ptr<Transport> make_solo_transport(WorkerGroup& g, size_t rank);
 
 inline size_t ring_dest(size_t r, size_t n, Direction d) {
   return d == Direction::Clockwise ? (r + 1) % n : (r + n - 1) % n;

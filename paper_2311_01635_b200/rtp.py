@@ -80,6 +80,13 @@ class WorkerGroup:
         check(lib.rtpb_group_create_ipc(n, rank, device, buf, C.byref(h)))
         return cls(n, _handle=h)
 
+    @classmethod
+    def solo(cls, n: int, rank: int = 0, device: int = 0) -> "WorkerGroup":
+        """Measurement: rank `rank` of an n-worker ring, no peers, shifts skipped."""
+        h = C.c_void_p()
+        check(lib.rtpb_group_create_solo(n, rank, device, C.byref(h)))
+        return cls(n, _handle=h)
+
     def size(self) -> int:
         return self.n
 

@@ -37,6 +37,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="b", choices=sorted(CONFIGS))
     ap.add_argument("--simulate", type=int, default=0)
+    ap.add_argument("--solo", type=int, default=0,
+                    help="one rank of an N-way ring on GPU 0, shifts skipped: per-GPU compute at N-way shapes")
     ap.add_argument("--mode", default="outofplace", choices=["inplace", "outofplace"])
     ap.add_argument("--blocks", type=int, default=None)
     ap.add_argument("--tokens-per-worker", type=int, default=None)
@@ -52,7 +54,12 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     dist = None
-    if args.simulate:
+    if args.solo:
+        n = args.solo
+        torch.cuda.set_device(0)
+        grp = rtp.WorkerGroup.solo(n, 0, 0)
+        how = f"solo: rank 0 of a {n}-way ring on one GPU, shifts skipped (per-GPU compute only)"
+    elif args.simulate:
         n = args.simulate
         torch.cuda.set_device(0)
         grp = rtp.WorkerGroup(n, "lockstep", devices=[0] * n)
@@ -136,6 +143,8 @@ def main():
         _lib.lib.rtpb_debug_skip_comm(0)
 
     flops = 12.0 * T * h * f * blocks
+    if args.solo:
+        flops /= n  # one rank's share
     wb = (h * f + f + f * h + h) * 2 * blocks  # bf16 weights, whole model
     gb = (h * f + f + f * h + h) * 4 * blocks  # fp32 gradients
     led = [grp.ledger(r) for r in ranks]
@@ -146,7 +155,7 @@ def main():
             "tokens_per_worker": M, "global_tokens": T, "steps": args.steps,
             "ms_per_step": ms, "ms_per_step_compute_only": ms_nocomm,
             "exposed_comm_ms": max(0.0, ms - ms_nocomm), "exposed_comm_frac": max(0.0, ms - ms_nocomm) / ms,
-            "tflops_whole_group": flops / (ms * 1e-3) / 1e12,
+            "tflops_whole_group" if not args.solo else "tflops_per_gpu": flops / (ms * 1e-3) / 1e12,
             "rotation_bytes_sent_per_gpu": bytes_sent,
             "memory_per_worker": {
                 "peak_param": worst["peak_param"], "peak_grad": worst["peak_grad"], "peak_comm": worst["peak_comm"],
@@ -154,6 +163,14 @@ def main():
                 "peak_total_ledger": worst["peak_total"], "param_grad_comm": pgc,
                 "model_inplace": (wb + gb) / n, "model_outofplace": (wb + gb + max(wb, gb)) / n,
                 "vs_model": pgc / ((wb + gb + (max(wb, gb) if args.mode == "outofplace" and n > 1 else 0)) / n)}}
+    if args.solo:
+        # projected N-GPU step from the measured per-GPU compute and the ring
+        # bytes over NVLink 5 (900 GB/s per direction): perfect / no overlap
+        t_nvl = bytes_sent / 900e9 * 1e3
+        line["projection"] = {"nvlink_ms": t_nvl, "step_ms_overlapped": max(ms, t_nvl),
+                              "step_ms_serial": ms + t_nvl,
+                              "tflops_per_gpu_overlapped": flops / (max(ms, t_nvl) * 1e-3) / 1e12,
+                              "note": "measured compute of one rank; rotation bytes modelled, not measured"}
     if rank == 0:
         print(json.dumps(line), flush=True)
         if args.out:
