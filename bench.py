@@ -188,6 +188,9 @@ def main():
     ap.add_argument("--eager", action="store_true", help="time host-issued launches instead of a CUDA graph")
     ap.add_argument("--transport", default="nccl", choices=["nccl", "ipc"],
                     help="N > 1 ring shift: ncclSend/ncclRecv (default) or copy-engine pushes through CUDA IPC")
+    ap.add_argument("--solo", type=int, default=0,
+                    help="measurement: rank 0 of an N-way ring on this GPU, shifts skipped (per-GPU compute at "
+                         "N-way shapes, plus the rotation bytes over NVLink as a model)")
     ap.add_argument("--same-device", action="store_true",
                     help="test mode: every rank on GPU 0 (IPC transport, gloo plumbing); numbers not meaningful")
     args = ap.parse_args()
@@ -221,6 +224,8 @@ def main():
         grp = make(world, rank, local, box[0])
         if args.transport == "ipc":
             args.eager = True  # the IPC flags carry per-shift sequence numbers: no graph replay
+    elif args.solo > 1:
+        grp = rtp.WorkerGroup.solo(args.solo, 0, local)
     else:
         grp = rtp.WorkerGroup(1)
 
@@ -232,6 +237,7 @@ def main():
         return float(t.item())
     M = args.tokens_per_gpu
     T = M * world
+    ring = args.solo if args.solo > 1 else world  # ring size the layers are sharded for
     mlp = rtp.RtpMlp(grp, "block0", H, F, "bf16", seed=SEED, stream_base=0)  # Flyweight init on device
     mlp.set_rotation_mode(args.mode)
     mlp.begin_step()
@@ -392,12 +398,12 @@ def main():
     torch_peak = torch.cuda.max_memory_allocated(dev) - flush.numel() * 4
     shard_w = mlp.ffn1.shard_len() * 2 + mlp.ffn2.shard_len() * 2
     shard_g = mlp.ffn1.shard_len() * 4 + mlp.ffn2.shard_len() * 4
-    W_total, G_total = shard_w * world, shard_g * world
+    W_total, G_total = shard_w * ring, shard_g * ring
     mem = {"peak_hbm_bytes_per_gpu": led["peak_total"] + torch_peak,
            "ledger_peak": {k[5:]: v for k, v in led.items() if k.startswith("peak_")},
            "caller_activations_bytes": torch_peak,
-           "model_inplace_bytes": (W_total + G_total) // world,
-           "model_outofplace_bytes": (W_total + G_total + max(W_total, G_total)) // world,
+           "model_inplace_bytes": (W_total + G_total) // ring,
+           "model_outofplace_bytes": (W_total + G_total + max(W_total, G_total)) // ring,
            "param_grad_comm_bytes": led["peak_param"] + led["peak_grad"] + led["peak_comm"]}
 
     # ---- exposed rotation time: T(step) - T(step without moving bytes)
@@ -424,8 +430,8 @@ def main():
                    "method": "eager steps with and without rtpb_debug_skip_comm (same schedule, no bytes moved), "
                              "max over ranks"}
     nvl_bw = 900e9  # NVLink 5 per direction per GPU
-    w_all = (mlp.ffn1.shard_len() + mlp.ffn2.shard_len()) * world
-    sent = (world - 1) / world * (2 * w_all * 2 + w_all * 4) if world > 1 else 0.0  # bf16 W fwd+bwd, fp32 G bwd
+    w_all = (mlp.ffn1.shard_len() + mlp.ffn2.shard_len()) * ring
+    sent = (ring - 1) / ring * (2 * w_all * 2 + w_all * 4) if ring > 1 else 0.0  # bf16 W fwd+bwd, fp32 G bwd
     t_gemm_peak = flops_per_step(T) / world / (burst * 1e12) * 1e3
     t_nvl = sent / nvl_bw * 1e3
     step_roofline = {"gemm_ms_at_peak": t_gemm_peak, "nvlink_ms": t_nvl, "bytes_sent_per_gpu": sent,
@@ -504,7 +510,7 @@ def main():
 
     if rank == 0:
         cpu = None
-        if world == 1 and not args.no_cpu_baseline:
+        if world == 1 and not args.no_cpu_baseline and not args.solo:
             try:
                 cpu = cpu_reference(target_s=12.0)
             except Exception as exc:  # noqa
@@ -516,7 +522,8 @@ def main():
                 "config": {"workload": "rtp_mlp_768x3072x768 (config b)", "h": H, "f": F,
                            "tokens_per_gpu": M, "global_tokens": T, "rotation_mode": args.mode,
                            "parallelism": f"rtp{world}", "transport": args.transport if world > 1 else None,
-                           "same_device_test": bool(args.same_device and world > 1), "l2": "flushed before every timed step (512 MiB written, then read back)",
+                           "same_device_test": bool(args.same_device and world > 1),
+                           "solo_ring": args.solo if args.solo > 1 else None, "l2": "flushed before every timed step (512 MiB written, then read back)",
                            "flops_per_step": flops_per_step(T)},
                 "tflops_per_gpu": value / world,
                 "gpu_launches": int(launches),

@@ -240,6 +240,21 @@ int dispatch_tile(int code, const Op& a, const Op& b, const Out& c0, const Out* 
   return launch_cfg<GemmCfg<EPI, 128, TF32, kEpiWarps, AMN, BMN>>(a, b, c0, c1, args, s);
 }
 
+// Tile raster: keep one operand L2-resident when it fits (n fastest when all
+// of B does: A is streamed once; m fastest when all of A does), else a grouped
+// raster over 8 row blocks, whose A and B panels (8 and ~9 of them for a
+// machine-wide wave) fit L2 together instead of re-streaming a whole operand
+// per wave from HBM.
+int raster_mode(int M, int N, int K, int tile_m, int bn, bool f32, bool prefer_m) {
+  const double esz = f32 ? 4.0 : 2.0;
+  const double a_bytes = double((M + tile_m - 1) / tile_m) * tile_m * K * esz;
+  const double b_bytes = double((N + bn - 1) / bn) * bn * K * esz;
+  if (prefer_m && a_bytes < 48e6) return 0;
+  if (b_bytes < 48e6) return 1;
+  if (a_bytes < 48e6) return 0;
+  return 8;
+}
+
 // Tile code (and, for dW, the split-K factor written into args.k_splits).
 template <int EPI>
 int pick_code(bool tf32, GemmArgs& args, int force) {
@@ -270,14 +285,10 @@ int dispatch(bool tf32, const Op& a, const Op& b, const Out& c0, const Out* c1, 
   const int code = pick_code<EPI>(tf32, args, force);
   const int bn = code % 1000;
   const int num_n = (args.N + bn - 1) / bn;
-  // Raster n fastest when the B operand (all n-blocks x K) fits comfortably in
-  // L2: concurrent CTAs then share each A row-block, which is read once.
-  const double b_bytes = double(num_n) * bn * args.K * (tf32 ? 4.0 : 2.0);
-#ifdef RTPB_WGRAD_NFAST  // dev A/B
-  args.n_fastest = b_bytes < 48e6;
-#else
-  args.n_fastest = (EPI != EPI_WGRAD) && b_bytes < 48e6;
-#endif
+  (void)num_n;
+  const int tile_m = code > 1000 ? 256 : 128;
+  // (dW keeps m fastest while its A fits: measured neutral-to-better there)
+  args.n_fastest = raster_mode(args.M, args.N, args.K, tile_m, bn, tf32, EPI == EPI_WGRAD);
   return tf32 ? dispatch_tile<EPI, true>(code, a, b, c0, c1, args, s)
               : dispatch_tile<EPI, false>(code, a, b, c0, c1, args, s);
 }
@@ -753,8 +764,7 @@ int gemm_dgrad(bool f32, const StepDgrad& p, cudaStream_t s) {
     Out pre{p.pre, f32, p.I, p.M, p.ldpre};
     int code = p.force_bn ? p.force_bn : choose_tile(g.M, g.N, f32);
     const int bn = (!f32 && code == 1256) ? 256 : 128;
-    const int num_n = (g.N + bn - 1) / bn;
-    g.n_fastest = double(num_n) * bn * g.K * (f32 ? 4.0 : 2.0) < 48e6;
+    g.n_fastest = raster_mode(g.M, g.N, g.K, bn == 256 ? 256 : 128, bn, f32, false);
     if (f32) return launch_cfg<GemmCfg<EPI_DGRAD, 128, true, kEpiWarps, false, false, true>>(a, b, c0, &pre, g, s);
     if (bn == 256)
       return launch_cfg<GemmCfg<EPI_DGRAD, 256, false, kEpiWarps, false, false, true, true>>(a, b, c0, &pre, g, s);

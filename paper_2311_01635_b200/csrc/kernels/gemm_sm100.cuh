@@ -44,7 +44,7 @@ enum EpiFlags : int {
 struct GemmArgs {
   int M, N, K;
   int flags;
-  int n_fastest;       // tile raster: n-block fastest (A streamed once)
+  int n_fastest;       // tile raster: 0 m fastest, 1 n fastest (A streamed once), >= 2 grouped (that many row blocks)
   const void* aux;     // FWD: bias (dtype, N values) | DGRAD: pre (dtype, M x N, ld_aux)
   int64_t ld_aux;
   const float* acc;    // DGRAD LAST && !FIRST: fp32 accumulator read (M x N, ld_acc)
@@ -427,7 +427,16 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
       x.split = it / num_tiles;
     }
     const int nm = x.prob ? num_m2 : num_m, nn = x.prob ? num_n2 : num_n;
-    if (x.prob ? args.n_fastest2 : args.n_fastest) {
+    const int nf = x.prob ? args.n_fastest2 : args.n_fastest;
+    if (nf >= 2) {
+      // grouped raster: nf row blocks at a time, n fastest within the group,
+      // so the concurrent tiles share a few A row panels and B column panels
+      const int first_m = (x.t / (nf * nn)) * nf;
+      const int gsz = min(nm - first_m, nf);
+      const int r = x.t % (nf * nn);
+      x.mb = first_m + r % gsz;
+      x.nb = r / gsz;
+    } else if (nf) {
       x.nb = x.t % nn;
       x.mb = x.t / nn;
     } else {
