@@ -70,6 +70,33 @@ bool n1_scheduling_pays(size_t rows, size_t a, size_t b) {
   return tiles <= size_t(12) * size_t(std::max(1, sm_budget() / 2));
 }
 
+// N > 1 (one worker per GPU): SMs for dX when a step's dX and dW run side by
+// side (dW on the aux stream). dX accumulates into an fp32 rows x I buffer,
+// 8 bytes of HBM traffic per element per step whatever its K (= per), so for
+// small per it is HBM-bound while dW stays tensor-bound: sharing
+// the SMs overlaps the two. Model: 1.5 PFLOP/s over all SMs, 6 TB/s HBM;
+// returns 0 (no split) unless the split step is >= 10 % faster.
+int nway_dx_sms(size_t rows, size_t I, size_t per) {
+  if (std::getenv("RTPB_NO_OVERLAP")) return 0;
+  if (const char* e = std::getenv("RTPB_NWAY_DX_SMS")) return std::atoi(e);
+  const int all = sm_budget();
+  const double flops = 2.0 * double(rows) * double(I) * double(per);
+  const double p_sm = 1.5e15 / 148.0, rmw = 8.0 * double(rows) * double(I) / 6e12;
+  auto t_dx = [&](int d) { return std::max(flops / (p_sm * d), rmw); };
+  auto t_dw = [&](int w) { return flops / (p_sm * w); };
+  const double seq = t_dx(all) + t_dw(all);
+  double best = seq;
+  int best_d = 0;
+  for (int d = 16; d <= all - 16; d += 2) {
+    const double t = std::max(t_dx(d), t_dw(all - d));
+    if (t < best) {
+      best = t;
+      best_d = d;
+    }
+  }
+  return best < 0.9 * seq ? best_d : 0;
+}
+
 class SmReserve {
  public:
   explicit SmReserve(const WorkerGroup& g) {
@@ -434,6 +461,15 @@ void RtpLinear::backward_ex(std::span<const DView> dy, size_t rows, std::span<co
     return;
   }
 
+  // One worker per GPU with an HBM-bound dX: dW runs on the aux stream beside
+  // it, each on its share of the SMs; the travelling gradient is then ordered
+  // after aux (its writer) instead of compute.
+  const bool distributed = group_->kind() == TransportKind::Nccl || group_->kind() == TransportKind::Ipc ||
+                           group_->kind() == TransportKind::Solo;
+  const int all_sms = sm_budget();
+  const int dx_sms = (n > 1 && distributed && dtype_ == DType::BF16) ? nway_dx_sms(rows, in_, per_) : 0;
+  if (dx_sms)
+    for (size_t r : local) group_->worker(r).fork_aux();
   for (size_t s = 0; s < n; ++s) {
     group_->each([&](size_t r) {
       const size_t j = slots_[r].logical_id;
@@ -456,6 +492,7 @@ void RtpLinear::backward_ex(std::span<const DView> dy, size_t rows, std::span<co
       for (size_t r : local) group_->worker(r).record(Ev::WDone, true);
     }
     // dX (+)= dY_j . W_j^T
+    if (dx_sms) set_sm_budget(dx_sms);
     group_->each([&](size_t r) {
       Worker& w = group_->worker(r);
       const size_t k = k_of[r];
@@ -482,11 +519,16 @@ void RtpLinear::backward_ex(std::span<const DView> dy, size_t rows, std::span<co
     }
     if (s > 0) {
       // dW accumulates into the travelling gradient shard: wait for its arrival.
-      for (size_t r : local) group_->worker(r).wait(Ev::GDone, false);
+      for (size_t r : local) {
+        Worker& w = group_->worker(r);
+        w.wait_on(Ev::GDone, dx_sms ? w.aux : w.compute);
+      }
     }
     // G_j += X^T . dY_j (+ bias column sums), in place on the resident shard.
+    if (dx_sms) set_sm_budget(all_sms - dx_sms);
     group_->each([&](size_t r) {
       Worker& w = group_->worker(r);
+      const cudaStream_t ws = dx_sms ? w.aux : w.compute;
       const size_t k = k_of[r];
       const size_t j = slots_[r].logical_id;
       float* g = static_cast<float*>(slots_[r].grad_acc.data());
@@ -494,10 +536,19 @@ void RtpLinear::backward_ex(std::span<const DView> dy, size_t rows, std::span<co
       const float* g_in = (grads_zero_pending_ && s == 0) ? nullptr : g;
       check_status(rtpb_wgrad_step(dt, x_cache_[r].data, x_cache_[r].ld ? x_cache_[r].ld : in_, dy[k].data,
                                    dy[k].ld ? dy[k].ld : out_, j * per_, g_in, g, rows, in_, per_,
-                                   workspace_[r].data(), workspace_[r].bytes(), w.compute));
+                                   workspace_[r].data(), workspace_[r].bytes(), ws));
     });
+    if (dx_sms) set_sm_budget(all_sms);
     if (!rotate) break;
-    group_->comm_after_compute();
+    if (dx_sms) {
+      for (size_t r : local) {  // the gradient's writer is aux
+        Worker& w = group_->worker(r);
+        w.record_on(Ev::AuxDone, w.aux);
+        w.wait_on(Ev::AuxDone, w.comm);
+      }
+    } else {
+      group_->comm_after_compute();
+    }
     for (size_t r : local) gp[r] = slots_[r].grad_acc.data();
     group_->exchange(Direction::CounterClockwise, gp, gp, slots_[local[0]].grad_acc.bytes());
     for (size_t r : local) group_->worker(r).record(Ev::GDone, true);

@@ -25,7 +25,8 @@ void cuda_check(cudaError_t e, const char* where);
 // work; WDone / GDone: completion of the latest weight / gradient exchange.
 // Fork / Join: compute <-> aux stream hand-offs (N = 1 dX || dW overlap).
 enum class Ev : int {
-  Compute = 0, WDone = 1, GDone = 2, Comm = 3, Ready = 4, Consumed = 5, Staged = 6, Fork = 7, Join = 8, kCount = 9
+  Compute = 0, WDone = 1, GDone = 2, Comm = 3, Ready = 4, Consumed = 5, Staged = 6, Fork = 7, Join = 8, AuxDone = 9,
+  kCount = 10
 };
 
 struct Worker {
@@ -60,6 +61,9 @@ struct Worker {
     cuda_check(cudaStreamWaitEvent(compute, ev[int(Ev::Join)], 0), "wait join");
     aux_pending = false;
   }
+  // Generic record / wait on any of this worker's streams.
+  void record_on(Ev e, cudaStream_t s) { cuda_check(cudaEventRecord(ev[int(e)], s), "record"); }
+  void wait_on(Ev e, cudaStream_t s) { cuda_check(cudaStreamWaitEvent(s, ev[int(e)], 0), "wait"); }
   // Staging for an in-place shift of `bytes`: one chunk, charged as CommBuffer.
   void* staging(size_t bytes, size_t* chunk);
 };

@@ -17,12 +17,13 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def spawn(case, n, mode, tmp_path):
+def spawn(case, n, mode, tmp_path, env=None):
     from paper_2311_01635_b200 import rtp
     uid = rtp.WorkerGroup.ipc_unique_id().hex()
     outs = [str(tmp_path / f"{case}_{mode}_{n}_{r}.npz") for r in range(n)]
     procs = [subprocess.Popen([sys.executable, os.path.join(ROOT, "tests", "ipc_worker.py"), case, str(n), str(r),
-                               uid, mode, outs[r]], stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)
+                               uid, mode, outs[r]], stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True,
+                              env={**os.environ, **(env or {})})
              for r in range(n)]
     logs = []
     for p in procs:
@@ -72,3 +73,17 @@ def test_mlp_multiprocess_ipc(golden, tmp_path, n):
     for r in range(n):
         assert np.array_equal(res[r]["grad1"], ref["grads1"][r]) and np.array_equal(res[r]["grad2"], ref["grads2"][r])
     assert nerr(y, g[f"n{n}_y"]) < TOL["bf16"] and nerr(dx, g[f"n{n}_dx"]) < TOL["bf16"]
+
+
+def test_mlp_multiprocess_ipc_dx_dw_side_by_side(golden, tmp_path):
+    """One worker per GPU with dW on the aux stream beside dX (forced split of
+    the SMs): the gradient shard's ordering moves from compute to aux."""
+    g = golden("mlp")
+    n = 2
+    res = spawn("mlp", n, "outofplace", tmp_path, env={"RTPB_NWAY_DX_SMS": "74"})
+    y = np.concatenate([r["y"] for r in res])
+    dx = np.concatenate([r["dx"] for r in res])
+    assert nerr(y, g[f"n{n}_y"]) < TOL["bf16"] and nerr(dx, g[f"n{n}_dx"]) < TOL["bf16"]
+    for r in range(n):
+        assert nerr(res[r]["grad1"], g[f"n{n}_grads1"][r]) < TOL["bf16"]
+        assert nerr(res[r]["grad2"], g[f"n{n}_grads2"][r]) < TOL["bf16"]
