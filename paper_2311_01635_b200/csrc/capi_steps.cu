@@ -49,14 +49,19 @@ int check_geom(size_t M, size_t I, size_t per) {
 cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
 
 // Zero-initialised, self-resetting part of a step workspace.
-size_t split_flag_bytes(size_t I, size_t per) { return ((I + 255) / 256) * ((per + 255) / 256) * sizeof(unsigned); }
+// (16 per tile: one per epilogue warp slot of a CTA pair, for the split-K
+// partials' per-region counters; the ordered split-K uses the first.)
+size_t split_flag_bytes(size_t I, size_t per) {
+  return ((I + 255) / 256) * ((per + 255) / 256) * 16 * sizeof(unsigned);
+}
 // Fused dW bias sums (CTA-pair dW): arrival counter per 64-column group, and
 // one partial row per (256-row tile block, K split <= 8).
 size_t bias_tick_bytes(size_t per) { return ((per + 63) / 64) * sizeof(unsigned); }
 size_t bias_part_bytes(size_t I, size_t per) { return ((I + 255) / 256) * 8 * per * sizeof(float); }
 size_t persistent_ws_bytes(size_t M, size_t I, size_t per) {
   return align256(colsum_workspace_bytes(M, per)) + align256(split_flag_bytes(I, per)) +
-         align256(bias_tick_bytes(per)) + align256(bias_part_bytes(I, per));
+         align256(bias_tick_bytes(per)) + align256(bias_part_bytes(I, per)) +
+         align256(wgrad_partial_floats(false, M, I, per) * sizeof(float));
 }
 
 // Optional per-launch timing of the step GEMMs: a CUDA event pair recorded on
@@ -144,16 +149,21 @@ int fused_bwd_step(FusedBwdArgs a, void* ws1, size_t ws1_bytes, void* ws2, size_
   int rc;
   if ((rc = check_geom(a.M, a.h, a.f))) return rc;
   // each layer's persistent workspace part, carved as rtpb_wgrad_step does
-  auto carve = [&](void* w, size_t bytes, size_t I, size_t per, float** part, unsigned** tick, unsigned** flags) {
+  auto carve = [&](void* w, size_t bytes, size_t I, size_t per, float** part, unsigned** tick, unsigned** flags,
+                   float** wpart) {
     Carve c{static_cast<char*>(w), w ? bytes : 0};
     c.take(colsum_workspace_bytes(a.M, per) / sizeof(float));
     *flags = reinterpret_cast<unsigned*>(c.take(split_flag_bytes(I, per) / sizeof(float)));
     *tick = reinterpret_cast<unsigned*>(c.take(bias_tick_bytes(per) / sizeof(float)));
     *part = c.take(bias_part_bytes(I, per) / sizeof(float));
+    const size_t wpf = wgrad_partial_floats(false, a.M, I, per);
+    // the layer's partial buffer holds its own (whole-machine) split count
+    if (plan.w_splits > 1 && size_t(plan.w_splits) * ((I + 255) / 256 * 256) * per > wpf) return false;
+    *wpart = wpf ? c.take(wpf) : nullptr;
     return c.ok;
   };
-  if (!carve(ws1, ws1_bytes, a.h, a.f, &a.bias_part1, &a.bias_tick1, &a.split_flags1) ||
-      !carve(ws2, ws2_bytes, a.f, a.h, &a.bias_part2, &a.bias_tick2, &a.split_flags2))
+  if (!carve(ws1, ws1_bytes, a.h, a.f, &a.bias_part1, &a.bias_tick1, &a.split_flags1, &a.wpart1) ||
+      !carve(ws2, ws2_bytes, a.f, a.h, &a.bias_part2, &a.bias_tick2, &a.split_flags2, &a.wpart2))
     return set_error(RTPB_ERR_DIMENSION, "fused backward: layer workspace too small");
   // profiled as the two launches: D (both dX GEMMs) and W (both dW GEMMs)
   const double fl = 2.0 * double(a.M) * double(a.h) * double(a.f) * 2.0;
@@ -290,10 +300,13 @@ int rtpb_wgrad_step(int dtype, const void* x, size_t ldx, const void* dy, size_t
   unsigned* flags = reinterpret_cast<unsigned*>(c.take(split_flag_bytes(I, per) / sizeof(float)));
   unsigned* btick = reinterpret_cast<unsigned*>(c.take(bias_tick_bytes(per) / sizeof(float)));
   float* bpart = c.take(bias_part_bytes(I, per) / sizeof(float));
+  const size_t wpf = f32 ? 0 : wgrad_partial_floats(false, M, I, per);
+  float* wpart = wpf ? c.take(wpf) : nullptr;
   StepWgrad p{};
   p.x = x; p.ldx = ldx; p.dy = static_cast<const char*>(dy) + col0 * esz; p.ldy = ldy;
   p.g_in = g_in; p.g_out = g_out; p.M = M; p.I = I; p.per = per; p.force_bn = g_force_bn;
   p.split_flags = flags;
+  p.wpart = wpart;
   if (f32) {
     const size_t Mp = (M + 7) & ~size_t(7);
     float *xh = c.take(Mp * I), *xl = c.take(Mp * I), *dh = c.take(Mp * per), *dl = c.take(Mp * per);

@@ -690,9 +690,13 @@ int gemm_bwd_fused(const FusedBwdArgs& a, const FusedBwdPlan& plan, const FusedB
     Out g2{a.g2, true, h, f, h};
     Op a1{a.x, nullptr, h, M, a.ldx}, b1{a.pre, nullptr, f, M, f};
     Out g1{a.g1, true, f, h, f};
+    const bool par = plan.w_splits > 1 && a.wpart1 && a.wpart2;
+    const size_t fpad = (f + 255) / 256 * 256, hpad = (h + 255) / 256 * 256;
+    Out part2{par ? static_cast<const void*>(a.wpart2) : a.g2, true, h, par ? plan.w_splits * fpad : f, h};
+    Out part1{par ? static_cast<const void*>(a.wpart1) : a.g1, true, f, par ? plan.w_splits * hpad : h, f};
     GemmMaps m1;
     int rc;
-    if ((rc = encode_maps<FusedWCfg>(a1, b1, g1, nullptr, m1))) return rc;
+    if ((rc = encode_maps<FusedWCfg>(a1, b1, g1, &part1, m1))) return rc;
     GemmArgs g{};
     g.M = int(f); g.N = int(h); g.K = int(M);
     g.flags = a.g2_zero ? EF_FIRST : 0;
@@ -707,7 +711,12 @@ int gemm_bwd_fused(const FusedBwdArgs& a, const FusedBwdPlan& plan, const FusedB
     g.bias_part2 = a.bias_part1; g.bias_tick2 = a.bias_tick1;
     g.dep_count = ws.dep_count; g.dep_target = plan.dep_target; g.dep_rows = plan.dep_rows; g.dep_on_k = 1;
     g.done_ctas = ws.done_ctas; g.done_target = done_target;
-    if ((rc = launch_cfg<FusedWCfg>(a0, b0, g2, nullptr, g, aux, &m1, plan.slots_w))) return rc;
+    if (par) {
+      g.wpar = 1;
+      g.wpart = a.wpart2; g.wpart_rows = int(fpad);
+      g.wpart2 = a.wpart1; g.wpart_rows2 = int(hpad);
+    }
+    if ((rc = launch_cfg<FusedWCfg>(a0, b0, g2, &part2, g, aux, &m1, plan.slots_w))) return rc;
   }
   return RTPB_OK;
 }
@@ -800,7 +809,41 @@ int gemm_wgrad(bool f32, const StepWgrad& p, cudaStream_t s) {
   g.gbias_out = p.gbias_out;
   g.bias_part = p.bias_part;
   g.bias_tick = p.bias_tick;
+  if (p.wpart && !f32) {
+    // split-K partials: one (I rounded up to 256) x per fp32 block per split
+    const size_t ipad = (p.I + 255) / 256 * 256;
+    const int smax = wgrad_splits(f32, p.M, p.I, p.per, p.force_bn);
+    Out part{p.wpart, true, p.per, size_t(smax) * ipad, p.per};
+    g.wpar = 1;
+    g.wpart = p.wpart;
+    g.wpart_rows = int(ipad);
+    return dispatch<EPI_WGRAD>(f32, a, b, c0, &part, g, s, p.force_bn);
+  }
   return dispatch<EPI_WGRAD>(f32, a, b, c0, nullptr, g, s, p.force_bn);
+}
+
+int wgrad_splits(bool f32, size_t M, size_t I, size_t per, int force_bn) {
+  GemmArgs g{};
+  g.M = int(I);
+  g.N = int(per);
+  g.K = int(M);
+  unsigned dummy = 0;
+  g.split_flags = &dummy;
+  const int saved = t_sm_budget;
+  t_sm_budget = 0;  // the whole machine: the most splits any budget can ask for
+  pick_code<EPI_WGRAD>(f32, g, force_bn);
+  t_sm_budget = saved;
+  return g.k_splits > 1 ? g.k_splits : 1;
+}
+
+size_t wgrad_partial_floats(bool f32, size_t M, size_t I, size_t per) {
+  // Unordered split-K partials are opt-in (RTPB_WGRAD_PAR): measured slower
+  // than the ordered chain (config (b) dW 72 vs 45 us; 8 splits 114 us), the
+  // completing warp's fold of the partials being latency-bound.
+  static const bool on = std::getenv("RTPB_WGRAD_PAR") != nullptr;
+  if (!on) return 0;
+  const int S = wgrad_splits(f32, M, I, per, 0);
+  return S > 1 ? size_t(S) * ((I + 255) / 256 * 256) * per : 0;
 }
 
 bool wgrad_fuses_bias(bool f32, size_t M, size_t I, size_t per, unsigned* split_flags, int force_bn) {

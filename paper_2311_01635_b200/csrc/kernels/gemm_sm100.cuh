@@ -98,6 +98,15 @@ struct GemmArgs {
   // sharing dep_count / done_ctas across launches (0: this grid).
   int dep_on_k;
   unsigned done_target;
+  // dW split over K without an ordered chain (wpar): every split stores its
+  // fp32 partial into map c1 (rows split * wpart_rows + row, wpart_rows = M
+  // rounded up to the tile height) and counts in on its region's counter
+  // (split_flags[tile * 16 + warp slot]); the warp that completes a region sums
+  // the partials in split order and adds them into G once. Deterministic.
+  int wpar;
+  int wpart_rows, wpart_rows2;
+  const float* wpart;
+  const float* wpart2;
   unsigned* dep_count;
   unsigned dep_target;
   int dep_rows;
@@ -141,7 +150,10 @@ struct GemmCfg {
   // (accumulator steps), WGRAD always does.
   static constexpr int NOUT = EPI == EPI_FWD ? 2 : 1;
   static constexpr int STG_ONE = 32 * 32 * (EPI == EPI_FWD ? ELEM : 4);
-  static constexpr int STG_WARP = NOUT * STG_ONE;
+  // dW: two fp32 staging buffers per warp, so a chunk's reduce-add into the
+  // travelling gradient is in flight while the next chunk is staged.
+  static constexpr int STG_BUFS = EPI == EPI_WGRAD ? 2 : NOUT;
+  static constexpr int STG_WARP = STG_BUFS * STG_ONE;
   static constexpr int STG_BYTES = EPI_WARPS * STG_WARP;
   // PRE_TMA: every chunk (32 x 32 tile, activation dtype) a warp handles in one tile.
   static constexpr int PRE_CHUNKS = BN / 32 / (EPI_WARPS / 4);
@@ -681,6 +693,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
     uint8_t* pre_w = pre_base + ew * Cfg::PRE_WARP;
     uint32_t pre_phase = 0;
     bool pending = false;
+    unsigned wbuf = 0;  // dW staging buffer alternation
     int acc = 0;
     uint32_t acc_phase = 0;
     int li = 0;
@@ -746,8 +759,10 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
       // dW split over K (per problem): its own counters
       unsigned* const wflags = x_.prob ? args.split_flags2 : args.split_flags;
       const int wsplits = x_.prob ? splits2 : splits;
+      const bool wpar = Cfg::EPI == EPI_WGRAD && args.wpar && wsplits > 1;
+      const int wprows = x_.prob ? args.wpart_rows2 : args.wpart_rows;
       if constexpr (Cfg::EPI == EPI_WGRAD) {
-        if (split > 0) {
+        if (split > 0 && !wpar) {
           // ordered split-K: wait until every warp of split-1 has landed its sums
           if (lane == 0) detail::wait_counter(wflags + t, unsigned(split * wgroup));
           __syncwarp();
@@ -770,9 +785,20 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
         float x[32];
 #pragma unroll
         for (int e = 0; e < 32; ++e) x[e] = __uint_as_float(v[e]);
-        // staging buffers free again (previous chunk's bulk stores read them)
+        // staging buffers free again (previous chunk's bulk stores read them);
+        // dW alternates two buffers and waits only for the older group
+        uint8_t* wstg = stg0;
+        if constexpr (Cfg::EPI == EPI_WGRAD) {
+          wstg = (wbuf & 1) ? stg1 : stg0;
+          ++wbuf;
+        }
         if (pending) {
-          if (lane == 0) bulk_wait_read0();
+          if (lane == 0) {
+            if constexpr (Cfg::EPI == EPI_WGRAD)
+              bulk_wait_read1();
+            else
+              bulk_wait_read0();
+          }
           __syncwarp();
         }
         if constexpr (Cfg::EPI == EPI_FWD) {
@@ -838,7 +864,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
           else
             detail::stage_row<true>(stg0, lane, x);
         } else {
-          detail::stage_row<true>(stg0, lane, x);
+          detail::stage_row<true>(wstg, lane, x);
         }
         fence_proxy_async_smem();
         __syncwarp();
@@ -859,14 +885,16 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
             else
               tma_reduce_add_2d(&mp.c0, stg0, nc, row0);  // acc += partial, in L2
           } else {
+            if (wpar)
+              tma_store_2d(&mp.c1, wstg, nc, split * wprows + row0);  // this split's partial
 #ifdef RTPB_WGRAD_STORE  // dev A/B: timing only, results wrong
-            if (true)
+            else if (true)
 #else
-            if (first && split == 0)
+            else if (first && split == 0)
 #endif
-              tma_store_2d(&mp.c0, stg0, nc, row0);  // G known zero: G = dW tile (split 0 lands first)
+              tma_store_2d(&mp.c0, wstg, nc, row0);  // G known zero: G = dW tile (split 0 lands first)
             else
-              tma_reduce_add_2d(&mp.c0, stg0, nc, row0);  // travelling G += dW tile
+              tma_reduce_add_2d(&mp.c0, wstg, nc, row0);  // travelling G += dW tile
           }
           bulk_commit();
         }
@@ -885,7 +913,62 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
         pending = false;
       }
       if constexpr (Cfg::EPI == EPI_WGRAD) {
-        if (wsplits > 1) {
+        if (wpar) {
+          // count in on this warp's region; the warp completing it folds the
+          // partials (split order) into G
+          const int slot = int(rank) * Cfg::EPI_WARPS + ew;
+          unsigned* cnt = wflags + t * wgroup + slot;
+          unsigned last = 0;
+          if (lane == 0) {
+            bulk_wait0();
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+            __threadfence();
+            last = atomicAdd(cnt, 1u) + 1 == unsigned(wsplits);
+            if (last) __threadfence();
+          }
+          last = __shfl_sync(0xffffffffu, last, 0);
+          pending = false;
+          if (last) {
+            const float* part = x_.prob ? args.wpart2 : args.wpart;
+#pragma unroll 1
+            for (int ch = half; ch < BN / 32; ch += NSPLIT) {
+              const int nc = n0 + ch * 32;
+              if (nc >= uN) break;
+              float x[32];
+#pragma unroll
+              for (int e = 0; e < 32; ++e) x[e] = 0.f;
+              if (row_ok) {
+                for (int sp = 0; sp < wsplits; ++sp) {
+                  const float* src = part + (size_t(sp) * wprows + row) * uN + nc;
+#pragma unroll
+                  for (int g = 0; g < 4; ++g)
+                    if (nc + g * 8 < uN) {
+                      const float4 a = __ldcg(reinterpret_cast<const float4*>(src + g * 8));
+                      const float4 b = __ldcg(reinterpret_cast<const float4*>(src + g * 8) + 1);
+                      x[g * 8 + 0] += a.x; x[g * 8 + 1] += a.y; x[g * 8 + 2] += a.z; x[g * 8 + 3] += a.w;
+                      x[g * 8 + 4] += b.x; x[g * 8 + 5] += b.y; x[g * 8 + 6] += b.z; x[g * 8 + 7] += b.w;
+                    }
+                }
+              }
+              if (pending) {
+                if (lane == 0) bulk_wait_read0();
+                __syncwarp();
+              }
+              detail::stage_row<true>(stg0, lane, x);
+              fence_proxy_async_smem();
+              __syncwarp();
+              if (lane == 0) {
+                if (first)
+                  tma_store_2d(&mp.c0, stg0, nc, row0);
+                else
+                  tma_reduce_add_2d(&mp.c0, stg0, nc, row0);
+                bulk_commit();
+              }
+              pending = true;
+            }
+            if (lane == 0) *cnt = 0u;  // every split of this region has counted in
+          }
+        } else if (wsplits > 1) {
           // publish: this warp's reduce-adds for (tile, split) are performed
           if (lane == 0) {
             bulk_wait0();

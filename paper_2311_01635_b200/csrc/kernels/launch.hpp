@@ -45,9 +45,14 @@ struct StepWgrad {
   unsigned* split_flags;                          // zeroed per-tile counters (split-K order)
   const float* gbias_in; float* gbias_out;        // bias gradient, when the GEMM fuses it
   float* bias_part; unsigned* bias_tick;          // its partial sums / zeroed arrival counters
+  float* wpart;                                   // split-K fp32 partials (nullable: ordered split-K)
   size_t M, I, per;
   int force_bn;
 };
+// K splits the dW launch uses on the whole machine (1: none) and the fp32
+// partial floats its workspace needs for them (splits x I rounded to 256 x per).
+int wgrad_splits(bool f32, size_t M, size_t I, size_t per, int force_bn);
+size_t wgrad_partial_floats(bool f32, size_t M, size_t I, size_t per);
 // True when gemm_wgrad runs a CTA-pair config, whose extra warp also sums dY
 // columns into the bias gradient (gbias_*); otherwise colsum_bias_grad does.
 bool wgrad_fuses_bias(bool f32, size_t M, size_t I, size_t per, unsigned* split_flags, int force_bn);
@@ -102,6 +107,7 @@ struct FusedBwdArgs {
   float* bias_part1; unsigned* bias_tick1;  // per-layer workspace parts (zeroed counters)
   float* bias_part2; unsigned* bias_tick2;
   unsigned* split_flags1; unsigned* split_flags2;
+  float* wpart1; float* wpart2;  // split-K partial buffers of the layers (nullable)
   size_t M, h, f;
 };
 bool plan_fused_bwd(size_t M, size_t h, size_t f, FusedBwdPlan& plan);
