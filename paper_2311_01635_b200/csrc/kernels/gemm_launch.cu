@@ -269,7 +269,19 @@ int pick_code(bool tf32, GemmArgs& args, int force) {
     const int tiles = ((args.M + 255) / 256) * ((args.N + 255) / 256);
     const int kb = (args.K + 63) / 64;
     if (!force && tiles < pairs) {
-      int s = std::min(pairs / tiles, std::min(8, kb / 8));
+      // The ordered split-K pays one fp32 epilogue per split in sequence
+      // (~3 us each with double-buffered staging) to divide the ~0.35 us /
+      // K-block mainloop: take the split count minimising the sum.
+      const int s_max = std::min(pairs / tiles, std::min(8, kb / 8));
+      int s = 1;
+      double best_t = kb * 0.35 / 64.0 * 64.0;
+      for (int c = 2; c <= s_max; ++c) {
+        const double t = kb * 0.35 / c + 3.0 * c;
+        if (t < best_t) {
+          best_t = t;
+          s = c;
+        }
+      }
       if (s >= 2) {
         code = 1256;
         args.k_splits = s;
