@@ -310,10 +310,17 @@ class RtpLinear : public RtpLayerBase {
   struct FwdEpi {
     std::span<const DView> act;  // gelu(pre) outputs (nullable span)
     bool store_pre = true;
+    std::function<void()> before_last_step;  // called once the layer's last shift is posted
   };
   struct BwdEpi {
     std::span<const DView> pre;  // multiply the final dX by gelu'(pre)
+    std::function<void()> before_last_step;
   };
+  // Cross-layer pipelining: post this layer's first weight
+  // shift of the coming forward (backward = false) or backward pass now, into
+  // the out-of-place spare, so it travels under the previous layer's last
+  // step; the pass then skips posting it. No-op unless out of place and N > 1.
+  void prefetch_first_shift(bool backward);
   void forward_ex(std::span<const DView> x, size_t rows, std::span<const DView> y, Mode mode, const FwdEpi& e);
   void backward_ex(std::span<const DView> dy, size_t rows, std::span<const DView> dx, const BwdEpi& e);
   // N = 1 (no rotation): the bookkeeping of forward_ex (position law, replay
@@ -345,6 +352,7 @@ class RtpLinear : public RtpLayerBase {
   std::vector<DeviceBuffer> workspace_; // per rank: step-kernel workspace
   size_t scratch_rows_ = 0;
   size_t cached_rows_ = 0;
+  bool pre_fwd_ = false, pre_bwd_ = false;  // first shift already posted
 };
 
 // ffn1 (h -> f) -> gelu -> ffn2 (f -> h), composed as model.cpp:77-83,99-105.

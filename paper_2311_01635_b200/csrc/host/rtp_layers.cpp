@@ -329,7 +329,7 @@ void RtpLinear::forward_ex(std::span<const DView> x, size_t rows, std::span<cons
       if (mode == Mode::Train) tapes_[r].record(slots_[r].logical_id, {});
     });
     const bool rotate = s + 1 < n;
-    if (rotate && prefetch) {
+    if (rotate && prefetch && !(s == 0 && pre_fwd_)) {
       // Shard for step s+1 streams into the spare while step s computes.
       group_->comm_after_compute();  // spare's last reader (step s-1) is done
       for (size_t r : local) {
@@ -338,6 +338,8 @@ void RtpLinear::forward_ex(std::span<const DView> x, size_t rows, std::span<cons
       }
       group_->exchange(Direction::Clockwise, wp, sp, slots_[local[0]].weight.bytes());
     }
+    pre_fwd_ = false;
+    if (s + 1 == n && e.before_last_step) e.before_last_step();
     group_->each([&](size_t r) {
       Worker& w = group_->worker(r);
       const size_t k = k_of[r];
@@ -366,6 +368,23 @@ void RtpLinear::forward_ex(std::span<const DView> x, size_t rows, std::span<cons
     }
   }
   if (mode == Mode::Eval) rehome_after_eval();
+}
+
+void RtpLinear::prefetch_first_shift(bool backward) {
+  const size_t n = group_->size();
+  if (n < 2 || !oop() || (backward ? pre_bwd_ : pre_fwd_) || !all_home()) return;
+  const auto& local = group_->local_ranks();
+  std::vector<void*> wp(n, nullptr), sp(n, nullptr);
+  group_->comm_after_compute();  // the spare's last reader is done
+  for (size_t r : local) {
+    wp[r] = slots_[r].weight.data();
+    sp[r] = spares_[r].data();
+  }
+  group_->exchange(backward ? Direction::CounterClockwise : Direction::Clockwise, wp, sp,
+                   slots_[local[0]].weight.bytes());
+  if (backward)
+    for (size_t r : local) group_->worker(r).record(Ev::WDone, true);
+  (backward ? pre_bwd_ : pre_fwd_) = true;
 }
 
 const void* RtpLinear::begin_forward_n1(const DView& x, size_t rows, Mode mode) {
@@ -482,7 +501,7 @@ void RtpLinear::backward_ex(std::span<const DView> dy, size_t rows, std::span<co
       // dX of this step needs the shifted weight.
       for (size_t r : local) group_->worker(r).wait(Ev::WDone, false);
     }
-    if (rotate && oopm) {
+    if (rotate && oopm && !(s == 0 && pre_bwd_)) {
       group_->comm_after_compute();
       for (size_t r : local) {
         wp[r] = slots_[r].weight.data();
@@ -491,6 +510,8 @@ void RtpLinear::backward_ex(std::span<const DView> dy, size_t rows, std::span<co
       group_->exchange(Direction::CounterClockwise, wp, sp, slots_[local[0]].weight.bytes());
       for (size_t r : local) group_->worker(r).record(Ev::WDone, true);
     }
+    pre_bwd_ = false;
+    if (s + 1 == n && e.before_last_step) e.before_last_step();
     // dX (+)= dY_j . W_j^T
     if (dx_sms) set_sm_budget(dx_sms);
     group_->each([&](size_t r) {
@@ -673,6 +694,8 @@ void RtpMlp::forward(std::span<const DView> x, size_t rows, std::span<const DVie
   RtpLinear::FwdEpi e1;
   e1.act = act;
   e1.store_pre = mode == Mode::Train;
+  // ffn2's first shift travels under ffn1's last step
+  if (!std::getenv("RTPB_NO_PREFETCH")) e1.before_last_step = [&] { ffn2_->prefetch_first_shift(false); };
   ffn1_->forward_ex(x, rows, pre, mode, e1);
   ffn2_->forward(act, rows, y, mode);  // model.cpp:83
 }
@@ -747,6 +770,7 @@ void RtpMlp::backward(std::span<const DView> dy, size_t rows, std::span<const DV
   // written over pre (same element reads then writes it) (model.cpp:99-104)
   RtpLinear::BwdEpi e2;
   e2.pre = pre;
+  if (!std::getenv("RTPB_NO_PREFETCH")) e2.before_last_step = [&] { ffn1_->prefetch_first_shift(true); };
   ffn2_->backward_ex(dy, rows, pre, e2);
   ffn1_->backward_ex(pre, rows, dx, RtpLinear::BwdEpi{});  // model.cpp:105
   group_->join_aux();
