@@ -346,8 +346,12 @@ struct TwoProb {
 // fraction is <= alpha x problem 0's (alpha < 0: only once problem 0 is
 // exhausted). Each slot's list is in simulated start order, which makes the
 // kernel's waits deadlock-free. Returns the makespan.
+// tail > 0 (dep 1, S1 = 1): the last `tail` problem-1 tiles taken are split
+// over K in two units (split code 0 / 1, costing c1_half each; the second's
+// epilogue follows the first's), all others run whole (split code 0xFF), so
+// the final wave is made of half-length units.
 double list_schedule(int P, const TwoProb& q, double alpha, std::vector<int>& sched,
-                     std::vector<double>* row_ready_out = nullptr) {
+                     std::vector<double>* row_ready_out = nullptr, int tail = 0, double c1_half = 0) {
   std::vector<std::vector<int>> lists(static_cast<size_t>(P));
   std::vector<double> free_at(static_cast<size_t>(P), 0.0);
   const int nm = q.n0 ? (q.T0 + q.n0 - 1) / q.n0 : 1;
@@ -357,7 +361,8 @@ double list_schedule(int P, const TwoProb& q, double alpha, std::vector<int>& sc
   std::vector<double> split_fin(size_t(std::max(q.T1, 1)), 0.0);
   size_t r1 = 0;
   int r1_u = 0, next0 = 0, next1 = 0, taken1 = 0;
-  const int U1 = q.T1 * q.S1;
+  int tiles1 = 0, cur_split = -1;  // tail mode: tiles started, next split of the current tile
+  const int U1 = q.T1 * q.S1 + (tail > 0 ? tail : 0);
   double makespan = 0;
   for (int done = 0; done < q.T0 + U1; ++done) {
     int p = 0;
@@ -367,12 +372,17 @@ double list_schedule(int P, const TwoProb& q, double alpha, std::vector<int>& sc
     // candidate problem-1 unit and its readiness
     int t1 = -1, sp = 0;
     double rdy = 0.0;
+    bool split_tile = false;
     if (q.dep == 1) {
       if (r1 < ready_rows.size()) {
         const int mb = ready_rows[r1];
         t1 = mb * q.n1 + r1_u / q.S1;
         sp = r1_u % q.S1;
         rdy = row_ready[size_t(mb)];
+        if (tail > 0) {
+          split_tile = tiles1 >= q.T1 - tail;
+          sp = split_tile ? (cur_split < 0 ? 0 : cur_split) : 0xFF;
+        }
       }
     } else if (next1 < U1) {
       t1 = next1 / q.S1;
@@ -390,12 +400,16 @@ double list_schedule(int P, const TwoProb& q, double alpha, std::vector<int>& sc
     else if (t1 >= 0 && rdy <= tp && alpha >= 0 && f1 <= alpha * f0) take1 = true;
     double fin;
     if (take1) {
-      fin = std::max(tp, rdy) + q.c1;
-      if (sp > 0) fin = std::max(fin, split_fin[size_t(t1)] + 0.5);
+      fin = std::max(tp, rdy) + (split_tile ? c1_half : q.c1);
+      if (sp > 0 && sp != 0xFF) fin = std::max(fin, split_fin[size_t(t1)] + 0.6);
       split_fin[size_t(t1)] = fin;
       lists[size_t(p)].push_back((1 << 28) | (sp << 20) | t1);
       ++taken1;
-      if (q.dep == 1) {
+      if (split_tile && sp == 0) {
+        cur_split = 1;  // the tile's second half comes next
+      } else if (q.dep == 1) {
+        cur_split = -1;
+        ++tiles1;
         if (++r1_u == q.n1 * q.S1) {
           r1_u = 0;
           ++r1;
@@ -540,6 +554,24 @@ bool plan_fused_fwd(size_t M, size_t h, size_t f, FusedFwdPlan& plan) {
   q.dep = 1;
   plan.est_us = best_schedule(P, q, plan.sched);
   plan.k_splits2 = S;
+  if (S == 1 && std::getenv("RTPB_TAIL_SPLIT")) {
+    // the final wave's ffn2 tiles split over K in two (ordered partials).
+    // Opt-in: measured slower (config (b) forward 96 vs 79 us) — the split
+    // units' partial / final epilogues cost more than the tail they trim.
+    const double c_half = tile_cost((f + 1) / 2, 2.0);
+    for (int tail : {P / 4, P / 2, (3 * P) / 4, P}) {
+      if (tail <= 0 || tail > T1) continue;
+      for (double al : kAlphas) {
+        std::vector<int> s_;
+        const double t = list_schedule(P, q, al, s_, nullptr, tail, c_half);
+        if (t < plan.est_us) {
+          plan.est_us = t;
+          plan.sched.swap(s_);
+          plan.k_splits2 = 2;
+        }
+      }
+    }
+  }
   plan.slots = P;
   plan.dep_rows = nm;
   plan.dep_target = unsigned(n0) * 2u * kEpiWarps;

@@ -425,6 +425,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
   const int kb_per2 = (num_kb2 + splits2 - 1) / splits2;
   struct Unit {
     int prob, t, mb, nb, split, kb0, kb1, M, N, flags;
+    bool whole;  // problem 1 of a split launch run unsplit (split code 0xFF)
   };
   auto decode = [&](int it) {
     Unit x;
@@ -455,7 +456,13 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
       x.mb = x.t % nm;
       x.nb = x.t / nm;
     }
-    if (x.prob) {
+    x.whole = false;
+    if (x.prob && x.split == 0xFF) {
+      x.whole = true;
+      x.split = 0;
+      x.kb0 = 0;
+      x.kb1 = num_kb2;
+    } else if (x.prob) {
       x.kb0 = x.split * kb_per2;
       x.kb1 = min(num_kb2, x.kb0 + kb_per2);
     } else {
@@ -749,7 +756,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
       if (tr) detail::trace_at(trace, 6 + 6 * li);
       // FWD problem 1 split over K: partial splits go to the fp32 workspace,
       // in split order; the last split folds the workspace into its output.
-      const bool split2 = Cfg::EPI == EPI_FWD && x_.prob == 1 && splits2 > 1;
+      const bool split2 = Cfg::EPI == EPI_FWD && x_.prob == 1 && splits2 > 1 && !x_.whole;
       const bool part2 = split2 && split < splits2 - 1;
       const bool fin2 = split2 && split == splits2 - 1;
       if (split2 && split > 0) {
