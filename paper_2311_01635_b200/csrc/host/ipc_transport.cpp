@@ -72,7 +72,6 @@ void cu_check(CUresult r, const char* where) {
   if (r != CUDA_SUCCESS) throw CudaError(std::string(where) + ": CUDA driver error " + std::to_string(int(r)));
 }
 
-constexpr uint64_t kMagic = 0x7274706269706331ull;  // "rtpbipc1"
 constexpr int kMaxRanks = 64;
 constexpr int kSlots = 64;  // mailbox depth (shifts a host may run ahead of its neighbour)
 
@@ -83,7 +82,6 @@ struct Mail {
   uint64_t offset;
 };
 struct Shm {
-  std::atomic<uint64_t> magic;
   std::atomic<uint32_t> joined, left;
   std::atomic<uint32_t> flags_ready[kMaxRanks];
   cudaIpcMemHandle_t flags_handle[kMaxRanks];

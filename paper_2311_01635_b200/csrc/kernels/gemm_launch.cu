@@ -224,13 +224,8 @@ constexpr int kEpiWarps = 8;
 template <int EPI, bool TF32>
 int dispatch_tile(int code, const Op& a, const Op& b, const Out& c0, const Out* c1, const GemmArgs& args,
                   cudaStream_t s) {
-#ifdef RTPB_WGRAD_KMAJOR_PROBE  // dev A/B: wgrad fed pre-transposed (K-major) operands
-  constexpr bool AMN = false;
-  constexpr bool BMN = !TF32 && EPI == EPI_FWD;
-#else
   constexpr bool AMN = !TF32 && EPI == EPI_WGRAD;
   constexpr bool BMN = !TF32 && EPI != EPI_DGRAD;
-#endif
   if constexpr (!TF32) {
     if (code == 1256) return launch_cfg<GemmCfg<EPI, 256, false, kEpiWarps, AMN, BMN, false, true>>(a, b, c0, c1, args, s);
     if (code == 1128) return launch_cfg<GemmCfg<EPI, 128, false, kEpiWarps, AMN, BMN, false, true>>(a, b, c0, c1, args, s);
@@ -829,11 +824,7 @@ int gemm_dgrad(bool f32, const StepDgrad& p, cudaStream_t s) {
 int gemm_wgrad(bool f32, const StepWgrad& p, cudaStream_t s) {
   // C[I x per] = X^T . dY_blk; bf16: X and dY_blk read MN-major in place.
   // tf32: the pre-pass wrote X^T (I x M) and dY_blk^T (per x M), both K-major.
-#ifdef RTPB_WGRAD_KMAJOR_PROBE
-  const bool kmaj = true;
-#else
   const bool kmaj = f32;
-#endif
   Op a = kmaj ? Op{p.x, p.x_lo, p.M, p.I, p.ldx} : Op{p.x, p.x_lo, p.I, p.M, p.ldx};
   Op b = kmaj ? Op{p.dy, p.dy_lo, p.M, p.per, p.ldy} : Op{p.dy, p.dy_lo, p.per, p.M, p.ldy};
   GemmArgs g{};

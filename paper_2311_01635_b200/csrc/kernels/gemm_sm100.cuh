@@ -894,11 +894,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
           } else {
             if (wpar)
               tma_store_2d(&mp.c1, wstg, nc, split * wprows + row0);  // this split's partial
-#ifdef RTPB_WGRAD_STORE  // dev A/B: timing only, results wrong
-            else if (true)
-#else
             else if (first && split == 0)
-#endif
               tma_store_2d(&mp.c0, wstg, nc, row0);  // G known zero: G = dW tile (split 0 lands first)
             else
               tma_reduce_add_2d(&mp.c0, wstg, nc, row0);  // travelling G += dW tile

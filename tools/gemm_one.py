@@ -36,14 +36,6 @@ if "wgrad_as_dgrad" in kinds:  # the dW product on the dgrad kernel: X^T (I x M)
     WT[:per * M].view(per, M).copy_(dY.t())
     OUT = torch.empty(I, per, dtype=torch.bfloat16, device=dev)
     fns["wgrad_as_dgrad"] = lambda: rtp.dgrad_step(XT2, 0, WT, None, OUT, I, per, M, True, True)
-if "wgrad_t" in kinds:  # needs an RTPB_WGRAD_KMAJOR_PROBE build: X^T (I x M) and dY^T (per x M)
-    import ctypes as C
-    XT, dYT = X.t().contiguous(), dY.t().contiguous()
-    ws = rtp._ws(2, 0, M, I, per, X.device)
-    fns["wgrad_t"] = lambda: _lib.check(_lib.lib.rtpb_wgrad_step(0, XT.data_ptr(), M, dYT.data_ptr(), M, 0,
-                                                                 G.data_ptr(), G.data_ptr(), M, I, per,
-                                                                 ws.data_ptr(), ws.numel(),
-                                                                 torch.cuda.current_stream().cuda_stream))
 fl = 2.0 * M * I * per
 for k in kinds:
     f = fns[k]
