@@ -453,7 +453,8 @@ def main():
         xd = [torch.empty_like(x) for _ in range(2)]
         dyd = [torch.empty_like(dy) for _ in range(2)]
         dxd = [torch.empty_like(dx) for _ in range(2)]
-        h2d, d2h = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+        # X and dY travel on two H2D streams (two copy engines in flight)
+        h2d, h2d_b, d2h = torch.cuda.Stream(dev), torch.cuda.Stream(dev), torch.cuda.Stream(dev)
         EV = lambda: torch.cuda.Event()  # noqa: E731
         e2e_steps = max(10, min(args.steps, 100))
 
@@ -463,16 +464,23 @@ def main():
             drained = [EV(), EV()]
             done_with_inputs = [None, None]
 
+            landed_b = [EV(), EV()]
+
             def issue_h2d(i):
                 b = i % 2
                 with torch.cuda.stream(h2d):
                     if done_with_inputs[b] is not None:
                         h2d.wait_event(done_with_inputs[b])  # step i-2 finished reading these buffers
                     xd[b].copy_(hx[b], non_blocking=True)
-                    dyd[b].copy_(hdy[b], non_blocking=True)
                     landed[b].record(h2d)
+                with torch.cuda.stream(h2d_b):
+                    if done_with_inputs[b] is not None:
+                        h2d_b.wait_event(done_with_inputs[b])
+                    dyd[b].copy_(hdy[b], non_blocking=True)
+                    landed_b[b].record(h2d_b)
 
             h2d.wait_stream(stream)
+            h2d_b.wait_stream(stream)
             d2h.wait_stream(stream)
             issue_h2d(0)
             for i in range(nsteps):
@@ -480,6 +488,7 @@ def main():
                 if i + 1 < nsteps:
                     issue_h2d(i + 1)
                 stream.wait_event(landed[b])
+                stream.wait_event(landed_b[b])
                 if i >= 2:
                     stream.wait_event(drained[b])  # dxd[b] read back before it is overwritten
                 mlp.zero_grads()
@@ -493,6 +502,7 @@ def main():
                     drained[b].record(d2h)
             stream.wait_stream(d2h)
             stream.wait_stream(h2d)
+            stream.wait_stream(h2d_b)
 
         run_e2e(4)
         barrier()
