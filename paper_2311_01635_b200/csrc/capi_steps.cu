@@ -158,7 +158,8 @@ int fused_bwd_step(FusedBwdArgs a, void* ws1, size_t ws1_bytes, void* ws2, size_
     *part = c.take(bias_part_bytes(I, per) / sizeof(float));
     const size_t wpf = wgrad_partial_floats(false, a.M, I, per);
     // the layer's partial buffer holds its own (whole-machine) split count
-    if (plan.w_splits > 1 && size_t(plan.w_splits) * ((I + 255) / 256 * 256) * per > wpf) return false;
+    // (no partial buffer: the dW launch falls back to the ordered split-K chain)
+    if (wpf && plan.w_splits > 1 && size_t(plan.w_splits) * ((I + 255) / 256 * 256) * per > wpf) return false;
     *wpart = wpf ? c.take(wpf) : nullptr;
     return c.ok;
   };
