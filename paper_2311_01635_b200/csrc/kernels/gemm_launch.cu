@@ -849,9 +849,12 @@ int gemm_wgrad(bool f32, const StepWgrad& p, cudaStream_t s) {
     const size_t ipad = (p.I + 255) / 256 * 256;
     const int smax = wgrad_splits(f32, p.M, p.I, p.per, p.force_bn);
     Out part{p.wpart, true, p.per, size_t(smax) * ipad, p.per};
-    g.wpar = 1;
+    // every unit of a split dW launch is resident (splits <= pairs / tiles):
+    // parallel slice folds; RTPB_WGRAD_LASTFOLD selects the last-arriver fold
+    g.wpar = std::atoi(std::getenv("RTPB_WGRAD_PAR")) == 1 ? 1 : 2;
     g.wpart = p.wpart;
     g.wpart_rows = int(ipad);
+    g.gout = p.g_out;
     return dispatch<EPI_WGRAD>(f32, a, b, c0, &part, g, s, p.force_bn);
   }
   return dispatch<EPI_WGRAD>(f32, a, b, c0, nullptr, g, s, p.force_bn);
@@ -872,11 +875,12 @@ int wgrad_splits(bool f32, size_t M, size_t I, size_t per, int force_bn) {
 }
 
 size_t wgrad_partial_floats(bool f32, size_t M, size_t I, size_t per) {
-  // Unordered split-K partials are opt-in (RTPB_WGRAD_PAR): measured slower
-  // than the ordered chain (config (b) dW 72 vs 45 us; 8 splits 114 us), the
-  // completing warp's fold of the partials being latency-bound.
-  static const bool on = std::getenv("RTPB_WGRAD_PAR") != nullptr;
-  if (!on) return 0;
+  // Split-K partials for the unordered dW modes, opt-in with RTPB_WGRAD_PAR
+  // (1: the last split folds them, 2: every split folds a row slice). Both
+  // measured slower than the ordered chain of epilogues (config (b) N=1 dW
+  // 2-way: epilogue 14 / 28 us vs 8 us), so the chain stays the default.
+  static const char* mode = std::getenv("RTPB_WGRAD_PAR");
+  if (!mode || f32) return 0;
   const int S = wgrad_splits(f32, M, I, per, 0);
   return S > 1 ? size_t(S) * ((I + 255) / 256 * 256) * per : 0;
 }

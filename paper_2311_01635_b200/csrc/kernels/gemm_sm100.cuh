@@ -103,10 +103,12 @@ struct GemmArgs {
   // rounded up to the tile height) and counts in on its region's counter
   // (split_flags[tile * 16 + warp slot]); the warp that completes a region sums
   // the partials in split order and adds them into G once. Deterministic.
-  int wpar;
+  int wpar;  // 1: the last split folds; 2: all splits resident, each folds a row slice
   int wpart_rows, wpart_rows2;
   const float* wpart;
   const float* wpart2;
+  float* gout;  // wpar 2: the gradient block written by plain stores (I x per, ld per)
+  float* gout2;
   unsigned* dep_count;
   unsigned dep_target;
   int dep_rows;
@@ -916,7 +918,70 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
         pending = false;
       }
       if constexpr (Cfg::EPI == EPI_WGRAD) {
-        if (wpar) {
+        if (wpar && args.wpar == 2) {
+          // All splits of the launch are resident (units <= slots): every
+          // split stores its partial, waits until the region's S partials are
+          // in, then folds its own slice of the region's 32 rows (partials in
+          // split order, then + G_in) with plain stores — no chain of
+          // serialised epilogues. Deterministic: one owner per row.
+          const int slot = int(rank) * Cfg::EPI_WARPS + ew;
+          unsigned* cnt = wflags + t * wgroup + slot;
+          if (lane == 0) {
+            bulk_wait0();
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+            __threadfence();
+            atomicAdd(cnt, 1u);
+            detail::wait_counter_nofence(cnt, unsigned(wsplits));
+            __threadfence();
+          }
+          __syncwarp();
+          pending = false;
+          const float* part = x_.prob ? args.wpart2 : args.wpart;
+          const int r_lo = (32 * split) / wsplits, r_hi = (32 * (split + 1)) / wsplits;
+          float* gout = const_cast<float*>(static_cast<const float*>(x_.prob ? args.gout2 : args.gout));
+          if (lane >= r_lo && lane < r_hi && row_ok) {
+            // all loads of a chunk are issued before its stores (the partials
+            // and G never alias, but the compiler cannot know): one round trip
+            // per split instead of one per 8 columns
+#pragma unroll 1
+            for (int ch = half; ch < BN / 32; ch += NSPLIT) {
+              const int nc = n0 + ch * 32;
+              if (nc >= uN) break;
+              const int nv = min(8, (uN - nc) / 4);  // float4s of this row inside N
+              float4 acc[8];
+#pragma unroll
+              for (int v = 0; v < 8; ++v) acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+              for (int sp = 0; sp < wsplits; ++sp) {
+                const float4* __restrict__ src =
+                    reinterpret_cast<const float4*>(part + (size_t(sp) * wprows + row) * uN + nc);
+                float4 tv[8];
+#pragma unroll
+                for (int v = 0; v < 8; ++v) tv[v] = v < nv ? __ldcg(src + v) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+                for (int v = 0; v < 8; ++v) {
+                  acc[v].x += tv[v].x; acc[v].y += tv[v].y; acc[v].z += tv[v].z; acc[v].w += tv[v].w;
+                }
+              }
+              float4* __restrict__ dst = reinterpret_cast<float4*>(gout + size_t(row) * uN + nc);
+              if (!first) {
+                float4 gv[8];
+#pragma unroll
+                for (int v = 0; v < 8; ++v) gv[v] = v < nv ? __ldcg(dst + v) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+                for (int v = 0; v < 8; ++v)
+                  acc[v] = make_float4(gv[v].x + acc[v].x, gv[v].y + acc[v].y, gv[v].z + acc[v].z, gv[v].w + acc[v].w);
+              }
+#pragma unroll
+              for (int v = 0; v < 8; ++v)
+                if (v < nv) dst[v] = acc[v];
+            }
+          }
+          __syncwarp();
+          if (lane == 0) {  // count out; the last split out re-zeroes the region counter
+            __threadfence();
+            if (atomicAdd(cnt, 1u) + 1 == unsigned(2 * wsplits)) *cnt = 0u;
+          }
+        } else if (wpar) {
           // count in on this warp's region; the warp completing it folds the
           // partials (split order) into G
           const int slot = int(rank) * Cfg::EPI_WARPS + ew;
