@@ -372,8 +372,14 @@ void RtpLinear::forward_ex(std::span<const DView> x, size_t rows, std::span<cons
 
 void RtpLinear::prefetch_first_shift(bool backward) {
   const size_t n = group_->size();
-  if (n < 2 || !oop() || (backward ? pre_bwd_ : pre_fwd_) || !all_home()) return;
+  if (n < 2 || !oop() || (backward ? pre_bwd_ : pre_fwd_)) return;
   const auto& local = group_->local_ranks();
+  // forward starts from home; backward from where the train forward left the
+  // shards (its tape is recorded)
+  if (!backward && !all_home()) return;
+  if (backward)
+    for (size_t r : local)
+      if (tapes_[r].empty()) return;
   std::vector<void*> wp(n, nullptr), sp(n, nullptr);
   group_->comm_after_compute();  // the spare's last reader is done
   for (size_t r : local) {
