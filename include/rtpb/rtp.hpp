@@ -282,6 +282,7 @@ class RtpLayerBase {
   std::vector<ShardSlot> slots_;  // indexed by rank (remote entries stay empty)
   std::vector<DeviceBuffer> spares_;
   size_t shard_len_ = 0;
+  size_t flag_base_ = 0;  // this layer's block of the workers' shard-arrival flags
   RotationMode rotation_mode_ = RotationMode::InPlace;
   std::vector<int64_t> trace_;
   bool grads_zero_pending_ = false;
@@ -344,6 +345,12 @@ class RtpLinear : public RtpLayerBase {
  private:
   void build(size_t in_dim, size_t out_dim, size_t n);
   void ensure_scratch(size_t rows);
+  // Shard-arrival flags (rtp_layers.cpp): forward W, backward W, backward G
+  // blocks of the layer's flag range, indexed by the step the shard is for.
+  static constexpr size_t kFlagFwd = 0, kFlagBwdW = 16, kFlagBwdG = 32;
+  bool use_flags() const;
+  void flagged_exchange(Direction dir, std::span<void* const> send, std::span<void* const> recv, size_t bytes,
+                        size_t flag);
 
   size_t in_ = 0, out_ = 0, per_ = 0;
   std::vector<ReplayTape<Empty>> tapes_;

@@ -1,6 +1,8 @@
 // WorkerGroup, transports (in-process device copies; NCCL over NVLink),
 // device buffers and per-worker ledgers.
 // Reference: proj/src/ring.cpp (rotation, transports), ledger.cpp, tensor.cpp:86-157.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <nccl.h>
 
 #include <algorithm>
@@ -146,6 +148,7 @@ Worker::Worker(size_t r, int dev) : rank(r), device(dev) {
   cuda_check(cudaStreamCreateWithFlags(&compute, cudaStreamNonBlocking), "stream");
   cuda_check(cudaStreamCreateWithFlags(&comm, cudaStreamNonBlocking), "stream");
   cuda_check(cudaStreamCreateWithFlags(&aux, cudaStreamNonBlocking), "stream");
+  flags = DeviceBuffer(dev, kFlagPool * sizeof(unsigned), nullptr, MemCategory::Other, true);
   for (auto& e : ev) cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
 }
 Worker::~Worker() {
@@ -158,6 +161,21 @@ Worker::~Worker() {
   cudaStreamDestroy(aux);
   cudaStreamDestroy(compute);
   cudaStreamDestroy(comm);
+}
+
+void stream_write_u32(cudaStream_t s, unsigned* addr, unsigned v) {
+  static PFN_cuStreamWriteValue32_v11070 fn = [] {
+    cudaDriverEntryPointQueryResult q;
+    void* f = nullptr;
+    if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      f = nullptr;
+    return reinterpret_cast<PFN_cuStreamWriteValue32_v11070>(f);
+  }();
+  if (!fn) throw CudaError("cuStreamWriteValue32 unavailable");
+  const CUresult r = fn(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(addr), v,
+                        CU_STREAM_WRITE_VALUE_DEFAULT);
+  if (r != CUDA_SUCCESS) throw CudaError("cuStreamWriteValue32 failed: " + std::to_string(int(r)));
 }
 
 size_t inplace_chunk_bytes(size_t shard_bytes) {

@@ -13,7 +13,9 @@
 // the next dW waits only for it. In-place mode: the weight shift follows dX
 // (overlapping dW), the gradient shift follows dW (overlapping the next dX);
 // forward shifts are exposed, as the paper accepts.
+#include <atomic>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 
@@ -120,7 +122,12 @@ class SmReserve {
 
 // ------------------------------------------------------------------ base
 RtpLayerBase::RtpLayerBase(WorkerGroup& group, std::string label, DType dtype)
-    : group_(&group), label_(std::move(label)), dtype_(dtype) {}
+    : group_(&group), label_(std::move(label)), dtype_(dtype) {
+  // one block of arrival flags per layer (forward W, backward W, backward G
+  // for up to 16 steps), reused cyclically across the pool
+  static std::atomic<size_t> next_layer{0};
+  flag_base_ = (next_layer.fetch_add(1) % (Worker::kFlagPool / Worker::kFlagsPerLayer)) * Worker::kFlagsPerLayer;
+}
 
 void RtpLayerBase::init_slots_alloc() {
   const size_t n = group_->size();
@@ -336,12 +343,17 @@ void RtpLinear::forward_ex(std::span<const DView> x, size_t rows, std::span<cons
         wp[r] = slots_[r].weight.data();
         sp[r] = spares_[r].data();
       }
-      group_->exchange(Direction::Clockwise, wp, sp, slots_[local[0]].weight.bytes());
+      flagged_exchange(Direction::Clockwise, wp, sp, slots_[local[0]].weight.bytes(), kFlagFwd + s + 1);
     }
     pre_fwd_ = false;
+    if (s + 1 == n && prefetch && use_flags())
+      for (size_t r : local) group_->worker(r).record(Ev::PassEnd, true);  // this pass's comm work
     if (s + 1 == n && e.before_last_step) e.before_last_step();
+    const bool wait_flag = prefetch && use_flags() && s > 0;
     group_->each([&](size_t r) {
       Worker& w = group_->worker(r);
+      // this step's shard landed in the previous step's spare
+      set_launch_wait_flag(wait_flag ? w.flag(flag_base_ + kFlagFwd + s) : nullptr);
       const size_t k = k_of[r];
       const size_t j = slots_[r].logical_id;
       int flags = e.store_pre ? RTPB_EPI_STORE_PRE : 0;
@@ -354,20 +366,65 @@ void RtpLinear::forward_ex(std::span<const DView> x, size_t rows, std::span<cons
       }
       void* yp = e.store_pre ? y[k].data : nullptr;
       const size_t ldy = e.store_pre && y[k].ld ? y[k].ld : out_;
-      check_status(rtpb_fwd_step(dt, x[k].data, x[k].ld ? x[k].ld : in_, slots_[r].weight.data(), yp, ldy, j * per_,
-                                 act, ld_act, rows, in_, per_, flags, workspace_[r].data(), workspace_[r].bytes(),
-                                 w.compute));
+      const int rc = rtpb_fwd_step(dt, x[k].data, x[k].ld ? x[k].ld : in_, slots_[r].weight.data(), yp, ldy,
+                                   j * per_, act, ld_act, rows, in_, per_, flags, workspace_[r].data(),
+                                   workspace_[r].bytes(), w.compute);
+      set_launch_wait_flag(nullptr);
+      check_status(rc);
     });
     if (!rotate) break;
     if (prefetch) {
-      group_->compute_after_comm();
+      if (!use_flags()) group_->compute_after_comm();
       for (size_t r : local) swap_data(slots_[r].weight, spares_[r]);
       group_->advance_slots(slots_, Direction::Clockwise, PayloadKind::Weight, label_, shard_len_);
     } else {
       rotate_forward();
     }
   }
+  // flags: the compute stream never waited for this pass's shifts; join them
+  // once at its end (stream capture requires it). A shift the hook prefetched
+  // for the next layer stays in flight; that layer's pass joins it.
+  if (n > 1 && prefetch && use_flags())
+    for (size_t r : local) group_->worker(r).wait(Ev::PassEnd, false);
   if (mode == Mode::Eval) rehome_after_eval();
+}
+
+// Arrival flags (bf16 mode, one worker per GPU, N <= 16): the shift's comm
+// stream clears the flag, moves the shard, then sets it with stream memory
+// operations (no SM needed); the consuming step GEMM waits for it on the device
+// instead of its stream waiting for comm, so consecutive step GEMMs keep their
+// programmatic (PDL) launch overlap. Deadlock freedom: every flag's writer was
+// issued before its waiter and waits only on earlier-issued kernels; a waiting
+// grid admits no successor (the kernel triggers PDL after the flag), so the
+// spinning grids hold at most the SM budgets of the two streams; shifts that
+// need SMs (NCCL) run on the SMs reserved for them. fp32 mode keeps event
+// ordering: its operand-split pre-passes read the shard before the GEMM.
+// Several workers on one device (Lockstep/Concurrent) also keep events: their
+// spinning grids would compete for the same SMs.
+bool RtpLinear::use_flags() const {
+  const TransportKind k = group_->kind();
+  const bool one_per_gpu = k == TransportKind::Nccl || k == TransportKind::Ipc || k == TransportKind::Solo;
+  return one_per_gpu && dtype_ == DType::BF16 && group_->size() > 1 && group_->size() <= 16 &&
+         !std::getenv("RTPB_NO_FLAGS");
+}
+
+void RtpLinear::flagged_exchange(Direction dir, std::span<void* const> send, std::span<void* const> recv,
+                                 size_t bytes, size_t flag) {
+  const auto& local = group_->local_ranks();
+  const bool fl = use_flags();
+  if (fl)
+    for (size_t r : local) {
+      Worker& w = group_->worker(r);
+      DeviceGuard dg(w.device);
+      stream_write_u32(w.comm, w.flag(flag_base_ + flag), 0u);
+    }
+  group_->exchange(dir, send, recv, bytes);
+  if (fl)
+    for (size_t r : local) {
+      Worker& w = group_->worker(r);
+      DeviceGuard dg(w.device);
+      stream_write_u32(w.comm, w.flag(flag_base_ + flag), 1u);
+    }
 }
 
 void RtpLinear::prefetch_first_shift(bool backward) {
@@ -386,8 +443,8 @@ void RtpLinear::prefetch_first_shift(bool backward) {
     wp[r] = slots_[r].weight.data();
     sp[r] = spares_[r].data();
   }
-  group_->exchange(backward ? Direction::CounterClockwise : Direction::Clockwise, wp, sp,
-                   slots_[local[0]].weight.bytes());
+  flagged_exchange(backward ? Direction::CounterClockwise : Direction::Clockwise, wp, sp,
+                   slots_[local[0]].weight.bytes(), backward ? kFlagBwdW + 1 : kFlagFwd + 1);
   if (backward)
     for (size_t r : local) group_->worker(r).record(Ev::WDone, true);
   (backward ? pre_bwd_ : pre_fwd_) = true;
@@ -503,7 +560,8 @@ void RtpLinear::backward_ex(std::span<const DView> dy, size_t rows, std::span<co
       trace_[n * n + s * n + r] = int64_t(j);
     });
     const bool rotate = s + 1 < n;
-    if (s > 0) {
+    const bool flags_on = use_flags();
+    if (s > 0 && !flags_on) {
       // dX of this step needs the shifted weight.
       for (size_t r : local) group_->worker(r).wait(Ev::WDone, false);
     }
@@ -513,10 +571,12 @@ void RtpLinear::backward_ex(std::span<const DView> dy, size_t rows, std::span<co
         wp[r] = slots_[r].weight.data();
         sp[r] = spares_[r].data();
       }
-      group_->exchange(Direction::CounterClockwise, wp, sp, slots_[local[0]].weight.bytes());
+      flagged_exchange(Direction::CounterClockwise, wp, sp, slots_[local[0]].weight.bytes(), kFlagBwdW + s + 1);
       for (size_t r : local) group_->worker(r).record(Ev::WDone, true);
     }
     pre_bwd_ = false;
+    if (s + 1 == n && n > 1 && use_flags())
+      for (size_t r : local) group_->worker(r).record(Ev::PassEnd, true);
     if (s + 1 == n && e.before_last_step) e.before_last_step();
     // dX (+)= dY_j . W_j^T
     if (dx_sms) set_sm_budget(dx_sms);
@@ -533,37 +593,48 @@ void RtpLinear::backward_ex(std::span<const DView> dy, size_t rows, std::span<co
         ldpre = e.pre[k].ld ? e.pre[k].ld : in_;
       }
       float* acc = n > 1 ? static_cast<float*>(dx_acc_[r].data()) : nullptr;
-      check_status(rtpb_dgrad_step(dt, dy[k].data, dy[k].ld ? dy[k].ld : out_, j * per_, slots_[r].weight.data(), acc,
-                                   in_, dx[k].data, dx[k].ld ? dx[k].ld : in_, pre, ldpre, rows, in_, per_, flags,
-                                   workspace_[r].data(), workspace_[r].bytes(), w.compute));
+      set_launch_wait_flag(flags_on && s > 0 ? w.flag(flag_base_ + kFlagBwdW + s) : nullptr);
+      const int rc = rtpb_dgrad_step(dt, dy[k].data, dy[k].ld ? dy[k].ld : out_, j * per_, slots_[r].weight.data(),
+                                     acc, in_, dx[k].data, dx[k].ld ? dx[k].ld : in_, pre, ldpre, rows, in_, per_,
+                                     flags, workspace_[r].data(), workspace_[r].bytes(), w.compute);
+      set_launch_wait_flag(nullptr);
+      check_status(rc);
     });
     if (rotate && !oopm) {
       // In place: the weight is free once dX has read it; shift it under dW.
       group_->comm_after_compute();
       for (size_t r : local) wp[r] = slots_[r].weight.data();
-      group_->exchange(Direction::CounterClockwise, wp, wp, slots_[local[0]].weight.bytes());
+      flagged_exchange(Direction::CounterClockwise, wp, wp, slots_[local[0]].weight.bytes(), kFlagBwdW + s + 1);
       for (size_t r : local) group_->worker(r).record(Ev::WDone, true);
     }
-    if (s > 0) {
+    // G_j += X^T . dY_j (+ bias column sums), in place on the resident shard.
+    if (dx_sms) set_sm_budget(all_sms - dx_sms);
+    // The travelling gradient arrives by flag when the dW launch is a single
+    // CTA-pair GEMM (bias sums fused in it); the per-tile kernels' separate
+    // bias column-sum pre-pass reads G, so those keep the stream wait.
+    unsigned dummy_flags = 0;
+    const bool g_flag = flags_on && wgrad_fuses_bias(false, rows, in_, per_, &dummy_flags, 0);
+    if (s > 0 && !g_flag) {
       // dW accumulates into the travelling gradient shard: wait for its arrival.
       for (size_t r : local) {
         Worker& w = group_->worker(r);
         w.wait_on(Ev::GDone, dx_sms ? w.aux : w.compute);
       }
     }
-    // G_j += X^T . dY_j (+ bias column sums), in place on the resident shard.
-    if (dx_sms) set_sm_budget(all_sms - dx_sms);
     group_->each([&](size_t r) {
       Worker& w = group_->worker(r);
       const cudaStream_t ws = dx_sms ? w.aux : w.compute;
+      set_launch_wait_flag(g_flag && s > 0 ? w.flag(flag_base_ + kFlagBwdG + s) : nullptr);
       const size_t k = k_of[r];
       const size_t j = slots_[r].logical_id;
       float* g = static_cast<float*>(slots_[r].grad_acc.data());
       // step 0 after zero_grads(): every resident gradient is zero -> overwrite
       const float* g_in = (grads_zero_pending_ && s == 0) ? nullptr : g;
-      check_status(rtpb_wgrad_step(dt, x_cache_[r].data, x_cache_[r].ld ? x_cache_[r].ld : in_, dy[k].data,
-                                   dy[k].ld ? dy[k].ld : out_, j * per_, g_in, g, rows, in_, per_,
-                                   workspace_[r].data(), workspace_[r].bytes(), ws));
+      const int rc = rtpb_wgrad_step(dt, x_cache_[r].data, x_cache_[r].ld ? x_cache_[r].ld : in_, dy[k].data,
+                                     dy[k].ld ? dy[k].ld : out_, j * per_, g_in, g, rows, in_, per_,
+                                     workspace_[r].data(), workspace_[r].bytes(), ws);
+      set_launch_wait_flag(nullptr);
+      check_status(rc);
     });
     if (dx_sms) set_sm_budget(all_sms);
     if (!rotate) break;
@@ -577,12 +648,14 @@ void RtpLinear::backward_ex(std::span<const DView> dy, size_t rows, std::span<co
       group_->comm_after_compute();
     }
     for (size_t r : local) gp[r] = slots_[r].grad_acc.data();
-    group_->exchange(Direction::CounterClockwise, gp, gp, slots_[local[0]].grad_acc.bytes());
+    flagged_exchange(Direction::CounterClockwise, gp, gp, slots_[local[0]].grad_acc.bytes(), kFlagBwdG + s + 1);
     for (size_t r : local) group_->worker(r).record(Ev::GDone, true);
     if (oopm)
       for (size_t r : local) swap_data(slots_[r].weight, spares_[r]);
     group_->advance_slots(slots_, Direction::CounterClockwise, PayloadKind::WeightAndGrad, label_, shard_len_);
   }
+  if (n > 1 && use_flags())
+    for (size_t r : local) group_->worker(r).wait(Ev::PassEnd, false);
   grads_zero_pending_ = false;
   for (size_t r : local) x_cache_[r] = {};
   require_home("end of backward");

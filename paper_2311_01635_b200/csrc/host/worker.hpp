@@ -26,7 +26,7 @@ void cuda_check(cudaError_t e, const char* where);
 // Fork / Join: compute <-> aux stream hand-offs (N = 1 dX || dW overlap).
 enum class Ev : int {
   Compute = 0, WDone = 1, GDone = 2, Comm = 3, Ready = 4, Consumed = 5, Staged = 6, Fork = 7, Join = 8, AuxDone = 9,
-  kCount = 10
+  PassEnd = 10, kCount = 11
 };
 
 struct Worker {
@@ -43,6 +43,11 @@ struct Worker {
   cudaEvent_t ev[int(Ev::kCount)] = {};
   MemoryLedger ledger;
   DeviceBuffer stage;  // in-place rotation staging chunk (CommBuffer)
+  // Shard-arrival flags written by the comm stream (stream memory ops) and
+  // waited on inside the step GEMMs; kFlagsPerLayer per layer.
+  static constexpr size_t kFlagPool = 8192, kFlagsPerLayer = 48;
+  DeviceBuffer flags;
+  unsigned* flag(size_t i) { return static_cast<unsigned*>(flags.data()) + i; }
 
   void record(Ev e, bool on_comm) { cuda_check(cudaEventRecord(ev[int(e)], on_comm ? comm : compute), "record"); }
   void wait(Ev e, bool on_comm) {
@@ -67,6 +72,10 @@ struct Worker {
   // Staging for an in-place shift of `bytes`: one chunk, charged as CommBuffer.
   void* staging(size_t bytes, size_t* chunk);
 };
+
+// Stream memory operation: *addr = v once the stream's prior work is done
+// (cuStreamWriteValue32 with its default memory barrier).
+void stream_write_u32(cudaStream_t s, unsigned* addr, unsigned v);
 
 // In-place rotation staging chunk: a small fraction of the shard so the
 // in-place mode stays within its (W+G)/N memory model.

@@ -96,6 +96,7 @@ int device_sms() {
 // persistent grid and the tile / split-K choice are sized for them, so two
 // GEMMs issued on two streams run side by side instead of queueing.
 thread_local int t_sm_budget = 0;
+thread_local const unsigned* t_wait_flag = nullptr;
 int sm_count() {
   const int all = device_sms();
   return (t_sm_budget >= 2 && t_sm_budget < all) ? (t_sm_budget & ~1) : all;
@@ -180,6 +181,7 @@ int launch_cfg(const Op& a, const Op& b, const Out& c0, const Out* c1, const Gem
   }
   GemmArgs a_ = args;
   a_.trace = next_trace(cfg.gridDim.x);
+  if (!a_.ready_flag) a_.ready_flag = t_wait_flag;  // set_launch_wait_flag()
   cudaError_t e = cudaLaunchKernelEx(&cfg, rtp_gemm_kernel<Cfg>, maps, maps2 ? *maps2 : maps, a_);
   if (e != cudaSuccess) return set_cuda_error(e, "rtp_gemm_kernel launch");
   count_launch();
@@ -761,6 +763,7 @@ int gemm_bwd_fused(const FusedBwdArgs& a, const FusedBwdPlan& plan, const FusedB
 }
 
 void set_sm_budget(int sms) { t_sm_budget = sms; }
+void set_launch_wait_flag(const unsigned* flag) { t_wait_flag = flag; }
 int sm_budget() { return sm_count(); }
 
 void set_trace(void* buf, size_t bytes) {

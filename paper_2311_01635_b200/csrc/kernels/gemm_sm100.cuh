@@ -109,6 +109,11 @@ struct GemmArgs {
   const float* wpart2;
   float* gout;  // wpar 2: the gradient block written by plain stores (I x per, ld per)
   float* gout2;
+  // Operand arrival written by another stream (the rotation's comm stream,
+  // cuStreamWriteValue32): the producers load nothing before *ready_flag >= 1.
+  // Replaces a stream-event dependency, so the launch keeps its programmatic
+  // (PDL) edge to the previous GEMM on its stream.
+  const unsigned* ready_flag;
   unsigned* dep_count;
   unsigned dep_target;
   int dep_rows;
@@ -522,6 +527,15 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
   // overlapped the previous kernel's tail; global data is touched only after
   // it has completed. Then let the next kernel's prologue start.
   griddep_wait();
+  if (args.ready_flag) {
+    // every role reads the arriving shard (operands, FWD bias, the travelling
+    // gradient's reduce-add and bias sums): each warp acquires the flag itself
+    if ((threadIdx.x & 31) == 0) detail::wait_counter(args.ready_flag, 1u);
+    __syncwarp();
+  }
+  // Only a running grid admits its successor: a grid still waiting for its
+  // shard must not let the next launch on its stream take the SMs that the
+  // other stream's kernels (the shard's producers' predecessors) need.
   griddep_launch();
   if (threadIdx.x == 0) detail::trace_at(trace, 1);
 

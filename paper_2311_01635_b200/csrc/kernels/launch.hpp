@@ -126,6 +126,9 @@ int fused_fwd_step(const void* x, size_t ldx, const void* w1_shard, void* pre, v
 // sm_budget() returns the effective count.
 void set_sm_budget(int sms);
 int sm_budget();
+// The calling thread's following GEMM launches load no operand before
+// *flag >= 1 (nullptr: no wait). See GemmArgs::ready_flag.
+void set_launch_wait_flag(const unsigned* flag);
 // Debug: route per-CTA timeline stamps of the following GEMM launches into buf.
 void set_trace(void* buf, size_t bytes);
 int gemm_dgrad(bool f32, const StepDgrad& p, cudaStream_t s);
