@@ -78,9 +78,20 @@ bool n1_scheduling_pays(size_t rows, size_t a, size_t b) {
 // small per it is HBM-bound while dW stays tensor-bound: sharing
 // the SMs overlaps the two. Model: 1.5 PFLOP/s over all SMs, 6 TB/s HBM;
 // returns 0 (no split) unless the split step is >= 10 % faster.
+// The model takes HBM as reachable from any number of SMs; it is not: the
+// dX epilogue streams its fp32 tiles at ~25-50 GB/s per SM, so on a share of
+// the SMs dX runs far below 6 TB/s. Measured (`bench.py --solo N`, config
+// (b), per-GPU TFLOP/s, both layers split / neither): N = 2 501 / 541, N = 4
+// 271 / 329, N = 8 204 / 186; at N = 8 splitting only ffn2 gives 188. The
+// gain is ffn1's: its dX (I = 768) is 96 CTA-pair tiles, 1.3 waves, and its
+// dW a short split-K chain, so the two fit side by side. So the split is
+// kept for a dX of under two waves of pair tiles: N = 2 / 4 / 8 then measure
+// 546 / 365 / 203 (vs 546 / 330 / 187 without any split).
 int nway_dx_sms(size_t rows, size_t I, size_t per) {
   if (std::getenv("RTPB_NO_OVERLAP")) return 0;
   if (const char* e = std::getenv("RTPB_NWAY_DX_SMS")) return std::atoi(e);
+  const size_t tiles_d = ((rows + 255) / 256) * ((I + 255) / 256);
+  if (tiles_d >= size_t(sm_budget())) return 0;
   const int all = sm_budget();
   const double flops = 2.0 * double(rows) * double(I) * double(per);
   const double p_sm = 1.5e15 / 148.0, rmw = 8.0 * double(rows) * double(I) / 6e12;

@@ -749,6 +749,41 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
           }
         }
       }
+      if constexpr (Cfg::EPI == EPI_DGRAD) {
+        // The epilogue reads the fp32 cross-step accumulator (last step) and
+        // pre (gelu'): with a short K it, not the MMAs, bounds the tile, and
+        // per-row loads from HBM leave too few bytes in flight. Pull the rows
+        // of this warp pair's slab into L2 two units ahead (the first unit
+        // also its own and the next), so the epilogue's loads hit L2.
+        if (half == 0) {
+          auto pf = [&](const Unit& u) {
+            const bool acc_in = (u.flags & EF_LAST) && !(u.flags & EF_FIRST);
+            const void* ux = u.prob ? args.aux2 : args.aux;
+            const bool pre_in = (u.flags & EF_LAST) && (u.flags & EF_GELU_BWD) && ux;
+            if (!acc_in && !pre_in) return;
+            const int r = u.mb * Cfg::TILE_M + int(rank) * BM + q * 32 + lane;
+            const int c0 = u.nb * BN;
+            if (r >= u.M || c0 >= u.N) return;
+            const int nc = min(BN, u.N - c0);
+            if (acc_in && args.acc) {
+              const uint32_t nb = uint32_t(nc * 4) & ~15u;
+              const float* src = args.acc + size_t(r) * args.ld_acc + c0;
+              if (nb && !(reinterpret_cast<uintptr_t>(src) & 15)) prefetch_l2_bulk(src, nb);
+            }
+            if (pre_in) {
+              const uint32_t nb = uint32_t(nc * Cfg::ELEM) & ~15u;
+              const uint8_t* src = static_cast<const uint8_t*>(ux) +
+                                   (size_t(r) * args.ld_aux + c0) * Cfg::ELEM;
+              if (nb && !(reinterpret_cast<uintptr_t>(src) & 15)) prefetch_l2_bulk(src, nb);
+            }
+          };
+          if (li == 0) {
+            pf(x_);
+            if (it + it_step < it_end) pf(decode(it + it_step));
+          }
+          if (it + 2 * it_step < it_end) pf(decode(it + 2 * it_step));
+        }
+      }
       float* bias_w = bias_base + ew * (Cfg::BIAS_WARP / 4);
       if constexpr (Cfg::EPI == EPI_FWD) {
         __syncwarp();  // every lane finished reading the previous tile's bias
@@ -767,6 +802,25 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
         }
         __syncwarp();
       }
+      // DGRAD last step: the fp32 accumulator's rows are loaded one chunk
+      // ahead into registers (the first before the accumulator wait), so
+      // each chunk's loads are in flight while the previous chunk is stored.
+      const bool acc_rd = Cfg::EPI == EPI_DGRAD && last && !first && row_ok;
+      float4 acc_nx[8];
+      auto load_acc = [&](int c, float4* d) {
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+          if (c + g * 8 < uN) {
+            const float4* p = reinterpret_cast<const float4*>(args.acc + row * args.ld_acc + c + g * 8);
+            d[2 * g] = p[0];
+            d[2 * g + 1] = p[1];
+          } else {
+            d[2 * g] = d[2 * g + 1] = make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+        }
+      };
+      if constexpr (Cfg::EPI == EPI_DGRAD)
+        if (acc_rd && n0 + half * 32 < uN) load_acc(n0 + half * 32, acc_nx);
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
       if (tr) detail::trace_at(trace, 6 + 6 * li);
@@ -802,6 +856,15 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
       for (int ch = half; ch < BN / 32; ch += NSPLIT) {
         const int nc = n0 + ch * 32;
         if (nc >= uN) break;  // warp-uniform
+        float4 acc_cur[8];
+        if constexpr (Cfg::EPI == EPI_DGRAD) {
+          if (acc_rd) {
+#pragma unroll
+            for (int g = 0; g < 8; ++g) acc_cur[g] = acc_nx[g];
+            const int nn = nc + NSPLIT * 32;
+            if (ch + NSPLIT < BN / 32 && nn < uN) load_acc(nn, acc_nx);
+          }
+        }
         uint32_t v[32];
         tmem_ld_32x32b_x32(t_row + ch * 32, v);
         tmem_ld_wait();
@@ -855,15 +918,12 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
             }
           }
         } else if constexpr (Cfg::EPI == EPI_DGRAD) {
-          if (last && !first && row_ok) {
+          if (acc_rd) {
 #pragma unroll
-            for (int g = 0; g < 4; ++g)
-              if (nc + g * 8 < uN) {
-                const float4* p = reinterpret_cast<const float4*>(args.acc + row * args.ld_acc + nc + g * 8);
-                const float4 a = p[0], b = p[1];
-                x[g * 8 + 0] += a.x; x[g * 8 + 1] += a.y; x[g * 8 + 2] += a.z; x[g * 8 + 3] += a.w;
-                x[g * 8 + 4] += b.x; x[g * 8 + 5] += b.y; x[g * 8 + 6] += b.z; x[g * 8 + 7] += b.w;
-              }
+            for (int g = 0; g < 8; ++g) {
+              const float4 a = acc_cur[g];
+              x[g * 4 + 0] += a.x; x[g * 4 + 1] += a.y; x[g * 4 + 2] += a.z; x[g * 4 + 3] += a.w;
+            }
           }
           if (pre_tma) {
             // pre chunk staged by TMA in the same swizzled 32 x 32 layout as the outputs

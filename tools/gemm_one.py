@@ -30,6 +30,12 @@ fns = {"fwd": lambda: rtp.fwd_step(X, sh, Y, 0, per),
        "dgrad_gelu": lambda: rtp.dgrad_step(dY, 0, sh, None, dX, M, I, per, True, True, pre=pre),
        "dgrad": lambda: rtp.dgrad_step(dY, 0, sh, None, dX, M, I, per, True, True),
        "wgrad": lambda: rtp.wgrad_step(X, dY, 0, G, G, per)}
+if any(k.startswith("dgrad_") and k != "dgrad_gelu" for k in kinds):  # cross-step fp32 accumulator kinds
+    ACC = torch.zeros(M, I, dtype=torch.float32, device=dev)
+    fns["dgrad_first"] = lambda: rtp.dgrad_step(dY, 0, sh, ACC, dX, M, I, per, True, False)
+    fns["dgrad_mid"] = lambda: rtp.dgrad_step(dY, 0, sh, ACC, dX, M, I, per, False, False)
+    fns["dgrad_last"] = lambda: rtp.dgrad_step(dY, 0, sh, ACC, dX, M, I, per, False, True)
+    fns["dgrad_last_gelu"] = lambda: rtp.dgrad_step(dY, 0, sh, ACC, dX, M, I, per, False, True, pre=pre)
 if "wgrad_as_dgrad" in kinds:  # the dW product on the dgrad kernel: X^T (I x M) . (dY^T (per x M))^T
     XT2 = X.t().contiguous()
     WT = torch.empty(per * M + M, dtype=torch.bfloat16, device=dev)
@@ -49,7 +55,9 @@ for k in kinds:
     b.record()
     torch.cuda.synchronize()
     us = a.elapsed_time(b) / 10 * 1e3
-    print(f"{k:6s} M={M} I={I} per={per} tile={code}: {us:8.1f} us {fl / us / 1e6:6.0f} TF/s", flush=True)
+    hbm = {"dgrad_first": 4, "dgrad_mid": 8, "dgrad_last": 6, "dgrad_last_gelu": 8}.get(k, 0) * M * I
+    extra = f" {hbm / us / 1e3:6.0f} GB/s acc traffic" if hbm else ""
+    print(f"{k:6s} M={M} I={I} per={per} tile={code}: {us:8.1f} us {fl / us / 1e6:6.0f} TF/s{extra}", flush=True)
 
 if os.environ.get("TRACE"):
     import numpy as np
