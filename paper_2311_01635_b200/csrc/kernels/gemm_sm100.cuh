@@ -749,41 +749,6 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
           }
         }
       }
-      if constexpr (Cfg::EPI == EPI_DGRAD) {
-        // The epilogue reads the fp32 cross-step accumulator (last step) and
-        // pre (gelu'): with a short K it, not the MMAs, bounds the tile, and
-        // per-row loads from HBM leave too few bytes in flight. Pull the rows
-        // of this warp pair's slab into L2 two units ahead (the first unit
-        // also its own and the next), so the epilogue's loads hit L2.
-        if (half == 0) {
-          auto pf = [&](const Unit& u) {
-            const bool acc_in = (u.flags & EF_LAST) && !(u.flags & EF_FIRST);
-            const void* ux = u.prob ? args.aux2 : args.aux;
-            const bool pre_in = (u.flags & EF_LAST) && (u.flags & EF_GELU_BWD) && ux;
-            if (!acc_in && !pre_in) return;
-            const int r = u.mb * Cfg::TILE_M + int(rank) * BM + q * 32 + lane;
-            const int c0 = u.nb * BN;
-            if (r >= u.M || c0 >= u.N) return;
-            const int nc = min(BN, u.N - c0);
-            if (acc_in && args.acc) {
-              const uint32_t nb = uint32_t(nc * 4) & ~15u;
-              const float* src = args.acc + size_t(r) * args.ld_acc + c0;
-              if (nb && !(reinterpret_cast<uintptr_t>(src) & 15)) prefetch_l2_bulk(src, nb);
-            }
-            if (pre_in) {
-              const uint32_t nb = uint32_t(nc * Cfg::ELEM) & ~15u;
-              const uint8_t* src = static_cast<const uint8_t*>(ux) +
-                                   (size_t(r) * args.ld_aux + c0) * Cfg::ELEM;
-              if (nb && !(reinterpret_cast<uintptr_t>(src) & 15)) prefetch_l2_bulk(src, nb);
-            }
-          };
-          if (li == 0) {
-            pf(x_);
-            if (it + it_step < it_end) pf(decode(it + it_step));
-          }
-          if (it + 2 * it_step < it_end) pf(decode(it + 2 * it_step));
-        }
-      }
       float* bias_w = bias_base + ew * (Cfg::BIAS_WARP / 4);
       if constexpr (Cfg::EPI == EPI_FWD) {
         __syncwarp();  // every lane finished reading the previous tile's bias
