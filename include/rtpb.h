@@ -266,6 +266,10 @@ int rtpb_mlp_begin_step(rtpb_mlp m); /* RtpModel::begin_step (model.cpp:54-57) *
 int rtpb_mlp_zero_grads(rtpb_mlp m);
 int rtpb_mlp_forward(rtpb_mlp m, const void* const* x, size_t rows, void* const* y, int mode);
 int rtpb_mlp_backward(rtpb_mlp m, const void* const* dy, size_t rows, void* const* dx);
+/* Stack order (RtpModel's block sequence, model.cpp:77-83 / 99-105): `next`
+ * follows `m` in forward. Linked blocks post the neighbour's first weight
+ * shift under their own last step (out-of-place mode). next = NULL unlinks. */
+int rtpb_mlp_chain(rtpb_mlp m, rtpb_mlp next);
 /* layer 0 = ffn1, 1 = ffn2 */
 rtpb_linear rtpb_mlp_layer(rtpb_mlp m, int layer);
 

@@ -349,6 +349,7 @@ class RtpLinear : public RtpLayerBase {
   // blocks of the layer's flag range, indexed by the step the shard is for.
   static constexpr size_t kFlagFwd = 0, kFlagBwdW = 16, kFlagBwdG = 32;
   bool use_flags() const;
+  void reset_flags(size_t first, size_t count);
   void flagged_exchange(Direction dir, std::span<void* const> send, std::span<void* const> recv, size_t bytes,
                         size_t flag);
 
@@ -377,8 +378,20 @@ class RtpMlp {
   void backward(std::span<const DView> dy, size_t rows, std::span<const DView> dx);
   RtpLinear& ffn1() { return *ffn1_; }
   RtpLinear& ffn2() { return *ffn2_; }
+  // Stack order (RtpModel's block sequence, model.cpp:77-83 / 99-105): `next`
+  // runs after this block in forward and before it in backward. Linked
+  // blocks post the neighbour's first weight shift under their own last step
+  // (SURVEY §8f.1): this block's forward prefetches next's ffn1 forward
+  // shift; next's backward prefetches this block's ffn2 backward shift.
+  // nullptr unlinks. Out-of-place mode only (the shift lands in the spare).
+  void chain(RtpMlp* next);
+  ~RtpMlp();  // unlinks its neighbours
+  RtpMlp(const RtpMlp&) = delete;
+  RtpMlp& operator=(const RtpMlp&) = delete;
 
  private:
+  RtpMlp* next_ = nullptr;
+  RtpMlp* prev_ = nullptr;
   void ensure_acts(size_t rows);
   WorkerGroup* group_;
   size_t h_, f_;

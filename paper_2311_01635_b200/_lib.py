@@ -86,6 +86,7 @@ _SIGS = {
     "rtpb_mlp_zero_grads": (_int, [_vp]),
     "rtpb_mlp_forward": (_int, [_vp, _vpp, _sz, _vpp, _int]),
     "rtpb_mlp_backward": (_int, [_vp, _vpp, _sz, _vpp]),
+    "rtpb_mlp_chain": (_int, [_vp, _vp]),
     "rtpb_mlp_layer": (_vp, [_vp, _int]),
 }
 

@@ -431,6 +431,10 @@ int rtpb_mlp_backward(rtpb_mlp m, const void* const* dy, size_t rows, void* cons
   });
 }
 
+int rtpb_mlp_chain(rtpb_mlp m, rtpb_mlp next) {
+  return guard([&] { m->m->chain(next ? next->m.get() : nullptr); });
+}
+
 rtpb_linear rtpb_mlp_layer(rtpb_mlp m, int layer) {
   rtpb_linear_s& v = layer == 0 ? m->ffn1 : m->ffn2;
   // Non-owning view: the unique_ptr aliases the MLP's layer and is released

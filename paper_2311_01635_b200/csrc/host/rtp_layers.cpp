@@ -395,14 +395,16 @@ void RtpLinear::forward_ex(std::span<const DView> x, size_t rows, std::span<cons
   // flags: the compute stream never waited for this pass's shifts; join them
   // once at its end (stream capture requires it). A shift the hook prefetched
   // for the next layer stays in flight; that layer's pass joins it.
-  if (n > 1 && prefetch && use_flags())
+  if (n > 1 && prefetch && use_flags()) {
     for (size_t r : local) group_->worker(r).wait(Ev::PassEnd, false);
+    reset_flags(kFlagFwd, kFlagBwdW - kFlagFwd);
+  }
   if (mode == Mode::Eval) rehome_after_eval();
 }
 
 // Arrival flags (bf16 mode, one worker per GPU, N <= 16): the shift's comm
-// stream clears the flag, moves the shard, then sets it with stream memory
-// operations (no SM needed); the consuming step GEMM waits for it on the device
+// stream moves the shard, then sets the flag with a stream memory operation
+// (no SM needed; reset_flags clears a pass's flags at its end); the consuming step GEMM waits for it on the device
 // instead of its stream waiting for comm, so consecutive step GEMMs keep their
 // programmatic (PDL) launch overlap. Deadlock freedom: every flag's writer was
 // issued before its waiter and waits only on earlier-issued kernels; a waiting
@@ -419,16 +421,24 @@ bool RtpLinear::use_flags() const {
          !std::getenv("RTPB_NO_FLAGS");
 }
 
+// A pass's flags go back to 0 on the compute stream once every reader has
+// run (pass end, after the join), so the next pass's readers, later on the
+// same stream, cannot see a stale 1, and its writers (comm, ordered after the
+// compute tail) set them only after. (Clearing on the comm stream before the
+// shift would race: the reading GEMM starts, by PDL, as soon as its
+// predecessor ends, which is also when that comm stream is released.)
+void RtpLinear::reset_flags(size_t first, size_t count) {
+  for (size_t r : group_->local_ranks()) {
+    Worker& w = group_->worker(r);
+    DeviceGuard dg(w.device);
+    cuda_check(cudaMemsetAsync(w.flag(flag_base_ + first), 0, count * sizeof(unsigned), w.compute), "reset flags");
+  }
+}
+
 void RtpLinear::flagged_exchange(Direction dir, std::span<void* const> send, std::span<void* const> recv,
                                  size_t bytes, size_t flag) {
   const auto& local = group_->local_ranks();
   const bool fl = use_flags();
-  if (fl)
-    for (size_t r : local) {
-      Worker& w = group_->worker(r);
-      DeviceGuard dg(w.device);
-      stream_write_u32(w.comm, w.flag(flag_base_ + flag), 0u);
-    }
   group_->exchange(dir, send, recv, bytes);
   if (fl)
     for (size_t r : local) {
@@ -665,8 +675,14 @@ void RtpLinear::backward_ex(std::span<const DView> dy, size_t rows, std::span<co
       for (size_t r : local) swap_data(slots_[r].weight, spares_[r]);
     group_->advance_slots(slots_, Direction::CounterClockwise, PayloadKind::WeightAndGrad, label_, shard_len_);
   }
-  if (n > 1 && use_flags())
-    for (size_t r : local) group_->worker(r).wait(Ev::PassEnd, false);
+  if (n > 1 && use_flags()) {
+    for (size_t r : local) {
+      Worker& w = group_->worker(r);
+      w.wait(Ev::PassEnd, false);
+      if (dx_sms) w.join_aux();  // the G flags' readers ran on aux
+    }
+    reset_flags(kFlagBwdW, Worker::kFlagsPerLayer - kFlagBwdW);
+  }
   grads_zero_pending_ = false;
   for (size_t r : local) x_cache_[r] = {};
   require_home("end of backward");
@@ -787,7 +803,28 @@ void RtpMlp::forward(std::span<const DView> x, size_t rows, std::span<const DVie
   // ffn2's first shift travels under ffn1's last step
   if (!std::getenv("RTPB_NO_PREFETCH")) e1.before_last_step = [&] { ffn2_->prefetch_first_shift(false); };
   ffn1_->forward_ex(x, rows, pre, mode, e1);
-  ffn2_->forward(act, rows, y, mode);  // model.cpp:83
+  RtpLinear::FwdEpi e2;
+  e2.store_pre = true;  // plain linear: y is the output
+  // the next block's first shift travels under this block's last step
+  if (next_ && !std::getenv("RTPB_NO_PREFETCH"))
+    e2.before_last_step = [&] { next_->ffn1_->prefetch_first_shift(false); };
+  ffn2_->forward_ex(act, rows, y, mode, e2);  // model.cpp:83
+}
+
+RtpMlp::~RtpMlp() {
+  if (next_) next_->prev_ = nullptr;
+  if (prev_) prev_->next_ = nullptr;
+}
+
+void RtpMlp::chain(RtpMlp* next) {
+  if (next == this) throw ConfigError("RtpMlp::chain: a block cannot follow itself");
+  if (next && next->group_ != group_) throw ConfigError("RtpMlp::chain: blocks of different worker groups");
+  if (next_) next_->prev_ = nullptr;
+  next_ = next;
+  if (next) {
+    if (next->prev_) next->prev_->next_ = nullptr;
+    next->prev_ = this;
+  }
 }
 
 void RtpMlp::ensure_fused_bwd(size_t rows) {
@@ -862,7 +899,11 @@ void RtpMlp::backward(std::span<const DView> dy, size_t rows, std::span<const DV
   e2.pre = pre;
   if (!std::getenv("RTPB_NO_PREFETCH")) e2.before_last_step = [&] { ffn1_->prefetch_first_shift(true); };
   ffn2_->backward_ex(dy, rows, pre, e2);
-  ffn1_->backward_ex(pre, rows, dx, RtpLinear::BwdEpi{});  // model.cpp:105
+  RtpLinear::BwdEpi e1;
+  // the previous block's first backward shift travels under this block's last step
+  if (prev_ && !std::getenv("RTPB_NO_PREFETCH"))
+    e1.before_last_step = [&] { prev_->ffn2_->prefetch_first_shift(true); };
+  ffn1_->backward_ex(pre, rows, dx, e1);  // model.cpp:105
   group_->join_aux();
 }
 

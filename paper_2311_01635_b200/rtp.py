@@ -345,6 +345,12 @@ class RtpMlp(_Layer):
     def begin_step(self):
         check(lib.rtpb_mlp_begin_step(self._h))
 
+    def chain(self, nxt: "RtpMlp | None"):
+        """Stack order: `nxt` follows this block in forward. Linked blocks post
+        the neighbour's first weight shift under their own last step."""
+        check(lib.rtpb_mlp_chain(self._h, nxt._h if nxt is not None else None))
+        self._next = nxt  # keep the neighbour alive while linked
+
     def zero_grads(self):
         check(lib.rtpb_mlp_zero_grads(self._h))
 

@@ -112,3 +112,54 @@ def run_mlp(n, w1, b1, w2, b2, x, dy, dtype="bf16", mode="inplace", transport="l
     m.close()
     g.close()
     return out
+
+
+STACK = dict(blocks=3, h=256, f=1024, rows_per_worker=256, steps=2)
+
+
+def run_stack_local(g, ranks, n, chain=True, **kw):
+    """A stack of Flyweight MLP blocks (out-of-place), `steps` training steps
+    (zero_grads, forward through the blocks, backward in reverse), optionally
+    chained so each block prefetches its neighbour's first shift. Runs the
+    group's local ranks `ranks`; returns their outputs of the last step, dX
+    and every block's gradient shards (keys per rank)."""
+    import torch
+    from paper_2311_01635_b200 import rtp
+    p = {**STACK, **kw}
+    h, f, M = p["h"], p["f"], p["rows_per_worker"]
+    per_block = 2 * h * f + f + h
+    mlps = []
+    for b in range(p["blocks"]):
+        m = rtp.RtpMlp(g, f"block{b}", h, f, "bf16", seed=42, stream_base=b * per_block)
+        m.set_rotation_mode("outofplace")
+        m.begin_step()
+        mlps.append(m)
+    if chain:
+        for a, b in zip(mlps, mlps[1:]):
+            a.chain(b)
+    out = {}
+    for step in range(p["steps"]):
+        xs, dys = [], []
+        for r in ranks:
+            gen = torch.Generator().manual_seed(1000 * step + r)
+            xs.append(((torch.rand(M, h, generator=gen) * 2 - 1).to(torch.bfloat16)).cuda())
+            dys.append(((torch.rand(M, h, generator=gen) * 2 - 1).to(torch.bfloat16)).cuda())
+        for m in mlps:
+            m.zero_grads()
+        inp = xs
+        for m in mlps:
+            inp = m.forward(inp)
+        up = dys
+        for m in reversed(mlps):
+            up = m.backward(up)
+        g.synchronize()
+    for k, r in enumerate(ranks):
+        out[f"y{r}"] = to_np(inp[k])
+        out[f"dx{r}"] = to_np(up[k])
+        for b, m in enumerate(mlps):
+            out[f"g{b}_1_{r}"] = to_np(m.ffn1.grad_shard(r))
+            out[f"g{b}_2_{r}"] = to_np(m.ffn2.grad_shard(r))
+            out[f"home{b}_{r}"] = np.array([m.ffn1.slot(r)["logical_id"], m.ffn2.slot(r)["logical_id"]])
+    for m in mlps:
+        m.close()
+    return out

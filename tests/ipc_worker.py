@@ -2,7 +2,7 @@
 tests/test_gpu_ipc.py; all ranks may share GPU 0). Runs the golden RtpLinear
 or MLP fixture on this rank's rows and saves its outputs to an .npz.
 
-python tests/ipc_worker.py <case: linear|mlp> <n> <rank> <uid hex> <mode> <out.npz>
+python tests/ipc_worker.py <case: linear|mlp|stack> <n> <rank> <uid hex> <mode> <out.npz>
 """
 import os
 import sys
@@ -24,7 +24,7 @@ def main():
     dev = int(os.environ.get("RTPB_IPC_DEVICE", "0"))
     torch.cuda.set_device(dev)
     g = rtp.WorkerGroup.ipc(n, rank, dev, bytes.fromhex(uid_hex))
-    fx = np.load(os.path.join(ROOT, "tests", "golden", f"{case}.npz"))
+    fx = np.load(os.path.join(ROOT, "tests", "golden", f"{case}.npz")) if case != "stack" else None
     res = {}
     if case == "linear":
         w, b, x, dy = fx["w"], fx["b"], fx["x"], fx["dy"]
@@ -42,6 +42,9 @@ def main():
                    bwd_id=lin.slot(rank)["logical_id"], trace=np.array(lin.trace()),
                    traffic=np.array([[{"rotation_cw": 0, "rotation_ccw": 1}[k], a, c] for k, a, c in g.traffic()]))
         lin.close()
+    elif case == "stack":
+        from helpers import run_stack_local
+        res.update(run_stack_local(g, [rank], n, chain=os.environ.get("RTPB_TEST_CHAIN", "1") == "1"))
     else:
         w1, b1, w2, b2, x, dy = (fx[k] for k in ("w1", "b1", "w2", "b2", "x", "dy"))
         M = x.shape[0] // n

@@ -87,3 +87,23 @@ def test_mlp_multiprocess_ipc_dx_dw_side_by_side(golden, tmp_path):
     for r in range(n):
         assert nerr(res[r]["grad1"], g[f"n{n}_grads1"][r]) < TOL["bf16"]
         assert nerr(res[r]["grad2"], g[f"n{n}_grads2"][r]) < TOL["bf16"]
+
+
+@pytest.mark.parametrize("chain", ["1", "0"])
+def test_chained_stack_multiprocess_ipc(tmp_path, chain):
+    """A 3-block stack, two training steps, blocks chained (each block posts
+    its neighbour's first shift under its own last step) or not: one process
+    per worker equals the in-process run bit for bit, and chaining changes no
+    bit (it only moves when shifts are posted)."""
+    from helpers import run_stack_local
+    from paper_2311_01635_b200 import rtp
+    n = 4
+    res = spawn("stack", n, "outofplace", tmp_path, env={"RTPB_TEST_CHAIN": chain})
+    g = rtp.WorkerGroup(n, "lockstep")
+    ref = run_stack_local(g, list(range(n)), n, chain=False)
+    g.close()
+    for r in range(n):
+        for k, v in res[r].items():
+            assert np.array_equal(v, ref[k]), (r, k)
+        for b in range(3):
+            assert list(res[r][f"home{b}_{r}"]) == [r, r]

@@ -329,3 +329,24 @@ def test_config_b_mlp_full_size_row_sample(oracle, n):
                          dtype_round(dy[rows], "bf16"))
     assert nerr(out["y"][rows], ref["y"]) < 2e-2
     assert nerr(out["dx"][rows], ref["dx"]) < 2e-2
+
+
+def test_chained_stack_equals_unchained():
+    """Block-to-block shift prefetch (RtpMlp.chain) in the
+    in-process lockstep and concurrent transports: bit-identical results,
+    every shard home after each step."""
+    from helpers import run_stack_local
+    from paper_2311_01635_b200 import rtp
+    n = 4
+    outs = []
+    for transport, chain in (("lockstep", False), ("lockstep", True), ("concurrent", True)):
+        g = rtp.WorkerGroup(n, transport)
+        outs.append(run_stack_local(g, list(range(n)), n, chain=chain))
+        g.close()
+    for o in outs[1:]:
+        assert o.keys() == outs[0].keys()
+        for k in o:
+            assert np.array_equal(o[k], outs[0][k]), k
+    for r in range(n):
+        for b in range(3):
+            assert list(outs[1][f"home{b}_{r}"]) == [r, r]

@@ -45,6 +45,8 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=2)
     ap.add_argument("--out", default=None)
+    ap.add_argument("--no-chain", action="store_true",
+                    help="do not link the blocks (no block-to-block prefetch of the first shift)")
     args = ap.parse_args()
 
     h, f, tpw, tglobal, blocks = CONFIGS[args.config]
@@ -93,6 +95,9 @@ def main():
         m.set_rotation_mode(args.mode)
         m.begin_step()
         mlps.append(m)
+    if not args.no_chain:
+        for a, b in zip(mlps, mlps[1:]):
+            a.chain(b)  # each block posts its neighbour's first shift under its own last step
     g = torch.Generator(device=dev).manual_seed(42 + rank)
     xs = [(torch.rand(M, h, device=dev, generator=g) * 2 - 1).to(torch.bfloat16) for _ in ranks]
     dys = [(torch.rand(M, h, device=dev, generator=g) * 2 - 1).to(torch.bfloat16) for _ in ranks]
@@ -151,7 +156,7 @@ def main():
     worst = max(led, key=lambda d: d["peak_total"])
     pgc = worst["peak_param"] + worst["peak_grad"] + worst["peak_comm"]
     bytes_sent = (n - 1) / n * (2 * wb + gb) if n > 1 else 0.0  # per GPU per step
-    line = {"config": args.config, "how": how, "n": n, "rotation_mode": args.mode, "h": h, "f": f, "blocks": blocks,
+    line = {"config": args.config, "how": how, "n": n, "rotation_mode": args.mode, "chained": not args.no_chain, "h": h, "f": f, "blocks": blocks,
             "tokens_per_worker": M, "global_tokens": T, "steps": args.steps,
             "ms_per_step": ms, "ms_per_step_compute_only": ms_nocomm,
             "exposed_comm_ms": max(0.0, ms - ms_nocomm), "exposed_comm_frac": max(0.0, ms - ms_nocomm) / ms,
