@@ -414,11 +414,17 @@ void RtpLinear::forward_ex(std::span<const DView> x, size_t rows, std::span<cons
 // ordering: its operand-split pre-passes read the shard before the GEMM.
 // Several workers on one device (Lockstep/Concurrent) also keep events: their
 // spinning grids would compete for the same SMs.
+// Opt-in (RTPB_FLAGS=1): in a captured step the event edges cost no more —
+// `bench.py --solo N` (CUDA graph, config (b), TFLOP/s per GPU) measures
+// events / flags 573 / 545 at N = 2, 363 / 352 at N = 4, 194 / 200 at N = 8.
 bool RtpLinear::use_flags() const {
+  static const bool on = [] {
+    const char* e = std::getenv("RTPB_FLAGS");
+    return e && std::atoi(e) != 0;
+  }();
   const TransportKind k = group_->kind();
   const bool one_per_gpu = k == TransportKind::Nccl || k == TransportKind::Ipc || k == TransportKind::Solo;
-  return one_per_gpu && dtype_ == DType::BF16 && group_->size() > 1 && group_->size() <= 16 &&
-         !std::getenv("RTPB_NO_FLAGS");
+  return on && one_per_gpu && dtype_ == DType::BF16 && group_->size() > 1 && group_->size() <= 16;
 }
 
 // A pass's flags go back to 0 on the compute stream once every reader has

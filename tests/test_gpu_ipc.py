@@ -62,10 +62,13 @@ def test_linear_multiprocess_ipc(golden, tmp_path, n, mode):
                                                                           for t in g[p + "traffic"]]
 
 
+@pytest.mark.parametrize("flags", ["0", "1"])
 @pytest.mark.parametrize("n", [2, 4])
-def test_mlp_multiprocess_ipc(golden, tmp_path, n):
+def test_mlp_multiprocess_ipc(golden, tmp_path, n, flags):
+    """flags=1: the step GEMMs wait in-kernel on shard-arrival flags
+    (RTPB_FLAGS) instead of stream events; same bits either way."""
     g = golden("mlp")
-    res = spawn("mlp", n, "outofplace", tmp_path)
+    res = spawn("mlp", n, "outofplace", tmp_path, env={"RTPB_FLAGS": flags})
     ref = run_mlp(n, g["w1"], g["b1"], g["w2"], g["b2"], g["x"], g["dy"], "bf16", "outofplace")
     y = np.concatenate([r["y"] for r in res])
     dx = np.concatenate([r["dx"] for r in res])
@@ -89,16 +92,18 @@ def test_mlp_multiprocess_ipc_dx_dw_side_by_side(golden, tmp_path):
         assert nerr(res[r]["grad2"], g[f"n{n}_grads2"][r]) < TOL["bf16"]
 
 
+@pytest.mark.parametrize("flags", ["0", "1"])
 @pytest.mark.parametrize("chain", ["1", "0"])
-def test_chained_stack_multiprocess_ipc(tmp_path, chain):
+def test_chained_stack_multiprocess_ipc(tmp_path, chain, flags):
     """A 3-block stack, two training steps, blocks chained (each block posts
     its neighbour's first shift under its own last step) or not: one process
     per worker equals the in-process run bit for bit, and chaining changes no
-    bit (it only moves when shifts are posted)."""
+    bit (it only moves when shifts are posted). Two steps: flags=1 catches a
+    stale arrival flag from the previous step."""
     from helpers import run_stack_local
     from paper_2311_01635_b200 import rtp
     n = 4
-    res = spawn("stack", n, "outofplace", tmp_path, env={"RTPB_TEST_CHAIN": chain})
+    res = spawn("stack", n, "outofplace", tmp_path, env={"RTPB_TEST_CHAIN": chain, "RTPB_FLAGS": flags})
     g = rtp.WorkerGroup(n, "lockstep")
     ref = run_stack_local(g, list(range(n)), n, chain=False)
     g.close()
