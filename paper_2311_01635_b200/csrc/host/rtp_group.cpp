@@ -9,6 +9,7 @@
 #include <atomic>
 #include <cmath>
 #include <condition_variable>
+#include <chrono>
 #include <cstring>
 #include <exception>
 #include <mutex>
@@ -385,7 +386,24 @@ class NcclTransport final : public Transport {
     nccl_check(ncclCommInitRank(&comm_, int(g.size()), uid, int(rank)), "ncclCommInitRank");
   }
   ~NcclTransport() override {
-    if (comm_) ncclCommDestroy(comm_);
+    if (comm_) ncclCommDestroy(comm_);  // an aborted communicator is already gone
+  }
+  bool polled() const override { return true; }
+  void check_async() override {
+    ncclResult_t st = ncclSuccess;
+    if (!comm_ || aborted_) return;
+    nccl_check(ncclCommGetAsyncError(comm_, &st), "ncclCommGetAsyncError");
+    if (st != ncclSuccess && st != ncclInProgress) {
+      abort();
+      throw NcclError(std::string("ring shift failed asynchronously: ") + ncclGetErrorString(st));
+    }
+  }
+  void abort() override {
+    if (comm_ && !aborted_) {
+      ncclCommAbort(comm_);
+      comm_ = nullptr;
+      aborted_ = true;
+    }
   }
   void each(const std::function<void(size_t)>& fn) override {
     DeviceGuard dg(g_.worker(rank_).device);
@@ -421,6 +439,7 @@ class NcclTransport final : public Transport {
   WorkerGroup& g_;
   size_t rank_;
   ncclComm_t comm_ = nullptr;
+  bool aborted_ = false;
 };
 
 }  // namespace
@@ -541,13 +560,44 @@ void WorkerGroup::join_aux() {
   }
 }
 
+// With a transport whose peers can fail (NCCL), the wait is polled: an
+// asynchronous communicator error aborts the communicator and raises
+// NcclError, and a wait longer than RTPB_COMM_TIMEOUT_S (default 120 s)
+// aborts it and raises ProtocolError — the reference's rendezvous timeout
+// (ring.cpp:78-81) for a ring whose neighbour never posts its shift.
 void WorkerGroup::synchronize() {
+  if (!transport_ || !transport_->polled()) {
+    for (size_t r : local_) {
+      Worker& w = *workers_[r];
+      DeviceGuard dg(w.device);
+      cuda_check(cudaStreamSynchronize(w.aux), "sync aux");
+      cuda_check(cudaStreamSynchronize(w.compute), "sync compute");
+      cuda_check(cudaStreamSynchronize(w.comm), "sync comm");
+    }
+    return;
+  }
+  static const double limit_s = [] {
+    const char* e = std::getenv("RTPB_COMM_TIMEOUT_S");
+    return e ? std::max(0.1, std::atof(e)) : 120.0;
+  }();
+  const auto t0 = std::chrono::steady_clock::now();
   for (size_t r : local_) {
     Worker& w = *workers_[r];
     DeviceGuard dg(w.device);
-    cuda_check(cudaStreamSynchronize(w.aux), "sync aux");
-    cuda_check(cudaStreamSynchronize(w.compute), "sync compute");
-    cuda_check(cudaStreamSynchronize(w.comm), "sync comm");
+    for (cudaStream_t s : {w.aux, w.compute, w.comm}) {
+      for (;;) {
+        const cudaError_t q = cudaStreamQuery(s);
+        if (q == cudaSuccess) break;
+        if (q != cudaErrorNotReady) cuda_check(q, "sync (polled)");
+        transport_->check_async();
+        if (std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() > limit_s) {
+          transport_->abort();
+          throw ProtocolError("ring shift timed out after " + std::to_string(limit_s) +
+                              " s: a neighbour never posted its shift (RTPB_COMM_TIMEOUT_S)");
+        }
+        std::this_thread::sleep_for(std::chrono::microseconds(50));
+      }
+    }
   }
 }
 

@@ -90,6 +90,15 @@ class Transport {
   // rank means in place. On return the comm streams are ordered after the
   // transfer (both the rank's receive and its send).
   virtual void shift(Direction dir, std::span<void* const> send, std::span<void* const> recv, size_t bytes) = 0;
+  // Host-side wait watchdog (WorkerGroup::synchronize): true when waits on
+  // this transport's streams must be polled (a peer can fail or vanish).
+  virtual bool polled() const { return false; }
+  // Called while polling: throws (after aborting the transport) on an
+  // asynchronous transport error.
+  virtual void check_async() {}
+  // The wait exceeded its deadline: abort the transport (unblocks the
+  // streams) before the caller throws.
+  virtual void abort() {}
 };
 
 std::unique_ptr<Transport> make_local_transport(WorkerGroup& g, bool concurrent);

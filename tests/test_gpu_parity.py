@@ -331,6 +331,69 @@ def test_config_b_mlp_full_size_row_sample(oracle, n):
     assert nerr(out["dx"][rows], ref["dx"]) < 2e-2
 
 
+def test_config_d_block_row_sample():
+    """Config (d) layer shapes: one Flyweight MLP block 4096->16384->4096 on 8
+    simulated workers (per = 2048 / 512: the fp32 cross-step dX accumulator
+    over 8 steps), out-of-place, 1024 rows per worker. Y and dX rows are
+    row-independent, so fp64 products of the device's own bf16 weights (read
+    back from the home shards) on a row sample are exact references for those
+    rows; db2 = colsum(dY) is checked whole."""
+    import torch
+    from helpers import to_dev, to_np
+    from paper_2311_01635_b200 import rtp
+    n, h, f, M = 8, 4096, 16384, 1024
+    T = n * M
+    rng = np.random.default_rng(3)
+    x = rng.uniform(-1, 1, (T, h))
+    dy = rng.uniform(-1, 1, (T, h))
+    g = rtp.WorkerGroup(n, "lockstep")
+    m = rtp.RtpMlp(g, "blk", h, f, "bf16", seed=42, stream_base=0)
+    m.set_rotation_mode("outofplace")
+    m.begin_step()
+    m.zero_grads()
+    ys = m.forward([to_dev(x[r * M:(r + 1) * M], "bf16") for r in range(n)])
+    dxs = m.backward([to_dev(dy[r * M:(r + 1) * M], "bf16") for r in range(n)])
+    g.synchronize()
+
+    def full(lin, I, O):
+        per = O // n
+        W, b = np.empty((I, O)), np.empty(O)
+        for r in range(n):
+            sh = to_np(lin.weight_shard(r))
+            j = lin.slot(r)["logical_id"]
+            W[:, j * per:(j + 1) * per] = sh[:I * per].reshape(I, per)
+            b[j * per:(j + 1) * per] = sh[I * per:]
+        return W, b
+
+    W1, b1 = full(m.ffn1, h, f)
+    W2, b2 = full(m.ffn2, f, h)
+    rows = np.sort(rng.choice(T, 32, replace=False))
+    xr, dyr = dtype_round(x[rows], "bf16"), dtype_round(dy[rows], "bf16")
+    pre = xr @ W1 + b1
+    from math import erf, sqrt, pi
+    gelu = pre * 0.5 * (1 + np.vectorize(erf)(pre / sqrt(2)))
+    y_ref = gelu @ W2 + b2
+    dact = dyr @ W2.T
+    cdf = 0.5 * (1 + np.vectorize(erf)(pre / sqrt(2)))
+    dpre = dact * (cdf + pre * np.exp(-0.5 * pre * pre) / sqrt(2 * pi))
+    dx_ref = dpre @ W1.T
+    y = np.concatenate([to_np(t) for t in ys])
+    dx = np.concatenate([to_np(t) for t in dxs])
+    assert nerr(y[rows], y_ref) < TOL["bf16"]
+    assert nerr(dx[rows], dx_ref) < TOL["bf16"]
+    per2 = h // n
+    db2_ref = dtype_round(dy, "bf16").sum(0)
+    for r in range(n):
+        j = m.ffn2.slot(r)["logical_id"]
+        gb = to_np(m.ffn2.grad_shard(r))[f * per2:]
+        # fp32 column sums of 8192 bf16 rows (1024 per step, 8 steps): fp32
+        # accumulation error, ~2.5e-5 measured; bf16 mode's bound is 2e-2
+        assert nerr(gb, db2_ref[j * per2:(j + 1) * per2]) < 1e-4
+    m.close()
+    g.close()
+    torch.cuda.empty_cache()
+
+
 def test_chained_stack_equals_unchained():
     """Block-to-block shift prefetch (RtpMlp.chain) in the
     in-process lockstep and concurrent transports: bit-identical results,
@@ -350,3 +413,29 @@ def test_chained_stack_equals_unchained():
     for r in range(n):
         for b in range(3):
             assert list(outs[1][f"home{b}_{r}"]) == [r, r]
+
+
+def test_nccl_single_rank_group_runs_and_polls():
+    """The NCCL transport on one rank (no peers to shift with): the MLP step
+    runs through it and WorkerGroup.synchronize takes the polled wait (async
+    communicator errors / RTPB_COMM_TIMEOUT_S watchdog) and returns."""
+    import torch
+    from helpers import to_dev, to_np
+    from paper_2311_01635_b200 import rtp
+    g1 = rtp.WorkerGroup.nccl(1, 0, 0, rtp.WorkerGroup.nccl_unique_id())
+    g2 = rtp.WorkerGroup(1)
+    rng = np.random.default_rng(5)
+    x, dy = rng.uniform(-1, 1, (512, 256)), rng.uniform(-1, 1, (512, 256))
+    outs = []
+    for g in (g1, g2):
+        m = rtp.RtpMlp(g, "m", 256, 1024, "bf16", seed=42, stream_base=0)
+        m.begin_step()
+        m.zero_grads()
+        y = m.forward([to_dev(x, "bf16")])[0]
+        dx = m.backward([to_dev(dy, "bf16")])[0]
+        g.synchronize()
+        outs.append((to_np(y), to_np(dx)))
+        m.close()
+        g.close()
+    assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
+    torch.cuda.synchronize()
