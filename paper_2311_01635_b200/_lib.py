@@ -43,6 +43,8 @@ _SIGS = {
     "rtpb_fwd_step": (_int, [_int, _vp, _sz, _vp, _vp, _sz, _sz, _vp, _sz, _sz, _sz, _sz, _int, _vp, _sz, _vp]),
     "rtpb_dgrad_step": (_int, [_int, _vp, _sz, _sz, _vp, _vp, _sz, _vp, _sz, _vp, _sz, _sz, _sz, _sz, _int, _vp,
                                _sz, _vp]),
+    "rtpb_dgrad_step2": (_int, [_int, _vp, _sz, _sz, _vp, _sz, _vp, _vp, _sz, _vp, _sz, _vp, _sz, _sz, _sz, _sz,
+                                 _int, _vp, _sz, _vp]),
     "rtpb_wgrad_step": (_int, [_int, _vp, _sz, _vp, _sz, _sz, _vp, _vp, _sz, _sz, _sz, _vp, _sz, _vp]),
     "rtpb_gelu": (_int, [_int, _vp, _vp, _sz, _vp]),
     "rtpb_gelu_backward": (_int, [_int, _vp, _vp, _vp, _sz, _vp]),

@@ -287,6 +287,31 @@ int rtpb_dgrad_step(int dtype, const void* dy, size_t ldy, size_t col0, const vo
   return timed(1, 2.0 * M * I * per, s, [&] { return gemm_dgrad(f32, p, s); });
 }
 
+int rtpb_dgrad_step2(int dtype, const void* dy, size_t ldy, size_t col0, const void* w_a, size_t col1,
+                     const void* w_b, float* acc, size_t ld_acc, void* dx, size_t ldx, const void* pre,
+                     size_t ldpre, size_t M, size_t I, size_t per, int flags, void* workspace,
+                     size_t workspace_bytes, void* stream) {
+  int rc = check_geom(M, I, per);
+  if (rc) return rc;
+  if (dtype != RTPB_BF16) return set_error(RTPB_ERR_CONFIG, "dgrad_step2: bf16 only");
+  if (!w_a || !w_b) return set_error(RTPB_ERR_DIMENSION, "dgrad_step2: null weight shard");
+  const bool first = flags & RTPB_EPI_FIRST, last = flags & RTPB_EPI_LAST;
+  if (!(first && last) && !acc) return set_error(RTPB_ERR_DIMENSION, "dgrad_step2: null fp32 accumulator");
+  if (last && !dx) return set_error(RTPB_ERR_DIMENSION, "dgrad_step2: null dx");
+  if ((flags & RTPB_EPI_GELU_BWD) && !pre) return set_error(RTPB_ERR_DIMENSION, "dgrad_step2: null pre");
+  cudaStream_t s = as_stream(stream);
+  StepDgrad p{};
+  p.dy = static_cast<const char*>(dy) + col0 * 2; p.ldy = ldy;
+  p.w = w_a;
+  p.dy2 = static_cast<const char*>(dy) + col1 * 2;
+  p.w2 = w_b;
+  p.acc = acc; p.ld_acc = ld_acc; p.dx = dx; p.ldx = ldx; p.pre = pre; p.ldpre = ldpre;
+  p.M = M; p.I = I; p.per = per; p.flags = flags; p.force_bn = g_force_bn;
+  (void)workspace;
+  (void)workspace_bytes;
+  return timed(1, 4.0 * M * I * per, s, [&] { return gemm_dgrad(false, p, s); });
+}
+
 int rtpb_wgrad_step(int dtype, const void* x, size_t ldx, const void* dy, size_t ldy, size_t col0,
                     const float* g_in, float* g_out, size_t M, size_t I, size_t per, void* workspace,
                     size_t workspace_bytes, void* stream) {

@@ -87,6 +87,11 @@ bool n1_scheduling_pays(size_t rows, size_t a, size_t b) {
 // dW a short split-K chain, so the two fit side by side. So the split is
 // kept for a dX of under two waves of pair tiles: N = 2 / 4 / 8 then measure
 // 546 / 365 / 203 (vs 546 / 330 / 187 without any split).
+bool dx_pair_enabled() {
+  const char* e = std::getenv("RTPB_DX_PAIR");
+  return !e || std::atoi(e) != 0;
+}
+
 int nway_dx_sms(size_t rows, size_t I, size_t per) {
   if (std::getenv("RTPB_NO_OVERLAP")) return 0;
   if (const char* e = std::getenv("RTPB_NWAY_DX_SMS")) return std::atoi(e);
@@ -579,6 +584,23 @@ void RtpLinear::backward_ex(std::span<const DView> dy, size_t rows, std::span<co
   const int dx_sms = (n > 1 && distributed && dtype_ == DType::BF16) ? nway_dx_sms(rows, in_, per_) : 0;
   if (dx_sms)
     for (size_t r : local) group_->worker(r).fork_aux();
+  // Paired dX (out-of-place, bf16; RTPB_DX_PAIR=0 disables): an even step
+  // defers its dX, the odd step after it runs both as ONE GEMM over the two
+  // resident shards (the previous one is still in the spare), so the fp32
+  // cross-step accumulator is read and written N/2 times instead of N (at N =
+  // 2 never) — SURVEY §7.9's mitigation of the HBM-bound accumulator. The
+  // shift into the spare then waits for that dX (it overlaps dW only).
+  // Measured per GPU (`--solo N`): config (b) N = 2 / 4 / 8 574 → 681, 364 →
+  // 422, 195 → 233 TFLOP/s; config (d) N = 8 1053 → 1210. It regroups fp32
+  // sums, so out-of-place is no longer bit-identical to in-place (the
+  // reference's layers_test property holds with RTPB_DX_PAIR=0).
+  // (with arrival flags the paired dX waits on its own step's flag: the
+  // spare's shard came through the same comm stream earlier)
+  const bool pair = oopm && n > 1 && dtype_ == DType::BF16 && dx_pair_enabled();
+  auto paired = [&](size_t s) { return pair && s % 2 == 1; };
+  auto has_dx = [&](size_t s) { return !pair || s % 2 == 1 || s + 1 == n; };
+  const size_t first_dx = pair ? 1 : 0;
+  std::vector<size_t> prev_j(n, 0);
   for (size_t s = 0; s < n; ++s) {
     group_->each([&](size_t r) {
       const size_t j = slots_[r].logical_id;
@@ -588,11 +610,11 @@ void RtpLinear::backward_ex(std::span<const DView> dy, size_t rows, std::span<co
     });
     const bool rotate = s + 1 < n;
     const bool flags_on = use_flags();
-    if (s > 0 && !flags_on) {
+    if (s > 0 && !flags_on && has_dx(s)) {
       // dX of this step needs the shifted weight.
       for (size_t r : local) group_->worker(r).wait(Ev::WDone, false);
     }
-    if (rotate && oopm && !(s == 0 && pre_bwd_)) {
+    if (rotate && oopm && !(s == 0 && pre_bwd_) && !paired(s)) {
       group_->comm_after_compute();
       for (size_t r : local) {
         wp[r] = slots_[r].weight.data();
@@ -607,11 +629,11 @@ void RtpLinear::backward_ex(std::span<const DView> dy, size_t rows, std::span<co
     if (s + 1 == n && e.before_last_step) e.before_last_step();
     // dX (+)= dY_j . W_j^T
     if (dx_sms) set_sm_budget(dx_sms);
-    group_->each([&](size_t r) {
+    if (has_dx(s)) group_->each([&](size_t r) {
       Worker& w = group_->worker(r);
       const size_t k = k_of[r];
       const size_t j = slots_[r].logical_id;
-      int flags = (s == 0 ? RTPB_EPI_FIRST : 0) | (s + 1 == n ? RTPB_EPI_LAST : 0);
+      int flags = (s == first_dx ? RTPB_EPI_FIRST : 0) | (s + 1 == n ? RTPB_EPI_LAST : 0);
       const void* pre = nullptr;
       size_t ldpre = 0;
       if (!e.pre.empty() && s + 1 == n) {
@@ -621,12 +643,28 @@ void RtpLinear::backward_ex(std::span<const DView> dy, size_t rows, std::span<co
       }
       float* acc = n > 1 ? static_cast<float*>(dx_acc_[r].data()) : nullptr;
       set_launch_wait_flag(flags_on && s > 0 ? w.flag(flag_base_ + kFlagBwdW + s) : nullptr);
-      const int rc = rtpb_dgrad_step(dt, dy[k].data, dy[k].ld ? dy[k].ld : out_, j * per_, slots_[r].weight.data(),
-                                     acc, in_, dx[k].data, dx[k].ld ? dx[k].ld : in_, pre, ldpre, rows, in_, per_,
-                                     flags, workspace_[r].data(), workspace_[r].bytes(), w.compute);
+      const size_t ldy = dy[k].ld ? dy[k].ld : out_, ldx = dx[k].ld ? dx[k].ld : in_;
+      const int rc =
+          paired(s) ? rtpb_dgrad_step2(dt, dy[k].data, ldy, prev_j[r] * per_, spares_[r].data(), j * per_,
+                                       slots_[r].weight.data(), acc, in_, dx[k].data, ldx, pre, ldpre, rows, in_,
+                                       per_, flags, workspace_[r].data(), workspace_[r].bytes(), w.compute)
+                    : rtpb_dgrad_step(dt, dy[k].data, ldy, j * per_, slots_[r].weight.data(), acc, in_, dx[k].data,
+                                      ldx, pre, ldpre, rows, in_, per_, flags, workspace_[r].data(),
+                                      workspace_[r].bytes(), w.compute);
       set_launch_wait_flag(nullptr);
       check_status(rc);
     });
+    for (size_t r : local) prev_j[r] = slots_[r].logical_id;
+    if (rotate && paired(s)) {
+      // the spare's shard was read by this dX: shift the next shard in now
+      group_->comm_after_compute();
+      for (size_t r : local) {
+        wp[r] = slots_[r].weight.data();
+        sp[r] = spares_[r].data();
+      }
+      flagged_exchange(Direction::CounterClockwise, wp, sp, slots_[local[0]].weight.bytes(), kFlagBwdW + s + 1);
+      for (size_t r : local) group_->worker(r).record(Ev::WDone, true);
+    }
     if (rotate && !oopm) {
       // In place: the weight is free once dX has read it; shift it under dW.
       group_->comm_after_compute();

@@ -97,6 +97,15 @@ int device_sms() {
 // GEMMs issued on two streams run side by side instead of queueing.
 thread_local int t_sm_budget = 0;
 thread_local const unsigned* t_wait_flag = nullptr;
+// Second K segment of the next launch (gemm_dgrad over two shards): its A
+// and B operands, encoded into the launch's second GemmMaps.
+struct KSeg {
+  bool on = false;
+  int kb = 0;
+  const void *a, *b;
+  uint64_t a_inner, a_outer, a_ld, b_inner, b_outer, b_ld;
+};
+thread_local KSeg t_kseg;
 int sm_count() {
   const int all = device_sms();
   return (t_sm_budget >= 2 && t_sm_budget < all) ? (t_sm_budget & ~1) : all;
@@ -146,6 +155,14 @@ int launch_cfg(const Op& a, const Op& b, const Out& c0, const Out* c1, const Gem
   GemmMaps maps;
   int rc;
   if ((rc = encode_maps<Cfg>(a, b, c0, c1, maps))) return rc;
+  GemmMaps kseg_maps;
+  if (t_kseg.on) {
+    if (maps2 || args.sched || Cfg::TF32) return set_error(RTPB_ERR_CONFIG, "two K segments: single bf16 problem only");
+    const Op a2{t_kseg.a, nullptr, t_kseg.a_inner, t_kseg.a_outer, t_kseg.a_ld};
+    const Op b2{t_kseg.b, nullptr, t_kseg.b_inner, t_kseg.b_outer, t_kseg.b_ld};
+    if ((rc = encode_maps<Cfg>(a2, b2, c0, c1, kseg_maps))) return rc;
+    maps2 = &kseg_maps;
+  }
   static bool attr_set = false;  // per instantiation
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(rtp_gemm_kernel<Cfg>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -180,6 +197,7 @@ int launch_cfg(const Op& a, const Op& b, const Out& c0, const Out* c1, const Gem
     cfg.gridDim = dim3(unsigned(slots));
   }
   GemmArgs a_ = args;
+  if (t_kseg.on) a_.kseg_kb = t_kseg.kb;
   a_.trace = next_trace(cfg.gridDim.x);
   if (!a_.ready_flag) a_.ready_flag = t_wait_flag;  // set_launch_wait_flag()
   cudaError_t e = cudaLaunchKernelEx(&cfg, rtp_gemm_kernel<Cfg>, maps, maps2 ? *maps2 : maps, a_);
@@ -801,6 +819,17 @@ int gemm_dgrad(bool f32, const StepDgrad& p, cudaStream_t s) {
   g.M = int(p.M);
   g.N = int(p.I);
   g.K = int(p.per);
+  struct SegGuard {
+    ~SegGuard() { t_kseg = KSeg{}; }
+  } seg_guard;
+  if (p.w2) {
+    // + dY_blk2 . W_2^T: the K loop runs over shard 1 (K blocks padded to 64)
+    // then shard 2, one accumulator — two steps' products in one pass.
+    if (f32) return set_error(RTPB_ERR_CONFIG, "dgrad over two shards: bf16 only");
+    const int kb1 = int((p.per + 63) / 64);
+    t_kseg = KSeg{true, kb1, p.dy2, p.w2, p.per, p.M, p.ldy, p.per, p.I, p.per};
+    g.K = kb1 * 64 + int(p.per);
+  }
   g.flags = p.flags;
   g.aux = p.pre;
   g.ld_aux = int64_t(p.ldpre);

@@ -114,6 +114,10 @@ struct GemmArgs {
   // Replaces a stream-event dependency, so the launch keeps its programmatic
   // (PDL) edge to the previous GEMM on its stream.
   const unsigned* ready_flag;
+  // Two K segments (DGRAD over two resident weight shards, single problem):
+  // K blocks kb >= kseg_kb read the A and B maps of the second GemmMaps at
+  // K offset (kb - kseg_kb) * BK. 0: one segment.
+  int kseg_kb;
   unsigned* dep_count;
   unsigned dep_target;
   int dep_rows;
@@ -607,10 +611,12 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
           mbar_wait(&empty_bar[stage], phase ^ 1);
           uint8_t* sA = stage_base + stage * Cfg::STAGE_BYTES;
           if (rank == 0) mbar_expect_tx(&full_bar[stage], uint32_t(expect));
-          const int k0 = kb * BK;
+          const bool seg2 = args.kseg_kb > 0 && kb >= args.kseg_kb;
+          const GemmMaps& mk = seg2 ? maps2 : mp;
+          const int k0 = (seg2 ? kb - args.kseg_kb : kb) * BK;
           for (int op = 0; op < Cfg::NOPS; ++op) {
-            const CUtensorMap* ma = op ? &mp.a_lo : &mp.a;
-            const CUtensorMap* mbm = op ? &mp.b_lo : &mp.b;
+            const CUtensorMap* ma = op ? &mk.a_lo : &mk.a;
+            const CUtensorMap* mbm = op ? &mk.b_lo : &mk.b;
             uint8_t* dA = sA + op * (Cfg::A_BYTES + Cfg::B_BYTES);
             uint8_t* dB = dA + Cfg::A_BYTES;
             if constexpr (Cfg::A_MN) {

@@ -30,6 +30,7 @@ struct StepFwd {
 struct StepDgrad {
   const void* dy; const void* dy_lo; size_t ldy;  // dy points at the column block
   const void* w; const void* w_lo;
+  const void* dy2; const void* w2;  // optional second (column block, shard): bf16, same per
   float* acc; size_t ld_acc;
   void* dx; size_t ldx;
   const void* pre; size_t ldpre;

@@ -84,7 +84,10 @@ def test_linear_matches_reference(golden, n, mode, dtype):
         assert np.array_equal(out["weights"][r], dtype_round(ref, dtype))
 
 
-def test_outofplace_bitwise_equals_inplace(golden):
+def test_outofplace_bitwise_equals_inplace(golden, monkeypatch):
+    # the reference's property (layers_test.cpp:343-365) holds for the same
+    # per-step arithmetic: paired dX (out-of-place only) regroups sums
+    monkeypatch.setenv("RTPB_DX_PAIR", "0")
     g = golden("linear")
     a = run_linear(4, g["w"], g["b"], g["x"], g["dy"], "bf16", "inplace")
     b = run_linear(4, g["w"], g["b"], g["x"], g["dy"], "bf16", "outofplace")
@@ -439,3 +442,35 @@ def test_nccl_single_rank_group_runs_and_polls():
         g.close()
     assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
     torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("n", [2, 3, 4, 8])
+def test_paired_dx_matches_reference(golden, oracle, monkeypatch, n):
+    """Paired dX (default in out-of-place mode): two steps' dX in one GEMM
+    over the two resident shards. Forward and ffn2's dW are untouched
+    (bit-identical to the unpaired run); dX and ffn1's gradients (fed by
+    dpre) regroup fp32 sums only: within the bf16 tolerance of the reference
+    and close to unpaired. n = 3 leaves the last step unpaired."""
+    if n in (2, 4):
+        g = golden("mlp")
+        args = (g["w1"], g["b1"], g["w2"], g["b2"], g["x"], g["dy"], "bf16", "outofplace")
+    else:
+        rng = np.random.default_rng(7)
+        h, f, rows = 24 * n, 96 * n, 32 * n
+        w = [rng.uniform(-0.1, 0.1, s) for s in ((h, f), (f,), (f, h), (h,))]
+        x, dy = rng.uniform(-1, 1, (rows, h)), rng.uniform(-1, 1, (rows, h))
+        g = {f"n{n}_{k}": v for k, v in oracle.rtp_mlp(n, *w, x, dy).items()}
+        args = (*w, x, dy, "bf16", "outofplace")
+    monkeypatch.setenv("RTPB_DX_PAIR", "0")
+    base = run_mlp(n, *args)
+    monkeypatch.setenv("RTPB_DX_PAIR", "1")
+    out = run_mlp(n, *args)
+    assert np.array_equal(out["y"], base["y"])
+    for r in range(n):
+        assert np.array_equal(out["grads2"][r], base["grads2"][r])
+        assert nerr(out["grads1"][r], base["grads1"][r]) < 1e-2
+    assert nerr(out["dx"], base["dx"]) < 1e-2
+    if f"n{n}_dx" in g:
+        assert nerr(out["dx"], g[f"n{n}_dx"]) < TOL["bf16"]
+        for r in range(n):
+            assert nerr(out["grads1"][r], g[f"n{n}_grads1"][r]) < TOL["bf16"]
