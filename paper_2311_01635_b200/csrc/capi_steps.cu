@@ -51,8 +51,8 @@ cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
 // Zero-initialised, self-resetting part of a step workspace.
 // (16 per tile: one per epilogue warp slot of a CTA pair, for the split-K
 // partials' per-region counters; the ordered split-K uses the first.)
-size_t split_flag_bytes(size_t I, size_t per) {
-  return ((I + 255) / 256) * ((per + 255) / 256) * 16 * sizeof(unsigned);
+size_t split_flag_bytes(size_t I, size_t per) {  // per-tile counters, tiles 256 x (256 or 128)
+  return ((I + 255) / 256) * ((per + 127) / 128) * 16 * sizeof(unsigned);
 }
 // Fused dW bias sums (CTA-pair dW): arrival counter per 64-column group, and
 // one partial row per (256-row tile block, K split <= 8).

@@ -285,22 +285,29 @@ int pick_code(bool tf32, GemmArgs& args, int force) {
     const int kb = (args.K + 63) / 64;
     if (!force && tiles < pairs) {
       // The ordered split-K pays one fp32 epilogue per split in sequence
-      // (~3 us each with double-buffered staging) to divide the ~0.35 us /
-      // K-block mainloop: take the split count minimising the sum.
-      const int s_max = std::min(pairs / tiles, std::min(8, kb / 8));
+      // (~3 us each for a 256 x 256 pair tile with double-buffered staging,
+      // ~1.7 us at 256 x 128) to divide the mainloop (~0.35 us per 64-deep K
+      // block at 256 x 256; ~0.27 us at 256 x 128, whose SMs ingest 24 instead
+      // of 32 KB per block): take the (width, split) minimising the sum. The
+      // narrow tile wins for thin gradient shards (per <= 128: a 256-wide tile
+      // would be mostly padding), e.g. config (b) at N = 8.
       int s = 1;
-      double best_t = kb * 0.35 / 64.0 * 64.0;
-      for (int c = 2; c <= s_max; ++c) {
-        const double t = kb * 0.35 / c + 3.0 * c;
-        if (t < best_t) {
-          best_t = t;
-          s = c;
+      double best_t = kb * 0.35;
+      for (int bn : {256, 128}) {
+        const int t_n = ((args.M + 255) / 256) * ((args.N + bn - 1) / bn);
+        if (t_n >= pairs) continue;
+        const double ck = bn == 256 ? 0.35 : 0.27, ce = bn == 256 ? 3.0 : 1.7;
+        const int s_max = std::min(pairs / t_n, std::min(8, kb / 8));
+        for (int c = 2; c <= s_max; ++c) {
+          const double t = kb * ck / c + ce * c;
+          if (t < best_t) {
+            best_t = t;
+            s = c;
+            code = 1000 + bn;
+          }
         }
       }
-      if (s >= 2) {
-        code = 1256;
-        args.k_splits = s;
-      }
+      if (s >= 2) args.k_splits = s;
     }
   }
   return code;

@@ -39,6 +39,8 @@ CASES = [
     (200, 64, 192, 3, "bf16", 0),     # ragged M, per = 64
     (1000, 768, 3072, 4, "bf16", 0),  # GPT-2 width, tail rows
     (8192, 768, 3072, 4, "bf16", 0),  # config (b) dW: 8-way ordered split-K + fused bias sums
+    (8192, 3072, 768, 8, "bf16", 0),  # ffn2 at N = 8 (per 96): split-K on 256 x 128 pair tiles
+    (8192, 768, 3072, 8, "bf16", 0),  # ffn1 at N = 8 (per 384)
     (4000, 768, 3000, 3, "bf16", 1128),  # pair 256 x 128, ragged K and N
     (8, 8, 16, 2, "bf16", 0),         # minimal aligned shape
     (512, 256, 512, 4, "f32", 0),
