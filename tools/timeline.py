@@ -21,7 +21,10 @@ NAMES = (["fwd1", "fwd2"] if os.environ.get("RTPB_NO_FUSED_FWD") else ["fwd1+fwd
     (["dgrad2", "wgrad2", "dgrad1", "wgrad1"] if os.environ.get("RTPB_NO_FUSED_BWD") else ["dgrad2+dgrad1", "wgrad2+wgrad1"])
 
 dev = torch.device("cuda", 0)
-grp = rtp.WorkerGroup(1)
+SOLO = int(os.environ.get("SOLO", "0"))  # rank 0 of an N-way ring, shifts skipped (per-GPU schedule)
+grp = rtp.WorkerGroup.solo(SOLO, 0, 0) if SOLO else rtp.WorkerGroup(1)
+if SOLO:
+    NAMES = [f"L{i}" for i in range(64)]
 mlp = rtp.RtpMlp(grp, "tl", H, F, "bf16", seed=42, stream_base=0)
 mlp.set_rotation_mode("outofplace")
 mlp.begin_step()
@@ -41,7 +44,7 @@ def step():
 for _ in range(5):
     step()
 torch.cuda.synchronize()
-buf = torch.zeros(6 * 148 * STRIDE + 1024, dtype=torch.int64, device=dev)
+buf = torch.zeros((64 if SOLO else 6) * 148 * STRIDE + 1024, dtype=torch.int64, device=dev)
 for rep in range(3):
     buf.zero_()
     flush.zero_()
