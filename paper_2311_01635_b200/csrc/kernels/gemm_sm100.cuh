@@ -773,25 +773,29 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
         }
         __syncwarp();
       }
-      // DGRAD last step: the fp32 accumulator's rows are loaded one chunk
-      // ahead into registers (the first before the accumulator wait), so
-      // each chunk's loads are in flight while the previous chunk is stored.
-      const bool acc_rd = Cfg::EPI == EPI_DGRAD && last && !first && row_ok;
-      float4 acc_nx[8];
+      // DGRAD last step: the warp's 32 x 32 fp32 accumulator chunk is loaded
+      // coalesced (each instruction: 4 rows x 128 B, 4 L1 wavefronts instead
+      // of 32 for one row per lane — the row-per-lane loads were bound by L1
+      // wavefronts), two chunks ahead into two register buffers used
+      // alternately, and transposed to row-per-lane through the staging
+      // buffer (128 B swizzle, conflict-free).
+      const bool acc_rd = Cfg::EPI == EPI_DGRAD && last && !first && row0 < uM;
+      float4 acc_a[8], acc_b[8];
       auto load_acc = [&](int c, float4* d) {
+        const int cc = c + (lane & 7) * 4;
 #pragma unroll
-        for (int g = 0; g < 4; ++g) {
-          if (c + g * 8 < uN) {
-            const float4* p = reinterpret_cast<const float4*>(args.acc + row * args.ld_acc + c + g * 8);
-            d[2 * g] = p[0];
-            d[2 * g + 1] = p[1];
-          } else {
-            d[2 * g] = d[2 * g + 1] = make_float4(0.f, 0.f, 0.f, 0.f);
-          }
+        for (int i = 0; i < 8; ++i) {
+          const int r = row0 + i * 4 + (lane >> 3);
+          d[i] = (r < uM && cc < uN)
+                     ? *reinterpret_cast<const float4*>(args.acc + size_t(r) * args.ld_acc + cc)
+                     : make_float4(0.f, 0.f, 0.f, 0.f);
         }
       };
-      if constexpr (Cfg::EPI == EPI_DGRAD)
-        if (acc_rd && n0 + half * 32 < uN) load_acc(n0 + half * 32, acc_nx);
+      if constexpr (Cfg::EPI == EPI_DGRAD) {
+        if (acc_rd && n0 + half * 32 < uN) load_acc(n0 + half * 32, acc_a);
+        if (acc_rd && half + NSPLIT < BN / 32 && n0 + (half + NSPLIT) * 32 < uN)
+          load_acc(n0 + (half + NSPLIT) * 32, acc_b);
+      }
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
       if (tr) detail::trace_at(trace, 6 + 6 * li);
@@ -827,15 +831,6 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
       for (int ch = half; ch < BN / 32; ch += NSPLIT) {
         const int nc = n0 + ch * 32;
         if (nc >= uN) break;  // warp-uniform
-        float4 acc_cur[8];
-        if constexpr (Cfg::EPI == EPI_DGRAD) {
-          if (acc_rd) {
-#pragma unroll
-            for (int g = 0; g < 8; ++g) acc_cur[g] = acc_nx[g];
-            const int nn = nc + NSPLIT * 32;
-            if (ch + NSPLIT < BN / 32 && nn < uN) load_acc(nn, acc_nx);
-          }
-        }
         uint32_t v[32];
         tmem_ld_32x32b_x32(t_row + ch * 32, v);
         tmem_ld_wait();
@@ -890,11 +885,30 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
           }
         } else if constexpr (Cfg::EPI == EPI_DGRAD) {
           if (acc_rd) {
+            // consume this chunk's buffer (transpose through stg0, free: the
+            // previous chunk's store has read it), refill it two chunks ahead
+            const int nn = nc + 2 * NSPLIT * 32;
+            const bool more = ch + 2 * NSPLIT < BN / 32 && nn < uN;
+            auto put = [&](const float4* d) {
 #pragma unroll
-            for (int g = 0; g < 8; ++g) {
-              const float4 a = acc_cur[g];
-              x[g * 4 + 0] += a.x; x[g * 4 + 1] += a.y; x[g * 4 + 2] += a.z; x[g * 4 + 3] += a.w;
+              for (int i = 0; i < 8; ++i) {
+                const int r = i * 4 + (lane >> 3), k = lane & 7;
+                *reinterpret_cast<float4*>(stg0 + r * 128 + ((k ^ (r & 7)) * 16)) = d[i];
+              }
+            };
+            if ((((ch - half) / NSPLIT) & 1) == 0) {
+              put(acc_a);
+              if (more) load_acc(nn, acc_a);
+            } else {
+              put(acc_b);
+              if (more) load_acc(nn, acc_b);
             }
+            __syncwarp();
+            float av[32];
+            detail::unstage_row<true>(stg0, lane, av);
+#pragma unroll
+            for (int e = 0; e < 32; ++e) x[e] += av[e];
+            __syncwarp();  // every lane has read stg0 before the output is staged over it
           }
           if (pre_tma) {
             // pre chunk staged by TMA in the same swizzled 32 x 32 layout as the outputs
