@@ -91,8 +91,9 @@ int rtpb_dgrad_step(int dtype, const void* dy, size_t ldy, size_t col0, const vo
                     size_t ld_acc, void* dx, size_t ldx, const void* pre, size_t ldpre, size_t M, size_t I,
                     size_t per, int flags, void* workspace, size_t workspace_bytes, void* stream);
 
-/* Two dX steps in one pass (bf16; two weight shards resident, out-of-place
- * mode): acc (+)= dY[:, col0:+per] . W_a^T + dY[:, col1:+per] . W_b^T, one
+/* Two dX steps in one pass (layers_linear.cpp:65 for two consecutive steps;
+ * bf16; two weight shards resident, out-of-place mode):
+ * acc (+)= dY[:, col0:+per] . W_a^T + dY[:, col1:+per] . W_b^T, one
  * fp32 accumulation over K = 2 per; flags as rtpb_dgrad_step. Halves the
  * cross-step accumulator passes (RTPB_DX_PAIR in the layers). */
 int rtpb_dgrad_step2(int dtype, const void* dy, size_t ldy, size_t col0, const void* w_a, size_t col1,
