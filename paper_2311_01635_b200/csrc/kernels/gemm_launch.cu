@@ -240,6 +240,7 @@ int choose_tile(int M, int N, bool tf32) {
 }
 
 constexpr int kEpiWarps = 8;
+constexpr int kParMinSplits = 5;  // dW split-K: unordered partials from this many splits
 
 template <int EPI, bool TF32>
 int dispatch_tile(int code, const Op& a, const Op& b, const Out& c0, const Out* c1, const GemmArgs& args,
@@ -883,14 +884,24 @@ int gemm_wgrad(bool f32, const StepWgrad& p, cudaStream_t s) {
   g.gbias_out = p.gbias_out;
   g.bias_part = p.bias_part;
   g.bias_tick = p.bias_tick;
+  int par = 0;
   if (p.wpart && !f32) {
+    // unordered partials + slice folds for long split chains (see
+    // wgrad_partial_floats); RTPB_WGRAD_PAR forces a mode (0 = the chain)
+    GemmArgs t = g;
+    pick_code<EPI_WGRAD>(false, t, p.force_bn);
+    const char* e = std::getenv("RTPB_WGRAD_PAR");
+    par = e ? std::atoi(e) : (t.k_splits >= kParMinSplits ? 2 : 0);
+    if (t.k_splits < 2) par = 0;
+  }
+  if (par) {
     // split-K partials: one (I rounded up to 256) x per fp32 block per split
     const size_t ipad = (p.I + 255) / 256 * 256;
     const int smax = wgrad_splits(f32, p.M, p.I, p.per, p.force_bn);
     Out part{p.wpart, true, p.per, size_t(smax) * ipad, p.per};
     // every unit of a split dW launch is resident (splits <= pairs / tiles):
-    // parallel slice folds; RTPB_WGRAD_LASTFOLD selects the last-arriver fold
-    g.wpar = std::atoi(std::getenv("RTPB_WGRAD_PAR")) == 1 ? 1 : 2;
+    // 2 = parallel slice folds, 1 = the last arriver folds
+    g.wpar = par == 1 ? 1 : 2;
     g.wpart = p.wpart;
     g.wpart_rows = int(ipad);
     g.gout = p.g_out;
@@ -914,13 +925,19 @@ int wgrad_splits(bool f32, size_t M, size_t I, size_t per, int force_bn) {
 }
 
 size_t wgrad_partial_floats(bool f32, size_t M, size_t I, size_t per) {
-  // Split-K partials for the unordered dW modes, opt-in with RTPB_WGRAD_PAR
-  // (1: the last split folds them, 2: every split folds a row slice). Both
-  // measured slower than the ordered chain of epilogues (config (b) N=1 dW
-  // 2-way: epilogue 14 / 28 us vs 8 us), so the chain stays the default.
-  static const char* mode = std::getenv("RTPB_WGRAD_PAR");
-  if (!mode || f32) return 0;
+  // Split-K partials for the unordered dW mode (every split stores its fp32
+  // partial, then folds a row slice of all of them into G in split order:
+  // deterministic). The ordered chain pays one epilogue + hand-off per split
+  // in sequence, the partials a store and a fold: the chain wins for short
+  // chains (config (b) N = 4, 3-4 splits: 440 vs 379 TFLOP/s per GPU), the
+  // partials for long ones (N = 8, 5-8 splits: 250 vs 243), so they are used
+  // from kParMinSplits splits. RTPB_WGRAD_PAR forces a mode (0 = the chain,
+  // 1 = the last arriver folds, 2 = slice folds).
+  if (f32) return 0;
+  const char* mode = std::getenv("RTPB_WGRAD_PAR");
+  if (mode && std::atoi(mode) == 0) return 0;
   const int S = wgrad_splits(f32, M, I, per, 0);
+  if (!mode && S < kParMinSplits) return 0;
   return S > 1 ? size_t(S) * ((I + 255) / 256 * 256) * per : 0;
 }
 

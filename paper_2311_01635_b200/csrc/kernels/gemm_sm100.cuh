@@ -998,41 +998,31 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
           const float* part = x_.prob ? args.wpart2 : args.wpart;
           const int r_lo = (32 * split) / wsplits, r_hi = (32 * (split + 1)) / wsplits;
           float* gout = const_cast<float*>(static_cast<const float*>(x_.prob ? args.gout2 : args.gout));
-          if (lane >= r_lo && lane < r_hi && row_ok) {
-            // all loads of a chunk are issued before its stores (the partials
-            // and G never alias, but the compiler cannot know): one round trip
-            // per split instead of one per 8 columns
+          // Each lane takes one column of every 32-column chunk of the slice's
+          // rows, so every load and store is a coalesced 128-byte row segment
+          // (a row per lane costs 32 L1 wavefronts per instruction). All S
+          // partials of an element are loaded before the sum, added in split
+          // order, then G: the same order, and bits, as the chained folds.
+          for (int r = r_lo; r < r_hi; ++r) {
+            const int grow = row0 + r;
+            if (grow >= uM) break;
 #pragma unroll 1
             for (int ch = half; ch < BN / 32; ch += NSPLIT) {
-              const int nc = n0 + ch * 32;
-              if (nc >= uN) break;
-              const int nv = min(8, (uN - nc) / 4);  // float4s of this row inside N
-              float4 acc[8];
+              const int col = n0 + ch * 32 + lane;
+              if (n0 + ch * 32 >= uN) break;  // warp-uniform
+              if (col < uN) {
+                float tv[8];
 #pragma unroll
-              for (int v = 0; v < 8; ++v) acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
-              for (int sp = 0; sp < wsplits; ++sp) {
-                const float4* __restrict__ src =
-                    reinterpret_cast<const float4*>(part + (size_t(sp) * wprows + row) * uN + nc);
-                float4 tv[8];
+                for (int sp = 0; sp < 8; ++sp)
+                  tv[sp] = sp < wsplits ? __ldcg(part + (size_t(sp) * wprows + grow) * uN + col) : 0.f;
+                float a = 0.f;
 #pragma unroll
-                for (int v = 0; v < 8; ++v) tv[v] = v < nv ? __ldcg(src + v) : make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-                for (int v = 0; v < 8; ++v) {
-                  acc[v].x += tv[v].x; acc[v].y += tv[v].y; acc[v].z += tv[v].z; acc[v].w += tv[v].w;
-                }
+                for (int sp = 0; sp < 8; ++sp)
+                  if (sp < wsplits) a += tv[sp];
+                float* dst = gout + size_t(grow) * uN + col;
+                if (!first) a = __ldcg(dst) + a;
+                *dst = a;
               }
-              float4* __restrict__ dst = reinterpret_cast<float4*>(gout + size_t(row) * uN + nc);
-              if (!first) {
-                float4 gv[8];
-#pragma unroll
-                for (int v = 0; v < 8; ++v) gv[v] = v < nv ? __ldcg(dst + v) : make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-                for (int v = 0; v < 8; ++v)
-                  acc[v] = make_float4(gv[v].x + acc[v].x, gv[v].y + acc[v].y, gv[v].z + acc[v].z, gv[v].w + acc[v].w);
-              }
-#pragma unroll
-              for (int v = 0; v < 8; ++v)
-                if (v < nv) dst[v] = acc[v];
             }
           }
           __syncwarp();
