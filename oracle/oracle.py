@@ -61,6 +61,7 @@ class Oracle:
         L.orc_rtp_linear.argtypes = [_sz, _sz, _sz, _sz, _dp, _dp, _dp, _dp, _dp, _dp, _dp, C.c_void_p]
         L.orc_rtp_linear.restype = C.c_int
         L.orc_rtp_mlp.argtypes = [_sz, _sz, _sz, _sz, _dp, _dp, _dp, _dp, _dp, _dp, _dp, _dp, _dp, _dp]
+        L.orc_rtp_attention.argtypes = [_sz, _sz, _sz, _sz, _sz, _dp, _dp, _dp, _dp, _dp, _dp, _dp, _dp, _dp]
         L.orc_rtp_mlp.restype = C.c_int
         L.orc_sampled_dots.argtypes = [_dp, _sz, _sz, _dp, _sz, _sz, _sz, _ip, _ip, _sz, _dp]
         L.orc_rtp_memory.argtypes = [_u64, _u64, _u64, C.c_int]
@@ -125,6 +126,16 @@ class Oracle:
             raise ValueError(f"orc_rtp_mlp: ConfigError (code {rc})")
         return {"y": y, "dx": dx, "grads1": g1, "grads2": g2}
 
+    def rtp_attention(self, n, heads, seq, wq, wk, wv, wo, x, dy):
+        wq, wk, wv, wo, x, dy = map(_f64, (wq, wk, wv, wo, x, dy))
+        rows, H = x.shape
+        y, dx = np.empty((rows, H)), np.empty((rows, H))
+        g = np.empty((n, 4 * H * (H // n)))
+        rc = self.L.orc_rtp_attention(n, rows, H, heads, seq, wq, wk, wv, wo, x, dy, y, dx, g)
+        if rc:
+            raise ValueError(f"orc_rtp_attention: ConfigError (code {rc})")
+        return {"y": y, "dx": dx, "grads": g}
+
     def sampled_dots(self, a, lda, sa, b, ldb, sb, k, ri, ci):
         ri = np.ascontiguousarray(ri, np.int64)
         ci = np.ascontiguousarray(ci, np.int64)
@@ -150,6 +161,8 @@ class Reference:
         L.ref_serial_linear.argtypes = [_sz, _sz, _sz, _dp, _dp, _dp, _dp, _dp, _dp, _dp, _dp]
         L.ref_rtp_linear.argtypes = [_sz, C.c_int, C.c_int, _sz, _sz, _sz, _dp, _dp, _dp, _dp, _dp,
                                      _dp, _dp, _ip, _ip, _ip, C.POINTER(_sz)]
+        L.ref_rtp_attention.argtypes = [_sz, C.c_int, _sz, _sz, _sz, _sz, _dp, _dp, _dp, _dp, _dp, _dp, _dp,
+                                        _dp, _dp]
         L.ref_rtp_mlp.argtypes = [_sz, C.c_int, C.c_int, _sz, _sz, _sz, _dp, _dp, _dp, _dp, _dp,
                                   _dp, _dp, _dp, _dp, _dp]
         L.ref_time_mlp.argtypes = [_sz, C.c_int, _sz, _sz, _sz, _u64, C.c_int, C.POINTER(C.c_double)]
@@ -216,6 +229,15 @@ class Reference:
         self._chk(self.L.ref_rtp_mlp(n, int(concurrent), int(outofplace), rows, h, f, w1, b1, w2, b2,
                                      x, dy, y, dx, g1, g2))
         return {"y": y, "dx": dx, "grads1": g1, "grads2": g2}
+
+    def rtp_attention(self, n, heads, seq, wq, wk, wv, wo, x, dy, concurrent=False):
+        wq, wk, wv, wo, x, dy = map(_f64, (wq, wk, wv, wo, x, dy))
+        rows, H = x.shape
+        y, dx = np.empty((rows, H)), np.empty((rows, H))
+        g = np.empty((n, 4 * H * (H // n)))
+        self._chk(self.L.ref_rtp_attention(n, int(concurrent), rows, H, heads, seq, wq, wk, wv, wo, x, dy,
+                                           y, dx, g))
+        return {"y": y, "dx": dx, "grads": g}
 
     def time_mlp(self, n, rows, h, f, seed=42, iters=1, concurrent=True) -> float:
         s = C.c_double(0)

@@ -153,6 +153,25 @@ int ref_rtp_linear(size_t n, int transport, int outofplace, size_t rows, size_t 
   })
 }
 
+// RtpAttention fwd (Train) + bwd (layers_attention.cpp:43-198) on a
+// WorkerGroup of n, batch-major row shards; grads: n * shard_len.
+int ref_rtp_attention(size_t n, int transport, size_t rows, size_t hidden, size_t heads, size_t seq,
+                      const double* wq, const double* wk, const double* wv, const double* wo,
+                      const double* x, const double* dy, double* y, double* dx, double* grads) {
+  REF_GUARD({
+    WorkerGroup g(n, kind_of(transport));
+    RtpAttention attn(g, "attn", from_ptr({hidden, hidden}, wq), from_ptr({hidden, hidden}, wk),
+                      from_ptr({hidden, hidden}, wv), from_ptr({hidden, hidden}, wo), heads, seq, n);
+    attn.zero_grads();
+    auto ys = attn.forward(shard(from_ptr({rows, hidden}, x), n), Mode::Train);
+    auto dxs = attn.backward(shard(from_ptr({rows, hidden}, dy), n));
+    to_ptr(concat(ys, 0), y);
+    to_ptr(concat(dxs, 0), dx);
+    const size_t L = attn.shard_len();
+    for (size_t r = 0; r < n; ++r) to_ptr(attn.slots()[r].grad_acc, grads + r * L);
+  })
+}
+
 // The FFN block exactly as RtpModel composes it (model.cpp:77-83 forward,
 // 99-105 backward): pre = ffn1(x); h = gelu(pre); y = ffn2(h);
 // dh = ffn2.backward(dy); dpre = gelu_backward(pre, dh); dx = ffn1.backward(dpre).

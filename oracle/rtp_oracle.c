@@ -231,6 +231,172 @@ int orc_rtp_mlp(size_t n, size_t rows, size_t h, size_t f, const double* w1, con
   return rc;
 }
 
+/* kernels_scalar.cpp:19-29 (matmul_acc): c[i,j] += a[i,t]*b[t,j], t ascending. */
+static void orc_matmul_acc(const double* a, size_t lda, const double* b, size_t ldb, double* c,
+                           size_t ldc, size_t m, size_t k, size_t n) {
+  for (size_t i = 0; i < m; ++i) {
+    double* crow = c + i * ldc;
+    for (size_t t = 0; t < k; ++t) {
+      const double av = a[i * lda + t];
+      const double* brow = b + t * ldb;
+      for (size_t j = 0; j < n; ++j) crow[j] += av * brow[j];
+    }
+  }
+}
+
+/* tensor.cpp:305-320: max-subtracted exp, row sum, divide. */
+static void orc_softmax_rows(const double* in, double* out, size_t m, size_t n) {
+  for (size_t i = 0; i < m; ++i) {
+    const double* row = in + i * n;
+    double* orow = out + i * n;
+    double mx = row[0];
+    for (size_t j = 1; j < n; ++j) mx = row[j] > mx ? row[j] : mx;
+    double sum = 0.0;
+    for (size_t j = 0; j < n; ++j) {
+      orow[j] = exp(row[j] - mx);
+      sum += orow[j];
+    }
+    for (size_t j = 0; j < n; ++j) orow[j] /= sum;
+  }
+}
+
+/* One (sequence b, head h) tile: rows b*seq .. +seq, columns h*hd .. +hd of
+ * a rows x width matrix (layers_attention.cpp:12-24). */
+static void read_head(const double* src, size_t width, size_t b, size_t h, size_t seq, size_t hd,
+                      double* dst) {
+  for (size_t t = 0; t < seq; ++t) memcpy(dst + t * hd, src + (b * seq + t) * width + h * hd, hd * sizeof(double));
+}
+static void write_head(double* dst, size_t width, size_t b, size_t h, size_t seq, size_t hd,
+                       const double* src) {
+  for (size_t t = 0; t < seq; ++t) memcpy(dst + (b * seq + t) * width + h * hd, src + t * hd, hd * sizeof(double));
+}
+
+int orc_rtp_attention(size_t n, size_t rows, size_t H, size_t heads, size_t seq, const double* wq,
+                      const double* wk, const double* wv, const double* wo, const double* x,
+                      const double* dy, double* y, double* dx, double* grads) {
+  /* layout_attention (partition.cpp:71-84), attention_shard_groups
+   * (layers_common.cpp:54-74): shard j = [Wq[:, blk j] | Wk[:, blk j] |
+   * Wv[:, blk j] | Wo[blk j, :]], each H x gw / gw x H row-major. */
+  if (n == 0 || heads == 0 || H % heads != 0 || heads % n != 0 || rows % n != 0) return 2;
+  const size_t hd = H / heads, g = heads / n, gw = g * hd, M = rows / n;
+  if (M % seq != 0) return 3;
+  const size_t batch = M / seq, L = 4 * H * gw;
+  const double inv_sqrt_hd = 1.0 / sqrt((double)hd);
+  double* store = (double*)calloc(2 * n * L, sizeof(double));
+  slot_t* slots = (slot_t*)malloc(n * sizeof(slot_t));
+  for (size_t r = 0; r < n; ++r) {
+    slots[r].weight = store + r * L;
+    slots[r].grad = store + (n + r) * L;
+    slots[r].logical_id = r;
+    double* w = slots[r].weight;
+    for (size_t i = 0; i < H; ++i)
+      for (size_t c = 0; c < gw; ++c) {
+        w[i * gw + c] = wq[i * H + r * gw + c];
+        w[H * gw + i * gw + c] = wk[i * H + r * gw + c];
+        w[2 * H * gw + i * gw + c] = wv[i * H + r * gw + c];
+      }
+    for (size_t i = 0; i < gw; ++i)
+      for (size_t c = 0; c < H; ++c) w[3 * H * gw + i * H + c] = wo[(r * gw + i) * H + c];
+  }
+  /* the tape (layers.hpp:26-55): per (rank, shard) the forward's q, k, v, probs, attn_out */
+  const size_t qs = M * gw, ps = batch * g * seq * seq;
+  double* tape = (double*)calloc(n * n * (4 * qs + ps), sizeof(double));
+#define TAPE(r, j) (tape + ((r) * n + (j)) * (4 * qs + ps))
+  double *qbh = (double*)malloc(seq * hd * sizeof(double)), *kbh = (double*)malloc(seq * hd * sizeof(double)),
+         *vbh = (double*)malloc(seq * hd * sizeof(double)), *dobh = (double*)malloc(seq * hd * sizeof(double)),
+         *obh = (double*)malloc(seq * hd * sizeof(double)), *sc = (double*)malloc(seq * seq * sizeof(double)),
+         *dprobs = (double*)malloc(seq * seq * sizeof(double)), *ds = (double*)malloc(seq * seq * sizeof(double)),
+         *t1 = (double*)malloc(seq * hd * sizeof(double)), *t2 = (double*)malloc(seq * hd * sizeof(double)),
+         *t3 = (double*)malloc(seq * hd * sizeof(double));
+  double* da = (double*)malloc(qs * sizeof(double));
+  double *dq = (double*)malloc(qs * sizeof(double)), *dk = (double*)malloc(qs * sizeof(double)),
+         *dv = (double*)malloc(qs * sizeof(double));
+  memset(y, 0, rows * H * sizeof(double));
+  /* forward (layers_attention.cpp:55-112) */
+  for (size_t s = 0; s < n; ++s) {
+    for (size_t r = 0; r < n; ++r) {
+      const size_t j = slots[r].logical_id;
+      const double* w = slots[r].weight;
+      const double* xr = x + r * M * H;
+      double* T = TAPE(r, j);
+      double *q = T, *k = T + qs, *v = T + 2 * qs, *probs = T + 3 * qs, *ao = T + 3 * qs + ps;
+      orc_matmul(xr, H, w, gw, q, gw, M, H, gw);
+      orc_matmul(xr, H, w + H * gw, gw, k, gw, M, H, gw);
+      orc_matmul(xr, H, w + 2 * H * gw, gw, v, gw, M, H, gw);
+      for (size_t b = 0; b < batch; ++b)
+        for (size_t h = 0; h < g; ++h) {
+          read_head(q, gw, b, h, seq, hd, qbh);
+          read_head(k, gw, b, h, seq, hd, kbh);
+          read_head(v, gw, b, h, seq, hd, vbh);
+          memset(sc, 0, seq * seq * sizeof(double));
+          orc_matmul_nt_acc(qbh, hd, kbh, hd, sc, seq, seq, hd, seq);
+          for (size_t e = 0; e < seq * seq; ++e) sc[e] = sc[e] * inv_sqrt_hd;
+          double* pbh = probs + (b * g + h) * seq * seq;
+          orc_softmax_rows(sc, pbh, seq, seq);
+          orc_matmul(pbh, seq, vbh, hd, obh, hd, seq, seq, hd);
+          write_head(ao, gw, b, h, seq, hd, obh);
+        }
+      orc_matmul_acc(ao, gw, w + 3 * H * gw, H, y + r * M * H, H, M, gw, H);
+    }
+    if (s + 1 < n) rotate_cw_weight(slots, n);
+  }
+  /* backward (layers_attention.cpp:114-198) */
+  memset(dx, 0, rows * H * sizeof(double));
+  for (size_t s = 0; s < n; ++s) {
+    for (size_t r = 0; r < n; ++r) {
+      const size_t j = slots[r].logical_id;
+      const double* w = slots[r].weight;
+      double* gr = slots[r].grad;
+      const double* T = TAPE(r, j);
+      const double *q = T, *k = T + qs, *v = T + 2 * qs, *probs = T + 3 * qs, *ao = T + 3 * qs + ps;
+      const double* dyr = dy + r * M * H;
+      const double* xr = x + r * M * H;
+      orc_matmul_tn_acc(ao, gw, dyr, H, gr + 3 * H * gw, H, gw, M, H);
+      memset(da, 0, qs * sizeof(double));
+      orc_matmul_nt_acc(dyr, H, w + 3 * H * gw, H, da, gw, M, H, gw);
+      for (size_t b = 0; b < batch; ++b)
+        for (size_t h = 0; h < g; ++h) {
+          read_head(da, gw, b, h, seq, hd, dobh);
+          read_head(q, gw, b, h, seq, hd, qbh);
+          read_head(k, gw, b, h, seq, hd, kbh);
+          read_head(v, gw, b, h, seq, hd, vbh);
+          const double* pbh = probs + (b * g + h) * seq * seq;
+          memset(dprobs, 0, seq * seq * sizeof(double));
+          orc_matmul_nt_acc(dobh, hd, vbh, hd, dprobs, seq, seq, hd, seq);
+          memset(t3, 0, seq * hd * sizeof(double)); /* dvbh */
+          orc_matmul_tn_acc(pbh, seq, dobh, hd, t3, hd, seq, seq, hd);
+          for (size_t i = 0; i < seq; ++i) { /* softmax_backward_rows (:27-36) */
+            double dot = 0.0;
+            for (size_t jj = 0; jj < seq; ++jj) dot += dprobs[i * seq + jj] * pbh[i * seq + jj];
+            for (size_t jj = 0; jj < seq; ++jj) ds[i * seq + jj] = pbh[i * seq + jj] * (dprobs[i * seq + jj] - dot);
+          }
+          for (size_t e = 0; e < seq * seq; ++e) ds[e] = ds[e] * inv_sqrt_hd;
+          orc_matmul(ds, seq, kbh, hd, t1, hd, seq, seq, hd); /* dqbh */
+          memset(t2, 0, seq * hd * sizeof(double));            /* dkbh */
+          orc_matmul_tn_acc(ds, seq, qbh, hd, t2, hd, seq, seq, hd);
+          write_head(dq, gw, b, h, seq, hd, t1);
+          write_head(dk, gw, b, h, seq, hd, t2);
+          write_head(dv, gw, b, h, seq, hd, t3);
+        }
+      orc_matmul_tn_acc(xr, H, dq, gw, gr, gw, H, M, gw);
+      orc_matmul_tn_acc(xr, H, dk, gw, gr + H * gw, gw, H, M, gw);
+      orc_matmul_tn_acc(xr, H, dv, gw, gr + 2 * H * gw, gw, H, M, gw);
+      orc_matmul_nt_acc(dq, gw, w, gw, dx + r * M * H, H, M, gw, H);
+      orc_matmul_nt_acc(dk, gw, w + H * gw, gw, dx + r * M * H, H, M, gw, H);
+      orc_matmul_nt_acc(dv, gw, w + 2 * H * gw, gw, dx + r * M * H, H, M, gw, H);
+    }
+    if (s + 1 < n) rotate_ccw_weight_grad(slots, n);
+  }
+#undef TAPE
+  for (size_t r = 0; r < n; ++r) memcpy(grads + r * L, slots[r].grad, L * sizeof(double));
+  free(qbh); free(kbh); free(vbh); free(dobh); free(obh); free(sc); free(dprobs); free(ds);
+  free(t1); free(t2); free(t3); free(da); free(dq); free(dk); free(dv);
+  free(tape);
+  free(slots);
+  free(store);
+  return 0;
+}
+
 void orc_sampled_dots(const double* a, size_t lda, size_t sa, const double* b, size_t ldb,
                       size_t sb, size_t k, const int64_t* ri, const int64_t* ci, size_t nq,
                       double* out) {

@@ -66,6 +66,13 @@ int orc_rtp_mlp(size_t n, size_t rows, size_t h, size_t f, const double* w1, con
 /* Sampled fp64 dot products for large configs (SURVEY §8c "spot-check"):
  * out[q] = sum_t a[ri[q]*lda + t*sa] * b[t*sb + ci[q]*ldb] over t < k, t ascending.
  * Covers Y = X.W (sa=1, sb=ldw, ldb=1), dX = dY.W^T and dW = X^T.dY via strides. */
+/* RtpAttention fwd (Train) + bwd (layers_attention.cpp:43-198), heads split
+ * across n workers (HeadPartition), batch-major row shards of `rows` (each a
+ * multiple of seq); grads = n shards of [gq | gk | gv | go] (4 H gw each). */
+int orc_rtp_attention(size_t n, size_t rows, size_t H, size_t heads, size_t seq, const double* wq,
+                      const double* wk, const double* wv, const double* wo, const double* x,
+                      const double* dy, double* y, double* dx, double* grads);
+
 void orc_sampled_dots(const double* a, size_t lda, size_t sa, const double* b, size_t ldb,
                       size_t sb, size_t k, const int64_t* ri, const int64_t* ci, size_t nq,
                       double* out);

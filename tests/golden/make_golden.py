@@ -90,6 +90,25 @@ def main():
             mlp[f"n{nn}_{k}"] = v
     out["mlp"] = mlp
 
+    # 4b. RtpAttention (layers_attention.cpp:43-198), heads split
+    #     over N in {1,2,4}, sequences of 8, two per worker, both transports.
+    #     Weights: one SplitMix64(42) stream, U[-0.1, 0.1], wq wk wv wo in order.
+    H, heads, seq = 32, 4, 8
+    wall = R.uniform(42, 0, 4 * H * H, -0.1, 0.1)
+    att = {"heads": heads, "seq": seq, "seed": 42}
+    for i, name in enumerate(("wq", "wk", "wv", "wo")):
+        att[name] = wall[i * H * H:(i + 1) * H * H].reshape(H, H)
+    for nn in (1, 2, 4):
+        rows_a = nn * 2 * seq
+        xa, dya = acts(R, 43 + nn, rows_a, H, H)
+        att[f"n{nn}_x"], att[f"n{nn}_dy"] = xa, dya
+        r = R.rtp_attention(nn, heads, seq, att["wq"], att["wk"], att["wv"], att["wo"], xa, dya)
+        rc = R.rtp_attention(nn, heads, seq, att["wq"], att["wk"], att["wv"], att["wo"], xa, dya, concurrent=True)
+        assert all(np.array_equal(r[k], rc[k]) for k in r), "lockstep != concurrent"
+        for k, v in r.items():
+            att[f"n{nn}_{k}"] = v
+    out["attention"] = att
+
     # 5. Ring primitive (ring.cpp:265-293) on id-encoded slots (ring_test.cpp:16-28)
     rng = np.random.default_rng(77)
     ring = {}
@@ -114,7 +133,10 @@ def main():
             led[f"table1_s{st}_N{N}"] = np.array(R.table1(st, 1000, 2000, 300, 40, N), np.int64)
     out["ledger"] = led
 
+    only = sys.argv[1:]  # e.g. `make_golden.py attention`: rewrite only those fixtures
     for name, d in out.items():
+        if only and name not in only:
+            continue
         np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **{k: np.asarray(v) for k, v in d.items()})
         print("wrote", name, len(d), "arrays")
 

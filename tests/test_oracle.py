@@ -86,6 +86,19 @@ def test_rtp_mlp_matches_reference_bitwise(golden, oracle, n):
         assert np.array_equal(r[k], g[f"n{n}_{k}"]), k
 
 
+@pytest.mark.parametrize("n", [1, 2, 4])
+def test_rtp_attention_matches_reference_bitwise(golden, oracle, n):
+    """SURVEY §8f.2 groundwork: the C restatement of RtpAttention (head
+    partition, per-(sequence, head) softmax attention, output projection
+    accumulated over the rotation, the tape, W+G backward rotation) reproduces
+    the reference's outputs and gradient shards bit for bit."""
+    g = golden("attention")
+    r = oracle.rtp_attention(n, int(g["heads"]), int(g["seq"]), g["wq"], g["wk"], g["wv"], g["wo"],
+                             g[f"n{n}_x"], g[f"n{n}_dy"])
+    for k in ("y", "dx", "grads"):
+        assert np.array_equal(r[k], g[f"n{n}_{k}"]), k
+
+
 def test_gelu_matches_reference_values(oracle):
     # tensor_test.cpp:371-393 style: exact erf form and derivative by central differences
     x = np.linspace(-4, 4, 101)
