@@ -45,14 +45,31 @@ for _ in range(5):
     step()
 torch.cuda.synchronize()
 buf = torch.zeros((64 if SOLO else 6) * 148 * STRIDE + 1024, dtype=torch.int64, device=dev)
-for rep in range(3):
-    buf.zero_()
-    flush.zero_()
-    flush.sum().item()
+if os.environ.get("GRAPH"):
+    # GRAPH=1: the step captured in a CUDA graph (as bench.py times it); the
+    # trace pointers are baked into the captured launches
+    cs = torch.cuda.Stream(dev)
+    cs.wait_stream(torch.cuda.current_stream(dev))
+    gph = torch.cuda.CUDAGraph()
     _lib.lib.rtpb_debug_trace(buf.data_ptr(), buf.numel() * 8)
-    step()
-    torch.cuda.synchronize()
+    with torch.cuda.graph(gph, stream=cs):
+        step()
     _lib.lib.rtpb_debug_trace(None, 0)
+    for rep in range(3):
+        buf.zero_()
+        flush.zero_()
+        flush.sum().item()
+        gph.replay()
+        torch.cuda.synchronize()
+else:
+    for rep in range(3):
+        buf.zero_()
+        flush.zero_()
+        flush.sum().item()
+        _lib.lib.rtpb_debug_trace(buf.data_ptr(), buf.numel() * 8)
+        step()
+        torch.cuda.synchronize()
+        _lib.lib.rtpb_debug_trace(None, 0)
 tr = buf.cpu().numpy().astype(np.float64)
 # locate launches: consecutive blocks, grid unknown -> infer from nonzero entries
 t_origin = None
