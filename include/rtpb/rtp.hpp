@@ -348,8 +348,9 @@ class RtpLinear : public RtpLayerBase {
   // Shard-arrival flags (rtp_layers.cpp): forward W, backward W, backward G
   // blocks of the layer's flag range, indexed by the step the shard is for.
   static constexpr size_t kFlagFwd = 0, kFlagBwdW = 16, kFlagBwdG = 32;
+  // CTA counters of the grids that clear each block (the pass's last reader)
+  static constexpr size_t kFlagCtrFwd = 48, kFlagCtrW = 49, kFlagCtrG = 50;
   bool use_flags() const;
-  void reset_flags(size_t first, size_t count);
   void flagged_exchange(Direction dir, std::span<void* const> send, std::span<void* const> recv, size_t bytes,
                         size_t flag);
 

@@ -370,6 +370,10 @@ void RtpLinear::forward_ex(std::span<const DView> x, size_t rows, std::span<cons
       Worker& w = group_->worker(r);
       // this step's shard landed in the previous step's spare
       set_launch_wait_flag(wait_flag ? w.flag(flag_base_ + kFlagFwd + s) : nullptr);
+      // the pass's last reader clears the pass's flags when it is done
+      if (wait_flag && s + 1 == n)
+        set_launch_flag_reset(w.flag(flag_base_ + kFlagFwd), int(kFlagBwdW - kFlagFwd),
+                              w.flag(flag_base_ + kFlagCtrFwd));
       const size_t k = k_of[r];
       const size_t j = slots_[r].logical_id;
       int flags = e.store_pre ? RTPB_EPI_STORE_PRE : 0;
@@ -386,6 +390,7 @@ void RtpLinear::forward_ex(std::span<const DView> x, size_t rows, std::span<cons
                                    j * per_, act, ld_act, rows, in_, per_, flags, workspace_[r].data(),
                                    workspace_[r].bytes(), w.compute);
       set_launch_wait_flag(nullptr);
+      set_launch_flag_reset(nullptr, 0, nullptr);
       check_status(rc);
     });
     if (!rotate) break;
@@ -402,14 +407,14 @@ void RtpLinear::forward_ex(std::span<const DView> x, size_t rows, std::span<cons
   // for the next layer stays in flight; that layer's pass joins it.
   if (n > 1 && prefetch && use_flags()) {
     for (size_t r : local) group_->worker(r).wait(Ev::PassEnd, false);
-    reset_flags(kFlagFwd, kFlagBwdW - kFlagFwd);
   }
   if (mode == Mode::Eval) rehome_after_eval();
 }
 
 // Arrival flags (bf16 mode, one worker per GPU, N <= 16): the shift's comm
 // stream moves the shard, then sets the flag with a stream memory operation
-// (no SM needed; reset_flags clears a pass's flags at its end); the consuming step GEMM waits for it on the device
+// (no SM needed; the pass's last reader grid clears the pass's flags when it
+// is done — GemmArgs::flag_reset — after every flag of the pass was set); the consuming step GEMM waits for it on the device
 // instead of its stream waiting for comm, so consecutive step GEMMs keep their
 // programmatic (PDL) launch overlap. Deadlock freedom: every flag's writer was
 // issued before its waiter and waits only on earlier-issued kernels; a waiting
@@ -430,20 +435,6 @@ bool RtpLinear::use_flags() const {
   const TransportKind k = group_->kind();
   const bool one_per_gpu = k == TransportKind::Nccl || k == TransportKind::Ipc || k == TransportKind::Solo;
   return on && one_per_gpu && dtype_ == DType::BF16 && group_->size() > 1 && group_->size() <= 16;
-}
-
-// A pass's flags go back to 0 on the compute stream once every reader has
-// run (pass end, after the join), so the next pass's readers, later on the
-// same stream, cannot see a stale 1, and its writers (comm, ordered after the
-// compute tail) set them only after. (Clearing on the comm stream before the
-// shift would race: the reading GEMM starts, by PDL, as soon as its
-// predecessor ends, which is also when that comm stream is released.)
-void RtpLinear::reset_flags(size_t first, size_t count) {
-  for (size_t r : group_->local_ranks()) {
-    Worker& w = group_->worker(r);
-    DeviceGuard dg(w.device);
-    cuda_check(cudaMemsetAsync(w.flag(flag_base_ + first), 0, count * sizeof(unsigned), w.compute), "reset flags");
-  }
 }
 
 void RtpLinear::flagged_exchange(Direction dir, std::span<void* const> send, std::span<void* const> recv,
@@ -643,6 +634,9 @@ void RtpLinear::backward_ex(std::span<const DView> dy, size_t rows, std::span<co
       }
       float* acc = n > 1 ? static_cast<float*>(dx_acc_[r].data()) : nullptr;
       set_launch_wait_flag(flags_on && s > 0 ? w.flag(flag_base_ + kFlagBwdW + s) : nullptr);
+      if (flags_on && s + 1 == n)  // the last dX clears the pass's W flags
+        set_launch_flag_reset(w.flag(flag_base_ + kFlagBwdW), int(kFlagBwdG - kFlagBwdW),
+                              w.flag(flag_base_ + kFlagCtrW));
       const size_t ldy = dy[k].ld ? dy[k].ld : out_, ldx = dx[k].ld ? dx[k].ld : in_;
       const int rc =
           paired(s) ? rtpb_dgrad_step2(dt, dy[k].data, ldy, prev_j[r] * per_, spares_[r].data(), j * per_,
@@ -652,6 +646,7 @@ void RtpLinear::backward_ex(std::span<const DView> dy, size_t rows, std::span<co
                                       ldx, pre, ldpre, rows, in_, per_, flags, workspace_[r].data(),
                                       workspace_[r].bytes(), w.compute);
       set_launch_wait_flag(nullptr);
+      set_launch_flag_reset(nullptr, 0, nullptr);
       check_status(rc);
     });
     for (size_t r : local) prev_j[r] = slots_[r].logical_id;
@@ -690,6 +685,9 @@ void RtpLinear::backward_ex(std::span<const DView> dy, size_t rows, std::span<co
       Worker& w = group_->worker(r);
       const cudaStream_t ws = dx_sms ? w.aux : w.compute;
       set_launch_wait_flag(g_flag && s > 0 ? w.flag(flag_base_ + kFlagBwdG + s) : nullptr);
+      if (flags_on && s + 1 == n)  // the last dW clears the pass's G flags
+        set_launch_flag_reset(w.flag(flag_base_ + kFlagBwdG), int(kFlagCtrFwd - kFlagBwdG),
+                              w.flag(flag_base_ + kFlagCtrG));
       const size_t k = k_of[r];
       const size_t j = slots_[r].logical_id;
       float* g = static_cast<float*>(slots_[r].grad_acc.data());
@@ -699,6 +697,7 @@ void RtpLinear::backward_ex(std::span<const DView> dy, size_t rows, std::span<co
                                      dy[k].ld ? dy[k].ld : out_, j * per_, g_in, g, rows, in_, per_,
                                      workspace_[r].data(), workspace_[r].bytes(), ws);
       set_launch_wait_flag(nullptr);
+      set_launch_flag_reset(nullptr, 0, nullptr);
       check_status(rc);
     });
     if (dx_sms) set_sm_budget(all_sms);
@@ -720,12 +719,7 @@ void RtpLinear::backward_ex(std::span<const DView> dy, size_t rows, std::span<co
     group_->advance_slots(slots_, Direction::CounterClockwise, PayloadKind::WeightAndGrad, label_, shard_len_);
   }
   if (n > 1 && use_flags()) {
-    for (size_t r : local) {
-      Worker& w = group_->worker(r);
-      w.wait(Ev::PassEnd, false);
-      if (dx_sms) w.join_aux();  // the G flags' readers ran on aux
-    }
-    reset_flags(kFlagBwdW, Worker::kFlagsPerLayer - kFlagBwdW);
+    for (size_t r : local) group_->worker(r).wait(Ev::PassEnd, false);
   }
   grads_zero_pending_ = false;
   for (size_t r : local) x_cache_[r] = {};

@@ -45,7 +45,7 @@ struct Worker {
   DeviceBuffer stage;  // in-place rotation staging chunk (CommBuffer)
   // Shard-arrival flags written by the comm stream (stream memory ops) and
   // waited on inside the step GEMMs; kFlagsPerLayer per layer.
-  static constexpr size_t kFlagPool = 8192, kFlagsPerLayer = 48;
+  static constexpr size_t kFlagPool = 16384, kFlagsPerLayer = 64;
   DeviceBuffer flags;
   unsigned* flag(size_t i) { return static_cast<unsigned*>(flags.data()) + i; }
 

@@ -97,6 +97,9 @@ int device_sms() {
 // GEMMs issued on two streams run side by side instead of queueing.
 thread_local int t_sm_budget = 0;
 thread_local const unsigned* t_wait_flag = nullptr;
+thread_local unsigned* t_reset_flags = nullptr;
+thread_local unsigned* t_reset_ctr = nullptr;
+thread_local int t_reset_count = 0;
 // Second K segment of the next launch (gemm_dgrad over two shards): its A
 // and B operands, encoded into the launch's second GemmMaps.
 struct KSeg {
@@ -200,6 +203,11 @@ int launch_cfg(const Op& a, const Op& b, const Out& c0, const Out* c1, const Gem
   if (t_kseg.on) a_.kseg_kb = t_kseg.kb;
   a_.trace = next_trace(cfg.gridDim.x);
   if (!a_.ready_flag) a_.ready_flag = t_wait_flag;  // set_launch_wait_flag()
+  if (!a_.flag_reset && t_reset_flags) {              // set_launch_flag_reset()
+    a_.flag_reset = t_reset_flags;
+    a_.flag_reset_ctr = t_reset_ctr;
+    a_.flag_reset_count = t_reset_count;
+  }
   cudaError_t e = cudaLaunchKernelEx(&cfg, rtp_gemm_kernel<Cfg>, maps, maps2 ? *maps2 : maps, a_);
   if (e != cudaSuccess) return set_cuda_error(e, "rtp_gemm_kernel launch");
   count_launch();
@@ -790,6 +798,11 @@ int gemm_bwd_fused(const FusedBwdArgs& a, const FusedBwdPlan& plan, const FusedB
 
 void set_sm_budget(int sms) { t_sm_budget = sms; }
 void set_launch_wait_flag(const unsigned* flag) { t_wait_flag = flag; }
+void set_launch_flag_reset(unsigned* flags, int count, unsigned* ctr) {
+  t_reset_flags = flags;
+  t_reset_count = flags ? count : 0;
+  t_reset_ctr = flags ? ctr : nullptr;
+}
 int sm_budget() { return sm_count(); }
 
 void set_trace(void* buf, size_t bytes) {

@@ -118,6 +118,14 @@ struct GemmArgs {
   // K blocks kb >= kseg_kb read the A and B maps of the second GemmMaps at
   // K offset (kb - kseg_kb) * BK. 0: one segment.
   int kseg_kb;
+  // The last reader of a pass's arrival flags clears them: once every CTA of
+  // this grid is done (counter flag_reset_ctr), [flag_reset, +flag_reset_count)
+  // and the counter return to 0. Every flag of the pass was set before this
+  // grid passed its own flag wait (one comm stream, in order), and the next
+  // pass's readers run after this grid (stream order / griddepcontrol.wait).
+  unsigned* flag_reset;
+  unsigned* flag_reset_ctr;
+  int flag_reset_count;
   unsigned* dep_count;
   unsigned dep_target;
   int dep_rows;
@@ -1295,6 +1303,14 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
       tmem_dealloc_pair(tmem_base, Cfg::TMEM_COLS);
     else
       tmem_dealloc(tmem_base, Cfg::TMEM_COLS);
+  }
+  if (args.flag_reset && threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(args.flag_reset_ctr, 1u) == gridDim.x - 1) {
+      for (int i = 0; i < args.flag_reset_count; ++i) args.flag_reset[i] = 0u;
+      *args.flag_reset_ctr = 0u;
+      __threadfence();
+    }
   }
   if (args.dep_count && threadIdx.x == 0) {
     // every thread of this CTA is past its last dependency read: the last CTA

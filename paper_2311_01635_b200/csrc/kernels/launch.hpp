@@ -130,6 +130,9 @@ int sm_budget();
 // The calling thread's following GEMM launches load no operand before
 // *flag >= 1 (nullptr: no wait). See GemmArgs::ready_flag.
 void set_launch_wait_flag(const unsigned* flag);
+// The calling thread's next step-GEMM launch clears [flags, +count) (and the
+// CTA counter ctr) when all its CTAs are done; nullptr = none.
+void set_launch_flag_reset(unsigned* flags, int count, unsigned* ctr);
 // Debug: route per-CTA timeline stamps of the following GEMM launches into buf.
 void set_trace(void* buf, size_t bytes);
 int gemm_dgrad(bool f32, const StepDgrad& p, cudaStream_t s);
