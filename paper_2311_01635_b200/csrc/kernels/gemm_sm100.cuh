@@ -1011,27 +1011,40 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
           // (a row per lane costs 32 L1 wavefronts per instruction). All S
           // partials of an element are loaded before the sum, added in split
           // order, then G: the same order, and bits, as the chained folds.
-          for (int r = r_lo; r < r_hi; ++r) {
-            const int grow = row0 + r;
-            if (grow >= uM) break;
-#pragma unroll 1
-            for (int ch = half; ch < BN / 32; ch += NSPLIT) {
-              const int col = n0 + ch * 32 + lane;
-              if (n0 + ch * 32 >= uN) break;  // warp-uniform
-              if (col < uN) {
-                float tv[8];
+          // Every load of a group (RPI rows x all of the warp's chunks x the S
+          // partials, and G) is issued before the first sum, so the fold costs
+          // one L2 round trip per group instead of two per (row, chunk).
+          constexpr int CH = BN / 32 / NSPLIT;      // chunks of this warp
+          constexpr int RPI = CH <= 2 ? 2 : 1;      // rows per group
+          for (int r = r_lo; r < r_hi; r += RPI) {
+            float tv[RPI][CH][8], gv[RPI][CH];
+#pragma unroll
+            for (int i = 0; i < RPI; ++i)
+#pragma unroll
+              for (int c = 0; c < CH; ++c) {
+                const int grow = row0 + r + i;
+                const int col = n0 + (half + c * NSPLIT) * 32 + lane;
+                const bool ok = r + i < r_hi && grow < uM && col < uN;
 #pragma unroll
                 for (int sp = 0; sp < 8; ++sp)
-                  tv[sp] = sp < wsplits ? __ldcg(part + (size_t(sp) * wprows + grow) * uN + col) : 0.f;
-                float a = 0.f;
-#pragma unroll
-                for (int sp = 0; sp < 8; ++sp)
-                  if (sp < wsplits) a += tv[sp];
-                float* dst = gout + size_t(grow) * uN + col;
-                if (!first) a = __ldcg(dst) + a;
-                *dst = a;
+                  tv[i][c][sp] = ok && sp < wsplits ? __ldcg(part + (size_t(sp) * wprows + grow) * uN + col) : 0.f;
+                gv[i][c] = ok && !first ? __ldcg(gout + size_t(grow) * uN + col) : 0.f;
               }
-            }
+#pragma unroll
+            for (int i = 0; i < RPI; ++i)
+#pragma unroll
+              for (int c = 0; c < CH; ++c) {
+                const int grow = row0 + r + i;
+                const int col = n0 + (half + c * NSPLIT) * 32 + lane;
+                if (r + i < r_hi && grow < uM && col < uN) {
+                  float a = 0.f;
+#pragma unroll
+                  for (int sp = 0; sp < 8; ++sp)
+                    if (sp < wsplits) a += tv[i][c][sp];
+                  if (!first) a = gv[i][c] + a;
+                  gout[size_t(grow) * uN + col] = a;
+                }
+              }
           }
           __syncwarp();
           if (lane == 0) {  // count out; the last split out re-zeroes the region counter
