@@ -1,14 +1,19 @@
 """RTP MLP fwd+bwd benchmark (BASELINE.json metric: "RTP MLP fwd+bwd TFLOP/s/GPU
 & peak HBM/GPU at 1/2/4/8 B200 vs CPU ref").
 
-Workload (config (b) of BASELINE.json, the metric's single-GPU config): one
-RTP MLP block ffn1 768->3072 -> GELU -> ffn2 3072->768, bf16, Flyweight init
-(SplitMix64 seed 42), 8192 tokens per GPU (GPT-2 seq 512 x 16, SURVEY §8d;
-global T = 8192 x N, batch-major row shards: weak scaling). A step = zero
-grads + forward + backward of the block through the library's public API.
-FLOPs per step = 12 * T * h * f (fwd, dX, dW at 2*T*h*f per linear).
+Workloads (BASELINE.json configs), bf16, Flyweight init
+(SplitMix64 seed 42, SerialModel parameter order), synthetic activations:
+  d (default)  stack of 32 RTP MLP blocks 4096 -> 16384 -> 4096, 16384 tokens
+               per GPU (seq 2048 x global batch 64 over 8 GPUs), weak scaling:
+               north_star's roofline target config; fits one GPU (~62 GB)
+  b            one MLP block 768 -> 3072 -> 768, 8192 tokens per GPU, weak
+  c            one MLP block 8192 -> 28672 -> 8192, 32768 global tokens
+               (strong scaling), in-place vs out-of-place peak memory
+A step = zero_grads + forward through every block + backward in reverse,
+through the library's public API (RtpMlp, C ABI). FLOPs per step =
+12 * T * h * f * blocks (fwd, dX, dW at 2*T*h*f per linear).
 
-python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+python bench.py [--config d] [--gpus N --steps K --warmup W] [--impl reference]
 N > 1: launch with torch.distributed.run, one process per GPU, NCCL ring.
 """
 from __future__ import annotations
@@ -16,6 +21,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import platform
 import subprocess
 import sys
 import threading
@@ -24,22 +30,46 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-H, F, TOKENS_PER_GPU, SEED = 768, 3072, 8192, 42
+SEED = 42
 METRIC = "RTP MLP fwd+bwd TFLOP/s/GPU & peak HBM/GPU at 1/2/4/8 B200 vs CPU ref"
 UNIT = "TFLOP/s"
 
+# name: (h, f, blocks, tokens per GPU (weak) or None, global tokens (strong) or None, label)
+CONFIGS = {
+    "b": (768, 3072, 1, 8192, None, "rtp_mlp_768x3072x768 (config b)"),
+    "c": (8192, 28672, 1, None, 32768, "rtp_mlp_8192x28672x8192 (config c)"),
+    "d": (4096, 16384, 32, 16384, None, "rtp_mlp_stack32_4096x16384 (config d)"),
+}
 
-def flops_per_step(tokens: int) -> float:
-    return 12.0 * tokens * H * F
+
+def flops_per_step(tokens: int, h: int, f: int, blocks: int) -> float:
+    return 12.0 * tokens * h * f * blocks
 
 
 def load_peaks():
     try:
-        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
-            p = json.load(f)
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            p = json.load(fh)
         return float(p["bf16_tflops"]), float(p.get("bf16_tflops_sustained", p["bf16_tflops"])), "measured"
     except Exception:
         return 1590.0, 1400.0, "fallback"
+
+
+def host_info():
+    model = platform.processor() or ""
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    try:
+        affinity = len(os.sched_getaffinity(0))
+    except Exception:
+        affinity = os.cpu_count()
+    return {"nproc": affinity, "cpu_count": os.cpu_count(), "cpu_model": model}
 
 
 class ClockSampler:
@@ -48,7 +78,6 @@ class ClockSampler:
     def __init__(self, gpu_index: int):
         self.gpu = gpu_index
         self.samples = []
-        self._stop = threading.Event()
         self._proc = None
 
     def __enter__(self):
@@ -105,86 +134,155 @@ def dist_env():
 
 
 # ------------------------------------------------------------------ reference arm
-def cpu_reference(sample_rows: int | None = None, target_s: float = 12.0, iters: int = 1):
+def _cpu_workers(h, f):
+    cores = host_info()["nproc"] or 1
+    workers = 1
+    while workers * 2 <= cores and f % (workers * 2) == 0 and h % (workers * 2) == 0:
+        workers *= 2
+    return workers
+
+
+def cpu_reference(cfg, sample_rows=None, target_s=12.0, iters=1):
     """Times the reference's own CPU implementation of the path (oracle/_ref:
-    the reference sources compiled by path; RtpLinear x2 + gelu on the
-    Concurrent transport, one worker thread per host core, fp64) on a bounded
-    row sample of the same workload. Falls back to the C restatement."""
+    the reference sources compiled by path; two RtpLinear + gelu composed as
+    model.cpp:77-105, Concurrent transport, one worker thread per host core,
+    fp64) on ONE block of the config at a bounded row sample. A stack's step
+    is linear in FLOPs, so the rate extrapolates to the whole workload
+    (labelled). Falls back to the C restatement when oracle/_ref is absent."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import oracle as orc
-    cores = os.cpu_count() or 1
-    workers = 1
-    while workers * 2 <= cores and (F % (workers * 2) == 0) and (H % (workers * 2) == 0):
-        workers *= 2
+    h, f, blocks = CONFIGS[cfg][:3]
+    workers = _cpu_workers(h, f)
     try:
         R = orc.Reference()
         kind = "reference"
 
-        def run(rows):
-            return R.time_mlp(workers, rows, H, F, SEED, iters=1, concurrent=True)
+        def run(rows, k=1):
+            return R.time_mlp(workers, rows, h, f, SEED, iters=k, concurrent=True)
     except Exception:
         O = orc.Oracle()
         kind = "port"
         import numpy as np
         rng = np.random.default_rng(SEED)
-        w1, b1 = rng.uniform(-0.1, 0.1, (H, F)), rng.uniform(-0.1, 0.1, F)
-        w2, b2 = rng.uniform(-0.1, 0.1, (F, H)), rng.uniform(-0.1, 0.1, H)
+        w1, b1 = rng.uniform(-0.1, 0.1, (h, f)), rng.uniform(-0.1, 0.1, f)
+        w2, b2 = rng.uniform(-0.1, 0.1, (f, h)), rng.uniform(-0.1, 0.1, h)
 
-        def run(rows):
-            x, dy = rng.uniform(-1, 1, (rows, H)), rng.uniform(-1, 1, (rows, H))
-            t0 = time.perf_counter()
-            O.rtp_mlp(workers, w1, b1, w2, b2, x, dy)
-            return time.perf_counter() - t0
+        def run(rows, k=1):
+            t = 0.0
+            for _ in range(k):
+                x, dy = rng.uniform(-1, 1, (rows, h)), rng.uniform(-1, 1, (rows, h))
+                t0 = time.perf_counter()
+                O.rtp_mlp(workers, w1, b1, w2, b2, x, dy)
+                t += time.perf_counter() - t0
+            return t
     if sample_rows is None:
-        probe = 32 * workers
+        probe = 8 * workers
         t = run(probe)
-        rate = flops_per_step(probe) / max(t, 1e-6)
-        sample_rows = int(target_s * rate / flops_per_step(1))
-        sample_rows = max(workers, min(TOKENS_PER_GPU, (sample_rows // workers) * workers))
-    secs = sum(run(sample_rows) for _ in range(iters))
-    value = flops_per_step(sample_rows) * iters / secs / 1e12
+        rate = flops_per_step(probe, h, f, 1) / max(t, 1e-6)
+        sample_rows = int(target_s * rate / flops_per_step(1, h, f, 1))
+        cap = CONFIGS[cfg][3] or CONFIGS[cfg][4]
+        sample_rows = max(workers, min(cap, (sample_rows // workers) * workers))
+    secs = run(sample_rows, iters)
+    value = flops_per_step(sample_rows, h, f, 1) * iters / secs / 1e12
+    info = host_info()
     return {"value": value, "unit": UNIT, "cores": workers, "kind": kind,
-            "sample": f"{iters}x MLP fwd+bwd over {sample_rows} of {TOKENS_PER_GPU} tokens (768->3072->768, fp64, "
-                      f"{workers} Concurrent-transport workers), {secs:.1f} s"}
+            "sample": f"{iters}x one {h}->{f}->{h} MLP block fwd+bwd over {sample_rows} rows (fp64, {workers} "
+                      f"Concurrent-transport worker threads), {secs:.1f} s"
+                      + (f"; extrapolated to the {blocks}-block stack (step time linear in FLOPs)" if blocks > 1
+                         else ""),
+            "extrapolated": blocks > 1 or sample_rows < (CONFIGS[cfg][3] or CONFIGS[cfg][4]),
+            "rows": sample_rows, "seconds": secs, "host": info}
 
 
 def run_reference_arm(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    steps = []
-    # bounded sample per step so --steps K --warmup W ends within minutes
-    per_step_target = max(2.0, 60.0 / max(1, args.steps + args.warmup))
-    base = cpu_reference(target_s=per_step_target)
-    rows = int(base["sample"].split(" over ")[1].split(" ")[0])
-    for _ in range(args.warmup):
-        cpu_reference(sample_rows=rows)
-    for _ in range(args.steps):
-        steps.append(cpu_reference(sample_rows=rows))
-    value = sum(s["value"] for s in steps) / len(steps)
-    ms = flops_per_step(rows) / (value * 1e12) * 1e3
+    h, f, blocks, tpg, tglob, label = CONFIGS[args.config]
+    per_step_target = max(1.5, 60.0 / max(1, args.steps + args.warmup))
+    base = cpu_reference(args.config, target_s=per_step_target)
+    rows = base["rows"]
+    if args.warmup:
+        cpu_reference(args.config, sample_rows=rows, iters=args.warmup)
+    timed = cpu_reference(args.config, sample_rows=rows, iters=args.steps)
+    value = timed["value"]
+    ms = flops_per_step(rows, h, f, 1) / (value * 1e12) * 1e3
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "rtp_mlp_768x3072x768", "tokens": rows, "tokens_per_gpu": TOKENS_PER_GPU,
-                       "note": "bounded row sample of the same workload on host cores"},
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak" if tpg else "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": label, "h": h, "f": f, "blocks": blocks, "sample_tokens": rows,
+                       "tokens_per_gpu": tpg or (tglob // max(1, args.gpus)),
+                       "note": "each step: one block over a bounded row sample on host cores; TFLOP/s "
+                               "extrapolates to the whole stack (linear in FLOPs)"},
             "impl": "reference",
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": steps[0]["cores"], "kind": steps[0]["kind"],
-                             "sample": steps[0]["sample"]},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": timed["cores"], "kind": timed["kind"],
+                             "sample": timed["sample"], "host": timed["host"]},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ ring self-check
+def ring_self_check(rtp, grp, ring, rank, mode, world):
+    """Before timing: the committed reference golden tests/golden/mlp_ring.npz
+    (the reference's own RtpMlp, N in {1,2,4,8}) through THIS group's transport
+    and ring size; every local rank's Y / dX rows and gradient shards within
+    the bf16 tolerance (normwise 2e-2). Returns (ok, detail)."""
+    import numpy as np
+    import torch
+    path = os.path.join(ROOT, "tests", "golden", "mlp_ring.npz")
+    try:
+        g = np.load(path)
+    except OSError as exc:
+        return None, f"fixture missing: {exc}"
+    if f"n{ring}_y" not in g:
+        return None, f"no golden for a ring of {ring}"
+    rows = g["x"].shape[0]
+    M = rows // ring
+    m = rtp.RtpMlp(grp, "selfcheck", g["w1"].shape[0], g["w1"].shape[1], "bf16", w1=g["w1"], b1=g["b1"],
+                   w2=g["w2"], b2=g["b2"])
+    m.set_rotation_mode(mode)
+    m.begin_step()
+    m.zero_grads()
+
+    def dev(a, r):
+        return torch.from_numpy(np.ascontiguousarray(a[r * M:(r + 1) * M])).to(torch.bfloat16).to(
+            grp.device_of(r)).contiguous()
+    ranks = grp.local_ranks
+    ys = m.forward([dev(g["x"], r) for r in ranks])
+    dxs = m.backward([dev(g["dy"], r) for r in ranks])
+    grp.synchronize()
+
+    def nerr(a, ref):
+        ref = np.asarray(ref, np.float64)
+        return float(np.max(np.abs(np.asarray(a, np.float64) - ref)) / max(np.max(np.abs(ref)), 1e-300))
+    worst = 0.0
+    for k, r in enumerate(ranks):
+        sl = slice(r * M, (r + 1) * M)
+        worst = max(worst, nerr(ys[k].double().cpu().numpy(), g[f"n{ring}_y"][sl]),
+                    nerr(dxs[k].double().cpu().numpy(), g[f"n{ring}_dx"][sl]),
+                    nerr(m.ffn1.grad_shard(r).double().cpu().numpy(), g[f"n{ring}_grads1"][r]),
+                    nerr(m.ffn2.grad_shard(r).double().cpu().numpy(), g[f"n{ring}_grads2"][r]))
+        home = (m.ffn1.slot(r)["logical_id"], m.ffn2.slot(r)["logical_id"])
+        if home != (r, r):
+            worst = float("inf")
+    m.close()
+    return worst < 2e-2, f"max normwise error {worst:.3e} over Y, dX, dW1|db1, dW2|db2 (tolerance 2e-2)"
 
 
 # ------------------------------------------------------------------ our arm
 def main():
     ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="d", choices=sorted(CONFIGS))
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=300)
-    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--mode", default="outofplace", choices=["inplace", "outofplace"])
-    ap.add_argument("--tokens-per-gpu", type=int, default=TOKENS_PER_GPU)
+    ap.add_argument("--blocks", type=int, default=None, help="override the config's block count")
+    ap.add_argument("--tokens-per-gpu", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer e2e leg (profiling runs)")
+    ap.add_argument("--no-profile", action="store_true", help="skip the profiled per-launch replay")
     ap.add_argument("--eager", action="store_true", help="time host-issued launches instead of a CUDA graph")
     ap.add_argument("--transport", default="nccl", choices=["nccl", "ipc"],
                     help="N > 1 ring shift: ncclSend/ncclRecv (default) or copy-engine pushes through CUDA IPC")
@@ -205,12 +303,16 @@ def main():
 
     from paper_2311_01635_b200 import _lib, rtp
 
+    H, F, BLOCKS, TPG, TGLOB, LABEL = CONFIGS[args.config]
+    if args.blocks:
+        BLOCKS = args.blocks
     rank, world, local = dist_env()
     if args.same_device:
         local = 0
         args.transport = "ipc"
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    graph_fallback = None
     if world > 1:
         # plumbing only (barriers, max over ranks, the id broadcast)
         if args.same_device:
@@ -224,6 +326,7 @@ def main():
         grp = make(world, rank, local, box[0])
         if args.transport == "ipc":
             args.eager = True  # the IPC flags carry per-shift sequence numbers: no graph replay
+            graph_fallback = "IPC transport: shift flags carry per-shift sequence numbers (not replayable)"
     elif args.solo > 1:
         grp = rtp.WorkerGroup.solo(args.solo, 0, local)
     else:
@@ -235,25 +338,6 @@ def main():
         t = torch.tensor([v], dtype=torch.float64, device="cpu" if args.same_device else dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
-    M = args.tokens_per_gpu
-    T = M * world
-    ring = args.solo if args.solo > 1 else world  # ring size the layers are sharded for
-    mlp = rtp.RtpMlp(grp, "block0", H, F, "bf16", seed=SEED, stream_base=0)  # Flyweight init on device
-    mlp.set_rotation_mode(args.mode)
-    mlp.begin_step()
-
-    g = torch.Generator(device=dev).manual_seed(SEED + rank)
-    x = (torch.rand(M, H, device=dev, generator=g) * 2 - 1).to(torch.bfloat16)
-    dy = (torch.rand(M, H, device=dev, generator=g) * 2 - 1).to(torch.bfloat16)
-    y = torch.empty(M, H, dtype=torch.bfloat16, device=dev)
-    dx = torch.empty(M, H, dtype=torch.bfloat16, device=dev)
-    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # 512 MiB > 126 MB L2
-    flush_sink = torch.zeros((), dtype=torch.float32, device=dev)
-
-    def step():
-        mlp.zero_grads()
-        mlp.forward([x], out=[y])
-        mlp.backward([dy], out=[dx])
 
     def barrier():
         torch.cuda.synchronize()
@@ -261,29 +345,78 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
 
+    ring = args.solo if args.solo > 1 else world  # ring size the layers are sharded for
+    if args.tokens_per_gpu:
+        M = args.tokens_per_gpu
+    else:
+        M = TPG if TPG else TGLOB // ring
+    T = M * world  # tokens processed by the whole job per step
+    fl_step = flops_per_step(T, H, F, BLOCKS)
+
+    # ---- self-check through the same transport and ring size (reference golden)
+    parity_ok, parity_detail = (None, "solo: no peers, shifts skipped") if args.solo > 1 else \
+        ring_self_check(rtp, grp, ring, rank, args.mode, world)
+    if parity_ok is not None and world > 1:
+        parity_ok = allmax(0.0 if parity_ok else 1.0) == 0.0
+
+    # ---- the model: BLOCKS Flyweight blocks, SerialModel stream order, chained
+    per_block_params = 2 * H * F + F + H
+    mlps = []
+    for b in range(BLOCKS):
+        m = rtp.RtpMlp(grp, f"block{b}", H, F, "bf16", seed=SEED, stream_base=b * per_block_params)
+        m.set_rotation_mode(args.mode)
+        m.begin_step()
+        mlps.append(m)
+    for a, b in zip(mlps, mlps[1:]):
+        a.chain(b)  # a block posts its neighbour's first weight shift under its own last step
+
+    g = torch.Generator(device=dev).manual_seed(SEED + rank)
+    x = (torch.rand(M, H, device=dev, generator=g) * 2 - 1).to(torch.bfloat16)
+    dy = (torch.rand(M, H, device=dev, generator=g) * 2 - 1).to(torch.bfloat16)
+    outs = [torch.empty(M, H, dtype=torch.bfloat16, device=dev) for _ in range(BLOCKS)]
+    grads = [torch.empty(M, H, dtype=torch.bfloat16, device=dev) for _ in range(2)]
+    dx = torch.empty(M, H, dtype=torch.bfloat16, device=dev)
+    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # 512 MiB > 126 MB L2
+    flush_sink = torch.zeros((), dtype=torch.float32, device=dev)
+
+    def step(x_in=None, dy_in=None, dx_out=None):
+        for m in mlps:
+            m.zero_grads()
+        inp = [x if x_in is None else x_in]
+        for b, m in enumerate(mlps):
+            m.forward(inp, out=[outs[b]])
+            inp = [outs[b]]
+        up = [dy if dy_in is None else dy_in]
+        for b in range(BLOCKS - 1, -1, -1):
+            o = (dx if dx_out is None else dx_out) if b == 0 else grads[b % 2]
+            mlps[b].backward(up, out=[o])
+            up = [o]
+
+    t0 = time.perf_counter()
     for _ in range(args.warmup):
         step()
     barrier()
+    est_ms = (time.perf_counter() - t0) * 1e3 / args.warmup
 
     stream = torch.cuda.current_stream(dev)
-    # ---- eager reference timing (host-issued launches), for the record
+    # ---- eager timing (host-issued launches), for the record
     eager_ms = None
     if not args.eager:
+        k = max(2, min(20, int(3000 / max(est_ms, 1e-3))))
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         barrier()
         e0.record(stream)
-        for _ in range(20):
+        for _ in range(k):
             step()
         e1.record(stream)
         barrier()
-        eager_ms = e0.elapsed_time(e1) / 20
+        eager_ms = allmax(e0.elapsed_time(e1) / k)
 
     # ---- capture one step (zero_grads + forward + backward through the public
-    # API, every library launch incl. PDL edges and CTA-pair clusters) into a
-    # CUDA graph. The timed graph carries no profiling events (event nodes
-    # between launches break their programmatic overlap: measured 16 us per
-    # config (b) step); the per-launch roofline numerator comes from a second,
-    # profiled capture replayed after the timed region.
+    # API, every library launch incl. PDL edges, CTA-pair clusters and the
+    # NCCL shifts) into a CUDA graph. The timed graph carries no profiling
+    # events (event nodes between launches break their programmatic overlap);
+    # the per-launch roofline numerator comes from a second, profiled capture.
     def capture(profiled):
         _lib.lib.rtpb_profile_enable(1 if profiled else 0)
         _lib.lib.rtpb_profile_read(None, None, None, None, None, 1 << 30)  # drop older records
@@ -295,13 +428,13 @@ def main():
             step()
         stream.wait_stream(cs)
         n_launch = rtp.launch_count() - l0
-        for _ in range(3):
+        for _ in range(2):
             g_.replay()
         barrier()
         return g_, n_launch
 
     graph = None
-    graph_note = "eager (--eager)"
+    graph_note = "eager (--eager)" if graph_fallback is None else f"eager ({graph_fallback})"
     _lib.lib.rtpb_profile_enable(0)
     launches_per_step = None
     if not args.eager:
@@ -310,8 +443,10 @@ def main():
             graph_note = "CUDA graph replay of the captured step (no profiling events in the timed graph)"
         except Exception as exc:  # noqa
             graph = None
-            graph_note = f"eager (graph capture failed: {exc!r})"
+            graph_fallback = f"graph capture failed: {exc!r}"
+            graph_note = f"eager ({graph_fallback})"
             _lib.lib.rtpb_profile_enable(0)
+            barrier()
 
     # ---- timed region: exactly K steps, L2 flushed before each, CUDA events on the stream
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
@@ -334,8 +469,127 @@ def main():
         barrier()
     launches = (launches_per_step * args.steps) if graph is not None else rtp.launch_count() - launches0
     step_ms = [a.elapsed_time(b) for a, b in ev]
+    total_ms = allmax(sum(step_ms))
+    ms_per_step = total_ms / args.steps
+    value = fl_step / (ms_per_step * 1e-3) / 1e12  # whole-job aggregate over all GPUs
+    burst, sustained, peak_src = load_peaks()
 
     # ---- profiled pass (per-launch CUDA events on each launching stream), same L2 flush
+    roofline = {"bound": "tensor", "achieved": None, "peak": burst, "unit": "TFLOP/s", "frac": None,
+                "traffic": None}
+    if not args.no_profile:
+        roofline = profiled_roofline(args, torch, _lib, rtp, dev, stream, step, capture, graph, flush, flush_sink,
+                                     barrier, burst, sustained, peak_src)
+
+    # ---- memory: device ledger (params, grads, comm, activations, workspace) + caller tensors
+    led = grp.ledger(rank)
+    torch_peak = torch.cuda.max_memory_allocated(dev) - flush.numel() * 4
+    shard_w = sum(m.ffn1.shard_len() * 2 + m.ffn2.shard_len() * 2 for m in mlps)
+    shard_g = sum(m.ffn1.shard_len() * 4 + m.ffn2.shard_len() * 4 for m in mlps)
+    W_total, G_total = shard_w * ring, shard_g * ring
+    pgc = led["peak_param"] + led["peak_grad"] + led["peak_comm"]
+    model_in = (W_total + G_total) // ring
+    model_oop = (W_total + G_total + max(W_total, G_total)) // ring
+    mem = {"peak_hbm_bytes_per_gpu": led["peak_total"] + torch_peak,
+           "ledger_peak": {k[5:]: v for k, v in led.items() if k.startswith("peak_")},
+           "caller_activations_bytes": torch_peak,
+           "model_inplace_bytes": model_in, "model_outofplace_bytes": model_oop,
+           "param_grad_comm_bytes": pgc,
+           "param_grad_comm_vs_model": pgc / (model_oop if (args.mode == "outofplace" and ring > 1) else model_in),
+           "note": "model rows: the paper's (W+G)/N and (W+G+max(W,G))/N with bf16 W, fp32 G; out of place the "
+                   "spare is one W shard per layer (G moves in place, ring.cpp:314,328), so the measured "
+                   "Param+Grad+Comm sits below the W+G+max(W,G) row"}
+
+    # ---- exposed rotation time: T(step) - T(step without moving bytes)
+    exposed = {"ms_per_step": 0.0, "frac": 0.0, "method": "N=1: no rotation, nothing to expose"}
+    shift = None
+    if world > 1:
+        def eager_step_ms(k):
+            barrier()
+            a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a_.record(stream)
+            for _ in range(k):
+                step()
+            b_.record(stream)
+            barrier()
+            return allmax(a_.elapsed_time(b_) / k)
+        k = max(2, min(10, int(2000 / max(ms_per_step, 1e-3))))
+        t_with = eager_step_ms(k)
+        _lib.lib.rtpb_debug_skip_comm(1)
+        try:
+            step()
+            t_without = eager_step_ms(k)
+        finally:
+            _lib.lib.rtpb_debug_skip_comm(0)
+        exposed = {"ms_per_step": max(0.0, t_with - t_without), "frac": max(0.0, t_with - t_without) / t_with,
+                   "ms_step_eager": t_with, "ms_step_compute_only": t_without,
+                   "method": "eager steps with and without rtpb_debug_skip_comm (same schedule, no bytes moved), "
+                             "max over ranks"}
+        shift = measure_shift(torch, grp, mlps[0], stream, barrier, allmax, args.transport)
+    nvl_bw = 900e9  # NVLink 5 per direction per GPU
+    w_all = sum(m.ffn1.shard_len() + m.ffn2.shard_len() for m in mlps) * ring
+    sent = (ring - 1) / ring * (2 * w_all * 2 + w_all * 4) if ring > 1 else 0.0  # bf16 W fwd+bwd, fp32 G bwd
+    t_gemm_peak = fl_step / world / (burst * 1e12) * 1e3
+    t_nvl = sent / nvl_bw * 1e3
+    step_roofline = {"gemm_ms_at_peak": t_gemm_peak, "nvlink_ms": t_nvl, "bytes_sent_per_gpu": sent,
+                     "bound": "tensor" if t_gemm_peak >= t_nvl else "nvlink",
+                     "roofline_ms": max(t_gemm_peak, t_nvl), "frac": max(t_gemm_peak, t_nvl) / ms_per_step,
+                     "note": "north_star roofline: slower of the step's GEMM flops at the bf16 peak and its "
+                             "rotation bytes over NVLink (900 GB/s/direction)"}
+
+    # ---- e2e through the public API with host buffers (pinned), copies timed
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e_leg(torch, dev, stream, step, x, dy, dx, M, H, barrier, allmax, ms_per_step, fl_step,
+                          args.steps)
+
+    if rank == 0:
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline and not args.solo:
+            try:
+                cpu = cpu_reference(args.config, target_s=12.0)
+            except Exception as exc:  # noqa
+                cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "unavailable", "sample": repr(exc)}
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+                "scaling": "weak" if (TPG or args.tokens_per_gpu) else "strong",
+                "vs_baseline": None, "dtype": "bf16",
+                "data": "synthetic (uniform activations, Flyweight SplitMix64 weights, seed 42)",
+                "value_scope": "whole job: TFLOP/s summed over all n_gpus (per GPU: tflops_per_gpu)",
+                "config": {"workload": LABEL, "h": H, "f": F, "blocks": BLOCKS,
+                           "tokens_per_gpu": M, "global_tokens": T, "rotation_mode": args.mode,
+                           "parallelism": f"rtp{world}", "transport": args.transport if world > 1 else None,
+                           "same_device_test": bool(args.same_device and world > 1),
+                           "solo_ring": args.solo if args.solo > 1 else None,
+                           "l2": "flushed before every timed step (512 MiB written, then read back)",
+                           "flops_per_step": fl_step},
+                "tflops_per_gpu": value / world,
+                "parity_ok": parity_ok, "parity_check": parity_detail,
+                "gpu_launches": int(launches),
+                "step_execution": graph_note,
+                "eager_ms_per_step": eager_ms,
+                "roofline": roofline,
+                "step_roofline": step_roofline,
+                "exposed_comm": exposed,
+                "shift": shift,
+                "memory": mem,
+                "cpu_baseline": cpu,
+                "e2e": e2e,
+                "clocks": clocks.summary()}
+        print(json.dumps(line), flush=True)
+    for m in mlps:
+        m.close()
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def profiled_roofline(args, torch, _lib, rtp, dev, stream, step, capture, graph, flush, flush_sink, barrier,
+                      burst, sustained, peak_src):
+    """Per-launch GEMM timing from a separately profiled replay: algorithmic
+    FLOPs per launch (2*M*I*per per product) over each launch's CUDA-event
+    duration x its share of the SMs."""
+    import ctypes as C
     prof_graph = None
     if graph is not None:
         try:
@@ -345,7 +599,7 @@ def main():
     if prof_graph is None:
         _lib.lib.rtpb_profile_enable(1)
         _lib.lib.rtpb_profile_read(None, None, None, None, None, 1 << 30)
-    prof_steps = 5
+    prof_steps = 3
     pev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
     for i in range(prof_steps):
         flush.zero_()
@@ -361,13 +615,6 @@ def main():
     barrier()
     prof_step_ms = pev[0].elapsed_time(pev[1])
     _lib.lib.rtpb_profile_enable(0)
-    total_ms = sum(step_ms)
-    total_ms = allmax(total_ms)
-    ms_per_step = total_ms / args.steps
-    value = flops_per_step(T) / (ms_per_step * 1e-3) / 1e12  # whole-job aggregate
-
-    # ---- per-launch GEMM timing (the roofline numerator), last timed step
-    import ctypes as C
     cnt = _lib.lib.rtpb_profile_read(None, None, None, None, None, 0)
     kinds = (C.c_int * cnt)()
     fl = (C.c_double * cnt)()
@@ -392,7 +639,6 @@ def main():
         d[3] += m_ * sm_ / all_sms  # GPU-time: duration x share of the SMs the launch was sized for
     gemm_flops = sum(d[0] for d in per_kind.values())
     gemm_gpu_ms = sum(d[3] for d in per_kind.values())
-    # wall time with at least one step GEMM running (union of launch intervals)
     iv = sorted((t0, t0 + m_) for _, _, m_, t0, _ in recs)
     busy, cur_a, cur_b = 0.0, None, None
     for a_, b_ in iv:
@@ -404,188 +650,135 @@ def main():
             cur_b = max(cur_b, b_)
     if cur_b is not None:
         busy += cur_b - cur_a
-    burst, sustained, peak_src = load_peaks()
-    # achieved: algorithmic flops per unit of GPU time the GEMM launches held
-    # (duration x their share of the SMs: two GEMMs side by side on halves of
-    # the machine are each compared with half the peak)
     achieved = gemm_flops / (gemm_gpu_ms * 1e-3) / 1e12 if gemm_gpu_ms else 0.0
-    traffic = None
+    traffic, traffic_src = None, None
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
-            traffic = json.load(fh).get("dram_bytes_per_launch")
+            tj = json.load(fh)
+        entry = tj.get("configs", {}).get(args.config)
+        if entry:
+            traffic, traffic_src = entry.get("dram_bytes_per_launch"), entry.get("source")
     except Exception:
         pass
-    roofline = {"bound": "tensor", "achieved": achieved, "peak": burst, "unit": "TFLOP/s",
-                "frac": achieved / burst, "traffic": traffic,
-                "kernel": "rtp_gemm_kernel (tcgen05 step GEMMs: fwd, dgrad, wgrad)",
-                "peak_source": f"{peak_src} bf16 burst; sustained {sustained}",
-                "frac_of_sustained": achieved / sustained,
-                "achieved_over_gemm_wall": gemm_flops / (busy * 1e-3) / 1e12 if busy else None,
-                "gemm_busy_share_of_step": busy / prof_step_ms if prof_step_ms else None,
-                "profiled_step_ms": prof_step_ms,
-                "note": "per-launch numbers from a separately captured, profiled replay of the step (event "
-                        "nodes between launches cost ~16 us per step, so the timed graph has none)",
-                "per_kernel": {k: {"tflops_per_gpu_time": v[0] / (v[3] * 1e-3) / 1e12, "launches": v[2],
-                                   "avg_us": v[1] / v[2] * 1e3} for k, v in per_kind.items()},
-                "per_launch_in_step_order": per_launch}
+    if len(per_launch) > 24:  # keep the line readable: first block's launches + the last
+        shown = per_launch[:6] + per_launch[-3:]
+    else:
+        shown = per_launch
+    return {"bound": "tensor", "achieved": achieved, "peak": burst, "unit": "TFLOP/s",
+            "frac": achieved / burst, "traffic": traffic, "traffic_source": traffic_src,
+            "kernel": "rtp_gemm_kernel (tcgen05 step GEMMs: fwd, dgrad, wgrad)",
+            "peak_source": f"{peak_src} bf16 burst; sustained {sustained}",
+            "frac_of_sustained": achieved / sustained,
+            "achieved_over_gemm_wall": gemm_flops / (busy * 1e-3) / 1e12 if busy else None,
+            "gemm_busy_share_of_step": busy / prof_step_ms if prof_step_ms else None,
+            "profiled_step_ms": prof_step_ms, "launches_per_step": len(per_launch),
+            "note": "per-launch numbers from a separately captured, profiled replay of the step (event "
+                    "nodes between launches break programmatic overlap, so the timed graph has none)",
+            "per_kernel": {k: {"tflops_per_gpu_time": v[0] / (v[3] * 1e-3) / 1e12, "launches": v[2],
+                               "avg_us": v[1] / v[2] * 1e3} for k, v in per_kind.items()},
+            "per_launch_in_step_order": shown}
 
-    # ---- memory: device ledger (params, grads, comm, activations, workspace) + caller tensors
-    led = grp.ledger(rank)
-    torch_peak = torch.cuda.max_memory_allocated(dev) - flush.numel() * 4
-    shard_w = mlp.ffn1.shard_len() * 2 + mlp.ffn2.shard_len() * 2
-    shard_g = mlp.ffn1.shard_len() * 4 + mlp.ffn2.shard_len() * 4
-    W_total, G_total = shard_w * ring, shard_g * ring
-    mem = {"peak_hbm_bytes_per_gpu": led["peak_total"] + torch_peak,
-           "ledger_peak": {k[5:]: v for k, v in led.items() if k.startswith("peak_")},
-           "caller_activations_bytes": torch_peak,
-           "model_inplace_bytes": (W_total + G_total) // ring,
-           "model_outofplace_bytes": (W_total + G_total + max(W_total, G_total)) // ring,
-           "param_grad_comm_bytes": led["peak_param"] + led["peak_grad"] + led["peak_comm"]}
 
-    # ---- exposed rotation time: T(step) - T(step without moving bytes)
-    exposed = {"ms_per_step": 0.0, "frac": 0.0, "method": "N=1: no rotation, nothing to expose"}
-    if world > 1:
-        def eager_step_ms(k=10):
-            barrier()
-            a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a_.record(stream)
-            for _ in range(k):
-                step()
-            b_.record(stream)
-            barrier()
-            return allmax(a_.elapsed_time(b_) / k)
-        t_with = eager_step_ms()
-        _lib.lib.rtpb_debug_skip_comm(1)
-        try:
-            step()
-            t_without = eager_step_ms()
-        finally:
-            _lib.lib.rtpb_debug_skip_comm(0)
-        exposed = {"ms_per_step": max(0.0, t_with - t_without), "frac": max(0.0, t_with - t_without) / t_with,
-                   "ms_step_eager": t_with, "ms_step_compute_only": t_without,
-                   "method": "eager steps with and without rtpb_debug_skip_comm (same schedule, no bytes moved), "
-                             "max over ranks"}
-    nvl_bw = 900e9  # NVLink 5 per direction per GPU
-    w_all = (mlp.ffn1.shard_len() + mlp.ffn2.shard_len()) * ring
-    sent = (ring - 1) / ring * (2 * w_all * 2 + w_all * 4) if ring > 1 else 0.0  # bf16 W fwd+bwd, fp32 G bwd
-    t_gemm_peak = flops_per_step(T) / world / (burst * 1e12) * 1e3
-    t_nvl = sent / nvl_bw * 1e3
-    step_roofline = {"gemm_ms_at_peak": t_gemm_peak, "nvlink_ms": t_nvl, "bytes_sent_per_gpu": sent,
-                     "bound": "tensor" if t_gemm_peak >= t_nvl else "nvlink",
-                     "roofline_ms": max(t_gemm_peak, t_nvl), "frac": max(t_gemm_peak, t_nvl) / ms_per_step,
-                     "note": "north_star roofline: slower of the step's GEMM flops at the bf16 peak and its "
-                             "rotation bytes over NVLink (900 GB/s/direction)"}
-
-    # ---- e2e through the public API with host buffers (pinned), copies timed
-    e2e = None
-    if rank == 0 or world > 1:
-        # Training-loop shape: step i+1's inputs are copied host->device on a
-        # copy stream while step i computes, and step i's dX goes device->host
-        # on another while step i+1 computes (double-buffered). Every step's
-        # H2D and D2H happen inside the timed region.
-        hx = [x.cpu().pin_memory() for _ in range(2)]
-        hdy = [dy.cpu().pin_memory() for _ in range(2)]
-        hdx = [torch.empty(M, H, dtype=torch.bfloat16).pin_memory() for _ in range(2)]
-        xd = [torch.empty_like(x) for _ in range(2)]
-        dyd = [torch.empty_like(dy) for _ in range(2)]
-        dxd = [torch.empty_like(dx) for _ in range(2)]
-        # X and dY travel on two H2D streams (two copy engines in flight)
-        h2d, h2d_b, d2h = torch.cuda.Stream(dev), torch.cuda.Stream(dev), torch.cuda.Stream(dev)
-        EV = lambda: torch.cuda.Event()  # noqa: E731
-        e2e_steps = max(10, min(args.steps, 100))
-
-        def run_e2e(nsteps):
-            landed = [EV(), EV()]
-            computed = [EV(), EV()]
-            drained = [EV(), EV()]
-            done_with_inputs = [None, None]
-
-            landed_b = [EV(), EV()]
-
-            def issue_h2d(i):
-                b = i % 2
-                with torch.cuda.stream(h2d):
-                    if done_with_inputs[b] is not None:
-                        h2d.wait_event(done_with_inputs[b])  # step i-2 finished reading these buffers
-                    xd[b].copy_(hx[b], non_blocking=True)
-                    landed[b].record(h2d)
-                with torch.cuda.stream(h2d_b):
-                    if done_with_inputs[b] is not None:
-                        h2d_b.wait_event(done_with_inputs[b])
-                    dyd[b].copy_(hdy[b], non_blocking=True)
-                    landed_b[b].record(h2d_b)
-
-            h2d.wait_stream(stream)
-            h2d_b.wait_stream(stream)
-            d2h.wait_stream(stream)
-            issue_h2d(0)
-            for i in range(nsteps):
-                b = i % 2
-                if i + 1 < nsteps:
-                    issue_h2d(i + 1)
-                stream.wait_event(landed[b])
-                stream.wait_event(landed_b[b])
-                if i >= 2:
-                    stream.wait_event(drained[b])  # dxd[b] read back before it is overwritten
-                mlp.zero_grads()
-                mlp.forward([xd[b]], out=[y])
-                mlp.backward([dyd[b]], out=[dxd[b]])
-                computed[b].record(stream)
-                done_with_inputs[b] = computed[b]
-                with torch.cuda.stream(d2h):
-                    d2h.wait_event(computed[b])
-                    hdx[b].copy_(dxd[b], non_blocking=True)
-                    drained[b].record(d2h)
-            stream.wait_stream(d2h)
-            stream.wait_stream(h2d)
-            stream.wait_stream(h2d_b)
-
-        run_e2e(4)
+def measure_shift(torch, grp, mlp, stream, barrier, allmax, transport):
+    """One ring shift of the model's largest weight shard (out of place, into a
+    spare) and one counter-clockwise W+G shift, timed with CUDA events on the
+    caller's stream (the library orders its comm stream inside it), max over
+    ranks: NVLink GB/s sent per GPU against 900 GB/s per direction."""
+    ranks = grp.local_ranks
+    dev = grp.device_of(ranks[0])
+    L = mlp.ffn1.shard_len()
+    W = [torch.empty(L, dtype=torch.bfloat16, device=dev).normal_() for _ in ranks]
+    SP = [torch.empty_like(w) for w in W]
+    G = [torch.zeros(L, dtype=torch.float32, device=dev) for _ in ranks]
+    out = {"transport": transport, "shard_bytes": L * 2}
+    for name, kw, nbytes in (("cw_w_outofplace", dict(spares=SP, keep_spare=True), L * 2),
+                             ("ccw_wg_outofplace", dict(grads=G, spares=SP, keep_spare=True), L * 6)):
+        op = "cw" if name.startswith("cw") else "ccw"
+        grp.rotate(op, W, **kw)
         barrier()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        run_e2e(e2e_steps)
-        e1.record(stream)
+        iters = 10
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(iters):
+            grp.rotate(op, W, **kw)
+        b.record(stream)
         barrier()
-        e2e_ms = e0.elapsed_time(e1) / e2e_steps
-        e2e_ms = allmax(e2e_ms)
-        e2e = {"value": flops_per_step(T) / (e2e_ms * 1e-3) / 1e12, "unit": UNIT,
-               "h2d_bytes_per_step": 2 * M * H * 2, "d2h_bytes_per_step": M * H * 2, "ms_per_step": e2e_ms,
-               "path": "RtpMlp.forward/backward (C ABI, eager launches) from pinned host X, dY; dX read "
-                       "back; step i+1 H2D and step i-1 D2H overlap step i on copy streams"}
+        ms = allmax(a.elapsed_time(b) / iters)
+        out[name] = {"ms": ms, "bytes_sent_per_gpu": nbytes, "gbs": nbytes / (ms * 1e-3) / 1e9,
+                     "frac_of_nvlink_900": nbytes / (ms * 1e-3) / 900e9}
+    return out
 
-    if rank == 0:
-        cpu = None
-        if world == 1 and not args.no_cpu_baseline and not args.solo:
-            try:
-                cpu = cpu_reference(target_s=12.0)
-            except Exception as exc:  # noqa
-                cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "unavailable", "sample": repr(exc)}
-        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-                "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
-                "vs_baseline": None, "dtype": "bf16", "data": "synthetic (uniform activations, Flyweight "
-                                                             "SplitMix64 weights, seed 42)",
-                "config": {"workload": "rtp_mlp_768x3072x768 (config b)", "h": H, "f": F,
-                           "tokens_per_gpu": M, "global_tokens": T, "rotation_mode": args.mode,
-                           "parallelism": f"rtp{world}", "transport": args.transport if world > 1 else None,
-                           "same_device_test": bool(args.same_device and world > 1),
-                           "solo_ring": args.solo if args.solo > 1 else None, "l2": "flushed before every timed step (512 MiB written, then read back)",
-                           "flops_per_step": flops_per_step(T)},
-                "tflops_per_gpu": value / world,
-                "gpu_launches": int(launches),
-                "step_execution": graph_note,
-                "eager_ms_per_step": eager_ms,
-                "roofline": roofline,
-                "step_roofline": step_roofline,
-                "exposed_comm": exposed,
-                "memory": mem,
-                "cpu_baseline": cpu,
-                "e2e": e2e,
-                "clocks": clocks.summary()}
-        print(json.dumps(line), flush=True)
-    if world > 1:
-        dist.barrier()
-        dist.destroy_process_group()
+
+def run_e2e_leg(torch, dev, stream, step, x, dy, dx, M, H, barrier, allmax, ms_per_step, fl_step, steps):
+    """The same step through RtpMlp.forward/backward from pinned host X / dY
+    with dX read back, copies inside the timed region. Training-loop shape:
+    step i+1's inputs are copied host->device on copy streams while step i
+    computes, and step i's dX goes device->host on another while step i+1
+    computes (double-buffered)."""
+    hx = [x.cpu().pin_memory() for _ in range(2)]
+    hdy = [dy.cpu().pin_memory() for _ in range(2)]
+    hdx = [torch.empty(M, H, dtype=torch.bfloat16).pin_memory() for _ in range(2)]
+    xd = [torch.empty_like(x) for _ in range(2)]
+    dyd = [torch.empty_like(dy) for _ in range(2)]
+    dxd = [torch.empty_like(dx) for _ in range(2)]
+    h2d, h2d_b, d2h = torch.cuda.Stream(dev), torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    EV = lambda: torch.cuda.Event()  # noqa: E731
+    e2e_steps = max(5, min(steps, 100, int(4000 / max(ms_per_step, 1e-3))))
+
+    def run(nsteps):
+        landed, landed_b = [EV(), EV()], [EV(), EV()]
+        computed, drained = [EV(), EV()], [EV(), EV()]
+        done_with_inputs = [None, None]
+
+        def issue_h2d(i):
+            b = i % 2
+            with torch.cuda.stream(h2d):
+                if done_with_inputs[b] is not None:
+                    h2d.wait_event(done_with_inputs[b])  # step i-2 finished reading these buffers
+                xd[b].copy_(hx[b], non_blocking=True)
+                landed[b].record(h2d)
+            with torch.cuda.stream(h2d_b):
+                if done_with_inputs[b] is not None:
+                    h2d_b.wait_event(done_with_inputs[b])
+                dyd[b].copy_(hdy[b], non_blocking=True)
+                landed_b[b].record(h2d_b)
+
+        h2d.wait_stream(stream)
+        h2d_b.wait_stream(stream)
+        d2h.wait_stream(stream)
+        issue_h2d(0)
+        for i in range(nsteps):
+            b = i % 2
+            if i + 1 < nsteps:
+                issue_h2d(i + 1)
+            stream.wait_event(landed[b])
+            stream.wait_event(landed_b[b])
+            if i >= 2:
+                stream.wait_event(drained[b])  # dxd[b] read back before it is overwritten
+            step(xd[b], dyd[b], dxd[b])
+            computed[b].record(stream)
+            done_with_inputs[b] = computed[b]
+            with torch.cuda.stream(d2h):
+                d2h.wait_event(computed[b])
+                hdx[b].copy_(dxd[b], non_blocking=True)
+                drained[b].record(d2h)
+        stream.wait_stream(d2h)
+        stream.wait_stream(h2d)
+        stream.wait_stream(h2d_b)
+
+    run(2)
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    run(e2e_steps)
+    e1.record(stream)
+    barrier()
+    e2e_ms = allmax(e0.elapsed_time(e1) / e2e_steps)
+    return {"value": fl_step / (e2e_ms * 1e-3) / 1e12, "unit": UNIT,
+            "h2d_bytes_per_step": 2 * M * H * 2, "d2h_bytes_per_step": M * H * 2, "ms_per_step": e2e_ms,
+            "steps": e2e_steps,
+            "path": "RtpMlp.forward/backward over every block (C ABI, eager launches) from pinned host X, dY; "
+                    "dX read back; step i+1 H2D and step i-1 D2H overlap step i on copy streams"}
 
 
 if __name__ == "__main__":

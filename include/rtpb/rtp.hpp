@@ -261,7 +261,7 @@ class RtpLayerBase {
   void allocate_comm_spares();
   void release_comm_spares();
   bool has_comm_spares() const { return !spares_.empty(); }
-  void set_rotation_mode(RotationMode m) { rotation_mode_ = m; }
+  void set_rotation_mode(RotationMode m);
   RotationMode rotation_mode() const { return rotation_mode_; }
   // Logical id seen by (phase 0 fwd / 1 bwd, step, rank) in the last pass.
   const std::vector<int64_t>& trace() const { return trace_; }
@@ -274,6 +274,9 @@ class RtpLayerBase {
   void rotate_forward();
   void rotate_backward();
   void rehome_after_eval();
+  // Forgets a prefetched first shift (RtpLinear); called whenever the spare
+  // it landed in is replaced or the pass that would consume it fails.
+  virtual void drop_prefetch() {}
   bool oop() const { return rotation_mode_ == RotationMode::OutOfPlace && !spares_.empty(); }
 
   WorkerGroup* group_;
@@ -345,6 +348,9 @@ class RtpLinear : public RtpLayerBase {
  private:
   void build(size_t in_dim, size_t out_dim, size_t n);
   void ensure_scratch(size_t rows);
+  void drop_prefetch() override;
+  void forward_impl(std::span<const DView> x, size_t rows, std::span<const DView> y, Mode mode, const FwdEpi& e);
+  void backward_impl(std::span<const DView> dy, size_t rows, std::span<const DView> dx, const BwdEpi& e);
   // Shard-arrival flags (rtp_layers.cpp): forward W, backward W, backward G
   // blocks of the layer's flag range, indexed by the step the shard is for.
   static constexpr size_t kFlagFwd = 0, kFlagBwdW = 16, kFlagBwdG = 32;
@@ -393,14 +399,16 @@ class RtpMlp {
  private:
   RtpMlp* next_ = nullptr;
   RtpMlp* prev_ = nullptr;
-  void ensure_acts(size_t rows);
+  void ensure_acts(size_t rows, Mode mode);
   WorkerGroup* group_;
   size_t h_, f_;
   DType dtype_;
   RotationMode mode_ = RotationMode::InPlace;
   std::unique_ptr<RtpLinear> ffn1_, ffn2_;
-  std::vector<DeviceBuffer> pre_, act_, dpre_;  // per rank, rows x f (Activation)
-  size_t act_rows_ = 0;
+  std::vector<DeviceBuffer> pre_, act_;  // per rank, rows x f (Activation): the Train batch
+  std::vector<DeviceBuffer> eval_act_;   // per rank, rows x f: Eval forwards only
+  size_t act_rows_ = 0, eval_rows_ = 0;
+  size_t saved_rows_ = 0;  // rows of the Train forward backward will read (0: none)
   // N = 1 fused forward: unit schedule + row-block counters (Other), per rows.
   void ensure_fused(size_t rows);
   DeviceBuffer fused_ws_;

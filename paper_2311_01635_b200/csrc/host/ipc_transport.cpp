@@ -161,8 +161,29 @@ class IpcTransport final : public Transport {
     fn(rank_);
   }
 
+  // A peer that dies after publishing its buffer leaves this rank's comm
+  // stream in cuStreamWaitValue32 with no deadline: the group's host wait is
+  // polled instead (WorkerGroup::synchronize, RTPB_COMM_TIMEOUT_S — the
+  // reference's rendezvous timeout, ring.cpp:78-81), and on timeout abort()
+  // releases the device waits by raising this rank's own flags past any
+  // sequence number, then refuses further shifts.
+  bool polled() const override { return true; }
+  void abort() override {
+    if (aborted_) return;
+    aborted_ = true;
+    Worker& w = g_.worker(rank_);
+    DeviceGuard dg(w.device);
+    cudaStream_t st = nullptr;
+    if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) == cudaSuccess) {
+      cudaMemsetAsync(flags_.data(), 0xFF, 4 * sizeof(uint32_t), st);  // ready[2], done[2] := UINT32_MAX
+      cudaStreamSynchronize(st);
+      cudaStreamDestroy(st);
+    }
+  }
+
   void shift(Direction dir, std::span<void* const> send, std::span<void* const> recv, size_t bytes) override {
     if (n_ == 1 || bytes == 0) return;
+    if (aborted_) throw ProtocolError("IPC transport: aborted after a ring shift timed out");
     Worker& w = g_.worker(rank_);
     DeviceGuard dg(w.device);
     const size_t dst = ring_dest(rank_, n_, dir), src = ring_src(rank_, n_, dir);
@@ -263,6 +284,7 @@ class IpcTransport final : public Transport {
   std::map<std::pair<size_t, uint64_t>, void*> mapped_;  // (peer rank, buffer id) -> mapping
   uint32_t seq_[2] = {0, 0};
   uint64_t host_seq_ = 0;
+  bool aborted_ = false;
 };
 
 }  // namespace

@@ -84,7 +84,13 @@ DeviceBuffer::DeviceBuffer(int device, size_t bytes, MemoryLedger* ledger, MemCa
   // receive buffers). The ledger keeps the requested size.
   const size_t page = size_t(2) << 20;
   cuda_check(cudaMalloc(&ptr_, (bytes + page - 1) / page * page), "cudaMalloc");
-  if (zero) cuda_check(cudaMemset(ptr_, 0, bytes), "cudaMemset");
+  if (zero) {
+    // The worker streams are non-blocking: they do not order behind the legacy
+    // stream, so the fill completes here, before any stream can touch the
+    // buffer (split-K / bias-tick counters must read 0 on first use).
+    cuda_check(cudaMemsetAsync(ptr_, 0, bytes, cudaStreamLegacy), "cudaMemsetAsync");
+    cuda_check(cudaStreamSynchronize(cudaStreamLegacy), "zero fill");
+  }
   if (ledger_) ledger_->on_alloc(cat_, bytes_);
 }
 DeviceBuffer::~DeviceBuffer() { reset(); }

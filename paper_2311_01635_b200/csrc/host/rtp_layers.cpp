@@ -160,6 +160,11 @@ void RtpLayerBase::init_slots_alloc() {
 
 void RtpLayerBase::zero_grads() { grads_zero_pending_ = true; }
 
+void RtpLayerBase::set_rotation_mode(RotationMode m) {
+  if (m != rotation_mode_) drop_prefetch();
+  rotation_mode_ = m;
+}
+
 void RtpLayerBase::materialize_grads() {
   if (!grads_zero_pending_) return;
   group_->each([&](size_t r) {
@@ -201,6 +206,7 @@ void RtpLayerBase::check_backward_position(size_t rank, size_t step) const {
 }
 
 void RtpLayerBase::allocate_comm_spares() {
+  drop_prefetch();
   if (group_->size() == 1) return;  // no rotation, no buffer (layers_common.cpp:153-160)
   // One weight-shard-sized spare per worker, as the reference (shard_len
   // elements of the weight dtype): the incoming W lands there while the
@@ -214,6 +220,7 @@ void RtpLayerBase::allocate_comm_spares() {
 }
 
 void RtpLayerBase::release_comm_spares() {
+  drop_prefetch();
   group_->synchronize();
   spares_.clear();
 }
@@ -324,6 +331,16 @@ void RtpLinear::backward(std::span<const DView> dy, size_t rows, std::span<const
 
 void RtpLinear::forward_ex(std::span<const DView> x, size_t rows, std::span<const DView> y, Mode mode,
                            const FwdEpi& e) {
+  try {
+    forward_impl(x, rows, y, mode, e);
+  } catch (...) {
+    drop_prefetch();  // a prefetched first shift is not trusted after a failed pass
+    throw;
+  }
+}
+
+void RtpLinear::forward_impl(std::span<const DView> x, size_t rows, std::span<const DView> y, Mode mode,
+                             const FwdEpi& e) {
   require_home("forward");
   SmReserve sm_reserve(*group_);
   const auto& local = group_->local_ranks();
@@ -450,6 +467,26 @@ void RtpLinear::flagged_exchange(Direction dir, std::span<void* const> send, std
     }
 }
 
+// A first shift posted by prefetch_first_shift lives in the spare until its
+// pass consumes it. Anything that replaces or re-purposes the spare (release
+// / allocate, a rotation-mode switch, a failed pass) drops it, so the next
+// pass posts its own step-0 shift instead of computing on a stale spare. With
+// arrival flags the prefetched shift also raised its step-1 flag; it is
+// lowered once the shift has landed.
+void RtpLinear::drop_prefetch() {
+  if (!pre_fwd_ && !pre_bwd_) return;
+  group_->synchronize();
+  if (use_flags())
+    for (size_t r : group_->local_ranks()) {
+      Worker& w = group_->worker(r);
+      DeviceGuard dg(w.device);
+      if (pre_fwd_) cuda_check(cudaMemsetAsync(w.flag(flag_base_ + kFlagFwd + 1), 0, 4, w.comm), "drop prefetch");
+      if (pre_bwd_) cuda_check(cudaMemsetAsync(w.flag(flag_base_ + kFlagBwdW + 1), 0, 4, w.comm), "drop prefetch");
+      cuda_check(cudaStreamSynchronize(w.comm), "drop prefetch");
+    }
+  pre_fwd_ = pre_bwd_ = false;
+}
+
 void RtpLinear::prefetch_first_shift(bool backward) {
   const size_t n = group_->size();
   if (n < 2 || !oop() || (backward ? pre_bwd_ : pre_fwd_)) return;
@@ -509,6 +546,16 @@ void RtpLinear::end_backward_n1() {
 }
 
 void RtpLinear::backward_ex(std::span<const DView> dy, size_t rows, std::span<const DView> dx, const BwdEpi& e) {
+  try {
+    backward_impl(dy, rows, dx, e);
+  } catch (...) {
+    drop_prefetch();
+    throw;
+  }
+}
+
+void RtpLinear::backward_impl(std::span<const DView> dy, size_t rows, std::span<const DView> dx,
+                              const BwdEpi& e) {
   SmReserve sm_reserve(*group_);
   const auto& local = group_->local_ranks();
   if (dy.size() != local.size() || dx.size() != local.size())
@@ -761,19 +808,31 @@ void RtpMlp::zero_grads() {
   ffn2_->zero_grads();
 }
 
-void RtpMlp::ensure_acts(size_t rows) {
-  if (rows == act_rows_) return;
+void RtpMlp::ensure_acts(size_t rows, Mode mode) {
+  // Train forwards write the activations backward reads (pre, gelu(pre));
+  // Eval forwards only need gelu(pre) as ffn2's input and get their own
+  // buffer, so Train fwd -> Eval fwd -> backward still differentiates the
+  // Train batch (the reference caches pre/h only in Train mode, model.cpp:79-80).
+  const bool train = mode == Mode::Train;
+  size_t& have = train ? act_rows_ : eval_rows_;
+  if (rows == have) return;
   group_->synchronize();
   const size_t n = group_->size();
-  pre_.resize(n);
-  act_.resize(n);
+  auto& act = train ? act_ : eval_act_;
+  act.resize(n);
+  if (train) pre_.resize(n);
   group_->each([&](size_t r) {
     Worker& w = group_->worker(r);
     const size_t b = rows * f_ * dtype_size(dtype_);
-    pre_[r] = DeviceBuffer(w.device, b, &w.ledger, MemCategory::Activation, false);
-    act_[r] = DeviceBuffer(w.device, b, &w.ledger, MemCategory::Activation, false);
+    act[r] = DeviceBuffer();  // release before allocating: the ledger peak is the live set
+    act[r] = DeviceBuffer(w.device, b, &w.ledger, MemCategory::Activation, false);
+    if (train) {
+      pre_[r] = DeviceBuffer();
+      pre_[r] = DeviceBuffer(w.device, b, &w.ledger, MemCategory::Activation, false);
+    }
   });
-  act_rows_ = rows;
+  have = rows;
+  if (train) saved_rows_ = 0;  // the previous Train batch's activations are gone
 }
 
 void RtpMlp::ensure_fused(size_t rows) {
@@ -801,7 +860,14 @@ void RtpMlp::ensure_fused(size_t rows) {
 }
 
 void RtpMlp::forward(std::span<const DView> x, size_t rows, std::span<const DView> y, Mode mode) {
-  ensure_acts(rows);
+  // the layers' own require_home, checked before any activation buffer moves
+  if (!ffn1_->all_home()) throw StateError(ffn1_->label() + ": forward requires every slot at its home position");
+  if (!ffn2_->all_home()) throw StateError(ffn2_->label() + ": forward requires every slot at its home position");
+  ensure_acts(rows, mode);
+  const bool train = mode == Mode::Train;
+  auto& actb = train ? act_ : eval_act_;
+  auto& preb = train ? pre_ : eval_act_;  // Eval: pre is not stored (no STORE_PRE); the map needs a buffer
+  if (train) saved_rows_ = 0;  // set again once this forward has been issued
   if (group_->size() == 1 && dtype_ == DType::BF16 && !std::getenv("RTPB_NO_FUSED_FWD") &&
       n1_scheduling_pays(rows, h_, f_)) {
     // N = 1: no rotation between ffn1 and ffn2, so both GEMMs run as one
@@ -811,7 +877,7 @@ void RtpMlp::forward(std::span<const DView> x, size_t rows, std::span<const DVie
     const size_t r = group_->local_ranks()[0];
     ensure_fused(rows);
     const void* w1 = ffn1_->begin_forward_n1(x[0], rows, mode);
-    const void* w2 = ffn2_->begin_forward_n1({act_[r].data(), f_}, rows, mode);
+    const void* w2 = ffn2_->begin_forward_n1({actb[r].data(), f_}, rows, mode);
     Worker& w = group_->worker(r);
     int* base = static_cast<int*>(fused_ws_.data());
     unsigned* dep = reinterpret_cast<unsigned*>(base + fused_sched_ints_);
@@ -824,15 +890,16 @@ void RtpMlp::forward(std::span<const DView> x, size_t rows, std::span<const DVie
     FusedFwdWs ws{base, dep, dep + fused_dep_rows_, dep + fused_dep_rows_ + 1,
                   fused_splits2_ > 1 ? reinterpret_cast<float*>(reinterpret_cast<char*>(base) + fused_acc_off_)
                                      : nullptr};
-    check_status(fused_fwd_step(x[0].data, x[0].ld ? x[0].ld : h_, w1, pre_[r].data(), act_[r].data(), w2, y[0].data,
-                                y[0].ld ? y[0].ld : h_, rows, h_, f_, mode == Mode::Train, plan, ws, w.compute));
+    check_status(fused_fwd_step(x[0].data, x[0].ld ? x[0].ld : h_, w1, preb[r].data(), actb[r].data(), w2,
+                                y[0].data, y[0].ld ? y[0].ld : h_, rows, h_, f_, train, plan, ws, w.compute));
+    if (train) saved_rows_ = rows;
     return;
   }
   const auto& local = group_->local_ranks();
   std::vector<DView> pre(local.size()), act(local.size());
   for (size_t k = 0; k < local.size(); ++k) {
-    pre[k] = {pre_[local[k]].data(), f_};
-    act[k] = {act_[local[k]].data(), f_};
+    pre[k] = {preb[local[k]].data(), f_};
+    act[k] = {actb[local[k]].data(), f_};
   }
   // pre = ffn1(x); act = gelu(pre) fused into ffn1's epilogue (model.cpp:77-82)
   RtpLinear::FwdEpi e1;
@@ -847,6 +914,7 @@ void RtpMlp::forward(std::span<const DView> x, size_t rows, std::span<const DVie
   if (next_ && !std::getenv("RTPB_NO_PREFETCH"))
     e2.before_last_step = [&] { next_->ffn1_->prefetch_first_shift(false); };
   ffn2_->forward_ex(act, rows, y, mode, e2);  // model.cpp:83
+  if (train) saved_rows_ = rows;
 }
 
 RtpMlp::~RtpMlp() {
@@ -891,6 +959,11 @@ void RtpMlp::ensure_fused_bwd(size_t rows) {
 }
 
 void RtpMlp::backward(std::span<const DView> dy, size_t rows, std::span<const DView> dx) {
+  // the saved Train activations must be this batch's (model.cpp:99-105 reads pre_cache)
+  if (saved_rows_ == 0) throw StateError(ffn2_->label() + ": backward invoked without a matching forward");
+  if (saved_rows_ != rows)
+    throw DimensionError(ffn2_->label() + ": backward over " + std::to_string(rows) +
+                         " rows, the saved forward had " + std::to_string(saved_rows_));
   if (group_->size() == 1 && dtype_ == DType::BF16 && !std::getenv("RTPB_NO_FUSED_BWD") &&
       n1_scheduling_pays(rows, h_, f_)) {
     // N = 1: the four backward GEMMs as two concurrent scheduled launches
@@ -926,6 +999,7 @@ void RtpMlp::backward(std::span<const DView> dy, size_t rows, std::span<const DV
     ffn2_->end_backward_n1();
     ffn1_->end_backward_n1();
     group_->join_aux();
+    saved_rows_ = 0;
     return;
   }
   const auto& local = group_->local_ranks();
@@ -943,6 +1017,7 @@ void RtpMlp::backward(std::span<const DView> dy, size_t rows, std::span<const DV
     e1.before_last_step = [&] { prev_->ffn2_->prefetch_first_shift(true); };
   ffn1_->backward_ex(pre, rows, dx, e1);  // model.cpp:105
   group_->join_aux();
+  saved_rows_ = 0;
 }
 
 }  // namespace rtpb

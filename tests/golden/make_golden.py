@@ -90,6 +90,26 @@ def main():
             mlp[f"n{nn}_{k}"] = v
     out["mlp"] = mlp
 
+    # 4a. Ring self-check fixture for bench.py --gpus N (every N in {1,2,4,8}
+    #     meets the device's 8-column shard constraint: per = 64/8 at N=8).
+    #     The reference's in-place and out-of-place results are bitwise equal
+    #     (layers_test.cpp:343-365; asserted here), so one set serves both.
+    rows, h, f = 128, 64, 256
+    p = R.mlp_params(42, h, f, 1)
+    w1 = p[: h * f].reshape(h, f)
+    b1 = p[h * f: h * f + f]
+    w2 = p[h * f + f: h * f + f + f * h].reshape(f, h)
+    b2 = p[h * f + f + f * h:]
+    x, dy = acts(R, 42, rows, h, h)
+    ring_mlp = {"w1": w1, "b1": b1, "w2": w2, "b2": b2, "x": x, "dy": dy, "seed": 42}
+    for nn in (1, 2, 4, 8):
+        r = R.rtp_mlp(nn, w1, b1, w2, b2, x, dy, outofplace=True)
+        ri = R.rtp_mlp(nn, w1, b1, w2, b2, x, dy, outofplace=False)
+        assert all(np.array_equal(r[k], ri[k]) for k in r), "out-of-place != in-place"
+        for k, v in r.items():
+            ring_mlp[f"n{nn}_{k}"] = v
+    out["mlp_ring"] = ring_mlp
+
     # 4b. RtpAttention (layers_attention.cpp:43-198), heads split
     #     over N in {1,2,4}, sequences of 8, two per worker, both transports.
     #     Weights: one SplitMix64(42) stream, U[-0.1, 0.1], wq wk wv wo in order.
