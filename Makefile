@@ -20,8 +20,8 @@ CPP_SRC := $(wildcard $(CSRC)/host/*.cpp)
 OBJS    := $(patsubst $(CSRC)/%.cu,$(OBJDIR)/%.o,$(CU_SRC)) $(patsubst $(CSRC)/%.cpp,$(OBJDIR)/%.o,$(CPP_SRC))
 HDRS    := $(wildcard include/*.h include/rtpb/*.hpp $(CSRC)/kernels/*.cuh $(CSRC)/kernels/*.hpp $(CSRC)/host/*.hpp)
 
-.PHONY: all lib oracle clean
-all: lib oracle
+.PHONY: all lib oracle cpptest clean
+all: lib oracle cpptest
 lib: $(OUT)
 oracle:
 	$(MAKE) -s -C oracle oracle
@@ -38,6 +38,12 @@ $(OUT): $(OBJS)
 	@mkdir -p $(dir $@)
 	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -L$(NCCL_DIR)/lib -l:libnccl.so.2 \
 	    -Xlinker -rpath,$(NCCL_DIR)/lib -lpthread
+
+# The C++ drop-in test: a reference-style caller compiled against include/rtpb/rtp.hpp only.
+cpptest: build/dropin_test
+build/dropin_test: tests/cpp/dropin_test.cpp include/rtpb/rtp.hpp include/rtpb.h $(OUT)
+	@mkdir -p build
+	$(CXX) -std=c++20 -O1 -g -Wall -Wextra -Iinclude $< -o $@ -L$(PKG) -lrtpb -Wl,-rpath,'$$ORIGIN/../$(PKG)'
 
 clean:
 	rm -rf build $(PKG)/librtpb.so

@@ -45,6 +45,7 @@ extern "C" {
 
 #define RTPB_BF16 0
 #define RTPB_F32 1
+#define RTPB_F64 2 /* host-API tensors and rtpb_convert only; the step kernels take BF16 / F32 */
 
 /* Step-kernel epilogue flags (rtpb_fwd_step / rtpb_dgrad_step). */
 #define RTPB_EPI_GELU 1      /* fwd: also write gelu(pre) to `act` (model.cpp:80)       */
@@ -120,6 +121,11 @@ size_t rtpb_step_workspace_bytes(int which, int dtype, size_t M, size_t I, size_
 
 /* Exact-erf GELU and derivative (tensor.cpp:323-351), elementwise. */
 int rtpb_gelu(int dtype, const void* x, void* y, size_t count, void* stream);
+/* Elementwise dtype conversion dst[i] = (dst_dtype) src[i], one rounding (RN)
+ * from the value read; fill sets every element to v. The device half of
+ * rtpb::Tensor's conversions (the reference's Tensor is fp64, tensor.hpp). */
+int rtpb_convert(const void* src, int src_dtype, void* dst, int dst_dtype, size_t count, void* stream);
+int rtpb_fill(void* dst, int dtype, size_t count, double v, void* stream);
 int rtpb_gelu_backward(int dtype, const void* x, const void* upstream, void* out, size_t count, void* stream);
 
 /* Per-launch timing of the step GEMMs: when enabled, a CUDA event pair is

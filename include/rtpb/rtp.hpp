@@ -55,12 +55,35 @@ enum class Direction { Clockwise, CounterClockwise };
 // Solo: one rank of an n-rank ring with no peers (shifts skipped; measurement only).
 enum class TransportKind { Lockstep, Concurrent, Nccl, Ipc, Solo };
 enum class PayloadKind { Weight, WeightAndGrad };
-enum class DType { BF16 = RTPB_BF16, F32 = RTPB_F32 };
-inline size_t dtype_size(DType d) { return d == DType::F32 ? 4 : 2; }
+// Layers compute in BF16 or F32 (3xTF32); F64 is the reference's Tensor
+// element type (tensor.hpp), accepted at the Tensor API boundary.
+enum class DType { BF16 = RTPB_BF16, F32 = RTPB_F32, F64 = RTPB_F64 };
+inline size_t dtype_size(DType d) { return d == DType::F64 ? 8 : d == DType::F32 ? 4 : 2; }
+
+// ---- rng (rng.hpp:10-32): the fixtures' generator, host side ----
+class SplitMix64 {
+ public:
+  explicit SplitMix64(uint64_t seed) : state_(seed) {}
+  uint64_t next_u64() {
+    state_ += 0x9E3779B97F4A7C15ULL;
+    uint64_t z = state_;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+  }
+  double next_unit() { return static_cast<double>(next_u64() >> 11) * 0x1.0p-53; }
+  double next_uniform(double lo, double hi) { return lo + (hi - lo) * next_unit(); }
+  uint64_t next_index(uint64_t n) { return next_u64() % n; }
+
+ private:
+  uint64_t state_;
+};
 
 // ---- ledger (ledger.hpp:10-41), per worker, device bytes ----
 enum class MemCategory : uint8_t { Param, Grad, Activation, CommBuffer, Other };
 inline constexpr size_t kNumMemCategories = 5;
+
+const char* mem_category_name(MemCategory c);
 
 class MemoryLedger {
  public:
@@ -70,13 +93,42 @@ class MemoryLedger {
   size_t peak(MemCategory c) const { return peak_[size_t(c)]; }
   size_t current_total() const { return current_total_; }
   size_t peak_total() const { return peak_total_; }
-  void reset_peaks();
+  void reset();        // all counters to zero (ledger.cpp)
+  void reset_peaks();  // peaks down to the current bytes
+  // Every charge / release is also applied to `m` (WorkerGroup::bind_ledgers);
+  // the bytes already held are charged to it at binding. nullptr unbinds.
+  void mirror_to(MemoryLedger* m);
 
  private:
   std::array<size_t, kNumMemCategories> current_{};
   std::array<size_t, kNumMemCategories> peak_{};
   size_t current_total_ = 0;
   size_t peak_total_ = 0;
+  MemoryLedger* mirror_ = nullptr;
+};
+
+// RAII binding of the calling thread's Tensor allocations to a ledger +
+// category (ledger.hpp LedgerScope / CategoryScope); scopes nest.
+class LedgerScope {
+ public:
+  LedgerScope(MemoryLedger* ledger, MemCategory category);
+  ~LedgerScope();
+  LedgerScope(const LedgerScope&) = delete;
+  LedgerScope& operator=(const LedgerScope&) = delete;
+  static MemoryLedger* current_ledger();
+  static MemCategory current_category();
+
+ private:
+  MemoryLedger* prev_ledger_;
+  MemCategory prev_category_;
+};
+
+class CategoryScope {
+ public:
+  explicit CategoryScope(MemCategory category) : inner_(LedgerScope::current_ledger(), category) {}
+
+ private:
+  LedgerScope inner_;
 };
 
 // Owning device allocation charged to a worker ledger under one category
@@ -108,10 +160,86 @@ class DeviceBuffer {
   MemCategory cat_ = MemCategory::Other;
 };
 
+// ---- tensor (tensor.hpp): dense row-major DEVICE tensor ----
+// Owns one device allocation, charged to a ledger under one category: the
+// calling thread's LedgerScope at construction (as Tensor::register_bytes,
+// tensor.cpp:86-97), or an explicit ledger. Copies are deep (device-to-
+// device) and charge the copying thread's scope; moves keep the charge;
+// swap_data exchanges storage between equal-sized tensors without touching
+// either charge — how rotation moves shard contents (tensor.hpp:65-72).
+// Host access (at, to_host, from_host) synchronises and is for setup and tests.
+class Tensor {
+ public:
+  Tensor() = default;
+  // Zero-filled, on the current device.
+  explicit Tensor(std::vector<size_t> shape, DType dtype = DType::F64);
+  // On `device`, charged to `ledger` (may be null) under `cat`.
+  Tensor(std::vector<size_t> shape, DType dtype, int device, MemoryLedger* ledger, MemCategory cat,
+         bool zero = true);
+  Tensor(const Tensor& other);
+  Tensor& operator=(const Tensor& other);
+  Tensor(Tensor&&) noexcept = default;
+  Tensor& operator=(Tensor&&) noexcept = default;
+
+  static Tensor zeros(std::vector<size_t> shape, DType dtype = DType::F64) { return Tensor(std::move(shape), dtype); }
+  // Host values (fp64, row-major) rounded once to dtype, uploaded to `device` (-1: current).
+  static Tensor from_host(std::vector<size_t> shape, std::span<const double> values, DType dtype = DType::F64,
+                          int device = -1);
+  // Tensor::uniform (tensor.cpp:99-103): draws on the host, then uploads.
+  static Tensor uniform(std::vector<size_t> shape, SplitMix64& rng, double lo, double hi,
+                        DType dtype = DType::F64, int device = -1);
+
+  const std::vector<size_t>& shape() const { return shape_; }
+  size_t rank() const { return shape_.size(); }
+  size_t dim(size_t i) const { return shape_[i]; }
+  size_t numel() const;
+  size_t rows() const;  // rank-2 only
+  size_t cols() const;
+  DType dtype() const { return dtype_; }
+  size_t bytes() const { return buf_.bytes(); }
+  int device() const { return buf_.device(); }
+  bool empty() const { return buf_.empty(); }
+  void* data() const { return buf_.data(); }
+  std::string shape_str() const;
+
+  // Element i widened to fp64 (synchronous device read).
+  double at(size_t i) const;
+  double at(size_t i, size_t j) const { return at(i * shape_[1] + j); }
+  std::vector<double> to_host() const;
+  void fill(double v);                // device fill (synchronous)
+  Tensor to(DType dtype) const;       // converted copy (one RN rounding per element)
+  Tensor reshaped(std::vector<size_t> shape) const&;
+  Tensor reshaped(std::vector<size_t> shape) &&;
+  void reset() { buf_.reset(); shape_.clear(); }
+
+  friend void swap_data(Tensor& a, Tensor& b);
+
+ private:
+  std::vector<size_t> shape_;
+  DType dtype_ = DType::F64;
+  DeviceBuffer buf_;
+};
+
+// ---- partition (partition.hpp:44-60) ----
+enum class PartitionStrategy { OutputPartition, HeadPartition, ExpertPartition };
+struct ShardRange {
+  size_t begin = 0;
+  size_t end = 0;
+  size_t extent() const { return end - begin; }
+};
+struct ShardLayout {
+  PartitionStrategy strategy = PartitionStrategy::OutputPartition;
+  size_t n_shards = 1;
+  std::vector<ShardRange> ranges;
+};
+// Columns of the weight (output features) plus the matching bias slice;
+// ConfigError unless out_dim % n == 0 (partition.cpp:58-69).
+ShardLayout layout_linear(size_t in_dim, size_t out_dim, size_t n);
+
 // ---- ring (ring.hpp:23-46) ----
 struct ShardSlot {
-  DeviceBuffer weight;    // [W_j : I x per | b_j : per] in the layer dtype
-  DeviceBuffer grad_acc;  // same element layout, fp32
+  Tensor weight;    // [W_j : I x per | b_j : per] in the layer dtype
+  Tensor grad_acc;  // same element layout, fp32
   size_t logical_id = 0;
   long rotation_offset = 0;
 };
@@ -159,12 +287,15 @@ class WorkerGroup {
                         std::string_view label = {}, size_t shard_elems = 0);
   void rotate_counterclockwise(std::span<ShardSlot> slots, PayloadKind kind = PayloadKind::WeightAndGrad,
                                std::string_view label = {}, size_t shard_elems = 0);
-  void rotate_outofplace(std::span<ShardSlot> slots, std::span<DeviceBuffer> spares, Direction dir,
+  void rotate_outofplace(std::span<ShardSlot> slots, std::span<Tensor> spares, Direction dir,
                          PayloadKind kind = PayloadKind::Weight, std::string_view label = {},
                          size_t shard_elems = 0);
   // ring_allgather (ring.cpp:335-376): out[r] holds all n chunks in canonical order.
   void ring_allgather(std::span<void* const> in, std::span<void* const> out, size_t bytes,
                       std::string_view label = {}, size_t elem_size = 1);
+  // Reference signature: every local worker ends with the n shards
+  // concatenated in canonical order.
+  std::vector<Tensor> ring_allgather(std::span<const Tensor> shards, std::string_view label = {});
 
   // Lower-level pieces used by the layers' overlap scheduler.
   // Raw ring shift of per-local-rank buffers: recv[dest(r)] <- send[r];
@@ -188,9 +319,18 @@ class WorkerGroup {
   enum class Corrupt { None, Tag, ShardId };
   void corrupt_next_exchange(size_t rank, Corrupt what);
 
+  // Per-worker device ledger (every allocation the library makes for the
+  // worker is charged to it).
   MemoryLedger& ledger_of(size_t rank);
+  // ring.hpp:69-71: caller-owned per-rank ledgers. Each local worker's ledger
+  // is mirrored into ledgers[rank] (bytes already held are charged at
+  // binding), and each() runs its thunks under LedgerScope(ledgers[rank],
+  // Activation), so Tensors the thunks create are charged there too.
+  void bind_ledgers(std::vector<MemoryLedger*> ledgers);
+  MemoryLedger* bound_ledger(size_t rank) const;
 
  private:
+  std::vector<MemoryLedger*> bound_;
   friend class Transport;
   size_t n_;
   TransportKind kind_;
@@ -283,7 +423,7 @@ class RtpLayerBase {
   std::string label_;
   DType dtype_;
   std::vector<ShardSlot> slots_;  // indexed by rank (remote entries stay empty)
-  std::vector<DeviceBuffer> spares_;
+  std::vector<Tensor> spares_;
   size_t shard_len_ = 0;
   size_t flag_base_ = 0;  // this layer's block of the workers' shard-arrival flags
   RotationMode rotation_mode_ = RotationMode::InPlace;
@@ -301,10 +441,24 @@ class RtpLinear : public RtpLayerBase {
   // starting at stream index stream_base; the full weight never exists.
   RtpLinear(WorkerGroup& group, std::string label, size_t in_dim, size_t out_dim, size_t n, uint64_t seed,
             uint64_t stream_base, DType dtype = DType::BF16);
+  // The reference's constructor (layers.hpp:133-134): weight (in x out) and
+  // bias (out) as Tensors of any dtype; the layer computes in BF16 for a BF16
+  // weight, else in F32 (3xTF32) — an F64 weight (the reference's type)
+  // selects the fp32 mode, the tolerance-1e-5 path.
+  RtpLinear(WorkerGroup& group, std::string label, const Tensor& weight, const Tensor& bias, size_t n);
 
   size_t in_dim() const { return in_; }
   size_t out_dim() const { return out_; }
   size_t per() const { return per_; }
+  const ShardLayout& layout() const { return layout_; }
+
+  // Reference signatures (layers.hpp:138-139). x: one (rows x in) Tensor per
+  // local worker (all n in-process; the own rank under NCCL / IPC), on the
+  // worker's device, any dtype (converted to the layer dtype). Returns
+  // (rows x out) per local worker in the layer dtype, charged to the worker's
+  // ledger as Activation. Train keeps a copy of X for backward (x_cache_).
+  std::vector<Tensor> forward(std::span<const Tensor> x, Mode mode);
+  std::vector<Tensor> backward(std::span<const Tensor> dy);
 
   // x[k] / y[k]: activations of local rank k (rows x in / rows x out).
   void forward(std::span<const DView> x, size_t rows, std::span<const DView> y, Mode mode);
@@ -347,6 +501,7 @@ class RtpLinear : public RtpLayerBase {
 
  private:
   void build(size_t in_dim, size_t out_dim, size_t n);
+  void upload_shards(const double* weight, const double* bias);
   void ensure_scratch(size_t rows);
   void drop_prefetch() override;
   void forward_impl(std::span<const DView> x, size_t rows, std::span<const DView> y, Mode mode, const FwdEpi& e);
@@ -361,6 +516,8 @@ class RtpLinear : public RtpLayerBase {
                         size_t flag);
 
   size_t in_ = 0, out_ = 0, per_ = 0;
+  ShardLayout layout_;
+  std::vector<Tensor> x_keep_;  // Tensor API: X (layer dtype) held from Train forward to backward
   std::vector<ReplayTape<Empty>> tapes_;
   std::vector<DView> x_cache_;          // per rank: caller-owned X kept for backward
   std::vector<DeviceBuffer> dx_acc_;    // per rank: fp32 cross-step dX accumulator
@@ -383,6 +540,10 @@ class RtpMlp {
   void zero_grads();
   void forward(std::span<const DView> x, size_t rows, std::span<const DView> y, Mode mode);
   void backward(std::span<const DView> dy, size_t rows, std::span<const DView> dx);
+  // Tensor API (the shapes of model.cpp:77-105's block): one (rows x h)
+  // Tensor per local worker in, one out.
+  std::vector<Tensor> forward(std::span<const Tensor> x, Mode mode);
+  std::vector<Tensor> backward(std::span<const Tensor> dy);
   RtpLinear& ffn1() { return *ffn1_; }
   RtpLinear& ffn2() { return *ffn2_; }
   // Stack order (RtpModel's block sequence, model.cpp:77-83 / 99-105): `next`
@@ -407,6 +568,7 @@ class RtpMlp {
   std::unique_ptr<RtpLinear> ffn1_, ffn2_;
   std::vector<DeviceBuffer> pre_, act_;  // per rank, rows x f (Activation): the Train batch
   std::vector<DeviceBuffer> eval_act_;   // per rank, rows x f: Eval forwards only
+  std::vector<Tensor> x_keep_;           // Tensor API: X held from Train forward to backward
   size_t act_rows_ = 0, eval_rows_ = 0;
   size_t saved_rows_ = 0;  // rows of the Train forward backward will read (0: none)
   // N = 1 fused forward: unit schedule + row-block counters (Other), per rows.

@@ -398,6 +398,20 @@ int rtpb_gelu(int dtype, const void* x, void* y, size_t count, void* stream) {
   return gelu_fwd(dtype == RTPB_F32, x, y, count, as_stream(stream));
 }
 
+int rtpb_convert(const void* src, int src_dtype, void* dst, int dst_dtype, size_t count, void* stream) {
+  auto ok = [](int d) { return d == RTPB_BF16 || d == RTPB_F32 || d == RTPB_F64; };
+  if (!ok(src_dtype) || !ok(dst_dtype)) return set_error(RTPB_ERR_CONFIG, "rtpb_convert: unknown dtype");
+  if (count && (!src || !dst)) return set_error(RTPB_ERR_DIMENSION, "rtpb_convert: null buffer");
+  return convert(src, src_dtype, dst, dst_dtype, count, as_stream(stream));
+}
+
+int rtpb_fill(void* dst, int dtype, size_t count, double v, void* stream) {
+  if (dtype != RTPB_BF16 && dtype != RTPB_F32 && dtype != RTPB_F64)
+    return set_error(RTPB_ERR_CONFIG, "rtpb_fill: unknown dtype");
+  if (count && !dst) return set_error(RTPB_ERR_DIMENSION, "rtpb_fill: null buffer");
+  return fill(dst, dtype, count, v, as_stream(stream));
+}
+
 int rtpb_gelu_backward(int dtype, const void* x, const void* upstream, void* out, size_t count, void* stream) {
   return gelu_bwd(dtype == RTPB_F32, x, upstream, out, count, as_stream(stream));
 }

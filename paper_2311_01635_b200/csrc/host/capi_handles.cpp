@@ -362,7 +362,7 @@ int rtpb_linear_read_shard(rtpb_linear l, size_t rank, int which, void* dst) {
       l->l->materialize_grads();
       G.synchronize();
     }
-    const DeviceBuffer& b = which ? l->l->slots()[rank].grad_acc : l->l->slots()[rank].weight;
+    const Tensor& b = which ? l->l->slots()[rank].grad_acc : l->l->slots()[rank].weight;
     cuda_check(cudaMemcpy(dst, b.data(), b.bytes(), cudaMemcpyDeviceToDevice), "read_shard");
   });
 }

@@ -63,14 +63,30 @@ void MemoryLedger::on_alloc(MemCategory c, size_t bytes) {
   peak_[i] = std::max(peak_[i], current_[i]);
   current_total_ += bytes;
   peak_total_ = std::max(peak_total_, current_total_);
+  if (mirror_) mirror_->on_alloc(c, bytes);
 }
 void MemoryLedger::on_release(MemCategory c, size_t bytes) {
   current_[size_t(c)] -= bytes;
   current_total_ -= bytes;
+  if (mirror_) mirror_->on_release(c, bytes);
+}
+void MemoryLedger::reset() {
+  current_.fill(0);
+  peak_.fill(0);
+  current_total_ = 0;
+  peak_total_ = 0;
 }
 void MemoryLedger::reset_peaks() {
   peak_ = current_;
   peak_total_ = current_total_;
+}
+void MemoryLedger::mirror_to(MemoryLedger* m) {
+  if (mirror_)
+    for (size_t c = 0; c < kNumMemCategories; ++c) mirror_->on_release(MemCategory(c), current_[c]);
+  mirror_ = m;
+  if (mirror_)
+    for (size_t c = 0; c < kNumMemCategories; ++c)
+      if (current_[c]) mirror_->on_alloc(MemCategory(c), current_[c]);
 }
 
 // ------------------------------------------------------------------ buffers
@@ -528,7 +544,27 @@ Worker& WorkerGroup::worker(size_t rank) {
 
 MemoryLedger& WorkerGroup::ledger_of(size_t rank) { return worker(rank).ledger; }
 
-void WorkerGroup::each(const std::function<void(size_t)>& fn) { transport_->each(fn); }
+void WorkerGroup::each(const std::function<void(size_t)>& fn) {
+  if (bound_.empty()) {
+    transport_->each(fn);
+    return;
+  }
+  // bind_ledgers: thunks allocate under the rank's ledger (ring.cpp each())
+  transport_->each([&](size_t r) {
+    LedgerScope scope(bound_[r], MemCategory::Activation);
+    fn(r);
+  });
+}
+
+void WorkerGroup::bind_ledgers(std::vector<MemoryLedger*> ledgers) {
+  if (!ledgers.empty() && ledgers.size() != n_)
+    throw ConfigError("bind_ledgers: got " + std::to_string(ledgers.size()) + " ledgers for " + std::to_string(n_) +
+                      " workers");
+  for (size_t r : local_) worker(r).ledger.mirror_to(ledgers.empty() ? nullptr : ledgers[r]);
+  bound_ = std::move(ledgers);
+}
+
+MemoryLedger* WorkerGroup::bound_ledger(size_t rank) const { return bound_.empty() ? nullptr : bound_.at(rank); }
 
 std::atomic<int> g_skip_comm{0};
 
@@ -619,6 +655,9 @@ void WorkerGroup::advance_slots(std::span<ShardSlot> slots, Direction dir, Paylo
   if (slots.size() != n_)
     throw ConfigError("rotate: got " + std::to_string(slots.size()) + " slots for " + std::to_string(n_) +
                       " workers");
+  // traffic volume per worker: the resident shard's element count unless the
+  // caller states it (ring.cpp record())
+  if (!shard_elems) shard_elems = slots[local_[0]].weight.numel();
   const uint64_t tag = tag_++;
   const long hop = dir == Direction::Clockwise ? +1 : -1;
   const Corrupt what = corrupt_;
@@ -697,7 +736,7 @@ void WorkerGroup::rotate_counterclockwise(std::span<ShardSlot> slots, PayloadKin
   advance_slots(slots, Direction::CounterClockwise, kind, label, shard_elems);
 }
 
-void WorkerGroup::rotate_outofplace(std::span<ShardSlot> slots, std::span<DeviceBuffer> spares, Direction dir,
+void WorkerGroup::rotate_outofplace(std::span<ShardSlot> slots, std::span<Tensor> spares, Direction dir,
                                     PayloadKind kind, std::string_view label, size_t shard_elems) {
   if (slots.size() != n_ || spares.size() != n_)
     throw ConfigError("rotate_outofplace: slot/spare counts do not match worker count");
@@ -748,6 +787,25 @@ void WorkerGroup::ring_allgather(std::span<void* const> in, std::span<void* cons
     traffic_.push_back({std::string(label), "allgather", bytes / elem_size, 0});
   }
   compute_after_comm();
+}
+
+std::vector<Tensor> WorkerGroup::ring_allgather(std::span<const Tensor> shards, std::string_view label) {
+  if (shards.size() != n_) throw ConfigError("ring_allgather: got wrong number of shards");
+  const Tensor& t0 = shards[local_[0]];
+  std::vector<Tensor> out(n_);
+  std::vector<void*> in(n_, nullptr), op(n_, nullptr);
+  for (size_t r : local_) {
+    if (shards[r].bytes() != t0.bytes() || shards[r].dtype() != t0.dtype())
+      throw DimensionError("ring_allgather: shards differ in size or dtype");
+    Worker& w = worker(r);
+    MemoryLedger* l = bound_.empty() ? LedgerScope::current_ledger() : bound_[r];
+    out[r] = Tensor({n_ * t0.numel()}, t0.dtype(), w.device, l, MemCategory::Activation, false);
+    in[r] = shards[r].data();
+    op[r] = out[r].data();
+  }
+  ring_allgather(in, op, t0.bytes(), label, dtype_size(t0.dtype()));
+  synchronize();
+  return out;
 }
 
 }  // namespace rtpb

@@ -151,8 +151,8 @@ void RtpLayerBase::init_slots_alloc() {
   group_->each([&](size_t r) {
     Worker& w = group_->worker(r);
     ShardSlot& s = slots_[r];
-    s.weight = DeviceBuffer(w.device, shard_len_ * dtype_size(dtype_), &w.ledger, MemCategory::Param, false);
-    s.grad_acc = DeviceBuffer(w.device, shard_len_ * sizeof(float), &w.ledger, MemCategory::Grad, true);
+    s.weight = Tensor({shard_len_}, dtype_, w.device, &w.ledger, MemCategory::Param, false);
+    s.grad_acc = Tensor({shard_len_}, DType::F32, w.device, &w.ledger, MemCategory::Grad, true);
     s.logical_id = r;
     s.rotation_offset = 0;
   });
@@ -212,10 +212,9 @@ void RtpLayerBase::allocate_comm_spares() {
   // elements of the weight dtype): the incoming W lands there while the
   // resident W is still read; gradients move in place (ring.cpp:314,328).
   spares_.resize(group_->size());
-  const size_t bytes = shard_len_ * dtype_size(dtype_);
   group_->each([&](size_t r) {
     Worker& w = group_->worker(r);
-    spares_[r] = DeviceBuffer(w.device, bytes, &w.ledger, MemCategory::CommBuffer, false);
+    spares_[r] = Tensor({shard_len_}, dtype_, w.device, &w.ledger, MemCategory::CommBuffer, false);
   });
 }
 
@@ -250,11 +249,7 @@ void RtpLinear::build(size_t in_dim, size_t out_dim, size_t n) {
   if (n != group_->size())
     throw ConfigError("RtpLinear: n = " + std::to_string(n) + " does not match the group of " +
                       std::to_string(group_->size()));
-  if (n == 0) throw ConfigError("layout_linear: shard count must be >= 1");
-  if (in_dim == 0 || out_dim == 0) throw ConfigError("layout_linear: dimensions must be positive");
-  if (out_dim % n != 0)
-    throw ConfigError("layout_linear: out_dim " + std::to_string(out_dim) + " not divisible by " +
-                      std::to_string(n) + " shards; choose out_dim as a multiple of the worker count");
+  layout_ = layout_linear(in_dim, out_dim, n);  // ConfigError with the reference's "multiple" hint
   in_ = in_dim;
   out_ = out_dim;
   per_ = out_dim / n;
@@ -274,9 +269,15 @@ RtpLinear::RtpLinear(WorkerGroup& group, std::string label, const double* weight
                      size_t in_dim, size_t out_dim, size_t n, DType dtype)
     : RtpLayerBase(group, std::move(label), dtype) {
   build(in_dim, out_dim, n);
-  // linear_shard_groups + flatten_shards + shard_view (layers_common.cpp:33-45):
-  // shard r = [W[:, r*per:(r+1)*per] row-major | b[r*per:(r+1)*per]].
+  upload_shards(weight, bias);
+}
+
+// linear_shard_groups + flatten_shards + shard_view (layers_common.cpp:33-45):
+// shard r = [W[:, r*per:(r+1)*per] row-major | b[r*per:(r+1)*per]].
+void RtpLinear::upload_shards(const double* weight, const double* bias) {
   group_->each([&](size_t r) {
+    Worker& w = group_->worker(r);
+    DeviceGuard dg(w.device);
     std::vector<double> host(shard_len_);
     for (size_t i = 0; i < in_; ++i)
       std::memcpy(&host[i * per_], weight + i * out_ + r * per_, per_ * sizeof(double));
@@ -291,6 +292,101 @@ RtpLinear::RtpLinear(WorkerGroup& group, std::string label, const double* weight
       cuda_check(cudaMemcpy(slots_[r].weight.data(), h.data(), h.size() * 2, cudaMemcpyHostToDevice), "upload");
     }
   });
+}
+
+namespace {
+DType layer_dtype_of(const Tensor& weight) { return weight.dtype() == DType::BF16 ? DType::BF16 : DType::F32; }
+}  // namespace
+
+RtpLinear::RtpLinear(WorkerGroup& group, std::string label, const Tensor& weight, const Tensor& bias, size_t n)
+    : RtpLayerBase(group, std::move(label), layer_dtype_of(weight)) {
+  if (weight.rank() != 2) throw DimensionError(label_ + ": weight must be rank 2 (in x out), got " + weight.shape_str());
+  if (bias.rank() != 1 || bias.dim(0) != weight.cols())
+    throw DimensionError(label_ + ": bias of shape " + bias.shape_str() + " does not match weight " +
+                         weight.shape_str());
+  build(weight.rows(), weight.cols(), n);
+  const std::vector<double> w = weight.to_host(), b = bias.to_host();
+  upload_shards(w.data(), b.data());
+}
+
+// ---- Tensor API (layers.hpp:138-139) over the device-view passes ----
+namespace {
+// x holds either one tensor per rank (n, all local) or one per local rank.
+std::vector<const Tensor*> per_local(WorkerGroup& g, std::span<const Tensor> x, const std::string& label,
+                                     const char* what) {
+  const auto& local = g.local_ranks();
+  std::vector<const Tensor*> out(local.size());
+  if (x.size() == g.size() && local.size() == g.size()) {
+    for (size_t k = 0; k < local.size(); ++k) out[k] = &x[local[k]];
+  } else if (x.size() == local.size()) {
+    for (size_t k = 0; k < local.size(); ++k) out[k] = &x[k];
+  } else {
+    throw DimensionError(label + ": " + what + " expects " + std::to_string(local.size()) +
+                         " tensors (one per local worker), got " + std::to_string(x.size()));
+  }
+  return out;
+}
+
+// The input for local rank r in the layer dtype on the worker's device:
+// `keep` receives a converted copy (or a plain copy when keep_same is set).
+const Tensor& as_layer_input(const Tensor& t, DType dt, Worker& w, size_t cols, const std::string& label,
+                             Tensor& keep, bool keep_same) {
+  if (t.rank() != 2 || t.cols() != cols)
+    throw DimensionError(label + ": activation of shape " + t.shape_str() + " does not have " +
+                         std::to_string(cols) + " columns");
+  if (t.device() != w.device)
+    throw DimensionError(label + ": activation on device " + std::to_string(t.device()) + ", worker " +
+                         std::to_string(w.rank) + " runs on device " + std::to_string(w.device));
+  if (t.dtype() == dt && !keep_same) return t;
+  LedgerScope scope(&w.ledger, MemCategory::Activation);
+  keep = t.to(dt);
+  return keep;
+}
+}  // namespace
+
+std::vector<Tensor> RtpLinear::forward(std::span<const Tensor> x, Mode mode) {
+  const auto& local = group_->local_ranks();
+  auto xs = per_local(*group_, x, label_, "forward");
+  const size_t rows = xs[0]->rank() == 2 ? xs[0]->rows() : 0;
+  std::vector<Tensor> tmp(local.size()), ys(local.size());
+  std::vector<DView> xv(local.size()), yv(local.size());
+  const bool train = mode == Mode::Train;
+  if (train) x_keep_.assign(group_->size(), Tensor());
+  for (size_t k = 0; k < local.size(); ++k) {
+    Worker& w = group_->worker(local[k]);
+    Tensor& keep = train ? x_keep_[local[k]] : tmp[k];
+    const Tensor& xin = as_layer_input(*xs[k], dtype_, w, in_, label_, keep, train);  // x_cache_ is a copy
+    if (xin.rows() != rows) throw DimensionError(label_ + ": workers' activations differ in row count");
+    ys[k] = Tensor({rows, out_}, dtype_, w.device, &w.ledger, MemCategory::Activation, false);
+    xv[k] = {xin.data(), in_};
+    yv[k] = {ys[k].data(), out_};
+  }
+  forward(xv, rows, yv, mode);
+  group_->synchronize();  // the reference returns completed tensors
+  return ys;
+}
+
+std::vector<Tensor> RtpLinear::backward(std::span<const Tensor> dy) {
+  const auto& local = group_->local_ranks();
+  auto ds = per_local(*group_, dy, label_, "backward");
+  const size_t rows = ds[0]->rank() == 2 ? ds[0]->rows() : 0;
+  std::vector<Tensor> tmp(local.size()), dxs(local.size());
+  std::vector<DView> dv(local.size()), xv(local.size());
+  for (size_t k = 0; k < local.size(); ++k) {
+    Worker& w = group_->worker(local[k]);
+    const Tensor& din = as_layer_input(*ds[k], dtype_, w, out_, label_, tmp[k], false);
+    if (din.rows() != rows) throw DimensionError(label_ + ": workers' gradients differ in row count");
+    dxs[k] = Tensor({rows, in_}, dtype_, w.device, &w.ledger, MemCategory::Activation, false);
+    dv[k] = {din.data(), out_};
+    xv[k] = {dxs[k].data(), in_};
+  }
+  if (!x_keep_.empty() && x_keep_[local[0]].empty() == false && x_keep_[local[0]].rows() != rows)
+    throw DimensionError(label_ + ": backward over " + std::to_string(rows) + " rows, forward saw " +
+                         std::to_string(x_keep_[local[0]].rows()));
+  backward(dv, rows, xv);
+  group_->synchronize();
+  x_keep_.clear();  // layers_linear.cpp:69
+  return dxs;
 }
 
 RtpLinear::RtpLinear(WorkerGroup& group, std::string label, size_t in_dim, size_t out_dim, size_t n,
@@ -1018,6 +1114,48 @@ void RtpMlp::backward(std::span<const DView> dy, size_t rows, std::span<const DV
   ffn1_->backward_ex(pre, rows, dx, e1);  // model.cpp:105
   group_->join_aux();
   saved_rows_ = 0;
+}
+
+std::vector<Tensor> RtpMlp::forward(std::span<const Tensor> x, Mode mode) {
+  const auto& local = group_->local_ranks();
+  auto xs = per_local(*group_, x, ffn1_->label(), "forward");
+  const size_t rows = xs[0]->rank() == 2 ? xs[0]->rows() : 0;
+  std::vector<Tensor> tmp(local.size()), ys(local.size());
+  std::vector<DView> xv(local.size()), yv(local.size());
+  const bool train = mode == Mode::Train;
+  if (train) x_keep_.assign(group_->size(), Tensor());
+  for (size_t k = 0; k < local.size(); ++k) {
+    Worker& w = group_->worker(local[k]);
+    Tensor& keep = train ? x_keep_[local[k]] : tmp[k];
+    const Tensor& xin = as_layer_input(*xs[k], dtype_, w, h_, ffn1_->label(), keep, train);
+    if (xin.rows() != rows) throw DimensionError(ffn1_->label() + ": workers' activations differ in row count");
+    ys[k] = Tensor({rows, h_}, dtype_, w.device, &w.ledger, MemCategory::Activation, false);
+    xv[k] = {xin.data(), h_};
+    yv[k] = {ys[k].data(), h_};
+  }
+  forward(xv, rows, yv, mode);
+  group_->synchronize();
+  return ys;
+}
+
+std::vector<Tensor> RtpMlp::backward(std::span<const Tensor> dy) {
+  const auto& local = group_->local_ranks();
+  auto ds = per_local(*group_, dy, ffn2_->label(), "backward");
+  const size_t rows = ds[0]->rank() == 2 ? ds[0]->rows() : 0;
+  std::vector<Tensor> tmp(local.size()), dxs(local.size());
+  std::vector<DView> dv(local.size()), xv(local.size());
+  for (size_t k = 0; k < local.size(); ++k) {
+    Worker& w = group_->worker(local[k]);
+    const Tensor& din = as_layer_input(*ds[k], dtype_, w, h_, ffn2_->label(), tmp[k], false);
+    if (din.rows() != rows) throw DimensionError(ffn2_->label() + ": workers' gradients differ in row count");
+    dxs[k] = Tensor({rows, h_}, dtype_, w.device, &w.ledger, MemCategory::Activation, false);
+    dv[k] = {din.data(), h_};
+    xv[k] = {dxs[k].data(), h_};
+  }
+  backward(dv, rows, xv);
+  group_->synchronize();
+  x_keep_.clear();
+  return dxs;
 }
 
 }  // namespace rtpb

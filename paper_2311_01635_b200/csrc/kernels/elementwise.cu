@@ -198,6 +198,31 @@ __global__ void cast_kernel(const float* __restrict__ src, __nv_bfloat16* __rest
     dst[i] = __float2bfloat16_rn(src[i]);
 }
 
+// Any-to-any dtype conversion (device Tensor casts): each element read as
+// fp64 then rounded once to the destination (RN; bf16 from fp64 directly, no
+// double rounding through fp32). code = src_dtype * 3 + dst_dtype.
+__device__ __forceinline__ double ld_any(const void* p, int dt, size_t i) {
+  if (dt == RTPB_F64) return static_cast<const double*>(p)[i];
+  if (dt == RTPB_F32) return double(static_cast<const float*>(p)[i]);
+  return double(__bfloat162float(static_cast<const __nv_bfloat16*>(p)[i]));
+}
+__device__ __forceinline__ void st_any(void* p, int dt, size_t i, double v) {
+  if (dt == RTPB_F64)
+    static_cast<double*>(p)[i] = v;
+  else if (dt == RTPB_F32)
+    static_cast<float*>(p)[i] = __double2float_rn(v);
+  else
+    static_cast<__nv_bfloat16*>(p)[i] = __double2bfloat16(v);
+}
+__global__ void convert_kernel(const void* __restrict__ src, int sdt, void* __restrict__ dst, int ddt, size_t n) {
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x)
+    st_any(dst, ddt, i, ld_any(src, sdt, i));
+}
+__global__ void fill_kernel(void* __restrict__ dst, int dt, size_t n, double v) {
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x)
+    st_any(dst, dt, i, v);
+}
+
 int post_launch(const char* what) {
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_cuda_error(e, what);
@@ -286,6 +311,18 @@ int gelu_bwd(bool f32, const void* x, const void* up, void* out, size_t n, cudaS
                                                       static_cast<const __nv_bfloat16*>(up),
                                                       static_cast<__nv_bfloat16*>(out), n);
   return post_launch("gelu_bwd_kernel");
+}
+
+int convert(const void* src, int src_dtype, void* dst, int dst_dtype, size_t n, cudaStream_t s) {
+  if (n == 0) return RTPB_OK;
+  convert_kernel<<<grid_for(n, 256), 256, 0, s>>>(src, src_dtype, dst, dst_dtype, n);
+  return post_launch("convert_kernel");
+}
+
+int fill(void* dst, int dtype, size_t n, double v, cudaStream_t s) {
+  if (n == 0) return RTPB_OK;
+  fill_kernel<<<grid_for(n, 256), 256, 0, s>>>(dst, dtype, n, v);
+  return post_launch("fill_kernel");
 }
 
 int cast_f32_to_bf16(const float* src, void* dst, size_t n, cudaStream_t s) {

@@ -150,5 +150,8 @@ int tf32_split_t(const float* src, size_t rows, size_t cols, size_t ld, float* h
 int gelu_fwd(bool f32, const void* x, void* y, size_t count, cudaStream_t s);
 int gelu_bwd(bool f32, const void* x, const void* up, void* out, size_t count, cudaStream_t s);
 int cast_f32_to_bf16(const float* src, void* dst, size_t count, cudaStream_t s);
+// dtype codes RTPB_BF16 / RTPB_F32 / RTPB_F64
+int convert(const void* src, int src_dtype, void* dst, int dst_dtype, size_t count, cudaStream_t s);
+int fill(void* dst, int dtype, size_t count, double v, cudaStream_t s);
 
 }  // namespace rtpb

@@ -127,10 +127,19 @@ except FileNotFoundError:
 open(f"{OUT}/ncu_{R}.md", "w").write("\n".join(lines) + "\n")
 json.dump(summary, open(f"{OUT}/ncu_{R}.json", "w"), indent=1)
 # dominant-kernel DRAM traffic per launch, for bench.py's roofline.traffic
+# (keyed by bench config: CONFIG env, default d)
 ks = [k for k in summary["kernels"] if k["time_us"]]
 if ks:
     avg = sum((k["dram_read_MB"] or 0) + (k["dram_write_MB"] or 0) for k in ks) / len(ks)
-    json.dump({"round": R, "kernel": "rtp_gemm_kernel (step GEMMs, average over captured launches)",
-               "dram_bytes_per_launch": avg * 1e6, "launches": len(ks)}, open(f"{OUT}/ncu_traffic.json", "w"),
-              indent=1)
+    cfg = os.environ.get("CONFIG", "d")
+    path = f"{OUT}/ncu_traffic.json"
+    try:
+        tj = json.load(open(path))
+    except (FileNotFoundError, ValueError):
+        tj = {}
+    tj.setdefault("configs", {})[cfg] = {
+        "source": f"profiles/ncu_{R}.md", "kernel": "rtp_gemm_kernel (step GEMMs, average over captured launches)",
+        "dram_bytes_per_launch": avg * 1e6, "launches": len(ks),
+        "per_launch_MB": [round((k["dram_read_MB"] or 0) + (k["dram_write_MB"] or 0), 1) for k in ks]}
+    json.dump(tj, open(path, "w"), indent=1)
 print("\n".join(lines))
