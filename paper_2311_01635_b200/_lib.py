@@ -47,6 +47,8 @@ _SIGS = {
                                  _int, _vp, _sz, _vp]),
     "rtpb_wgrad_step": (_int, [_int, _vp, _sz, _vp, _sz, _sz, _vp, _vp, _sz, _sz, _sz, _vp, _sz, _vp]),
     "rtpb_gelu": (_int, [_int, _vp, _vp, _sz, _vp]),
+    "rtpb_convert": (_int, [_vp, _int, _vp, _int, _sz, _vp]),
+    "rtpb_fill": (_int, [_vp, _int, _sz, _dbl, _vp]),
     "rtpb_gelu_backward": (_int, [_int, _vp, _vp, _vp, _sz, _vp]),
     "rtpb_ring_plan": (_int, [_sz, _sz, _int, _sz, C.POINTER(_i64), C.POINTER(_i64), C.POINTER(_i64)]),
     # group / layer handles
