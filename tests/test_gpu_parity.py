@@ -271,22 +271,62 @@ def test_inplace_rotation_larger_than_staging_chunk():
 
 
 # ---------------------------------------------------------------- memory
+def _chunk(shard_bytes):
+    """In-place staging chunk (rtp_group.cpp inplace_chunk_bytes): max(1 MiB,
+    shard/32) rounded to 256 B, at most the shard."""
+    c = max(1 << 20, shard_bytes // 32)
+    c = (c + 255) & ~255
+    return min(c, shard_bytes)
+
+
 @pytest.mark.parametrize("n", [2, 4])
-def test_memory_ledger_matches_model(golden, n):
+def test_memory_ledger_exact_bytes(golden, n):
+    """Exact per-worker peaks (analysis_test.cpp:151-194 pins exact bytes):
+    Param = W/N (bf16), Grad = G/N (fp32); in place the only CommBuffer is the
+    staging chunk the in-place shifts go through (the reference does not
+    charge its in-flight message; the device path does); out of place one
+    weight-shard spare (layers_common.cpp:153-160) plus the chunk the
+    gradient's in-place shift uses (G moves in place, ring.cpp:314,328)."""
     g = golden("linear")
     i_dim, o_dim = g["w"].shape
     L = i_dim * (o_dim // n) + o_dim // n
     for mode in ("inplace", "outofplace"):
         out = run_linear(n, g["w"], g["b"], g["x"], g["dy"], "bf16", mode)
         for led in out["ledger"]:
-            assert led["peak_param"] == L * 2  # W/N, bf16
-            assert led["peak_grad"] == L * 4  # G/N, fp32
-            if mode == "outofplace":
-                # one weight-shard spare (+ the gradient staging chunk)
-                assert led["peak_comm"] >= L * 2
-                assert led["peak_comm"] <= L * 2 + L * 4
+            assert led["peak_param"] == L * 2
+            assert led["peak_grad"] == L * 4
+            spare = L * 2 if mode == "outofplace" else 0
+            assert led["peak_comm"] == spare + _chunk(L * 4), (mode, led)
+
+
+@pytest.mark.parametrize("n", [1, 2, 4])
+def test_mlp_ledger_element_counts_match_reference(golden, n):
+    """The MLP step's Param / Grad / CommBuffer peaks against the reference's
+    own ledger (tests/golden/ledger.npz: RtpLinear x2 under bound ledgers,
+    fp64 = 8 B/element): same element counts, our bytes per element bf16 W /
+    fp32 G; out of place the reference's CommBuffer is max(W,G)/N of fp64
+    spares (W-sized, = G-sized in fp64), ours the W-sized bf16 spares plus
+    the gradient shift's staging chunk."""
+    from helpers import run_mlp
+    led = golden("ledger")
+    m = golden("mlp")
+    h, f = m["w1"].shape
+    L1, L2 = h * (f // n) + f // n, f * (h // n) + h // n
+    for oop in (0, 1):
+        out = run_mlp(n, m["w1"], m["b1"], m["w2"], m["b2"], m["x"], m["dy"], "bf16",
+                      "outofplace" if oop else "inplace")
+        ref = {k: int(led[f"n{n}_oop{oop}_{k}"]) for k in ("param", "grad", "comm")}
+        for lg in out["ledger"]:
+            assert lg["peak_param"] * 4 == ref["param"]  # bf16 vs fp64
+            assert lg["peak_grad"] * 2 == ref["grad"]    # fp32 vs fp64
+            if n == 1:
+                assert lg["peak_comm"] == 0 and ref["comm"] == 0
+            elif oop:
+                assert ref["comm"] == 8 * (L1 + L2)  # both layers' spares, fp64
+                assert lg["peak_comm"] == 2 * (L1 + L2) + _chunk(4 * max(L1, L2))
             else:
-                assert led["peak_comm"] <= L * 4  # staging chunk only
+                assert ref["comm"] == 0
+                assert lg["peak_comm"] == _chunk(4 * max(L1, L2))
 
 
 # ---------------------------------------------------------------- larger configs
