@@ -97,6 +97,7 @@ int device_sms() {
 // GEMMs issued on two streams run side by side instead of queueing.
 thread_local int t_sm_budget = 0;
 thread_local const unsigned* t_wait_flag = nullptr;
+thread_local const unsigned* t_g_flag = nullptr;
 thread_local unsigned* t_reset_flags = nullptr;
 thread_local unsigned* t_reset_ctr = nullptr;
 thread_local int t_reset_count = 0;
@@ -203,6 +204,7 @@ int launch_cfg(const Op& a, const Op& b, const Out& c0, const Out* c1, const Gem
   if (t_kseg.on) a_.kseg_kb = t_kseg.kb;
   a_.trace = next_trace(cfg.gridDim.x);
   if (!a_.ready_flag) a_.ready_flag = t_wait_flag;  // set_launch_wait_flag()
+  if (!a_.g_flag && Cfg::EPI == EPI_WGRAD) a_.g_flag = t_g_flag;  // set_launch_g_flag()
   if (!a_.flag_reset && t_reset_flags) {              // set_launch_flag_reset()
     a_.flag_reset = t_reset_flags;
     a_.flag_reset_ctr = t_reset_ctr;
@@ -798,6 +800,7 @@ int gemm_bwd_fused(const FusedBwdArgs& a, const FusedBwdPlan& plan, const FusedB
 
 void set_sm_budget(int sms) { t_sm_budget = sms; }
 void set_launch_wait_flag(const unsigned* flag) { t_wait_flag = flag; }
+void set_launch_g_flag(const unsigned* flag) { t_g_flag = flag; }
 void set_launch_flag_reset(unsigned* flags, int count, unsigned* ctr) {
   t_reset_flags = flags;
   t_reset_count = flags ? count : 0;

@@ -114,6 +114,13 @@ struct GemmArgs {
   // Replaces a stream-event dependency, so the launch keeps its programmatic
   // (PDL) edge to the previous GEMM on its stream.
   const unsigned* ready_flag;
+  // WGRAD: the travelling gradient shard G arrives by flag (comm stream,
+  // cuStreamWriteValue32 once the neighbour's G has landed). Only the roles
+  // that read or reduce into G wait for *g_flag >= 1 — the epilogue warps
+  // before their first tile's G update, the bias-sum warps before adding
+  // G's bias part — so the producer and MMA run the mainloop while G is in
+  // flight: the accumulation is applied in the epilogue as the shard arrives.
+  const unsigned* g_flag;
   // Two K segments (DGRAD over two resident weight shards, single problem):
   // K blocks kb >= kseg_kb read the A and B maps of the second GemmMaps at
   // K offset (kb - kseg_kb) * BK. 0: one segment.
@@ -730,6 +737,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
     uint8_t* pre_w = pre_base + ew * Cfg::PRE_WARP;
     uint32_t pre_phase = 0;
     bool pending = false;
+    bool g_ready = args.g_flag == nullptr;  // WGRAD: travelling G landed
     unsigned wbuf = 0;  // dW staging buffer alternation
     int acc = 0;
     uint32_t acc_phase = 0;
@@ -771,7 +779,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
         for (int k = 0; k < Cfg::PRE_CHUNKS; ++k) {
           const int col = n0 + (half + k * NSPLIT) * 32 + lane;
           float bv = 0.f;
-          if (col < uN) {
+          if (col < uN && uaux) {  // no bias: projection blocks (RTPB_EPI_NO_BIAS)
             if constexpr (F32)
               bv = static_cast<const float*>(uaux)[col];
             else
@@ -822,6 +830,14 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
       const bool wpar = Cfg::EPI == EPI_WGRAD && args.wpar && wsplits > 1;
       const int wprows = x_.prob ? args.wpart_rows2 : args.wpart_rows;
       if constexpr (Cfg::EPI == EPI_WGRAD) {
+        // the travelling G must have landed before this warp's first update
+        // of it (first && split 0 overwrite it: G is known zero, no wait;
+        // split partials go to the workspace: their folds wait below)
+        if (!g_ready && !wpar && !(first && split == 0)) {
+          if (lane == 0) detail::wait_counter(args.g_flag, 1u);
+          __syncwarp();
+          g_ready = true;
+        }
         if (split > 0 && !wpar) {
           // ordered split-K: wait until every warp of split-1 has landed its sums
           if (lane == 0) detail::wait_counter(wflags + t, unsigned(split * wgroup));
@@ -1003,6 +1019,11 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
           }
           __syncwarp();
           pending = false;
+          if (!g_ready && !first) {  // the fold reads G
+            if (lane == 0) detail::wait_counter_nofence(args.g_flag, 1u);
+            __syncwarp();
+            g_ready = true;
+          }
           const float* part = x_.prob ? args.wpart2 : args.wpart;
           const int r_lo = (32 * split) / wsplits, r_hi = (32 * (split + 1)) / wsplits;
           float* gout = const_cast<float*>(static_cast<const float*>(x_.prob ? args.gout2 : args.gout));
@@ -1066,6 +1087,11 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
           }
           last = __shfl_sync(0xffffffffu, last, 0);
           pending = false;
+          if (last && !g_ready && !first) {  // the fold reduce-adds into G
+            if (lane == 0) detail::wait_counter(args.g_flag, 1u);
+            __syncwarp();
+            g_ready = true;
+          }
           if (last) {
             const float* part = x_.prob ? args.wpart2 : args.wpart;
 #pragma unroll 1
@@ -1287,6 +1313,10 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
             s0.z += __shfl_sync(0xffffffffu, t0.z, src); s0.w += __shfl_sync(0xffffffffu, t0.w, src);
             s1.x += __shfl_sync(0xffffffffu, t1.x, src); s1.y += __shfl_sync(0xffffffffu, t1.y, src);
             s1.z += __shfl_sync(0xffffffffu, t1.z, src); s1.w += __shfl_sync(0xffffffffu, t1.w, src);
+          }
+          if (!first && args.g_flag) {  // G's bias part is read below
+            if (lane == 0) detail::wait_counter_nofence(args.g_flag, 1u);
+            __syncwarp();
           }
           if (lane < LPR && cl < uN) {
             float4* o = reinterpret_cast<float4*>(ugb_out + cl);

@@ -130,6 +130,9 @@ int sm_budget();
 // The calling thread's following GEMM launches load no operand before
 // *flag >= 1 (nullptr: no wait). See GemmArgs::ready_flag.
 void set_launch_wait_flag(const unsigned* flag);
+// The next dW launch of this thread: its epilogue (not its mainloop) waits
+// for the travelling gradient's arrival flag (GemmArgs::g_flag).
+void set_launch_g_flag(const unsigned* flag);
 // The calling thread's next step-GEMM launch clears [flags, +count) (and the
 // CTA counter ctr) when all its CTAs are done; nullptr = none.
 void set_launch_flag_reset(unsigned* flags, int count, unsigned* ctr);
@@ -150,6 +153,13 @@ int tf32_split_t(const float* src, size_t rows, size_t cols, size_t ld, float* h
 int gelu_fwd(bool f32, const void* x, void* y, size_t count, cudaStream_t s);
 int gelu_bwd(bool f32, const void* x, const void* up, void* out, size_t count, cudaStream_t s);
 int cast_f32_to_bf16(const float* src, void* dst, size_t count, cudaStream_t s);
+// attention.cu: the attention core of one head group (rows = batch * seq,
+// q/k/v/o rows x g*hd; lse / delta rows x g fp32).
+int attention_core_fwd(bool f32, const void* q, const void* k, const void* v, void* o, float* lse, size_t rows,
+                       size_t seq, size_t g, size_t hd, float scale, cudaStream_t s);
+int attention_core_bwd(bool f32, const void* q, const void* k, const void* v, const void* o, const float* lse,
+                       const void* dout, void* dq, void* dk, void* dv, float* delta, size_t rows, size_t seq,
+                       size_t g, size_t hd, float scale, cudaStream_t s);
 // dtype codes RTPB_BF16 / RTPB_F32 / RTPB_F64
 int convert(const void* src, int src_dtype, void* dst, int dst_dtype, size_t count, cudaStream_t s);
 int fill(void* dst, int dtype, size_t count, double v, cudaStream_t s);
