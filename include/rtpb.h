@@ -53,6 +53,7 @@ extern "C" {
 #define RTPB_EPI_LAST 4      /* dgrad: last step, emit dX in the activation dtype        */
 #define RTPB_EPI_GELU_BWD 8  /* dgrad last step: dX *= gelu'(pre) (model.cpp:101-104)   */
 #define RTPB_EPI_STORE_PRE 16 /* fwd: write X.W_j + b_j to `y` (default for plain linear) */
+#define RTPB_EPI_NO_BIAS 32   /* fwd / wgrad_ex: the shard block has no bias part (projections) */
 
 const char* rtpb_last_error(void);
 const char* rtpb_version(void);
@@ -112,6 +113,13 @@ int rtpb_dgrad_step2(int dtype, const void* dy, size_t ldy, size_t col0, const v
 int rtpb_wgrad_step(int dtype, const void* x, size_t ldx, const void* dy, size_t ldy, size_t col0,
                     const float* g_in, float* g_out, size_t M, size_t I, size_t per, void* workspace,
                     size_t workspace_bytes, void* stream);
+
+/* rtpb_wgrad_step with epilogue flags: RTPB_EPI_NO_BIAS computes only
+ * g_out[0 : I*per] (= g_in + X^T . dY block), for bias-free projection blocks
+ * (RtpAttention: layers_attention.cpp:136-137, :164-166). */
+int rtpb_wgrad_step_ex(int dtype, const void* x, size_t ldx, const void* dy, size_t ldy, size_t col0,
+                       const float* g_in, float* g_out, size_t M, size_t I, size_t per, int epi_flags,
+                       void* workspace, size_t workspace_bytes, void* stream);
 
 /* Workspace bytes for a step kernel: which = 0 fwd, 1 dgrad, 2 wgrad.
  * A workspace must be zero-filled before its first use; the kernels leave
@@ -175,6 +183,7 @@ int rtpb_ring_plan(size_t n, size_t rank, int phase, size_t step, int64_t* logic
 typedef struct rtpb_group_s* rtpb_group;
 typedef struct rtpb_linear_s* rtpb_linear;
 typedef struct rtpb_mlp_s* rtpb_mlp;
+typedef struct rtpb_attention_s* rtpb_attention;
 
 #define RTPB_TRANSPORT_LOCKSTEP 0   /* one host thread drives all local workers        */
 #define RTPB_TRANSPORT_CONCURRENT 1 /* one host thread per local worker                */
@@ -288,6 +297,28 @@ int rtpb_mlp_backward(rtpb_mlp m, const void* const* dy, size_t rows, void* cons
 int rtpb_mlp_chain(rtpb_mlp m, rtpb_mlp next);
 /* layer 0 = ffn1, 1 = ffn2 */
 rtpb_linear rtpb_mlp_layer(rtpb_mlp m, int layer);
+
+/* RtpAttention(group, label, wq, wk, wv, wo, heads, seq, n)
+ * (layers.hpp:170-191, layers_attention.cpp:43-198): head-partitioned
+ * attention, projections without bias. wq..wo: hidden x hidden fp64 host
+ * arrays. Activations are (batch * seq) x hidden per local rank. */
+int rtpb_attention_create(rtpb_group g, const char* label, size_t hidden, size_t heads, size_t seq, int dtype,
+                          const double* wq, const double* wk, const double* wv, const double* wo,
+                          rtpb_attention* out);
+int rtpb_attention_destroy(rtpb_attention a);
+int rtpb_attention_set_rotation_mode(rtpb_attention a, int mode);
+int rtpb_attention_allocate_comm_spares(rtpb_attention a);
+int rtpb_attention_release_comm_spares(rtpb_attention a);
+int rtpb_attention_zero_grads(rtpb_attention a);
+size_t rtpb_attention_shard_len(rtpb_attention a);
+int rtpb_attention_forward(rtpb_attention a, const void* const* x, size_t rows, void* const* y, int mode);
+int rtpb_attention_backward(rtpb_attention a, const void* const* dy, size_t rows, void* const* dx);
+int rtpb_attention_slot(rtpb_attention a, size_t rank, int64_t* logical_id, int64_t* rotation_offset);
+int rtpb_attention_trace(rtpb_attention a, int64_t* ids);
+/* Shard resident at local rank r in the reference's flat layout
+ * [Wq_j | Wk_j | Wv_j | Wo_j] as fp64 into host memory dst (shard_len values):
+ * which 0 = weight, 1 = gradient. */
+int rtpb_attention_read_shard(rtpb_attention a, size_t rank, int which, double* dst);
 
 #ifdef __cplusplus
 }

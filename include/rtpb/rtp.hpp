@@ -527,6 +527,65 @@ class RtpLinear : public RtpLayerBase {
   bool pre_fwd_ = false, pre_bwd_ = false;  // first shift already posted
 };
 
+// Q/K/V projections split by head group; the output projection owns the
+// matching row block (partition.cpp:71-84): ConfigError unless hidden % heads
+// == 0 and heads % n == 0.
+ShardLayout layout_attention(size_t hidden, size_t heads, size_t n);
+
+// Multi-head attention sharded by head group (layers.hpp:170-191,
+// layers_attention.cpp:43-198): shard j holds head group j's Q/K/V column
+// blocks and the matching row block of the output projection, no bias.
+// Forward step s (shard j): Q,K,V = X Wq_j, X Wk_j, X Wv_j (step GEMMs), the
+// attention core per (sequence, head) (kernels/attention.cu), Y += A Wo_j
+// through the dX kernel's fp32 cross-step accumulator. Backward: dWo_j,
+// dA, the core's backward, dWq/k/v_j (dW kernel, fused into the travelling
+// gradient) and dX += dQ Wq_j^T + dK Wk_j^T + dV Wv_j^T (fp32 accumulator).
+// Device shard layout: [Wq_j | Wk_j | Wv_j | Wo_j^T], each hidden x gw
+// row-major (gw = heads/n * head_dim): the reference's flat shard with the
+// Wo block stored transposed, so every product maps onto the three step
+// kernels; shard_host() returns the reference layout.
+class RtpAttention : public RtpLayerBase {
+ public:
+  // Host fp64 weights (hidden x hidden each, as the reference).
+  RtpAttention(WorkerGroup& group, std::string label, const double* wq, const double* wk, const double* wv,
+               const double* wo, size_t hidden, size_t heads, size_t seq, size_t n, DType dtype = DType::BF16);
+  // The reference's constructor (layers.hpp:175-176); dtype as RtpLinear's.
+  RtpAttention(WorkerGroup& group, std::string label, const Tensor& wq, const Tensor& wk, const Tensor& wv,
+               const Tensor& wo, size_t heads, size_t seq, size_t n);
+
+  size_t hidden() const { return hidden_; }
+  size_t heads() const { return heads_; }
+  size_t seq() const { return seq_; }
+  size_t head_dim() const { return hd_; }
+  size_t group_heads() const { return g_; }
+  size_t group_width() const { return gw_; }
+  const ShardLayout& layout() const { return layout_; }
+
+  // x[k]: (batch * seq) x hidden per local worker; y, dx the same shape.
+  void forward(std::span<const DView> x, size_t rows, std::span<const DView> y, Mode mode);
+  void backward(std::span<const DView> dy, size_t rows, std::span<const DView> dx);
+  std::vector<Tensor> forward(std::span<const Tensor> x, Mode mode);
+  std::vector<Tensor> backward(std::span<const Tensor> dy);
+
+  // The resident weight (grad = false) or gradient shard of a local rank in
+  // the reference's flat layout [Wq_j | Wk_j | Wv_j | Wo_j (gw x hidden)].
+  std::vector<double> shard_host(size_t rank, bool grad);
+
+ private:
+  void init(const double* wq, const double* wk, const double* wv, const double* wo);
+  void ensure_scratch(size_t rows);
+  size_t hidden_, heads_, seq_, hd_, g_, gw_;
+  ShardLayout layout_;
+  std::vector<ReplayTape<size_t>> tapes_;  // saved: the forward step whose buffers backward reads
+  std::vector<DView> x_cache_;
+  std::vector<Tensor> x_keep_;
+  size_t scratch_rows_ = 0, cached_rows_ = 0;
+  // per rank: per forward step s: q, k, v, o (rows x gw, dtype) and lse
+  // (rows x g fp32); backward scratch dA, dq, dk, dv, delta; fp32 Y / dX
+  // cross-step accumulators (rows x hidden)
+  std::vector<DeviceBuffer> saved_, lse_, scratch_, acc_;
+};
+
 // ffn1 (h -> f) -> gelu -> ffn2 (f -> h), composed as model.cpp:77-83,99-105.
 class RtpMlp {
  public:

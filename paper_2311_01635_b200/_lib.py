@@ -17,7 +17,7 @@ RTPB_OK = 0
 ERR_NAMES = {1: "Generic", 2: "Config", 3: "Dimension", 4: "Protocol", 5: "State", 6: "Index", 7: "Cuda", 8: "Nccl"}
 
 BF16, F32 = 0, 1
-EPI_GELU, EPI_FIRST, EPI_LAST, EPI_GELU_BWD, EPI_STORE_PRE = 1, 2, 4, 8, 16
+EPI_GELU, EPI_FIRST, EPI_LAST, EPI_GELU_BWD, EPI_STORE_PRE, EPI_NO_BIAS = 1, 2, 4, 8, 16, 32
 TRANSPORT_LOCKSTEP, TRANSPORT_CONCURRENT, TRANSPORT_NCCL = 0, 1, 2
 MODE_TRAIN, MODE_EVAL = 0, 1
 ROT_INPLACE, ROT_OUTOFPLACE = 0, 1
@@ -92,6 +92,19 @@ _SIGS = {
     "rtpb_mlp_backward": (_int, [_vp, _vpp, _sz, _vpp]),
     "rtpb_mlp_chain": (_int, [_vp, _vp]),
     "rtpb_mlp_layer": (_vp, [_vp, _int]),
+    "rtpb_attention_create": (_int, [_vp, C.c_char_p, _sz, _sz, _sz, _int, _vp, _vp, _vp, _vp, _vpp]),
+    "rtpb_attention_destroy": (_int, [_vp]),
+    "rtpb_attention_set_rotation_mode": (_int, [_vp, _int]),
+    "rtpb_attention_allocate_comm_spares": (_int, [_vp]),
+    "rtpb_attention_release_comm_spares": (_int, [_vp]),
+    "rtpb_attention_zero_grads": (_int, [_vp]),
+    "rtpb_attention_shard_len": (_sz, [_vp]),
+    "rtpb_attention_forward": (_int, [_vp, _vpp, _sz, _vpp, _int]),
+    "rtpb_attention_backward": (_int, [_vp, _vpp, _sz, _vpp]),
+    "rtpb_attention_slot": (_int, [_vp, _sz, C.POINTER(_i64), C.POINTER(_i64)]),
+    "rtpb_attention_trace": (_int, [_vp, C.POINTER(_i64)]),
+    "rtpb_attention_read_shard": (_int, [_vp, _sz, _int, C.POINTER(_dbl)]),
+    "rtpb_wgrad_step_ex": (_int, [_int, _vp, _sz, _vp, _sz, _sz, _vp, _vp, _sz, _sz, _sz, _int, _vp, _sz, _vp]),
 }
 
 

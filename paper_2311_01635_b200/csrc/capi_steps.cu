@@ -244,7 +244,8 @@ int rtpb_fwd_step(int dtype, const void* x, size_t ldx, const void* w_shard, voi
   cudaStream_t s = as_stream(stream);
   StepFwd p{};
   p.x = x; p.ldx = ldx; p.w = w_shard;
-  p.bias = static_cast<const char*>(w_shard) + I * per * esz;
+  p.bias = (flags & RTPB_EPI_NO_BIAS) ? nullptr : static_cast<const char*>(w_shard) + I * per * esz;
+  flags &= ~RTPB_EPI_NO_BIAS;
   p.y = y; p.ldy = ldy; p.col0 = col0; p.act = act; p.ld_act = ld_act;
   p.M = M; p.I = I; p.per = per; p.flags = flags; p.force_bn = g_force_bn;
   if (f32) {
@@ -315,6 +316,14 @@ int rtpb_dgrad_step2(int dtype, const void* dy, size_t ldy, size_t col0, const v
 int rtpb_wgrad_step(int dtype, const void* x, size_t ldx, const void* dy, size_t ldy, size_t col0,
                     const float* g_in, float* g_out, size_t M, size_t I, size_t per, void* workspace,
                     size_t workspace_bytes, void* stream) {
+  return rtpb_wgrad_step_ex(dtype, x, ldx, dy, ldy, col0, g_in, g_out, M, I, per, 0, workspace, workspace_bytes,
+                            stream);
+}
+
+int rtpb_wgrad_step_ex(int dtype, const void* x, size_t ldx, const void* dy, size_t ldy, size_t col0,
+                       const float* g_in, float* g_out, size_t M, size_t I, size_t per, int epi_flags,
+                       void* workspace, size_t workspace_bytes, void* stream) {
+  const bool no_bias = epi_flags & RTPB_EPI_NO_BIAS;
   int rc = check_geom(M, I, per);
   if (rc) return rc;
   if (!g_out) return set_error(RTPB_ERR_DIMENSION, "wgrad_step: null gradient shard");
@@ -344,10 +353,12 @@ int rtpb_wgrad_step(int dtype, const void* x, size_t ldx, const void* dy, size_t
   if (!c.ok) return set_error(RTPB_ERR_DIMENSION, "wgrad_step: workspace too small");
   if ((reinterpret_cast<uintptr_t>(g_out) | reinterpret_cast<uintptr_t>(g_in)) & 15)
     return set_error(RTPB_ERR_CONFIG, "wgrad_step: gradient shards must be 16-byte aligned");
-  const float* gb_in = g_in ? g_in + I * per : nullptr;
-  float* gb_out = g_out + I * per;
+  const float* gb_in = g_in && !no_bias ? g_in + I * per : nullptr;
+  float* gb_out = no_bias ? nullptr : g_out + I * per;
   return timed(2, 2.0 * M * I * per, s, [&] {
-    if (wgrad_fuses_bias(f32, M, I, per, flags, g_force_bn)) {
+    if (no_bias) {
+      // projection without bias (RtpAttention's Wq/Wk/Wv/Wo blocks): G only
+    } else if (wgrad_fuses_bias(f32, M, I, per, flags, g_force_bn)) {
       // CTA-pair dW: the kernel's column-sum warp reduces the staged dY tiles.
       p.gbias_in = gb_in;
       p.gbias_out = gb_out;

@@ -29,6 +29,10 @@ struct rtpb_linear_s {
   std::unique_ptr<RtpLinear> l;
   bool owned = true;
 };
+struct rtpb_attention_s {
+  rtpb_group_s* grp;
+  std::unique_ptr<RtpAttention> a;
+};
 struct rtpb_mlp_s {
   rtpb_group_s* grp;
   std::unique_ptr<RtpMlp> m;
@@ -441,6 +445,79 @@ rtpb_linear rtpb_mlp_layer(rtpb_mlp m, int layer) {
   // (never deleted) in rtpb_mlp_destroy.
   if (!v.l) v.l.reset(layer == 0 ? &m->m->ffn1() : &m->m->ffn2());
   return &v;
+}
+
+int rtpb_attention_create(rtpb_group g, const char* label, size_t hidden, size_t heads, size_t seq, int dtype,
+                          const double* wq, const double* wk, const double* wv, const double* wo,
+                          rtpb_attention* out) {
+  return guard([&] {
+    if (!wq || !wk || !wv || !wo) throw DimensionError("attention_create: all four projection weights are required");
+    auto h = std::make_unique<rtpb_attention_s>();
+    h->grp = g;
+    h->a = std::make_unique<RtpAttention>(*g->g, label ? label : "attn", wq, wk, wv, wo, hidden, heads, seq,
+                                          g->g->size(), dt(dtype));
+    ++g->refs;
+    *out = h.release();
+  });
+}
+
+int rtpb_attention_destroy(rtpb_attention a) {
+  return guard([&] {
+    if (a) {
+      rtpb_group_s* g = a->grp;
+      delete a;
+      group_release(g);
+    }
+  });
+}
+
+int rtpb_attention_set_rotation_mode(rtpb_attention a, int mode) {
+  return guard([&] { a->a->set_rotation_mode(mode == RTPB_ROT_OUTOFPLACE ? RotationMode::OutOfPlace : RotationMode::InPlace); });
+}
+int rtpb_attention_allocate_comm_spares(rtpb_attention a) { return guard([&] { a->a->allocate_comm_spares(); }); }
+int rtpb_attention_release_comm_spares(rtpb_attention a) { return guard([&] { a->a->release_comm_spares(); }); }
+int rtpb_attention_zero_grads(rtpb_attention a) { return guard([&] { a->a->zero_grads(); }); }
+size_t rtpb_attention_shard_len(rtpb_attention a) { return a ? a->a->shard_len() : 0; }
+
+int rtpb_attention_forward(rtpb_attention a, const void* const* x, size_t rows, void* const* y, int mode) {
+  return guard([&] {
+    const size_t k = a->grp->g->local_ranks().size();
+    auto xv = views(x, k);
+    auto yv = views(y, k);
+    a->a->forward(xv, rows, yv, mode == RTPB_MODE_EVAL ? Mode::Eval : Mode::Train);
+  });
+}
+
+int rtpb_attention_backward(rtpb_attention a, const void* const* dy, size_t rows, void* const* dx) {
+  return guard([&] {
+    const size_t k = a->grp->g->local_ranks().size();
+    auto dyv = views(dy, k);
+    auto dxv = views(dx, k);
+    a->a->backward(dyv, rows, dxv);
+  });
+}
+
+int rtpb_attention_slot(rtpb_attention a, size_t rank, int64_t* logical_id, int64_t* rotation_offset) {
+  return guard([&] {
+    if (!a->grp->g->is_local(rank)) throw IndexError("slot of a non-local rank");
+    ShardSlot& s = a->a->slots()[rank];
+    if (logical_id) *logical_id = int64_t(s.logical_id);
+    if (rotation_offset) *rotation_offset = s.rotation_offset;
+  });
+}
+
+int rtpb_attention_trace(rtpb_attention a, int64_t* ids) {
+  return guard([&] {
+    const auto& t = a->a->trace();
+    std::memcpy(ids, t.data(), t.size() * sizeof(int64_t));
+  });
+}
+
+int rtpb_attention_read_shard(rtpb_attention a, size_t rank, int which, double* dst) {
+  return guard([&] {
+    const std::vector<double> v = a->a->shard_host(rank, which != 0);
+    std::memcpy(dst, v.data(), v.size() * sizeof(double));
+  });
 }
 
 }  // extern "C"

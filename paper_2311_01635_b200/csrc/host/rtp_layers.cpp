@@ -310,7 +310,7 @@ RtpLinear::RtpLinear(WorkerGroup& group, std::string label, const Tensor& weight
 }
 
 // ---- Tensor API (layers.hpp:138-139) over the device-view passes ----
-namespace {
+namespace detail {
 // x holds either one tensor per rank (n, all local) or one per local rank.
 std::vector<const Tensor*> per_local(WorkerGroup& g, std::span<const Tensor> x, const std::string& label,
                                      const char* what) {
@@ -342,7 +342,9 @@ const Tensor& as_layer_input(const Tensor& t, DType dt, Worker& w, size_t cols, 
   keep = t.to(dt);
   return keep;
 }
-}  // namespace
+}  // namespace detail
+using detail::as_layer_input;
+using detail::per_local;
 
 std::vector<Tensor> RtpLinear::forward(std::span<const Tensor> x, Mode mode) {
   const auto& local = group_->local_ranks();
@@ -813,8 +815,11 @@ void RtpLinear::backward_impl(std::span<const DView> dy, size_t rows, std::span<
     // G_j += X^T . dY_j (+ bias column sums), in place on the resident shard.
     if (dx_sms) set_sm_budget(all_sms - dx_sms);
     // The travelling gradient arrives by flag when the dW launch is a single
-    // CTA-pair GEMM (bias sums fused in it); the per-tile kernels' separate
-    // bias column-sum pre-pass reads G, so those keep the stream wait.
+    // CTA-pair GEMM (bias sums fused in it): the launch starts at once and
+    // only its epilogue / bias-sum warps wait for G (GemmArgs::g_flag), so the
+    // dW mainloop overlaps G's transfer and the accumulation is applied as
+    // the shard lands. The per-tile kernels' separate bias column-sum
+    // pre-pass reads G, so those keep the stream wait.
     unsigned dummy_flags = 0;
     const bool g_flag = flags_on && wgrad_fuses_bias(false, rows, in_, per_, &dummy_flags, 0);
     if (s > 0 && !g_flag) {
@@ -827,7 +832,7 @@ void RtpLinear::backward_impl(std::span<const DView> dy, size_t rows, std::span<
     group_->each([&](size_t r) {
       Worker& w = group_->worker(r);
       const cudaStream_t ws = dx_sms ? w.aux : w.compute;
-      set_launch_wait_flag(g_flag && s > 0 ? w.flag(flag_base_ + kFlagBwdG + s) : nullptr);
+      set_launch_g_flag(g_flag && s > 0 ? w.flag(flag_base_ + kFlagBwdG + s) : nullptr);
       if (flags_on && s + 1 == n)  // the last dW clears the pass's G flags
         set_launch_flag_reset(w.flag(flag_base_ + kFlagBwdG), int(kFlagCtrFwd - kFlagBwdG),
                               w.flag(flag_base_ + kFlagCtrG));
@@ -839,7 +844,7 @@ void RtpLinear::backward_impl(std::span<const DView> dy, size_t rows, std::span<
       const int rc = rtpb_wgrad_step(dt, x_cache_[r].data, x_cache_[r].ld ? x_cache_[r].ld : in_, dy[k].data,
                                      dy[k].ld ? dy[k].ld : out_, j * per_, g_in, g, rows, in_, per_,
                                      workspace_[r].data(), workspace_[r].bytes(), ws);
-      set_launch_wait_flag(nullptr);
+      set_launch_g_flag(nullptr);
       set_launch_flag_reset(nullptr, 0, nullptr);
       check_status(rc);
     });

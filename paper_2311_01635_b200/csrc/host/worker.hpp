@@ -113,4 +113,17 @@ inline size_t ring_src(size_t r, size_t n, Direction d) {
   return d == Direction::Clockwise ? (r + n - 1) % n : (r + 1) % n;
 }
 
+// Tensor-API helpers shared by the layers (rtp_layers.cpp).
+namespace detail {
+// x holds one tensor per rank (n, all local) or one per local rank: the
+// tensors of the local ranks, in local order.
+std::vector<const Tensor*> per_local(WorkerGroup& g, std::span<const Tensor> x, const std::string& label,
+                                     const char* what);
+// t as a layer input on worker w: checked (rank 2, `cols` columns, w's
+// device); converted to dt into `keep` when its dtype differs, or copied
+// there when keep_same (the layer holds it past the call).
+const Tensor& as_layer_input(const Tensor& t, DType dt, Worker& w, size_t cols, const std::string& label,
+                             Tensor& keep, bool keep_same);
+}  // namespace detail
+
 }  // namespace rtpb

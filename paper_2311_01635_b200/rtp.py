@@ -387,6 +387,93 @@ class RtpMlp(_Layer):
             pass
 
 
+class RtpAttention(_Layer):
+    """RtpAttention(group, label, wq, wk, wv, wo, heads, seq, n)
+    (layers.hpp:170-191, layers_attention.cpp:43-198): heads split into N
+    groups, projections without bias. wq..wo: host fp64 hidden x hidden.
+    Activations: (batch * seq) x hidden CUDA tensors, one per local worker."""
+
+    def __init__(self, group: WorkerGroup, label: str, hidden: int, heads: int, seq: int, wq, wk, wv, wo,
+                 dtype="bf16"):
+        self.group, self.label, self.hidden, self.heads, self.seq = group, label, hidden, heads, seq
+        self.dtype_code = _DT[dtype]
+        ws = [_as_host_f64(w) for w in (wq, wk, wv, wo)]
+        for w in ws:
+            if w.shape != (hidden, hidden):
+                raise DimensionError(f"projection weight shape {w.shape} does not match ({hidden}, {hidden})")
+        h = C.c_void_p()
+        check(lib.rtpb_attention_create(group._h, label.encode(), hidden, heads, seq, self.dtype_code,
+                                        *[w.ctypes.data for w in ws], C.byref(h)))
+        self._h = h
+
+    def shard_len(self) -> int:
+        return int(lib.rtpb_attention_shard_len(self._h))
+
+    def set_rotation_mode(self, mode: str):
+        check(lib.rtpb_attention_set_rotation_mode(self._h, {"inplace": 0, "outofplace": 1}[mode]))
+
+    def allocate_comm_spares(self):
+        check(lib.rtpb_attention_allocate_comm_spares(self._h))
+
+    def release_comm_spares(self):
+        check(lib.rtpb_attention_release_comm_spares(self._h))
+
+    def zero_grads(self):
+        check(lib.rtpb_attention_zero_grads(self._h))
+
+    def forward(self, xs, mode: str = "train", out=None):
+        rows = self._check_inputs(xs, self.hidden)
+        ys = out if out is not None else self._acts(rows, self.hidden)
+        self.group._enter([[x, y] for x, y in zip(xs, ys)])
+        check(lib.rtpb_attention_forward(self._h, ptr_array(xs), rows, ptr_array(ys),
+                                         _lib.MODE_EVAL if mode == "eval" else _lib.MODE_TRAIN))
+        self.group._leave()
+        if mode != "eval":
+            self._x_keep = list(xs)
+        return ys
+
+    def backward(self, dys, out=None):
+        rows = self._check_inputs(dys, self.hidden)
+        dxs = out if out is not None else self._acts(rows, self.hidden)
+        self.group._enter([[a, b] for a, b in zip(dys, dxs)])
+        check(lib.rtpb_attention_backward(self._h, ptr_array(dys), rows, ptr_array(dxs)))
+        self.group._leave()
+        self._x_keep = None
+        return dxs
+
+    def slot(self, rank: int) -> dict:
+        lid, off = C.c_int64(), C.c_int64()
+        check(lib.rtpb_attention_slot(self._h, rank, C.byref(lid), C.byref(off)))
+        return {"logical_id": lid.value, "rotation_offset": off.value}
+
+    def shard(self, rank: int, grad: bool = False):
+        """Resident weight / gradient shard in the reference's flat layout
+        [Wq_j | Wk_j | Wv_j | Wo_j] (fp64 numpy)."""
+        import numpy as np
+        out = np.empty(self.shard_len(), dtype=np.float64)
+        check(lib.rtpb_attention_read_shard(self._h, rank, int(grad), out.ctypes.data_as(C.POINTER(C.c_double))))
+        return out
+
+    def trace(self):
+        n = self.group.n
+        arr = (C.c_int64 * (2 * n * n))()
+        check(lib.rtpb_attention_trace(self._h, arr))
+        vals = list(arr)
+        return ([vals[s * n:(s + 1) * n] for s in range(n)],
+                [vals[n * n + s * n: n * n + (s + 1) * n] for s in range(n)])
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib.rtpb_attention_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 # --- step kernels (layer (1) of rtpb.h), on torch tensors ---
 
 def _ws(which, dtype_code, M, I, per, device):
