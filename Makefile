@@ -16,6 +16,7 @@ CXX     ?= g++
 CXXFLAGS := -std=c++20 -O2 -g -fPIC -Wall -Wextra -Wno-unused-parameter -Iinclude -I$(CSRC) \
             -I/usr/local/cuda/include -I$(NCCL_DIR)/include $(EXTRA)
 CU_SRC  := $(CSRC)/kernels/gemm_launch.cu $(CSRC)/kernels/elementwise.cu $(CSRC)/kernels/attention.cu \
+           $(CSRC)/kernels/moe_embed.cu \
            $(CSRC)/capi_steps.cu
 CPP_SRC := $(wildcard $(CSRC)/host/*.cpp)
 OBJS    := $(patsubst $(CSRC)/%.cu,$(OBJDIR)/%.o,$(CU_SRC)) $(patsubst $(CSRC)/%.cpp,$(OBJDIR)/%.o,$(CPP_SRC))

@@ -184,6 +184,8 @@ typedef struct rtpb_group_s* rtpb_group;
 typedef struct rtpb_linear_s* rtpb_linear;
 typedef struct rtpb_mlp_s* rtpb_mlp;
 typedef struct rtpb_attention_s* rtpb_attention;
+typedef struct rtpb_embedding_s* rtpb_embedding;
+typedef struct rtpb_moe_s* rtpb_moe;
 
 #define RTPB_TRANSPORT_LOCKSTEP 0   /* one host thread drives all local workers        */
 #define RTPB_TRANSPORT_CONCURRENT 1 /* one host thread per local worker                */
@@ -319,6 +321,45 @@ int rtpb_attention_trace(rtpb_attention a, int64_t* ids);
  * [Wq_j | Wk_j | Wv_j | Wo_j] as fp64 into host memory dst (shard_len values):
  * which 0 = weight, 1 = gradient. */
 int rtpb_attention_read_shard(rtpb_attention a, size_t rank, int which, double* dst);
+
+/* RtpEmbedding(group, label, table, n) (layers.hpp:150-168,
+ * layers_linear.cpp:74-136): table vocab x emb fp64 host, sharded on the
+ * embedding dimension. forward: ids[k] = `counts[k]` int64 host token ids of
+ * local rank k, y[k] device counts[k] x emb. backward: dy[k] device, no input
+ * gradient. */
+int rtpb_embedding_create(rtpb_group g, const char* label, size_t vocab, size_t emb, int dtype, const double* table,
+                          rtpb_embedding* out);
+int rtpb_embedding_destroy(rtpb_embedding e);
+int rtpb_embedding_set_rotation_mode(rtpb_embedding e, int mode);
+int rtpb_embedding_allocate_comm_spares(rtpb_embedding e);
+int rtpb_embedding_release_comm_spares(rtpb_embedding e);
+int rtpb_embedding_zero_grads(rtpb_embedding e);
+size_t rtpb_embedding_shard_len(rtpb_embedding e);
+int rtpb_embedding_forward(rtpb_embedding e, const int64_t* const* ids, const size_t* counts, void* const* y,
+                           int mode);
+int rtpb_embedding_backward(rtpb_embedding e, const void* const* dy, size_t rows);
+int rtpb_embedding_slot(rtpb_embedding e, size_t rank, int64_t* logical_id, int64_t* rotation_offset);
+/* shard resident at local rank r (vocab x emb/n) as fp64 host values: which 0 weight, 1 gradient */
+int rtpb_embedding_read_shard(rtpb_embedding e, size_t rank, int which, double* dst);
+
+/* RtpMoe(group, label, gate, experts, n) (layers.hpp:193-229,
+ * layers_moe.cpp:18-198): gate hidden x n fp64 host; experts[e] packed
+ * [w1 (hidden x ffn) | b1 | w2 (ffn x hidden) | b2] fp64 host, one per worker. */
+int rtpb_moe_create(rtpb_group g, const char* label, size_t hidden, size_t ffn, int dtype, const double* gate,
+                    const double* const* experts, rtpb_moe* out);
+int rtpb_moe_destroy(rtpb_moe m);
+int rtpb_moe_set_rotation_mode(rtpb_moe m, int mode);
+int rtpb_moe_allocate_comm_spares(rtpb_moe m);
+int rtpb_moe_release_comm_spares(rtpb_moe m);
+int rtpb_moe_zero_grads(rtpb_moe m);
+size_t rtpb_moe_shard_len(rtpb_moe m);
+int rtpb_moe_forward(rtpb_moe m, const void* const* x, size_t rows, void* const* y, int mode);
+int rtpb_moe_backward(rtpb_moe m, const void* const* dy, size_t rows, void* const* dx);
+int rtpb_moe_slot(rtpb_moe m, size_t rank, int64_t* logical_id, int64_t* rotation_offset);
+/* expert shard resident at local rank r (fp64 host, packed as created): which 0 weight, 1 gradient */
+int rtpb_moe_read_shard(rtpb_moe m, size_t rank, int which, double* dst);
+/* the per-worker gate gradient (hidden x n, fp64 host) */
+int rtpb_moe_gate_grad(rtpb_moe m, size_t rank, double* dst);
 
 #ifdef __cplusplus
 }

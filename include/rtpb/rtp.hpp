@@ -586,6 +586,95 @@ class RtpAttention : public RtpLayerBase {
   std::vector<DeviceBuffer> saved_, lse_, scratch_, acc_;
 };
 
+// Embedding sharded on the embedding dimension (layers.hpp:150-168,
+// layers_linear.cpp:74-136): shard j = table[:, j*per:(j+1)*per] (vocab x
+// per), the same rotation schedule as RtpLinear; forward gathers rows into
+// the output's column block, backward scatter-adds dY's block into the
+// travelling gradient in token order (no input gradient). Ids are host
+// vectors as in the reference (IndexError outside the vocabulary).
+class RtpEmbedding : public RtpLayerBase {
+ public:
+  RtpEmbedding(WorkerGroup& group, std::string label, const double* table, size_t vocab, size_t emb, size_t n,
+               DType dtype = DType::BF16);
+  RtpEmbedding(WorkerGroup& group, std::string label, const Tensor& table, size_t n);  // layers.hpp:153
+
+  size_t vocab() const { return vocab_; }
+  size_t emb_dim() const { return emb_; }
+  const ShardLayout& layout() const { return layout_; }
+
+  // ids[k]: the token ids of local rank k; y[k]: ids[k].size() x emb.
+  void forward(std::span<const std::vector<int64_t>> ids, std::span<const DView> y, Mode mode);
+  void backward(std::span<const DView> dy, size_t rows, const std::function<void()>& after_last_rotation = {});
+  std::vector<Tensor> forward(std::span<const std::vector<int64_t>> ids, Mode mode);
+  void backward(std::span<const Tensor> dy, const std::function<void()>& after_last_rotation = {});
+
+ private:
+  size_t vocab_, emb_, per_;
+  ShardLayout layout_;
+  std::vector<ReplayTape<Empty>> tapes_;
+  // per rank: device ids (int64) and, for backward, the CSR of token
+  // positions per unique id (uniq int64, offsets int32, tokens int32)
+  std::vector<DeviceBuffer> ids_dev_, csr_;
+  std::vector<size_t> n_ids_, n_uniq_;
+};
+
+// One expert per shard; ConfigError unless n_experts == n (partition.cpp:86-96).
+ShardLayout layout_moe(size_t n_experts, size_t n);
+
+// One two-layer GELU expert per shard (layers.hpp:113-116).
+struct ExpertParams {
+  Tensor w1, b1, w2, b2;
+};
+
+// Mixture of experts (layers.hpp:193-229, layers_moe.cpp:18-198): top-1
+// gating with a replicated gate (hidden x n, fp64 on every worker so routing
+// follows the reference's fp64 arithmetic), one expert per shard; tokens meet
+// every expert as experts rotate past the sharded batch (no all-to-all).
+// Shard j = [w1 (hidden x f) | b1 | w2 (f x hidden) | b2]: two linear shards
+// back to back, so the expert MLP runs on the step GEMMs (GELU fused).
+class RtpMoe : public RtpLayerBase {
+ public:
+  // gate: hidden x n fp64; experts[e]: packed [w1 | b1 | w2 | b2] fp64.
+  RtpMoe(WorkerGroup& group, std::string label, const double* gate, const double* const* experts, size_t hidden,
+         size_t ffn, size_t n, DType dtype = DType::BF16);
+  RtpMoe(WorkerGroup& group, std::string label, const Tensor& gate, std::span<const ExpertParams> experts,
+         size_t n);  // layers.hpp:197-198
+
+  size_t hidden() const { return hidden_; }
+  size_t ffn_dim() const { return ffn_; }
+  size_t n_experts() const { return n(); }
+  size_t gate_bytes() const { return hidden_ * n() * sizeof(double); }
+  const ShardLayout& layout() const { return layout_; }
+
+  void forward(std::span<const DView> x, size_t rows, std::span<const DView> y, Mode mode);
+  void backward(std::span<const DView> dy, size_t rows, std::span<const DView> dx);
+  std::vector<Tensor> forward(std::span<const Tensor> x, Mode mode);
+  std::vector<Tensor> backward(std::span<const Tensor> dy);
+
+  // Per-worker gate gradient over the local batch shard (data-parallel
+  // semantics: the caller combines replicas), and the replicated gate (fp64).
+  const Tensor& gate_grad(size_t rank) const { return gate_grads_[rank]; }
+  const Tensor& gate_weight(size_t rank) const { return gates_[rank]; }
+  Tensor& gate_weight_mut(size_t rank) { return gates_[rank]; }
+  void zero_grads() override;
+
+ private:
+  void init(const double* gate, const double* const* experts);
+  void ensure_scratch(size_t rows);
+  size_t hidden_, ffn_;
+  ShardLayout layout_;
+  std::vector<Tensor> gates_, gate_grads_;
+  std::vector<ReplayTape<Empty>> tapes_;
+  std::vector<DView> x_cache_;
+  std::vector<Tensor> x_keep_;
+  size_t scratch_rows_ = 0, cached_rows_ = 0;
+  bool gate_zero_pending_ = false;
+  // per rank: routing (probs fp64 rows x n, sel / pos / rows-by-expert int32,
+  // dlogits fp64), per-expert saved pre1 / h1 / eout segments, scratch
+  std::vector<DeviceBuffer> route_, saved_, scratch_;
+  std::vector<std::vector<size_t>> seg_off_, seg_cnt_;  // per rank: expert segment offsets / counts
+};
+
 // ffn1 (h -> f) -> gelu -> ffn2 (f -> h), composed as model.cpp:77-83,99-105.
 class RtpMlp {
  public:

@@ -165,13 +165,15 @@ class Reference:
                                         _dp, _dp]
         L.ref_rtp_mlp.argtypes = [_sz, C.c_int, C.c_int, _sz, _sz, _sz, _dp, _dp, _dp, _dp, _dp,
                                   _dp, _dp, _dp, _dp, _dp]
+        L.ref_rtp_moe.argtypes = [_sz, C.c_int, _sz, _sz, _sz, _dp, _dp, _dp, _dp, _dp, _dp, _dp, _dp]
+        L.ref_rtp_embedding.argtypes = [_sz, C.c_int, _sz, _sz, _sz, _dp, C.POINTER(C.c_int64), _dp, _dp, _dp]
         L.ref_time_mlp.argtypes = [_sz, C.c_int, _sz, _sz, _sz, _u64, C.c_int, C.POINTER(C.c_double)]
         L.ref_mlp_ledger.argtypes = [_sz, C.c_int, _sz, _sz, _sz, _u64, C.POINTER(_sz), C.POINTER(_sz)]
         L.ref_ring_ops.argtypes = [_sz, C.c_int, C.POINTER(C.c_int), _sz, _sz, _ip, _ip, _dp, _dp]
         L.ref_table1.argtypes = [C.c_int, _u64, _u64, _u64, _u64, _u64, C.POINTER(_u64)]
         for name in ("ref_uniform", "ref_linear_shard", "ref_mlp_params", "ref_serial_linear",
                      "ref_rtp_linear", "ref_rtp_mlp", "ref_time_mlp", "ref_mlp_ledger",
-                     "ref_ring_ops", "ref_table1"):
+                     "ref_ring_ops", "ref_table1", "ref_rtp_moe", "ref_rtp_embedding"):
             getattr(L, name).restype = C.c_int
         self.L = L
 
@@ -238,6 +240,30 @@ class Reference:
         self._chk(self.L.ref_rtp_attention(n, int(concurrent), rows, H, heads, seq, wq, wk, wv, wo, x, dy,
                                            y, dx, g))
         return {"y": y, "dx": dx, "grads": g}
+
+    def rtp_moe(self, n, gate, experts, x, dy, concurrent=False):
+        """experts: list of n (w1, b1, w2, b2)."""
+        gate, x, dy = map(_f64, (gate, x, dy))
+        rows, H = x.shape
+        f = experts[0][0].shape[1]
+        packed = _f64(np.concatenate([np.concatenate([_f64(a).ravel() for a in e]) for e in experts]))
+        L = 2 * H * f + f + H
+        y, dx = np.empty((rows, H)), np.empty((rows, H))
+        g, gg = np.empty((n, L)), np.empty((n, H, n))
+        self._chk(self.L.ref_rtp_moe(n, int(concurrent), rows, H, f, gate, packed, x, dy, y, dx, g, gg))
+        return {"y": y, "dx": dx, "grads": g, "gate_grads": gg}
+
+    def rtp_embedding(self, n, table, ids, dy, concurrent=False):
+        """ids: (n, rows_per_worker) int64."""
+        table, dy = _f64(table), _f64(dy)
+        vocab, emb = table.shape
+        ids = np.ascontiguousarray(ids, np.int64)
+        rpw = ids.shape[1]
+        y = np.empty((n * rpw, emb))
+        g = np.empty((n, vocab * (emb // n)))
+        self._chk(self.L.ref_rtp_embedding(n, int(concurrent), vocab, emb, rpw, table,
+                                           ids.ctypes.data_as(C.POINTER(C.c_int64)), dy, y, g))
+        return {"y": y, "grads": g}
 
     def time_mlp(self, n, rows, h, f, seed=42, iters=1, concurrent=True) -> float:
         s = C.c_double(0)

@@ -340,4 +340,56 @@ int ref_table1(int strategy, uint64_t W, uint64_t G, uint64_t A, uint64_t Ap, ui
   })
 }
 
+// RtpMoe (layers_moe.cpp:18-198): gate (hidden x n), n experts of
+// [w1 (hidden x f) | b1 (f) | w2 (f x hidden) | b2 (hidden)] packed per expert
+// in `experts` (n * (2*hidden*f + f + hidden)); one Train forward + backward
+// from zeroed gradients. grads: n * shard_len; gate_grads: n * hidden * n
+// (per worker, before any data-parallel combine).
+int ref_rtp_moe(size_t n, int transport, size_t rows, size_t hidden, size_t f, const double* gate,
+                const double* experts, const double* x, const double* dy, double* y, double* dx,
+                double* grads, double* gate_grads) {
+  REF_GUARD({
+    WorkerGroup g(n, kind_of(transport));
+    std::vector<ExpertParams> ex(n);
+    const size_t per = 2 * hidden * f + f + hidden;
+    for (size_t e = 0; e < n; ++e) {
+      const double* p = experts + e * per;
+      ex[e].w1 = from_ptr({hidden, f}, p);
+      ex[e].b1 = from_ptr({f}, p + hidden * f);
+      ex[e].w2 = from_ptr({f, hidden}, p + hidden * f + f);
+      ex[e].b2 = from_ptr({hidden}, p + hidden * f + f + f * hidden);
+    }
+    RtpMoe moe(g, "moe", from_ptr({hidden, n}, gate), ex, n);
+    moe.zero_grads();
+    auto ys = moe.forward(shard(from_ptr({rows, hidden}, x), n), Mode::Train);
+    auto dxs = moe.backward(shard(from_ptr({rows, hidden}, dy), n));
+    to_ptr(concat(ys, 0), y);
+    to_ptr(concat(dxs, 0), dx);
+    const size_t L = moe.shard_len();
+    for (size_t r = 0; r < n; ++r) {
+      to_ptr(moe.slots()[r].grad_acc, grads + r * L);
+      to_ptr(moe.gate_grad(r), gate_grads + r * hidden * n);
+    }
+  })
+}
+
+// RtpEmbedding (layers_linear.cpp:74-136): table vocab x emb, ids[r] the
+// rows_per_worker token ids of worker r; Train forward + backward.
+// y: (n * rows_per_worker) x emb, grads: n * shard_len (vocab x emb/n each).
+int ref_rtp_embedding(size_t n, int transport, size_t vocab, size_t emb, size_t rows_per_worker,
+                      const double* table, const int64_t* ids, const double* dy, double* y, double* grads) {
+  REF_GUARD({
+    WorkerGroup g(n, kind_of(transport));
+    RtpEmbedding layer(g, "emb", from_ptr({vocab, emb}, table), n);
+    layer.zero_grads();
+    std::vector<std::vector<int64_t>> id(n);
+    for (size_t r = 0; r < n; ++r) id[r].assign(ids + r * rows_per_worker, ids + (r + 1) * rows_per_worker);
+    auto ys = layer.forward(id, Mode::Train);
+    layer.backward(shard(from_ptr({n * rows_per_worker, emb}, dy), n));
+    to_ptr(concat(ys, 0), y);
+    const size_t L = layer.shard_len();
+    for (size_t r = 0; r < n; ++r) to_ptr(layer.slots()[r].grad_acc, grads + r * L);
+  })
+}
+
 }  // extern "C"

@@ -104,6 +104,29 @@ _SIGS = {
     "rtpb_attention_slot": (_int, [_vp, _sz, C.POINTER(_i64), C.POINTER(_i64)]),
     "rtpb_attention_trace": (_int, [_vp, C.POINTER(_i64)]),
     "rtpb_attention_read_shard": (_int, [_vp, _sz, _int, C.POINTER(_dbl)]),
+    "rtpb_embedding_create": (_int, [_vp, C.c_char_p, _sz, _sz, _int, _vp, _vpp]),
+    "rtpb_embedding_destroy": (_int, [_vp]),
+    "rtpb_embedding_set_rotation_mode": (_int, [_vp, _int]),
+    "rtpb_embedding_allocate_comm_spares": (_int, [_vp]),
+    "rtpb_embedding_release_comm_spares": (_int, [_vp]),
+    "rtpb_embedding_zero_grads": (_int, [_vp]),
+    "rtpb_embedding_shard_len": (_sz, [_vp]),
+    "rtpb_embedding_forward": (_int, [_vp, _vpp, C.POINTER(_sz), _vpp, _int]),
+    "rtpb_embedding_backward": (_int, [_vp, _vpp, _sz]),
+    "rtpb_embedding_slot": (_int, [_vp, _sz, C.POINTER(_i64), C.POINTER(_i64)]),
+    "rtpb_embedding_read_shard": (_int, [_vp, _sz, _int, C.POINTER(_dbl)]),
+    "rtpb_moe_create": (_int, [_vp, C.c_char_p, _sz, _sz, _int, _vp, _vpp, _vpp]),
+    "rtpb_moe_destroy": (_int, [_vp]),
+    "rtpb_moe_set_rotation_mode": (_int, [_vp, _int]),
+    "rtpb_moe_allocate_comm_spares": (_int, [_vp]),
+    "rtpb_moe_release_comm_spares": (_int, [_vp]),
+    "rtpb_moe_zero_grads": (_int, [_vp]),
+    "rtpb_moe_shard_len": (_sz, [_vp]),
+    "rtpb_moe_forward": (_int, [_vp, _vpp, _sz, _vpp, _int]),
+    "rtpb_moe_backward": (_int, [_vp, _vpp, _sz, _vpp]),
+    "rtpb_moe_slot": (_int, [_vp, _sz, C.POINTER(_i64), C.POINTER(_i64)]),
+    "rtpb_moe_read_shard": (_int, [_vp, _sz, _int, C.POINTER(_dbl)]),
+    "rtpb_moe_gate_grad": (_int, [_vp, _sz, C.POINTER(_dbl)]),
     "rtpb_wgrad_step_ex": (_int, [_int, _vp, _sz, _vp, _sz, _sz, _vp, _vp, _sz, _sz, _sz, _int, _vp, _sz, _vp]),
 }
 

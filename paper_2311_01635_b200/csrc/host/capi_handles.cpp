@@ -33,6 +33,14 @@ struct rtpb_attention_s {
   rtpb_group_s* grp;
   std::unique_ptr<RtpAttention> a;
 };
+struct rtpb_embedding_s {
+  rtpb_group_s* grp;
+  std::unique_ptr<RtpEmbedding> e;
+};
+struct rtpb_moe_s {
+  rtpb_group_s* grp;
+  std::unique_ptr<RtpMoe> m;
+};
 struct rtpb_mlp_s {
   rtpb_group_s* grp;
   std::unique_ptr<RtpMlp> m;
@@ -76,6 +84,34 @@ DType dt(int d) {
   return d == RTPB_F32 ? DType::F32 : DType::BF16;
 }
 
+}  // namespace
+
+namespace {
+template <class H>
+int layer_destroy(H* h) {
+  return guard([&] {
+    if (h) {
+      rtpb_group_s* g = h->grp;
+      delete h;
+      group_release(g);
+    }
+  });
+}
+RotationMode rot(int mode) { return mode == RTPB_ROT_OUTOFPLACE ? RotationMode::OutOfPlace : RotationMode::InPlace; }
+void slot_of(RtpLayerBase& l, WorkerGroup& g, size_t rank, int64_t* id, int64_t* off) {
+  if (!g.is_local(rank)) throw IndexError("slot of a non-local rank");
+  ShardSlot& s = l.slots()[rank];
+  if (id) *id = int64_t(s.logical_id);
+  if (off) *off = s.rotation_offset;
+}
+void read_host(RtpLayerBase& l, WorkerGroup& g, size_t rank, int which, double* dst) {
+  if (!g.is_local(rank)) throw IndexError("shard of a non-local rank");
+  if (which) l.materialize_grads();
+  g.synchronize();
+  const Tensor& t = which ? l.slots()[rank].grad_acc : l.slots()[rank].weight;
+  const std::vector<double> v = t.to_host();
+  std::memcpy(dst, v.data(), v.size() * sizeof(double));
+}
 }  // namespace
 
 extern "C" {
@@ -516,6 +552,98 @@ int rtpb_attention_trace(rtpb_attention a, int64_t* ids) {
 int rtpb_attention_read_shard(rtpb_attention a, size_t rank, int which, double* dst) {
   return guard([&] {
     const std::vector<double> v = a->a->shard_host(rank, which != 0);
+    std::memcpy(dst, v.data(), v.size() * sizeof(double));
+  });
+}
+
+int rtpb_embedding_create(rtpb_group g, const char* label, size_t vocab, size_t emb, int dtype, const double* table,
+                          rtpb_embedding* out) {
+  return guard([&] {
+    if (!table) throw DimensionError("embedding_create: table is required");
+    auto h = std::make_unique<rtpb_embedding_s>();
+    h->grp = g;
+    h->e = std::make_unique<RtpEmbedding>(*g->g, label ? label : "emb", table, vocab, emb, g->g->size(), dt(dtype));
+    ++g->refs;
+    *out = h.release();
+  });
+}
+int rtpb_embedding_destroy(rtpb_embedding e) { return layer_destroy(e); }
+int rtpb_embedding_set_rotation_mode(rtpb_embedding e, int mode) {
+  return guard([&] { e->e->set_rotation_mode(rot(mode)); });
+}
+int rtpb_embedding_allocate_comm_spares(rtpb_embedding e) { return guard([&] { e->e->allocate_comm_spares(); }); }
+int rtpb_embedding_release_comm_spares(rtpb_embedding e) { return guard([&] { e->e->release_comm_spares(); }); }
+int rtpb_embedding_zero_grads(rtpb_embedding e) { return guard([&] { e->e->zero_grads(); }); }
+size_t rtpb_embedding_shard_len(rtpb_embedding e) { return e ? e->e->shard_len() : 0; }
+int rtpb_embedding_forward(rtpb_embedding e, const int64_t* const* ids, const size_t* counts, void* const* y,
+                           int mode) {
+  return guard([&] {
+    const size_t k = e->grp->g->local_ranks().size();
+    std::vector<std::vector<int64_t>> v(k);
+    for (size_t i = 0; i < k; ++i) v[i].assign(ids[i], ids[i] + counts[i]);
+    auto yv = views(y, k);
+    e->e->forward(v, yv, mode == RTPB_MODE_EVAL ? Mode::Eval : Mode::Train);
+  });
+}
+int rtpb_embedding_backward(rtpb_embedding e, const void* const* dy, size_t rows) {
+  return guard([&] {
+    const size_t k = e->grp->g->local_ranks().size();
+    auto dyv = views(dy, k);
+    e->e->backward(dyv, rows);
+  });
+}
+int rtpb_embedding_slot(rtpb_embedding e, size_t rank, int64_t* logical_id, int64_t* rotation_offset) {
+  return guard([&] { slot_of(*e->e, *e->grp->g, rank, logical_id, rotation_offset); });
+}
+int rtpb_embedding_read_shard(rtpb_embedding e, size_t rank, int which, double* dst) {
+  return guard([&] { read_host(*e->e, *e->grp->g, rank, which, dst); });
+}
+
+int rtpb_moe_create(rtpb_group g, const char* label, size_t hidden, size_t ffn, int dtype, const double* gate,
+                    const double* const* experts, rtpb_moe* out) {
+  return guard([&] {
+    if (!gate || !experts) throw DimensionError("moe_create: gate and experts are required");
+    auto h = std::make_unique<rtpb_moe_s>();
+    h->grp = g;
+    h->m = std::make_unique<RtpMoe>(*g->g, label ? label : "moe", gate, experts, hidden, ffn, g->g->size(),
+                                    dt(dtype));
+    ++g->refs;
+    *out = h.release();
+  });
+}
+int rtpb_moe_destroy(rtpb_moe m) { return layer_destroy(m); }
+int rtpb_moe_set_rotation_mode(rtpb_moe m, int mode) { return guard([&] { m->m->set_rotation_mode(rot(mode)); }); }
+int rtpb_moe_allocate_comm_spares(rtpb_moe m) { return guard([&] { m->m->allocate_comm_spares(); }); }
+int rtpb_moe_release_comm_spares(rtpb_moe m) { return guard([&] { m->m->release_comm_spares(); }); }
+int rtpb_moe_zero_grads(rtpb_moe m) { return guard([&] { m->m->zero_grads(); }); }
+size_t rtpb_moe_shard_len(rtpb_moe m) { return m ? m->m->shard_len() : 0; }
+int rtpb_moe_forward(rtpb_moe m, const void* const* x, size_t rows, void* const* y, int mode) {
+  return guard([&] {
+    const size_t k = m->grp->g->local_ranks().size();
+    auto xv = views(x, k);
+    auto yv = views(y, k);
+    m->m->forward(xv, rows, yv, mode == RTPB_MODE_EVAL ? Mode::Eval : Mode::Train);
+  });
+}
+int rtpb_moe_backward(rtpb_moe m, const void* const* dy, size_t rows, void* const* dx) {
+  return guard([&] {
+    const size_t k = m->grp->g->local_ranks().size();
+    auto dyv = views(dy, k);
+    auto dxv = views(dx, k);
+    m->m->backward(dyv, rows, dxv);
+  });
+}
+int rtpb_moe_slot(rtpb_moe m, size_t rank, int64_t* logical_id, int64_t* rotation_offset) {
+  return guard([&] { slot_of(*m->m, *m->grp->g, rank, logical_id, rotation_offset); });
+}
+int rtpb_moe_read_shard(rtpb_moe m, size_t rank, int which, double* dst) {
+  return guard([&] { read_host(*m->m, *m->grp->g, rank, which, dst); });
+}
+int rtpb_moe_gate_grad(rtpb_moe m, size_t rank, double* dst) {
+  return guard([&] {
+    if (!m->grp->g->is_local(rank)) throw IndexError("gate gradient of a non-local rank");
+    m->grp->g->synchronize();
+    const std::vector<double> v = m->m->gate_grad(rank).to_host();
     std::memcpy(dst, v.data(), v.size() * sizeof(double));
   });
 }

@@ -160,6 +160,23 @@ int attention_core_fwd(bool f32, const void* q, const void* k, const void* v, vo
 int attention_core_bwd(bool f32, const void* q, const void* k, const void* v, const void* o, const float* lse,
                        const void* dout, void* dq, void* dk, void* dv, float* delta, size_t rows, size_t seq,
                        size_t g, size_t hd, float scale, cudaStream_t s);
+// moe_embed.cu: RtpMoe routing / combine and RtpEmbedding gather / scatter.
+int moe_gate(bool f32, const void* x, size_t rows, size_t H, const double* gate, size_t n, double* probs, int* sel,
+             cudaStream_t s);
+int gather_rows(bool f32, const void* src, size_t lds, const int* idx, size_t cnt, size_t cols, void* dst,
+                cudaStream_t s);
+int moe_combine(bool f32, const void* eout, const int* pos, const int* sel, const double* probs, size_t n, size_t rows,
+                size_t H, void* y, size_t ldy, cudaStream_t s);
+int moe_route_bwd(bool f32, const void* dy, size_t ldy, const void* eout, const int* rows_j, size_t cnt, size_t j,
+                  const double* probs, size_t n, size_t H, void* de, double* dlogits, cudaStream_t s);
+int moe_dx(bool f32, const void* dxs, const int* pos, const double* dlogits, const double* gate, size_t n, size_t rows,
+           size_t H, void* dx, size_t ldx, cudaStream_t s);
+int moe_gate_grad(bool f32, const void* x, size_t ldx, const double* dlogits, size_t n, size_t rows, size_t H,
+                  double* gg, bool accumulate, cudaStream_t s);
+int embed_gather(bool f32, const void* block, size_t per, const int64_t* ids, size_t cnt, void* y, size_t ldy,
+                 size_t col0, cudaStream_t s);
+int embed_scatter(bool f32, const void* dy, size_t ldy, size_t col0, const int64_t* uniq, const int* offs,
+                  const int* toks, size_t nuniq, size_t per, float* grad, cudaStream_t s);
 // dtype codes RTPB_BF16 / RTPB_F32 / RTPB_F64
 int convert(const void* src, int src_dtype, void* dst, int dst_dtype, size_t count, cudaStream_t s);
 int fill(void* dst, int dtype, size_t count, double v, cudaStream_t s);

@@ -16,7 +16,7 @@ import ctypes as C
 import torch
 
 from . import _lib
-from ._lib import (BF16, F32, ConfigError, DimensionError, ProtocolError, RtpError,  # noqa: F401
+from ._lib import (BF16, F32, ConfigError, DimensionError, IndexError_, ProtocolError, RtpError,  # noqa: F401
                    StateError, check, lib, ptr_array)
 
 _DT = {"bf16": BF16, "f32": F32, BF16: BF16, F32: F32}
@@ -465,6 +465,163 @@ class RtpAttention(_Layer):
     def close(self):
         if getattr(self, "_h", None):
             lib.rtpb_attention_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def _read_host(fn, h, rank, which, count):
+    import numpy as np
+    out = np.empty(count, dtype=np.float64)
+    check(fn(h, rank, which, out.ctypes.data_as(C.POINTER(C.c_double))))
+    return out
+
+
+class RtpEmbedding(_Layer):
+    """RtpEmbedding(group, label, table, n) (layers.hpp:150-168,
+    layers_linear.cpp:74-136): table (vocab x emb, host fp64) sharded on the
+    embedding dimension. forward(ids) takes host int64 id lists, one per
+    local worker; backward(dy) has no input gradient."""
+
+    def __init__(self, group: WorkerGroup, label: str, table, dtype="bf16"):
+        t = _as_host_f64(table)
+        self.group, self.label = group, label
+        self.vocab, self.emb = t.shape
+        self.dtype_code = _DT[dtype]
+        h = C.c_void_p()
+        check(lib.rtpb_embedding_create(group._h, label.encode(), self.vocab, self.emb, self.dtype_code,
+                                        t.ctypes.data, C.byref(h)))
+        self._h = h
+
+    def shard_len(self) -> int:
+        return int(lib.rtpb_embedding_shard_len(self._h))
+
+    def set_rotation_mode(self, mode: str):
+        check(lib.rtpb_embedding_set_rotation_mode(self._h, {"inplace": 0, "outofplace": 1}[mode]))
+
+    def allocate_comm_spares(self):
+        check(lib.rtpb_embedding_allocate_comm_spares(self._h))
+
+    def zero_grads(self):
+        check(lib.rtpb_embedding_zero_grads(self._h))
+
+    def forward(self, ids, mode: str = "train"):
+        import numpy as np
+        arrs = [np.ascontiguousarray(np.asarray(v, dtype=np.int64)) for v in ids]
+        if len(arrs) != len(self.group.local_ranks):
+            raise DimensionError("expected one id list per local worker")
+        ys = [torch.empty(len(a), self.emb, dtype=_TORCH_DT[self.dtype_code], device=self.group.device_of(r))
+              for a, r in zip(arrs, self.group.local_ranks)]
+        self.group._enter(None)
+        ptrs = (C.c_void_p * len(arrs))(*[a.ctypes.data for a in arrs])
+        counts = (C.c_size_t * len(arrs))(*[len(a) for a in arrs])
+        check(lib.rtpb_embedding_forward(self._h, ptrs, counts, ptr_array(ys),
+                                         _lib.MODE_EVAL if mode == "eval" else _lib.MODE_TRAIN))
+        self.group._leave()
+        return ys
+
+    def backward(self, dys):
+        rows = self._check_inputs(dys, self.emb)
+        self.group._enter(None)
+        check(lib.rtpb_embedding_backward(self._h, ptr_array(dys), rows))
+        self.group._leave()
+
+    def slot(self, rank: int) -> dict:
+        lid, off = C.c_int64(), C.c_int64()
+        check(lib.rtpb_embedding_slot(self._h, rank, C.byref(lid), C.byref(off)))
+        return {"logical_id": lid.value, "rotation_offset": off.value}
+
+    def shard(self, rank: int, grad: bool = False):
+        return _read_host(lib.rtpb_embedding_read_shard, self._h, rank, int(grad), self.shard_len())
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib.rtpb_embedding_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class RtpMoe(_Layer):
+    """RtpMoe(group, label, gate, experts, n) (layers.hpp:193-229,
+    layers_moe.cpp:18-198): top-1 gating (gate hidden x n, replicated),
+    one expert (w1, b1, w2, b2) per worker; experts rotate past the batch."""
+
+    def __init__(self, group: WorkerGroup, label: str, gate, experts, dtype="bf16"):
+        import numpy as np
+        g = _as_host_f64(gate)
+        if len(experts) != group.n:
+            raise ConfigError(f"moe_shard_groups: {len(experts)} experts for {group.n} shards")
+        if g.ndim != 2 or g.shape[1] != group.n:
+            raise ConfigError(f"gate weight {g.shape} must have one column per expert ({group.n})")
+        self.group, self.label = group, label
+        self.hidden = g.shape[0]
+        self.ffn = np.asarray(experts[0][0]).shape[1]
+        self.dtype_code = _DT[dtype]
+        self._packed = [np.ascontiguousarray(np.concatenate([_as_host_f64(a).ravel() for a in e])) for e in experts]
+        ptrs = (C.c_void_p * len(self._packed))(*[p.ctypes.data for p in self._packed])
+        h = C.c_void_p()
+        check(lib.rtpb_moe_create(group._h, label.encode(), self.hidden, self.ffn, self.dtype_code, g.ctypes.data,
+                                  ptrs, C.byref(h)))
+        self._h = h
+
+    def shard_len(self) -> int:
+        return int(lib.rtpb_moe_shard_len(self._h))
+
+    def set_rotation_mode(self, mode: str):
+        check(lib.rtpb_moe_set_rotation_mode(self._h, {"inplace": 0, "outofplace": 1}[mode]))
+
+    def allocate_comm_spares(self):
+        check(lib.rtpb_moe_allocate_comm_spares(self._h))
+
+    def zero_grads(self):
+        check(lib.rtpb_moe_zero_grads(self._h))
+
+    def forward(self, xs, mode: str = "train", out=None):
+        rows = self._check_inputs(xs, self.hidden)
+        ys = out if out is not None else self._acts(rows, self.hidden)
+        self.group._enter(None)
+        check(lib.rtpb_moe_forward(self._h, ptr_array(xs), rows, ptr_array(ys),
+                                   _lib.MODE_EVAL if mode == "eval" else _lib.MODE_TRAIN))
+        self.group._leave()
+        if mode != "eval":
+            self._x_keep = list(xs)
+        return ys
+
+    def backward(self, dys, out=None):
+        rows = self._check_inputs(dys, self.hidden)
+        dxs = out if out is not None else self._acts(rows, self.hidden)
+        self.group._enter(None)
+        check(lib.rtpb_moe_backward(self._h, ptr_array(dys), rows, ptr_array(dxs)))
+        self.group._leave()
+        self._x_keep = None
+        return dxs
+
+    def slot(self, rank: int) -> dict:
+        lid, off = C.c_int64(), C.c_int64()
+        check(lib.rtpb_moe_slot(self._h, rank, C.byref(lid), C.byref(off)))
+        return {"logical_id": lid.value, "rotation_offset": off.value}
+
+    def shard(self, rank: int, grad: bool = False):
+        return _read_host(lib.rtpb_moe_read_shard, self._h, rank, int(grad), self.shard_len())
+
+    def gate_grad(self, rank: int):
+        import numpy as np
+        out = np.empty((self.hidden, self.group.n), dtype=np.float64)
+        check(lib.rtpb_moe_gate_grad(self._h, rank, out.ctypes.data_as(C.POINTER(C.c_double))))
+        return out
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib.rtpb_moe_destroy(self._h)
             self._h = None
 
     def __del__(self):

@@ -129,6 +129,53 @@ def main():
             att[f"n{nn}_{k}"] = v
     out["attention"] = att
 
+    # 4c. RtpMoe (layers_moe.cpp:18-198): top-1 gating over N
+    #     experts that rotate past the batch. X (and dY) are bf16-representable
+    #     values so a bf16 device run sees the reference's exact routing inputs.
+    H, F = 32, 64
+    moe = {"hidden": H, "ffn": F}
+    import sys as _s
+    _s.path.insert(0, os.path.join(ROOT, "tests"))
+    from helpers import bf16_round
+    for nn in (1, 2, 4):
+        p = R.uniform(4242 + nn, 0, H * nn + nn * (2 * H * F + F + H), -0.1, 0.1)
+        gate = p[:H * nn].reshape(H, nn)
+        experts, off = [], H * nn
+        for e in range(nn):
+            w1 = p[off:off + H * F].reshape(H, F); off += H * F
+            b1 = p[off:off + F]; off += F
+            w2 = p[off:off + F * H].reshape(F, H); off += F * H
+            b2 = p[off:off + H]; off += H
+            experts.append((w1, b1, w2, b2))
+        rows_m = nn * 16
+        xm, dym = acts(R, 77 + nn, rows_m, H, H)
+        xm, dym = bf16_round(xm), bf16_round(dym)
+        r = R.rtp_moe(nn, gate, experts, xm, dym)
+        rc = R.rtp_moe(nn, gate, experts, xm, dym, concurrent=True)
+        assert all(np.array_equal(r[k], rc[k]) for k in r), "lockstep != concurrent"
+        moe[f"n{nn}_gate"] = gate
+        moe[f"n{nn}_experts"] = np.stack([np.concatenate([a.ravel() for a in e]) for e in experts])
+        moe[f"n{nn}_x"], moe[f"n{nn}_dy"] = xm, dym
+        for k, v in r.items():
+            moe[f"n{nn}_{k}"] = v
+    out["moe"] = moe
+
+    # 4d. RtpEmbedding (layers_linear.cpp:74-136): table sharded on the
+    #     embedding dimension, repeated ids (scatter-add order), N in {1,2,4}.
+    vocab, emb, rpw = 64, 32, 16
+    table = R.uniform(99, 0, vocab * emb, -0.1, 0.1).reshape(vocab, emb)
+    embd = {"table": table}
+    rng_ids = np.random.default_rng(5)
+    for nn in (1, 2, 4):
+        ids = rng_ids.integers(0, vocab, size=(nn, rpw)).astype(np.int64)
+        ids[:, 1] = ids[:, 0]  # a repeated id on every worker
+        dye = R.uniform(100 + nn, 0, nn * rpw * emb, -1, 1).reshape(nn * rpw, emb)
+        r = R.rtp_embedding(nn, table, ids, dye)
+        embd[f"n{nn}_ids"], embd[f"n{nn}_dy"] = ids, dye
+        for k, v in r.items():
+            embd[f"n{nn}_{k}"] = v
+    out["embedding"] = embd
+
     # 5. Ring primitive (ring.cpp:265-293) on id-encoded slots (ring_test.cpp:16-28)
     rng = np.random.default_rng(77)
     ring = {}
