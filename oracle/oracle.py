@@ -167,13 +167,14 @@ class Reference:
                                   _dp, _dp, _dp, _dp, _dp]
         L.ref_rtp_moe.argtypes = [_sz, C.c_int, _sz, _sz, _sz, _dp, _dp, _dp, _dp, _dp, _dp, _dp, _dp]
         L.ref_rtp_embedding.argtypes = [_sz, C.c_int, _sz, _sz, _sz, _dp, C.POINTER(C.c_int64), _dp, _dp, _dp]
+        L.ref_cmd_csv.argtypes = [C.c_int, _sz, C.c_char_p, _sz, C.c_char_p, _sz]
         L.ref_time_mlp.argtypes = [_sz, C.c_int, _sz, _sz, _sz, _u64, C.c_int, C.POINTER(C.c_double)]
         L.ref_mlp_ledger.argtypes = [_sz, C.c_int, _sz, _sz, _sz, _u64, C.POINTER(_sz), C.POINTER(_sz)]
         L.ref_ring_ops.argtypes = [_sz, C.c_int, C.POINTER(C.c_int), _sz, _sz, _ip, _ip, _dp, _dp]
         L.ref_table1.argtypes = [C.c_int, _u64, _u64, _u64, _u64, _u64, C.POINTER(_u64)]
         for name in ("ref_uniform", "ref_linear_shard", "ref_mlp_params", "ref_serial_linear",
                      "ref_rtp_linear", "ref_rtp_mlp", "ref_time_mlp", "ref_mlp_ledger",
-                     "ref_ring_ops", "ref_table1", "ref_rtp_moe", "ref_rtp_embedding"):
+                     "ref_ring_ops", "ref_table1", "ref_rtp_moe", "ref_rtp_embedding", "ref_cmd_csv"):
             getattr(L, name).restype = C.c_int
         self.L = L
 
@@ -264,6 +265,13 @@ class Reference:
         self._chk(self.L.ref_rtp_embedding(n, int(concurrent), vocab, emb, rpw, table,
                                            ids.ctypes.data_as(C.POINTER(C.c_int64)), dy, y, g))
         return {"y": y, "grads": g}
+
+    def cmd_csv(self, which: str, n: int, strategy: str, batch: int) -> str:
+        """CSV text of the reference's `rtpsim memtable|ledger|sweep` commands."""
+        buf = C.create_string_buffer(1 << 20)
+        code = {"memtable": 0, "ledger": 1, "sweep": 2}[which]
+        self._chk(self.L.ref_cmd_csv(code, n, strategy.encode(), batch, buf, len(buf)))
+        return buf.value.decode()
 
     def time_mlp(self, n, rows, h, f, seed=42, iters=1, concurrent=True) -> float:
         s = C.c_double(0)

@@ -15,7 +15,11 @@
 #include <string>
 #include <vector>
 
+#include <sstream>
+
 #include "rtp/analysis.hpp"
+#include "rtp/commands.hpp"
+#include "rtp/config.hpp"
 #include "rtp/layers.hpp"
 #include "rtp/ledger.hpp"
 #include "rtp/model.hpp"
@@ -389,6 +393,31 @@ int ref_rtp_embedding(size_t n, int transport, size_t vocab, size_t emb, size_t 
     to_ptr(concat(ys, 0), y);
     const size_t L = layer.shard_len();
     for (size_t r = 0; r < n; ++r) to_ptr(layer.slots()[r].grad_acc, grads + r * L);
+  })
+}
+
+// The reference's own report commands (commands.cpp:87-181): which 0 =
+// cmd_memtable (analytic, no literals), 1 = cmd_ledger, 2 = cmd_sweep over
+// per-worker batches {1, 2}; default ExperimentConfig with n_workers, strategy
+// and batch_size set. The CSV text is copied into out (NUL-terminated).
+int ref_cmd_csv(int which, size_t n, const char* strategy, size_t batch, char* out, size_t cap) {
+  REF_GUARD({
+    ExperimentConfig cfg;
+    cfg.n_workers = n;
+    cfg.strategy = strategy;
+    cfg.batch_size = batch;
+    std::ostringstream csv, summary;
+    if (which == 0) {
+      cmd_memtable(cfg, std::nullopt, csv);
+    } else if (which == 1) {
+      cmd_ledger(cfg, csv, summary);
+    } else {
+      const size_t b[2] = {1, 2};
+      cmd_sweep(cfg, b, csv);
+    }
+    const std::string t = csv.str();
+    if (t.size() + 1 > cap) throw DimensionError("ref_cmd_csv: output buffer too small");
+    std::memcpy(out, t.c_str(), t.size() + 1);
   })
 }
 

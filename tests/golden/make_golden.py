@@ -200,6 +200,17 @@ def main():
             led[f"table1_s{st}_N{N}"] = np.array(R.table1(st, 1000, 2000, 300, 40, N), np.int64)
     out["ledger"] = led
 
+    # 7. The reference's report commands (commands.cpp:87-181) as CSV text:
+    #    the schemas the device reports (paper_2311_01635_b200/reports.py) keep.
+    import json
+    reports = {}
+    for which in ("memtable", "ledger", "sweep"):
+        for nn in (2, 4):
+            for strat in ("rtp-inplace", "rtp-outofplace"):
+                reports[f"{which}_n{nn}_{strat}"] = R.cmd_csv(which, nn, strat, 8)
+    with open(os.path.join(HERE, "reports.json"), "w") as fh:
+        json.dump(reports, fh, indent=1, sort_keys=True)
+
     only = sys.argv[1:]  # e.g. `make_golden.py attention`: rewrite only those fixtures
     for name, d in out.items():
         if only and name not in only:

@@ -19,7 +19,7 @@ import sys
 import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-from paper_2311_01635_b200 import rtp  # noqa: E402
+from paper_2311_01635_b200 import reports, rtp  # noqa: E402
 
 CATS = ("Param", "Grad", "Activation", "CommBuffer", "Other")
 KEYS = ("param", "grad", "activation", "comm", "other")
@@ -63,20 +63,15 @@ def main():
     runs = [("serial", 1, serial)]
     for strat, mode in (("rtp-inplace", "inplace"), ("rtp-outofplace", "outofplace")):
         runs.append((strat, args.n, run(args.n, mode, args.rows // args.n, args.h, args.f)))
-    lines = ["strategy,n,category,peak_bytes,duplication"]
-    for strat, n, pk in runs:
-        for c in CATS:
-            lines.append(f"{strat},{n},{c},{pk[c]},{n * pk[c] - serial[c]}")
-    ledger = "\n".join(lines) + "\n"
-
-    lines = ["strategy,n,batch_per_worker,global_batch,param_peak,grad_peak,activation_peak,"
-             "commbuffer_peak,other_peak,total_peak"]
+    ledger = reports.ledger_csv(serial, runs[1:])
+    sweep = ""
     for strat, mode in (("rtp-inplace", "inplace"), ("rtp-outofplace", "outofplace")):
+        pts = []
         for b in (int(v) for v in args.sweep.split(",")):
             pk = run(args.n, mode, b, args.h, args.f)
-            lines.append(f"{strat},{args.n},{b},{b * args.n},{pk['Param']},{pk['Grad']},{pk['Activation']},"
-                         f"{pk['CommBuffer']},{pk['Other']},{pk['total']}")
-    sweep = "\n".join(lines) + "\n"
+            pts.append((b, pk, pk["total"]))
+        text = reports.sweep_csv(strat, args.n, pts)
+        sweep += text if not sweep else text.split("\n", 1)[1]
     if args.out:
         os.makedirs(args.out, exist_ok=True)
         open(os.path.join(args.out, "ledger.csv"), "w").write(ledger)
