@@ -54,6 +54,7 @@ extern "C" {
 #define RTPB_EPI_GELU_BWD 8  /* dgrad last step: dX *= gelu'(pre) (model.cpp:101-104)   */
 #define RTPB_EPI_STORE_PRE 16 /* fwd: write X.W_j + b_j to `y` (default for plain linear) */
 #define RTPB_EPI_NO_BIAS 32   /* fwd / wgrad_ex: the shard block has no bias part (projections) */
+#define RTPB_EPI_EXACT_GELU 64 /* bf16: exact-erf GELU / GELU' in the epilogue (default: tanh.approx form) */
 
 const char* rtpb_last_error(void);
 const char* rtpb_version(void);
@@ -279,6 +280,16 @@ int rtpb_linear_trace(rtpb_linear l, int64_t* ids);
 /* Synchronous copy of the shard resident at local rank r into dst (device
  * memory): which 0 = weight [W_j | b_j] (layer dtype), 1 = grad_acc (fp32). */
 int rtpb_linear_read_shard(rtpb_linear l, size_t rank, int which, void* dst);
+/* Numerics options of a layer (and of both layers of an MLP):
+ *  RTPB_OPT_EXACT_GELU (default 0): bf16 epilogues evaluate the exact-erf
+ *    GELU / GELU' (tensor.cpp:323-351) instead of the tanh.approx form.
+ *  RTPB_OPT_PAIRED_DX (default 1, or RTPB_DX_PAIR): out-of-place bf16
+ *    backward runs two steps' dX as one GEMM over the two resident shards;
+ *    0 restores the reference's per-step summation (out-of-place ==
+ *    in-place bitwise, layers_test.cpp:343-365). */
+#define RTPB_OPT_EXACT_GELU 1
+#define RTPB_OPT_PAIRED_DX 2
+int rtpb_linear_set_option(rtpb_linear l, int option, int value);
 
 /* The FFN block (model.cpp:77-83, 99-105): ffn1 (h->f) -> gelu -> ffn2 (f->h),
  * GELU fused into ffn1's forward epilogue and ffn2's last dX epilogue.
@@ -297,6 +308,7 @@ int rtpb_mlp_backward(rtpb_mlp m, const void* const* dy, size_t rows, void* cons
  * follows `m` in forward. Linked blocks post the neighbour's first weight
  * shift under their own last step (out-of-place mode). next = NULL unlinks. */
 int rtpb_mlp_chain(rtpb_mlp m, rtpb_mlp next);
+int rtpb_mlp_set_option(rtpb_mlp m, int option, int value); /* RTPB_OPT_*, both layers */
 /* layer 0 = ffn1, 1 = ffn2 */
 rtpb_linear rtpb_mlp_layer(rtpb_mlp m, int layer);
 

@@ -402,6 +402,13 @@ class RtpLayerBase {
   void release_comm_spares();
   bool has_comm_spares() const { return !spares_.empty(); }
   void set_rotation_mode(RotationMode m);
+  // Numerics options (rtpb.h RTPB_OPT_*): exact-erf GELU in bf16 epilogues
+  // (default: tanh.approx form); paired dX steps out of place (default on,
+  // or RTPB_DX_PAIR; off restores out-of-place == in-place bitwise).
+  void set_exact_gelu(bool on) { exact_gelu_ = on; }
+  bool exact_gelu() const { return exact_gelu_; }
+  void set_paired_dx(bool on) { paired_dx_ = on; }
+  bool paired_dx() const { return paired_dx_; }
   RotationMode rotation_mode() const { return rotation_mode_; }
   // Logical id seen by (phase 0 fwd / 1 bwd, step, rank) in the last pass.
   const std::vector<int64_t>& trace() const { return trace_; }
@@ -427,6 +434,8 @@ class RtpLayerBase {
   size_t shard_len_ = 0;
   size_t flag_base_ = 0;  // this layer's block of the workers' shard-arrival flags
   RotationMode rotation_mode_ = RotationMode::InPlace;
+  bool exact_gelu_ = false;
+  bool paired_dx_ = true;  // initialised from RTPB_DX_PAIR
   std::vector<int64_t> trace_;
   bool grads_zero_pending_ = false;
 };
@@ -684,6 +693,8 @@ class RtpMlp {
          uint64_t stream_base);
 
   void set_rotation_mode(RotationMode m);
+  void set_exact_gelu(bool on);  // both layers and the fused N = 1 launches
+  void set_paired_dx(bool on);   // both layers
   void begin_step();  // RtpModel::begin_step (model.cpp:54-57)
   void zero_grads();
   void forward(std::span<const DView> x, size_t rows, std::span<const DView> y, Mode mode);

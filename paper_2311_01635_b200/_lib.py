@@ -127,6 +127,8 @@ _SIGS = {
     "rtpb_moe_slot": (_int, [_vp, _sz, C.POINTER(_i64), C.POINTER(_i64)]),
     "rtpb_moe_read_shard": (_int, [_vp, _sz, _int, C.POINTER(_dbl)]),
     "rtpb_moe_gate_grad": (_int, [_vp, _sz, C.POINTER(_dbl)]),
+    "rtpb_linear_set_option": (_int, [_vp, _int, _int]),
+    "rtpb_mlp_set_option": (_int, [_vp, _int, _int]),
     "rtpb_wgrad_step_ex": (_int, [_int, _vp, _sz, _vp, _sz, _sz, _vp, _vp, _sz, _sz, _sz, _int, _vp, _sz, _vp]),
 }
 

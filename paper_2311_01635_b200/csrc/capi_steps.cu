@@ -128,7 +128,7 @@ void count_launch(uint64_t n) { g_launches.fetch_add(n, std::memory_order_relaxe
 
 int fused_fwd_step(const void* x, size_t ldx, const void* w1_shard, void* pre, void* act, const void* w2_shard,
                    void* y, size_t ldy, size_t M, size_t h, size_t f, bool store_pre, const FusedFwdPlan& plan,
-                   const FusedFwdWs& ws, cudaStream_t s) {
+                   const FusedFwdWs& ws, cudaStream_t s, bool exact_gelu) {
   int rc;
   if ((rc = check_geom(M, h, f))) return rc;
   const auto* w1 = static_cast<const uint16_t*>(w1_shard);  // bf16 elements
@@ -137,7 +137,7 @@ int fused_fwd_step(const void* x, size_t ldx, const void* w1_shard, void* pre, v
   p0.x = x; p0.ldx = ldx; p0.w = w1; p0.bias = w1 + h * f;
   p0.y = pre; p0.ldy = f; p0.act = act; p0.ld_act = f;
   p0.M = M; p0.I = h; p0.per = f;
-  p0.flags = RTPB_EPI_GELU | (store_pre ? RTPB_EPI_STORE_PRE : 0);
+  p0.flags = RTPB_EPI_GELU | (store_pre ? RTPB_EPI_STORE_PRE : 0) | (exact_gelu ? RTPB_EPI_EXACT_GELU : 0);
   StepFwd p1{};
   p1.x = act; p1.ldx = f; p1.w = w2; p1.bias = w2 + f * h;
   p1.y = y; p1.ldy = ldy; p1.M = M; p1.I = f; p1.per = h; p1.flags = RTPB_EPI_STORE_PRE;

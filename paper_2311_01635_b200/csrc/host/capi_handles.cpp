@@ -648,4 +648,26 @@ int rtpb_moe_gate_grad(rtpb_moe m, size_t rank, double* dst) {
   });
 }
 
+int rtpb_linear_set_option(rtpb_linear l, int option, int value) {
+  return guard([&] {
+    if (option == RTPB_OPT_EXACT_GELU)
+      l->l->set_exact_gelu(value != 0);
+    else if (option == RTPB_OPT_PAIRED_DX)
+      l->l->set_paired_dx(value != 0);
+    else
+      throw ConfigError("unknown option " + std::to_string(option));
+  });
+}
+
+int rtpb_mlp_set_option(rtpb_mlp m, int option, int value) {
+  return guard([&] {
+    if (option == RTPB_OPT_EXACT_GELU)
+      m->m->set_exact_gelu(value != 0);
+    else if (option == RTPB_OPT_PAIRED_DX)
+      m->m->set_paired_dx(value != 0);
+    else
+      throw ConfigError("unknown option " + std::to_string(option));
+  });
+}
+
 }  // extern "C"

@@ -138,7 +138,7 @@ class SmReserve {
 
 // ------------------------------------------------------------------ base
 RtpLayerBase::RtpLayerBase(WorkerGroup& group, std::string label, DType dtype)
-    : group_(&group), label_(std::move(label)), dtype_(dtype) {
+    : group_(&group), label_(std::move(label)), dtype_(dtype), paired_dx_(dx_pair_enabled()) {
   // one block of arrival flags per layer (forward W, backward W, backward G
   // for up to 16 steps), reused cyclically across the pool
   static std::atomic<size_t> next_layer{0};
@@ -495,7 +495,7 @@ void RtpLinear::forward_impl(std::span<const DView> x, size_t rows, std::span<co
       void* act = nullptr;
       size_t ld_act = 0;
       if (!e.act.empty()) {
-        flags |= RTPB_EPI_GELU;
+        flags |= RTPB_EPI_GELU | (exact_gelu_ ? RTPB_EPI_EXACT_GELU : 0);
         act = e.act[k].data;
         ld_act = e.act[k].ld ? e.act[k].ld : out_;
       }
@@ -690,7 +690,7 @@ void RtpLinear::backward_impl(std::span<const DView> dy, size_t rows, std::span<
     const void* pre = nullptr;
     size_t ldpre = 0;
     if (gelu) {
-      flags |= RTPB_EPI_GELU_BWD;
+      flags |= RTPB_EPI_GELU_BWD | (exact_gelu_ ? RTPB_EPI_EXACT_GELU : 0);
       pre = e.pre[0].data;
       ldpre = e.pre[0].ld ? e.pre[0].ld : in_;
     }
@@ -732,7 +732,7 @@ void RtpLinear::backward_impl(std::span<const DView> dy, size_t rows, std::span<
   // reference's layers_test property holds with RTPB_DX_PAIR=0).
   // (with arrival flags the paired dX waits on its own step's flag: the
   // spare's shard came through the same comm stream earlier)
-  const bool pair = oopm && n > 1 && dtype_ == DType::BF16 && dx_pair_enabled();
+  const bool pair = oopm && n > 1 && dtype_ == DType::BF16 && paired_dx_;
   auto paired = [&](size_t s) { return pair && s % 2 == 1; };
   auto has_dx = [&](size_t s) { return !pair || s % 2 == 1 || s + 1 == n; };
   const size_t first_dx = pair ? 1 : 0;
@@ -773,7 +773,7 @@ void RtpLinear::backward_impl(std::span<const DView> dy, size_t rows, std::span<
       const void* pre = nullptr;
       size_t ldpre = 0;
       if (!e.pre.empty() && s + 1 == n) {
-        flags |= RTPB_EPI_GELU_BWD;
+        flags |= RTPB_EPI_GELU_BWD | (exact_gelu_ ? RTPB_EPI_EXACT_GELU : 0);
         pre = e.pre[k].data;
         ldpre = e.pre[k].ld ? e.pre[k].ld : in_;
       }
@@ -897,6 +897,16 @@ void RtpMlp::set_rotation_mode(RotationMode m) {
   ffn2_->set_rotation_mode(m);
 }
 
+void RtpMlp::set_exact_gelu(bool on) {
+  ffn1_->set_exact_gelu(on);
+  ffn2_->set_exact_gelu(on);
+}
+
+void RtpMlp::set_paired_dx(bool on) {
+  ffn1_->set_paired_dx(on);
+  ffn2_->set_paired_dx(on);
+}
+
 void RtpMlp::begin_step() {
   if (mode_ == RotationMode::OutOfPlace) {
     if (!ffn1_->has_comm_spares()) ffn1_->allocate_comm_spares();
@@ -992,7 +1002,8 @@ void RtpMlp::forward(std::span<const DView> x, size_t rows, std::span<const DVie
                   fused_splits2_ > 1 ? reinterpret_cast<float*>(reinterpret_cast<char*>(base) + fused_acc_off_)
                                      : nullptr};
     check_status(fused_fwd_step(x[0].data, x[0].ld ? x[0].ld : h_, w1, preb[r].data(), actb[r].data(), w2,
-                                y[0].data, y[0].ld ? y[0].ld : h_, rows, h_, f_, train, plan, ws, w.compute));
+                                y[0].data, y[0].ld ? y[0].ld : h_, rows, h_, f_, train, plan, ws, w.compute,
+                                ffn1_->exact_gelu()));
     if (train) saved_rows_ = rows;
     return;
   }
@@ -1085,6 +1096,7 @@ void RtpMlp::backward(std::span<const DView> dy, size_t rows, std::span<const DV
     a.w1 = b1.weight; a.w2 = b2.weight;
     a.g1 = b1.grad; a.g2 = b2.grad; a.g1_zero = b1.grad_zero; a.g2_zero = b2.grad_zero;
     a.M = rows; a.h = h_; a.f = f_;
+    a.exact_gelu = ffn2_->exact_gelu();
     int* base = static_cast<int*>(fused_bwd_ws_.data());
     unsigned* dep = reinterpret_cast<unsigned*>(base + fused_bwd_sd_ints_ + fused_bwd_sw_ints_);
     FusedBwdPlan plan;

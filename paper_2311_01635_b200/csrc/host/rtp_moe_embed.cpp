@@ -391,7 +391,9 @@ void RtpMoe::forward(std::span<const DView> x, size_t rows, std::span<const DVie
       check_status(gather_rows(f32, x[k].data, x[k].ld ? x[k].ld : H, byexp, cnt, H, xs, w.compute));
       // expert j: h1 = gelu(xs W1 + b1) (GELU fused), eout = h1 W2 + b2  (:80-88)
       check_status(rtpb_fwd_step(dt, xs, H, W, pre1, F, 0, h1, F, cnt, H, F,
-                                 (train ? RTPB_EPI_STORE_PRE : 0) | RTPB_EPI_GELU, ws, ws_bytes, w.compute));
+                                 (train ? RTPB_EPI_STORE_PRE : 0) | RTPB_EPI_GELU |
+                                     (exact_gelu_ ? RTPB_EPI_EXACT_GELU : 0),
+                                 ws, ws_bytes, w.compute));
       check_status(rtpb_fwd_step(dt, h1, F, W + (H * F + F) * esz, eout, H, 0, nullptr, 0, cnt, F, H,
                                  RTPB_EPI_STORE_PRE, ws, ws_bytes, w.compute));
     });
@@ -460,7 +462,9 @@ void RtpMoe::backward(std::span<const DView> dy, size_t rows, std::span<const DV
                                    w.compute));
       // dpre1 = (de W2^T) * gelu'(pre1), written over pre1  (:168-171)
       check_status(rtpb_dgrad_step(dt, de, H, 0, W + (H * F + F) * esz, nullptr, F, pre1, F, pre1, F, cnt, F, H,
-                                   RTPB_EPI_FIRST | RTPB_EPI_LAST | RTPB_EPI_GELU_BWD, ws, ws_bytes, w.compute));
+                                   RTPB_EPI_FIRST | RTPB_EPI_LAST | RTPB_EPI_GELU_BWD |
+                                       (exact_gelu_ ? RTPB_EPI_EXACT_GELU : 0),
+                                   ws, ws_bytes, w.compute));
       // [gW1 | gb1] += xs^T dpre1 (+ colsum)  (:172-175)
       check_status(rtpb_wgrad_step(dt, xs, H, pre1, F, 0, G, G, cnt, H, F, ws, ws_bytes, w.compute));
       // dxs = dpre1 W1^T  (:176-178)

@@ -750,7 +750,7 @@ int gemm_bwd_fused(const FusedBwdArgs& a, const FusedBwdPlan& plan, const FusedB
     if ((rc = encode_maps<FusedDCfg>(a1, b1, dx, nullptr, m1))) return rc;
     GemmArgs g{};
     g.M = int(M); g.N = int(f); g.K = int(h);
-    g.flags = EF_FIRST | EF_LAST | EF_GELU_BWD;
+    g.flags = EF_FIRST | EF_LAST | EF_GELU_BWD | (a.exact_gelu ? EF_EXACT_GELU : 0);
     g.aux = a.pre; g.ld_aux = int64_t(f);
     g.n_fastest = 1; g.k_splits = 1;
     g.sched = ws.sched_d;

@@ -38,7 +38,8 @@ enum EpiFlags : int {
   EF_FIRST = 2,     // DGRAD: first step (accumulator not read)
   EF_LAST = 4,      // DGRAD: last step (emit the cast result through map c0)
   EF_GELU_BWD = 8,  // DGRAD last step: multiply by gelu'(pre)
-  EF_STORE_PRE = 16 // FWD: store pre through map c0
+  EF_STORE_PRE = 16, // FWD: store pre through map c0
+  EF_EXACT_GELU = 64 // bf16: exact-erf GELU / GELU' instead of the tanh.approx form
 };
 
 struct GemmArgs {
@@ -903,7 +904,8 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
             if (uflags & EF_STORE_PRE) detail::stage_row<F32>(stg0, lane, x);
             if (uflags & EF_GELU) {
 #pragma unroll
-              for (int e = 0; e < 32; ++e) x[e] = detail::gelu_f<F32>(x[e]);
+              for (int e = 0; e < 32; ++e)
+                x[e] = (uflags & EF_EXACT_GELU) ? detail::gelu_f<true>(x[e]) : detail::gelu_f<F32>(x[e]);
               detail::stage_row<F32>(stg1, lane, x);
             }
           }
@@ -940,7 +942,8 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
             float pre[32];
             detail::unstage_row<F32>(pc, lane, pre);
 #pragma unroll
-            for (int e = 0; e < 32; ++e) x[e] *= detail::gelu_grad_f<F32>(pre[e]);
+            for (int e = 0; e < 32; ++e)
+              x[e] *= (uflags & EF_EXACT_GELU) ? detail::gelu_grad_f<true>(pre[e]) : detail::gelu_grad_f<F32>(pre[e]);
           } else if (last && (uflags & EF_GELU_BWD) && row_ok) {
 #pragma unroll
             for (int g = 0; g < 4; ++g)
@@ -948,7 +951,9 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
                 float pre[8];
                 detail::load8<F32>(uaux, row * args.ld_aux + nc + g * 8, pre);
 #pragma unroll
-                for (int e = 0; e < 8; ++e) x[g * 8 + e] *= detail::gelu_grad_f<F32>(pre[e]);
+                for (int e = 0; e < 8; ++e)
+                  x[g * 8 + e] *= (uflags & EF_EXACT_GELU) ? detail::gelu_grad_f<true>(pre[e])
+                                                           : detail::gelu_grad_f<F32>(pre[e]);
               }
           }
           if (last)

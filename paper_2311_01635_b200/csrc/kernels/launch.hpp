@@ -110,6 +110,7 @@ struct FusedBwdArgs {
   unsigned* split_flags1; unsigned* split_flags2;
   float* wpart1; float* wpart2;  // split-K partial buffers of the layers (nullable)
   size_t M, h, f;
+  bool exact_gelu;  // RTPB_EPI_EXACT_GELU in ffn2's dX epilogue
 };
 bool plan_fused_bwd(size_t M, size_t h, size_t f, FusedBwdPlan& plan);
 int gemm_bwd_fused(const FusedBwdArgs& a, const FusedBwdPlan& plan, const FusedBwdWs& ws, cudaStream_t compute,
@@ -121,7 +122,7 @@ int fused_bwd_step(FusedBwdArgs a, void* ws1, size_t ws1_bytes, void* ws2, size_
 // store_pre: also write pre (Train). Timed as one fwd launch when profiling.
 int fused_fwd_step(const void* x, size_t ldx, const void* w1_shard, void* pre, void* act, const void* w2_shard,
                    void* y, size_t ldy, size_t M, size_t h, size_t f, bool store_pre, const FusedFwdPlan& plan,
-                   const FusedFwdWs& ws, cudaStream_t s);
+                   const FusedFwdWs& ws, cudaStream_t s, bool exact_gelu = false);
 
 // Caps the SMs the calling thread's following GEMM launches occupy (0 = all);
 // sm_budget() returns the effective count.

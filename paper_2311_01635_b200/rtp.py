@@ -23,6 +23,7 @@ _DT = {"bf16": BF16, "f32": F32, BF16: BF16, F32: F32}
 _TORCH_DT = {BF16: torch.bfloat16, F32: torch.float32}
 _TRANSPORT = {"lockstep": _lib.TRANSPORT_LOCKSTEP, "concurrent": _lib.TRANSPORT_CONCURRENT}
 MEM_CATEGORIES = ("param", "grad", "activation", "comm", "other")
+_OPTIONS = {"exact_gelu": 1, "paired_dx": 2}
 
 
 class WorkerGroup:
@@ -254,6 +255,12 @@ class RtpLinear(_Layer):
     def allocate_comm_spares(self):
         check(lib.rtpb_linear_allocate_comm_spares(self._h))
 
+    def set_option(self, name: str, value: bool):
+        """"exact_gelu" (bf16 epilogues: exact-erf GELU instead of tanh.approx)
+        or "paired_dx" (out-of-place: two steps' dX in one GEMM; off restores
+        the reference's per-step sums, out-of-place == in-place bitwise)."""
+        check(lib.rtpb_linear_set_option(self._h, _OPTIONS[name], int(bool(value))))
+
     def release_comm_spares(self):
         check(lib.rtpb_linear_release_comm_spares(self._h))
 
@@ -344,6 +351,10 @@ class RtpMlp(_Layer):
 
     def begin_step(self):
         check(lib.rtpb_mlp_begin_step(self._h))
+
+    def set_option(self, name: str, value: bool):
+        """RtpLinear.set_option on both layers (and the fused N = 1 launches)."""
+        check(lib.rtpb_mlp_set_option(self._h, _OPTIONS[name], int(bool(value))))
 
     def chain(self, nxt: "RtpMlp | None"):
         """Stack order: `nxt` follows this block in forward. Linked blocks post
@@ -638,11 +649,12 @@ def _ws(which, dtype_code, M, I, per, device):
     return torch.zeros(max(16, n), dtype=torch.uint8, device=device)  # zero-filled before first use
 
 
-def fwd_step(x, w_shard, y, col0, per, act=None, store_pre=True, stream=None):
+def fwd_step(x, w_shard, y, col0, per, act=None, store_pre=True, stream=None, exact_gelu=False):
     dt = F32 if x.dtype == torch.float32 else BF16
     M, I = x.shape
     ws = _ws(0, dt, M, I, per, x.device)
-    flags = (_lib.EPI_STORE_PRE if store_pre else 0) | (_lib.EPI_GELU if act is not None else 0)
+    flags = (_lib.EPI_STORE_PRE if store_pre else 0) | (_lib.EPI_GELU if act is not None else 0) | \
+        (64 if exact_gelu else 0)
     s = (stream or torch.cuda.current_stream(x.device)).cuda_stream
     check(lib.rtpb_fwd_step(dt, x.data_ptr(), x.stride(0), w_shard.data_ptr(),
                             y.data_ptr() if y is not None else None, y.stride(0) if y is not None else 0, col0,

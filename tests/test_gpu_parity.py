@@ -514,3 +514,83 @@ def test_paired_dx_matches_reference(golden, oracle, monkeypatch, n):
         assert nerr(out["dx"], g[f"n{n}_dx"]) < TOL["bf16"]
         for r in range(n):
             assert nerr(out["grads1"][r], g[f"n{n}_grads1"][r]) < TOL["bf16"]
+
+
+# ---------------------------------------------------------------- numerics options
+def test_paired_dx_option_restores_bitwise_inplace_equality(golden):
+    """RTPB_OPT_PAIRED_DX from the API (no environment): with it off the
+    out-of-place MLP is bitwise the in-place one (layers_test.cpp:343-365)."""
+    from paper_2311_01635_b200 import rtp
+    from helpers import to_dev, to_np
+    g = golden("mlp_ring")
+    n = 4
+    M = g["x"].shape[0] // n
+    outs = []
+    for mode in ("inplace", "outofplace"):
+        grp = rtp.WorkerGroup(n)
+        m = rtp.RtpMlp(grp, "m", 64, 256, "bf16", w1=g["w1"], b1=g["b1"], w2=g["w2"], b2=g["b2"])
+        m.set_option("paired_dx", False)
+        m.set_rotation_mode(mode)
+        m.begin_step()
+        m.zero_grads()
+        ys = m.forward([to_dev(g["x"][r * M:(r + 1) * M], "bf16") for r in range(n)])
+        dxs = m.backward([to_dev(g["dy"][r * M:(r + 1) * M], "bf16") for r in range(n)])
+        grp.synchronize()
+        outs.append([to_np(t) for t in ys + dxs] + [to_np(m.ffn1.grad_shard(r)) for r in range(n)] +
+                    [to_np(m.ffn2.grad_shard(r)) for r in range(n)])
+        m.close()
+        grp.close()
+    for a, b in zip(*outs):
+        assert np.array_equal(a, b)
+
+
+def test_exact_gelu_option_in_the_epilogue():
+    """RTPB_OPT_EXACT_GELU: the bf16 forward epilogue's gelu(pre) is the
+    exact-erf GELU rounded once to bf16 (tensor.cpp:323-351), not the
+    tanh.approx form."""
+    import torch
+    from math import erf, sqrt
+    from paper_2311_01635_b200 import rtp
+    rng = np.random.default_rng(12)
+    M, I, per = 256, 128, 256
+    x = rng.uniform(-1, 1, (M, I))
+    w = np.concatenate([rng.uniform(-0.3, 0.3, I * per), rng.uniform(-0.1, 0.1, per)])
+    xd = torch.from_numpy(x).to(torch.bfloat16).cuda()
+    wd = torch.from_numpy(w).to(torch.bfloat16).cuda()
+    xb, wb = xd.double().cpu().numpy(), wd.double().cpu().numpy()
+    pre = xb @ wb[:I * per].reshape(I, per) + wb[I * per:]
+    ref = pre * 0.5 * (1 + np.vectorize(erf)(pre / sqrt(2)))
+    acts = {}
+    for exact in (False, True):
+        y = torch.empty(M, per, dtype=torch.bfloat16, device="cuda")
+        act = torch.empty_like(y)
+        rtp.fwd_step(xd, wd, y, 0, per, act=act, exact_gelu=exact)
+        torch.cuda.synchronize()
+        acts[exact] = act.double().cpu().numpy()
+    err = np.abs(acts[True] - ref)
+    assert np.all(err <= np.abs(ref) * 2.0 ** -8 + 1e-4 * np.abs(ref).max())
+    assert not np.array_equal(acts[True], acts[False])  # the option reaches the kernel
+
+
+def test_exact_gelu_mlp_matches_reference(golden):
+    from helpers import run_mlp
+    g = golden("mlp_ring")
+    from paper_2311_01635_b200 import rtp
+    n = 2
+    grp = rtp.WorkerGroup(n)
+    m = rtp.RtpMlp(grp, "m", 64, 256, "bf16", w1=g["w1"], b1=g["b1"], w2=g["w2"], b2=g["b2"])
+    m.set_option("exact_gelu", True)
+    m.set_rotation_mode("outofplace")
+    m.begin_step()
+    m.zero_grads()
+    from helpers import to_dev, to_np
+    M = g["x"].shape[0] // n
+    ys = m.forward([to_dev(g["x"][r * M:(r + 1) * M], "bf16") for r in range(n)])
+    dxs = m.backward([to_dev(g["dy"][r * M:(r + 1) * M], "bf16") for r in range(n)])
+    grp.synchronize()
+    assert nerr(np.concatenate([to_np(t) for t in ys]), g["n2_y"]) < TOL["bf16"]
+    assert nerr(np.concatenate([to_np(t) for t in dxs]), g["n2_dx"]) < TOL["bf16"]
+    for r in range(n):
+        assert nerr(to_np(m.ffn1.grad_shard(r)), g["n2_grads1"][r]) < TOL["bf16"]
+    m.close()
+    grp.close()
