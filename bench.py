@@ -284,6 +284,10 @@ def main():
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer e2e leg (profiling runs)")
     ap.add_argument("--no-profile", action="store_true", help="skip the profiled per-launch replay")
     ap.add_argument("--eager", action="store_true", help="time host-issued launches instead of a CUDA graph")
+    ap.add_argument("--exact-gelu", action="store_true",
+                    help="bf16 epilogues evaluate the exact-erf GELU (default: the tanh.approx form)")
+    ap.add_argument("--no-paired-dx", action="store_true",
+                    help="per-step dX sums (the reference's order; out-of-place == in-place bitwise)")
     ap.add_argument("--transport", default="nccl", choices=["nccl", "ipc"],
                     help="N > 1 ring shift: ncclSend/ncclRecv (default) or copy-engine pushes through CUDA IPC")
     ap.add_argument("--solo", type=int, default=0,
@@ -365,8 +369,17 @@ def main():
     for b in range(BLOCKS):
         m = rtp.RtpMlp(grp, f"block{b}", H, F, "bf16", seed=SEED, stream_base=b * per_block_params)
         m.set_rotation_mode(args.mode)
+        if args.exact_gelu:
+            m.set_option("exact_gelu", True)
+        if args.no_paired_dx:
+            m.set_option("paired_dx", False)
         m.begin_step()
         mlps.append(m)
+    paired = (not args.no_paired_dx) and os.environ.get("RTPB_DX_PAIR", "1") != "0"
+    numerics = {"gelu": "exact erf" if args.exact_gelu else
+                "tanh form on tanh.approx.f32 in the bf16 epilogues (|d| <= 4.7e-4; --exact-gelu for exact erf)",
+                "paired_dx": bool(paired and args.mode == "outofplace" and ring > 1),
+                "accumulation": "fp32 (TMEM), fp32 gradient shards and cross-step dX accumulator"}
     for a, b in zip(mlps, mlps[1:]):
         a.chain(b)  # a block posts its neighbour's first weight shift under its own last step
 
@@ -564,7 +577,7 @@ def main():
                            "l2": "flushed before every timed step (512 MiB written, then read back)",
                            "flops_per_step": fl_step},
                 "tflops_per_gpu": value / world,
-                "parity_ok": parity_ok, "parity_check": parity_detail,
+                "parity_ok": parity_ok, "parity_check": parity_detail, "numerics": numerics,
                 "gpu_launches": int(launches),
                 "step_execution": graph_note,
                 "eager_ms_per_step": eager_ms,

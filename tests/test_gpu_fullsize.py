@@ -212,3 +212,56 @@ def test_fp64_reference_pinned_to_oracle(oracle, golden):
                              db2[r * per2:(r + 1) * per2].cpu().numpy()])
         assert np.max(np.abs(s1 - ref["grads1"][r])) < 1e-12
         assert np.max(np.abs(s2 - ref["grads2"][r])) < 1e-12
+
+
+# ---------------------------------------------------------------- chained stack
+@pytest.mark.parametrize("mode", ["outofplace", "inplace"])
+def test_chained_stack_vs_fp64(mode):
+    """A 3-block Flyweight stack, blocks chained (each block posts its
+    neighbour's first shift under its own last step), 4 workers, two training
+    steps: the second step's outputs, dX and every block's gradient shards
+    against the fp64 composition y = mlp3(mlp2(mlp1(x))) and its backward."""
+    import torch
+    from paper_2311_01635_b200 import rtp
+    n, h, f, M, blocks = 4, 256, 1024, 512, 3
+    g = rtp.WorkerGroup(n, "lockstep")
+    per_block = 2 * h * f + f + h
+    mlps = []
+    for b in range(blocks):
+        m = rtp.RtpMlp(g, f"block{b}", h, f, "bf16", seed=42, stream_base=b * per_block)
+        m.set_rotation_mode(mode)
+        m.begin_step()
+        mlps.append(m)
+    for a, b in zip(mlps, mlps[1:]):
+        a.chain(b)
+    gen = torch.Generator(device="cuda").manual_seed(3)
+    for step in range(2):
+        xs = [(torch.rand(M, h, device="cuda", generator=gen) * 2 - 1).to(torch.bfloat16) for _ in range(n)]
+        dys = [(torch.rand(M, h, device="cuda", generator=gen) * 2 - 1).to(torch.bfloat16) for _ in range(n)]
+        for m in mlps:
+            m.zero_grads()
+        acts = [xs]
+        for m in mlps:
+            acts.append(m.forward(acts[-1]))
+        ups = [dys]  # ups[i]: upstream gradient of block blocks-1-i (device bf16)
+        for m in reversed(mlps):
+            ups.append(m.backward(ups[-1]))
+        g.synchronize()
+    # fp64 reference per block from the bf16 input and upstream the device saw:
+    # Y, dX and both layers' gradient shards of every block of the chain
+    for b in range(blocks):
+        (W1, b1), (W2, b2) = home_weights(mlps[b].ffn1, n, h, f), home_weights(mlps[b].ffn2, n, f, h)
+        up = ups[blocks - 1 - b]
+        ys_ref, dx_ref, dW1, db1, dW2, db2 = mlp_ref_fp64(acts[b], up, W1, b1, W2, b2)
+        assert max(_nerr(a, r) for a, r in zip(acts[b + 1], ys_ref)) < TOL["bf16"], b
+        assert max(_nerr(a, r) for a, r in zip(ups[blocks - b], dx_ref)) < TOL["bf16"], b
+        for lin, dW, db, O in ((mlps[b].ffn1, dW1, db1, f), (mlps[b].ffn2, dW2, db2, h)):
+            pr = O // n
+            for r in range(n):
+                ref = torch.cat([dW[:, r * pr:(r + 1) * pr].reshape(-1), db[r * pr:(r + 1) * pr]])
+                assert _nerr(lin.grad_shard(r), ref) < TOL["bf16"], (b, r)
+    for m in mlps:
+        for r in range(n):
+            assert m.ffn1.slot(r)["logical_id"] == r and m.ffn2.slot(r)["logical_id"] == r
+        m.close()
+    g.close()
