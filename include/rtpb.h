@@ -135,6 +135,8 @@ int rtpb_gelu(int dtype, const void* x, void* y, size_t count, void* stream);
  * rtpb::Tensor's conversions (the reference's Tensor is fp64, tensor.hpp). */
 int rtpb_convert(const void* src, int src_dtype, void* dst, int dst_dtype, size_t count, void* stream);
 int rtpb_fill(void* dst, int dtype, size_t count, double v, void* stream);
+/* out = a + b elementwise (the model's residual connections, model.cpp:72,85). */
+int rtpb_add(int dtype, const void* a, const void* b, void* out, size_t count, void* stream);
 int rtpb_gelu_backward(int dtype, const void* x, const void* upstream, void* out, size_t count, void* stream);
 
 /* Per-launch timing of the step GEMMs: when enabled, a CUDA event pair is
@@ -187,6 +189,7 @@ typedef struct rtpb_mlp_s* rtpb_mlp;
 typedef struct rtpb_attention_s* rtpb_attention;
 typedef struct rtpb_embedding_s* rtpb_embedding;
 typedef struct rtpb_moe_s* rtpb_moe;
+typedef struct rtpb_model_s* rtpb_model;
 
 #define RTPB_TRANSPORT_LOCKSTEP 0   /* one host thread drives all local workers        */
 #define RTPB_TRANSPORT_CONCURRENT 1 /* one host thread per local worker                */
@@ -372,6 +375,25 @@ int rtpb_moe_slot(rtpb_moe m, size_t rank, int64_t* logical_id, int64_t* rotatio
 int rtpb_moe_read_shard(rtpb_moe m, size_t rank, int which, double* dst);
 /* the per-worker gate gradient (hidden x n, fp64 host) */
 int rtpb_moe_gate_grad(rtpb_moe m, size_t rank, double* dst);
+
+/* RtpModel (model.cpp:7-121) with SerialModel(dims, seed)'s parameters
+ * (serial.cpp:325-353): embedding -> layers x (attention + FFN or MoE with
+ * residual connections) -> head. moe != 0: one expert per worker. */
+int rtpb_model_create(rtpb_group g, size_t heads, size_t hidden, size_t layers, size_t seq, size_t vocab, size_t ffn,
+                      int moe, uint64_t seed, int rotation_mode, int dtype, rtpb_model* out);
+int rtpb_model_destroy(rtpb_model m);
+int rtpb_model_begin_step(rtpb_model m);
+int rtpb_model_zero_grads(rtpb_model m);
+/* ids[k]: counts[k] host token ids of local rank k; logits[k]: device
+ * counts[k] x vocab in the layer dtype. */
+int rtpb_model_forward(rtpb_model m, const int64_t* const* ids, const size_t* counts, void* const* logits, int mode);
+int rtpb_model_backward(rtpb_model m, const void* const* dlogits, size_t rows);
+/* layers in all_layers() order: embedding, per block attention, ffn1, ffn2
+ * (or moe), head */
+size_t rtpb_model_layer_count(rtpb_model m);
+size_t rtpb_model_layer_shard_len(rtpb_model m, size_t layer);
+int rtpb_model_read_layer_shard(rtpb_model m, size_t layer, size_t rank, int which, double* dst);
+int rtpb_model_gate_grad(rtpb_model m, size_t block, size_t rank, double* dst);
 
 #ifdef __cplusplus
 }

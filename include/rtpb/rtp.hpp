@@ -412,6 +412,9 @@ class RtpLayerBase {
   RotationMode rotation_mode() const { return rotation_mode_; }
   // Logical id seen by (phase 0 fwd / 1 bwd, step, rank) in the last pass.
   const std::vector<int64_t>& trace() const { return trace_; }
+  // The weight (grad = false) or gradient shard resident at a local rank as
+  // host fp64 values in the reference's flat shard layout (synchronous).
+  virtual std::vector<double> shard_host(size_t rank, bool grad);
 
  protected:
   void init_slots_alloc();
@@ -578,7 +581,7 @@ class RtpAttention : public RtpLayerBase {
 
   // The resident weight (grad = false) or gradient shard of a local rank in
   // the reference's flat layout [Wq_j | Wk_j | Wv_j | Wo_j (gw x hidden)].
-  std::vector<double> shard_host(size_t rank, bool grad);
+  std::vector<double> shard_host(size_t rank, bool grad) override;
 
  private:
   void init(const double* wq, const double* wk, const double* wv, const double* wo);
@@ -743,6 +746,64 @@ class RtpMlp {
   size_t fused_bwd_rows_ = 0, fused_bwd_sd_ints_ = 0, fused_bwd_sw_ints_ = 0;
   int fused_bwd_slots_d_ = 0, fused_bwd_slots_w_ = 0, fused_bwd_dep_rows_ = 0, fused_bwd_w_splits_ = 1;
   unsigned fused_bwd_dep_target_ = 0;
+};
+
+// ---- model (model.hpp:15-61, model.cpp:7-121) ----
+struct ModelDims {  // serial.hpp:74-83
+  size_t heads = 4;
+  size_t hidden = 32;
+  size_t layers = 2;
+  size_t seq = 16;
+  size_t vocab = 64;
+  size_t ffn = 128;
+  bool moe = false;
+  size_t n_experts = 1;  // MoE variant: equals the worker count
+};
+
+// Embedding -> layers x (attention + FFN-or-MoE, residual connections) ->
+// linear head, every layer rotated (model.cpp:64-121). Parameters are drawn
+// from SplitMix64(seed) in SerialModel's order (serial.cpp:325-353), so the
+// model equals the reference's RtpModel(SerialModel(dims, seed), ...). The
+// FFN of a dense block is an RtpMlp (GELU fused into the step epilogues).
+class RtpModel {
+ public:
+  RtpModel(const ModelDims& dims, uint64_t seed, WorkerGroup& group, RotationMode mode, DType dtype = DType::BF16);
+  ~RtpModel();
+
+  // ids[k]: local rank k's tokens (local_batch * seq); returns its logits
+  // ((local_batch * seq) x vocab, layer dtype).
+  std::vector<Tensor> forward(std::span<const std::vector<int64_t>> ids, Mode mode);
+  // Gradients land in the travelling accumulators (and MoE gate gradients).
+  void backward(std::span<const Tensor> dlogits);
+  void zero_grads();
+  // Out of place: one shard-sized spare per layer per worker for the step,
+  // all released right after the step's final rotation (model.cpp:113-120).
+  void begin_step();
+  std::function<void()> on_comm_release;
+  bool comm_spares_active() const;
+
+  WorkerGroup& group() { return *group_; }
+  RotationMode rotation_mode() const { return mode_; }
+  const ModelDims& dims() const { return dims_; }
+  // embedding, per block: attention, ffn1, ffn2 (or moe), head (model.cpp:34-52)
+  std::vector<RtpLayerBase*> all_layers();
+  RtpEmbedding& embedding() { return *embedding_; }
+  RtpLinear& head() { return *head_; }
+  struct Block {
+    std::unique_ptr<RtpAttention> attn;
+    std::unique_ptr<RtpMlp> mlp;
+    std::unique_ptr<RtpMoe> moe;
+  };
+  std::vector<Block>& rtp_blocks() { return blocks_; }
+
+ private:
+  WorkerGroup* group_;
+  RotationMode mode_;
+  ModelDims dims_;
+  DType dtype_;
+  std::unique_ptr<RtpEmbedding> embedding_;
+  std::vector<Block> blocks_;
+  std::unique_ptr<RtpLinear> head_;
 };
 
 // Host fp64 -> device dtype, round-to-nearest-even from the double (no

@@ -167,6 +167,9 @@ class Reference:
                                   _dp, _dp, _dp, _dp, _dp]
         L.ref_rtp_moe.argtypes = [_sz, C.c_int, _sz, _sz, _sz, _dp, _dp, _dp, _dp, _dp, _dp, _dp, _dp]
         L.ref_rtp_embedding.argtypes = [_sz, C.c_int, _sz, _sz, _sz, _dp, C.POINTER(C.c_int64), _dp, _dp, _dp]
+        L.ref_rtp_model.argtypes = [_sz, C.c_int, C.c_int, _sz, _sz, _sz, _sz, _sz, _sz, C.c_int, _u64, _sz,
+                                    C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(_sz),
+                                    C.POINTER(_sz)]
         L.ref_cmd_csv.argtypes = [C.c_int, _sz, C.c_char_p, _sz, C.c_char_p, _sz]
         L.ref_time_mlp.argtypes = [_sz, C.c_int, _sz, _sz, _sz, _u64, C.c_int, C.POINTER(C.c_double)]
         L.ref_mlp_ledger.argtypes = [_sz, C.c_int, _sz, _sz, _sz, _u64, C.POINTER(_sz), C.POINTER(_sz)]
@@ -174,7 +177,7 @@ class Reference:
         L.ref_table1.argtypes = [C.c_int, _u64, _u64, _u64, _u64, _u64, C.POINTER(_u64)]
         for name in ("ref_uniform", "ref_linear_shard", "ref_mlp_params", "ref_serial_linear",
                      "ref_rtp_linear", "ref_rtp_mlp", "ref_time_mlp", "ref_mlp_ledger",
-                     "ref_ring_ops", "ref_table1", "ref_rtp_moe", "ref_rtp_embedding", "ref_cmd_csv"):
+                     "ref_ring_ops", "ref_table1", "ref_rtp_moe", "ref_rtp_embedding", "ref_cmd_csv", "ref_rtp_model"):
             getattr(L, name).restype = C.c_int
         self.L = L
 
@@ -265,6 +268,29 @@ class Reference:
         self._chk(self.L.ref_rtp_embedding(n, int(concurrent), vocab, emb, rpw, table,
                                            ids.ctypes.data_as(C.POINTER(C.c_int64)), dy, y, g))
         return {"y": y, "grads": g}
+
+    def rtp_model(self, n, heads, hidden, layers, seq, vocab, ffn, moe=False, seed=42, batch=4, outofplace=False,
+                  concurrent=False):
+        """RtpModel(SerialModel(dims, seed)) one training step (verify.cpp:54-79)."""
+        nl = _sz(0)
+        lens = (_sz * 64)()
+        args = [n, int(concurrent), int(outofplace), heads, hidden, layers, seq, vocab, ffn, int(moe), seed, batch]
+        self._chk(self.L.ref_rtp_model(*args, None, None, None, None, None, C.byref(nl), lens))
+        L = [int(lens[i]) for i in range(nl.value)]
+        rows = batch * seq
+        ids = np.empty(rows, np.int64)
+        logits, dlogits = np.empty((rows, vocab)), np.empty((rows, vocab))
+        grads = np.empty(n * sum(L))
+        gg = np.empty(max(1, layers * n * hidden * n))
+        ptr = lambda a: a.ctypes.data_as(C.c_void_p)  # noqa: E731
+        self._chk(self.L.ref_rtp_model(*args, ptr(ids), ptr(logits), ptr(dlogits), ptr(grads), ptr(gg),
+                                       C.byref(nl), lens))
+        out, off = [], 0
+        for ln in L:
+            out.append(grads[off:off + n * ln].reshape(n, ln))
+            off += n * ln
+        return {"ids": ids, "logits": logits, "dlogits": dlogits, "grads": out,
+                "gate_grads": gg[:layers * n * hidden * n].reshape(layers, n, hidden, n) if moe else None}
 
     def cmd_csv(self, which: str, n: int, strategy: str, batch: int) -> str:
         """CSV text of the reference's `rtpsim memtable|ledger|sweep` commands."""

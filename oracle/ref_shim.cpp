@@ -421,4 +421,60 @@ int ref_cmd_csv(int which, size_t n, const char* strategy, size_t batch, char* o
   })
 }
 
+// The whole RtpModel (model.cpp:7-121): SerialModel(dims, seed) parameters
+// (serial.cpp:325-353), make_batch_fixture ids / MSE target, Train forward,
+// dlogits = mse_grad, backward — verify.cpp:54-79's equivalence run. Outputs:
+// ids (batch*seq), logits and dlogits ((batch*seq) x vocab, rank-major),
+// grads: every layer of all_layers() in order, n * shard_len each
+// (layer_lens[l] = shard_len), gate_grads: per MoE block n * hidden * n.
+// Query sizes with grads == nullptr: *n_layers and layer_lens are filled.
+int ref_rtp_model(size_t n, int transport, int oop, size_t heads, size_t hidden, size_t layers, size_t seq,
+                  size_t vocab, size_t ffn, int moe, uint64_t seed, size_t batch, int64_t* ids, double* logits,
+                  double* dlogits, double* grads, double* gate_grads, size_t* n_layers, size_t* layer_lens) {
+  REF_GUARD({
+    ModelDims d;
+    d.heads = heads;
+    d.hidden = hidden;
+    d.layers = layers;
+    d.seq = seq;
+    d.vocab = vocab;
+    d.ffn = ffn;
+    d.moe = moe != 0;
+    d.n_experts = moe ? n : 1;
+    SerialModel serial(d, seed);
+    WorkerGroup g(n, kind_of(transport));
+    RtpModel model(serial, g, oop ? RotationMode::OutOfPlace : RotationMode::InPlace);
+    auto all = model.all_layers();
+    *n_layers = all.size();
+    for (size_t l = 0; l < all.size(); ++l) layer_lens[l] = all[l]->shard_len();
+    if (!grads) return 0;
+    BatchFixture fx = make_batch_fixture(d, batch, seed);
+    std::memcpy(ids, fx.ids.data(), fx.ids.size() * sizeof(int64_t));
+    auto ids_sh = shard_ids(fx, n);
+    auto target_sh = shard_rows(fx.target, batch, n);
+    model.zero_grads();
+    model.begin_step();
+    auto out = model.forward(ids_sh, Mode::Train);
+    std::vector<Tensor> dl(n);
+    for (size_t r = 0; r < n; ++r) dl[r] = mse_grad(out[r], target_sh[r], fx.target.numel());
+    model.backward(dl);
+    to_ptr(concat(out, 0), logits);
+    to_ptr(concat(dl, 0), dlogits);
+    double* gp = grads;
+    for (RtpLayerBase* l : all)
+      for (size_t r = 0; r < n; ++r) {
+        to_ptr(l->slots()[r].grad_acc, gp);
+        gp += l->shard_len();
+      }
+    if (moe) {
+      double* q = gate_grads;
+      for (auto& b : model.rtp_blocks())
+        for (size_t r = 0; r < n; ++r) {
+          to_ptr(b.moe->gate_grad(r), q);
+          q += hidden * n;
+        }
+    }
+  })
+}
+
 }  // extern "C"

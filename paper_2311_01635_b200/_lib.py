@@ -129,6 +129,17 @@ _SIGS = {
     "rtpb_moe_gate_grad": (_int, [_vp, _sz, C.POINTER(_dbl)]),
     "rtpb_linear_set_option": (_int, [_vp, _int, _int]),
     "rtpb_mlp_set_option": (_int, [_vp, _int, _int]),
+    "rtpb_add": (_int, [_int, _vp, _vp, _vp, _sz, _vp]),
+    "rtpb_model_create": (_int, [_vp, _sz, _sz, _sz, _sz, _sz, _sz, _int, _u64, _int, _int, _vpp]),
+    "rtpb_model_destroy": (_int, [_vp]),
+    "rtpb_model_begin_step": (_int, [_vp]),
+    "rtpb_model_zero_grads": (_int, [_vp]),
+    "rtpb_model_forward": (_int, [_vp, _vpp, C.POINTER(_sz), _vpp, _int]),
+    "rtpb_model_backward": (_int, [_vp, _vpp, _sz]),
+    "rtpb_model_layer_count": (_sz, [_vp]),
+    "rtpb_model_layer_shard_len": (_sz, [_vp, _sz]),
+    "rtpb_model_read_layer_shard": (_int, [_vp, _sz, _sz, _int, C.POINTER(_dbl)]),
+    "rtpb_model_gate_grad": (_int, [_vp, _sz, _sz, C.POINTER(_dbl)]),
     "rtpb_wgrad_step_ex": (_int, [_int, _vp, _sz, _vp, _sz, _sz, _vp, _vp, _sz, _sz, _sz, _int, _vp, _sz, _vp]),
 }
 

@@ -423,6 +423,13 @@ int rtpb_fill(void* dst, int dtype, size_t count, double v, void* stream) {
   return fill(dst, dtype, count, v, as_stream(stream));
 }
 
+int rtpb_add(int dtype, const void* a, const void* b, void* out, size_t count, void* stream) {
+  if (dtype != RTPB_BF16 && dtype != RTPB_F32 && dtype != RTPB_F64)
+    return set_error(RTPB_ERR_CONFIG, "rtpb_add: unknown dtype");
+  if (count && (!a || !b || !out)) return set_error(RTPB_ERR_DIMENSION, "rtpb_add: null buffer");
+  return add(a, b, out, dtype, count, as_stream(stream));
+}
+
 int rtpb_gelu_backward(int dtype, const void* x, const void* upstream, void* out, size_t count, void* stream) {
   return gelu_bwd(dtype == RTPB_F32, x, upstream, out, count, as_stream(stream));
 }

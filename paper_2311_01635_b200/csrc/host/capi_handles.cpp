@@ -41,6 +41,10 @@ struct rtpb_moe_s {
   rtpb_group_s* grp;
   std::unique_ptr<RtpMoe> m;
 };
+struct rtpb_model_s {
+  rtpb_group_s* grp;
+  std::unique_ptr<RtpModel> m;
+};
 struct rtpb_mlp_s {
   rtpb_group_s* grp;
   std::unique_ptr<RtpMlp> m;
@@ -667,6 +671,82 @@ int rtpb_mlp_set_option(rtpb_mlp m, int option, int value) {
       m->m->set_paired_dx(value != 0);
     else
       throw ConfigError("unknown option " + std::to_string(option));
+  });
+}
+
+int rtpb_model_create(rtpb_group g, size_t heads, size_t hidden, size_t layers, size_t seq, size_t vocab, size_t ffn,
+                      int moe, uint64_t seed, int rotation_mode, int dtype, rtpb_model* out) {
+  return guard([&] {
+    ModelDims d;
+    d.heads = heads;
+    d.hidden = hidden;
+    d.layers = layers;
+    d.seq = seq;
+    d.vocab = vocab;
+    d.ffn = ffn;
+    d.moe = moe != 0;
+    d.n_experts = moe ? g->g->size() : 1;
+    auto h = std::make_unique<rtpb_model_s>();
+    h->grp = g;
+    h->m = std::make_unique<RtpModel>(d, seed, *g->g, rot(rotation_mode), dt(dtype));
+    ++g->refs;
+    *out = h.release();
+  });
+}
+int rtpb_model_destroy(rtpb_model m) { return layer_destroy(m); }
+int rtpb_model_begin_step(rtpb_model m) { return guard([&] { m->m->begin_step(); }); }
+int rtpb_model_zero_grads(rtpb_model m) { return guard([&] { m->m->zero_grads(); }); }
+int rtpb_model_forward(rtpb_model m, const int64_t* const* ids, const size_t* counts, void* const* logits, int mode) {
+  return guard([&] {
+    WorkerGroup& G = *m->grp->g;
+    const size_t k = G.local_ranks().size();
+    std::vector<std::vector<int64_t>> v(k);
+    for (size_t i = 0; i < k; ++i) v[i].assign(ids[i], ids[i] + counts[i]);
+    auto out = m->m->forward(v, mode == RTPB_MODE_EVAL ? Mode::Eval : Mode::Train);
+    for (size_t i = 0; i < k; ++i) {
+      DeviceGuard dg(out[i].device());
+      cuda_check(cudaMemcpy(logits[i], out[i].data(), out[i].bytes(), cudaMemcpyDeviceToDevice), "model logits");
+    }
+  });
+}
+int rtpb_model_backward(rtpb_model m, const void* const* dlogits, size_t rows) {
+  return guard([&] {
+    WorkerGroup& G = *m->grp->g;
+    const auto& local = G.local_ranks();
+    const size_t V = m->m->dims().vocab;
+    const DType d = m->m->head().dtype();
+    std::vector<Tensor> t(local.size());
+    for (size_t i = 0; i < local.size(); ++i) {
+      Worker& w = G.worker(local[i]);
+      t[i] = Tensor({rows, V}, d, w.device, &w.ledger, MemCategory::Activation, false);
+      DeviceGuard dg(w.device);
+      cuda_check(cudaMemcpy(t[i].data(), dlogits[i], t[i].bytes(), cudaMemcpyDeviceToDevice), "model dlogits");
+    }
+    m->m->backward(t);
+  });
+}
+size_t rtpb_model_layer_count(rtpb_model m) { return m ? m->m->all_layers().size() : 0; }
+size_t rtpb_model_layer_shard_len(rtpb_model m, size_t layer) {
+  if (!m) return 0;
+  auto all = m->m->all_layers();
+  return layer < all.size() ? all[layer]->shard_len() : 0;
+}
+int rtpb_model_read_layer_shard(rtpb_model m, size_t layer, size_t rank, int which, double* dst) {
+  return guard([&] {
+    auto all = m->m->all_layers();
+    if (layer >= all.size()) throw IndexError("layer index out of range");
+    const std::vector<double> v = all[layer]->shard_host(rank, which != 0);
+    std::memcpy(dst, v.data(), v.size() * sizeof(double));
+  });
+}
+int rtpb_model_gate_grad(rtpb_model m, size_t block, size_t rank, double* dst) {
+  return guard([&] {
+    auto& blocks = m->m->rtp_blocks();
+    if (block >= blocks.size() || !blocks[block].moe) throw IndexError("not an MoE block");
+    if (!m->grp->g->is_local(rank)) throw IndexError("gate gradient of a non-local rank");
+    m->grp->g->synchronize();
+    const std::vector<double> v = blocks[block].moe->gate_grad(rank).to_host();
+    std::memcpy(dst, v.data(), v.size() * sizeof(double));
   });
 }
 

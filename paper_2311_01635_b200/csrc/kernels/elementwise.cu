@@ -218,6 +218,11 @@ __global__ void convert_kernel(const void* __restrict__ src, int sdt, void* __re
   for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x)
     st_any(dst, ddt, i, ld_any(src, sdt, i));
 }
+__global__ void add_kernel(const void* __restrict__ a, const void* __restrict__ b, void* __restrict__ out, int dt,
+                           size_t n) {
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x)
+    st_any(out, dt, i, ld_any(a, dt, i) + ld_any(b, dt, i));
+}
 __global__ void fill_kernel(void* __restrict__ dst, int dt, size_t n, double v) {
   for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x)
     st_any(dst, dt, i, v);
@@ -317,6 +322,12 @@ int convert(const void* src, int src_dtype, void* dst, int dst_dtype, size_t n, 
   if (n == 0) return RTPB_OK;
   convert_kernel<<<grid_for(n, 256), 256, 0, s>>>(src, src_dtype, dst, dst_dtype, n);
   return post_launch("convert_kernel");
+}
+
+int add(const void* a, const void* b, void* out, int dtype, size_t n, cudaStream_t s) {
+  if (n == 0) return RTPB_OK;
+  add_kernel<<<grid_for(n, 256), 256, 0, s>>>(a, b, out, dtype, n);
+  return post_launch("add_kernel");
 }
 
 int fill(void* dst, int dtype, size_t n, double v, cudaStream_t s) {

@@ -181,5 +181,7 @@ int embed_scatter(bool f32, const void* dy, size_t ldy, size_t col0, const int64
 // dtype codes RTPB_BF16 / RTPB_F32 / RTPB_F64
 int convert(const void* src, int src_dtype, void* dst, int dst_dtype, size_t count, cudaStream_t s);
 int fill(void* dst, int dtype, size_t count, double v, cudaStream_t s);
+// out = a + b elementwise (residual connections, model.cpp:72,85,108,111)
+int add(const void* a, const void* b, void* out, int dtype, size_t count, cudaStream_t s);
 
 }  // namespace rtpb

@@ -642,6 +642,71 @@ class RtpMoe(_Layer):
             pass
 
 
+class RtpModel:
+    """RtpModel (model.cpp:7-121) with SerialModel(dims, seed)'s parameters:
+    embedding -> layers x (attention + FFN or MoE, residuals) -> head."""
+
+    def __init__(self, group: WorkerGroup, heads=4, hidden=32, layers=2, seq=16, vocab=64, ffn=128, moe=False,
+                 seed=42, mode="inplace", dtype="bf16"):
+        self.group, self.vocab, self.hidden, self.layers = group, vocab, hidden, layers
+        self.dtype_code = _DT[dtype]
+        h = C.c_void_p()
+        check(lib.rtpb_model_create(group._h, heads, hidden, layers, seq, vocab, ffn, int(moe), seed,
+                                    {"inplace": 0, "outofplace": 1}[mode], self.dtype_code, C.byref(h)))
+        self._h = h
+
+    def begin_step(self):
+        check(lib.rtpb_model_begin_step(self._h))
+
+    def zero_grads(self):
+        check(lib.rtpb_model_zero_grads(self._h))
+
+    def forward(self, ids, mode="train"):
+        import numpy as np
+        arrs = [np.ascontiguousarray(np.asarray(v, dtype=np.int64)) for v in ids]
+        outs = [torch.empty(len(a), self.vocab, dtype=_TORCH_DT[self.dtype_code], device=self.group.device_of(r))
+                for a, r in zip(arrs, self.group.local_ranks)]
+        self.group._enter(None)
+        ptrs = (C.c_void_p * len(arrs))(*[a.ctypes.data for a in arrs])
+        counts = (C.c_size_t * len(arrs))(*[len(a) for a in arrs])
+        check(lib.rtpb_model_forward(self._h, ptrs, counts, ptr_array(outs),
+                                     _lib.MODE_EVAL if mode == "eval" else _lib.MODE_TRAIN))
+        self.group._leave()
+        return outs
+
+    def backward(self, dlogits):
+        self.group._enter(None)
+        check(lib.rtpb_model_backward(self._h, ptr_array(dlogits), dlogits[0].shape[0]))
+        self.group._leave()
+
+    def layer_count(self) -> int:
+        return int(lib.rtpb_model_layer_count(self._h))
+
+    def layer_shard(self, layer: int, rank: int, grad: bool = False):
+        import numpy as np
+        out = np.empty(int(lib.rtpb_model_layer_shard_len(self._h, layer)), dtype=np.float64)
+        check(lib.rtpb_model_read_layer_shard(self._h, layer, rank, int(grad),
+                                              out.ctypes.data_as(C.POINTER(C.c_double))))
+        return out
+
+    def gate_grad(self, block: int, rank: int):
+        import numpy as np
+        out = np.empty((self.hidden, self.group.n), dtype=np.float64)
+        check(lib.rtpb_model_gate_grad(self._h, block, rank, out.ctypes.data_as(C.POINTER(C.c_double))))
+        return out
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib.rtpb_model_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 # --- step kernels (layer (1) of rtpb.h), on torch tensors ---
 
 def _ws(which, dtype_code, M, I, per, device):

@@ -176,6 +176,28 @@ def main():
             embd[f"n{nn}_{k}"] = v
     out["embedding"] = embd
 
+    # 4e. The whole RtpModel (model.cpp:7-121; SURVEY §8f.2 block wiring,
+    #     §8f.4 embedding + head): SerialModel(dims, 42) parameters,
+    #     make_batch_fixture ids, mse_grad upstream; dense N in {1,2,4} and
+    #     MoE N in {2,4} (one expert per worker).
+    model = {}
+    dims = dict(heads=4, hidden=32, layers=2, seq=8, vocab=64, ffn=128)
+    for moe_on, ns in ((False, (1, 2, 4)), (True, (2, 4))):
+        for nn in ns:
+            r = R.rtp_model(nn, dims["heads"], dims["hidden"], dims["layers"], dims["seq"], dims["vocab"],
+                            dims["ffn"], moe=moe_on, seed=42, batch=4)
+            ro = R.rtp_model(nn, dims["heads"], dims["hidden"], dims["layers"], dims["seq"], dims["vocab"],
+                             dims["ffn"], moe=moe_on, seed=42, batch=4, outofplace=True)
+            assert np.array_equal(r["logits"], ro["logits"]), "out-of-place != in-place"
+            p = f"{'moe' if moe_on else 'dense'}_n{nn}_"
+            model[p + "ids"], model[p + "logits"], model[p + "dlogits"] = r["ids"], r["logits"], r["dlogits"]
+            for li, gr in enumerate(r["grads"]):
+                model[p + f"grads{li}"] = gr
+            if moe_on:
+                model[p + "gate_grads"] = r["gate_grads"]
+    model.update({k: np.int64(v) for k, v in dims.items()})
+    out["model"] = model
+
     # 5. Ring primitive (ring.cpp:265-293) on id-encoded slots (ring_test.cpp:16-28)
     rng = np.random.default_rng(77)
     ring = {}

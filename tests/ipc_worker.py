@@ -38,6 +38,8 @@ def main():
         res["fwd_id"] = lin.slot(rank)["logical_id"]
         dx = lin.backward([to_dev(dy[rank * M:(rank + 1) * M], "bf16")])[0]
         g.synchronize()
+        led = g.ledger(rank)  # this process's device ledger (per-rank memory, not a simulation)
+        res["ledger"] = np.array([led["peak_param"], led["peak_grad"], led["peak_comm"]], np.int64)
         res.update(y=to_np(y), dx=to_np(dx), grad=to_np(lin.grad_shard(rank)), weight=to_np(lin.weight_shard(rank)),
                    bwd_id=lin.slot(rank)["logical_id"], trace=np.array(lin.trace()),
                    traffic=np.array([[{"rotation_cw": 0, "rotation_ccw": 1}[k], a, c] for k, a, c in g.traffic()]))

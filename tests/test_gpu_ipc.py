@@ -58,6 +58,16 @@ def test_linear_multiprocess_ipc(golden, tmp_path, n, mode):
         fwd, bwd = res[r]["trace"]
         for s in range(n):  # each process records its own rank's column
             assert fwd[s][r] == (r - s) % n and bwd[s][r] == (r + 1 + s) % n
+    # per-rank device memory measured in each process, exact bytes: W/N bf16,
+    # G/N fp32, CommBuffer = out-of-place spare (W/N) + the staging chunk of
+    # the in-place shifts (test_memory_ledger_exact_bytes' model)
+    i_dim, o_dim = g["w"].shape
+    L = i_dim * (o_dim // n) + o_dim // n
+    chunk = min(max(1 << 20, (L * 4) // 32) + 255 & ~255, L * 4)
+    for r in range(n):
+        param, grad, comm = (int(v) for v in res[r]["ledger"])
+        assert (param, grad) == (2 * L, 4 * L), r
+        assert comm == (2 * L if mode == "outofplace" else 0) + chunk, (r, comm)
         assert [tuple(int(v) for v in t) for t in res[r]["traffic"]] == [tuple(int(v) for v in t)
                                                                           for t in g[p + "traffic"]]
 
