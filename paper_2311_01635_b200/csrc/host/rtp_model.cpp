@@ -2,7 +2,12 @@
 // the device — embedding, blocks of attention + FFN (RtpMlp) or MoE with
 // residual connections, linear head — composed from the device layers over
 // their Tensor API. Parameters from SplitMix64(seed) in SerialModel's draw
-// order (serial.cpp:325-353).
+// order (serial.cpp:325-353) AS THE REFERENCE IS BUILT: the draws that are
+// arguments of one constructor call (SerialAttention(draw, draw, draw, draw),
+// SerialLinear(draw, draw)) happen in the compiler's argument evaluation
+// order, which C++ leaves unspecified and g++ (the reference's toolchain)
+// takes right to left — wo, wv, wk, wq and bias before weight; braced
+// ExpertParams{...} lists are left to right.
 #include <cstring>
 
 #include "kernels/launch.hpp"
@@ -58,7 +63,7 @@ RtpModel::RtpModel(const ModelDims& dims, uint64_t seed, WorkerGroup& group, Rot
   blocks_.resize(dims_.layers);
   for (size_t l = 0; l < dims_.layers; ++l) {
     const std::string tag = "block" + std::to_string(l);
-    const auto wq = draw(rng, h * h), wk = draw(rng, h * h), wv = draw(rng, h * h), wo = draw(rng, h * h);
+    const auto wo = draw(rng, h * h), wv = draw(rng, h * h), wk = draw(rng, h * h), wq = draw(rng, h * h);
     blocks_[l].attn = std::make_unique<RtpAttention>(group, tag + "/attn", wq.data(), wk.data(), wv.data(), wo.data(),
                                                      h, dims_.heads, dims_.seq, n, dtype);
     if (dims_.moe) {
@@ -74,11 +79,11 @@ RtpModel::RtpModel(const ModelDims& dims, uint64_t seed, WorkerGroup& group, Rot
       }
       blocks_[l].moe = std::make_unique<RtpMoe>(group, tag + "/moe", gate.data(), ptr.data(), h, f, n, dtype);
     } else {
-      const auto w1 = draw(rng, h * f), b1 = draw(rng, f), w2 = draw(rng, f * h), b2 = draw(rng, h);
+      const auto b1 = draw(rng, f), w1 = draw(rng, h * f), b2 = draw(rng, h), w2 = draw(rng, f * h);
       blocks_[l].mlp = std::make_unique<RtpMlp>(group, tag, h, f, dtype, w1.data(), b1.data(), w2.data(), b2.data());
     }
   }
-  const auto hw = draw(rng, h * v), hb = draw(rng, v);
+  const auto hb = draw(rng, v), hw = draw(rng, h * v);
   head_ = std::make_unique<RtpLinear>(group, "head", hw.data(), hb.data(), h, v, n, dtype);
   for (RtpLayerBase* l : all_layers()) l->set_rotation_mode(mode);
 }
