@@ -903,9 +903,13 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
             }
             if (uflags & EF_STORE_PRE) detail::stage_row<F32>(stg0, lane, x);
             if (uflags & EF_GELU) {
+              if (!F32 && (uflags & EF_EXACT_GELU)) {  // warp-uniform: one loop or the other
 #pragma unroll
-              for (int e = 0; e < 32; ++e)
-                x[e] = (uflags & EF_EXACT_GELU) ? detail::gelu_f<true>(x[e]) : detail::gelu_f<F32>(x[e]);
+                for (int e = 0; e < 32; ++e) x[e] = detail::gelu_f<true>(x[e]);
+              } else {
+#pragma unroll
+                for (int e = 0; e < 32; ++e) x[e] = detail::gelu_f<F32>(x[e]);
+              }
               detail::stage_row<F32>(stg1, lane, x);
             }
           }
@@ -941,19 +945,26 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
             const uint8_t* pc = pre_w + ((ch - half) / NSPLIT) * 32 * 32 * Cfg::ELEM;
             float pre[32];
             detail::unstage_row<F32>(pc, lane, pre);
+            if (!F32 && (uflags & EF_EXACT_GELU)) {
 #pragma unroll
-            for (int e = 0; e < 32; ++e)
-              x[e] *= (uflags & EF_EXACT_GELU) ? detail::gelu_grad_f<true>(pre[e]) : detail::gelu_grad_f<F32>(pre[e]);
+              for (int e = 0; e < 32; ++e) x[e] *= detail::gelu_grad_f<true>(pre[e]);
+            } else {
+#pragma unroll
+              for (int e = 0; e < 32; ++e) x[e] *= detail::gelu_grad_f<F32>(pre[e]);
+            }
           } else if (last && (uflags & EF_GELU_BWD) && row_ok) {
 #pragma unroll
             for (int g = 0; g < 4; ++g)
               if (nc + g * 8 < uN) {
                 float pre[8];
                 detail::load8<F32>(uaux, row * args.ld_aux + nc + g * 8, pre);
+                if (!F32 && (uflags & EF_EXACT_GELU)) {
 #pragma unroll
-                for (int e = 0; e < 8; ++e)
-                  x[g * 8 + e] *= (uflags & EF_EXACT_GELU) ? detail::gelu_grad_f<true>(pre[e])
-                                                           : detail::gelu_grad_f<F32>(pre[e]);
+                  for (int e = 0; e < 8; ++e) x[g * 8 + e] *= detail::gelu_grad_f<true>(pre[e]);
+                } else {
+#pragma unroll
+                  for (int e = 0; e < 8; ++e) x[g * 8 + e] *= detail::gelu_grad_f<F32>(pre[e]);
+                }
               }
           }
           if (last)
