@@ -278,7 +278,11 @@ int raster_mode(int M, int N, int K, int tile_m, int bn, bool f32, bool prefer_m
   if (prefer_m && a_bytes < 48e6) return 0;
   if (b_bytes < 48e6) return 1;
   if (a_bytes < 48e6) return 0;
-  return 8;
+  static const int group = [] {  // A/B experiments only (RTPB_RASTER_GROUP)
+    const char* e = std::getenv("RTPB_RASTER_GROUP");
+    return e ? std::max(2, std::atoi(e)) : 8;
+  }();
+  return group;
 }
 
 // Tile code (and, for dW, the split-K factor written into args.k_splits).

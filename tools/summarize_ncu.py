@@ -32,8 +32,10 @@ try:
         if hdr and len(r) == len(hdr):
             d = dict(zip(hdr, r))
             if d.get("Metric Name") == "gpu__time_duration.sum":
+                scale = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}.get(
+                    d.get("Metric Unit", "nsecond"), 1e-3)
                 agg[short(d["Kernel Name"])][0] += 1
-                agg[short(d["Kernel Name"])][1] += float(d["Metric Value"]) / 1e3  # us
+                agg[short(d["Kernel Name"])][1] += float(d["Metric Value"].replace(",", "")) * scale  # us
 except FileNotFoundError:
     pass
 tot = sum(v[1] for v in agg.values()) or 1.0
@@ -68,7 +70,10 @@ try:
     lines.append("|---|---|---:|---:|---:|---:|---:|---:|---:|---:|")
     for r in rows[2:]:
         name = short(r[idx["Kernel Name"]])
-        t, _ = g(r, "gpu__time_duration.sum")
+        t, tu = g(r, "gpu__time_duration.sum")
+        if t:  # normalise to microseconds whatever unit ncu chose
+            t = str(float(t) * {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3,
+                                "ms": 1e3, "second": 1e6, "s": 1e6}.get(tu, 1.0))
         tp, _ = g(r, "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active")
         dr, dru = g(r, "dram__bytes_read.sum")
         dw, dwu = g(r, "dram__bytes_write.sum")
