@@ -55,6 +55,8 @@ extern "C" {
 #define RTPB_EPI_STORE_PRE 16 /* fwd: write X.W_j + b_j to `y` (default for plain linear) */
 #define RTPB_EPI_NO_BIAS 32   /* fwd / wgrad_ex: the shard block has no bias part (projections) */
 #define RTPB_EPI_EXACT_GELU 64 /* bf16: exact-erf GELU / GELU' in the epilogue (default: tanh.approx form) */
+#define RTPB_PASS_PAIR 128    /* rtpb_dgrad_pass: each unit covers a step pair (2g, 2g+1), one accumulation over
+                                 K = 2 per (paired dX); counters and the done target per pair */
 
 const char* rtpb_last_error(void);
 const char* rtpb_version(void);
@@ -103,6 +105,40 @@ int rtpb_dgrad_step2(int dtype, const void* dy, size_t ldy, size_t col0, const v
                      const void* w_b, float* acc, size_t ld_acc, void* dx, size_t ldx, const void* pre,
                      size_t ldpre, size_t M, size_t I, size_t per, int flags, void* workspace,
                      size_t workspace_bytes, void* stream);
+
+/* Pass launches (bf16, one worker per GPU, out-of-place mode): every rotation
+ * step of one layer pass (layers_linear.cpp:29-43 forward, :57-67 dX) in ONE
+ * persistent launch instead of one launch per step. Step s (0 <= s < steps)
+ * computes on the weight shard in buffer (buf_mask >> s) & 1 (buf0 = the
+ * resident shard at pass start, buf1 = the spare; they alternate) and on the
+ * activation column block col0[s] (= j_s * per):
+ *   fwd  : y / act[:, col0[s] : +per] = (gelu)(X . W_{j_s} + b_{j_s})   (flags as rtpb_fwd_step)
+ *   dgrad: dX = sum_s dY[:, col0[s] : +per] . W_{j_s}^T, accumulated in the
+ *          fp32 `acc` in step order (bit-identical to `steps` rtpb_dgrad_step
+ *          calls), times gelu'(pre) with RTPB_EPI_GELU_BWD.
+ * `ready` (nullable): step s >= 1 reads its shard only once ready[s] >= 1
+ * (written by the comm stream when the shard landed). `done` (steps zeroed
+ * counters): once step s's operands have been read, done[s] reaches
+ * *done_target (written by the call; with RTPB_PASS_PAIR done[g] counts the
+ * pair (2g, 2g + 1)) — the comm stream waits for that value
+ * (cuStreamWaitValue32) before it lands step s + 2's shard in step s's
+ * buffer. The launch re-zeroes `done` (and, with reset_flags, the `ready`
+ * range) when it completes; reset_ctr is a zeroed counter. y_cols / dy_cols:
+ * width of the Y / dY activations (N * per). Requires per % 32 == 0 and
+ * steps <= 16. */
+/* The count-in total a pass launch of this geometry reaches on done[s]
+ * (which = 0 fwd, 1 dgrad; steps and flags as the launch's), for
+ * comm-stream waits enqueued before the launch. */
+unsigned rtpb_pass_done_target(int which, size_t M, size_t I, size_t per, size_t steps, int flags);
+int rtpb_fwd_pass(const void* x, size_t ldx, const void* buf0, const void* buf1, void* y, size_t ldy, void* act,
+                  size_t ld_act, size_t y_cols, const size_t* col0, unsigned buf_mask, size_t steps, size_t M,
+                  size_t I, size_t per, int flags, const unsigned* ready, unsigned* done, unsigned* done_target,
+                  unsigned* reset_ctr, void* stream);
+int rtpb_dgrad_pass(const void* dy, size_t ldy, size_t dy_cols, const void* buf0, const void* buf1,
+                    const size_t* col0, unsigned buf_mask, size_t steps, float* acc, size_t ld_acc, void* dx,
+                    size_t ldx, const void* pre, size_t ldpre, size_t M, size_t I, size_t per, int flags,
+                    const unsigned* ready, unsigned* done, unsigned* done_target, unsigned* reset_ctr,
+                    void* stream);
 
 /* dW step with the travelling-gradient accumulation fused into the epilogue
  * (layers_linear.cpp:61-63, kern::matmul_tn_acc + bias column sums):
@@ -238,6 +274,13 @@ size_t rtpb_group_local_ranks(rtpb_group g, size_t* ranks);
 void* rtpb_group_stream(rtpb_group g, size_t rank, int comm);
 int rtpb_group_device(rtpb_group g, size_t rank);
 int rtpb_group_synchronize(rtpb_group g);
+
+/* Debug hook: copy `count` entries of a local worker's arrival-flag pool
+ * (from index `first`) to host memory through a private stream (does not
+ * wait for the worker's streams), and report which of its streams (bit 0
+ * compute, 1 comm, 2 aux) still have work pending. */
+int rtpb_debug_read_flags(rtpb_group g, size_t rank, size_t first, size_t count, unsigned* host_dst,
+                          int* busy_streams);
 /* Traffic log (ring.hpp:41-46): kind 0 rotation_cw, 1 rotation_ccw, 2 allgather. */
 size_t rtpb_group_traffic(rtpb_group g, int64_t* kinds, int64_t* w_elems, int64_t* g_elems, size_t cap);
 void rtpb_group_clear_traffic(rtpb_group g);

@@ -518,12 +518,16 @@ class RtpLinear : public RtpLayerBase {
   void drop_prefetch() override;
   void forward_impl(std::span<const DView> x, size_t rows, std::span<const DView> y, Mode mode, const FwdEpi& e);
   void backward_impl(std::span<const DView> dy, size_t rows, std::span<const DView> dx, const BwdEpi& e);
+  void backward_pass(std::span<const DView> dy, size_t rows, std::span<const DView> dx, const BwdEpi& e);
   // Shard-arrival flags (rtp_layers.cpp): forward W, backward W, backward G
   // blocks of the layer's flag range, indexed by the step the shard is for.
   static constexpr size_t kFlagFwd = 0, kFlagBwdW = 16, kFlagBwdG = 32;
   // CTA counters of the grids that clear each block (the pass's last reader)
   static constexpr size_t kFlagCtrFwd = 48, kFlagCtrW = 49, kFlagCtrG = 50;
+  // Pass launches: per-step count-in counters of the forward / dX launch
+  static constexpr size_t kFlagDoneFwd = 64, kFlagDoneBwd = 80;
   bool use_flags() const;
+  bool pass_launch_ok() const;
   void flagged_exchange(Direction dir, std::span<void* const> send, std::span<void* const> recv, size_t bytes,
                         size_t flag);
 

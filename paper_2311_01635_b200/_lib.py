@@ -33,6 +33,7 @@ _SIGS = {
     "rtpb_debug_force_bn": (None, [_int]),
     "rtpb_debug_trace": (None, [_vp, _sz]),
     "rtpb_debug_skip_comm": (None, [_int]),
+    "rtpb_debug_read_flags": (_int, [_vp, _sz, _sz, _sz, C.POINTER(C.c_uint), C.POINTER(_int)]),
     "rtpb_profile_enable": (None, [_int]),
     "rtpb_profile_read": (_sz, [C.POINTER(_int), C.POINTER(_dbl), C.POINTER(C.c_float), C.POINTER(C.c_float),
                                 C.POINTER(_int), _sz]),
@@ -45,6 +46,11 @@ _SIGS = {
                                _sz, _vp]),
     "rtpb_dgrad_step2": (_int, [_int, _vp, _sz, _sz, _vp, _sz, _vp, _vp, _sz, _vp, _sz, _vp, _sz, _sz, _sz, _sz,
                                  _int, _vp, _sz, _vp]),
+    "rtpb_pass_done_target": (C.c_uint, [_int, _sz, _sz, _sz, _sz, _int]),
+    "rtpb_fwd_pass": (_int, [_vp, _sz, _vp, _vp, _vp, _sz, _vp, _sz, _sz, C.POINTER(_sz), C.c_uint, _sz, _sz, _sz,
+                             _sz, _int, _vp, _vp, C.POINTER(C.c_uint), _vp, _vp]),
+    "rtpb_dgrad_pass": (_int, [_vp, _sz, _sz, _vp, _vp, C.POINTER(_sz), C.c_uint, _sz, _vp, _sz, _vp, _sz, _vp, _sz,
+                               _sz, _sz, _sz, _int, _vp, _vp, C.POINTER(C.c_uint), _vp, _vp]),
     "rtpb_wgrad_step": (_int, [_int, _vp, _sz, _vp, _sz, _sz, _vp, _vp, _sz, _sz, _sz, _vp, _sz, _vp]),
     "rtpb_gelu": (_int, [_int, _vp, _vp, _sz, _vp]),
     "rtpb_convert": (_int, [_vp, _int, _vp, _int, _sz, _vp]),

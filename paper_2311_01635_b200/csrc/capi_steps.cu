@@ -288,6 +288,72 @@ int rtpb_dgrad_step(int dtype, const void* dy, size_t ldy, size_t col0, const vo
   return timed(1, 2.0 * M * I * per, s, [&] { return gemm_dgrad(f32, p, s); });
 }
 
+namespace {
+int check_pass(size_t M, size_t I, size_t per, const size_t* col0, size_t steps, size_t cols, int* icol) {
+  int rc = check_geom(M, I, per);
+  if (rc) return rc;
+  if (steps < 2 || steps > 16) return set_error(RTPB_ERR_CONFIG, "pass launch: 2..16 steps");
+  if (per % 32) return set_error(RTPB_ERR_CONFIG, "pass launch: out_dim / N must be a multiple of 32");
+  if (!col0) return set_error(RTPB_ERR_DIMENSION, "pass launch: null column offsets");
+  for (size_t s = 0; s < steps; ++s) {
+    if (col0[s] + per > cols) return set_error(RTPB_ERR_DIMENSION, "pass launch: column block out of range");
+    icol[s] = int(col0[s]);
+  }
+  return RTPB_OK;
+}
+}  // namespace
+
+unsigned rtpb_pass_done_target(int which, size_t M, size_t I, size_t per, size_t steps, int flags) {
+  const int groups = int((which == 1 && (flags & RTPB_PASS_PAIR)) ? (steps + 1) / 2 : steps);
+  return which == 1 ? pass_done_target(true, M, I, flags & RTPB_EPI_GELU_BWD, g_force_bn, groups)
+                    : pass_done_target(false, M, per, false, g_force_bn, groups);
+}
+
+int rtpb_fwd_pass(const void* x, size_t ldx, const void* buf0, const void* buf1, void* y, size_t ldy, void* act,
+                  size_t ld_act, size_t y_cols, const size_t* col0, unsigned buf_mask, size_t steps, size_t M,
+                  size_t I, size_t per, int flags, const unsigned* ready, unsigned* done, unsigned* done_target,
+                  unsigned* reset_ctr, void* stream) {
+  int icol[16];
+  int rc = check_pass(M, I, per, col0, steps, y_cols, icol);
+  if (rc) return rc;
+  if (!buf0 || !buf1 || !done_target) return set_error(RTPB_ERR_DIMENSION, "fwd_pass: null shard buffer / target");
+  if ((flags & RTPB_EPI_STORE_PRE) && !y) return set_error(RTPB_ERR_DIMENSION, "fwd_pass: null y");
+  if ((flags & RTPB_EPI_GELU) && !act) return set_error(RTPB_ERR_DIMENSION, "fwd_pass: null act");
+  if (!(flags & (RTPB_EPI_STORE_PRE | RTPB_EPI_GELU))) flags |= RTPB_EPI_STORE_PRE;
+  cudaStream_t s = as_stream(stream);
+  StepFwd p{};
+  p.x = x; p.ldx = ldx; p.w = buf0;
+  p.bias = (flags & RTPB_EPI_NO_BIAS) ? nullptr : static_cast<const char*>(buf0) + I * per * 2;
+  flags &= ~RTPB_EPI_NO_BIAS;
+  p.y = y; p.ldy = ldy; p.act = act; p.ld_act = ld_act;
+  p.M = M; p.I = I; p.per = per; p.flags = flags; p.force_bn = g_force_bn;
+  const PassArgs pa{int(steps), buf_mask, icol, ready, done, reset_ctr};
+  return timed(0, 2.0 * M * I * per * steps, s, [&] { return gemm_fwd_pass(p, buf1, y_cols, pa, s, done_target); });
+}
+
+int rtpb_dgrad_pass(const void* dy, size_t ldy, size_t dy_cols, const void* buf0, const void* buf1,
+                    const size_t* col0, unsigned buf_mask, size_t steps, float* acc, size_t ld_acc, void* dx,
+                    size_t ldx, const void* pre, size_t ldpre, size_t M, size_t I, size_t per, int flags,
+                    const unsigned* ready, unsigned* done, unsigned* done_target, unsigned* reset_ctr,
+                    void* stream) {
+  int icol[16];
+  int rc = check_pass(M, I, per, col0, steps, dy_cols, icol);
+  if (rc) return rc;
+  if (!buf0 || !buf1 || !done_target) return set_error(RTPB_ERR_DIMENSION, "dgrad_pass: null shard buffer / target");
+  if (!acc || !dx) return set_error(RTPB_ERR_DIMENSION, "dgrad_pass: null accumulator / dx");
+  if ((flags & RTPB_EPI_GELU_BWD) && !pre) return set_error(RTPB_ERR_DIMENSION, "dgrad_pass: null pre");
+  cudaStream_t s = as_stream(stream);
+  StepDgrad p{};
+  p.dy = dy; p.ldy = ldy; p.w = buf0; p.acc = acc; p.ld_acc = ld_acc; p.dx = dx; p.ldx = ldx;
+  p.pre = pre; p.ldpre = ldpre;
+  const int pair = (flags & RTPB_PASS_PAIR) ? 1 : 0;
+  flags &= ~RTPB_PASS_PAIR;
+  p.M = M; p.I = I; p.per = per; p.flags = flags; p.force_bn = g_force_bn;
+  const PassArgs pa{int(steps), buf_mask, icol, ready, done, reset_ctr, pair};
+  return timed(1, 2.0 * M * I * per * steps, s,
+               [&] { return gemm_dgrad_pass(p, buf1, dy_cols, pa, s, done_target); });
+}
+
 int rtpb_dgrad_step2(int dtype, const void* dy, size_t ldy, size_t col0, const void* w_a, size_t col1,
                      const void* w_b, float* acc, size_t ld_acc, void* dx, size_t ldx, const void* pre,
                      size_t ldpre, size_t M, size_t I, size_t per, int flags, void* workspace,

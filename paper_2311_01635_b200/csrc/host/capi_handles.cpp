@@ -220,6 +220,28 @@ int rtpb_group_device(rtpb_group g, size_t rank) {
   }
 }
 
+int rtpb_debug_read_flags(rtpb_group g, size_t rank, size_t first, size_t count, unsigned* host_dst,
+                          int* busy_streams) {
+  return guard([&] {
+    Worker& w = g->g->worker(rank);
+    DeviceGuard dg(w.device);
+    if (first + count > Worker::kFlagPool) throw DimensionError("debug_read_flags: out of range");
+    cudaStream_t s = nullptr;
+    cuda_check(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "debug stream");
+    cuda_check(cudaMemcpyAsync(host_dst, w.flag(first), count * sizeof(unsigned), cudaMemcpyDeviceToHost, s),
+               "debug read flags");
+    cuda_check(cudaStreamSynchronize(s), "debug read flags");
+    cudaStreamDestroy(s);
+    if (busy_streams) {
+      int b = 0;
+      if (cudaStreamQuery(w.compute) == cudaErrorNotReady) b |= 1;
+      if (cudaStreamQuery(w.comm) == cudaErrorNotReady) b |= 2;
+      if (cudaStreamQuery(w.aux) == cudaErrorNotReady) b |= 4;
+      *busy_streams = b;
+    }
+  });
+}
+
 int rtpb_group_synchronize(rtpb_group g) {
   return guard([&] { g->g->synchronize(); });
 }

@@ -15,6 +15,7 @@
 #include <mutex>
 #include <thread>
 
+#include "kernels/launch.hpp"
 #include "worker.hpp"
 
 namespace rtpb {
@@ -173,6 +174,7 @@ Worker::Worker(size_t r, int dev) : rank(r), device(dev) {
   cuda_check(cudaStreamCreateWithFlags(&aux, cudaStreamNonBlocking), "stream");
   flags = DeviceBuffer(dev, kFlagPool * sizeof(unsigned), nullptr, MemCategory::Other, true);
   for (auto& e : ev) cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+  preload_device_kernels();  // no lazy kernel load may wait behind a spinning grid (launch.hpp)
 }
 Worker::~Worker() {
   DeviceGuard g(device);
@@ -199,6 +201,21 @@ void stream_write_u32(cudaStream_t s, unsigned* addr, unsigned v) {
   const CUresult r = fn(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(addr), v,
                         CU_STREAM_WRITE_VALUE_DEFAULT);
   if (r != CUDA_SUCCESS) throw CudaError("cuStreamWriteValue32 failed: " + std::to_string(int(r)));
+}
+
+void stream_wait_geq_u32(cudaStream_t s, const unsigned* addr, unsigned v) {
+  static PFN_cuStreamWaitValue32_v11070 fn = [] {
+    cudaDriverEntryPointQueryResult q;
+    void* f = nullptr;
+    if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      f = nullptr;
+    return reinterpret_cast<PFN_cuStreamWaitValue32_v11070>(f);
+  }();
+  if (!fn) throw CudaError("cuStreamWaitValue32 unavailable");
+  const CUresult r = fn(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(const_cast<unsigned*>(addr)), v,
+                        CU_STREAM_WAIT_VALUE_GEQ);
+  if (r != CUDA_SUCCESS) throw CudaError("cuStreamWaitValue32 failed: " + std::to_string(int(r)));
 }
 
 size_t inplace_chunk_bytes(size_t shard_bytes) {

@@ -460,6 +460,59 @@ void RtpLinear::forward_impl(std::span<const DView> x, size_t rows, std::span<co
   const bool prefetch = oop();
   std::vector<void*> wp(n, nullptr), sp(n, nullptr);
 
+  if (pass_launch_ok()) {
+    // The whole pass as ONE persistent launch (rtpb_fwd_pass): the host does
+    // the N steps' bookkeeping up front, the comm stream lands shard s + 1
+    // in the buffer step s - 1 read once the launch has counted step s - 1
+    // out (cuStreamWaitValue32), and the launch's step s + 1 tiles wait for
+    // its arrival flag. Same tiles, same bits as the per-step launches.
+    const size_t r = local[0];
+    Worker& w = group_->worker(r);
+    void* buf[2] = {slots_[r].weight.data(), spares_[r].data()};
+    size_t cols[16];
+    unsigned mask = 0;
+    for (size_t s = 0; s < n; ++s) {
+      check_forward_position(r, s);
+      trace_[s * n + r] = int64_t(slots_[r].logical_id);
+      if (mode == Mode::Train) tapes_[r].record(slots_[r].logical_id, {});
+      cols[s] = slots_[r].logical_id * per_;
+      if (s & 1) mask |= 1u << s;
+      if (s + 1 < n) group_->advance_slots(slots_, Direction::Clockwise, PayloadKind::Weight, label_, shard_len_);
+    }
+    int flags = e.store_pre ? RTPB_EPI_STORE_PRE : 0;
+    void* act = nullptr;
+    size_t ld_act = 0;
+    if (!e.act.empty()) {
+      flags |= RTPB_EPI_GELU | (exact_gelu_ ? RTPB_EPI_EXACT_GELU : 0);
+      act = e.act[0].data;
+      ld_act = e.act[0].ld ? e.act[0].ld : out_;
+    }
+    const unsigned target = rtpb_pass_done_target(0, rows, in_, per_, n, flags);
+    unsigned* done = w.flag(flag_base_ + kFlagDoneFwd);
+    group_->comm_after_compute();  // the spare's last reader (the previous pass) is done
+    for (size_t s = 0; s + 1 < n; ++s) {
+      if (s == 0 && pre_fwd_) continue;  // posted under the previous layer's last step
+      if (s >= 1) stream_wait_geq_u32(w.comm, done + (s - 1), target);  // step s - 1's buffer is free
+      wp[r] = buf[s & 1];
+      sp[r] = buf[(s + 1) & 1];
+      flagged_exchange(Direction::Clockwise, wp, sp, slots_[r].weight.bytes(), kFlagFwd + s + 1);
+    }
+    pre_fwd_ = false;
+    w.record(Ev::PassEnd, true);
+    if (e.before_last_step) e.before_last_step();  // its shifts queue behind this pass's
+    void* yp = e.store_pre ? y[0].data : nullptr;
+    const size_t ldy = e.store_pre && y[0].ld ? y[0].ld : out_;
+    unsigned tgt = 0;
+    check_status(rtpb_fwd_pass(x[0].data, x[0].ld ? x[0].ld : in_, buf[0], buf[1], yp, ldy, act, ld_act, out_, cols,
+                               mask, n, rows, in_, per_, flags, w.flag(flag_base_ + kFlagFwd), done, &tgt,
+                               w.flag(flag_base_ + kFlagCtrFwd), w.compute));
+    if (tgt != target) throw StateError(label_ + ": pass launch count-in target mismatch");
+    if ((n - 1) & 1) swap_data(slots_[r].weight, spares_[r]);  // the pass's n - 1 swaps
+    w.wait(Ev::PassEnd, false);  // join the pass's shifts (stream capture requires it)
+    if (mode == Mode::Eval) rehome_after_eval();
+    return;
+  }
+
   for (size_t s = 0; s < n; ++s) {
     group_->each([&](size_t r) {
       check_forward_position(r, s);
@@ -550,6 +603,20 @@ bool RtpLinear::use_flags() const {
   const TransportKind k = group_->kind();
   const bool one_per_gpu = k == TransportKind::Nccl || k == TransportKind::Ipc || k == TransportKind::Solo;
   return on && one_per_gpu && dtype_ == DType::BF16 && group_->size() > 1 && group_->size() <= 16;
+}
+
+// Pass launches (rtpb_fwd_pass / rtpb_dgrad_pass) ride on the arrival flags:
+// one worker per GPU, out of place (the shard alternates between the resident
+// buffer and the spare), column blocks in whole 32-column store boxes.
+// RTPB_NO_PASS=1 keeps one launch per step.
+bool RtpLinear::pass_launch_ok() const {
+  static const bool off = [] {
+    const char* e = std::getenv("RTPB_NO_PASS");
+    return e && std::atoi(e) != 0;
+  }();
+  const size_t n = group_->size();
+  return !off && use_flags() && oop() && group_->local_ranks().size() == 1 && n >= 2 && n <= 16 && per_ % 32 == 0 &&
+         spares_.size() == n;
 }
 
 void RtpLinear::flagged_exchange(Direction dir, std::span<void* const> send, std::span<void* const> recv,
@@ -708,6 +775,11 @@ void RtpLinear::backward_impl(std::span<const DView> dy, size_t rows, std::span<
     check_status(rc);
     grads_zero_pending_ = false;
     x_cache_[r] = {};
+    return;
+  }
+
+  if (pass_launch_ok()) {
+    backward_pass(dy, rows, dx, e);
     return;
   }
 
@@ -871,6 +943,122 @@ void RtpLinear::backward_impl(std::span<const DView> dy, size_t rows, std::span<
   }
   grads_zero_pending_ = false;
   for (size_t r : local) x_cache_[r] = {};
+  require_home("end of backward");
+}
+
+// Backward as a dX pass launch beside per-step dW launches (one worker per
+// GPU, out of place, arrival flags). The dX of all N steps is ONE persistent
+// launch (rtpb_dgrad_pass) on the compute stream, holding its share of the
+// SMs; the dW of step s runs on the aux stream on the rest, its epilogue
+// waiting for the travelling gradient G (GemmArgs::g_flag). The comm stream
+// moves, per step, the next weight shard into the buffer the dX launch has
+// counted out (cuStreamWaitValue32 on its count-ins) and the gradient shard
+// once dW(s) is done (event from aux). No wait closes a cycle: dW depends only
+// on G shifts, each G shift only on the dW before it and earlier shifts (it
+// is posted ahead of the step's W shift), dX only on W shifts; the dX grid
+// holds its SM share, a dW grid the rest. Paired dX (paired_dx_) pairs the steps as
+// rtpb_dgrad_step2 does; otherwise the bits equal the per-step launches'.
+void RtpLinear::backward_pass(std::span<const DView> dy, size_t rows, std::span<const DView> dx, const BwdEpi& e) {
+  const size_t n = group_->size();
+  const size_t r = group_->local_ranks()[0];
+  Worker& w = group_->worker(r);
+  void* buf[2] = {slots_[r].weight.data(), spares_[r].data()};
+  size_t cols[16];
+  unsigned mask = 0;
+  for (size_t s = 0; s < n; ++s) {
+    const size_t j = slots_[r].logical_id;
+    tapes_[r].replay(j);
+    check_backward_position(r, s);
+    trace_[n * n + s * n + r] = int64_t(j);
+    cols[s] = j * per_;
+    if (s & 1) mask |= 1u << s;
+    if (s + 1 < n)
+      group_->advance_slots(slots_, Direction::CounterClockwise, PayloadKind::WeightAndGrad, label_, shard_len_);
+  }
+  const bool pair = paired_dx_;
+  int flags = pair ? RTPB_PASS_PAIR : 0;
+  const void* pre = nullptr;
+  size_t ldpre = 0;
+  if (!e.pre.empty()) {
+    flags |= RTPB_EPI_GELU_BWD | (exact_gelu_ ? RTPB_EPI_EXACT_GELU : 0);
+    pre = e.pre[0].data;
+    ldpre = e.pre[0].ld ? e.pre[0].ld : in_;
+  }
+  unsigned* done = w.flag(flag_base_ + kFlagDoneBwd);
+  auto group_of = [&](size_t s) { return pair ? s / 2 : s; };
+  const int all = sm_budget();
+  int d_sms = all / 2 & ~1;
+  if (const char* ev = std::getenv("RTPB_PASS_DX_SMS")) d_sms = std::max(2, std::min(all - 2, std::atoi(ev))) & ~1;
+  set_sm_budget(d_sms);  // the tiles (and count-ins) of the dX launch depend on its SM share
+  const unsigned target = rtpb_pass_done_target(1, rows, in_, per_, n, flags);
+  set_sm_budget(all);
+  const size_t ldy = dy[0].ld ? dy[0].ld : out_, ldx = dx[0].ld ? dx[0].ld : in_;
+  const size_t ldxc = x_cache_[r].ld ? x_cache_[r].ld : in_;
+
+  group_->comm_after_compute();  // the spare's last reader is done
+  w.fork_aux();                  // dW reads dY and X, complete on compute
+  // The dX launch first, so its grid takes its SM share before the dW grids
+  // (which then fill the rest).
+  set_sm_budget(d_sms);
+  unsigned tgt = 0;
+  int rc = rtpb_dgrad_pass(dy[0].data, ldy, out_, buf[0], buf[1], cols, mask, n,
+                           static_cast<float*>(dx_acc_[r].data()), in_, dx[0].data, ldx, pre, ldpre, rows, in_, per_,
+                           flags, w.flag(flag_base_ + kFlagBwdW), done, &tgt, w.flag(flag_base_ + kFlagCtrW),
+                           w.compute);
+  set_sm_budget(all);
+  check_status(rc);
+  if (tgt != target) throw StateError(label_ + ": pass launch count-in target mismatch");
+  std::vector<void*> wp(n, nullptr), sp(n, nullptr), gp(n, nullptr);
+  unsigned dummy_flags = 0;
+  set_sm_budget(all - d_sms);
+  const bool g_flag = wgrad_fuses_bias(false, rows, in_, per_, &dummy_flags, 0);
+  float* g = static_cast<float*>(slots_[r].grad_acc.data());
+  try {
+    for (size_t s = 0; s < n; ++s) {
+      // dW(s): G_j += X^T dY_j on aux; G(s) arrives by flag (or stream event)
+      if (s > 0 && !g_flag) w.wait_on(Ev::GDone, w.aux);
+      set_launch_g_flag(g_flag && s > 0 ? w.flag(flag_base_ + kFlagBwdG + s) : nullptr);
+      if (s + 1 == n)  // the last dW clears the pass's G flags
+        set_launch_flag_reset(w.flag(flag_base_ + kFlagBwdG), int(kFlagCtrFwd - kFlagBwdG),
+                              w.flag(flag_base_ + kFlagCtrG));
+      const float* g_in = (grads_zero_pending_ && s == 0) ? nullptr : g;
+      rc = rtpb_wgrad_step(RTPB_BF16, x_cache_[r].data, ldxc, dy[0].data, ldy, cols[s], g_in, g, rows, in_, per_,
+                           workspace_[r].data(), workspace_[r].bytes(), w.aux);
+      set_launch_g_flag(nullptr);
+      set_launch_flag_reset(nullptr, 0, nullptr);
+      check_status(rc);
+      if (s + 1 == n) break;
+      w.record_on(Ev::AuxDone, w.aux);
+      // G shift once dW(s) is done: the gradient travels with its
+      // accumulation. It precedes the step's W shift on the comm stream, so
+      // the dW chain never waits for the dX launch (a dW grid spinning for G
+      // may hold the SMs the dX launch needs: G must not queue behind W).
+      w.wait_on(Ev::AuxDone, w.comm);
+      gp[r] = g;
+      flagged_exchange(Direction::CounterClockwise, gp, gp, slots_[r].grad_acc.bytes(), kFlagBwdG + s + 1);
+      w.record(Ev::GDone, true);
+      // W shift for step s + 1 into the buffer step s - 1 read
+      if (!(s == 0 && pre_bwd_)) {
+        if (s >= 1) stream_wait_geq_u32(w.comm, done + group_of(s - 1), target);
+        wp[r] = buf[s & 1];
+        sp[r] = buf[(s + 1) & 1];
+        flagged_exchange(Direction::CounterClockwise, wp, sp, slots_[r].weight.bytes(), kFlagBwdW + s + 1);
+      }
+    }
+  } catch (...) {
+    set_sm_budget(all);
+    throw;
+  }
+  pre_bwd_ = false;
+  w.record(Ev::PassEnd, true);
+  set_sm_budget(all);
+  // the next layer's prefetched shift queues behind this pass's (it waits for
+  // the dX launch too: its comm fence records the compute stream's tail)
+  if (e.before_last_step) e.before_last_step();
+  if ((n - 1) & 1) swap_data(slots_[r].weight, spares_[r]);  // the pass's n - 1 swaps
+  w.wait(Ev::PassEnd, false);
+  grads_zero_pending_ = false;
+  x_cache_[r] = {};
   require_home("end of backward");
 }
 

@@ -45,7 +45,7 @@ struct Worker {
   DeviceBuffer stage;  // in-place rotation staging chunk (CommBuffer)
   // Shard-arrival flags written by the comm stream (stream memory ops) and
   // waited on inside the step GEMMs; kFlagsPerLayer per layer.
-  static constexpr size_t kFlagPool = 16384, kFlagsPerLayer = 64;
+  static constexpr size_t kFlagPool = 16384, kFlagsPerLayer = 128;
   DeviceBuffer flags;
   unsigned* flag(size_t i) { return static_cast<unsigned*>(flags.data()) + i; }
 
@@ -76,6 +76,10 @@ struct Worker {
 // Stream memory operation: *addr = v once the stream's prior work is done
 // (cuStreamWriteValue32 with its default memory barrier).
 void stream_write_u32(cudaStream_t s, unsigned* addr, unsigned v);
+// Stream memory operation: the stream waits until *addr >= v
+// (cuStreamWaitValue32, GEQ) — written by a kernel still running on another
+// stream (a pass launch's count-ins).
+void stream_wait_geq_u32(cudaStream_t s, const unsigned* addr, unsigned v);
 
 // In-place rotation staging chunk: a small fraction of the shard so the
 // in-place mode stays within its (W+G)/N memory model.

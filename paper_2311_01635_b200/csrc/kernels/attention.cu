@@ -371,4 +371,8 @@ int attention_core_bwd(bool f32, const void* q, const void* k, const void* v, co
   return post("attn_bwd_dkdv_kernel");
 }
 
+const void* kernel_anchor_attention() {
+  return reinterpret_cast<const void*>(&attn_bwd_delta_kernel<__nv_bfloat16>);
+}
+
 }  // namespace rtpb

@@ -341,4 +341,8 @@ int cast_f32_to_bf16(const float* src, void* dst, size_t n, cudaStream_t s) {
   return post_launch("cast_kernel");
 }
 
+// Module anchor for preload_device_kernels (launch.hpp): any kernel of this
+// translation unit's module.
+const void* kernel_anchor_elementwise() { return reinterpret_cast<const void*>(&tf32_split_kernel); }
+
 }  // namespace rtpb

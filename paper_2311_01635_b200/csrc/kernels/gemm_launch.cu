@@ -221,7 +221,7 @@ int launch_cfg(const Op& a, const Op& b, const Out& c0, const Out* c1, const Gem
 // Choice minimises wave-quantised time: ceil(tiles / slots) * per-tile cost,
 // per-tile cost = per-SM work / relative MMA efficiency + fixed overhead
 // (relative efficiencies from measured B200 throughput of each shape).
-int choose_tile(int M, int N, bool tf32) {
+int choose_tile(int M, int N, bool tf32, int mult = 1) {
   struct Cand {
     int code, rows, bn;
     double eff;
@@ -237,7 +237,7 @@ int choose_tile(int M, int N, bool tf32) {
   double best_cost = -1;
   for (int i = 0; i < nc; ++i) {
     const bool pair = c[i].code > 1000;
-    const long tiles = long((M + c[i].rows - 1) / c[i].rows) * ((N + c[i].bn - 1) / c[i].bn);
+    const long tiles = long((M + c[i].rows - 1) / c[i].rows) * ((N + c[i].bn - 1) / c[i].bn) * mult;
     const long slots = pair ? sms / 2 : sms;
     const long waves = (tiles + slots - 1) / slots;
     const double cost = double(waves) * (128.0 * c[i].bn / c[i].eff + 48.0 * 128.0);
@@ -323,6 +323,26 @@ int pick_code(bool tf32, GemmArgs& args, int force) {
         }
       }
       if (s >= 2) args.k_splits = s;
+    } else if (!force && code == 1256 && tiles % pairs != 0) {
+      // Enough tiles for every pair, but the last wave is partial (config (d)
+      // at N = 8: 128 pair tiles over 74 pairs = 1.73 waves run as 2). Split
+      // K in S ordered parts so the S x tiles units quantise better; the
+      // epilogue of a unit overlaps the next unit's mainloop (two TMEM
+      // accumulators), the ordered chain's partner is ~tiles units earlier.
+      // Time ~ rounds(S) x mainloop / S, +1 exposed epilogue per split.
+      const double ck = 0.35, ce = 3.0;
+      auto cost = [&](int c) {
+        const int rounds = (tiles * c + pairs - 1) / pairs;
+        return rounds * std::max(kb * ck / c, ce) + ce * c;
+      };
+      int s = 1;
+      double best_t = cost(1);
+      for (int c = 2; c <= 4 && kb / c >= 16; ++c)
+        if (cost(c) < 0.95 * best_t) {
+          best_t = cost(c);
+          s = c;
+        }
+      if (s >= 2) args.k_splits = s;
     }
   }
   return code;
@@ -342,7 +362,125 @@ int dispatch(bool tf32, const Op& a, const Op& b, const Out& c0, const Out* c1, 
               : dispatch_tile<EPI, false>(code, a, b, c0, c1, args, s);
 }
 
+// Pass launch (GemmArgs::pass_steps): maps carry buffer 0's B operand and the
+// outputs, maps2 buffer 1's B operand (and, DGRAD, the dX output as c0).
+template <class Cfg>
+int launch_pass(const Op& a, const Op& b0, const Op& b1, const Out& c0, const Out* c1, const Out& d0,
+                const Out* d1, const GemmArgs& args, cudaStream_t s, unsigned* done_target) {
+  GemmMaps m2;
+  int rc;
+  if ((rc = encode_maps<Cfg>(a, b1, d0, d1, m2))) return rc;
+  const unsigned tiles = unsigned((args.M + Cfg::TILE_M - 1) / Cfg::TILE_M) * unsigned((args.N + Cfg::BN - 1) / Cfg::BN);
+  *done_target = tiles * unsigned(Cfg::EPI_WARPS * (Cfg::PAIR ? 2 : 1));  // count-ins per step
+  return launch_cfg<Cfg>(a, b0, c0, c1, args, s, &m2);
+}
+
+template <int EPI>
+int dispatch_pass(int code, bool pre_tma, const Op& a, const Op& b0, const Op& b1, const Out& c0, const Out* c1,
+                  const Out& d0, const Out* d1, const GemmArgs& args, cudaStream_t s, unsigned* target) {
+  constexpr bool BMN = EPI != EPI_DGRAD;
+  if constexpr (EPI == EPI_DGRAD) {
+    if (pre_tma) {
+      if (code == 1256)
+        return launch_pass<GemmCfg<EPI, 256, false, kEpiWarps, false, false, true, true>>(a, b0, b1, c0, c1, d0, d1,
+                                                                                           args, s, target);
+      return launch_pass<GemmCfg<EPI, 128, false, kEpiWarps, false, false, true>>(a, b0, b1, c0, c1, d0, d1, args,
+                                                                                  s, target);
+    }
+  }
+  if (code == 1256)
+    return launch_pass<GemmCfg<EPI, 256, false, kEpiWarps, false, BMN, false, true>>(a, b0, b1, c0, c1, d0, d1, args,
+                                                                                       s, target);
+  if (code == 1128)
+    return launch_pass<GemmCfg<EPI, 128, false, kEpiWarps, false, BMN, false, true>>(a, b0, b1, c0, c1, d0, d1, args,
+                                                                                       s, target);
+  if (code == 256)
+    return launch_pass<GemmCfg<EPI, 256, false, kEpiWarps, false, BMN>>(a, b0, b1, c0, c1, d0, d1, args, s, target);
+  if (code == 64)
+    return launch_pass<GemmCfg<EPI, 64, false, kEpiWarps, false, BMN>>(a, b0, b1, c0, c1, d0, d1, args, s, target);
+  return launch_pass<GemmCfg<EPI, 128, false, kEpiWarps, false, BMN>>(a, b0, b1, c0, c1, d0, d1, args, s, target);
+}
+
+void fill_pass_args(GemmArgs& g, const PassArgs& p) {
+  g.pass_steps = p.steps;
+  g.pass_pair = p.pair;
+  g.pass_buf = p.buf_mask;
+  for (int s = 0; s < p.steps; ++s) g.pass_col[s] = p.cols[s];
+  g.pass_ready = p.ready;
+  g.pass_done = p.done;
+  g.flag_reset = p.reset_ctr ? const_cast<unsigned*>(p.ready) : nullptr;
+  g.flag_reset_count = p.reset_ctr && p.ready ? p.steps : 0;
+  g.flag_reset_ctr = p.reset_ctr;
+}
+
 }  // namespace
+
+// The tile code a pass launch of this geometry uses and its count-ins per
+// step. The shape is chosen for the pass's units (steps x tiles over the
+// slots: one wave-quantisation tail per pass, not per step); the tile shape
+// does not change a result's bits (same K order per element; checked by
+// tests/test_gpu_pass.py against the per-step launches).
+int pass_code(bool dgrad, size_t M, size_t N, bool gelu, int force, int groups) {
+  int code = force ? force : choose_tile(int(M), int(N), false, groups);
+  if (dgrad && gelu) code = code == 1256 ? 1256 : 128;  // the PRE_TMA shapes (as the last per-step launch)
+  return code;
+}
+unsigned pass_done_target(bool dgrad, size_t M, size_t N, bool gelu, int force, int groups) {
+  const int code = pass_code(dgrad, M, N, gelu, force, groups);
+  const size_t tm = code > 1000 ? 256 : 128, bn = code % 1000;
+  return unsigned(((M + tm - 1) / tm) * ((N + bn - 1) / bn)) * unsigned(kEpiWarps * (code > 1000 ? 2 : 1));
+}
+
+int gemm_fwd_pass(const StepFwd& p, const void* w1, size_t y_cols, const PassArgs& pa, cudaStream_t s,
+                  unsigned* done_target) {
+  // Step s: C[M x per] = X . W(s) with W(s) the I x per block of buffer s.
+  Op a{p.x, nullptr, p.I, p.M, p.ldx};
+  Op b0{p.w, nullptr, p.per, p.I, p.per}, b1{w1, nullptr, p.per, p.I, p.per};
+  GemmArgs g{};
+  g.M = int(p.M);
+  g.N = int(p.per);
+  g.K = int(p.I);
+  g.flags = p.flags;
+  g.aux = p.bias;
+  g.aux2 = p.bias ? static_cast<const char*>(w1) + p.I * p.per * 2 : nullptr;
+  fill_pass_args(g, pa);
+  // full-width outputs: step s stores at column pass_col[s] + n
+  Out y{p.y, false, y_cols, p.M, p.ldy}, act{p.act, false, y_cols, p.M, p.ld_act};
+  const bool has_y = (p.flags & EF_STORE_PRE) && p.y;
+  const bool has_act = (p.flags & EF_GELU) && p.act;
+  const Out& c0 = has_y ? y : act;
+  const int code = pass_code(false, p.M, p.per, false, p.force_bn, pa.steps);
+  const int bn = code % 1000;
+  g.n_fastest = raster_mode(g.M, g.N, g.K, code > 1000 ? 256 : 128, bn, false, false);
+  const Out* c1 = has_act ? &act : nullptr;
+  return dispatch_pass<EPI_FWD>(code, false, a, b0, b1, c0, c1, c0, c1, g, s, done_target);
+}
+
+int gemm_dgrad_pass(const StepDgrad& p, const void* w1, size_t dy_cols, const PassArgs& pa, cudaStream_t s,
+                    unsigned* done_target) {
+  // Step s: acc (+)= dY[:, pass_col[s] :] . W(s)^T; A = the whole dY, K-major,
+  // read from column pass_col[s] (K past per multiplies W rows past per: zeros).
+  Op a{p.dy, nullptr, dy_cols, p.M, p.ldy};
+  Op b0{p.w, nullptr, p.per, p.I, p.per}, b1{w1, nullptr, p.per, p.I, p.per};
+  GemmArgs g{};
+  g.M = int(p.M);
+  g.N = int(p.I);
+  g.K = int(p.per);
+  g.flags = p.flags & ~(EF_FIRST | EF_LAST);
+  g.aux = p.pre;
+  g.ld_aux = int64_t(p.ldpre);
+  g.acc = p.acc;
+  g.ld_acc = int64_t(p.ld_acc);
+  fill_pass_args(g, pa);
+  Out acc{p.acc, true, p.I, p.M, p.ld_acc}, dx{p.dx, false, p.I, p.M, p.ldx};
+  const bool gelu = p.flags & EF_GELU_BWD;
+  Out pre{p.pre, false, p.I, p.M, p.ldpre};
+  const int code = pass_code(true, p.M, p.I, gelu, p.force_bn, pa.pair ? (pa.steps + 1) / 2 : pa.steps);
+  const int bn = code % 1000;
+  g.n_fastest = raster_mode(g.M, g.N, g.K, code > 1000 ? 256 : 128, bn, false, false);
+  return dispatch_pass<EPI_DGRAD>(code, gelu, a, b0, b1, acc, gelu ? &pre : nullptr, dx, gelu ? &pre : nullptr, g,
+                                  s, done_target);
+}
 
 // ------------------------------------------------------------------ fused MLP forward (N = 1)
 // ffn1 (h -> f, + bias, GELU) and ffn2 (f -> h, + bias) in ONE persistent
@@ -802,6 +940,53 @@ int gemm_bwd_fused(const FusedBwdArgs& a, const FusedBwdPlan& plan, const FusedB
   return RTPB_OK;
 }
 
+const void* kernel_anchor_elementwise();
+const void* kernel_anchor_attention();
+const void* kernel_anchor_moe_embed();
+
+namespace {
+template <class T>
+T driver_fn(const char* name, int version) {
+  void* f = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPointByVersion(name, &f, version, cudaEnableDefault, &q) != cudaSuccess ||
+      q != cudaDriverEntryPointSuccess)
+    return nullptr;
+  return reinterpret_cast<T>(f);
+}
+}  // namespace
+
+void preload_device_kernels() {
+  static std::mutex mu;
+  static unsigned long long done_mask = 0;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return;
+  std::lock_guard lk(mu);
+  if (done_mask >> dev & 1ull) return;
+  done_mask |= 1ull << dev;
+  static const auto get_module = driver_fn<PFN_cuFuncGetModule_v11000>("cuFuncGetModule", 11000);
+  static const auto count_fns = driver_fn<PFN_cuModuleGetFunctionCount_v12040>("cuModuleGetFunctionCount", 12040);
+  static const auto enum_fns = driver_fn<PFN_cuModuleEnumerateFunctions_v12040>("cuModuleEnumerateFunctions", 12040);
+  static const auto load_fn = driver_fn<PFN_cuFuncLoad_v12040>("cuFuncLoad", 12040);
+  // one kernel per translation unit (= module of the fat binary)
+  const void* anchors[] = {
+      reinterpret_cast<const void*>(&rtp_gemm_kernel<GemmCfg<EPI_FWD, 256, false, kEpiWarps, false, true, false, true>>),
+      kernel_anchor_elementwise(), kernel_anchor_attention(), kernel_anchor_moe_embed()};
+  for (const void* a : anchors) {
+    cudaFunction_t f = nullptr;
+    if (cudaGetFuncBySymbol(&f, a) != cudaSuccess || !f) continue;  // (loads that kernel)
+    CUmodule mod = nullptr;
+    unsigned cnt = 0;
+    if (!get_module || !count_fns || !enum_fns || !load_fn || get_module(&mod, reinterpret_cast<CUfunction>(f)) ||
+        count_fns(&cnt, mod) || cnt == 0)
+      continue;
+    std::vector<CUfunction> fns(cnt);
+    if (enum_fns(fns.data(), cnt, mod)) continue;
+    for (CUfunction fn : fns) load_fn(fn);
+  }
+  cudaGetLastError();  // a failed probe leaves no sticky state behind
+}
+
 void set_sm_budget(int sms) { t_sm_budget = sms; }
 void set_launch_wait_flag(const unsigned* flag) { t_wait_flag = flag; }
 void set_launch_g_flag(const unsigned* flag) { t_g_flag = flag; }
@@ -937,11 +1122,19 @@ int wgrad_splits(bool f32, size_t M, size_t I, size_t per, int force_bn) {
   g.K = int(M);
   unsigned dummy = 0;
   g.split_flags = &dummy;
+  // the most splits any SM budget can ask for (workspace sizing): the
+  // split-to-fill choice grows with the budget, the wave-quantisation one
+  // does not, so every budget is evaluated
   const int saved = t_sm_budget;
-  t_sm_budget = 0;  // the whole machine: the most splits any budget can ask for
-  pick_code<EPI_WGRAD>(f32, g, force_bn);
+  int most = 1;
+  for (int b = device_sms(); b >= 2; b -= 2) {
+    t_sm_budget = b;
+    GemmArgs t = g;
+    pick_code<EPI_WGRAD>(f32, t, force_bn);
+    most = std::max(most, t.k_splits);
+  }
   t_sm_budget = saved;
-  return g.k_splits > 1 ? g.k_splits : 1;
+  return most;
 }
 
 size_t wgrad_partial_floats(bool f32, size_t M, size_t I, size_t per) {

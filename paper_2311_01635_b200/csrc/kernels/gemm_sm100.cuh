@@ -138,6 +138,39 @@ struct GemmArgs {
   unsigned dep_target;
   int dep_rows;
   unsigned* done_ctas;
+  // Pass launch (pass_steps = S > 0; FWD or DGRAD, one problem, no split-K):
+  // every rotation step of one layer pass in ONE persistent launch, so the
+  // N small step GEMMs of a ring pass pay one prologue and no launch gaps, and
+  // a tile's epilogue overlaps the next tile's MMAs across step boundaries.
+  // Work unit = (step s, tile t); slot k runs its tiles t = k, k + slots, ...
+  // for s = 0, 1, ... in order. Step s reads its weight shard through maps.b
+  // (bit s of pass_buf clear) or maps2.b (set): the resident shard and the
+  // out-of-place spare alternate.
+  //   FWD  : output at column pass_col[s] + n of the full-width maps c0 / c1
+  //          (the shard's column block j * per); bias from aux (buffer 0) or
+  //          aux2 (buffer 1). Requires per % 32 == 0 (32-column store boxes).
+  //   DGRAD: A (dY) read from column pass_col[s]; step 0 stores the fp32
+  //          accumulator (maps.c0), middle steps reduce-add into it, the last
+  //          loads it and writes dX through maps2.c0. A tile's successive
+  //          steps run on the same slot and warps, which drain their bulk
+  //          reductions at every step boundary: the summation order is the
+  //          step order, as with one launch per step.
+  // Step s >= 1 loads nothing before pass_ready[s] >= 1 (the comm stream's
+  // arrival flag). Once a tile's MMAs completed (its operands were read),
+  // every epilogue warp counts in on pass_done[g] (g: the unit's group, see
+  // pass_pair): the comm stream waits for tiles x warps there
+  // (cuStreamWaitValue32) before it lands a later shard in the group's
+  // buffers. The grid's last CTA re-zeroes pass_done.
+  // pass_pair (DGRAD): a unit covers the step pair (2g, 2g + 1) as two K
+  // segments — buffer 0 at dY column pass_col[2g], then buffer 1 at
+  // pass_col[2g + 1] — one accumulation over K = 2 per (paired dX: half the
+  // fp32 accumulator passes).
+  int pass_steps;
+  int pass_pair;
+  unsigned pass_buf;
+  int pass_col[16];
+  const unsigned* pass_ready;
+  unsigned* pass_done;
 };
 constexpr int TRACE_UNITS = 12;  // 2 + 6 * 12 slots + grid marker at TRACE_STRIDE - 1
 constexpr int TRACE_STRIDE = 80;
@@ -445,6 +478,15 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
     it_end = __ldg(args.sched + unit + 1);
     it_step = 1;
   }
+  // pass launch: this slot's tiles per step; iteration it -> (step, tile)
+  const bool pass = args.pass_steps > 0;
+  const int pass_nt = pass ? (num_tiles - unit + units - 1) / units : 0;
+  const int pass_groups = args.pass_pair ? (args.pass_steps + 1) / 2 : args.pass_steps;
+  if (pass) {
+    it_beg = 0;
+    it_end = pass_groups * pass_nt;
+    it_step = 1;
+  }
   const int num_m2 = (args.M2 + Cfg::TILE_M - 1) / Cfg::TILE_M;
   const int num_n2 = (args.N2 + BN - 1) / BN;
   const int num_kb2 = (args.K2 + BK - 1) / BK;
@@ -453,10 +495,22 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
   struct Unit {
     int prob, t, mb, nb, split, kb0, kb1, M, N, flags;
     bool whole;  // problem 1 of a split launch run unsplit (split code 0xFF)
+    int step;    // pass launch: rotation step, or step pair (pass_pair) (else 0)
+    bool buf1;   // pass launch: the step's shard is in buffer 1 (maps2.b / aux2)
+    int seg_kb;  // pass_pair: K blocks of the first step (the second step's start); 0 = one step
   };
   auto decode = [&](int it) {
     Unit x;
-    if (args.sched) {
+    x.step = 0;
+    x.buf1 = false;
+    x.seg_kb = 0;
+    if (pass) {
+      x.prob = 0;
+      x.split = 0;
+      x.step = it / pass_nt;
+      x.t = unit + (it % pass_nt) * units;
+      x.buf1 = !args.pass_pair && ((args.pass_buf >> x.step) & 1u);
+    } else if (args.sched) {
       const int e = __ldg(args.sched + it);
       x.prob = e >> 28;
       x.split = (e >> 20) & 0xFF;
@@ -499,6 +553,15 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
     x.M = x.prob ? args.M2 : args.M;
     x.N = x.prob ? args.N2 : args.N;
     x.flags = x.prob ? args.flags2 : args.flags;
+    if (pass) {  // DGRAD: the pass's first step stores the accumulator, its last emits dX
+      x.flags &= ~(EF_FIRST | EF_LAST);
+      if (x.step == 0) x.flags |= EF_FIRST;
+      if (x.step == pass_groups - 1) x.flags |= EF_LAST;
+      if (args.pass_pair && 2 * x.step + 1 < args.pass_steps) {
+        x.seg_kb = num_kb;
+        x.kb1 = 2 * num_kb;
+      }
+    }
     return x;
   };
 
@@ -555,8 +618,10 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
   }
   // Only a running grid admits its successor: a grid still waiting for its
   // shard must not let the next launch on its stream take the SMs that the
-  // other stream's kernels (the shard's producers' predecessors) need.
-  griddep_launch();
+  // other stream's kernels (the shard's producers' predecessors) need. (A
+  // pass launch admits it once its producer is past the last step's wait; a
+  // dW launch waiting for its travelling gradient once its epilogue has it.)
+  if (!pass && !(Cfg::EPI == EPI_WGRAD && args.g_flag)) griddep_launch();
   if (threadIdx.x == 0) detail::trace_at(trace, 1);
 
 
@@ -595,10 +660,20 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
         }
         return b * Cfg::NOPS;
       };
+      int ready_step = 0;  // pass launch: steps whose shard is known to have landed
       for (int it = it_beg; it < it_end; it += it_step) {
         const Unit x = decode(it);
         const int mb = x.mb, nb = x.nb, kb0 = x.kb0, kb1 = x.kb1, uM = x.M, uN = x.N;
         const GemmMaps& mp = x.prob ? maps2 : maps;
+        if (pass && x.step > ready_step) {
+          // (a pair's second shard came through the same comm stream after its first)
+          const int last_step = args.pass_pair ? min(2 * x.step + 1, args.pass_steps - 1) : x.step;
+          if (args.pass_ready) detail::wait_counter(args.pass_ready + last_step, 1u);
+          ready_step = x.step;
+        }
+        if (pass && it == it_beg + (pass_groups - 1) * pass_nt) griddep_launch();  // last shard landed
+        // pass launch: the step's shard buffer; DGRAD reads dY at its column block
+        const int first_step = args.pass_pair ? 2 * x.step : x.step;
         if (x.prob && args.dep_count && !args.dep_on_k) {
           // problem 1 reads problem 0's output rows of this row block: wait
           // until every warp of every problem-0 tile of the block has landed
@@ -629,10 +704,14 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
           if (rank == 0) mbar_expect_tx(&full_bar[stage], uint32_t(expect));
           const bool seg2 = args.kseg_kb > 0 && kb >= args.kseg_kb;
           const GemmMaps& mk = seg2 ? maps2 : mp;
-          const int k0 = (seg2 ? kb - args.kseg_kb : kb) * BK;
+          const int k0 = (seg2 ? kb - args.kseg_kb : x.seg_kb && kb >= x.seg_kb ? kb - x.seg_kb : kb) * BK;
+          // pass launch: this K block's shard buffer and dY column block
+          const bool pseg2 = x.seg_kb && kb >= x.seg_kb;
+          const CUtensorMap* b_map = (pass && (x.buf1 || pseg2)) ? &maps2.b : &mp.b;
+          const int a_koff = (pass && Cfg::EPI == EPI_DGRAD) ? args.pass_col[first_step + (pseg2 ? 1 : 0)] : 0;
           for (int op = 0; op < Cfg::NOPS; ++op) {
             const CUtensorMap* ma = op ? &mk.a_lo : &mk.a;
-            const CUtensorMap* mbm = op ? &mk.b_lo : &mk.b;
+            const CUtensorMap* mbm = op ? &mk.b_lo : (seg2 ? &mk.b : b_map);
             uint8_t* dA = sA + op * (Cfg::A_BYTES + Cfg::B_BYTES);
             uint8_t* dB = dA + Cfg::A_BYTES;
             if constexpr (Cfg::A_MN) {
@@ -641,7 +720,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
                 if (m0 + c * Cfg::ATOM_MN < uM)
                   load(dA + c * (BK * 128), ma, &full_bar[stage], m0 + c * Cfg::ATOM_MN, k0);
             } else {
-              if (m0 < uM) load(dA, ma, &full_bar[stage], k0, m0);
+              if (m0 < uM) load(dA, ma, &full_bar[stage], k0 + a_koff, m0);
             }
             if constexpr (Cfg::B_MN) {
 #pragma unroll
@@ -743,12 +822,31 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
     int acc = 0;
     uint32_t acc_phase = 0;
     int li = 0;
+    int e_step = 0;  // pass launch: step of the previous unit / whose shard is known landed
     for (int it = it_beg; it < it_end; it += it_step, ++li) {
       const bool tr = trace && li < TRACE_UNITS && ew == 0 && lane == 0;
       const Unit x_ = decode(it);
       const int t = x_.t, split = x_.split, mb = x_.mb, nb = x_.nb, uM = x_.M, uN = x_.N, uflags = x_.flags;
       const GemmMaps& mp = x_.prob ? maps2 : maps;
       const void* uaux = x_.prob ? args.aux2 : args.aux;
+      if (pass && x_.step != e_step) {
+        // Step boundary. DGRAD: this warp's bulk reductions of the previous
+        // step are complete before the same tiles' next step reduces into /
+        // reads the accumulator (fixed step order). FWD: the bias below lives
+        // in the arriving shard.
+        if (lane == 0) {
+          if (Cfg::EPI == EPI_DGRAD) {
+            bulk_wait0();
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+          }
+          if (Cfg::EPI == EPI_FWD && args.pass_ready) detail::wait_counter_nofence(args.pass_ready + x_.step, 1u);
+        }
+        __syncwarp();
+        if (Cfg::EPI == EPI_DGRAD) pending = false;
+        e_step = x_.step;
+      }
+      if (pass && Cfg::EPI == EPI_FWD) uaux = x_.buf1 ? args.aux2 : args.aux;
+      const int col_off = (pass && Cfg::EPI == EPI_FWD) ? args.pass_col[x_.step] : 0;
       const bool last = uflags & EF_LAST;
       const bool first = uflags & EF_FIRST;
       const bool pre_tma = Cfg::PRE_TMA && last && (uflags & EF_GELU_BWD);
@@ -816,6 +914,11 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
       if (tr) detail::trace_at(trace, 6 + 6 * li);
+      if (pass && args.pass_done && lane == 0) {
+        // the tile's MMAs are done: its operand loads (and, FWD, this warp's
+        // bias reads above) are complete — count in for the step's buffer
+        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(args.pass_done + x_.step) : "memory");
+      }
       // FWD problem 1 split over K: partial splits go to the fp32 workspace,
       // in split order; the last split folds the workspace into its output.
       const bool split2 = Cfg::EPI == EPI_FWD && x_.prob == 1 && splits2 > 1 && !x_.whole;
@@ -838,6 +941,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
           if (lane == 0) detail::wait_counter(args.g_flag, 1u);
           __syncwarp();
           g_ready = true;
+          if (ew == 0 && lane == 0) griddep_launch();  // G landed: admit the successor
         }
         if (split > 0 && !wpar) {
           // ordered split-K: wait until every warp of split-1 has landed its sums
@@ -984,11 +1088,13 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
               else
                 tma_reduce_add_2d(&mp.c1, stg0, nc, row0);  // workspace += partial s
             } else {
-              if (uflags & EF_STORE_PRE) tma_store_2d(&mp.c0, stg0, nc, row0);
-              if (uflags & EF_GELU) tma_store_2d(&mp.c1, stg1, nc, row0);
+              if (uflags & EF_STORE_PRE) tma_store_2d(&mp.c0, stg0, col_off + nc, row0);
+              if (uflags & EF_GELU) tma_store_2d(&mp.c1, stg1, col_off + nc, row0);
             }
           } else if constexpr (Cfg::EPI == EPI_DGRAD) {
-            if (last || first)
+            if (pass && last)
+              tma_store_2d(&maps2.c0, stg0, nc, row0);  // pass launch: dX map beside the accumulator's
+            else if (last || first)
               tma_store_2d(&mp.c0, stg0, nc, row0);  // dX (dtype) or first partial (fp32)
             else
               tma_reduce_add_2d(&mp.c0, stg0, nc, row0);  // acc += partial, in L2
@@ -1039,6 +1145,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
             if (lane == 0) detail::wait_counter_nofence(args.g_flag, 1u);
             __syncwarp();
             g_ready = true;
+            if (ew == 0 && lane == 0) griddep_launch();  // G landed: admit the successor
           }
           const float* part = x_.prob ? args.wpart2 : args.wpart;
           const int r_lo = (32 * split) / wsplits, r_hi = (32 * (split + 1)) / wsplits;
@@ -1107,6 +1214,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
             if (lane == 0) detail::wait_counter(args.g_flag, 1u);
             __syncwarp();
             g_ready = true;
+            if (ew == 0 && lane == 0) griddep_launch();  // G landed: admit the successor
           }
           if (last) {
             const float* part = x_.prob ? args.wpart2 : args.wpart;
@@ -1367,6 +1475,11 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
     __threadfence();
     if (atomicAdd(args.flag_reset_ctr, 1u) == gridDim.x - 1) {
       for (int i = 0; i < args.flag_reset_count; ++i) args.flag_reset[i] = 0u;
+      // pass launch: every count-in happened before this CTA's exit, and the
+      // comm stream's waits on them were satisfied before the pass's last
+      // arrival flag it raised (which every CTA passed)
+      if (args.pass_done)
+        for (int i = 0; i < args.pass_steps; ++i) args.pass_done[i] = 0u;
       *args.flag_reset_ctr = 0u;
       __threadfence();
     }

@@ -59,6 +59,23 @@ size_t wgrad_partial_floats(bool f32, size_t M, size_t I, size_t per);
 bool wgrad_fuses_bias(bool f32, size_t M, size_t I, size_t per, unsigned* split_flags, int force_bn);
 
 int gemm_fwd(bool f32, const StepFwd& p, cudaStream_t s);
+// Pass launches (bf16): every rotation step of one layer pass in one
+// persistent launch (GemmArgs::pass_steps). p.w = buffer 0's shard block,
+// w1 = buffer 1's; *done_target: the per-step count-in total on pa.done.
+struct PassArgs {
+  int steps;
+  unsigned buf_mask;         // bit s: step s reads buffer 1
+  const int* cols;           // [steps] column block offsets (elements)
+  const unsigned* ready;     // [steps] arrival flags (nullable)
+  unsigned* done;            // [steps] zeroed count-in counters (nullable)
+  unsigned* reset_ctr;       // zeroed CTA counter: the launch re-zeroes ready / done (nullable)
+  int pair = 0;              // DGRAD: units over step pairs (GemmArgs::pass_pair)
+};
+unsigned pass_done_target(bool dgrad, size_t M, size_t N, bool gelu, int force, int groups);
+int gemm_fwd_pass(const StepFwd& p, const void* w1, size_t y_cols, const PassArgs& pa, cudaStream_t s,
+                  unsigned* done_target);
+int gemm_dgrad_pass(const StepDgrad& p, const void* w1, size_t dy_cols, const PassArgs& pa, cudaStream_t s,
+                    unsigned* done_target);
 // Fused N = 1 MLP forward (ffn1 + GELU and ffn2 in one scheduled launch).
 struct FusedFwdPlan {
   std::vector<int> sched;  // [slots + 1 offsets][unit codes], uploaded by the caller
@@ -126,6 +143,14 @@ int fused_fwd_step(const void* x, size_t ldx, const void* w1_shard, void* pre, v
 
 // Caps the SMs the calling thread's following GEMM launches occupy (0 = all);
 // sm_budget() returns the effective count.
+// Load every device kernel of the library on the current device now. Under
+// CUDA's lazy module loading (the default), the first launch of a kernel
+// loads it, and a load may wait for the device's running work — which
+// deadlocks once a running grid spins on an arrival flag that work queued
+// behind the load would raise (pass launches, flag waits). Called once per
+// device by every Worker.
+void preload_device_kernels();
+
 void set_sm_budget(int sms);
 int sm_budget();
 // The calling thread's following GEMM launches load no operand before

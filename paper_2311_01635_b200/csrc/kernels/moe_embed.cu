@@ -290,4 +290,8 @@ int embed_scatter(bool f32, const void* dy, size_t ldy, size_t col0, const int64
   return post("embed_scatter_kernel");
 }
 
+const void* kernel_anchor_moe_embed() {
+  return reinterpret_cast<const void*>(&gather_rows_kernel<__nv_bfloat16>);
+}
+
 }  // namespace rtpb

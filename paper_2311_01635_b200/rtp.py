@@ -750,6 +750,54 @@ def wgrad_step(x, dy, col0, g_in, g_out, per, stream=None):
                               ws.numel(), s))
 
 
+def _pass_cols(cols):
+    arr = (C.c_size_t * len(cols))(*cols)
+    return arr
+
+
+def pass_done_target(which, M, I, per, steps, flags=0) -> int:
+    return int(lib.rtpb_pass_done_target(which, M, I, per, steps, flags))
+
+
+def fwd_pass(x, buf0, buf1, y, cols, per, act=None, store_pre=True, ready=None, done=None, reset_ctr=None,
+             exact_gelu=False, stream=None):
+    """rtpb_fwd_pass: step s of a layer's forward pass (shard in buffer s & 1,
+    output column block cols[s]) for every s, in one launch. Returns the
+    per-step count-in target on `done`."""
+    M, I = x.shape
+    flags = (_lib.EPI_STORE_PRE if store_pre else 0) | (_lib.EPI_GELU if act is not None else 0) | \
+        (64 if exact_gelu else 0)
+    ycols = (y if y is not None else act).shape[1]
+    mask = sum(1 << s for s in range(len(cols)) if s & 1)
+    tgt = C.c_uint(0)
+    s = (stream or torch.cuda.current_stream(x.device)).cuda_stream
+    check(lib.rtpb_fwd_pass(x.data_ptr(), x.stride(0), buf0.data_ptr(), buf1.data_ptr(),
+                            y.data_ptr() if y is not None else None, y.stride(0) if y is not None else 0,
+                            act.data_ptr() if act is not None else None, act.stride(0) if act is not None else 0,
+                            ycols, _pass_cols(cols), mask, len(cols), M, I, per, flags,
+                            None if ready is None else ready.data_ptr(), None if done is None else done.data_ptr(),
+                            C.byref(tgt), None if reset_ctr is None else reset_ctr.data_ptr(), s))
+    return tgt.value
+
+
+def dgrad_pass(dy, buf0, buf1, cols, acc, dx, I, per, pre=None, pair=False, ready=None, done=None, reset_ctr=None,
+               stream=None):
+    """rtpb_dgrad_pass: dX = sum_s dY[:, cols[s]:+per] . W_s^T over the pass's
+    steps (shard s in buffer s & 1) in one launch; pair: paired dX units."""
+    M = dy.shape[0]
+    flags = (_lib.EPI_GELU_BWD if pre is not None else 0) | (128 if pair else 0)
+    mask = sum(1 << s for s in range(len(cols)) if s & 1)
+    tgt = C.c_uint(0)
+    s = (stream or torch.cuda.current_stream(dy.device)).cuda_stream
+    check(lib.rtpb_dgrad_pass(dy.data_ptr(), dy.stride(0), dy.shape[1], buf0.data_ptr(), buf1.data_ptr(),
+                              _pass_cols(cols), mask, len(cols), acc.data_ptr(), acc.stride(0), dx.data_ptr(),
+                              dx.stride(0), None if pre is None else pre.data_ptr(), 0 if pre is None else pre.stride(0),
+                              M, I, per, flags, None if ready is None else ready.data_ptr(),
+                              None if done is None else done.data_ptr(), C.byref(tgt),
+                              None if reset_ctr is None else reset_ctr.data_ptr(), s))
+    return tgt.value
+
+
 def flyweight_init(dst, seed, stream_base, I, O, n, j, lo=-0.1, hi=0.1, stream=None):
     dt = F32 if dst.dtype == torch.float32 else BF16
     s = (stream or torch.cuda.current_stream(dst.device)).cuda_stream
