@@ -59,6 +59,12 @@ extern "C" {
                                  K = 2 per (paired dX); counters and the done target per pair */
 
 const char* rtpb_last_error(void);
+/* Load every kernel of the library on the current device now (groups do it
+ * for their devices). Under CUDA's lazy loading a kernel is loaded at its
+ * first launch, and a load may wait for running work: a caller that queues
+ * waits on a kernel's progress (stream memory operations on pass-launch
+ * counters) before that kernel's first launch must preload. */
+void rtpb_preload_kernels(void);
 const char* rtpb_version(void);
 /* Number of device kernels this library has launched (all threads). */
 uint64_t rtpb_launch_count(void);
@@ -127,7 +133,7 @@ int rtpb_dgrad_step2(int dtype, const void* dy, size_t ldy, size_t col0, const v
  * width of the Y / dY activations (N * per). Requires per % 32 == 0 and
  * steps <= 16. */
 /* The count-in total a pass launch of this geometry reaches on done[s]
- * (which = 0 fwd, 1 dgrad; steps and flags as the launch's), for
+ * (which = 0 fwd, 1 dgrad, 2 wgrad; steps and flags as the launch's), for
  * comm-stream waits enqueued before the launch. */
 unsigned rtpb_pass_done_target(int which, size_t M, size_t I, size_t per, size_t steps, int flags);
 int rtpb_fwd_pass(const void* x, size_t ldx, const void* buf0, const void* buf1, void* y, size_t ldy, void* act,
@@ -139,6 +145,27 @@ int rtpb_dgrad_pass(const void* dy, size_t ldy, size_t dy_cols, const void* buf0
                     size_t ldx, const void* pre, size_t ldpre, size_t M, size_t I, size_t per, int flags,
                     const unsigned* ready, unsigned* done, unsigned* done_target, unsigned* reset_ctr,
                     void* stream);
+
+/* dW of every step of a pass into the travelling gradient shard g = [W | b]
+ * (fp32) in ONE persistent launch:
+ *   step s: g[0 : I*per] += X^T . dY[:, col0[s] : +per]   (RTPB_EPI_FIRST in
+ *           flags: g known zero at step 0, stored instead of accumulated)
+ *           g[I*per : +per] += db[col0[s] : +per]          (db nullable: dY's
+ *           column sums, rtpb_colsum)
+ * The mainloops run ahead; each step's accumulation waits for ready[s] >= 1
+ * (s >= 1: the comm stream's flag that G(s) landed) and counts in on done[s]
+ * once its updates of g have landed (*done_target per step, also from
+ * rtpb_pass_done_target(2, ...)): the comm stream then sends g on. Workspace:
+ * rtpb_step_workspace_bytes(2, BF16, M, I, per), zeroed once. bf16 only. */
+int rtpb_wgrad_pass(const void* x, size_t ldx, const void* dy, size_t ldy, size_t dy_cols, float* g,
+                    const size_t* col0, size_t steps, size_t M, size_t I, size_t per, int flags, const float* db,
+                    const unsigned* ready, unsigned* done, unsigned* done_target, unsigned* reset_ctr,
+                    void* workspace, size_t workspace_bytes, void* stream);
+/* out[c] = sum over the M rows of dy[:, c] (bf16 in, fp32 out; fixed order,
+ * deterministic). Workspace: rtpb_colsum_workspace_bytes(M, cols), zeroed once. */
+size_t rtpb_colsum_workspace_bytes(size_t M, size_t cols);
+int rtpb_colsum(const void* dy, size_t ldy, size_t M, size_t cols, float* out, void* workspace, size_t workspace_bytes,
+                void* stream);
 
 /* dW step with the travelling-gradient accumulation fused into the epilogue
  * (layers_linear.cpp:61-63, kern::matmul_tn_acc + bias column sums):
@@ -281,6 +308,8 @@ int rtpb_group_synchronize(rtpb_group g);
  * compute, 1 comm, 2 aux) still have work pending. */
 int rtpb_debug_read_flags(rtpb_group g, size_t rank, size_t first, size_t count, unsigned* host_dst,
                           int* busy_streams);
+/* Debug hook: device address of entry `index` of a local worker's flag pool. */
+uint64_t rtpb_debug_flag_address(rtpb_group g, size_t rank, size_t index);
 /* Traffic log (ring.hpp:41-46): kind 0 rotation_cw, 1 rotation_ccw, 2 allgather. */
 size_t rtpb_group_traffic(rtpb_group g, int64_t* kinds, int64_t* w_elems, int64_t* g_elems, size_t cap);
 void rtpb_group_clear_traffic(rtpb_group g);

@@ -270,6 +270,8 @@ class WorkerGroup {
 
   size_t size() const { return n_; }
   TransportKind kind() const { return kind_; }
+  // A peer process shares a local worker's GPU (IPC transport on one device).
+  bool device_shared() const;
   const std::vector<size_t>& local_ranks() const { return local_; }
   bool is_local(size_t rank) const;
   Worker& worker(size_t rank);
@@ -308,6 +310,11 @@ class WorkerGroup {
 
   // compute stream <-> comm stream fencing per local worker.
   void comm_after_compute();
+  // While set, comm_after_compute() is a no-op: a pass launch that already
+  // fenced its comm streams (before its grids) runs the next layer's
+  // prefetch hook after queueing those grids, whose first shift must not
+  // wait for them.
+  void set_comm_fenced(bool on) { comm_fenced_ = on; }
   void compute_after_comm();
   void synchronize();
   // Orders each local worker's compute stream after its aux stream.
@@ -337,6 +344,7 @@ class WorkerGroup {
   std::vector<size_t> local_;
   std::vector<std::unique_ptr<Worker>> workers_;  // indexed by rank; null when remote
   std::unique_ptr<Transport> transport_;
+  bool comm_fenced_ = false;
   std::vector<CommRecord> traffic_;
   uint64_t tag_ = 0;
   size_t corrupt_rank_ = 0;
@@ -525,9 +533,10 @@ class RtpLinear : public RtpLayerBase {
   // CTA counters of the grids that clear each block (the pass's last reader)
   static constexpr size_t kFlagCtrFwd = 48, kFlagCtrW = 49, kFlagCtrG = 50;
   // Pass launches: per-step count-in counters of the forward / dX launch
-  static constexpr size_t kFlagDoneFwd = 64, kFlagDoneBwd = 80;
+  static constexpr size_t kFlagDoneFwd = 64, kFlagDoneBwd = 80, kFlagDoneW = 96;
   bool use_flags() const;
   bool pass_launch_ok() const;
+  bool backward_pass_pays(size_t rows) const;
   void flagged_exchange(Direction dir, std::span<void* const> send, std::span<void* const> recv, size_t bytes,
                         size_t flag);
 
@@ -538,6 +547,8 @@ class RtpLinear : public RtpLayerBase {
   std::vector<DView> x_cache_;          // per rank: caller-owned X kept for backward
   std::vector<DeviceBuffer> dx_acc_;    // per rank: fp32 cross-step dX accumulator
   std::vector<DeviceBuffer> workspace_; // per rank: step-kernel workspace
+  std::vector<DeviceBuffer> pass_ws_;   // per rank, pass launches: [dY column sums (out) | colsum workspace]
+  size_t pass_ws_rows_ = 0;
   size_t scratch_rows_ = 0;
   size_t cached_rows_ = 0;
   bool pre_fwd_ = false, pre_bwd_ = false;  // first shift already posted

@@ -30,10 +30,12 @@ _SIGS = {
     "rtpb_last_error": (C.c_char_p, []),
     "rtpb_version": (C.c_char_p, []),
     "rtpb_launch_count": (_u64, []),
+    "rtpb_preload_kernels": (None, []),
     "rtpb_debug_force_bn": (None, [_int]),
     "rtpb_debug_trace": (None, [_vp, _sz]),
     "rtpb_debug_skip_comm": (None, [_int]),
     "rtpb_debug_read_flags": (_int, [_vp, _sz, _sz, _sz, C.POINTER(C.c_uint), C.POINTER(_int)]),
+    "rtpb_debug_flag_address": (_u64, [_vp, _sz, _sz]),
     "rtpb_profile_enable": (None, [_int]),
     "rtpb_profile_read": (_sz, [C.POINTER(_int), C.POINTER(_dbl), C.POINTER(C.c_float), C.POINTER(C.c_float),
                                 C.POINTER(_int), _sz]),
@@ -51,6 +53,10 @@ _SIGS = {
                              _sz, _int, _vp, _vp, C.POINTER(C.c_uint), _vp, _vp]),
     "rtpb_dgrad_pass": (_int, [_vp, _sz, _sz, _vp, _vp, C.POINTER(_sz), C.c_uint, _sz, _vp, _sz, _vp, _sz, _vp, _sz,
                                _sz, _sz, _sz, _int, _vp, _vp, C.POINTER(C.c_uint), _vp, _vp]),
+    "rtpb_wgrad_pass": (_int, [_vp, _sz, _vp, _sz, _sz, _vp, C.POINTER(_sz), _sz, _sz, _sz, _sz, _int, _vp, _vp, _vp,
+                               C.POINTER(C.c_uint), _vp, _vp, _sz, _vp]),
+    "rtpb_colsum_workspace_bytes": (_sz, [_sz, _sz]),
+    "rtpb_colsum": (_int, [_vp, _sz, _sz, _sz, _vp, _vp, _sz, _vp]),
     "rtpb_wgrad_step": (_int, [_int, _vp, _sz, _vp, _sz, _sz, _vp, _vp, _sz, _sz, _sz, _vp, _sz, _vp]),
     "rtpb_gelu": (_int, [_int, _vp, _vp, _sz, _vp]),
     "rtpb_convert": (_int, [_vp, _int, _vp, _int, _sz, _vp]),

@@ -303,7 +303,10 @@ int check_pass(size_t M, size_t I, size_t per, const size_t* col0, size_t steps,
 }
 }  // namespace
 
+void rtpb_preload_kernels(void) { preload_device_kernels(); }
+
 unsigned rtpb_pass_done_target(int which, size_t M, size_t I, size_t per, size_t steps, int flags) {
+  if (which == 2) return wgrad_pass_done_target(M, I, per, g_force_bn);
   const int groups = int((which == 1 && (flags & RTPB_PASS_PAIR)) ? (steps + 1) / 2 : steps);
   return which == 1 ? pass_done_target(true, M, I, flags & RTPB_EPI_GELU_BWD, g_force_bn, groups)
                     : pass_done_target(false, M, per, false, g_force_bn, groups);
@@ -352,6 +355,39 @@ int rtpb_dgrad_pass(const void* dy, size_t ldy, size_t dy_cols, const void* buf0
   const PassArgs pa{int(steps), buf_mask, icol, ready, done, reset_ctr, pair};
   return timed(1, 2.0 * M * I * per * steps, s,
                [&] { return gemm_dgrad_pass(p, buf1, dy_cols, pa, s, done_target); });
+}
+
+size_t rtpb_colsum_workspace_bytes(size_t M, size_t cols) { return colsum_workspace_bytes(M, cols); }
+
+int rtpb_colsum(const void* dy, size_t ldy, size_t M, size_t cols, float* out, void* workspace, size_t workspace_bytes,
+                void* stream) {
+  if (!dy || !out) return set_error(RTPB_ERR_DIMENSION, "colsum: null buffer");
+  if (!workspace || workspace_bytes < colsum_workspace_bytes(M, cols))
+    return set_error(RTPB_ERR_DIMENSION, "colsum: workspace too small");
+  return colsum_bias_grad(false, dy, ldy, M, cols, nullptr, out, workspace, as_stream(stream));
+}
+
+int rtpb_wgrad_pass(const void* x, size_t ldx, const void* dy, size_t ldy, size_t dy_cols, float* g,
+                    const size_t* col0, size_t steps, size_t M, size_t I, size_t per, int flags, const float* db,
+                    const unsigned* ready, unsigned* done, unsigned* done_target, unsigned* reset_ctr,
+                    void* workspace, size_t workspace_bytes, void* stream) {
+  int icol[16];
+  int rc = check_pass(M, I, per, col0, steps, dy_cols, icol);
+  if (rc) return rc;
+  if (!g || !done_target) return set_error(RTPB_ERR_DIMENSION, "wgrad_pass: null gradient shard / target");
+  if (reinterpret_cast<uintptr_t>(g) & 15) return set_error(RTPB_ERR_CONFIG, "wgrad_pass: gradient shard not 16-byte aligned");
+  cudaStream_t s = as_stream(stream);
+  Carve c{static_cast<char*>(workspace), workspace ? workspace_bytes : 0};
+  c.take(colsum_workspace_bytes(M, per) / sizeof(float));
+  unsigned* sflags = reinterpret_cast<unsigned*>(c.take(split_flag_bytes(I, per) / sizeof(float)));
+  if (!c.ok) return set_error(RTPB_ERR_DIMENSION, "wgrad_pass: workspace too small");
+  StepWgrad p{};
+  p.x = x; p.ldx = ldx; p.dy = dy; p.ldy = ldy; p.g_in = g; p.g_out = g;
+  p.M = M; p.I = I; p.per = per; p.force_bn = g_force_bn; p.split_flags = sflags;
+  const PassArgs pa{int(steps), 0u, icol, ready, done, reset_ctr};
+  return timed(2, 2.0 * M * I * per * steps, s, [&] {
+    return gemm_wgrad_pass(p, dy_cols, (flags & RTPB_EPI_FIRST) != 0, db, pa, s, done_target);
+  });
 }
 
 int rtpb_dgrad_step2(int dtype, const void* dy, size_t ldy, size_t col0, const void* w_a, size_t col1,

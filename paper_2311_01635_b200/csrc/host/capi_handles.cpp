@@ -226,12 +226,13 @@ int rtpb_debug_read_flags(rtpb_group g, size_t rank, size_t first, size_t count,
     Worker& w = g->g->worker(rank);
     DeviceGuard dg(w.device);
     if (first + count > Worker::kFlagPool) throw DimensionError("debug_read_flags: out of range");
-    cudaStream_t s = nullptr;
-    cuda_check(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "debug stream");
+    // one private stream per process, made on the first call (call once
+    // before the work to watch starts); host_dst should be pinned memory
+    static cudaStream_t s = nullptr;
+    if (!s) cuda_check(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "debug stream");
     cuda_check(cudaMemcpyAsync(host_dst, w.flag(first), count * sizeof(unsigned), cudaMemcpyDeviceToHost, s),
                "debug read flags");
     cuda_check(cudaStreamSynchronize(s), "debug read flags");
-    cudaStreamDestroy(s);
     if (busy_streams) {
       int b = 0;
       if (cudaStreamQuery(w.compute) == cudaErrorNotReady) b |= 1;
@@ -240,6 +241,14 @@ int rtpb_debug_read_flags(rtpb_group g, size_t rank, size_t first, size_t count,
       *busy_streams = b;
     }
   });
+}
+
+uint64_t rtpb_debug_flag_address(rtpb_group g, size_t rank, size_t index) {
+  try {
+    return reinterpret_cast<uint64_t>(g->g->worker(rank).flag(index));
+  } catch (...) {
+    return 0;
+  }
 }
 
 int rtpb_group_synchronize(rtpb_group g) {

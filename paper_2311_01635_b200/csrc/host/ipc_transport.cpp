@@ -84,6 +84,7 @@ struct Mail {
 struct Shm {
   std::atomic<uint32_t> joined, left;
   std::atomic<uint32_t> flags_ready[kMaxRanks];
+  char bus_id[kMaxRanks][32];  // PCI bus id of each rank's device (written before flags_ready)
   cudaIpcMemHandle_t flags_handle[kMaxRanks];
   std::atomic<uint64_t> consumed[kMaxRanks];  // highest q+1 whose mailbox entry the reader took
   Mail mail[kMaxRanks][kSlots];
@@ -125,6 +126,7 @@ class IpcTransport final : public Transport {
     // flags: ready[2], done[2] (uint32, zeroed), exported to every peer
     flags_ = DeviceBuffer(w.device, 256, nullptr, MemCategory::Other, true);
     cuda_check(cudaIpcGetMemHandle(&shm_->flags_handle[rank_], flags_.data()), "cudaIpcGetMemHandle(flags)");
+    cuda_check(cudaDeviceGetPCIBusId(shm_->bus_id[rank_], 32, w.device), "cudaDeviceGetPCIBusId");
     shm_->flags_ready[rank_].store(1, std::memory_order_release);
     shm_->joined.fetch_add(1);
     peer_flags_.assign(n_, nullptr);
@@ -139,8 +141,11 @@ class IpcTransport final : public Transport {
                  "cudaIpcOpenMemHandle(flags)");
       peer_flags_[r] = static_cast<uint32_t*>(p);
       opened_.push_back(p);
+      if (std::strncmp(shm_->bus_id[r], shm_->bus_id[rank_], 32) == 0) shared_ = true;
     }
   }
+
+  bool device_shared() const override { return shared_; }
 
   ~IpcTransport() override {
     try {
@@ -285,6 +290,7 @@ class IpcTransport final : public Transport {
   uint32_t seq_[2] = {0, 0};
   uint64_t host_seq_ = 0;
   bool aborted_ = false;
+  bool shared_ = false;  // a peer process runs on the same GPU
 };
 
 }  // namespace

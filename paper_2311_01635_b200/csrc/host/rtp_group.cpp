@@ -593,7 +593,10 @@ void WorkerGroup::exchange(Direction dir, std::span<void* const> send, std::span
   transport_->shift(dir, send, recv, bytes);
 }
 
+bool WorkerGroup::device_shared() const { return transport_ && transport_->device_shared(); }
+
 void WorkerGroup::comm_after_compute() {
+  if (comm_fenced_) return;
   for (size_t r : local_) {
     Worker& w = *workers_[r];
     DeviceGuard dg(w.device);

@@ -13,6 +13,7 @@
 // the next dW waits only for it. In-place mode: the weight shift follows dX
 // (overlapping dW), the gradient shift follows dW (overlapping the next dX);
 // forward shifts are exposed, as the paper accepts.
+#include <array>
 #include <atomic>
 #include <cmath>
 #include <cstdio>
@@ -115,9 +116,38 @@ int nway_dx_sms(size_t rows, size_t I, size_t per) {
   return best < 0.9 * seq ? best_d : 0;
 }
 
+// Simulated distributed flags (RTPB_SIM_FLAGS=1, tests / measurement): the
+// arrival-flag and pass-launch paths on a Lockstep group whose workers share
+// one GPU. Every worker's grids are sized to its share of the SMs and launched
+// without programmatic (PDL) overlap, so all workers' spinning grids are
+// resident together and the protocol runs as on one GPU per worker.
+// RTPB_TRACE_HOST=1: the layers report their pass launches on stderr (debug)
+void host_trace(const std::string& label, const char* what) {
+  static const bool on = [] {
+    const char* e = std::getenv("RTPB_TRACE_HOST");
+    return e && std::atoi(e) != 0;
+  }();
+  if (on) std::fprintf(stderr, "[rtpb] %s: %s\n", label.c_str(), what);
+}
+
+bool sim_flags() {
+  static const bool on = [] {
+    const char* e = std::getenv("RTPB_SIM_FLAGS");
+    return e && std::atoi(e) != 0;
+  }();
+  return on;
+}
+
 class SmReserve {
  public:
   explicit SmReserve(const WorkerGroup& g) {
+    if (sim_flags() && g.kind() == TransportKind::Lockstep && g.local_ranks().size() > 1) {
+      set_sm_budget(0);
+      set_sm_budget(std::max(2, sm_budget() / int(g.local_ranks().size())) & ~1);
+      set_pdl_enabled(false);
+      active_ = true;
+      return;
+    }
     if (g.kind() != TransportKind::Nccl || g.size() < 2) return;
     int reserve = 8;
     if (const char* e = std::getenv("RTPB_NCCL_RESERVED_SMS")) reserve = std::max(0, std::atoi(e));
@@ -128,7 +158,10 @@ class SmReserve {
     active_ = true;
   }
   ~SmReserve() {
-    if (active_) set_sm_budget(0);
+    if (active_) {
+      set_sm_budget(0);
+      set_pdl_enabled(true);
+    }
   }
 
  private:
@@ -461,54 +494,76 @@ void RtpLinear::forward_impl(std::span<const DView> x, size_t rows, std::span<co
   std::vector<void*> wp(n, nullptr), sp(n, nullptr);
 
   if (pass_launch_ok()) {
-    // The whole pass as ONE persistent launch (rtpb_fwd_pass): the host does
-    // the N steps' bookkeeping up front, the comm stream lands shard s + 1
-    // in the buffer step s - 1 read once the launch has counted step s - 1
-    // out (cuStreamWaitValue32), and the launch's step s + 1 tiles wait for
-    // its arrival flag. Same tiles, same bits as the per-step launches.
-    const size_t r = local[0];
-    Worker& w = group_->worker(r);
-    void* buf[2] = {slots_[r].weight.data(), spares_[r].data()};
-    size_t cols[16];
+    // The whole pass as ONE persistent launch per worker (rtpb_fwd_pass): the
+    // host does the N steps' bookkeeping up front, each worker's comm stream
+    // lands shard s + 1 in the buffer step s - 1 read once the launch has
+    // counted step s - 1 out (cuStreamWaitValue32), and the launch's step
+    // s + 1 tiles wait for its arrival flag. Same bits as the per-step launches.
+    std::vector<std::array<void*, 2>> buf(n);
+    std::vector<std::array<size_t, 16>> cols(n);
+    for (size_t r : local) buf[r] = {slots_[r].weight.data(), spares_[r].data()};
     unsigned mask = 0;
     for (size_t s = 0; s < n; ++s) {
-      check_forward_position(r, s);
-      trace_[s * n + r] = int64_t(slots_[r].logical_id);
-      if (mode == Mode::Train) tapes_[r].record(slots_[r].logical_id, {});
-      cols[s] = slots_[r].logical_id * per_;
+      group_->each([&](size_t r) {
+        check_forward_position(r, s);
+        trace_[s * n + r] = int64_t(slots_[r].logical_id);
+        if (mode == Mode::Train) tapes_[r].record(slots_[r].logical_id, {});
+        cols[r][s] = slots_[r].logical_id * per_;
+      });
       if (s & 1) mask |= 1u << s;
       if (s + 1 < n) group_->advance_slots(slots_, Direction::Clockwise, PayloadKind::Weight, label_, shard_len_);
     }
     int flags = e.store_pre ? RTPB_EPI_STORE_PRE : 0;
-    void* act = nullptr;
-    size_t ld_act = 0;
-    if (!e.act.empty()) {
-      flags |= RTPB_EPI_GELU | (exact_gelu_ ? RTPB_EPI_EXACT_GELU : 0);
-      act = e.act[0].data;
-      ld_act = e.act[0].ld ? e.act[0].ld : out_;
-    }
+    if (!e.act.empty()) flags |= RTPB_EPI_GELU | (exact_gelu_ ? RTPB_EPI_EXACT_GELU : 0);
     const unsigned target = rtpb_pass_done_target(0, rows, in_, per_, n, flags);
-    unsigned* done = w.flag(flag_base_ + kFlagDoneFwd);
+    // Grids first, then the shifts: every stream memory wait is queued after
+    // the work it waits for (a wait ahead of it on a hardware queue shared
+    // by two streams would block it), and nothing between the launches and
+    // the shifts blocks the host (kernels preloaded, no allocation).
     group_->comm_after_compute();  // the spare's last reader (the previous pass) is done
+    host_trace(label_, "forward pass: launches");
+    group_->each([&](size_t r) {
+      Worker& w = group_->worker(r);
+      const size_t k = k_of[r];
+      void* act = e.act.empty() ? nullptr : e.act[k].data;
+      const size_t ld_act = e.act.empty() ? 0 : (e.act[k].ld ? e.act[k].ld : out_);
+      void* yp = e.store_pre ? y[k].data : nullptr;
+      const size_t ldy = e.store_pre && y[k].ld ? y[k].ld : out_;
+      unsigned tgt = 0;
+      check_status(rtpb_fwd_pass(x[k].data, x[k].ld ? x[k].ld : in_, buf[r][0], buf[r][1], yp, ldy, act, ld_act, out_,
+                                 cols[r].data(), mask, n, rows, in_, per_, flags, w.flag(flag_base_ + kFlagFwd),
+                                 w.flag(flag_base_ + kFlagDoneFwd), &tgt, w.flag(flag_base_ + kFlagCtrFwd),
+                                 w.compute));
+      if (tgt != target) throw StateError(label_ + ": pass launch count-in target mismatch");
+    });
+    host_trace(label_, "forward pass: shifts");
     for (size_t s = 0; s + 1 < n; ++s) {
       if (s == 0 && pre_fwd_) continue;  // posted under the previous layer's last step
-      if (s >= 1) stream_wait_geq_u32(w.comm, done + (s - 1), target);  // step s - 1's buffer is free
-      wp[r] = buf[s & 1];
-      sp[r] = buf[(s + 1) & 1];
-      flagged_exchange(Direction::Clockwise, wp, sp, slots_[r].weight.bytes(), kFlagFwd + s + 1);
+      for (size_t r : local) {
+        Worker& w = group_->worker(r);
+        DeviceGuard dg(w.device);
+        if (s >= 1) stream_wait_geq_u32(w.comm, w.flag(flag_base_ + kFlagDoneFwd + s - 1), target);
+        wp[r] = buf[r][s & 1];
+        sp[r] = buf[r][(s + 1) & 1];
+      }
+      flagged_exchange(Direction::Clockwise, wp, sp, slots_[local[0]].weight.bytes(), kFlagFwd + s + 1);
     }
     pre_fwd_ = false;
-    w.record(Ev::PassEnd, true);
-    if (e.before_last_step) e.before_last_step();  // its shifts queue behind this pass's
-    void* yp = e.store_pre ? y[0].data : nullptr;
-    const size_t ldy = e.store_pre && y[0].ld ? y[0].ld : out_;
-    unsigned tgt = 0;
-    check_status(rtpb_fwd_pass(x[0].data, x[0].ld ? x[0].ld : in_, buf[0], buf[1], yp, ldy, act, ld_act, out_, cols,
-                               mask, n, rows, in_, per_, flags, w.flag(flag_base_ + kFlagFwd), done, &tgt,
-                               w.flag(flag_base_ + kFlagCtrFwd), w.compute));
-    if (tgt != target) throw StateError(label_ + ": pass launch count-in target mismatch");
-    if ((n - 1) & 1) swap_data(slots_[r].weight, spares_[r]);  // the pass's n - 1 swaps
-    w.wait(Ev::PassEnd, false);  // join the pass's shifts (stream capture requires it)
+    for (size_t r : local) group_->worker(r).record(Ev::PassEnd, true);
+    if (e.before_last_step) {  // the next layer's first shift, queued behind this pass's (fenced above)
+      group_->set_comm_fenced(true);
+      try {
+        e.before_last_step();
+      } catch (...) {
+        group_->set_comm_fenced(false);
+        throw;
+      }
+      group_->set_comm_fenced(false);
+    }
+    for (size_t r : local) {
+      if ((n - 1) & 1) swap_data(slots_[r].weight, spares_[r]);  // the pass's n - 1 swaps
+      group_->worker(r).wait(Ev::PassEnd, false);  // join the pass's shifts (stream capture requires it)
+    }
     if (mode == Mode::Eval) rehome_after_eval();
     return;
   }
@@ -601,13 +656,15 @@ bool RtpLinear::use_flags() const {
     return e && std::atoi(e) != 0;
   }();
   const TransportKind k = group_->kind();
-  const bool one_per_gpu = k == TransportKind::Nccl || k == TransportKind::Ipc || k == TransportKind::Solo;
+  const bool one_per_gpu = k == TransportKind::Nccl || k == TransportKind::Ipc || k == TransportKind::Solo ||
+                           (k == TransportKind::Lockstep && sim_flags());
   return on && one_per_gpu && dtype_ == DType::BF16 && group_->size() > 1 && group_->size() <= 16;
 }
 
 // Pass launches (rtpb_fwd_pass / rtpb_dgrad_pass) ride on the arrival flags:
-// one worker per GPU, out of place (the shard alternates between the resident
-// buffer and the spare), column blocks in whole 32-column store boxes.
+// one worker per GPU (or the simulated form, RTPB_SIM_FLAGS), out of place
+// (the shard alternates between the resident buffer and the spare), column
+// blocks in whole 32-column store boxes, no other process on the GPU.
 // RTPB_NO_PASS=1 keeps one launch per step.
 bool RtpLinear::pass_launch_ok() const {
   static const bool off = [] {
@@ -615,8 +672,8 @@ bool RtpLinear::pass_launch_ok() const {
     return e && std::atoi(e) != 0;
   }();
   const size_t n = group_->size();
-  return !off && use_flags() && oop() && group_->local_ranks().size() == 1 && n >= 2 && n <= 16 && per_ % 32 == 0 &&
-         spares_.size() == n;
+  return !off && use_flags() && oop() && n >= 2 && n <= 16 && per_ % 32 == 0 &&
+         spares_.size() == n && !group_->device_shared();
 }
 
 void RtpLinear::flagged_exchange(Direction dir, std::span<void* const> send, std::span<void* const> recv,
@@ -778,7 +835,7 @@ void RtpLinear::backward_impl(std::span<const DView> dy, size_t rows, std::span<
     return;
   }
 
-  if (pass_launch_ok()) {
+  if (pass_launch_ok() && backward_pass_pays(rows)) {
     backward_pass(dy, rows, dx, e);
     return;
   }
@@ -946,45 +1003,59 @@ void RtpLinear::backward_impl(std::span<const DView> dy, size_t rows, std::span<
   require_home("end of backward");
 }
 
-// Backward as a dX pass launch beside per-step dW launches (one worker per
-// GPU, out of place, arrival flags). The dX of all N steps is ONE persistent
-// launch (rtpb_dgrad_pass) on the compute stream, holding its share of the
-// SMs; the dW of step s runs on the aux stream on the rest, its epilogue
-// waiting for the travelling gradient G (GemmArgs::g_flag). The comm stream
-// moves, per step, the next weight shard into the buffer the dX launch has
-// counted out (cuStreamWaitValue32 on its count-ins) and the gradient shard
-// once dW(s) is done (event from aux). No wait closes a cycle: dW depends only
-// on G shifts, each G shift only on the dW before it and earlier shifts (it
-// is posted ahead of the step's W shift), dX only on W shifts; the dX grid
-// holds its SM share, a dW grid the rest. Paired dX (paired_dx_) pairs the steps as
+// The backward pass launch splits the SMs between the dX launch and the dW
+// chain for the whole pass; per-step launches give each step's dX and dW the
+// whole machine one after the other. The split pays while a step's GEMMs are
+// a few microseconds (launch gaps and one-wave tails dominate: config (b));
+// for large steps (configs (c), (d): ~170 us each on all SMs) the per-step
+// schedule was measured faster. RTPB_PASS_BWD=0/1 forces either.
+bool RtpLinear::backward_pass_pays(size_t rows) const {
+  static const int force = [] {
+    const char* e = std::getenv("RTPB_PASS_BWD");
+    return e ? std::atoi(e) : -1;
+  }();
+  if (force >= 0) return force != 0;
+  return 2.0 * double(rows) * double(in_) * double(per_) < 40e9;
+}
+
+// Backward as two pass launches side by side (one worker per GPU, out of
+// place, arrival flags): the dX of all N steps in ONE persistent launch
+// (rtpb_dgrad_pass) on the compute stream, the dW of all N steps in one
+// (rtpb_wgrad_pass) on the aux stream, each on its share of the SMs. The dW
+// launch runs its mainloops ahead; each step's accumulation waits (in the
+// epilogue) for the travelling gradient G to land. The comm stream moves, per
+// step, the next weight shard into the buffer the dX launch has counted out
+// and G once the dW launch has counted its step in (cuStreamWaitValue32 on
+// the count-ins). No wait closes a cycle: the dX launch waits only for W
+// shifts, a W shift only for the dX launch's earlier steps, the dW launch for
+// G shifts, a G shift only for the dW launch's earlier steps and the shifts
+// posted ahead of it; both grids are resident (launched first, each within
+// its SM share) before any of their waits. Paired dX (paired_dx_) pairs the steps as
 // rtpb_dgrad_step2 does; otherwise the bits equal the per-step launches'.
 void RtpLinear::backward_pass(std::span<const DView> dy, size_t rows, std::span<const DView> dx, const BwdEpi& e) {
   const size_t n = group_->size();
-  const size_t r = group_->local_ranks()[0];
-  Worker& w = group_->worker(r);
-  void* buf[2] = {slots_[r].weight.data(), spares_[r].data()};
-  size_t cols[16];
+  const auto& local = group_->local_ranks();
+  std::vector<size_t> k_of(n, 0);
+  for (size_t k = 0; k < local.size(); ++k) k_of[local[k]] = k;
+  std::vector<std::array<void*, 2>> buf(n);
+  std::vector<std::array<size_t, 16>> cols(n);
+  for (size_t r : local) buf[r] = {slots_[r].weight.data(), spares_[r].data()};
   unsigned mask = 0;
   for (size_t s = 0; s < n; ++s) {
-    const size_t j = slots_[r].logical_id;
-    tapes_[r].replay(j);
-    check_backward_position(r, s);
-    trace_[n * n + s * n + r] = int64_t(j);
-    cols[s] = j * per_;
+    group_->each([&](size_t r) {
+      const size_t j = slots_[r].logical_id;
+      tapes_[r].replay(j);
+      check_backward_position(r, s);
+      trace_[n * n + s * n + r] = int64_t(j);
+      cols[r][s] = j * per_;
+    });
     if (s & 1) mask |= 1u << s;
     if (s + 1 < n)
       group_->advance_slots(slots_, Direction::CounterClockwise, PayloadKind::WeightAndGrad, label_, shard_len_);
   }
   const bool pair = paired_dx_;
   int flags = pair ? RTPB_PASS_PAIR : 0;
-  const void* pre = nullptr;
-  size_t ldpre = 0;
-  if (!e.pre.empty()) {
-    flags |= RTPB_EPI_GELU_BWD | (exact_gelu_ ? RTPB_EPI_EXACT_GELU : 0);
-    pre = e.pre[0].data;
-    ldpre = e.pre[0].ld ? e.pre[0].ld : in_;
-  }
-  unsigned* done = w.flag(flag_base_ + kFlagDoneBwd);
+  if (!e.pre.empty()) flags |= RTPB_EPI_GELU_BWD | (exact_gelu_ ? RTPB_EPI_EXACT_GELU : 0);
   auto group_of = [&](size_t s) { return pair ? s / 2 : s; };
   const int all = sm_budget();
   int d_sms = all / 2 & ~1;
@@ -992,73 +1063,119 @@ void RtpLinear::backward_pass(std::span<const DView> dy, size_t rows, std::span<
   set_sm_budget(d_sms);  // the tiles (and count-ins) of the dX launch depend on its SM share
   const unsigned target = rtpb_pass_done_target(1, rows, in_, per_, n, flags);
   set_sm_budget(all);
-  const size_t ldy = dy[0].ld ? dy[0].ld : out_, ldx = dx[0].ld ? dx[0].ld : in_;
-  const size_t ldxc = x_cache_[r].ld ? x_cache_[r].ld : in_;
 
-  group_->comm_after_compute();  // the spare's last reader is done
-  w.fork_aux();                  // dW reads dY and X, complete on compute
-  // The dX launch first, so its grid takes its SM share before the dW grids
-  // (which then fill the rest).
-  set_sm_budget(d_sms);
-  unsigned tgt = 0;
-  int rc = rtpb_dgrad_pass(dy[0].data, ldy, out_, buf[0], buf[1], cols, mask, n,
-                           static_cast<float*>(dx_acc_[r].data()), in_, dx[0].data, ldx, pre, ldpre, rows, in_, per_,
-                           flags, w.flag(flag_base_ + kFlagBwdW), done, &tgt, w.flag(flag_base_ + kFlagCtrW),
-                           w.compute);
-  set_sm_budget(all);
-  check_status(rc);
-  if (tgt != target) throw StateError(label_ + ": pass launch count-in target mismatch");
-  std::vector<void*> wp(n, nullptr), sp(n, nullptr), gp(n, nullptr);
-  unsigned dummy_flags = 0;
-  set_sm_budget(all - d_sms);
-  const bool g_flag = wgrad_fuses_bias(false, rows, in_, per_, &dummy_flags, 0);
-  float* g = static_cast<float*>(slots_[r].grad_acc.data());
-  try {
-    for (size_t s = 0; s < n; ++s) {
-      // dW(s): G_j += X^T dY_j on aux; G(s) arrives by flag (or stream event)
-      if (s > 0 && !g_flag) w.wait_on(Ev::GDone, w.aux);
-      set_launch_g_flag(g_flag && s > 0 ? w.flag(flag_base_ + kFlagBwdG + s) : nullptr);
-      if (s + 1 == n)  // the last dW clears the pass's G flags
-        set_launch_flag_reset(w.flag(flag_base_ + kFlagBwdG), int(kFlagCtrFwd - kFlagBwdG),
-                              w.flag(flag_base_ + kFlagCtrG));
-      const float* g_in = (grads_zero_pending_ && s == 0) ? nullptr : g;
-      rc = rtpb_wgrad_step(RTPB_BF16, x_cache_[r].data, ldxc, dy[0].data, ldy, cols[s], g_in, g, rows, in_, per_,
-                           workspace_[r].data(), workspace_[r].bytes(), w.aux);
-      set_launch_g_flag(nullptr);
-      set_launch_flag_reset(nullptr, 0, nullptr);
-      check_status(rc);
-      if (s + 1 == n) break;
-      w.record_on(Ev::AuxDone, w.aux);
-      // G shift once dW(s) is done: the gradient travels with its
-      // accumulation. It precedes the step's W shift on the comm stream, so
-      // the dW chain never waits for the dX launch (a dW grid spinning for G
-      // may hold the SMs the dX launch needs: G must not queue behind W).
-      w.wait_on(Ev::AuxDone, w.comm);
-      gp[r] = g;
-      flagged_exchange(Direction::CounterClockwise, gp, gp, slots_[r].grad_acc.bytes(), kFlagBwdG + s + 1);
-      w.record(Ev::GDone, true);
-      // W shift for step s + 1 into the buffer step s - 1 read
-      if (!(s == 0 && pre_bwd_)) {
-        if (s >= 1) stream_wait_geq_u32(w.comm, done + group_of(s - 1), target);
-        wp[r] = buf[s & 1];
-        sp[r] = buf[(s + 1) & 1];
-        flagged_exchange(Direction::CounterClockwise, wp, sp, slots_[r].weight.bytes(), kFlagBwdW + s + 1);
-      }
+  // [dY's column sums | their workspace] for the dW launch (before any launch:
+  // allocation synchronizes)
+  const size_t db_bytes = (out_ * sizeof(float) + 255) & ~size_t(255);
+  if (pass_ws_rows_ != rows) {
+    group_->synchronize();
+    pass_ws_.resize(n);
+    for (size_t r : local) {
+      Worker& w = group_->worker(r);
+      pass_ws_[r] = DeviceBuffer();
+      pass_ws_[r] = DeviceBuffer(w.device, db_bytes + rtpb_colsum_workspace_bytes(rows, out_), &w.ledger,
+                                 MemCategory::Other, true);
     }
+    pass_ws_rows_ = rows;
+  }
+  set_sm_budget(all - d_sms);
+  const unsigned target_w = rtpb_pass_done_target(2, rows, in_, per_, n, 0);
+  set_sm_budget(all);
+  // The in-place G shifts' staging chunk, sized now: growing it later would
+  // free device memory (a device-wide synchronisation) while the launches
+  // below wait for shifts not yet queued.
+  for (size_t r : local) {
+    size_t chunk = 0;
+    group_->worker(r).staging(slots_[r].grad_acc.bytes(), &chunk);
+  }
+
+  // Grids first, then the shifts (as the forward pass: every stream memory
+  // wait is queued after the work it waits for). The dX grid is launched
+  // first so it takes its SM share before the dW grid fills the rest.
+  group_->comm_after_compute();  // the spares' last readers are done
+  group_->each([&](size_t r) { group_->worker(r).fork_aux(); });  // dW reads dY and X, complete on compute
+  host_trace(label_, "backward pass: launches");
+  set_sm_budget(d_sms);
+  try {
+    group_->each([&](size_t r) {
+      Worker& w = group_->worker(r);
+      const size_t k = k_of[r];
+      const void* pre = e.pre.empty() ? nullptr : e.pre[k].data;
+      const size_t ldpre = e.pre.empty() ? 0 : (e.pre[k].ld ? e.pre[k].ld : in_);
+      unsigned tgt = 0;
+      check_status(rtpb_dgrad_pass(dy[k].data, dy[k].ld ? dy[k].ld : out_, out_, buf[r][0], buf[r][1], cols[r].data(),
+                                   mask, n, static_cast<float*>(dx_acc_[r].data()), in_, dx[k].data,
+                                   dx[k].ld ? dx[k].ld : in_, pre, ldpre, rows, in_, per_, flags,
+                                   w.flag(flag_base_ + kFlagBwdW), w.flag(flag_base_ + kFlagDoneBwd), &tgt,
+                                   w.flag(flag_base_ + kFlagCtrW), w.compute));
+      if (tgt != target) throw StateError(label_ + ": pass launch count-in target mismatch");
+    });
+    // dW of every step: one launch on aux (rtpb_wgrad_pass) after dY's
+    // column sums (the bias parts, added as each G arrives)
+    set_sm_budget(all - d_sms);
+    group_->each([&](size_t r) {
+      Worker& w = group_->worker(r);
+      const size_t k = k_of[r];
+      const size_t ldy = dy[k].ld ? dy[k].ld : out_;
+      float* db = static_cast<float*>(pass_ws_[r].data());
+      check_status(rtpb_colsum(dy[k].data, ldy, rows, out_, db, static_cast<char*>(pass_ws_[r].data()) + db_bytes,
+                               pass_ws_[r].bytes() - db_bytes, w.aux));
+      unsigned tgt = 0;
+      check_status(rtpb_wgrad_pass(x_cache_[r].data, x_cache_[r].ld ? x_cache_[r].ld : in_, dy[k].data, ldy, out_,
+                                   static_cast<float*>(slots_[r].grad_acc.data()), cols[r].data(), n, rows, in_, per_,
+                                   grads_zero_pending_ ? RTPB_EPI_FIRST : 0, db, w.flag(flag_base_ + kFlagBwdG),
+                                   w.flag(flag_base_ + kFlagDoneW), &tgt, w.flag(flag_base_ + kFlagCtrG),
+                                   workspace_[r].data(), workspace_[r].bytes(), w.aux));
+      if (tgt != target_w) throw StateError(label_ + ": dW pass launch count-in target mismatch");
+    });
   } catch (...) {
     set_sm_budget(all);
     throw;
   }
-  pre_bwd_ = false;
-  w.record(Ev::PassEnd, true);
   set_sm_budget(all);
-  // the next layer's prefetched shift queues behind this pass's (it waits for
-  // the dX launch too: its comm fence records the compute stream's tail)
-  if (e.before_last_step) e.before_last_step();
-  if ((n - 1) & 1) swap_data(slots_[r].weight, spares_[r]);  // the pass's n - 1 swaps
-  w.wait(Ev::PassEnd, false);
+  host_trace(label_, "backward pass: shifts");
+  std::vector<void*> wp(n, nullptr), sp(n, nullptr), gp(n, nullptr);
+  for (size_t s = 0; s + 1 < n; ++s) {
+    // W shift for step s + 1 into the buffer step s - 1 read
+    if (!(s == 0 && pre_bwd_)) {
+      for (size_t r : local) {
+        Worker& w = group_->worker(r);
+        DeviceGuard dg(w.device);
+        if (s >= 1) stream_wait_geq_u32(w.comm, w.flag(flag_base_ + kFlagDoneBwd + group_of(s - 1)), target);
+        wp[r] = buf[r][s & 1];
+        sp[r] = buf[r][(s + 1) & 1];
+      }
+      flagged_exchange(Direction::CounterClockwise, wp, sp, slots_[local[0]].weight.bytes(), kFlagBwdW + s + 1);
+    }
+    // G shift once dW(s) has landed: the gradient travels with its accumulation
+    for (size_t r : local) {
+      Worker& w = group_->worker(r);
+      DeviceGuard dg(w.device);
+      stream_wait_geq_u32(w.comm, w.flag(flag_base_ + kFlagDoneW + s), target_w);
+      gp[r] = slots_[r].grad_acc.data();
+    }
+    flagged_exchange(Direction::CounterClockwise, gp, gp, slots_[local[0]].grad_acc.bytes(), kFlagBwdG + s + 1);
+  }
+  pre_bwd_ = false;
+  for (size_t r : local) group_->worker(r).record(Ev::PassEnd, true);
+  if (e.before_last_step) {  // the next layer's first shift, queued behind this pass's (fenced above)
+    group_->set_comm_fenced(true);
+    try {
+      e.before_last_step();
+    } catch (...) {
+      group_->set_comm_fenced(false);
+      throw;
+    }
+    group_->set_comm_fenced(false);
+  }
+  set_sm_budget(all);
+  for (size_t r : local) {
+    if ((n - 1) & 1) swap_data(slots_[r].weight, spares_[r]);  // the pass's n - 1 swaps
+    group_->worker(r).wait(Ev::PassEnd, false);
+  }
+  host_trace(label_, "backward pass: queued");
   grads_zero_pending_ = false;
-  x_cache_[r] = {};
+  for (size_t r : local) x_cache_[r] = {};
   require_home("end of backward");
 }
 

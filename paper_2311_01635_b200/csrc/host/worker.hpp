@@ -103,6 +103,11 @@ class Transport {
   // The wait exceeded its deadline: abort the transport (unblocks the
   // streams) before the caller throws.
   virtual void abort() {}
+  // Another worker's process shares this worker's GPU (time-sliced between
+  // processes): a grid that spins on arrival flags for a whole pass can hold
+  // the GPU while the peer it waits for is switched out, so pass launches
+  // are off for such groups (RtpLinear::pass_launch_ok).
+  virtual bool device_shared() const { return false; }
 };
 
 std::unique_ptr<Transport> make_local_transport(WorkerGroup& g, bool concurrent);

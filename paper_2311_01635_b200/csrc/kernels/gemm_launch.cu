@@ -96,6 +96,7 @@ int device_sms() {
 // persistent grid and the tile / split-K choice are sized for them, so two
 // GEMMs issued on two streams run side by side instead of queueing.
 thread_local int t_sm_budget = 0;
+thread_local bool t_pdl = true;
 thread_local const unsigned* t_wait_flag = nullptr;
 thread_local const unsigned* t_g_flag = nullptr;
 thread_local unsigned* t_reset_flags = nullptr;
@@ -151,6 +152,25 @@ int encode_maps(const Op& a, const Op& b, const Out& c0, const Out* c1, GemmMaps
   return RTPB_OK;
 }
 
+// The kernel's dynamic shared memory opt-in, once per instantiation and
+// device. preload_device_kernels sets it for every instantiation up front:
+// setting a kernel's attribute may wait for running instances of it, which
+// deadlocks when those spin on work the caller has yet to launch.
+template <class Cfg>
+int set_smem_attr() {
+  static unsigned long long done_mask = 0;
+  static std::mutex mu;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard lk(mu);
+  if (dev >= 0 && dev < 64 && (done_mask >> dev & 1ull)) return RTPB_OK;
+  cudaError_t e = cudaFuncSetAttribute(rtp_gemm_kernel<Cfg>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       Cfg::SMEM_BYTES);
+  if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute(gemm)");
+  if (dev >= 0 && dev < 64) done_mask |= 1ull << dev;
+  return RTPB_OK;
+}
+
 // maps2: problem 1 of a scheduled launch (args.sched); slots_override: the
 // unit slots (CTA pairs / CTAs) the schedule was built for.
 template <class Cfg>
@@ -167,15 +187,10 @@ int launch_cfg(const Op& a, const Op& b, const Out& c0, const Out* c1, const Gem
     if ((rc = encode_maps<Cfg>(a2, b2, c0, c1, kseg_maps))) return rc;
     maps2 = &kseg_maps;
   }
-  static bool attr_set = false;  // per instantiation
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(rtp_gemm_kernel<Cfg>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         Cfg::SMEM_BYTES);
-    if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute(gemm)");
-    attr_set = true;
-  }
-  const int tiles = ((args.M + Cfg::TILE_M - 1) / Cfg::TILE_M) * ((args.N + Cfg::BN - 1) / Cfg::BN) *
-                    (args.k_splits > 1 ? args.k_splits : 1);  // work units
+  if ((rc = set_smem_attr<Cfg>())) return rc;  // (normally done by preload_device_kernels)
+  int tiles = ((args.M + Cfg::TILE_M - 1) / Cfg::TILE_M) * ((args.N + Cfg::BN - 1) / Cfg::BN) *
+              (args.k_splits > 1 ? args.k_splits : 1);  // work units
+  if (args.pass_steps && Cfg::EPI == EPI_FWD) tiles *= args.pass_steps;  // flat (step, tile) units
   // Persistent grid: one CTA pair (cluster of 2 on a TPC) per 256-row tile
   // slot, or one CTA per SM. Programmatic stream serialization lets the
   // kernel's prologue run under the previous kernel's tail (griddep_wait()
@@ -186,7 +201,7 @@ int launch_cfg(const Op& a, const Op& b, const Out& c0, const Out* c1, const Gem
   cfg.stream = stream;
   cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  attr[0].val.programmaticStreamSerializationAllowed = t_pdl ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   const int slots = slots_override > 0 ? slots_override : std::min(tiles, Cfg::PAIR ? sm_count() / 2 : sm_count());
@@ -285,6 +300,14 @@ int raster_mode(int M, int N, int K, int tile_m, int bn, bool f32, bool prefer_m
   return group;
 }
 
+bool wave_split_off() {  // A/B: RTPB_NO_WAVE_SPLIT=1
+  static const bool off = [] {
+    const char* e = std::getenv("RTPB_NO_WAVE_SPLIT");
+    return e && std::atoi(e) != 0;
+  }();
+  return off;
+}
+
 // Tile code (and, for dW, the split-K factor written into args.k_splits).
 template <int EPI>
 int pick_code(bool tf32, GemmArgs& args, int force) {
@@ -323,7 +346,7 @@ int pick_code(bool tf32, GemmArgs& args, int force) {
         }
       }
       if (s >= 2) args.k_splits = s;
-    } else if (!force && code == 1256 && tiles % pairs != 0) {
+    } else if (!force && code == 1256 && tiles % pairs != 0 && !wave_split_off()) {
       // Enough tiles for every pair, but the last wave is partial (config (d)
       // at N = 8: 128 pair tiles over 74 pairs = 1.73 waves run as 2). Split
       // K in S ordered parts so the S x tiles units quantise better; the
@@ -370,7 +393,8 @@ int launch_pass(const Op& a, const Op& b0, const Op& b1, const Out& c0, const Ou
   GemmMaps m2;
   int rc;
   if ((rc = encode_maps<Cfg>(a, b1, d0, d1, m2))) return rc;
-  const unsigned tiles = unsigned((args.M + Cfg::TILE_M - 1) / Cfg::TILE_M) * unsigned((args.N + Cfg::BN - 1) / Cfg::BN);
+  const unsigned tiles = unsigned((args.M + Cfg::TILE_M - 1) / Cfg::TILE_M) * unsigned((args.N + Cfg::BN - 1) / Cfg::BN) *
+                         unsigned(args.k_splits > 1 ? args.k_splits : 1);  // units per step
   *done_target = tiles * unsigned(Cfg::EPI_WARPS * (Cfg::PAIR ? 2 : 1));  // count-ins per step
   return launch_cfg<Cfg>(a, b0, c0, c1, args, s, &m2);
 }
@@ -379,6 +403,7 @@ template <int EPI>
 int dispatch_pass(int code, bool pre_tma, const Op& a, const Op& b0, const Op& b1, const Out& c0, const Out* c1,
                   const Out& d0, const Out* d1, const GemmArgs& args, cudaStream_t s, unsigned* target) {
   constexpr bool BMN = EPI != EPI_DGRAD;
+  constexpr bool AMN = EPI == EPI_WGRAD;
   if constexpr (EPI == EPI_DGRAD) {
     if (pre_tma) {
       if (code == 1256)
@@ -389,16 +414,16 @@ int dispatch_pass(int code, bool pre_tma, const Op& a, const Op& b0, const Op& b
     }
   }
   if (code == 1256)
-    return launch_pass<GemmCfg<EPI, 256, false, kEpiWarps, false, BMN, false, true>>(a, b0, b1, c0, c1, d0, d1, args,
+    return launch_pass<GemmCfg<EPI, 256, false, kEpiWarps, AMN, BMN, false, true>>(a, b0, b1, c0, c1, d0, d1, args,
                                                                                        s, target);
   if (code == 1128)
-    return launch_pass<GemmCfg<EPI, 128, false, kEpiWarps, false, BMN, false, true>>(a, b0, b1, c0, c1, d0, d1, args,
+    return launch_pass<GemmCfg<EPI, 128, false, kEpiWarps, AMN, BMN, false, true>>(a, b0, b1, c0, c1, d0, d1, args,
                                                                                        s, target);
   if (code == 256)
-    return launch_pass<GemmCfg<EPI, 256, false, kEpiWarps, false, BMN>>(a, b0, b1, c0, c1, d0, d1, args, s, target);
+    return launch_pass<GemmCfg<EPI, 256, false, kEpiWarps, AMN, BMN>>(a, b0, b1, c0, c1, d0, d1, args, s, target);
   if (code == 64)
-    return launch_pass<GemmCfg<EPI, 64, false, kEpiWarps, false, BMN>>(a, b0, b1, c0, c1, d0, d1, args, s, target);
-  return launch_pass<GemmCfg<EPI, 128, false, kEpiWarps, false, BMN>>(a, b0, b1, c0, c1, d0, d1, args, s, target);
+    return launch_pass<GemmCfg<EPI, 64, false, kEpiWarps, AMN, BMN>>(a, b0, b1, c0, c1, d0, d1, args, s, target);
+  return launch_pass<GemmCfg<EPI, 128, false, kEpiWarps, AMN, BMN>>(a, b0, b1, c0, c1, d0, d1, args, s, target);
 }
 
 void fill_pass_args(GemmArgs& g, const PassArgs& p) {
@@ -454,6 +479,42 @@ int gemm_fwd_pass(const StepFwd& p, const void* w1, size_t y_cols, const PassArg
   g.n_fastest = raster_mode(g.M, g.N, g.K, code > 1000 ? 256 : 128, bn, false, false);
   const Out* c1 = has_act ? &act : nullptr;
   return dispatch_pass<EPI_FWD>(code, false, a, b0, b1, c0, c1, c0, c1, g, s, done_target);
+}
+
+// dW of every step of a pass into the travelling gradient (GemmArgs
+// pass_steps, WGRAD): A = X, B = the whole dY read at the step's column block
+// (both MN-major), the per-step split-K of the per-step launches (ordered).
+int gemm_wgrad_pass(const StepWgrad& p, size_t dy_cols, bool g_zero, const float* db, const PassArgs& pa,
+                    cudaStream_t s, unsigned* done_target) {
+  Op a{p.x, nullptr, p.I, p.M, p.ldx};
+  Op b{p.dy, nullptr, dy_cols, p.M, p.ldy};
+  GemmArgs g{};
+  g.M = int(p.I);
+  g.N = int(p.per);
+  g.K = int(p.M);
+  g.flags = g_zero ? EF_FIRST : 0;
+  g.split_flags = p.split_flags;
+  fill_pass_args(g, pa);
+  g.pass_db = db;
+  g.pass_gbias = db ? p.g_out + p.I * p.per : nullptr;
+  const int code = pick_code<EPI_WGRAD>(false, g, p.force_bn);  // sets g.k_splits
+  const int bn = code % 1000;
+  g.n_fastest = raster_mode(g.M, g.N, g.K, code > 1000 ? 256 : 128, bn, false, true);
+  Out c0{p.g_out, true, p.per, p.I, p.per};
+  return dispatch_pass<EPI_WGRAD>(code, false, a, b, b, c0, nullptr, c0, nullptr, g, s, done_target);
+}
+
+unsigned wgrad_pass_done_target(size_t M, size_t I, size_t per, int force) {
+  GemmArgs g{};
+  g.M = int(I);
+  g.N = int(per);
+  g.K = int(M);
+  unsigned dummy = 0;
+  g.split_flags = &dummy;
+  const int code = pick_code<EPI_WGRAD>(false, g, force);
+  const size_t tm = code > 1000 ? 256 : 128, bn = code % 1000;
+  return unsigned(((I + tm - 1) / tm) * ((per + bn - 1) / bn) * size_t(g.k_splits > 1 ? g.k_splits : 1)) *
+         unsigned(kEpiWarps * (code > 1000 ? 2 : 1));
 }
 
 int gemm_dgrad_pass(const StepDgrad& p, const void* w1, size_t dy_cols, const PassArgs& pa, cudaStream_t s,
@@ -984,10 +1045,36 @@ void preload_device_kernels() {
     if (enum_fns(fns.data(), cnt, mod)) continue;
     for (CUfunction fn : fns) load_fn(fn);
   }
+  // every step-GEMM instantiation's shared-memory opt-in (launch_cfg)
+  set_smem_attr<GemmCfg<0, 128, false, 8, false, true, false, false>>();
+  set_smem_attr<GemmCfg<0, 128, false, 8, false, true, false, true>>();
+  set_smem_attr<GemmCfg<0, 128, true, 8, false, false, false, false>>();
+  set_smem_attr<GemmCfg<0, 256, false, 8, false, true, false, false>>();
+  set_smem_attr<GemmCfg<0, 256, false, 8, false, true, false, true>>();
+  set_smem_attr<GemmCfg<0, 64, false, 8, false, true, false, false>>();
+  set_smem_attr<GemmCfg<0, 64, true, 8, false, false, false, false>>();
+  set_smem_attr<GemmCfg<1, 128, false, 8, false, false, false, false>>();
+  set_smem_attr<GemmCfg<1, 128, false, 8, false, false, false, true>>();
+  set_smem_attr<GemmCfg<1, 128, false, 8, false, false, true, false>>();
+  set_smem_attr<GemmCfg<1, 128, true, 8, false, false, false, false>>();
+  set_smem_attr<GemmCfg<1, 128, true, 8, false, false, true, false>>();
+  set_smem_attr<GemmCfg<1, 256, false, 8, false, false, false, false>>();
+  set_smem_attr<GemmCfg<1, 256, false, 8, false, false, false, true>>();
+  set_smem_attr<GemmCfg<1, 256, false, 8, false, false, true, true>>();
+  set_smem_attr<GemmCfg<1, 64, false, 8, false, false, false, false>>();
+  set_smem_attr<GemmCfg<1, 64, true, 8, false, false, false, false>>();
+  set_smem_attr<GemmCfg<2, 128, false, 8, true, true, false, false>>();
+  set_smem_attr<GemmCfg<2, 128, false, 8, true, true, false, true>>();
+  set_smem_attr<GemmCfg<2, 128, true, 8, false, false, false, false>>();
+  set_smem_attr<GemmCfg<2, 256, false, 8, true, true, false, false>>();
+  set_smem_attr<GemmCfg<2, 256, false, 8, true, true, false, true>>();
+  set_smem_attr<GemmCfg<2, 64, false, 8, true, true, false, false>>();
+  set_smem_attr<GemmCfg<2, 64, true, 8, false, false, false, false>>();
   cudaGetLastError();  // a failed probe leaves no sticky state behind
 }
 
 void set_sm_budget(int sms) { t_sm_budget = sms; }
+void set_pdl_enabled(bool on) { t_pdl = on; }
 void set_launch_wait_flag(const unsigned* flag) { t_wait_flag = flag; }
 void set_launch_g_flag(const unsigned* flag) { t_g_flag = flag; }
 void set_launch_flag_reset(unsigned* flags, int count, unsigned* ctr) {

@@ -165,12 +165,25 @@ struct GemmArgs {
   // segments — buffer 0 at dY column pass_col[2g], then buffer 1 at
   // pass_col[2g + 1] — one accumulation over K = 2 per (paired dX: half the
   // fp32 accumulator passes).
+  //   WGRAD: G += X^T dY[:, pass_col[s] :] for every step into the ONE
+  //          travelling gradient buffer (units (tile, split) of step s per
+  //          slot, ordered split-K chain within a step). pass_ready[s] is G's
+  //          arrival flag: only the epilogue waits for it (the mainloops of
+  //          step s run while G(s) is in flight), and every epilogue warp
+  //          counts in on pass_done[s] once its reductions of the unit have
+  //          LANDED — the comm stream then sends G on. The bias part: the
+  //          warp of unit (tile 0, split 0) adds pass_db[pass_col[s] + c]
+  //          (dY's column sums, computed once for the pass) into
+  //          pass_gbias[c] after G(s) landed. EF_FIRST (args.flags): G is known
+  //          zero at step 0 (stores instead of reduce-adds).
   int pass_steps;
   int pass_pair;
   unsigned pass_buf;
   int pass_col[16];
   const unsigned* pass_ready;
   unsigned* pass_done;
+  const float* pass_db;
+  float* pass_gbias;
 };
 constexpr int TRACE_UNITS = 12;  // 2 + 6 * 12 slots + grid marker at TRACE_STRIDE - 1
 constexpr int TRACE_STRIDE = 80;
@@ -283,7 +296,11 @@ __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
 __device__ __forceinline__ void wait_counter_nofence(const unsigned* p, unsigned need) {
   const long long t0 = clock64();
   while (ld_acquire(p) < need)
-    if (clock64() - t0 > (20ll << 30)) __trap();
+    if (clock64() - t0 > (20ll << 30)) {
+      printf("rtpb: bounded wait expired: block %d thread %d counter %p holds %u, needs %u\n", int(blockIdx.x),
+             int(threadIdx.x), static_cast<const void*>(p), ld_acquire(p), need);
+      __trap();
+    }
 }
 __device__ __forceinline__ void wait_counter(const unsigned* p, unsigned need) {
   wait_counter_nofence(p, need);
@@ -478,11 +495,19 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
     it_end = __ldg(args.sched + unit + 1);
     it_step = 1;
   }
-  // pass launch: this slot's tiles per step; iteration it -> (step, tile)
+  // pass launch: iteration it -> (step, tile). DGRAD: this slot's tiles
+  // (t = unit + k * units) step by step, so a tile's steps run on one slot in
+  // order. FWD (no cross-step state): the flat (step, tile) sequence over all
+  // slots, so a pass with fewer tiles per step than slots still fills them.
   const bool pass = args.pass_steps > 0;
-  const int pass_nt = pass ? (num_tiles - unit + units - 1) / units : 0;
+  const bool pass_flat = pass && Cfg::EPI == EPI_FWD;
+  const int pass_nt = pass ? (num_units - unit + units - 1) / units : 0;  // per-step units (tile, split)
   const int pass_groups = args.pass_pair ? (args.pass_steps + 1) / 2 : args.pass_steps;
-  if (pass) {
+  if (pass_flat) {
+    it_beg = unit;
+    it_end = pass_groups * num_tiles;
+    it_step = units;
+  } else if (pass) {
     it_beg = 0;
     it_end = pass_groups * pass_nt;
     it_step = 1;
@@ -506,9 +531,10 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
     x.seg_kb = 0;
     if (pass) {
       x.prob = 0;
-      x.split = 0;
-      x.step = it / pass_nt;
-      x.t = unit + (it % pass_nt) * units;
+      x.step = pass_flat ? it / num_tiles : it / pass_nt;
+      const int u = pass_flat ? it % num_tiles : unit + (it % pass_nt) * units;
+      x.split = u / num_tiles;  // split-major within a step (WGRAD split-K)
+      x.t = u % num_tiles;
       x.buf1 = !args.pass_pair && ((args.pass_buf >> x.step) & 1u);
     } else if (args.sched) {
       const int e = __ldg(args.sched + it);
@@ -553,7 +579,9 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
     x.M = x.prob ? args.M2 : args.M;
     x.N = x.prob ? args.N2 : args.N;
     x.flags = x.prob ? args.flags2 : args.flags;
-    if (pass) {  // DGRAD: the pass's first step stores the accumulator, its last emits dX
+    if (pass && Cfg::EPI == EPI_WGRAD) {  // G known zero at step 0 only
+      if (x.step > 0) x.flags &= ~EF_FIRST;
+    } else if (pass) {  // DGRAD: the pass's first step stores the accumulator, its last emits dX
       x.flags &= ~(EF_FIRST | EF_LAST);
       if (x.step == 0) x.flags |= EF_FIRST;
       if (x.step == pass_groups - 1) x.flags |= EF_LAST;
@@ -661,17 +689,21 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
         return b * Cfg::NOPS;
       };
       int ready_step = 0;  // pass launch: steps whose shard is known to have landed
+      bool admitted = false;
       for (int it = it_beg; it < it_end; it += it_step) {
         const Unit x = decode(it);
         const int mb = x.mb, nb = x.nb, kb0 = x.kb0, kb1 = x.kb1, uM = x.M, uN = x.N;
         const GemmMaps& mp = x.prob ? maps2 : maps;
-        if (pass && x.step > ready_step) {
+        if (pass && Cfg::EPI != EPI_WGRAD && x.step > ready_step) {
           // (a pair's second shard came through the same comm stream after its first)
           const int last_step = args.pass_pair ? min(2 * x.step + 1, args.pass_steps - 1) : x.step;
           if (args.pass_ready) detail::wait_counter(args.pass_ready + last_step, 1u);
           ready_step = x.step;
         }
-        if (pass && it == it_beg + (pass_groups - 1) * pass_nt) griddep_launch();  // last shard landed
+        if (pass && Cfg::EPI != EPI_WGRAD && x.step == pass_groups - 1 && !admitted) {  // the last shard landed
+          griddep_launch();
+          admitted = true;
+        }
         // pass launch: the step's shard buffer; DGRAD reads dY at its column block
         const int first_step = args.pass_pair ? 2 * x.step : x.step;
         if (x.prob && args.dep_count && !args.dep_on_k) {
@@ -709,6 +741,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
           const bool pseg2 = x.seg_kb && kb >= x.seg_kb;
           const CUtensorMap* b_map = (pass && (x.buf1 || pseg2)) ? &maps2.b : &mp.b;
           const int a_koff = (pass && Cfg::EPI == EPI_DGRAD) ? args.pass_col[first_step + (pseg2 ? 1 : 0)] : 0;
+          const int b_noff = (pass && Cfg::EPI == EPI_WGRAD) ? args.pass_col[x.step] : 0;  // dY column block
           for (int op = 0; op < Cfg::NOPS; ++op) {
             const CUtensorMap* ma = op ? &mk.a_lo : &mk.a;
             const CUtensorMap* mbm = op ? &mk.b_lo : (seg2 ? &mk.b : b_map);
@@ -726,7 +759,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
 #pragma unroll
               for (int c = 0; c < Cfg::B_ROWS / Cfg::ATOM_MN; ++c)
                 if (n0 + c * Cfg::ATOM_MN < uN)
-                  load(dB + c * (BK * 128), mbm, &full_bar[stage], n0 + c * Cfg::ATOM_MN, k0);
+                  load(dB + c * (BK * 128), mbm, &full_bar[stage], n0 + c * Cfg::ATOM_MN + b_noff, k0);
             } else {
               if (n0 < uN) load(dB, mbm, &full_bar[stage], k0, n0);
             }
@@ -817,7 +850,8 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
     uint8_t* pre_w = pre_base + ew * Cfg::PRE_WARP;
     uint32_t pre_phase = 0;
     bool pending = false;
-    bool g_ready = args.g_flag == nullptr;  // WGRAD: travelling G landed
+    bool g_ready = pass || args.g_flag == nullptr;  // WGRAD: travelling G landed (pass: step 0's is resident)
+    const unsigned* gflag = pass ? nullptr : args.g_flag;  // WGRAD: the arrival flag of the unit's G
     unsigned wbuf = 0;  // dW staging buffer alternation
     int acc = 0;
     uint32_t acc_phase = 0;
@@ -833,7 +867,11 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
         // Step boundary. DGRAD: this warp's bulk reductions of the previous
         // step are complete before the same tiles' next step reduces into /
         // reads the accumulator (fixed step order). FWD: the bias below lives
-        // in the arriving shard.
+        // in the arriving shard. WGRAD: the step's G is a new arrival.
+        if (Cfg::EPI == EPI_WGRAD) {
+          gflag = args.pass_ready ? args.pass_ready + x_.step : nullptr;
+          g_ready = gflag == nullptr;
+        }
         if (lane == 0) {
           if (Cfg::EPI == EPI_DGRAD) {
             bulk_wait0();
@@ -914,7 +952,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
       if (tr) detail::trace_at(trace, 6 + 6 * li);
-      if (pass && args.pass_done && lane == 0) {
+      if (pass && Cfg::EPI != EPI_WGRAD && args.pass_done && lane == 0) {
         // the tile's MMAs are done: its operand loads (and, FWD, this warp's
         // bias reads above) are complete — count in for the step's buffer
         asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(args.pass_done + x_.step) : "memory");
@@ -938,10 +976,10 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
         // of it (first && split 0 overwrite it: G is known zero, no wait;
         // split partials go to the workspace: their folds wait below)
         if (!g_ready && !wpar && !(first && split == 0)) {
-          if (lane == 0) detail::wait_counter(args.g_flag, 1u);
+          if (lane == 0) detail::wait_counter(gflag, 1u);
           __syncwarp();
           g_ready = true;
-          if (ew == 0 && lane == 0) griddep_launch();  // G landed: admit the successor
+          if (ew == 0 && lane == 0 && (!pass || x_.step == pass_groups - 1)) griddep_launch();  // G landed: admit the successor
         }
         if (split > 0 && !wpar) {
           // ordered split-K: wait until every warp of split-1 has landed its sums
@@ -1142,10 +1180,10 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
           __syncwarp();
           pending = false;
           if (!g_ready && !first) {  // the fold reads G
-            if (lane == 0) detail::wait_counter_nofence(args.g_flag, 1u);
+            if (lane == 0) detail::wait_counter_nofence(gflag, 1u);
             __syncwarp();
             g_ready = true;
-            if (ew == 0 && lane == 0) griddep_launch();  // G landed: admit the successor
+            if (ew == 0 && lane == 0 && (!pass || x_.step == pass_groups - 1)) griddep_launch();  // G landed: admit the successor
           }
           const float* part = x_.prob ? args.wpart2 : args.wpart;
           const int r_lo = (32 * split) / wsplits, r_hi = (32 * (split + 1)) / wsplits;
@@ -1211,10 +1249,10 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
           last = __shfl_sync(0xffffffffu, last, 0);
           pending = false;
           if (last && !g_ready && !first) {  // the fold reduce-adds into G
-            if (lane == 0) detail::wait_counter(args.g_flag, 1u);
+            if (lane == 0) detail::wait_counter(gflag, 1u);
             __syncwarp();
             g_ready = true;
-            if (ew == 0 && lane == 0) griddep_launch();  // G landed: admit the successor
+            if (ew == 0 && lane == 0 && (!pass || x_.step == pass_groups - 1)) griddep_launch();  // G landed: admit the successor
           }
           if (last) {
             const float* part = x_.prob ? args.wpart2 : args.wpart;
@@ -1263,6 +1301,32 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
             __threadfence();
             const unsigned old = atomicAdd(wflags + t, 1u);
             if (old + 1 == unsigned(wsplits * wgroup)) wflags[t] = 0u;  // last arrival re-zeroes
+          }
+          __syncwarp();
+          pending = false;
+        }
+      }
+      if constexpr (Cfg::EPI == EPI_WGRAD) {
+        if (pass) {
+          if (t == 0 && split == 0 && ew == 0 && rank == 0 && args.pass_db) {
+            // G's bias part: + this step's dY column sums, once G(s) is here
+            if (!g_ready && !first) {
+              if (lane == 0) detail::wait_counter_nofence(gflag, 1u);
+              __syncwarp();
+              g_ready = true;
+            }
+            const float* db = args.pass_db + args.pass_col[x_.step];
+            for (int c = lane; c < uN; c += 32) args.pass_gbias[c] = (first ? 0.f : args.pass_gbias[c]) + db[c];
+            __syncwarp();
+          }
+          // count in once this warp's updates of G have landed: the comm
+          // stream sends G on when the step's count-ins are complete
+          if (lane == 0) {
+            bulk_wait0();
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+            __threadfence();
+            if (args.pass_done)
+              asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(args.pass_done + x_.step) : "memory");
           }
           __syncwarp();
           pending = false;

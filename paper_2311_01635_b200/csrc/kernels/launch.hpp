@@ -76,6 +76,12 @@ int gemm_fwd_pass(const StepFwd& p, const void* w1, size_t y_cols, const PassArg
                   unsigned* done_target);
 int gemm_dgrad_pass(const StepDgrad& p, const void* w1, size_t dy_cols, const PassArgs& pa, cudaStream_t s,
                     unsigned* done_target);
+// p.dy = the whole dY (dy_cols wide), p.g_out = the travelling gradient
+// shard [W | b]; db (nullable): dY's column sums (dy_cols floats), added to
+// the bias part at each step; g_zero: the shard is known zero at step 0.
+int gemm_wgrad_pass(const StepWgrad& p, size_t dy_cols, bool g_zero, const float* db, const PassArgs& pa,
+                    cudaStream_t s, unsigned* done_target);
+unsigned wgrad_pass_done_target(size_t M, size_t I, size_t per, int force);
 // Fused N = 1 MLP forward (ffn1 + GELU and ffn2 in one scheduled launch).
 struct FusedFwdPlan {
   std::vector<int> sched;  // [slots + 1 offsets][unit codes], uploaded by the caller
@@ -152,6 +158,8 @@ int fused_fwd_step(const void* x, size_t ldx, const void* w1_shard, void* pre, v
 void preload_device_kernels();
 
 void set_sm_budget(int sms);
+// Programmatic (PDL) launch overlap between consecutive step GEMMs (default on).
+void set_pdl_enabled(bool on);
 int sm_budget();
 // The calling thread's following GEMM launches load no operand before
 // *flag >= 1 (nullptr: no wait). See GemmArgs::ready_flag.

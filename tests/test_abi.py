@@ -154,3 +154,22 @@ def test_fused_n1_schedules_cover_the_config_shapes():
         for which in (0, 1):
             t = _lib.lib.rtpb_debug_fused_plan(M, h, f, which)
             assert t > 0 and math.isfinite(t), (M, h, f, which)
+
+
+def test_every_gemm_instantiation_is_preloaded():
+    """preload_device_kernels sets every step-GEMM instantiation's shared-memory
+    opt-in up front (a lazy attribute set may wait for running instances of the
+    kernel, which deadlocks against grids spinning on later launches): the
+    list in gemm_launch.cu must cover every instantiation the library holds."""
+    import os
+    from paper_2311_01635_b200 import _lib
+    out = subprocess.run(["nm", "-C", "-D", "--defined-only", _lib.LIB_PATH], capture_output=True, text=True).stdout
+    out += subprocess.run(["nm", "-C", _lib.LIB_PATH], capture_output=True, text=True).stdout
+    inst = set(re.findall(r"rtp_gemm_kernel<rtpb::GemmCfg<([^>]*)>", out))
+    src = open(os.path.join(os.path.dirname(HEADER), "..", "paper_2311_01635_b200", "csrc", "kernels",
+                            "gemm_launch.cu")).read()
+    listed = set(re.findall(r"set_smem_attr<GemmCfg<([^>]*)>>\(\);", src))
+    norm = lambda s: ",".join(p.strip() for p in s.replace("(int)", "").replace("(bool)", "").split(","))  # noqa: E731
+    assert inst, "no instantiations found"
+    missing = {norm(i) for i in inst} - {norm(i) for i in listed}
+    assert not missing, missing
