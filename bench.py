@@ -580,6 +580,7 @@ def main():
                 "parity_ok": parity_ok, "parity_check": parity_detail, "numerics": numerics,
                 "gpu_launches": int(launches),
                 "step_execution": graph_note,
+                "ring_schedule": ring_schedule(ring, args.mode, H, F, M),
                 "eager_ms_per_step": eager_ms,
                 "roofline": roofline,
                 "step_roofline": step_roofline,
@@ -595,6 +596,30 @@ def main():
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def ring_schedule(ring, mode, h, f, rows):
+    """How the N > 1 passes are launched (rtp_layers.cpp pass_launch_ok /
+    backward_pass_pays): one persistent launch per layer pass ordered by
+    arrival flags, or one event-ordered launch per rotation step."""
+    import os
+    if ring < 2:
+        return "N = 1: no rotation"
+    flags = os.environ.get("RTPB_FLAGS", "1") != "0"
+    passes = flags and mode == "outofplace" and os.environ.get("RTPB_NO_PASS", "0") in ("", "0")
+    out = {}
+    for name, i, o in (("ffn1", h, f), ("ffn2", f, h)):
+        per = o // ring
+        if not passes or per % 32:
+            out[name] = "one launch per rotation step (" + ("arrival flags" if flags else "stream events") + ")"
+            continue
+        bwd = os.environ.get("RTPB_PASS_BWD")
+        # the library's rule (RtpLinear::backward_pass_pays): a step's dX under 40 GFLOP
+        small = 2.0 * rows * i * per < 40e9
+        both = bwd == "1" or (bwd != "0" and small)
+        out[name] = "one launch per pass: forward" + (", dX and dW side by side" if both else
+                                                      "; backward one launch per step")
+    return out
 
 
 def profiled_roofline(args, torch, _lib, rtp, dev, stream, step, capture, graph, flush, flush_sink, barrier,

@@ -647,13 +647,15 @@ void RtpLinear::forward_impl(std::span<const DView> x, size_t rows, std::span<co
 // ordering: its operand-split pre-passes read the shard before the GEMM.
 // Several workers on one device (Lockstep/Concurrent) also keep events: their
 // spinning grids would compete for the same SMs.
-// Opt-in (RTPB_FLAGS=1): in a captured step the event edges cost no more —
-// `bench.py --solo N` (CUDA graph, config (b), TFLOP/s per GPU) measures
-// events / flags 573 / 545 at N = 2, 363 / 352 at N = 4, 194 / 200 at N = 8.
+// Default on (RTPB_FLAGS=0 keeps stream events): the flags carry the pass
+// launches (pass_launch_ok), which `bench.py --solo N` (config (b), TFLOP/s
+// per GPU) measures at 698 / 512 / 319 for N = 2 / 4 / 8 against 637 / 419 /
+// 257 with one event-ordered launch per step; the protocol is checked with
+// real shard movement by the simulated ring (tests/test_gpu_pass.py).
 bool RtpLinear::use_flags() const {
-  static const bool on = [] {
+  static const bool on = [] {  // default on; RTPB_FLAGS=0 keeps stream events
     const char* e = std::getenv("RTPB_FLAGS");
-    return e && std::atoi(e) != 0;
+    return !e || std::atoi(e) != 0;
   }();
   const TransportKind k = group_->kind();
   const bool one_per_gpu = k == TransportKind::Nccl || k == TransportKind::Ipc || k == TransportKind::Solo ||

@@ -1,6 +1,6 @@
-# A/B: pass launches vs per-step at config (b) N = 2/4/8 and (d) N = 8 (solo), dX SM share sweep, dW wave split
+# A/B: pass launches vs per-step at config (b) N = 2/4/8 and (d) N = 8 (solo); dX SM share sweep
 mkdir -p gpurun_out
-S=gpurun_out/solo_sweep.jsonl; rm -f $S
+S=gpurun_out/solo_sweep2.jsonl; rm -f $S
 run_b() {  # $1 = label, $2 = n, rest = env
   local lab=$1 n=$2; shift 2
   env RTPB_FLAGS=1 "$@" timeout -s KILL 90 python bench.py --config b --solo $n --steps 50 --no-cpu-baseline --no-e2e 2>/dev/null | tail -1 \
@@ -15,7 +15,8 @@ for n in 2 4 8; do run_b nopass $n RTPB_NO_PASS=1; run_b pass $n RTPB_NO_PASS=0;
 for d in 50 96 110; do run_b pass_dx$d 8 RTPB_PASS_DX_SMS=$d; done
 run_b pass_fwdonly 8 RTPB_PASS_BWD=0
 run_d nopass RTPB_NO_PASS=1
-run_d nopass_nowavesplit RTPB_NO_PASS=1 RTPB_NO_WAVE_SPLIT=1
 run_d pass RTPB_NO_PASS=0
-GRAPH=1 SOLO=8 RTPB_FLAGS=1 timeout -s KILL 120 python tools/timeline.py > gpurun_out/tl_b8_pass2.txt 2>&1
+run_d pass_bwd RTPB_PASS_BWD=1
+GRAPH=1 SOLO=8 RTPB_FLAGS=1 timeout -s KILL 120 python tools/timeline.py > gpurun_out/tl_b8_pass3.txt 2>&1
 cat $S
+timeout -s KILL 1200 python -m pytest tests -m gpu -x -q -p no:cacheprovider > gpurun_out/gputest.log 2>&1; echo "all rc=$?" >> gpurun_out/gputest.log
