@@ -536,6 +536,7 @@ class RtpLinear : public RtpLayerBase {
   static constexpr size_t kFlagDoneFwd = 64, kFlagDoneBwd = 80, kFlagDoneW = 96;
   bool use_flags() const;
   bool pass_launch_ok() const;
+  bool serial_profile() const;  // RTPB_SERIAL_PROFILE on a Solo group
   bool backward_pass_pays(size_t rows) const;
   void flagged_exchange(Direction dir, std::span<void* const> send, std::span<void* const> recv, size_t bytes,
                         size_t flag);

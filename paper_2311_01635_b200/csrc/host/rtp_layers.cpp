@@ -130,6 +130,17 @@ void host_trace(const std::string& label, const char* what) {
   if (on) std::fprintf(stderr, "[rtpb] %s: %s\n", label.c_str(), what);
 }
 
+// RTPB_SERIAL_PROFILE=1 on a Solo group (no peers, no bytes move): every
+// shift's arrival flag is raised before the pass launches instead of after
+// them, so a profiler that runs kernels one at a time (ncu) can replay them.
+bool serial_profile_env() {
+  static const bool on = [] {
+    const char* e = std::getenv("RTPB_SERIAL_PROFILE");
+    return e && std::atoi(e) != 0;
+  }();
+  return on;
+}
+
 bool sim_flags() {
   static const bool on = [] {
     const char* e = std::getenv("RTPB_SIM_FLAGS");
@@ -521,6 +532,22 @@ void RtpLinear::forward_impl(std::span<const DView> x, size_t rows, std::span<co
     // by two streams would block it), and nothing between the launches and
     // the shifts blocks the host (kernels preloaded, no allocation).
     group_->comm_after_compute();  // the spare's last reader (the previous pass) is done
+    const bool serial = serial_profile();
+    auto post_shifts = [&] {
+      host_trace(label_, "forward pass: shifts");
+      for (size_t s = 0; s + 1 < n; ++s) {
+        if (s == 0 && pre_fwd_) continue;  // posted under the previous layer's last step
+        for (size_t r : local) {
+          Worker& w = group_->worker(r);
+          DeviceGuard dg(w.device);
+          if (s >= 1 && !serial) stream_wait_geq_u32(w.comm, w.flag(flag_base_ + kFlagDoneFwd + s - 1), target);
+          wp[r] = buf[r][s & 1];
+          sp[r] = buf[r][(s + 1) & 1];
+        }
+        flagged_exchange(Direction::Clockwise, wp, sp, slots_[local[0]].weight.bytes(), kFlagFwd + s + 1);
+      }
+    };
+    if (serial) post_shifts();  // (profiling a Solo group: every flag up front)
     host_trace(label_, "forward pass: launches");
     group_->each([&](size_t r) {
       Worker& w = group_->worker(r);
@@ -536,18 +563,7 @@ void RtpLinear::forward_impl(std::span<const DView> x, size_t rows, std::span<co
                                  w.compute));
       if (tgt != target) throw StateError(label_ + ": pass launch count-in target mismatch");
     });
-    host_trace(label_, "forward pass: shifts");
-    for (size_t s = 0; s + 1 < n; ++s) {
-      if (s == 0 && pre_fwd_) continue;  // posted under the previous layer's last step
-      for (size_t r : local) {
-        Worker& w = group_->worker(r);
-        DeviceGuard dg(w.device);
-        if (s >= 1) stream_wait_geq_u32(w.comm, w.flag(flag_base_ + kFlagDoneFwd + s - 1), target);
-        wp[r] = buf[r][s & 1];
-        sp[r] = buf[r][(s + 1) & 1];
-      }
-      flagged_exchange(Direction::Clockwise, wp, sp, slots_[local[0]].weight.bytes(), kFlagFwd + s + 1);
-    }
+    if (!serial) post_shifts();
     pre_fwd_ = false;
     for (size_t r : local) group_->worker(r).record(Ev::PassEnd, true);
     if (e.before_last_step) {  // the next layer's first shift, queued behind this pass's (fenced above)
@@ -668,6 +684,10 @@ bool RtpLinear::use_flags() const {
 // (the shard alternates between the resident buffer and the spare), column
 // blocks in whole 32-column store boxes, no other process on the GPU.
 // RTPB_NO_PASS=1 keeps one launch per step.
+bool RtpLinear::serial_profile() const {
+  return serial_profile_env() && group_->kind() == TransportKind::Solo;
+}
+
 bool RtpLinear::pass_launch_ok() const {
   static const bool off = [] {
     const char* e = std::getenv("RTPB_NO_PASS");
@@ -1096,6 +1116,54 @@ void RtpLinear::backward_pass(std::span<const DView> dy, size_t rows, std::span<
   // first so it takes its SM share before the dW grid fills the rest.
   group_->comm_after_compute();  // the spares' last readers are done
   group_->each([&](size_t r) { group_->worker(r).fork_aux(); });  // dW reads dY and X, complete on compute
+  const bool serial = serial_profile();
+  // One comm stream carries both chains in order. W first: the dW chain
+  // waits for the dX launch's progress where a W shift waits for it; G first
+  // (RTPB_PASS_G_FIRST=1): the dX launch waits for the dW chain's. Measured
+  // (config (b) --solo N = 8 / 4 / 2): W first 319 / 512 / 695, G first
+  // 307 / 470 / 693 TFLOP/s per GPU, also with the dX launch given 96 SMs.
+  const bool g_first = [] {
+    const char* e = std::getenv("RTPB_PASS_G_FIRST");
+    return e && std::atoi(e) != 0;
+  }();
+  auto post_shifts = [&] {
+    host_trace(label_, "backward pass: shifts");
+    std::vector<void*> wp(n, nullptr), sp(n, nullptr), gp(n, nullptr);
+    for (size_t s = 0; s + 1 < n; ++s) {
+      auto shift_w = [&] {
+        // W shift for step s + 1 into the buffer step s - 1 read
+        if (!(s == 0 && pre_bwd_)) {
+          for (size_t r : local) {
+            Worker& w = group_->worker(r);
+            DeviceGuard dg(w.device);
+            if (s >= 1 && !serial)
+              stream_wait_geq_u32(w.comm, w.flag(flag_base_ + kFlagDoneBwd + group_of(s - 1)), target);
+            wp[r] = buf[r][s & 1];
+            sp[r] = buf[r][(s + 1) & 1];
+          }
+          flagged_exchange(Direction::CounterClockwise, wp, sp, slots_[local[0]].weight.bytes(), kFlagBwdW + s + 1);
+        }
+      };
+      auto shift_g = [&] {
+        // G shift once dW(s) has landed: the gradient travels with its accumulation
+        for (size_t r : local) {
+          Worker& w = group_->worker(r);
+          DeviceGuard dg(w.device);
+          if (!serial) stream_wait_geq_u32(w.comm, w.flag(flag_base_ + kFlagDoneW + s), target_w);
+          gp[r] = slots_[r].grad_acc.data();
+        }
+        flagged_exchange(Direction::CounterClockwise, gp, gp, slots_[local[0]].grad_acc.bytes(), kFlagBwdG + s + 1);
+      };
+      if (g_first) {
+        shift_g();
+        shift_w();
+      } else {
+        shift_w();
+        shift_g();
+      }
+    }
+  };
+  if (serial) post_shifts();  // (profiling a Solo group: every flag up front)
   host_trace(label_, "backward pass: launches");
   set_sm_budget(d_sms);
   try {
@@ -1135,29 +1203,7 @@ void RtpLinear::backward_pass(std::span<const DView> dy, size_t rows, std::span<
     throw;
   }
   set_sm_budget(all);
-  host_trace(label_, "backward pass: shifts");
-  std::vector<void*> wp(n, nullptr), sp(n, nullptr), gp(n, nullptr);
-  for (size_t s = 0; s + 1 < n; ++s) {
-    // W shift for step s + 1 into the buffer step s - 1 read
-    if (!(s == 0 && pre_bwd_)) {
-      for (size_t r : local) {
-        Worker& w = group_->worker(r);
-        DeviceGuard dg(w.device);
-        if (s >= 1) stream_wait_geq_u32(w.comm, w.flag(flag_base_ + kFlagDoneBwd + group_of(s - 1)), target);
-        wp[r] = buf[r][s & 1];
-        sp[r] = buf[r][(s + 1) & 1];
-      }
-      flagged_exchange(Direction::CounterClockwise, wp, sp, slots_[local[0]].weight.bytes(), kFlagBwdW + s + 1);
-    }
-    // G shift once dW(s) has landed: the gradient travels with its accumulation
-    for (size_t r : local) {
-      Worker& w = group_->worker(r);
-      DeviceGuard dg(w.device);
-      stream_wait_geq_u32(w.comm, w.flag(flag_base_ + kFlagDoneW + s), target_w);
-      gp[r] = slots_[r].grad_acc.data();
-    }
-    flagged_exchange(Direction::CounterClockwise, gp, gp, slots_[local[0]].grad_acc.bytes(), kFlagBwdG + s + 1);
-  }
+  if (!serial) post_shifts();
   pre_bwd_ = false;
   for (size_t r : local) group_->worker(r).record(Ev::PassEnd, true);
   if (e.before_last_step) {  // the next layer's first shift, queued behind this pass's (fenced above)

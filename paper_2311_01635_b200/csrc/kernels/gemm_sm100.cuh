@@ -971,6 +971,9 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
       const int wsplits = x_.prob ? splits2 : splits;
       const bool wpar = Cfg::EPI == EPI_WGRAD && args.wpar && wsplits > 1;
       const int wprows = x_.prob ? args.wpart_rows2 : args.wpart_rows;
+      // ordered split-K chain counter of the tile (a pass launch: one per
+      // step among the tile's 16 slots, so steps never share a chain)
+      unsigned* const chain_ctr = pass ? wflags + t * 16 + (x_.step & 15) : wflags + t;
       if constexpr (Cfg::EPI == EPI_WGRAD) {
         // the travelling G must have landed before this warp's first update
         // of it (first && split 0 overwrite it: G is known zero, no wait;
@@ -983,7 +986,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
         }
         if (split > 0 && !wpar) {
           // ordered split-K: wait until every warp of split-1 has landed its sums
-          if (lane == 0) detail::wait_counter(wflags + t, unsigned(split * wgroup));
+          if (lane == 0) detail::wait_counter(chain_ctr, unsigned(split * wgroup));
           __syncwarp();
         }
       }
@@ -1299,8 +1302,8 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
           if (lane == 0) {
             bulk_wait0();
             __threadfence();
-            const unsigned old = atomicAdd(wflags + t, 1u);
-            if (old + 1 == unsigned(wsplits * wgroup)) wflags[t] = 0u;  // last arrival re-zeroes
+            const unsigned old = atomicAdd(chain_ctr, 1u);
+            if (old + 1 == unsigned(wsplits * wgroup)) *chain_ctr = 0u;  // last arrival re-zeroes
           }
           __syncwarp();
           pending = false;
