@@ -302,7 +302,9 @@ class WorkerGroup {
   // Lower-level pieces used by the layers' overlap scheduler.
   // Raw ring shift of per-local-rank buffers: recv[dest(r)] <- send[r];
   // send == recv means in place (chunked through a staging buffer).
-  void exchange(Direction dir, std::span<void* const> send, std::span<void* const> recv, size_t bytes);
+  // channel: 0 weights (and per-step gradients), 1 a backward pass launch's travelling gradient
+  void exchange(Direction dir, std::span<void* const> send, std::span<void* const> recv, size_t bytes,
+                int channel = 0);
   // Advances slot bookkeeping for one hop (ids, offsets, tag, fault hook,
   // traffic record) exactly as the reference's install_payload does.
   void advance_slots(std::span<ShardSlot> slots, Direction dir, PayloadKind kind, std::string_view label,
@@ -539,7 +541,7 @@ class RtpLinear : public RtpLayerBase {
   bool serial_profile() const;  // RTPB_SERIAL_PROFILE on a Solo group
   bool backward_pass_pays(size_t rows) const;
   void flagged_exchange(Direction dir, std::span<void* const> send, std::span<void* const> recv, size_t bytes,
-                        size_t flag);
+                        size_t flag, int channel = 0);
 
   size_t in_ = 0, out_ = 0, per_ = 0;
   ShardLayout layout_;

@@ -180,27 +180,30 @@ class IpcTransport final : public Transport {
     DeviceGuard dg(w.device);
     cudaStream_t st = nullptr;
     if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) == cudaSuccess) {
-      cudaMemsetAsync(flags_.data(), 0xFF, 4 * sizeof(uint32_t), st);  // ready[2], done[2] := UINT32_MAX
+      cudaMemsetAsync(flags_.data(), 0xFF, 8 * sizeof(uint32_t), st);  // both channels' ready / done := UINT32_MAX
       cudaStreamSynchronize(st);
       cudaStreamDestroy(st);
     }
   }
 
-  void shift(Direction dir, std::span<void* const> send, std::span<void* const> recv, size_t bytes) override {
+  void shift(Direction dir, std::span<void* const> send, std::span<void* const> recv, size_t bytes,
+             int ch) override {
     if (n_ == 1 || bytes == 0) return;
     if (aborted_) throw ProtocolError("IPC transport: aborted after a ring shift timed out");
     Worker& w = g_.worker(rank_);
     DeviceGuard dg(w.device);
     const size_t dst = ring_dest(rank_, n_, dir), src = ring_src(rank_, n_, dir);
-    const int d = dir == Direction::Clockwise ? 0 : 1;
+    // flag words per channel: [ready cw, ready ccw, done cw, done ccw]
+    const int d = (dir == Direction::Clockwise ? 0 : 1) + 4 * ch;
     uint32_t* mine = static_cast<uint32_t*>(flags_.data());
+    cudaStream_t st = w.comm_of(ch);
     auto write = [&](uint32_t* addr, uint32_t v) {
-      cu_check(p_write(reinterpret_cast<CUstream>(w.comm), reinterpret_cast<CUdeviceptr>(addr), v,
+      cu_check(p_write(reinterpret_cast<CUstream>(st), reinterpret_cast<CUdeviceptr>(addr), v,
                        CU_STREAM_WRITE_VALUE_DEFAULT),
                "cuStreamWriteValue32");
     };
     auto wait = [&](uint32_t* addr, uint32_t v) {
-      cu_check(p_wait(reinterpret_cast<CUstream>(w.comm), reinterpret_cast<CUdeviceptr>(addr), v,
+      cu_check(p_wait(reinterpret_cast<CUstream>(st), reinterpret_cast<CUdeviceptr>(addr), v,
                       CU_STREAM_WAIT_VALUE_GEQ),
                "cuStreamWaitValue32");
     };
@@ -209,7 +212,7 @@ class IpcTransport final : public Transport {
       void* peer_recv = publish_and_fetch(recv[rank_], dst, src);
       write(peer_flags_[src] + 0 + d, q);  // a) my receive buffer is free
       wait(mine + 0 + d, q);               // b) the destination's is
-      cuda_check(cudaMemcpyAsync(peer_recv, send[rank_], bytes, cudaMemcpyDeviceToDevice, w.comm), "IPC push");
+      cuda_check(cudaMemcpyAsync(peer_recv, send[rank_], bytes, cudaMemcpyDeviceToDevice, st), "IPC push");
       write(peer_flags_[dst] + 2 + d, q);  // d) the destination's data landed
       wait(mine + 2 + d, q);               // e) mine has
       return;
@@ -224,10 +227,10 @@ class IpcTransport final : public Transport {
       const uint32_t q = ++seq_[d];
       write(peer_flags_[src] + 0 + d, q);  // my staging chunk is free
       wait(mine + 0 + d, q);
-      cuda_check(cudaMemcpyAsync(peer_stage, buf + off, c, cudaMemcpyDeviceToDevice, w.comm), "IPC push chunk");
+      cuda_check(cudaMemcpyAsync(peer_stage, buf + off, c, cudaMemcpyDeviceToDevice, st), "IPC push chunk");
       write(peer_flags_[dst] + 2 + d, q);
       wait(mine + 2 + d, q);               // the source's chunk is in my staging
-      cuda_check(cudaMemcpyAsync(buf + off, stage, c, cudaMemcpyDeviceToDevice, w.comm), "IPC stage copy");
+      cuda_check(cudaMemcpyAsync(buf + off, stage, c, cudaMemcpyDeviceToDevice, st), "IPC stage copy");
     }
   }
 
@@ -287,7 +290,7 @@ class IpcTransport final : public Transport {
   std::vector<uint32_t*> peer_flags_;
   std::vector<void*> opened_;
   std::map<std::pair<size_t, uint64_t>, void*> mapped_;  // (peer rank, buffer id) -> mapping
-  uint32_t seq_[2] = {0, 0};
+  uint32_t seq_[8] = {};  // per flag word (direction + 4 * channel)
   uint64_t host_seq_ = 0;
   bool aborted_ = false;
   bool shared_ = false;  // a peer process runs on the same GPU

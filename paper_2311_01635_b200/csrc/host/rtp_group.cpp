@@ -171,21 +171,28 @@ Worker::Worker(size_t r, int dev) : rank(r), device(dev) {
   DeviceGuard g(dev);
   cuda_check(cudaStreamCreateWithFlags(&compute, cudaStreamNonBlocking), "stream");
   cuda_check(cudaStreamCreateWithFlags(&comm, cudaStreamNonBlocking), "stream");
+  cuda_check(cudaStreamCreateWithFlags(&comm_g, cudaStreamNonBlocking), "stream");
   cuda_check(cudaStreamCreateWithFlags(&aux, cudaStreamNonBlocking), "stream");
   flags = DeviceBuffer(dev, kFlagPool * sizeof(unsigned), nullptr, MemCategory::Other, true);
   for (auto& e : ev) cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+  for (auto& c : ch_ev)
+    for (auto& e : c) cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
   preload_device_kernels();  // no lazy kernel load may wait behind a spinning grid (launch.hpp)
 }
 Worker::~Worker() {
   DeviceGuard g(device);
   cudaStreamSynchronize(compute);
   cudaStreamSynchronize(comm);
+  cudaStreamSynchronize(comm_g);
   cudaStreamSynchronize(aux);
   stage.reset();
   for (auto& e : ev) cudaEventDestroy(e);
+  for (auto& c : ch_ev)
+    for (auto& e : c) cudaEventDestroy(e);
   cudaStreamDestroy(aux);
   cudaStreamDestroy(compute);
   cudaStreamDestroy(comm);
+  cudaStreamDestroy(comm_g);
 }
 
 void stream_write_u32(cudaStream_t s, unsigned* addr, unsigned v) {
@@ -228,7 +235,8 @@ size_t inplace_chunk_bytes(size_t shard_bytes) {
 void* Worker::staging(size_t bytes, size_t* chunk) {
   const size_t want = inplace_chunk_bytes(bytes);
   if (stage.bytes() < want) {
-    cuda_check(cudaStreamSynchronize(comm), "stage sync");
+    cuda_check(cudaStreamSynchronize(comm), "stage sync");  // both channels use the chunk
+    cuda_check(cudaStreamSynchronize(comm_g), "stage sync");
     stage.reset();  // release before growing: one staging chunk is ever resident
     stage = DeviceBuffer(device, want, &ledger, MemCategory::CommBuffer, false);
   }
@@ -341,21 +349,32 @@ class LocalTransport final : public Transport {
     }
   }
 
-  void shift(Direction dir, std::span<void* const> send, std::span<void* const> recv, size_t bytes) override {
+  void shift(Direction dir, std::span<void* const> send, std::span<void* const> recv, size_t bytes,
+             int ch) override {
     const size_t n = g_.size();
     if (n == 1 || bytes == 0) return;
+    auto rec = [&](Worker& w, ChEv e, cudaStream_t st) {
+      cuda_check(cudaEventRecord(w.ch_event(ch, e), st), "record");
+    };
+    auto wait = [&](cudaStream_t st, const Worker& w, ChEv e) {
+      cuda_check(cudaStreamWaitEvent(st, w.ch_event(ch, e), 0), "wait");
+    };
     bool inplace = false;
     for (size_t r = 0; r < n; ++r) inplace = inplace || send[r] == recv[r];
     if (!inplace) {
-      for (size_t r = 0; r < n; ++r) g_.worker(r).record(Ev::Ready, true);
+      for (size_t r = 0; r < n; ++r) {
+        Worker& w = g_.worker(r);
+        DeviceGuard dg(w.device);
+        rec(w, ChEv::Ready, w.comm_of(ch));
+      }
       for (size_t r = 0; r < n; ++r) {
         Worker& dst = g_.worker(ring_dest(r, n, dir));
         Worker& src = g_.worker(r);
         DeviceGuard dg(dst.device);
-        cuda_check(cudaStreamWaitEvent(dst.comm, src.ev[int(Ev::Ready)], 0), "wait ready");
-        copy(recv[dst.rank], dst.device, send[r], src.device, bytes, dst.comm);
+        wait(dst.comm_of(ch), src, ChEv::Ready);
+        copy(recv[dst.rank], dst.device, send[r], src.device, bytes, dst.comm_of(ch));
       }
-      finish(dir);
+      finish(dir, ch);
       return;
     }
     // In place: chunked ring shift through each sender's staging chunk.
@@ -371,24 +390,25 @@ class LocalTransport final : public Transport {
       for (size_t r = 0; r < n; ++r) {
         Worker& w = g_.worker(r);
         DeviceGuard dg(w.device);
-        if (off) w.wait(Ev::Consumed, true);  // previous chunk left my staging buffer
-        copy(stage[r], w.device, static_cast<char*>(send[r]) + off, w.device, c, w.comm);
-        w.record(Ev::Staged, true);
+        if (off) wait(w.comm_of(ch), w, ChEv::Consumed);  // previous chunk left my staging buffer
+        copy(stage[r], w.device, static_cast<char*>(send[r]) + off, w.device, c, w.comm_of(ch));
+        rec(w, ChEv::Staged, w.comm_of(ch));
       }
       for (size_t r = 0; r < n; ++r) {
         Worker& src = g_.worker(r);
         Worker& dst = g_.worker(ring_dest(r, n, dir));
         DeviceGuard dg(dst.device);
-        cuda_check(cudaStreamWaitEvent(dst.comm, src.ev[int(Ev::Staged)], 0), "wait staged");
-        copy(static_cast<char*>(recv[dst.rank]) + off, dst.device, stage[r], src.device, c, dst.comm);
-        cuda_check(cudaEventRecord(src.ev[int(Ev::Consumed)], dst.comm), "record consumed");
+        wait(dst.comm_of(ch), src, ChEv::Staged);
+        copy(static_cast<char*>(recv[dst.rank]) + off, dst.device, stage[r], src.device, c, dst.comm_of(ch));
+        rec(src, ChEv::Consumed, dst.comm_of(ch));
       }
     }
     for (size_t r = 0; r < n; ++r) {
-      DeviceGuard dg(g_.worker(r).device);
-      g_.worker(r).wait(Ev::Consumed, true);
+      Worker& w = g_.worker(r);
+      DeviceGuard dg(w.device);
+      wait(w.comm_of(ch), w, ChEv::Consumed);
     }
-    finish(dir);
+    finish(dir, ch);
   }
 
  private:
@@ -400,14 +420,18 @@ class LocalTransport final : public Transport {
   }
   // Each rank's comm stream must also be ordered after the copy that read
   // its send buffer (issued on its destination's comm stream).
-  void finish(Direction dir) {
+  void finish(Direction dir, int ch) {
     const size_t n = g_.size();
-    for (size_t r = 0; r < n; ++r) g_.worker(r).record(Ev::Comm, true);
+    for (size_t r = 0; r < n; ++r) {
+      Worker& w = g_.worker(r);
+      DeviceGuard dg(w.device);
+      cuda_check(cudaEventRecord(w.ch_event(ch, ChEv::Comm), w.comm_of(ch)), "record");
+    }
     for (size_t r = 0; r < n; ++r) {
       Worker& w = g_.worker(r);
       Worker& reader = g_.worker(ring_dest(r, n, dir));
       DeviceGuard dg(w.device);
-      cuda_check(cudaStreamWaitEvent(w.comm, reader.ev[int(Ev::Comm)], 0), "wait reader");
+      cuda_check(cudaStreamWaitEvent(w.comm_of(ch), reader.ch_event(ch, ChEv::Comm), 0), "wait reader");
     }
   }
 
@@ -425,6 +449,7 @@ class NcclTransport final : public Transport {
     nccl_check(ncclCommInitRank(&comm_, int(g.size()), uid, int(rank)), "ncclCommInitRank");
   }
   ~NcclTransport() override {
+    if (comm2_) ncclCommDestroy(comm2_);
     if (comm_) ncclCommDestroy(comm_);  // an aborted communicator is already gone
   }
   bool polled() const override { return true; }
@@ -432,6 +457,8 @@ class NcclTransport final : public Transport {
     ncclResult_t st = ncclSuccess;
     if (!comm_ || aborted_) return;
     nccl_check(ncclCommGetAsyncError(comm_, &st), "ncclCommGetAsyncError");
+    if ((st == ncclSuccess || st == ncclInProgress) && comm2_)
+      nccl_check(ncclCommGetAsyncError(comm2_, &st), "ncclCommGetAsyncError");
     if (st != ncclSuccess && st != ncclInProgress) {
       abort();
       throw NcclError(std::string("ring shift failed asynchronously: ") + ncclGetErrorString(st));
@@ -439,8 +466,9 @@ class NcclTransport final : public Transport {
   }
   void abort() override {
     if (comm_ && !aborted_) {
+      if (comm2_) ncclCommAbort(comm2_);
       ncclCommAbort(comm_);
-      comm_ = nullptr;
+      comm_ = comm2_ = nullptr;
       aborted_ = true;
     }
   }
@@ -448,16 +476,27 @@ class NcclTransport final : public Transport {
     DeviceGuard dg(g_.worker(rank_).device);
     fn(rank_);
   }
-  void shift(Direction dir, std::span<void* const> send, std::span<void* const> recv, size_t bytes) override {
+  void shift(Direction dir, std::span<void* const> send, std::span<void* const> recv, size_t bytes,
+             int ch) override {
     const size_t n = g_.size();
     if (n == 1 || bytes == 0) return;
+    if (aborted_) throw NcclError("ring shift on an aborted communicator");
     Worker& w = g_.worker(rank_);
     DeviceGuard dg(w.device);
+    if (ch && !comm2_) {
+      // channel 1 (the travelling gradient of a backward pass launch) gets
+      // its own communicator: two streams must not issue on one. Collective
+      // over the ring; every rank reaches its first channel-1 shift in the
+      // same order.
+      nccl_check(ncclCommSplit(comm_, 0, int(rank_), &comm2_, nullptr), "ncclCommSplit");
+    }
+    ncclComm_t comm = ch ? comm2_ : comm_;
+    cudaStream_t st = w.comm_of(ch);
     const int dst = int(ring_dest(rank_, n, dir)), src = int(ring_src(rank_, n, dir));
     if (send[rank_] != recv[rank_]) {
       nccl_check(ncclGroupStart(), "ncclGroupStart");
-      nccl_check(ncclSend(send[rank_], bytes, ncclUint8, dst, comm_, w.comm), "ncclSend");
-      nccl_check(ncclRecv(recv[rank_], bytes, ncclUint8, src, comm_, w.comm), "ncclRecv");
+      nccl_check(ncclSend(send[rank_], bytes, ncclUint8, dst, comm, st), "ncclSend");
+      nccl_check(ncclRecv(recv[rank_], bytes, ncclUint8, src, comm, st), "ncclRecv");
       nccl_check(ncclGroupEnd(), "ncclGroupEnd");
       return;
     }
@@ -467,10 +506,10 @@ class NcclTransport final : public Transport {
     for (size_t off = 0; off < bytes; off += chunk) {
       const size_t c = std::min(chunk, bytes - off);
       nccl_check(ncclGroupStart(), "ncclGroupStart");
-      nccl_check(ncclSend(buf + off, c, ncclUint8, dst, comm_, w.comm), "ncclSend");
-      nccl_check(ncclRecv(stage, c, ncclUint8, src, comm_, w.comm), "ncclRecv");
+      nccl_check(ncclSend(buf + off, c, ncclUint8, dst, comm, st), "ncclSend");
+      nccl_check(ncclRecv(stage, c, ncclUint8, src, comm, st), "ncclRecv");
       nccl_check(ncclGroupEnd(), "ncclGroupEnd");
-      cuda_check(cudaMemcpyAsync(buf + off, stage, c, cudaMemcpyDeviceToDevice, w.comm), "stage copy");
+      cuda_check(cudaMemcpyAsync(buf + off, stage, c, cudaMemcpyDeviceToDevice, st), "stage copy");
     }
   }
 
@@ -478,6 +517,7 @@ class NcclTransport final : public Transport {
   WorkerGroup& g_;
   size_t rank_;
   ncclComm_t comm_ = nullptr;
+  ncclComm_t comm2_ = nullptr;  // channel 1, split from comm_ on first use
   bool aborted_ = false;
 };
 
@@ -494,7 +534,7 @@ class SoloTransport final : public Transport {
     DeviceGuard dg(g_.worker(rank_).device);
     fn(rank_);
   }
-  void shift(Direction, std::span<void* const>, std::span<void* const>, size_t) override {}
+  void shift(Direction, std::span<void* const>, std::span<void* const>, size_t, int) override {}
 
  private:
   WorkerGroup& g_;
@@ -585,12 +625,13 @@ MemoryLedger* WorkerGroup::bound_ledger(size_t rank) const { return bound_.empty
 
 std::atomic<int> g_skip_comm{0};
 
-void WorkerGroup::exchange(Direction dir, std::span<void* const> send, std::span<void* const> recv, size_t bytes) {
+void WorkerGroup::exchange(Direction dir, std::span<void* const> send, std::span<void* const> recv, size_t bytes,
+                           int channel) {
   if (send.size() != n_ || recv.size() != n_) throw ConfigError("exchange: buffer arrays must have n entries");
   // rtpb_debug_skip_comm: the schedule, events and bookkeeping stay; only the
   // bytes do not move (compute-only baseline for the exposed-comm measurement).
   if (g_skip_comm.load(std::memory_order_relaxed)) return;
-  transport_->shift(dir, send, recv, bytes);
+  transport_->shift(dir, send, recv, bytes, channel);
 }
 
 bool WorkerGroup::device_shared() const { return transport_ && transport_->device_shared(); }
@@ -602,6 +643,8 @@ void WorkerGroup::comm_after_compute() {
     DeviceGuard dg(w.device);
     w.record(Ev::Compute, false);
     w.wait(Ev::Compute, true);
+    // channel 1 too: its stream joins a stream capture through this edge
+    cuda_check(cudaStreamWaitEvent(w.comm_g, w.ev[int(Ev::Compute)], 0), "wait");
   }
 }
 
@@ -635,6 +678,7 @@ void WorkerGroup::synchronize() {
       cuda_check(cudaStreamSynchronize(w.aux), "sync aux");
       cuda_check(cudaStreamSynchronize(w.compute), "sync compute");
       cuda_check(cudaStreamSynchronize(w.comm), "sync comm");
+      cuda_check(cudaStreamSynchronize(w.comm_g), "sync comm (channel 1)");
     }
     return;
   }
@@ -646,7 +690,7 @@ void WorkerGroup::synchronize() {
   for (size_t r : local_) {
     Worker& w = *workers_[r];
     DeviceGuard dg(w.device);
-    for (cudaStream_t s : {w.aux, w.compute, w.comm}) {
+    for (cudaStream_t s : {w.aux, w.compute, w.comm, w.comm_g}) {
       for (;;) {
         const cudaError_t q = cudaStreamQuery(s);
         if (q == cudaSuccess) break;

@@ -665,7 +665,7 @@ void RtpLinear::forward_impl(std::span<const DView> x, size_t rows, std::span<co
 // spinning grids would compete for the same SMs.
 // Default on (RTPB_FLAGS=0 keeps stream events): the flags carry the pass
 // launches (pass_launch_ok), which `bench.py --solo N` (config (b), TFLOP/s
-// per GPU) measures at 698 / 512 / 319 for N = 2 / 4 / 8 against 637 / 419 /
+// per GPU) measures at 693 / 577 / 352 for N = 2 / 4 / 8 against 637 / 419 /
 // 257 with one event-ordered launch per step; the protocol is checked with
 // real shard movement by the simulated ring (tests/test_gpu_pass.py).
 bool RtpLinear::use_flags() const {
@@ -699,15 +699,15 @@ bool RtpLinear::pass_launch_ok() const {
 }
 
 void RtpLinear::flagged_exchange(Direction dir, std::span<void* const> send, std::span<void* const> recv,
-                                 size_t bytes, size_t flag) {
+                                 size_t bytes, size_t flag, int channel) {
   const auto& local = group_->local_ranks();
   const bool fl = use_flags();
-  group_->exchange(dir, send, recv, bytes);
+  group_->exchange(dir, send, recv, bytes, channel);
   if (fl)
     for (size_t r : local) {
       Worker& w = group_->worker(r);
       DeviceGuard dg(w.device);
-      stream_write_u32(w.comm, w.flag(flag_base_ + flag), 1u);
+      stream_write_u32(w.comm_of(channel), w.flag(flag_base_ + flag), 1u);
     }
 }
 
@@ -1079,9 +1079,17 @@ void RtpLinear::backward_pass(std::span<const DView> dy, size_t rows, std::span<
   int flags = pair ? RTPB_PASS_PAIR : 0;
   if (!e.pre.empty()) flags |= RTPB_EPI_GELU_BWD | (exact_gelu_ ? RTPB_EPI_EXACT_GELU : 0);
   auto group_of = [&](size_t s) { return pair ? s / 2 : s; };
+  // SM shares of the two launches. The dX launch's fp32 accumulator is read
+  // and written per step pair (8 B per dX element) at ~25 GB/s per SM of TMA
+  // reduce-add, so a wide-in, thin-shard layer (in >= 16 per) is dX-bound and
+  // gets ~2/3 of the SMs; otherwise the dW chain is the slower one and dX gets
+  // ~0.45. Measured (config (b) --solo, per-launch times): ffn2 (3072 -> 96 at
+  // N = 8) 354 / 203 us dX / dW at 74 SMs for dX, 295 / 240 at 96; ffn1
+  // (768 -> 384) 123 / 174 at 74, 98 / 199 at 96. RTPB_PASS_DX_SMS overrides.
   const int all = sm_budget();
-  int d_sms = all / 2 & ~1;
-  if (const char* ev = std::getenv("RTPB_PASS_DX_SMS")) d_sms = std::max(2, std::min(all - 2, std::atoi(ev))) & ~1;
+  int d_sms = int(all * (in_ >= 16 * per_ ? 0.65 : 0.45)) & ~1;
+  if (const char* ev = std::getenv("RTPB_PASS_DX_SMS")) d_sms = std::atoi(ev);
+  d_sms = std::max(2, std::min(all - 2, d_sms)) & ~1;
   set_sm_budget(d_sms);  // the tiles (and count-ins) of the dX launch depend on its SM share
   const unsigned target = rtpb_pass_done_target(1, rows, in_, per_, n, flags);
   set_sm_budget(all);
@@ -1117,15 +1125,16 @@ void RtpLinear::backward_pass(std::span<const DView> dy, size_t rows, std::span<
   group_->comm_after_compute();  // the spares' last readers are done
   group_->each([&](size_t r) { group_->worker(r).fork_aux(); });  // dW reads dY and X, complete on compute
   const bool serial = serial_profile();
-  // One comm stream carries both chains in order. W first: the dW chain
-  // waits for the dX launch's progress where a W shift waits for it; G first
-  // (RTPB_PASS_G_FIRST=1): the dX launch waits for the dW chain's. Measured
-  // (config (b) --solo N = 8 / 4 / 2): W first 319 / 512 / 695, G first
-  // 307 / 470 / 693 TFLOP/s per GPU, also with the dX launch given 96 SMs.
-  const bool g_first = [] {
-    const char* e = std::getenv("RTPB_PASS_G_FIRST");
-    return e && std::atoi(e) != 0;
+  // The W shifts (channel 0) and the G shifts (channel 1) run on separate
+  // comm streams, so neither chain queues behind the other's waits
+  // (RTPB_PASS_ONE_CHANNEL=1: both on channel 0 in step order, W first — on
+  // one stream W first measured better than G first: config (b) --solo
+  // N = 8 / 4 / 2 319 / 512 / 695 vs 307 / 470 / 693 TFLOP/s per GPU).
+  static const int kGChannelSel = [] {
+    const char* e = std::getenv("RTPB_PASS_ONE_CHANNEL");
+    return (e && std::atoi(e) != 0) ? 0 : 1;
   }();
+  const int kGChannel = kGChannelSel;
   auto post_shifts = [&] {
     host_trace(label_, "backward pass: shifts");
     std::vector<void*> wp(n, nullptr), sp(n, nullptr), gp(n, nullptr);
@@ -1145,22 +1154,19 @@ void RtpLinear::backward_pass(std::span<const DView> dy, size_t rows, std::span<
         }
       };
       auto shift_g = [&] {
-        // G shift once dW(s) has landed: the gradient travels with its accumulation
+        // G shift once dW(s) has landed: the gradient travels with its
+        // accumulation, on channel 1 (its own comm stream)
         for (size_t r : local) {
           Worker& w = group_->worker(r);
           DeviceGuard dg(w.device);
-          if (!serial) stream_wait_geq_u32(w.comm, w.flag(flag_base_ + kFlagDoneW + s), target_w);
+          if (!serial) stream_wait_geq_u32(w.comm_of(kGChannel), w.flag(flag_base_ + kFlagDoneW + s), target_w);
           gp[r] = slots_[r].grad_acc.data();
         }
-        flagged_exchange(Direction::CounterClockwise, gp, gp, slots_[local[0]].grad_acc.bytes(), kFlagBwdG + s + 1);
+        flagged_exchange(Direction::CounterClockwise, gp, gp, slots_[local[0]].grad_acc.bytes(), kFlagBwdG + s + 1,
+                         kGChannel);
       };
-      if (g_first) {
-        shift_g();
-        shift_w();
-      } else {
-        shift_w();
-        shift_g();
-      }
+      shift_w();
+      shift_g();
     }
   };
   if (serial) post_shifts();  // (profiling a Solo group: every flag up front)
@@ -1205,7 +1211,11 @@ void RtpLinear::backward_pass(std::span<const DView> dy, size_t rows, std::span<
   set_sm_budget(all);
   if (!serial) post_shifts();
   pre_bwd_ = false;
-  for (size_t r : local) group_->worker(r).record(Ev::PassEnd, true);
+  for (size_t r : local) {
+    Worker& w = group_->worker(r);
+    w.record(Ev::PassEnd, true);
+    w.record_on(Ev::PassEndG, w.comm_of(kGChannel));
+  }
   if (e.before_last_step) {  // the next layer's first shift, queued behind this pass's (fenced above)
     group_->set_comm_fenced(true);
     try {
@@ -1219,7 +1229,9 @@ void RtpLinear::backward_pass(std::span<const DView> dy, size_t rows, std::span<
   set_sm_budget(all);
   for (size_t r : local) {
     if ((n - 1) & 1) swap_data(slots_[r].weight, spares_[r]);  // the pass's n - 1 swaps
-    group_->worker(r).wait(Ev::PassEnd, false);
+    Worker& w = group_->worker(r);
+    w.wait(Ev::PassEnd, false);
+    w.wait_on(Ev::PassEndG, w.compute);
   }
   host_trace(label_, "backward pass: queued");
   grads_zero_pending_ = false;

@@ -26,8 +26,16 @@ void cuda_check(cudaError_t e, const char* where);
 // Fork / Join: compute <-> aux stream hand-offs (N = 1 dX || dW overlap).
 enum class Ev : int {
   Compute = 0, WDone = 1, GDone = 2, Comm = 3, Ready = 4, Consumed = 5, Staged = 6, Fork = 7, Join = 8, AuxDone = 9,
-  PassEnd = 10, kCount = 11
+  PassEnd = 10, PassEndG = 11, kCount = 12
 };
+
+// Ring-shift channels: 0 carries the weight shards (and, outside the pass
+// launches, the gradients), 1 the travelling gradient of a backward pass
+// launch, so the dW chain and the dX launch's weight shifts do not queue
+// behind each other on one stream. Each channel has its own comm stream and
+// transport events (and, under NCCL, its own communicator).
+constexpr int kChannels = 2;
+enum class ChEv : int { Ready = 0, Comm = 1, Staged = 2, Consumed = 3, kCount = 4 };
 
 struct Worker {
   Worker(size_t rank, int device);
@@ -35,7 +43,11 @@ struct Worker {
   size_t rank;
   int device;
   cudaStream_t compute = nullptr;
-  cudaStream_t comm = nullptr;
+  cudaStream_t comm = nullptr;    // channel 0
+  cudaStream_t comm_g = nullptr;  // channel 1
+  cudaEvent_t ch_ev[kChannels][int(ChEv::kCount)] = {};
+  cudaStream_t comm_of(int channel) const { return channel ? comm_g : comm; }
+  cudaEvent_t ch_event(int channel, ChEv e) const { return ch_ev[channel][int(e)]; }
   // Second compute stream: with no rotation to wait for (N = 1), dW runs here
   // beside dX, each GEMM on its share of the SMs (RtpLinear::backward_ex).
   cudaStream_t aux = nullptr;
@@ -93,7 +105,8 @@ class Transport {
   // local entries are read). Enqueued on the comm streams; send == recv at a
   // rank means in place. On return the comm streams are ordered after the
   // transfer (both the rank's receive and its send).
-  virtual void shift(Direction dir, std::span<void* const> send, std::span<void* const> recv, size_t bytes) = 0;
+  virtual void shift(Direction dir, std::span<void* const> send, std::span<void* const> recv, size_t bytes,
+                     int channel) = 0;
   // Host-side wait watchdog (WorkerGroup::synchronize): true when waits on
   // this transport's streams must be polled (a peer can fail or vanish).
   virtual bool polled() const { return false; }
