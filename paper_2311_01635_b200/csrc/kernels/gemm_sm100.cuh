@@ -293,14 +293,19 @@ __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+// RTPB_HANG_DEBUG builds report the expired counter first (a printf costs
+// every instantiation a stack frame, so release builds only trap).
+__device__ __forceinline__ void wait_expired(const unsigned* p, unsigned need) {
+#ifdef RTPB_HANG_DEBUG
+  printf("rtpb: bounded wait expired: block %d thread %d counter %p holds %u, needs %u\n", int(blockIdx.x),
+         int(threadIdx.x), static_cast<const void*>(p), ld_acquire(p), need);
+#endif
+  __trap();
+}
 __device__ __forceinline__ void wait_counter_nofence(const unsigned* p, unsigned need) {
   const long long t0 = clock64();
   while (ld_acquire(p) < need)
-    if (clock64() - t0 > (20ll << 30)) {
-      printf("rtpb: bounded wait expired: block %d thread %d counter %p holds %u, needs %u\n", int(blockIdx.x),
-             int(threadIdx.x), static_cast<const void*>(p), ld_acquire(p), need);
-      __trap();
-    }
+    if (clock64() - t0 > (20ll << 30)) wait_expired(p, need);
 }
 __device__ __forceinline__ void wait_counter(const unsigned* p, unsigned need) {
   wait_counter_nofence(p, need);
@@ -447,7 +452,7 @@ __device__ __forceinline__ void unstage_row(const uint8_t* stg, int row, float* 
 template <class Cfg>
 __global__ void __launch_bounds__(Cfg::THREADS, 1)
     rtp_gemm_kernel(const __grid_constant__ GemmMaps maps, const __grid_constant__ GemmMaps maps2,
-                    const GemmArgs args) {
+                    const __grid_constant__ GemmArgs args) {
   using namespace ptx;
   constexpr int BM = Cfg::BM, BN = Cfg::BN, BK = Cfg::BK, STAGES = Cfg::STAGES;
   constexpr bool F32 = Cfg::TF32;  // activation / output dtype is fp32 in TF32 mode
@@ -704,8 +709,13 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
           griddep_launch();
           admitted = true;
         }
-        // pass launch: the step's shard buffer; DGRAD reads dY at its column block
+        // pass launch: the step's shard buffers and dY column blocks (per unit)
         const int first_step = args.pass_pair ? 2 * x.step : x.step;
+        const bool dg_pass = pass && Cfg::EPI == EPI_DGRAD;
+        const int a_koff0 = dg_pass ? args.pass_col[first_step] : 0;
+        const int a_koff1 = dg_pass && x.seg_kb ? args.pass_col[first_step + 1] : 0;
+        const int b_noff = (pass && Cfg::EPI == EPI_WGRAD) ? args.pass_col[x.step] : 0;  // dY column block
+        const CUtensorMap* b_map0 = (pass && x.buf1) ? &maps2.b : &mp.b;
         if (x.prob && args.dep_count && !args.dep_on_k) {
           // problem 1 reads problem 0's output rows of this row block: wait
           // until every warp of every problem-0 tile of the block has landed
@@ -739,9 +749,8 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
           const int k0 = (seg2 ? kb - args.kseg_kb : x.seg_kb && kb >= x.seg_kb ? kb - x.seg_kb : kb) * BK;
           // pass launch: this K block's shard buffer and dY column block
           const bool pseg2 = x.seg_kb && kb >= x.seg_kb;
-          const CUtensorMap* b_map = (pass && (x.buf1 || pseg2)) ? &maps2.b : &mp.b;
-          const int a_koff = (pass && Cfg::EPI == EPI_DGRAD) ? args.pass_col[first_step + (pseg2 ? 1 : 0)] : 0;
-          const int b_noff = (pass && Cfg::EPI == EPI_WGRAD) ? args.pass_col[x.step] : 0;  // dY column block
+          const CUtensorMap* b_map = pseg2 ? &maps2.b : b_map0;
+          const int a_koff = pseg2 ? a_koff1 : a_koff0;
           for (int op = 0; op < Cfg::NOPS; ++op) {
             const CUtensorMap* ma = op ? &mk.a_lo : &mk.a;
             const CUtensorMap* mbm = op ? &mk.b_lo : (seg2 ? &mk.b : b_map);
