@@ -665,7 +665,7 @@ void RtpLinear::forward_impl(std::span<const DView> x, size_t rows, std::span<co
 // spinning grids would compete for the same SMs.
 // Default on (RTPB_FLAGS=0 keeps stream events): the flags carry the pass
 // launches (pass_launch_ok), which `bench.py --solo N` (config (b), TFLOP/s
-// per GPU) measures at 693 / 577 / 352 for N = 2 / 4 / 8 against 637 / 419 /
+// per GPU) measures at 710 / 585 / 353 for N = 2 / 4 / 8 against 637 / 419 /
 // 257 with one event-ordered launch per step; the protocol is checked with
 // real shard movement by the simulated ring (tests/test_gpu_pass.py).
 bool RtpLinear::use_flags() const {
