@@ -126,7 +126,9 @@ int rtpb_dgrad_step2(int dtype, const void* dy, size_t ldy, size_t col0, const v
  * (written by the comm stream when the shard landed). `done` (steps zeroed
  * counters): once step s's operands have been read, done[s] reaches
  * *done_target (written by the call; with RTPB_PASS_PAIR done[g] counts the
- * pair (2g, 2g + 1)) — the comm stream waits for that value
+ * pair (2g, 2g + 1)); a nonzero *done_target on entry is the target the
+ * caller announced (rtpb_pass_done_target): the call fails without
+ * launching if the launch would count to another — the comm stream waits for that value
  * (cuStreamWaitValue32) before it lands step s + 2's shard in step s's
  * buffer. The launch re-zeroes `done` (and, with reset_flags, the `ready`
  * range) when it completes; reset_ctr is a zeroed counter. y_cols / dy_cols:

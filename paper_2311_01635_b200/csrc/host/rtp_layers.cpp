@@ -556,12 +556,11 @@ void RtpLinear::forward_impl(std::span<const DView> x, size_t rows, std::span<co
       const size_t ld_act = e.act.empty() ? 0 : (e.act[k].ld ? e.act[k].ld : out_);
       void* yp = e.store_pre ? y[k].data : nullptr;
       const size_t ldy = e.store_pre && y[k].ld ? y[k].ld : out_;
-      unsigned tgt = 0;
+      unsigned tgt = target;  // checked before the launch
       check_status(rtpb_fwd_pass(x[k].data, x[k].ld ? x[k].ld : in_, buf[r][0], buf[r][1], yp, ldy, act, ld_act, out_,
                                  cols[r].data(), mask, n, rows, in_, per_, flags, w.flag(flag_base_ + kFlagFwd),
                                  w.flag(flag_base_ + kFlagDoneFwd), &tgt, w.flag(flag_base_ + kFlagCtrFwd),
                                  w.compute));
-      if (tgt != target) throw StateError(label_ + ": pass launch count-in target mismatch");
     });
     if (!serial) post_shifts();
     pre_fwd_ = false;
@@ -1178,13 +1177,12 @@ void RtpLinear::backward_pass(std::span<const DView> dy, size_t rows, std::span<
       const size_t k = k_of[r];
       const void* pre = e.pre.empty() ? nullptr : e.pre[k].data;
       const size_t ldpre = e.pre.empty() ? 0 : (e.pre[k].ld ? e.pre[k].ld : in_);
-      unsigned tgt = 0;
+      unsigned tgt = target;  // checked before the launch
       check_status(rtpb_dgrad_pass(dy[k].data, dy[k].ld ? dy[k].ld : out_, out_, buf[r][0], buf[r][1], cols[r].data(),
                                    mask, n, static_cast<float*>(dx_acc_[r].data()), in_, dx[k].data,
                                    dx[k].ld ? dx[k].ld : in_, pre, ldpre, rows, in_, per_, flags,
                                    w.flag(flag_base_ + kFlagBwdW), w.flag(flag_base_ + kFlagDoneBwd), &tgt,
                                    w.flag(flag_base_ + kFlagCtrW), w.compute));
-      if (tgt != target) throw StateError(label_ + ": pass launch count-in target mismatch");
     });
     // dW of every step: one launch on aux (rtpb_wgrad_pass) after dY's
     // column sums (the bias parts, added as each G arrives)
@@ -1196,13 +1194,12 @@ void RtpLinear::backward_pass(std::span<const DView> dy, size_t rows, std::span<
       float* db = static_cast<float*>(pass_ws_[r].data());
       check_status(rtpb_colsum(dy[k].data, ldy, rows, out_, db, static_cast<char*>(pass_ws_[r].data()) + db_bytes,
                                pass_ws_[r].bytes() - db_bytes, w.aux));
-      unsigned tgt = 0;
+      unsigned tgt = target_w;  // checked before the launch
       check_status(rtpb_wgrad_pass(x_cache_[r].data, x_cache_[r].ld ? x_cache_[r].ld : in_, dy[k].data, ldy, out_,
                                    static_cast<float*>(slots_[r].grad_acc.data()), cols[r].data(), n, rows, in_, per_,
                                    grads_zero_pending_ ? RTPB_EPI_FIRST : 0, db, w.flag(flag_base_ + kFlagBwdG),
                                    w.flag(flag_base_ + kFlagDoneW), &tgt, w.flag(flag_base_ + kFlagCtrG),
                                    workspace_[r].data(), workspace_[r].bytes(), w.aux));
-      if (tgt != target_w) throw StateError(label_ + ": dW pass launch count-in target mismatch");
     });
   } catch (...) {
     set_sm_budget(all);

@@ -395,7 +395,12 @@ int launch_pass(const Op& a, const Op& b0, const Op& b1, const Out& c0, const Ou
   if ((rc = encode_maps<Cfg>(a, b1, d0, d1, m2))) return rc;
   const unsigned tiles = unsigned((args.M + Cfg::TILE_M - 1) / Cfg::TILE_M) * unsigned((args.N + Cfg::BN - 1) / Cfg::BN) *
                          unsigned(args.k_splits > 1 ? args.k_splits : 1);  // units per step
-  *done_target = tiles * unsigned(Cfg::EPI_WARPS * (Cfg::PAIR ? 2 : 1));  // count-ins per step
+  const unsigned target = tiles * unsigned(Cfg::EPI_WARPS * (Cfg::PAIR ? 2 : 1));  // count-ins per step
+  // a caller that queued waits for an announced target gets no launch that
+  // would count to another one (its waits would never be satisfied)
+  if (*done_target && *done_target != target)
+    return set_error(RTPB_ERR_STATE, "pass launch: count-in target differs from the announced one");
+  *done_target = target;
   return launch_cfg<Cfg>(a, b0, c0, c1, args, s, &m2);
 }
 

@@ -760,7 +760,7 @@ def pass_done_target(which, M, I, per, steps, flags=0) -> int:
 
 
 def fwd_pass(x, buf0, buf1, y, cols, per, act=None, store_pre=True, ready=None, done=None, reset_ctr=None,
-             exact_gelu=False, stream=None):
+             exact_gelu=False, stream=None, announced_target=0):
     """rtpb_fwd_pass: step s of a layer's forward pass (shard in buffer s & 1,
     output column block cols[s]) for every s, in one launch. Returns the
     per-step count-in target on `done`."""
@@ -769,7 +769,7 @@ def fwd_pass(x, buf0, buf1, y, cols, per, act=None, store_pre=True, ready=None, 
         (64 if exact_gelu else 0)
     ycols = (y if y is not None else act).shape[1]
     mask = sum(1 << s for s in range(len(cols)) if s & 1)
-    tgt = C.c_uint(0)
+    tgt = C.c_uint(announced_target)
     s = (stream or torch.cuda.current_stream(x.device)).cuda_stream
     check(lib.rtpb_fwd_pass(x.data_ptr(), x.stride(0), buf0.data_ptr(), buf1.data_ptr(),
                             y.data_ptr() if y is not None else None, y.stride(0) if y is not None else 0,

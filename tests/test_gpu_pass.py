@@ -180,6 +180,22 @@ def test_wgrad_pass_matches_per_step(M, I, per, n, zero):
     assert int(done.abs().sum()) == 0 and int(ready[:n].abs().sum()) == 0
 
 
+def test_pass_launch_refuses_a_different_announced_target():
+    """A caller that queued its comm-stream waits for an announced count-in
+    target gets an error, not a launch that would count to another value."""
+    from paper_2311_01635_b200 import rtp
+    M, I, per, n = 512, 256, 96, 4
+    x, bufs, _, cols = _setup(M, I, per, n)
+    y = torch.zeros(M, n * per, dtype=torch.bfloat16, device="cuda")
+    right = rtp.pass_done_target(0, M, I, per, n)
+    before = rtp.launch_count()
+    with pytest.raises(rtp.StateError):
+        rtp.fwd_pass(x, bufs[0], bufs[1], y, cols, per, announced_target=right + 1)
+    assert rtp.launch_count() == before
+    assert rtp.fwd_pass(x, bufs[0], bufs[1], y, cols, per, announced_target=right) == right
+    torch.cuda.synchronize()
+
+
 def test_pass_rejects_bad_geometry():
     from paper_2311_01635_b200 import rtp
     x, bufs, _, cols = _setup(256, 128, 48, 2)  # per not a multiple of 32

@@ -1,5 +1,8 @@
 mkdir -p gpurun_out
 timeout -s KILL 1500 python -m pytest tests -m gpu -x -q -p no:cacheprovider > gpurun_out/gputest.log 2>&1; echo "all rc=$?" >> gpurun_out/gputest.log
 timeout -s KILL 200 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log
+S=gpurun_out/solo_final.jsonl; rm -f $S
+for n in 2 4 8; do
+  timeout -s KILL 90 python bench.py --config b --solo $n --steps 50 --no-cpu-baseline --no-e2e 2>/dev/null | tail -1 >> $S
+done
 timeout -s KILL 400 python bench.py > gpurun_out/bench_d.log 2>&1
-timeout -s KILL 600 compute-sanitizer --tool memcheck --print-limit 20 python -m pytest tests/test_gpu_pass.py -x -q -p no:cacheprovider -k "fwd_pass_equals or dgrad_pass_equals or paired" > gpurun_out/sanitize_pass.log 2>&1; echo "rc=$?" >> gpurun_out/sanitize_pass.log
