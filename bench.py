@@ -580,7 +580,7 @@ def main():
                 "parity_ok": parity_ok, "parity_check": parity_detail, "numerics": numerics,
                 "gpu_launches": int(launches),
                 "step_execution": graph_note,
-                "ring_schedule": ring_schedule(ring, args.mode, H, F, M),
+                "ring_schedule": ring_schedule(ring, args.mode, H, F, M, bool(args.same_device and world > 1)),
                 "eager_ms_per_step": eager_ms,
                 "roofline": roofline,
                 "step_roofline": step_roofline,
@@ -598,15 +598,17 @@ def main():
         dist.destroy_process_group()
 
 
-def ring_schedule(ring, mode, h, f, rows):
+def ring_schedule(ring, mode, h, f, rows, shared_gpu=False):
     """How the N > 1 passes are launched (rtp_layers.cpp pass_launch_ok /
     backward_pass_pays): one persistent launch per layer pass ordered by
     arrival flags, or one event-ordered launch per rotation step."""
     import os
     if ring < 2:
         return "N = 1: no rotation"
-    flags = os.environ.get("RTPB_FLAGS", "1") != "0"
-    passes = flags and mode == "outofplace" and os.environ.get("RTPB_NO_PASS", "0") in ("", "0")
+    env = os.environ.get("RTPB_FLAGS")
+    flags = (env != "0") if env is not None else not shared_gpu  # the library's default (use_flags)
+    passes_ok = not shared_gpu
+    passes = passes_ok and flags and mode == "outofplace" and os.environ.get("RTPB_NO_PASS", "0") in ("", "0")
     out = {}
     for name, i, o in (("ffn1", h, f), ("ffn2", f, h)):
         per = o // ring

@@ -668,10 +668,14 @@ void RtpLinear::forward_impl(std::span<const DView> x, size_t rows, std::span<co
 // 257 with one event-ordered launch per step; the protocol is checked with
 // real shard movement by the simulated ring (tests/test_gpu_pass.py).
 bool RtpLinear::use_flags() const {
-  static const bool on = [] {  // default on; RTPB_FLAGS=0 keeps stream events
+  // RTPB_FLAGS=0/1 forces; unset: on, except where processes share a GPU
+  // (time-sliced: a grid spinning on a flag can hold the GPU while the peer
+  // process that would raise it is switched out)
+  static const int env = [] {
     const char* e = std::getenv("RTPB_FLAGS");
-    return !e || std::atoi(e) != 0;
+    return e ? (std::atoi(e) != 0 ? 1 : 0) : -1;
   }();
+  const bool on = env >= 0 ? env == 1 : !group_->device_shared();
   const TransportKind k = group_->kind();
   const bool one_per_gpu = k == TransportKind::Nccl || k == TransportKind::Ipc || k == TransportKind::Solo ||
                            (k == TransportKind::Lockstep && sim_flags());
