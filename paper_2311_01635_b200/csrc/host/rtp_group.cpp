@@ -447,6 +447,11 @@ class NcclTransport final : public Transport {
     std::memcpy(&uid, id, sizeof uid);
     DeviceGuard dg(g.worker(rank).device);
     nccl_check(ncclCommInitRank(&comm_, int(g.size()), uid, int(rank)), "ncclCommInitRank");
+    // channel 1 (a backward pass launch's travelling gradient) gets its own
+    // communicator — two streams must not issue on one — made here, not on
+    // first use: a collective that may synchronise the device must not run
+    // between a pass launch and the shifts it waits for
+    nccl_check(ncclCommSplit(comm_, 0, int(rank), &comm2_, nullptr), "ncclCommSplit");
   }
   ~NcclTransport() override {
     if (comm2_) ncclCommDestroy(comm2_);
@@ -483,13 +488,6 @@ class NcclTransport final : public Transport {
     if (aborted_) throw NcclError("ring shift on an aborted communicator");
     Worker& w = g_.worker(rank_);
     DeviceGuard dg(w.device);
-    if (ch && !comm2_) {
-      // channel 1 (the travelling gradient of a backward pass launch) gets
-      // its own communicator: two streams must not issue on one. Collective
-      // over the ring; every rank reaches its first channel-1 shift in the
-      // same order.
-      nccl_check(ncclCommSplit(comm_, 0, int(rank_), &comm2_, nullptr), "ncclCommSplit");
-    }
     ncclComm_t comm = ch ? comm2_ : comm_;
     cudaStream_t st = w.comm_of(ch);
     const int dst = int(ring_dest(rank_, n, dir)), src = int(ring_src(rank_, n, dir));
@@ -517,7 +515,7 @@ class NcclTransport final : public Transport {
   WorkerGroup& g_;
   size_t rank_;
   ncclComm_t comm_ = nullptr;
-  ncclComm_t comm2_ = nullptr;  // channel 1, split from comm_ on first use
+  ncclComm_t comm2_ = nullptr;  // channel 1, split from comm_ at construction
   bool aborted_ = false;
 };
 
