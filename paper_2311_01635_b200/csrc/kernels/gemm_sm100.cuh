@@ -598,6 +598,10 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
     return x;
   };
 
+  // The bias column-sum warps take part in the stage pipeline only when a
+  // launch asks for the bias gradient (a launch without it — a pass launch,
+  // a projection, a separately summed bias — runs as if they were absent).
+  const bool colsum_live = Cfg::COLSUM && (args.gbias_out != nullptr || args.gbias_out2 != nullptr);
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&maps.a);
     prefetch_tmap(&maps.b);
@@ -610,7 +614,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full_bar[s], 1);
       // COLSUM: the stage is free once the MMA commit AND the column-sum warp release it.
-      mbar_init(&empty_bar[s], 1 + Cfg::COLSUM_WARPS);
+      mbar_init(&empty_bar[s], 1 + (colsum_live ? Cfg::COLSUM_WARPS : 0));
       if constexpr (Cfg::COLSUM) mbar_init(&ready_bar[s], 1);
     }
     for (int s = 0; s < 2; ++s) {
@@ -1389,7 +1393,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
     const int chunk = (lane % LPR) / 8, piece = lane & 7, rsub = lane / LPR;
     int stage = 0;
     uint32_t phase = 0;
-    for (int it = it_beg; it < it_end; it += it_step) {
+    for (int it = it_beg; colsum_live && it < it_end; it += it_step) {
       const Unit x_ = decode(it);
       const int split = x_.split, mb = x_.mb, nb = x_.nb, kb0 = x_.kb0, kb1 = x_.kb1, uN = x_.N;
       const bool first = x_.flags & EF_FIRST;
