@@ -307,7 +307,9 @@ int rtpb_group_synchronize(rtpb_group g);
 /* Debug hook: copy `count` entries of a local worker's arrival-flag pool
  * (from index `first`) to host memory through a private stream (does not
  * wait for the worker's streams), and report which of its streams (bit 0
- * compute, 1 comm, 2 aux) still have work pending. */
+ * compute, 1 comm, 2 aux) still have work pending. The private stream is
+ * made on the first call, on the device current then (call it once before
+ * the work to watch starts); host_dst should be pinned memory. */
 int rtpb_debug_read_flags(rtpb_group g, size_t rank, size_t first, size_t count, unsigned* host_dst,
                           int* busy_streams);
 /* Debug hook: device address of entry `index` of a local worker's flag pool. */
