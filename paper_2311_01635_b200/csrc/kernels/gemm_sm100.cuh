@@ -225,7 +225,11 @@ struct GemmCfg {
   static constexpr int STG_ONE = 32 * 32 * (EPI == EPI_FWD ? ELEM : 4);
   // dW: two fp32 staging buffers per warp, so a chunk's reduce-add into the
   // travelling gradient is in flight while the next chunk is staged.
+#ifdef RTPB_WGRAD_STG1
+  static constexpr int STG_BUFS = NOUT;
+#else
   static constexpr int STG_BUFS = EPI == EPI_WGRAD ? 2 : NOUT;
+#endif
   static constexpr int STG_WARP = STG_BUFS * STG_ONE;
   static constexpr int STG_BYTES = EPI_WARPS * STG_WARP;
   // PRE_TMA: every chunk (32 x 32 tile, activation dtype) a warp handles in one tile.
@@ -1023,13 +1027,13 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
         // staging buffers free again (previous chunk's bulk stores read them);
         // dW alternates two buffers and waits only for the older group
         uint8_t* wstg = stg0;
-        if constexpr (Cfg::EPI == EPI_WGRAD) {
+        if constexpr (Cfg::EPI == EPI_WGRAD && Cfg::STG_BUFS == 2) {
           wstg = (wbuf & 1) ? stg1 : stg0;
           ++wbuf;
         }
         if (pending) {
           if (lane == 0) {
-            if constexpr (Cfg::EPI == EPI_WGRAD)
+            if constexpr (Cfg::EPI == EPI_WGRAD && Cfg::STG_BUFS == 2)
               bulk_wait_read1();
             else
               bulk_wait_read0();
