@@ -42,6 +42,12 @@ if "wgrad_as_dgrad" in kinds:  # the dW product on the dgrad kernel: X^T (I x M)
     WT[:per * M].view(per, M).copy_(dY.t())
     OUT = torch.empty(I, per, dtype=torch.bfloat16, device=dev)
     fns["wgrad_as_dgrad"] = lambda: rtp.dgrad_step(XT2, 0, WT, None, OUT, I, per, M, True, True)
+if "wgrad_as_fwd" in kinds:  # the dW product on the forward kernel: A = X^T K-major, B = dY MN-major
+    XT1 = X.t().contiguous()
+    DYS = torch.zeros(M * per + per, dtype=torch.bfloat16, device=dev)
+    DYS[:M * per].view(M, per).copy_(dY)
+    OUTF = torch.empty(I, per, dtype=torch.bfloat16, device=dev)
+    fns["wgrad_as_fwd"] = lambda: rtp.fwd_step(XT1, DYS, OUTF, 0, per)
 fl = 2.0 * M * I * per
 for k in kinds:
     f = fns[k]
