@@ -222,7 +222,6 @@ size_t rtpb_step_workspace_bytes(int which, int dtype, size_t M, size_t I, size_
     const size_t Mp = (M + 7) & ~size_t(7);  // transposed operands: 16-byte rows
     if (which == 2) b += 2 * align256(Mp * I * 4) + 2 * align256(Mp * per * 4);
   }
-  if (which == 2 && wgrad_xt_pays(f32, M, I, per)) b += align256(M * I * 2);  // X^T
   return b;
 }
 
@@ -452,13 +451,6 @@ int rtpb_wgrad_step_ex(int dtype, const void* x, size_t ldx, const void* dy, siz
     if ((rc = tf32_split_t(static_cast<const float*>(x), M, I, ldx, xh, xl, s))) return rc;
     if ((rc = tf32_split_t(static_cast<const float*>(p.dy), M, per, ldy, dh, dl, s))) return rc;
     p.x = xh; p.x_lo = xl; p.ldx = Mp; p.dy = dh; p.dy_lo = dl; p.ldy = Mp;
-  }
-  if (!f32 && wgrad_xt_pays(f32, M, I, per)) {
-    void* xt = c.take((M * I * 2 + 3) / 4);
-    if (!c.ok) return set_error(RTPB_ERR_DIMENSION, "wgrad_step: workspace too small");
-    if ((rc = transpose_bf16(x, M, I, ldx, xt, s))) return rc;
-    p.xt = xt;
-    p.ldxt = M;
   }
   if (!c.ok) return set_error(RTPB_ERR_DIMENSION, "wgrad_step: workspace too small");
   if ((reinterpret_cast<uintptr_t>(g_out) | reinterpret_cast<uintptr_t>(g_in)) & 15)

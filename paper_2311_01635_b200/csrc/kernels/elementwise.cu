@@ -235,38 +235,6 @@ int post_launch(const char* what) {
   return RTPB_OK;
 }
 
-// dst (cols x rows, row stride rows) = src^T (rows x cols, stride ld), bf16, in
-// 64 x 64 tiles through shared memory: 16-byte loads and stores on both sides
-// (rows, cols multiples of 64). Feeds the dW's A operand K-major
-// (wgrad_xt_pays, launch.hpp).
-__global__ void __launch_bounds__(256) transpose_bf16_kernel(const uint16_t* __restrict__ src, size_t ld,
-                                                             uint16_t* __restrict__ dst, size_t rows) {
-  __shared__ uint16_t tile[64][64 + 8];
-  const size_t r0 = size_t(blockIdx.y) * 64, c0 = size_t(blockIdx.x) * 64;
-#pragma unroll
-  for (int i = 0; i < 2; ++i) {
-    const int v = int(threadIdx.x) + i * 256;  // 512 vectors of 8: row v / 8, columns (v % 8) * 8
-    const int r = v >> 3, c = (v & 7) * 8;
-    const uint4 q = *reinterpret_cast<const uint4*>(src + (r0 + r) * ld + c0 + c);
-    *reinterpret_cast<uint4*>(&tile[r][c]) = q;
-  }
-  __syncthreads();
-#pragma unroll
-  for (int i = 0; i < 2; ++i) {
-    const int v = int(threadIdx.x) + i * 256;  // output row c = v / 8 (a source column), rows (v % 8) * 8
-    const int c = v >> 3, r = (v & 7) * 8;
-    uint16_t e[8];
-#pragma unroll
-    for (int k = 0; k < 8; ++k) e[k] = tile[r + k][c];
-    uint4 q;
-    q.x = e[0] | (uint32_t(e[1]) << 16);
-    q.y = e[2] | (uint32_t(e[3]) << 16);
-    q.z = e[4] | (uint32_t(e[5]) << 16);
-    q.w = e[6] | (uint32_t(e[7]) << 16);
-    *reinterpret_cast<uint4*>(dst + (c0 + c) * rows + r0 + r) = q;
-  }
-}
-
 }  // namespace
 
 int flyweight_init(void* dst, bool f32, uint64_t seed, uint64_t base, size_t I, size_t O, size_t n, size_t j,
@@ -371,13 +339,6 @@ int fill(void* dst, int dtype, size_t n, double v, cudaStream_t s) {
 int cast_f32_to_bf16(const float* src, void* dst, size_t n, cudaStream_t s) {
   cast_kernel<<<grid_for(n, 256), 256, 0, s>>>(src, static_cast<__nv_bfloat16*>(dst), n);
   return post_launch("cast_kernel");
-}
-
-int transpose_bf16(const void* src, size_t rows, size_t cols, size_t ld, void* dst, cudaStream_t s) {
-  if (rows % 64 || cols % 64 || ld % 8) return set_error(RTPB_ERR_CONFIG, "transpose_bf16: rows, cols % 64");
-  const dim3 grid(unsigned(cols / 64), unsigned(rows / 64));
-  transpose_bf16_kernel<<<grid, 256, 0, s>>>(static_cast<const uint16_t*>(src), ld, static_cast<uint16_t*>(dst), rows);
-  return post_launch("transpose_bf16_kernel");
 }
 
 // Module anchor for preload_device_kernels (launch.hpp): any kernel of this

@@ -1068,7 +1068,6 @@ void preload_device_kernels() {
   set_smem_attr<GemmCfg<1, 256, false, 8, false, false, true, true>>();
   set_smem_attr<GemmCfg<1, 64, false, 8, false, false, false, false>>();
   set_smem_attr<GemmCfg<1, 64, true, 8, false, false, false, false>>();
-  set_smem_attr<GemmCfg<2, 256, false, 8, false, true, false, true>>();  // dW on X^T (wgrad_xt_pays)
   set_smem_attr<GemmCfg<2, 128, false, 8, true, true, false, false>>();
   set_smem_attr<GemmCfg<2, 128, false, 8, true, true, false, true>>();
   set_smem_attr<GemmCfg<2, 128, true, 8, false, false, false, false>>();
@@ -1182,17 +1181,6 @@ int gemm_wgrad(bool f32, const StepWgrad& p, cudaStream_t s) {
   g.gbias_out = p.gbias_out;
   g.bias_part = p.bias_part;
   g.bias_tick = p.bias_tick;
-  if (!f32 && p.xt) {
-    // A = X^T (I x M) read K-major from the caller's transposed copy; only
-    // the unsplit CTA-pair config (the long-K dW the copy pays for)
-    GemmArgs t = g;
-    const int code = pick_code<EPI_WGRAD>(false, t, p.force_bn);
-    if (code == 1256 && t.k_splits == 1) {
-      const Op axt{p.xt, nullptr, p.M, p.I, p.ldxt};
-      t.n_fastest = raster_mode(t.M, t.N, t.K, 256, 256, false, true);
-      return launch_cfg<GemmCfg<EPI_WGRAD, 256, false, kEpiWarps, false, true, false, true>>(axt, b, c0, nullptr, t, s);
-    }
-  }
   int par = 0;
   if (p.wpart && !f32) {
     // unordered partials + slice folds for long split chains (see
@@ -1217,16 +1205,6 @@ int gemm_wgrad(bool f32, const StepWgrad& p, cudaStream_t s) {
     return dispatch<EPI_WGRAD>(f32, a, b, c0, &part, g, s, p.force_bn);
   }
   return dispatch<EPI_WGRAD>(f32, a, b, c0, nullptr, g, s, p.force_bn);
-}
-
-bool wgrad_xt_pays(bool f32, size_t M, size_t I, size_t per) {
-  static const int env = [] {
-    const char* e = std::getenv("RTPB_WGRAD_XT");
-    return e ? std::atoi(e) : -1;
-  }();
-  if (f32 || env == 0 || M % 64 || I % 64) return false;
-  if (env == 1) return true;
-  return false;
 }
 
 int wgrad_splits(bool f32, size_t M, size_t I, size_t per, int force_bn) {

@@ -49,14 +49,7 @@ struct StepWgrad {
   float* wpart;                                   // split-K fp32 partials (nullable: ordered split-K)
   size_t M, I, per;
   int force_bn;
-  const void* xt = nullptr; size_t ldxt = 0;      // bf16: X^T (I x M), when wgrad_xt_pays
 };
-// bf16 dW with A = X^T read K-major from a transposed copy (transpose_bf16)
-// instead of X read MN-major in place: the MN-major A costs the dW launch
-// 5-11 % (profiles/wgrad_mn_r2/), the copy pays only where X is much smaller
-// than dY (ffn1-shaped layers). RTPB_WGRAD_XT=0/1 forces it off / on.
-bool wgrad_xt_pays(bool f32, size_t M, size_t I, size_t per);
-int transpose_bf16(const void* src, size_t rows, size_t cols, size_t ld, void* dst, cudaStream_t s);
 // K splits the dW launch uses on the whole machine (1: none) and the fp32
 // partial floats its workspace needs for them (splits x I rounded to 256 x per).
 int wgrad_splits(bool f32, size_t M, size_t I, size_t per, int force_bn);
